@@ -1,0 +1,282 @@
+// gd_algo.cu -- batch staging, validation, out-degrees and the weak-component flood.
+#include "gd_algo.cuh"
+
+namespace gdb {
+
+namespace {
+
+// validation bits
+constexpr int kBadKind = 1, kBadNode = 2, kBadWeight = 4;
+
+__global__ void k_stage_host(const uint8_t* kind, const int64_t* s64, const int64_t* d64, const int64_t* w64,
+                             int64_t k, int64_t n, int32_t* s, int32_t* d, int32_t* w, uint8_t* isdel,
+                             uint8_t* isadd, int* err, unsigned long long* bad_index) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < k; i += (int64_t)gridDim.x * blockDim.x) {
+        uint8_t kd = kind[i];
+        int64_t a = s64[i], b = d64[i];
+        int64_t wt = w64 ? w64[i] : 1;
+        int e = 0;
+        if (kd != 'a' && kd != 'd') e |= kBadKind;
+        if (a < 0 || a >= n || b < 0 || b >= n) e |= kBadNode;
+        if (kd == 'a' && (wt < INT32_MIN || wt > INT32_MAX)) e |= kBadWeight;
+        if (e) {
+            atomicOr(err, e);
+            atomicMin(bad_index, (unsigned long long)i);
+        }
+        s[i] = (int32_t)a;
+        d[i] = (int32_t)b;
+        w[i] = (int32_t)(kd == 'a' ? wt : 1);
+        isdel[i] = kd == 'd';
+        isadd[i] = kd == 'a';
+    }
+}
+
+__global__ void k_stage_dev(const uint8_t* kind, const int32_t* s, const int32_t* d, int64_t k, int64_t n,
+                            uint8_t* isdel, uint8_t* isadd, int* err, unsigned long long* bad_index) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < k; i += (int64_t)gridDim.x * blockDim.x) {
+        uint8_t kd = kind[i];
+        int e = 0;
+        if (kd != 'a' && kd != 'd') e |= kBadKind;
+        if (s[i] < 0 || s[i] >= n || d[i] < 0 || d[i] >= n) e |= kBadNode;
+        if (e) {
+            atomicOr(err, e);
+            atomicMin(bad_index, (unsigned long long)i);
+        }
+        isdel[i] = kd == 'd';
+        isadd[i] = kd == 'a';
+    }
+}
+
+__global__ void k_gather_i32(const int32_t* in, const int32_t* sel, int64_t m, int32_t* out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = in[sel[i]];
+}
+
+}  // namespace
+
+void AlgoBase::split(DevBatch& b, const uint8_t* isdel_isadd, const int32_t* s, const int32_t* d, const int32_t* w,
+                     int64_t k) {
+    cudaStream_t st = stream();
+    const uint8_t* isdel = isdel_isadd;
+    const uint8_t* isadd = isdel_isadd + k;
+    DBuf<int32_t> sel(k, st);
+    b.kdel = select_flagged_index(st, isdel, k, sel.get());
+    b.ds.alloc(b.kdel, st);
+    b.dd.alloc(b.kdel, st);
+    if (b.kdel) {
+        GD_KERNEL(k_gather_i32, grid_for(b.kdel, 256), 256, 0, st, s, sel.get(), b.kdel, b.ds.get());
+        GD_KERNEL(k_gather_i32, grid_for(b.kdel, 256), 256, 0, st, d, sel.get(), b.kdel, b.dd.get());
+    }
+    b.kadd = select_flagged_index(st, isadd, k, sel.get());
+    b.as.alloc(b.kadd, st);
+    b.ad.alloc(b.kadd, st);
+    b.aw.alloc(b.kadd, st);
+    if (b.kadd) {
+        GD_KERNEL(k_gather_i32, grid_for(b.kadd, 256), 256, 0, st, s, sel.get(), b.kadd, b.as.get());
+        GD_KERNEL(k_gather_i32, grid_for(b.kadd, 256), 256, 0, st, d, sel.get(), b.kadd, b.ad.get());
+        if (w) GD_KERNEL(k_gather_i32, grid_for(b.kadd, 256), 256, 0, st, w, sel.get(), b.kadd, b.aw.get());
+        else fill_i32(st, b.aw.get(), b.kadd, 1);
+    }
+}
+
+// message format of _validate_batch (engine/interp.py:563-570)
+static void raise_validation(int err, unsigned long long idx, int64_t n, char kind, int64_t s, int64_t d) {
+    if (err & kBadKind)
+        throw GdError(GD_ERR_MALFORMED, "unknown update kind at record " + std::to_string(idx));
+    if (err & kBadNode)
+        throw GdError(GD_ERR_EXEC, std::string("update record ") + kind + " " + std::to_string(s) + " " +
+                                       std::to_string(d) + " references a node outside [0, " + std::to_string(n) +
+                                       ")");
+    if (err & kBadWeight)
+        throw GdError(GD_ERR_CONTRACT, "update record " + std::to_string(idx) +
+                                           ": weight outside the int32 range of the B200 layout");
+}
+
+void AlgoBase::stage_host(DevBatch& b, const uint8_t* kind, const int64_t* src, const int64_t* dst,
+                          const int64_t* w, int64_t k) {
+    cudaStream_t st = stream();
+    if (k == 0) {
+        b.kdel = b.kadd = 0;
+        return;
+    }
+    h_stage.ensure(3 * k, st);
+    k_stage.ensure(k, st);
+    GD_CUDA(cudaMemcpyAsync(h_stage.get(), src, k * 8, cudaMemcpyHostToDevice, st));
+    GD_CUDA(cudaMemcpyAsync(h_stage.get() + k, dst, k * 8, cudaMemcpyHostToDevice, st));
+    if (w) GD_CUDA(cudaMemcpyAsync(h_stage.get() + 2 * k, w, k * 8, cudaMemcpyHostToDevice, st));
+    GD_CUDA(cudaMemcpyAsync(k_stage.get(), kind, k, cudaMemcpyHostToDevice, st));
+    DBuf<int32_t> s(k, st), d(k, st), ww(k, st);
+    DBuf<uint8_t> flags(2 * k, st);
+    DBuf<int> err(1, st);
+    DBuf<unsigned long long> bad(1, st);
+    err.zero(st);
+    GD_CUDA(cudaMemsetAsync(bad.get(), 0xff, sizeof(unsigned long long), st));
+    GD_KERNEL(k_stage_host, grid_for(k, 256), 256, 0, st, k_stage.get(), h_stage.get(), h_stage.get() + k,
+              w ? h_stage.get() + 2 * k : nullptr, k, g->n, s.get(), d.get(), ww.get(), flags.get(),
+              flags.get() + k, err.get(), bad.get());
+    int e = read_scalar(st, err.get());
+    if (e) {
+        unsigned long long i = read_scalar(st, bad.get());
+        raise_validation(e, i, g->n, (char)kind[i], src[i], dst[i]);
+    }
+    split(b, flags.get(), s.get(), d.get(), ww.get(), k);
+}
+
+void AlgoBase::stage_device(DevBatch& b, const uint8_t* kind, const int32_t* src, const int32_t* dst,
+                            const int32_t* w, int64_t k) {
+    cudaStream_t st = stream();
+    if (k == 0) {
+        b.kdel = b.kadd = 0;
+        return;
+    }
+    DBuf<uint8_t> flags(2 * k, st);
+    DBuf<int> err(1, st);
+    DBuf<unsigned long long> bad(1, st);
+    err.zero(st);
+    GD_CUDA(cudaMemsetAsync(bad.get(), 0xff, sizeof(unsigned long long), st));
+    GD_KERNEL(k_stage_dev, grid_for(k, 256), 256, 0, st, kind, src, dst, k, g->n, flags.get(), flags.get() + k,
+              err.get(), bad.get());
+    int e = read_scalar(st, err.get());
+    if (e) {
+        unsigned long long i = read_scalar(st, bad.get());
+        raise_validation(e, i, g->n, (char)read_scalar(st, kind + i), read_scalar(st, src + i),
+                         read_scalar(st, dst + i));
+    }
+    split(b, flags.get(), src, dst, w, k);
+}
+
+// ---------------------------------------------------------------- degrees ---
+
+namespace {
+__global__ void k_out_degrees(OutView ov, int64_t n, int32_t* deg) {
+    // one thread per row for the count over all segments; warp-cooperative
+    // reading is not needed: rows are read once and coalescing across rows is
+    // poor only for long rows, which the warp path below handles.
+    const int lane = threadIdx.x & 31;
+    int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t v0 = warp * 32; v0 < n; v0 += nwarps * 32) {
+        // 32 consecutive rows per warp: each lane owns one row
+        int64_t v = v0 + lane;
+        int32_t d = 0;
+        if (v < n) {
+            for (int sg = 0; sg < ov.nseg; ++sg) {
+                const int64_t* off = ov.off[sg];
+                const int32_t* col = ov.col[sg];
+                for (int64_t i = off[v]; i < off[v + 1]; ++i) d += col[i] >= 0;
+            }
+            deg[v] = d;
+        }
+    }
+}
+}  // namespace
+
+void out_degrees(Store& g, int32_t* deg) {
+    if (g.n == 0) return;
+    GD_KERNEL(k_out_degrees, grid_for(g.n, 256), 256, 0, g.stream, g.out_view(), g.n, deg);
+}
+
+// ------------------------------------------------------------------ flood ---
+
+namespace {
+
+// Parents only ever decrease (a root is hooked under a smaller root), so the
+// walk terminates; path halving re-points each visited node at its
+// grandparent (atomicMin keeps concurrent halvings monotone).
+__device__ inline int32_t uf_find(int32_t* p, int32_t v) {
+    int32_t cur = v;
+    while (true) {
+        int32_t nx = p[cur];
+        if (nx == cur) return cur;
+        int32_t nn = p[nx];
+        if (nn < nx) atomicMin(&p[cur], nn);
+        cur = nx;
+    }
+}
+
+// hook the larger root under the smaller (deterministic result: roots are
+// component minima after compression)
+__device__ inline void uf_union(int32_t* p, int32_t a, int32_t b) {
+    while (true) {
+        a = uf_find(p, a);
+        b = uf_find(p, b);
+        if (a == b) return;
+        if (a > b) {
+            int32_t t = a;
+            a = b;
+            b = t;
+        }
+        // b is the larger root: try p[b] = a
+        int32_t old = atomicCAS(&p[b], b, a);
+        if (old == b) return;
+        b = old;
+    }
+}
+
+__global__ void k_uf_init(int32_t* p, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        p[i] = (int32_t)i;
+}
+
+// Rows are processed by 32-lane warps over the concatenated slot range of each
+// segment: every lane owns one slot, so reads are coalesced regardless of the
+// degree distribution.  The row of a slot comes from a per-warp search.
+__global__ void k_uf_hook(OutView ov, int64_t n, int32_t* p) {
+    const int lane = threadIdx.x & 31;
+    int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int sg = 0; sg < ov.nseg; ++sg) {
+        const int64_t* off = ov.off[sg];
+        const int32_t* col = ov.col[sg];
+        int64_t m = off[n];
+        for (int64_t base = warp * 32; base < m; base += nwarps * 32) {
+            int64_t i = base + lane;
+            int64_t last = min(base + 31, m - 1);
+            // rows of the first and last slot of the chunk bound every lane's search
+            int64_t r0 = 0, r1 = 0;
+            if (lane == 0) r0 = upper_bound_dev<int64_t>(off, 0, n + 1, base) - 1;
+            if (lane == 31) r1 = upper_bound_dev<int64_t>(off, 0, n + 1, last) - 1;
+            r0 = __shfl_sync(0xffffffffu, r0, 0);
+            r1 = __shfl_sync(0xffffffffu, r1, 31);
+            if (i >= m) continue;
+            int32_t c = col[i];
+            if (c < 0) continue;
+            int32_t r = (int32_t)(upper_bound_dev<int64_t>(off, r0, r1 + 1, i) - 1);
+            if (r != c) uf_union(p, r, c);
+        }
+    }
+}
+
+__global__ void k_uf_compress_seed(int32_t* p, int64_t n, const uint8_t* flags, uint8_t* root_has_seed) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        int32_t r = uf_find(p, (int32_t)i);
+        p[i] = r;
+        if (flags[i]) root_has_seed[r] = 1;
+    }
+}
+
+__global__ void k_uf_mark(const int32_t* p, int64_t n, const uint8_t* root_has_seed, uint8_t* flags) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        if (root_has_seed[p[i]]) flags[i] = 1;
+}
+
+}  // namespace
+
+int64_t flood_weak_components(Store& g, uint8_t* flags, KernelProf* prof) {
+    (void)prof;
+    cudaStream_t s = g.stream;
+    int64_t n = g.n;
+    if (n == 0) return 0;
+    DBuf<int32_t> p(n, s);
+    DBuf<uint8_t> seed(n, s);
+    seed.zero(s);
+    GD_KERNEL(k_uf_init, grid_for(n, 256), 256, 0, s, p.get(), n);
+    int64_t slots = g.total_slots();
+    GD_KERNEL_T("flood_hook", 0, k_uf_hook, grid_for(std::max<int64_t>(slots, 1), 256), 256, 0, s, g.out_view(), n,
+                p.get());
+    GD_KERNEL_T("flood_mark", 0, k_uf_compress_seed, grid_for(n, 256), 256, 0, s, p.get(), n, flags, seed.get());
+    GD_KERNEL(k_uf_mark, grid_for(n, 256), 256, 0, s, p.get(), n, seed.get(), flags);
+    return 1;
+}
+
+}  // namespace gdb

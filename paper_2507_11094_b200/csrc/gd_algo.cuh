@@ -1,0 +1,72 @@
+// gd_algo.cuh -- shared machinery of the three dynamic algorithms: batch
+// staging/validation, phase timing, kernel profiling, frontier queues and the
+// weak-component flood.
+#pragma once
+
+#include <map>
+#include <memory>
+#include <string>
+
+#include "gd_launch.cuh"
+#include "gd_store.cuh"
+
+namespace gdb {
+
+// One batch on the device, split by kind in stream order
+// (UpdateBatch.deletes / .adds, graph/updates.py:42-48).
+struct DevBatch {
+    DBuf<int32_t> ds, dd;      // deletes
+    DBuf<int32_t> as, ad, aw;  // adds
+    int64_t kdel = 0, kadd = 0;
+};
+
+enum AlgoKind { ALGO_SSSP = 1, ALGO_PR = 2, ALGO_TC = 3 };
+
+struct AlgoBase {
+    int kind;
+    Store* g;
+    PhaseTimer timer;
+    KernelProf prof;
+    int64_t iterations = 0;  // fixedPoint / while iterations, summed
+    explicit AlgoBase(int k, Store* st) : kind(k), g(st) { timer.s = st->stream; }
+    virtual ~AlgoBase() = default;
+    cudaStream_t stream() const { return g->stream; }
+
+    // Stage host records (int64, 'a'/'d'), validate like _validate_batch
+    // (engine/interp.py:563-570) and split by kind.  Throws GdError.
+    void stage_host(DevBatch& b, const uint8_t* kind, const int64_t* src, const int64_t* dst, const int64_t* w,
+                    int64_t k);
+    // Same from device int32 records.
+    void stage_device(DevBatch& b, const uint8_t* kind, const int32_t* src, const int32_t* dst, const int32_t* w,
+                      int64_t k);
+
+  private:
+    void split(DevBatch& b, const uint8_t* kind, const int32_t* s, const int32_t* d, const int32_t* w, int64_t k);
+    DBuf<int64_t> h_stage;  // reusable device staging for host uploads
+    DBuf<uint8_t> k_stage;
+};
+
+// ---- frontier queue ----------------------------------------------------------
+struct Frontier {
+    DBuf<int32_t> q[2];
+    DBuf<unsigned long long> cnt;  // [2]
+    int cur = 0;
+    void init(int64_t n, cudaStream_t s) {
+        q[0].ensure(n + 1, s);
+        q[1].ensure(n + 1, s);
+        cnt.ensure(2, s);
+    }
+};
+
+// Weak-component flood of true flags (engine/interp.py:70-109): a vertex ends
+// up flagged iff its weak component (over live arcs, either direction)
+// contains a flagged vertex.  Computed by union-find over the live out-arcs
+// instead of a level-synchronous BFS: same set, no diameter-bound rounds.
+// flags is an n-byte device array, updated in place.  Returns the number of
+// union-find hooking passes.
+int64_t flood_weak_components(Store& g, uint8_t* d_flags, KernelProf* prof);
+
+// out-degree (live arcs over all segments) per node, int32
+void out_degrees(Store& g, int32_t* deg);
+
+}  // namespace gdb

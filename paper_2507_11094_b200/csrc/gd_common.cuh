@@ -1,0 +1,208 @@
+// gd_common.cuh -- shared device types, error plumbing and primitives for the
+// B200 dynamic-graph path (sm_100a only).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/gd_capi.h"
+
+namespace gdb {
+
+// Device vertex ids are int32 (scale-26 = 67.1M < 2^31), offsets int64,
+// weights int32.  A deleted out-slot holds kSentinel (-1); it is exported as
+// INT64_MAX, the reference's SENTINEL (csr.py:14).
+constexpr int32_t kSentinel = -1;
+constexpr int64_t kInf = INT64_MAX;  // properties.py:20 INT_INF
+constexpr int kWarp = 32;
+constexpr int kSMs = 148;
+
+// Error carried from the device path to the C ABI (gd_capi.cu maps it to a
+// status code and gd_last_error()).
+struct GdError : std::runtime_error {
+    int code;
+    GdError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define GD_CUDA(call)                                                                               \
+    do {                                                                                            \
+        cudaError_t _e = (call);                                                                    \
+        if (_e != cudaSuccess)                                                                      \
+            throw ::gdb::GdError(GD_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(_e) + \
+                                                  " (" __FILE__ ":" + std::to_string(__LINE__) + ")"); \
+    } while (0)
+
+#define GD_LAUNCH_CHECK() GD_CUDA(cudaGetLastError())
+
+// Stream-ordered device buffer (cudaMallocAsync pool); freed on the stream.
+template <typename T>
+struct DBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    cudaStream_t s = nullptr;
+    DBuf() = default;
+    DBuf(size_t count, cudaStream_t st) { alloc(count, st); }
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    DBuf(DBuf&& o) noexcept : p(o.p), n(o.n), s(o.s) {
+        o.p = nullptr;
+        o.n = 0;
+    }
+    DBuf& operator=(DBuf&& o) noexcept {
+        if (this != &o) {
+            release();
+            p = o.p;
+            n = o.n;
+            s = o.s;
+            o.p = nullptr;
+            o.n = 0;
+        }
+        return *this;
+    }
+    ~DBuf() { release(); }
+    void alloc(size_t count, cudaStream_t st) {
+        release();
+        s = st;
+        n = count;
+        if (count) GD_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), st));
+    }
+    // grow-only reuse: keeps the allocation when large enough
+    void ensure(size_t count, cudaStream_t st) {
+        if (count > n || p == nullptr) alloc(count ? count : 1, st);
+    }
+    void release() {
+        if (p) cudaFreeAsync(p, s);
+        p = nullptr;
+        n = 0;
+    }
+    T* get() const { return p; }
+    void zero(cudaStream_t st) const {
+        if (n) GD_CUDA(cudaMemsetAsync(p, 0, n * sizeof(T), st));
+    }
+};
+
+inline unsigned grid_for(int64_t items, int block, int64_t cap = 148LL * 64) {
+    int64_t g = (items + block - 1) / block;
+    if (g < 1) g = 1;
+    if (g > cap) g = cap;
+    return static_cast<unsigned>(g);
+}
+
+__host__ __device__ inline int64_t sat_add(int64_t a, int64_t b) {  // graphdyn_rt.h:40-44
+    return (a >= kInf || b >= kInf) ? kInf : a + b;
+}
+
+// In-index tombstone: the entry keeps its (decodable) column so rows stay
+// sorted for binary search; tomb(c) = ~c is negative.
+__host__ __device__ inline int32_t tomb(int32_t c) { return ~c; }
+__host__ __device__ inline int32_t untomb(int32_t c) { return c < 0 ? ~c : c; }
+
+// 64-bit key of a directed pair (row, col), both non-negative int32.
+__host__ __device__ inline uint64_t pair_key(int32_t r, int32_t c) {
+    return (static_cast<uint64_t>(static_cast<uint32_t>(r)) << 32) | static_cast<uint32_t>(c);
+}
+__host__ __device__ inline int32_t key_row(uint64_t k) { return static_cast<int32_t>(k >> 32); }
+__host__ __device__ inline int32_t key_col(uint64_t k) { return static_cast<int32_t>(k & 0xffffffffu); }
+
+template <typename T>
+__device__ inline int64_t lower_bound_dev(const T* a, int64_t lo, int64_t hi, T x) {
+    while (lo < hi) {
+        int64_t m = (lo + hi) >> 1;
+        if (a[m] < x) lo = m + 1;
+        else hi = m;
+    }
+    return lo;
+}
+template <typename T>
+__device__ inline int64_t upper_bound_dev(const T* a, int64_t lo, int64_t hi, T x) {
+    while (lo < hi) {
+        int64_t m = (lo + hi) >> 1;
+        if (a[m] <= x) lo = m + 1;
+        else hi = m;
+    }
+    return lo;
+}
+// lower/upper bound on in-index columns, decoding tombstones
+__device__ inline int64_t col_lower(const int32_t* a, int64_t lo, int64_t hi, int32_t x) {
+    while (lo < hi) {
+        int64_t m = (lo + hi) >> 1;
+        if (untomb(a[m]) < x) lo = m + 1;
+        else hi = m;
+    }
+    return lo;
+}
+__device__ inline int64_t col_upper(const int32_t* a, int64_t lo, int64_t hi, int32_t x) {
+    while (lo < hi) {
+        int64_t m = (lo + hi) >> 1;
+        if (untomb(a[m]) <= x) lo = m + 1;
+        else hi = m;
+    }
+    return lo;
+}
+
+// ---- host-side primitive wrappers (CUB radix sort / scan / select) -----------
+// Implemented in gd_prims.cu.
+void sort_pairs_u64(cudaStream_t s, uint64_t* keys, int32_t* vals, int64_t n, int end_bit = 64);
+void sort_pairs_u32(cudaStream_t s, uint32_t* keys, int32_t* vals, int64_t n, int end_bit = 32);
+void sort_keys_u64(cudaStream_t s, uint64_t* keys, int64_t n, int end_bit = 64);
+void exclusive_scan_i64(cudaStream_t s, const int64_t* in, int64_t* out, int64_t n);
+void inclusive_scan_i64(cudaStream_t s, const int64_t* in, int64_t* out, int64_t n);
+int64_t sum_i64(cudaStream_t s, const int64_t* in, int64_t n);  // synchronous result
+// Compact indices i in [0, n) with flags[i] != 0 into out (ordered); returns count (sync).
+int64_t select_flagged_index(cudaStream_t s, const uint8_t* flags, int64_t n, int32_t* out);
+void iota_i32(cudaStream_t s, int32_t* a, int64_t n);
+void fill_i64(cudaStream_t s, int64_t* a, int64_t n, int64_t v);
+void fill_i32(cudaStream_t s, int32_t* a, int64_t n, int32_t v);
+template <typename T>
+inline T read_scalar(cudaStream_t s, const T* dptr) {
+    T h{};
+    GD_CUDA(cudaMemcpyAsync(&h, dptr, sizeof(T), cudaMemcpyDeviceToHost, s));
+    GD_CUDA(cudaStreamSynchronize(s));
+    return h;
+}
+
+// Phase timer with CUDA events on the handle's stream.  Phase names follow
+// the reference's ExecContext.add_phase (interp.py:141-145).
+enum Phase { PH_STATIC = 0, PH_PRE = 1, PH_STRUCT = 2, PH_PROP = 3, PH_MERGE = 4, PH_COUNT = 5 };
+
+struct PhaseTimer {
+    cudaStream_t s = nullptr;
+    std::vector<cudaEvent_t> evs;
+    std::vector<int> phases;
+    double total_ms[PH_COUNT] = {0, 0, 0, 0, 0};
+    int open = -1;
+    void begin(int ph) {
+        cudaEvent_t e;
+        GD_CUDA(cudaEventCreate(&e));
+        GD_CUDA(cudaEventRecord(e, s));
+        evs.push_back(e);
+        phases.push_back(ph);
+    }
+    // Called at a sync point: turn consecutive event pairs into phase times.
+    void end_all() {
+        cudaEvent_t e;
+        GD_CUDA(cudaEventCreate(&e));
+        GD_CUDA(cudaEventRecord(e, s));
+        evs.push_back(e);
+        phases.push_back(-1);
+        GD_CUDA(cudaEventSynchronize(e));
+        for (size_t i = 0; i + 1 < evs.size(); ++i) {
+            float ms = 0;
+            GD_CUDA(cudaEventElapsedTime(&ms, evs[i], evs[i + 1]));
+            if (phases[i] >= 0) total_ms[phases[i]] += ms;
+        }
+        for (auto ev : evs) cudaEventDestroy(ev);
+        evs.clear();
+        phases.clear();
+    }
+    ~PhaseTimer() {
+        for (auto ev : evs) cudaEventDestroy(ev);
+    }
+};
+
+}  // namespace gdb

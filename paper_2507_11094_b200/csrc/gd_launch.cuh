@@ -1,0 +1,68 @@
+// gd_launch.cuh -- kernel launch accounting and optional per-kernel event timing.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <map>
+#include <string>
+#include <vector>
+
+#include "gd_common.cuh"
+
+namespace gdb {
+
+void count_launch();          // one of our own kernels
+void count_library_launch();  // a CUB primitive call (sort / scan / select)
+int64_t launches_total();
+
+struct KernelStat {
+    double ms = 0;
+    int64_t launches = 0;
+    int64_t bytes = 0;
+};
+
+// Per-kernel CUDA-event timing on the launching stream.  Enabled per
+// algorithm handle (gd_set_profiling); the handle installs itself as the
+// thread's active profiler for the duration of an API call.
+struct KernelProf {
+    bool on = false;
+    struct Rec {
+        const char* name;
+        cudaEvent_t a, b;
+        int64_t bytes;
+    };
+    std::vector<Rec> pending;
+    std::map<std::string, KernelStat> last;  // stats of the last flushed call
+    void reset_last() { last.clear(); }
+    void flush();  // sync on the recorded events and fold them into `last`
+    ~KernelProf();
+};
+
+extern thread_local KernelProf* tl_prof;
+
+struct ProfScope {
+    KernelProf* prev;
+    explicit ProfScope(KernelProf* p) : prev(tl_prof) { tl_prof = p; }
+    ~ProfScope() { tl_prof = prev; }
+};
+
+int prof_begin(const char* name, int64_t bytes, cudaStream_t s);
+void prof_end(int idx, cudaStream_t s);
+
+}  // namespace gdb
+
+#define GD_KERNEL(kern, grid, block, smem, stream, ...)           \
+    do {                                                          \
+        kern<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__); \
+        ::gdb::count_launch();                                    \
+        GD_LAUNCH_CHECK();                                        \
+    } while (0)
+
+#define GD_KERNEL_T(name, bytes, kern, grid, block, smem, stream, ...)  \
+    do {                                                                \
+        int _pi = ::gdb::prof_begin((name), (bytes), (stream));         \
+        kern<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);       \
+        ::gdb::count_launch();                                          \
+        GD_LAUNCH_CHECK();                                              \
+        ::gdb::prof_end(_pi, (stream));                                 \
+    } while (0)

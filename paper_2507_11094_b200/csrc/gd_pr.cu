@@ -1,0 +1,295 @@
+// gd_pr.cu -- dynamic PageRank (programs/pr_dynamic.sp:7-102,
+// tests/golden/pr_dynamic_omp.cc:9-138) on the GPU store.
+//
+// Per batch: OnDelete/OnAdd bookkeeping (affected marks, +-1 out-degree for
+// every record, misses included), the structural update, merge-if-due, the
+// weak-component flood of `affected`, then the incremental power iteration
+// over the affected vertices only (dangling mass still summed over all V).
+// fp64 throughout; per-term values rank[u]/outdeg[u] are computed exactly as
+// the reference computes them, only the summation order differs.
+#include <cmath>
+
+#include "gd_algo.cuh"
+#include "gd_pr.cuh"
+
+namespace gdb {
+
+namespace {
+
+constexpr int kPullThreads = 256;
+constexpr int kGroup = 8;          // lanes per light vertex
+constexpr int kHeavyDeg = 8 * 64;  // rows longer than this go to the block kernel
+constexpr int kRedBlocks = 148 * 4;
+
+__global__ void k_pr_init(double* rank, int64_t n, double v) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        rank[i] = v;
+}
+
+// contrib[u] = rank[u] / outdeg[u]; per-block partial of the dangling sum
+// (outdeg == 0) -- pr_dynamic_omp.cc:68-73.
+__global__ void __launch_bounds__(256) k_pr_contrib(const double* rank, const int32_t* outdeg, int64_t n,
+                                                    double* contrib, double* partial) {
+    double acc = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        double r = rank[i];
+        int32_t d = outdeg[i];
+        contrib[i] = r / (double)d;
+        if (d == 0) acc += r;
+    }
+    __shared__ double sh[256 / 32];
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < 256 / 32; ++w) t += sh[w];
+        partial[blockIdx.x] = t;
+    }
+}
+
+// deterministic final sum of the partials (fixed order)
+__global__ void k_sum_partials(const double* partial, int np, double* out) {
+    __shared__ double sh[1024];
+    double t = 0.0;
+    for (int i = threadIdx.x; i < np; i += blockDim.x) t += partial[i];
+    sh[threadIdx.x] = t;
+    __syncthreads();
+    for (int s = blockDim.x / 2; s; s >>= 1) {
+        if ((int)threadIdx.x < s) sh[threadIdx.x] += sh[threadIdx.x + s];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *out = sh[0];
+}
+
+__device__ inline double atomic_max_pos(double* a, double v) {  // v >= 0
+    return __longlong_as_double(atomicMax(reinterpret_cast<long long*>(a), __double_as_longlong(v)));
+}
+
+// Light rows: a group of kGroup lanes per affected vertex pulls
+// sum(contrib[src]) over the in-arcs, then computes the new rank and |delta|
+// (pr_dynamic_omp.cc:75-98).
+__global__ void __launch_bounds__(kPullThreads) k_pr_pull_light(const int32_t* list, int64_t m, IdxView ix,
+                                                                  const double* contrib, const double* rank,
+                                                                  const double* dangling, double base,
+                                                                  double damping, double inv_n, double* rank_new,
+                                                                  double* diff) {
+    const int lane = threadIdx.x & (kGroup - 1);
+    const int gw = (threadIdx.x & 31) / kGroup;  // group within the warp
+    constexpr int kPerWarp = 32 / kGroup;
+    int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const double dn = *dangling * inv_n;
+    double dmax = 0.0;
+    for (int64_t t0 = warp * kPerWarp; t0 < m; t0 += nwarps * kPerWarp) {  // warp-uniform trip count
+        int64_t t = t0 + gw;
+        bool valid = t < m;
+        int32_t v = valid ? list[t] : 0;
+        int64_t a = valid ? ix.off[v] : 0, b = valid ? ix.off[v + 1] : 0;
+        double acc = 0.0;
+        for (int64_t e = a + lane; e < b; e += kGroup) {
+            int32_t u = ix.col[e];
+            if (u >= 0) acc += __ldg(&contrib[u]);
+        }
+#pragma unroll
+        for (int o = kGroup / 2; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o, kGroup);
+        if (valid && lane == 0) {
+            double nr = base + damping * (acc + dn);
+            double dl = fabs(nr - rank[v]);
+            dmax = fmax(dmax, dl);
+            rank_new[v] = nr;
+        }
+    }
+    for (int o = 16; o; o >>= 1) dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+    if ((threadIdx.x & 31) == 0 && dmax > 0.0) atomic_max_pos(diff, dmax);
+}
+
+// Heavy rows: one block per vertex.
+__global__ void __launch_bounds__(kPullThreads) k_pr_pull_heavy(const int32_t* list, int64_t m, IdxView ix,
+                                                                  const double* contrib, const double* rank,
+                                                                  const double* dangling, double base,
+                                                                  double damping, double inv_n, double* rank_new,
+                                                                  double* diff) {
+    __shared__ double sh[kPullThreads / 32];
+    const double dn = *dangling * inv_n;
+    for (int64_t t = blockIdx.x; t < m; t += gridDim.x) {
+        int32_t v = list[t];
+        int64_t a = ix.off[v], b = ix.off[v + 1];
+        double acc = 0.0;
+        for (int64_t e = a + threadIdx.x; e < b; e += blockDim.x) {
+            int32_t u = ix.col[e];
+            if (u >= 0) acc += __ldg(&contrib[u]);
+        }
+        for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double s = 0.0;
+            for (int w = 0; w < kPullThreads / 32; ++w) s += sh[w];
+            double nr = base + damping * (s + dn);
+            double dl = fabs(nr - rank[v]);
+            if (dl > 0.0) atomic_max_pos(diff, dl);
+            rank_new[v] = nr;
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void k_pr_commit(const int32_t* list, int64_t m, const double* rank_new, double* rank) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+        int32_t v = list[i];
+        rank[v] = rank_new[v];
+    }
+}
+
+// OnDelete / OnAdd handlers (pr_dynamic.sp:87-97): mark both endpoints,
+// outdeg[src] -= 1 (deletes, misses included) / += 1 (adds).
+__global__ void k_pr_onupdate(const int32_t* s, const int32_t* d, int64_t k, int32_t delta, uint8_t* affected,
+                              int32_t* outdeg) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < k; i += (int64_t)gridDim.x * blockDim.x) {
+        affected[s[i]] = 1;
+        affected[d[i]] = 1;
+        atomicAdd(&outdeg[s[i]], delta);
+    }
+}
+
+__global__ void k_heavy_flags(const int32_t* list, int64_t m, const int64_t* off, uint8_t* heavy, uint8_t* light) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+        int32_t v = list[i];
+        bool h = (off[v + 1] - off[v]) > kHeavyDeg;
+        heavy[i] = h;
+        light[i] = !h;
+    }
+}
+
+__global__ void k_gather_list(const int32_t* list, const int32_t* sel, int64_t m, int32_t* out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = list[sel[i]];
+}
+
+}  // namespace
+
+PR::PR(Store* st, double d, double b, int64_t mi) : AlgoBase(ALGO_PR, st), damping(d), beta(b), maxiter(mi) {
+    if (!st->with_reverse)
+        throw GdError(GD_ERR_CONFIG, "graph was loaded without reverse-adjacency maintenance");
+    cudaStream_t s = stream();
+    int64_t n = g->n;
+    rank.alloc(std::max<int64_t>(n, 1), s);
+    rank_new.alloc(std::max<int64_t>(n, 1), s);
+    contrib.alloc(std::max<int64_t>(n, 1), s);
+    outdeg.alloc(std::max<int64_t>(n, 1), s);
+    affected.alloc(std::max<int64_t>(n, 1), s);
+    partial.alloc(kRedBlocks, s);
+    scal.alloc(2, s);  // [0] dangling, [1] diff
+    ProfScope ps(&prof);
+    timer.begin(PH_STATIC);
+    if (n) {
+        GD_KERNEL(k_pr_init, grid_for(n, 256), 256, 0, s, rank.get(), n, 1.0 / (double)n);
+        out_degrees(*g, outdeg.get());
+    }
+    // staticPR: every node participates
+    DBuf<int32_t> all(n, s);
+    iota_i32(s, all.get(), n);
+    set_lists(all.get(), n);
+    power_loop();
+    timer.end_all();
+    prof.flush();
+}
+
+void PR::set_lists(const int32_t* list, int64_t m) {
+    cudaStream_t s = stream();
+    g->compact_rev();
+    light.alloc(m, s);
+    heavy.alloc(m, s);
+    nlight = nheavy = 0;
+    if (!m) return;
+    DBuf<uint8_t> hf(m, s), lf(m, s);
+    GD_KERNEL(k_heavy_flags, grid_for(m, 256), 256, 0, s, list, m, g->rev.off.get(), hf.get(), lf.get());
+    DBuf<int32_t> sel(m, s);
+    nheavy = select_flagged_index(s, hf.get(), m, sel.get());
+    if (nheavy) GD_KERNEL(k_gather_list, grid_for(nheavy, 256), 256, 0, s, list, sel.get(), nheavy, heavy.get());
+    nlight = select_flagged_index(s, lf.get(), m, sel.get());
+    if (nlight) GD_KERNEL(k_gather_list, grid_for(nlight, 256), 256, 0, s, list, sel.get(), nlight, light.get());
+}
+
+// while (diff >= beta && iter < maxiter) { dangling; pull; commit }
+void PR::power_loop() {
+    cudaStream_t s = stream();
+    int64_t n = g->n;
+    if (n == 0) return;
+    IdxView ix = g->rev.view();
+    const double base = (1.0 - damping) / (double)n;
+    const double inv_n = 1.0 / (double)n;
+    int64_t iter = 0;
+    double diff = beta + 1.0;
+    last_sweeps = 0;
+    while (diff >= beta && iter < maxiter) {
+        GD_KERNEL_T("pr_contrib", n * 20, k_pr_contrib, kRedBlocks, 256, 0, s, rank.get(), outdeg.get(), n,
+                    contrib.get(), partial.get());
+        GD_KERNEL(k_sum_partials, 1, 1024, 0, s, partial.get(), kRedBlocks, scal.get());
+        GD_CUDA(cudaMemsetAsync(scal.get() + 1, 0, sizeof(double), s));
+        if (nlight) {
+            int64_t groups = nlight;
+            unsigned grid = grid_for(groups * kGroup, kPullThreads, 148LL * 32);
+            GD_KERNEL_T("pr_pull", 0, k_pr_pull_light, grid, kPullThreads, 0, s, light.get(), nlight, ix,
+                        contrib.get(), rank.get(), scal.get(), base, damping, inv_n, rank_new.get(), scal.get() + 1);
+        }
+        if (nheavy)
+            GD_KERNEL_T("pr_pull_heavy", 0, k_pr_pull_heavy, (unsigned)std::min<int64_t>(nheavy, 148LL * 8),
+                        kPullThreads, 0, s, heavy.get(), nheavy, ix, contrib.get(), rank.get(), scal.get(), base,
+                        damping, inv_n, rank_new.get(), scal.get() + 1);
+        if (nlight) GD_KERNEL(k_pr_commit, grid_for(nlight, 256), 256, 0, s, light.get(), nlight, rank_new.get(), rank.get());
+        if (nheavy) GD_KERNEL(k_pr_commit, grid_for(nheavy, 256), 256, 0, s, heavy.get(), nheavy, rank_new.get(), rank.get());
+        diff = read_scalar(s, scal.get() + 1);
+        ++iter;
+    }
+    last_sweeps = iter;
+    iterations += iter;
+}
+
+void PR::batch(DevBatch& b, int64_t batch_index) {
+    cudaStream_t s = stream();
+    int64_t n = g->n;
+    ProfScope ps(&prof);
+    prof.reset_last();
+    timer.begin(PH_PRE);
+    affected.zero(s);
+    if (b.kdel) GD_KERNEL(k_pr_onupdate, grid_for(b.kdel, 256), 256, 0, s, b.ds.get(), b.dd.get(), b.kdel, -1,
+                          affected.get(), outdeg.get());
+    if (b.kadd) GD_KERNEL(k_pr_onupdate, grid_for(b.kadd, 256), 256, 0, s, b.as.get(), b.ad.get(), b.kadd, 1,
+                          affected.get(), outdeg.get());
+    timer.begin(PH_STRUCT);
+    g->apply_deletes(b.ds.get(), b.dd.get(), b.kdel, nullptr);
+    g->apply_adds(b.as.get(), b.ad.get(), b.aw.get(), b.kadd);
+    // merge-if-due runs before the recompute: it does not change the live
+    // multiset the recompute reads (interp.py:877-880 runs it after).
+    if (g->merge_due(batch_index)) {
+        timer.begin(PH_MERGE);
+        g->merge();
+    }
+    timer.begin(PH_PROP);
+    flood_weak_components(*g, affected.get(), &prof);
+    DBuf<int32_t> list(std::max<int64_t>(n, 1), s);
+    int64_t m = select_flagged_index(s, affected.get(), n, list.get());
+    last_affected = m;
+    set_lists(list.get(), m);
+    power_loop();
+    timer.end_all();
+    prof.flush();
+}
+
+void PR::read(double* h_rank, int64_t* h_outdeg) {
+    cudaStream_t s = stream();
+    int64_t n = g->n;
+    if (!n) return;
+    GD_CUDA(cudaMemcpyAsync(h_rank, rank.get(), n * 8, cudaMemcpyDeviceToHost, s));
+    if (h_outdeg) {
+        std::vector<int32_t> tmp(n);
+        GD_CUDA(cudaMemcpyAsync(tmp.data(), outdeg.get(), n * 4, cudaMemcpyDeviceToHost, s));
+        GD_CUDA(cudaStreamSynchronize(s));
+        for (int64_t i = 0; i < n; ++i) h_outdeg[i] = tmp[i];
+    }
+    GD_CUDA(cudaStreamSynchronize(s));
+}
+
+}  // namespace gdb

@@ -1,0 +1,27 @@
+// gd_pr.cuh -- dynamic PageRank state (programs/pr_dynamic.sp).
+#pragma once
+
+#include "gd_algo.cuh"
+
+namespace gdb {
+
+struct PR : AlgoBase {
+    double damping, beta;
+    int64_t maxiter;
+    DBuf<double> rank, rank_new, contrib, partial, scal;
+    DBuf<int32_t> outdeg;  // maintained per record (misses included), int32 on device
+    DBuf<uint8_t> affected;
+    DBuf<int32_t> light, heavy;
+    int64_t nlight = 0, nheavy = 0;
+    int64_t last_sweeps = 0, last_affected = 0;
+
+    PR(Store* st, double damping, double beta, int64_t maxiter);  // = staticPR
+    void batch(DevBatch& b, int64_t batch_index);                 // one Batch body
+    void read(double* rank, int64_t* outdeg);
+
+  private:
+    void set_lists(const int32_t* list, int64_t m);
+    void power_loop();
+};
+
+}  // namespace gdb

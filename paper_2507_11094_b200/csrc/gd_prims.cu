@@ -1,0 +1,130 @@
+// gd_prims.cu -- device-wide sort / scan / select primitives (CUB, stream-ordered).
+#include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
+
+#include "gd_common.cuh"
+#include "gd_launch.cuh"
+
+namespace gdb {
+
+namespace {
+struct Temp {
+    void* p = nullptr;
+    size_t bytes = 0;
+    cudaStream_t s;
+    Temp(size_t b, cudaStream_t st) : bytes(b), s(st) {
+        if (b) GD_CUDA(cudaMallocAsync(&p, b, st));
+    }
+    ~Temp() {
+        if (p) cudaFreeAsync(p, s);
+    }
+};
+}  // namespace
+
+void sort_pairs_u64(cudaStream_t s, uint64_t* keys, int32_t* vals, int64_t n, int end_bit) {
+    if (n <= 1) return;
+    DBuf<uint64_t> k2(n, s);
+    DBuf<int32_t> v2(n, s);
+    cub::DoubleBuffer<uint64_t> kb(keys, k2.get());
+    cub::DoubleBuffer<int32_t> vb(vals, v2.get());
+    size_t bytes = 0;
+    GD_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, kb, vb, n, 0, end_bit, s));
+    Temp t(bytes, s);
+    GD_CUDA(cub::DeviceRadixSort::SortPairs(t.p, bytes, kb, vb, n, 0, end_bit, s));
+    count_library_launch();
+    if (kb.Current() != keys) GD_CUDA(cudaMemcpyAsync(keys, kb.Current(), n * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
+    if (vb.Current() != vals) GD_CUDA(cudaMemcpyAsync(vals, vb.Current(), n * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+}
+
+void sort_pairs_u32(cudaStream_t s, uint32_t* keys, int32_t* vals, int64_t n, int end_bit) {
+    if (n <= 1) return;
+    DBuf<uint32_t> k2(n, s);
+    DBuf<int32_t> v2(n, s);
+    cub::DoubleBuffer<uint32_t> kb(keys, k2.get());
+    cub::DoubleBuffer<int32_t> vb(vals, v2.get());
+    size_t bytes = 0;
+    GD_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, kb, vb, n, 0, end_bit, s));
+    Temp t(bytes, s);
+    GD_CUDA(cub::DeviceRadixSort::SortPairs(t.p, bytes, kb, vb, n, 0, end_bit, s));
+    count_library_launch();
+    if (kb.Current() != keys) GD_CUDA(cudaMemcpyAsync(keys, kb.Current(), n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+    if (vb.Current() != vals) GD_CUDA(cudaMemcpyAsync(vals, vb.Current(), n * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+}
+
+void sort_keys_u64(cudaStream_t s, uint64_t* keys, int64_t n, int end_bit) {
+    if (n <= 1) return;
+    DBuf<uint64_t> k2(n, s);
+    cub::DoubleBuffer<uint64_t> kb(keys, k2.get());
+    size_t bytes = 0;
+    GD_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, bytes, kb, n, 0, end_bit, s));
+    Temp t(bytes, s);
+    GD_CUDA(cub::DeviceRadixSort::SortKeys(t.p, bytes, kb, n, 0, end_bit, s));
+    count_library_launch();
+    if (kb.Current() != keys) GD_CUDA(cudaMemcpyAsync(keys, kb.Current(), n * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
+}
+
+void exclusive_scan_i64(cudaStream_t s, const int64_t* in, int64_t* out, int64_t n) {
+    if (n <= 0) return;
+    size_t bytes = 0;
+    GD_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, n, s));
+    Temp t(bytes, s);
+    GD_CUDA(cub::DeviceScan::ExclusiveSum(t.p, bytes, in, out, n, s));
+    count_library_launch();
+}
+
+void inclusive_scan_i64(cudaStream_t s, const int64_t* in, int64_t* out, int64_t n) {
+    if (n <= 0) return;
+    size_t bytes = 0;
+    GD_CUDA(cub::DeviceScan::InclusiveSum(nullptr, bytes, in, out, n, s));
+    Temp t(bytes, s);
+    GD_CUDA(cub::DeviceScan::InclusiveSum(t.p, bytes, in, out, n, s));
+    count_library_launch();
+}
+
+int64_t sum_i64(cudaStream_t s, const int64_t* in, int64_t n) {
+    if (n <= 0) return 0;
+    DBuf<int64_t> o(1, s);
+    size_t bytes = 0;
+    GD_CUDA(cub::DeviceReduce::Sum(nullptr, bytes, in, o.get(), n, s));
+    Temp t(bytes, s);
+    GD_CUDA(cub::DeviceReduce::Sum(t.p, bytes, in, o.get(), n, s));
+    count_library_launch();
+    return read_scalar(s, o.get());
+}
+
+int64_t select_flagged_index(cudaStream_t s, const uint8_t* flags, int64_t n, int32_t* out) {
+    if (n <= 0) return 0;
+    DBuf<int64_t> cnt(1, s);
+    thrust::counting_iterator<int32_t> it(0);
+    size_t bytes = 0;
+    GD_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, it, flags, out, cnt.get(), n, s));
+    Temp t(bytes, s);
+    GD_CUDA(cub::DeviceSelect::Flagged(t.p, bytes, it, flags, out, cnt.get(), n, s));
+    count_library_launch();
+    return read_scalar(s, cnt.get());
+}
+
+__global__ void k_iota_i32(int32_t* a, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        a[i] = static_cast<int32_t>(i);
+}
+__global__ void k_fill_i64(int64_t* a, int64_t n, int64_t v) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        a[i] = v;
+}
+__global__ void k_fill_i32(int32_t* a, int64_t n, int32_t v) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        a[i] = v;
+}
+
+void iota_i32(cudaStream_t s, int32_t* a, int64_t n) {
+    if (n > 0) GD_KERNEL(k_iota_i32, grid_for(n, 256), 256, 0, s, a, n);
+}
+void fill_i64(cudaStream_t s, int64_t* a, int64_t n, int64_t v) {
+    if (n > 0) GD_KERNEL(k_fill_i64, grid_for(n, 256), 256, 0, s, a, n, v);
+}
+void fill_i32(cudaStream_t s, int32_t* a, int64_t n, int32_t v) {
+    if (n > 0) GD_KERNEL(k_fill_i32, grid_for(n, 256), 256, 0, s, a, n, v);
+}
+
+}  // namespace gdb

@@ -1,0 +1,1046 @@
+// gd_store.cu -- the GPU diff-CSR store.  See gd_store.cuh for the layout.
+//
+// Batch application is sort + segmented-scan shaped: records are radix-sorted
+// by (src, dst), each source's chain is scanned ONCE by one warp against the
+// sorted requests of that source, and the j-th record of a pair resolves to
+// the j-th live occurrence of that pair in chain order -- the exact outcome
+// of the reference's sequential per-record scans (dynamic.py:208-286).
+#include <algorithm>
+#include <cstring>
+
+#include "gd_launch.cuh"
+#include "gd_store.cuh"
+
+namespace gdb {
+
+namespace {
+
+constexpr int kChainShift = 40;  // chain position = seg << 40 | slot
+constexpr int64_t kSlotMask = (1LL << kChainShift) - 1;
+
+// ---------------------------------------------------------------- build ----
+
+__global__ void k_expand_edges(const int64_t* src, const int64_t* dst, const int64_t* w, int64_t m, bool directed,
+                               uint32_t* key, int32_t* val, int32_t* adst, int32_t* aw) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+        int32_t s = (int32_t)src[i], d = (int32_t)dst[i];
+        int32_t wi = w ? (int32_t)w[i] : 1;
+        if (directed) {
+            key[i] = (uint32_t)s;
+            val[i] = (int32_t)i;
+            adst[i] = d;
+            aw[i] = wi;
+        } else {  // dynamic.py:113-115: (src,dst) then (dst,src)
+            key[2 * i] = (uint32_t)s;
+            val[2 * i] = (int32_t)(2 * i);
+            adst[2 * i] = d;
+            aw[2 * i] = wi;
+            key[2 * i + 1] = (uint32_t)d;
+            val[2 * i + 1] = (int32_t)(2 * i + 1);
+            adst[2 * i + 1] = s;
+            aw[2 * i + 1] = wi;
+        }
+    }
+}
+
+// off[v] = number of sorted rows < v, via histogram + scan (rows need not be
+// sorted for the histogram).
+__global__ void k_hist_rows(const int32_t* rows, int64_t m, int64_t* cnt) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+        atomicAdd(reinterpret_cast<unsigned long long*>(&cnt[rows[i]]), 1ULL);
+}
+__global__ void k_hist_rows_u32(const uint32_t* rows, int64_t m, int64_t* cnt) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+        atomicAdd(reinterpret_cast<unsigned long long*>(&cnt[rows[i]]), 1ULL);
+}
+
+template <typename T>
+__global__ void k_gather(const T* in, const int32_t* idx, int64_t m, T* out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = in[idx[i]];
+}
+
+__global__ void k_key_split(const uint64_t* key, int64_t m, int32_t* row, int32_t* col) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+        if (row) row[i] = key_row(key[i]);
+        if (col) col[i] = key_col(key[i]);
+    }
+}
+
+void offsets_from_rows(cudaStream_t s, int64_t n, const int32_t* rows, int64_t m, DBuf<int64_t>& off) {
+    DBuf<int64_t> cnt(n + 1, s);
+    cnt.zero(s);
+    if (m) GD_KERNEL(k_hist_rows, grid_for(m, 256), 256, 0, s, rows, m, cnt.get());
+    off.alloc(n + 1, s);
+    exclusive_scan_i64(s, cnt.get(), off.get(), n + 1);
+}
+
+// ------------------------------------------------------- delete requests ----
+
+// Directed: key (s,d).  Undirected: key (min,max) -- records of one unordered
+// pair consume occurrences of both arcs in stream order (dynamic.py:221-234).
+__global__ void k_del_keys(const int32_t* s, const int32_t* d, int64_t k, bool directed, uint64_t* key,
+                           int32_t* val) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < k; i += (int64_t)gridDim.x * blockDim.x) {
+        int32_t a = s[i], b = d[i];
+        if (!directed && a > b) {
+            int32_t t = a;
+            a = b;
+            b = t;
+        }
+        key[i] = pair_key(a, b);
+        val[i] = (int32_t)i;
+    }
+}
+
+// Expand sorted records into directed requests (row, col, occurrence).
+__global__ void k_del_requests(const uint64_t* skey, const int32_t* srec, int64_t k, const int32_t* s,
+                               const int32_t* d, bool directed, uint64_t* rq_key, int32_t* rq_occ, int32_t* rq_rec,
+                               uint8_t* rq_which, int32_t* rq_ord) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < k; i += (int64_t)gridDim.x * blockDim.x) {
+        uint64_t key = skey[i];
+        int32_t j = (int32_t)(i - lower_bound_dev<uint64_t>(skey, 0, i, key));
+        int32_t r = srec[i];
+        int32_t a = s[r], b = d[r];
+        if (directed) {
+            rq_key[i] = pair_key(a, b);
+            rq_occ[i] = j;
+            rq_rec[i] = r;
+            rq_which[i] = 0;
+            rq_ord[i] = (int32_t)i;
+        } else {
+            int64_t o = 2 * i;
+            if (a != b) {
+                rq_key[o] = pair_key(a, b);
+                rq_occ[o] = j;
+                rq_key[o + 1] = pair_key(b, a);
+                rq_occ[o + 1] = j;
+            } else {  // self-loop: two slots per record (dynamic.py:231-234)
+                rq_key[o] = pair_key(a, a);
+                rq_occ[o] = 2 * j;
+                rq_key[o + 1] = pair_key(a, a);
+                rq_occ[o + 1] = 2 * j + 1;
+            }
+            rq_rec[o] = r;
+            rq_rec[o + 1] = r;
+            rq_which[o] = 0;
+            rq_which[o + 1] = 1;
+            rq_ord[o] = (int32_t)o;
+            rq_ord[o + 1] = (int32_t)(o + 1);
+        }
+    }
+}
+
+// first index of each row run in a (row,col)-sorted key array
+__global__ void k_row_starts(const uint64_t* key, int64_t m, uint8_t* flag) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+        flag[i] = (i == 0 || key_row(key[i]) != key_row(key[i - 1])) ? 1 : 0;
+}
+__global__ void k_row_starts_u32(const uint32_t* key, int64_t m, uint8_t* flag) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+        flag[i] = (i == 0 || key[i] != key[i - 1]) ? 1 : 0;
+}
+
+// One warp per requested source row: scan the chain (base, then deltas, in
+// slot order) once and emit every live slot whose column is requested.
+__global__ void k_del_scan(OutView ov, const int32_t* row_first, int64_t nrows, const uint64_t* rq_key,
+                           int64_t nrq, uint64_t* m_key, int64_t* m_pos, unsigned long long* m_cnt, int64_t cap) {
+    const int lane = threadIdx.x & 31;
+    int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t r = warp; r < nrows; r += nwarps) {
+        int64_t lo = row_first[r];
+        int64_t hi = (r + 1 < nrows) ? row_first[r + 1] : nrq;
+        int32_t row = key_row(rq_key[lo]);
+        uint64_t klo = pair_key(row, 0);
+        for (int sg = 0; sg < ov.nseg; ++sg) {
+            const int64_t* off = ov.off[sg];
+            const int32_t* col = ov.col[sg];
+            int64_t a = off[row], b = off[row + 1];
+            for (int64_t base = a; base < b; base += 32) {
+                int64_t i = base + lane;
+                bool hit = false;
+                int32_t c = -1;
+                if (i < b) {
+                    c = col[i];
+                    if (c >= 0) {
+                        uint64_t want = klo | (uint32_t)c;
+                        int64_t p = lower_bound_dev<uint64_t>(rq_key, lo, hi, want);
+                        hit = (p < hi && rq_key[p] == want);
+                    }
+                }
+                unsigned mask = __ballot_sync(0xffffffffu, hit);
+                if (mask) {
+                    unsigned long long basei = 0;
+                    if (lane == 0) basei = atomicAdd(m_cnt, (unsigned long long)__popc(mask));
+                    basei = __shfl_sync(0xffffffffu, basei, 0);
+                    if (hit) {
+                        int64_t slot = (int64_t)basei + __popc(mask & ((1u << lane) - 1));
+                        if (slot < cap) {
+                            m_key[slot] = klo | (uint32_t)c;
+                            m_pos[slot] = ((int64_t)sg << kChainShift) | i;
+                        }
+                    }
+                }
+            }
+        }
+    }
+}
+
+// Resolve each request against the (key, chain-pos)-sorted matches.
+__global__ void k_del_resolve(const uint64_t* rq_key, const int32_t* rq_occ, const int32_t* rq_rec,
+                              const uint8_t* rq_which, int64_t nrq, const uint64_t* m_key, const int64_t* m_pos,
+                              int64_t nm, int64_t* rq_pos, uint8_t* found_fwd) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nrq; i += (int64_t)gridDim.x * blockDim.x) {
+        uint64_t key = rq_key[i];
+        int64_t lo = lower_bound_dev<uint64_t>(m_key, 0, nm, key);
+        int64_t hi = upper_bound_dev<uint64_t>(m_key, lo, nm, key);
+        int64_t occ = rq_occ[i];
+        int64_t pos = (occ < hi - lo) ? m_pos[lo + occ] : -1;
+        rq_pos[i] = pos;
+        if (rq_which[i] == 0) found_fwd[rq_rec[i]] = pos >= 0 ? 1 : 0;
+    }
+}
+
+// Tombstone the resolved slots.  A reverse-direction request only applies
+// when its record's forward arc was found (dynamic.py:221-229).
+__global__ void k_del_kill(OutView ov, const uint64_t* rq_key, const int32_t* rq_rec, const uint8_t* rq_which,
+                           const int64_t* rq_pos, int64_t nrq, const uint8_t* found_fwd, int32_t* k_row,
+                           int32_t* k_col, int32_t* k_w, int64_t* k_pos, unsigned long long* k_cnt) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nrq; i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t pos = rq_pos[i];
+        if (pos < 0) continue;
+        if (rq_which[i] == 1 && !found_fwd[rq_rec[i]]) continue;
+        int sg = (int)(pos >> kChainShift);
+        int64_t slot = pos & kSlotMask;
+        int32_t* col = const_cast<int32_t*>(ov.col[sg]);
+        const int32_t* w = ov.w[sg];
+        int32_t c = col[slot];
+        int32_t wt = w ? w[slot] : 1;
+        col[slot] = kSentinel;
+        unsigned long long o = atomicAdd(k_cnt, 1ULL);
+        k_row[o] = key_row(rq_key[i]);
+        k_col[o] = c;
+        k_w[o] = wt;
+        k_pos[o] = pos;
+    }
+}
+
+// ---------------------------------------------------------------- adds -----
+
+__global__ void k_add_arcs(const int32_t* s, const int32_t* d, const int32_t* w, int64_t k, bool directed,
+                           uint32_t* key, int32_t* val, int32_t* a_row, int32_t* a_col, int32_t* a_w) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < k; i += (int64_t)gridDim.x * blockDim.x) {
+        int32_t wi = w ? w[i] : 1;
+        if (directed) {
+            key[i] = (uint32_t)s[i];
+            val[i] = (int32_t)i;
+            a_row[i] = s[i];
+            a_col[i] = d[i];
+            a_w[i] = wi;
+        } else {  // dynamic.py:177-183 _expand_arcs: (s,d) then (d,s)
+            key[2 * i] = (uint32_t)s[i];
+            val[2 * i] = (int32_t)(2 * i);
+            a_row[2 * i] = s[i];
+            a_col[2 * i] = d[i];
+            a_w[2 * i] = wi;
+            key[2 * i + 1] = (uint32_t)d[i];
+            val[2 * i + 1] = (int32_t)(2 * i + 1);
+            a_row[2 * i + 1] = d[i];
+            a_col[2 * i + 1] = s[i];
+            a_w[2 * i + 1] = wi;
+        }
+    }
+}
+
+// One warp per source row with inserts: list the first `want` vacancies of
+// the chain in slot order (ballot + prefix keeps the order).
+__global__ void k_add_vacancies(OutView ov, const uint32_t* skey, const int32_t* row_first, int64_t nrows,
+                                int64_t narcs, int64_t* vac_pos) {
+    const int lane = threadIdx.x & 31;
+    int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t r = warp; r < nrows; r += nwarps) {
+        int64_t lo = row_first[r];
+        int64_t hi = (r + 1 < nrows) ? row_first[r + 1] : narcs;
+        int32_t row = (int32_t)skey[lo];
+        int64_t want = hi - lo, got = 0;
+        for (int sg = 0; sg < ov.nseg && got < want; ++sg) {
+            const int64_t* off = ov.off[sg];
+            const int32_t* col = ov.col[sg];
+            int64_t a = off[row], b = off[row + 1];
+            for (int64_t base = a; base < b && got < want; base += 32) {
+                int64_t i = base + lane;
+                bool vac = (i < b) && col[i] < 0;
+                unsigned mask = __ballot_sync(0xffffffffu, vac);
+                if (vac) {
+                    int64_t t = got + __popc(mask & ((1u << lane) - 1));
+                    if (t < want) vac_pos[lo + t] = ((int64_t)sg << kChainShift) | i;
+                }
+                got += __popc(mask);
+            }
+        }
+    }
+}
+
+__global__ void k_add_claim(OutView ov, const int32_t* sval, const int32_t* a_row, const int32_t* a_col,
+                            const int32_t* a_w, const int64_t* vac_pos, int64_t narcs, uint8_t* leftover) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < narcs; i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t pos = vac_pos[i];
+        if (pos < 0) {
+            leftover[i] = 1;
+            continue;
+        }
+        leftover[i] = 0;
+        int32_t a = sval[i];
+        int sg = (int)(pos >> kChainShift);
+        int64_t slot = pos & kSlotMask;
+        const_cast<int32_t*>(ov.col[sg])[slot] = a_col[a];
+        if (ov.w[sg]) const_cast<int32_t*>(ov.w[sg])[slot] = a_w[a];
+    }
+}
+
+__global__ void k_gather_arcs(const int32_t* sel, int64_t m, const int32_t* sval, const int32_t* a_row,
+                              const int32_t* a_col, const int32_t* a_w, int32_t* o_row, int32_t* o_col,
+                              int32_t* o_w) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+        int32_t a = sval[sel ? sel[i] : i];
+        if (o_row) o_row[i] = a_row[a];
+        o_col[i] = a_col[a];
+        if (o_w) o_w[i] = a_w[a];
+    }
+}
+
+__global__ void k_tomb_still_dead(const int64_t* pos, int64_t m, const int32_t* col0, uint8_t* keep) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+        keep[i] = col0[pos[i]] < 0 ? 1 : 0;
+}
+
+// ----------------------------------------------------- index maintenance ----
+
+// For each killed arc, the index entry (ix_row, ix_col, w) it maps to.
+__global__ void k_kill_to_index(const int32_t* k_row, const int32_t* k_col, const int32_t* k_w, int64_t m,
+                                bool rows_are_dst, uint64_t* key, int32_t* val, int32_t* wkey) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+        int32_t r = rows_are_dst ? k_col[i] : k_row[i];
+        int32_t c = rows_are_dst ? k_row[i] : k_col[i];
+        key[i] = pair_key(r, c);
+        val[i] = (int32_t)i;
+        wkey[i] = k_w[i];
+    }
+}
+
+// Items sorted by (key, w); the j-th item of an equal (key, w) run tombstones
+// the j-th live entry with that column and weight in the (clean) row.
+__global__ void k_index_kill(const uint64_t* key, const int32_t* wk, int64_t m, int64_t* off, int32_t* col,
+                             const int32_t* w, int64_t* t_pos, int32_t* t_row, unsigned long long* t_cnt) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+        uint64_t kk = key[i];
+        int32_t wt = wk[i];
+        int64_t j = 0;
+        for (int64_t p = i - 1; p >= 0 && key[p] == kk && wk[p] == wt; --p) ++j;
+        int32_t r = key_row(kk), c = key_col(kk);
+        int64_t lo = col_lower(col, off[r], off[r + 1], c);
+        int64_t hi = col_upper(col, lo, off[r + 1], c);
+        for (int64_t e = lo; e < hi; ++e) {
+            int32_t v = col[e];
+            if (v < 0) continue;
+            if (w && w[e] != wt) continue;
+            if (j == 0) {
+                col[e] = tomb(v);
+                unsigned long long o = atomicAdd(t_cnt, 1ULL);
+                t_pos[o] = e;
+                t_row[o] = r;
+                break;
+            }
+            --j;
+        }
+    }
+}
+
+__global__ void k_added_to_index(const int32_t* a_row, const int32_t* a_col, int64_t m, bool rows_are_dst,
+                                  uint64_t* key, int32_t* val) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+        int32_t r = rows_are_dst ? a_col[i] : a_row[i];
+        int32_t c = rows_are_dst ? a_row[i] : a_col[i];
+        key[i] = pair_key(r, c);
+        val[i] = (int32_t)i;
+    }
+}
+
+// insertion point of delta entry (row, col) in the base: after equal columns
+__global__ void k_index_ins_pos(const int32_t* drow, const int32_t* dcol, int64_t m, const int64_t* off,
+                                const int32_t* col, int64_t* ipos) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+        int32_t r = drow[i];
+        ipos[i] = col_upper(col, off[r], off[r + 1], dcol[i]);
+    }
+}
+
+// out-store merge: delta arcs go after the base slots of their row
+__global__ void k_out_ins_pos(const int32_t* irow, int64_t m, const int64_t* off0, int64_t* ipos) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+        ipos[i] = off0[irow[i] + 1];
+}
+
+// row of every slot of a (small) delta segment, live flag
+__global__ void k_delta_rows(const int64_t* off, int64_t n, const int32_t* col, int64_t nslots, int32_t* row,
+                             uint8_t* live) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nslots;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        row[i] = (int32_t)(upper_bound_dev<int64_t>(off, 0, n + 1, i) - 1);
+        live[i] = col[i] >= 0 ? 1 : 0;
+    }
+}
+
+// --------------------------------------------------------- edit merge -----
+
+__global__ void k_shift_hist(const int32_t* trow, int64_t ntomb, const int32_t* irow, int64_t nins, int64_t* cnt) {
+    int64_t tot = ntomb + nins;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
+        if (i < ntomb)
+            atomicAdd(reinterpret_cast<unsigned long long*>(&cnt[trow[i]]), (unsigned long long)(-1LL));
+        else
+            atomicAdd(reinterpret_cast<unsigned long long*>(&cnt[irow[i - ntomb]]), 1ULL);
+    }
+}
+
+__global__ void k_add_offsets(const int64_t* off, const int64_t* shift, int64_t n1, int64_t* out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n1; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = off[i] + shift[i];
+}
+
+constexpr int kTile = 2048;
+constexpr int kEditThreads = 256;
+
+// Base entries: newpos(i) = i - #tombs(< i) + #inserts(P <= i).  Each CTA
+// owns a tile; it locates the tombs / inserts overlapping the tile once, so
+// per-entry searches run over the (usually empty) in-tile range.
+__global__ void __launch_bounds__(kEditThreads) k_edit_base(const int32_t* col, const int32_t* w, int64_t nnz,
+                                                            const int64_t* tpos, int64_t ntomb, const int64_t* ipos,
+                                                            int64_t nins, int32_t* ocol, int32_t* ow) {
+    __shared__ int64_t sh[4];
+    for (int64_t t0 = (int64_t)blockIdx.x * kTile; t0 < nnz; t0 += (int64_t)gridDim.x * kTile) {
+        int64_t t1 = min(t0 + (int64_t)kTile, nnz);
+        if (threadIdx.x == 0) {
+            sh[0] = lower_bound_dev<int64_t>(tpos, 0, ntomb, t0);
+            sh[1] = lower_bound_dev<int64_t>(tpos, sh[0], ntomb, t1);
+            sh[2] = upper_bound_dev<int64_t>(ipos, 0, nins, t0 - 1);  // #P <= t0-1
+            sh[3] = upper_bound_dev<int64_t>(ipos, sh[2], nins, t1 - 1);
+        }
+        __syncthreads();
+        int64_t tb0 = sh[0], tb1 = sh[1], pj0 = sh[2], pj1 = sh[3];
+        for (int64_t i = t0 + threadIdx.x; i < t1; i += blockDim.x) {
+            int32_t c = col[i];
+            if (c < 0) continue;
+            int64_t tb = (tb0 == tb1) ? tb0 : lower_bound_dev<int64_t>(tpos, tb0, tb1, i);
+            int64_t pj = (pj0 == pj1) ? pj0 : upper_bound_dev<int64_t>(ipos, pj0, pj1, i);
+            int64_t np = i - tb + pj;
+            ocol[np] = c;
+            if (ow) ow[np] = w[i];
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void k_edit_ins(const int32_t* icol, const int32_t* iw, const int64_t* ipos, int64_t nins,
+                           const int64_t* tpos, int64_t ntomb, int32_t* ocol, int32_t* ow) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < nins; j += (int64_t)gridDim.x * blockDim.x) {
+        int64_t p = ipos[j];
+        int64_t np = p - lower_bound_dev<int64_t>(tpos, 0, ntomb, p) + j;
+        ocol[np] = icol[j];
+        if (ow) ow[np] = iw ? iw[j] : 1;
+    }
+}
+
+__global__ void k_export_seg(const int32_t* col, const int32_t* w, int64_t m, int64_t* ocol, int64_t* ow) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+        int32_t c = col[i];
+        ocol[i] = c < 0 ? INT64_MAX : (int64_t)c;
+        ow[i] = w ? (int64_t)w[i] : 1;
+    }
+}
+
+__global__ void k_live_flags(const int32_t* col, int64_t m, uint8_t* f) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+        f[i] = col[i] >= 0 ? 1 : 0;
+}
+
+}  // namespace
+
+// ==========================================================================
+
+void edit_merge(cudaStream_t s, int64_t n, const int64_t* off, const int32_t* col, const int32_t* w, int64_t nnz,
+                const int64_t* tpos, const int32_t* trow, int64_t ntomb, const int32_t* irow, const int32_t* icol,
+                const int32_t* iw, const int64_t* ipos, int64_t nins, DBuf<int64_t>& new_off,
+                DBuf<int32_t>& new_col, DBuf<int32_t>& new_w, int64_t& new_nnz, bool weighted) {
+    new_nnz = nnz - ntomb + nins;
+    DBuf<int64_t> cnt(n + 1, s);
+    cnt.zero(s);
+    if (ntomb + nins)
+        GD_KERNEL(k_shift_hist, grid_for(ntomb + nins, 256), 256, 0, s, trow, ntomb, irow, nins, cnt.get());
+    DBuf<int64_t> shift(n + 1, s);
+    exclusive_scan_i64(s, cnt.get(), shift.get(), n + 1);
+    new_off.alloc(n + 1, s);
+    GD_KERNEL(k_add_offsets, grid_for(n + 1, 256), 256, 0, s, off, shift.get(), n + 1, new_off.get());
+    new_col.alloc(new_nnz, s);
+    if (weighted) new_w.alloc(new_nnz, s);
+    else new_w.release();
+    if (nnz) {
+        unsigned g = (unsigned)std::min<int64_t>((nnz + kTile - 1) / kTile, 148LL * 16);
+        GD_KERNEL_T("merge_copy", 0, k_edit_base, g, kEditThreads, 0, s, col, weighted ? w : nullptr, nnz, tpos,
+                    ntomb, ipos, nins, new_col.get(), weighted ? new_w.get() : nullptr);
+    }
+    if (nins)
+        GD_KERNEL(k_edit_ins, grid_for(nins, 256), 256, 0, s, icol, iw, ipos, nins, tpos, ntomb, new_col.get(),
+                  weighted ? new_w.get() : nullptr);
+}
+
+// ==========================================================================
+
+Store::Store(int dev, int64_t n_, const int64_t* src, const int64_t* dst, const int64_t* w, int64_t m, bool dir,
+             bool wtd, bool with_rev, int64_t mi, bool as_arcs)
+    : device(dev), n(n_), directed(dir), weighted(wtd), with_reverse(with_rev), merge_interval(mi) {
+    GD_CUDA(cudaSetDevice(device));
+    GD_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    cudaStream_t s = stream;
+    bool expand = !directed && !as_arcs;
+    int64_t na = expand ? 2 * m : m;
+    // host edge arrays -> device (int64 as given; converted in the expand kernel)
+    DBuf<int64_t> hs(m, s), hd(m, s), hw(w ? m : 0, s);
+    if (m) {
+        GD_CUDA(cudaMemcpyAsync(hs.get(), src, m * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+        GD_CUDA(cudaMemcpyAsync(hd.get(), dst, m * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+        if (w) GD_CUDA(cudaMemcpyAsync(hw.get(), w, m * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    }
+    DBuf<uint32_t> key(na, s);
+    DBuf<int32_t> val(na, s), adst(na, s), aw(na, s);
+    if (m)
+        GD_KERNEL(k_expand_edges, grid_for(m, 256), 256, 0, s, hs.get(), hd.get(), w ? hw.get() : nullptr, m,
+                  !expand, key.get(), val.get(), adst.get(), aw.get());
+    // stable sort by source keeps insertion order within a source (dynamic.py:116)
+    sort_pairs_u32(s, key.get(), val.get(), na);
+    OutSeg base;
+    base.nslots = na;
+    base.col.alloc(na, s);
+    if (weighted) base.w.alloc(na, s);
+    if (na) {
+        GD_KERNEL(k_gather<int32_t>, grid_for(na, 256), 256, 0, s, adst.get(), val.get(), na, base.col.get());
+        if (weighted) GD_KERNEL(k_gather<int32_t>, grid_for(na, 256), 256, 0, s, aw.get(), val.get(), na, base.w.get());
+    }
+    {
+        DBuf<int64_t> cnt(n + 1, s);
+        cnt.zero(s);
+        if (na) GD_KERNEL(k_hist_rows_u32, grid_for(na, 256), 256, 0, s, key.get(), na, cnt.get());
+        base.off.alloc(n + 1, s);
+        exclusive_scan_i64(s, cnt.get(), base.off.get(), n + 1);
+    }
+    segs.push_back(std::move(base));
+    live = na;
+    upload_tables();
+    if (with_reverse) build_index(rev, true);
+    GD_CUDA(cudaStreamSynchronize(s));
+}
+
+Store::~Store() {
+    if (stream) {
+        cudaSetDevice(device);
+        segs.clear();
+        cudaStreamSynchronize(stream);
+    }
+}
+
+void Store::upload_tables() {
+    std::vector<const int64_t*> o;
+    std::vector<const int32_t*> c, w;
+    for (auto& sg : segs) {
+        o.push_back(sg.off.get());
+        c.push_back(sg.col.get());
+        w.push_back(sg.w.n ? sg.w.get() : nullptr);
+    }
+    size_t k = segs.size();
+    tab_off.ensure(k, stream);
+    tab_col.ensure(k, stream);
+    tab_w.ensure(k, stream);
+    GD_CUDA(cudaMemcpyAsync(tab_off.get(), o.data(), k * sizeof(void*), cudaMemcpyHostToDevice, stream));
+    GD_CUDA(cudaMemcpyAsync(tab_col.get(), c.data(), k * sizeof(void*), cudaMemcpyHostToDevice, stream));
+    GD_CUDA(cudaMemcpyAsync(tab_w.get(), w.data(), k * sizeof(void*), cudaMemcpyHostToDevice, stream));
+    // the host vectors die at scope exit: make the copies complete first
+    GD_CUDA(cudaStreamSynchronize(stream));
+}
+
+OutView Store::out_view() const {
+    return OutView{(int)segs.size(), tab_off.get(), tab_col.get(), tab_w.get()};
+}
+
+int64_t Store::total_slots() const {
+    int64_t t = 0;
+    for (auto& sg : segs) t += sg.nslots;
+    return t;
+}
+
+int64_t Store::device_bytes() const {
+    int64_t b = 0;
+    for (auto& sg : segs) b += (int64_t)(sg.off.n * 8 + sg.col.n * 4 + sg.w.n * 4);
+    for (const SortedIndex* ix : {&rev, &fwd})
+        b += (int64_t)(ix->off.n * 8 + ix->col.n * 4 + ix->w.n * 4 + ix->dcol.n * 12 + ix->tpos.n * 12);
+    return b;
+}
+
+// Build a sorted index from the current live out-arcs (all segments).
+void Store::build_index(SortedIndex& ix, bool rows_are_dst) {
+    cudaStream_t s = stream;
+    ix.rows_are_dst = rows_are_dst;
+    // gather live arcs (row, col, w) of every segment
+    int64_t tot = total_slots();
+    DBuf<uint64_t> key(tot, s);
+    DBuf<int32_t> val(tot, s), wv(tot, s);
+    int64_t m = 0;
+    for (auto& sg : segs) {
+        if (!sg.nslots) continue;
+        DBuf<int32_t> row(sg.nslots, s);
+        DBuf<uint8_t> livef(sg.nslots, s);
+        GD_KERNEL(k_delta_rows, grid_for(sg.nslots, 256), 256, 0, s, sg.off.get(), n, sg.col.get(), sg.nslots,
+                  row.get(), livef.get());
+        DBuf<int32_t> sel(sg.nslots, s);
+        int64_t c = select_flagged_index(s, livef.get(), sg.nslots, sel.get());
+        if (!c) continue;
+        AddedArcs tmp;
+        tmp.row.alloc(c, s);
+        tmp.col.alloc(c, s);
+        tmp.w.alloc(c, s);
+        GD_KERNEL(k_gather<int32_t>, grid_for(c, 256), 256, 0, s, row.get(), sel.get(), c, tmp.row.get());
+        GD_KERNEL(k_gather<int32_t>, grid_for(c, 256), 256, 0, s, sg.col.get(), sel.get(), c, tmp.col.get());
+        if (weighted)
+            GD_KERNEL(k_gather<int32_t>, grid_for(c, 256), 256, 0, s, sg.w.get(), sel.get(), c, tmp.w.get());
+        else
+            fill_i32(s, tmp.w.get(), c, 1);
+        GD_KERNEL(k_added_to_index, grid_for(c, 256), 256, 0, s, tmp.row.get(), tmp.col.get(), c, rows_are_dst,
+                  key.get() + m, val.get() + m);
+        GD_CUDA(cudaMemcpyAsync(wv.get() + m, tmp.w.get(), c * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+        m += c;
+    }
+    // val = position in the concatenation (indexes wv); the key carries (row, col)
+    iota_i32(s, val.get(), m);
+    sort_pairs_u64(s, key.get(), val.get(), m);
+    ix.nnz = m;
+    ix.col.alloc(m, s);
+    DBuf<int32_t> rows(m, s);
+    if (m) GD_KERNEL(k_key_split, grid_for(m, 256), 256, 0, s, key.get(), m, rows.get(), ix.col.get());
+    if (weighted) {
+        ix.w.alloc(m, s);
+        if (m) GD_KERNEL(k_gather<int32_t>, grid_for(m, 256), 256, 0, s, wv.get(), val.get(), m, ix.w.get());
+    } else {
+        ix.w.release();
+    }
+    offsets_from_rows(s, n, rows.get(), m, ix.off);
+    ix.ntomb = 0;
+    ix.dnnz = 0;
+    ix.built = true;
+}
+
+void Store::require_rev() {
+    if (!rev.built) build_index(rev, true);
+}
+void Store::require_fwd() {
+    if (!fwd.built) build_index(fwd, false);
+}
+
+// Fold tombstones and the delta into a clean index.
+void Store::compact_index(SortedIndex& ix) {
+    if (!ix.built || !ix.dirty()) return;
+    cudaStream_t s = stream;
+    DBuf<int64_t> ipos(ix.dnnz, s);
+    if (ix.dnnz)
+        GD_KERNEL(k_index_ins_pos, grid_for(ix.dnnz, 256), 256, 0, s, ix.drow.get(), ix.dcol.get(), ix.dnnz,
+                  ix.off.get(), ix.col.get(), ipos.get());
+    DBuf<int64_t> noff;
+    DBuf<int32_t> ncol, nw;
+    int64_t nnz2 = 0;
+    edit_merge(s, n, ix.off.get(), ix.col.get(), ix.w.n ? ix.w.get() : nullptr, ix.nnz, ix.tpos.get(),
+               ix.trow.get(), ix.ntomb, ix.drow.get(), ix.dcol.get(), ix.dw.n ? ix.dw.get() : nullptr, ipos.get(),
+               ix.dnnz, noff, ncol, nw, nnz2, weighted);
+    ix.off = std::move(noff);
+    ix.col = std::move(ncol);
+    ix.w = std::move(nw);
+    ix.nnz = nnz2;
+    ix.ntomb = 0;
+    ix.dnnz = 0;
+    ix.tpos.release();
+    ix.trow.release();
+    ix.drow.release();
+    ix.dcol.release();
+    ix.dw.release();
+}
+
+void Store::index_delete(SortedIndex& ix, const KilledArcs& ka) {
+    if (!ix.built || ka.count == 0) return;
+    cudaStream_t s = stream;
+    int64_t m = ka.count;
+    DBuf<uint64_t> key(m, s);
+    DBuf<int32_t> val(m, s), wk(m, s);
+    GD_KERNEL(k_kill_to_index, grid_for(m, 256), 256, 0, s, ka.row.get(), ka.col.get(), ka.w.get(), m,
+              ix.rows_are_dst, key.get(), val.get(), wk.get());
+    // order by (key, w): stable sort by w, then by key
+    {
+        DBuf<uint32_t> wkey(m, s);
+        GD_CUDA(cudaMemcpyAsync(wkey.get(), wk.get(), m * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+        DBuf<int32_t> perm(m, s);
+        iota_i32(s, perm.get(), m);
+        sort_pairs_u32(s, wkey.get(), perm.get(), m);  // weights are >= 0 here
+        DBuf<uint64_t> k2(m, s);
+        GD_KERNEL(k_gather<uint64_t>, grid_for(m, 256), 256, 0, s, key.get(), perm.get(), m, k2.get());
+        sort_pairs_u64(s, k2.get(), perm.get(), m);
+        DBuf<int32_t> w2(m, s);
+        GD_KERNEL(k_gather<int32_t>, grid_for(m, 256), 256, 0, s, wk.get(), perm.get(), m, w2.get());
+        key = std::move(k2);
+        wk = std::move(w2);
+    }
+    // append to the index tomb log
+    int64_t old = ix.ntomb;
+    DBuf<int64_t> tpos(old + m, s);
+    DBuf<int32_t> trow(old + m, s);
+    if (old) {
+        GD_CUDA(cudaMemcpyAsync(tpos.get(), ix.tpos.get(), old * 8, cudaMemcpyDeviceToDevice, s));
+        GD_CUDA(cudaMemcpyAsync(trow.get(), ix.trow.get(), old * 4, cudaMemcpyDeviceToDevice, s));
+    }
+    DBuf<unsigned long long> cnt(1, s);
+    cnt.zero(s);
+    GD_KERNEL(k_index_kill, grid_for(m, 256), 256, 0, s, key.get(), wk.get(), m, ix.off.get(), ix.col.get(),
+              ix.w.n ? ix.w.get() : nullptr, tpos.get() + old, trow.get() + old, cnt.get());
+    int64_t killed = (int64_t)read_scalar(s, cnt.get());
+    int64_t tot = old + killed;
+    // keep the log sorted by position
+    DBuf<uint64_t> pk(tot, s);
+    GD_CUDA(cudaMemcpyAsync(pk.get(), tpos.get(), tot * 8, cudaMemcpyDeviceToDevice, s));
+    sort_pairs_u64(s, pk.get(), trow.get(), tot);
+    GD_CUDA(cudaMemcpyAsync(tpos.get(), pk.get(), tot * 8, cudaMemcpyDeviceToDevice, s));
+    ix.tpos = std::move(tpos);
+    ix.trow = std::move(trow);
+    ix.ntomb = tot;
+}
+
+void Store::index_add(SortedIndex& ix, const AddedArcs& aa) {
+    if (!ix.built || aa.count == 0) return;
+    if (ix.dnnz) compact_index(ix);  // keep at most one delta
+    cudaStream_t s = stream;
+    int64_t m = aa.count;
+    DBuf<uint64_t> key(m, s);
+    DBuf<int32_t> val(m, s);
+    GD_KERNEL(k_added_to_index, grid_for(m, 256), 256, 0, s, aa.row.get(), aa.col.get(), m, ix.rows_are_dst,
+              key.get(), val.get());
+    sort_pairs_u64(s, key.get(), val.get(), m);
+    ix.drow.alloc(m, s);
+    ix.dcol.alloc(m, s);
+    GD_KERNEL(k_key_split, grid_for(m, 256), 256, 0, s, key.get(), m, ix.drow.get(), ix.dcol.get());
+    if (weighted) {
+        ix.dw.alloc(m, s);
+        GD_KERNEL(k_gather<int32_t>, grid_for(m, 256), 256, 0, s, aa.w.get(), val.get(), m, ix.dw.get());
+    }
+    ix.dnnz = m;
+}
+
+void Store::append_out_tombs(const int64_t* d_pos, const int32_t* d_row, int64_t cnt) {
+    if (!cnt) return;
+    cudaStream_t s = stream;
+    int64_t tot = notomb + cnt;
+    DBuf<uint64_t> pk(tot, s);
+    DBuf<int32_t> rw(tot, s);
+    if (notomb) {
+        GD_CUDA(cudaMemcpyAsync(pk.get(), otpos.get(), notomb * 8, cudaMemcpyDeviceToDevice, s));
+        GD_CUDA(cudaMemcpyAsync(rw.get(), otrow.get(), notomb * 4, cudaMemcpyDeviceToDevice, s));
+    }
+    GD_CUDA(cudaMemcpyAsync(pk.get() + notomb, d_pos, cnt * 8, cudaMemcpyDeviceToDevice, s));
+    GD_CUDA(cudaMemcpyAsync(rw.get() + notomb, d_row, cnt * 4, cudaMemcpyDeviceToDevice, s));
+    sort_pairs_u64(s, pk.get(), rw.get(), tot);
+    otpos.alloc(tot, s);
+    GD_CUDA(cudaMemcpyAsync(otpos.get(), pk.get(), tot * 8, cudaMemcpyDeviceToDevice, s));
+    otrow = std::move(rw);
+    notomb = tot;
+}
+
+namespace {
+__global__ void k_select_base_kills(const int64_t* pos, const int32_t* row, int64_t m, uint8_t* flag) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+        flag[i] = (pos[i] >> kChainShift) == 0 ? 1 : 0;
+}
+template <typename T>
+__global__ void k_gather_sel(const T* in, const int32_t* sel, int64_t m, T* out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = in[sel[i]];
+}
+}  // namespace
+
+int64_t Store::apply_deletes(const int32_t* d_src, const int32_t* d_dst, int64_t k, uint8_t* d_found) {
+    cudaStream_t s = stream;
+    if (k == 0) return 0;
+    if (rev.built) compact_index(rev);
+    if (fwd.built) compact_index(fwd);
+    DBuf<uint64_t> skey(k, s);
+    DBuf<int32_t> srec(k, s);
+    GD_KERNEL(k_del_keys, grid_for(k, 256), 256, 0, s, d_src, d_dst, k, directed, skey.get(), srec.get());
+    sort_pairs_u64(s, skey.get(), srec.get(), k);
+    int64_t nrq = directed ? k : 2 * k;
+    DBuf<uint64_t> rq_key(nrq, s);
+    DBuf<int32_t> rq_occ(nrq, s), rq_rec(nrq, s), rq_ord(nrq, s);
+    DBuf<uint8_t> rq_which(nrq, s);
+    GD_KERNEL(k_del_requests, grid_for(k, 256), 256, 0, s, skey.get(), srec.get(), k, d_src, d_dst, directed,
+              rq_key.get(), rq_occ.get(), rq_rec.get(), rq_which.get(), rq_ord.get());
+    if (!directed) {  // order the requests by directed key (stable: occ order kept)
+        sort_pairs_u64(s, rq_key.get(), rq_ord.get(), nrq);
+        DBuf<int32_t> o2(nrq, s), r2(nrq, s);
+        DBuf<uint8_t> w2(nrq, s);
+        GD_KERNEL(k_gather_sel<int32_t>, grid_for(nrq, 256), 256, 0, s, rq_occ.get(), rq_ord.get(), nrq, o2.get());
+        GD_KERNEL(k_gather_sel<int32_t>, grid_for(nrq, 256), 256, 0, s, rq_rec.get(), rq_ord.get(), nrq, r2.get());
+        GD_KERNEL(k_gather_sel<uint8_t>, grid_for(nrq, 256), 256, 0, s, rq_which.get(), rq_ord.get(), nrq,
+                  w2.get());
+        rq_occ = std::move(o2);
+        rq_rec = std::move(r2);
+        rq_which = std::move(w2);
+    }
+    // distinct source rows
+    DBuf<uint8_t> rflag(nrq, s);
+    GD_KERNEL(k_row_starts, grid_for(nrq, 256), 256, 0, s, rq_key.get(), nrq, rflag.get());
+    DBuf<int32_t> row_first(nrq, s);
+    int64_t nrows = select_flagged_index(s, rflag.get(), nrq, row_first.get());
+    // scan chains, collect matches (retry once with the exact size on overflow)
+    OutView ov = out_view();
+    int64_t cap = 2 * nrq + 1024;
+    DBuf<uint64_t> m_key;
+    DBuf<int64_t> m_pos;
+    DBuf<unsigned long long> m_cnt(1, s);
+    int64_t nm = 0;
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        m_key.alloc(cap, s);
+        m_pos.alloc(cap, s);
+        m_cnt.zero(s);
+        GD_KERNEL_T("del_scan", 0, k_del_scan, grid_for(nrows * 32, 256, 148LL * 32), 256, 0, s, ov,
+                    row_first.get(), nrows, rq_key.get(), nrq, m_key.get(), m_pos.get(), m_cnt.get(), cap);
+        nm = (int64_t)read_scalar(s, m_cnt.get());
+        if (nm <= cap) break;
+        cap = nm;
+    }
+    // order matches by (key, chain position): LSD = sort by pos, then stable by key
+    {
+        DBuf<int32_t> perm(nm, s);
+        iota_i32(s, perm.get(), nm);
+        DBuf<uint64_t> pk(nm, s);
+        GD_CUDA(cudaMemcpyAsync(pk.get(), m_pos.get(), nm * 8, cudaMemcpyDeviceToDevice, s));
+        sort_pairs_u64(s, pk.get(), perm.get(), nm);
+        DBuf<uint64_t> k2(nm, s);
+        if (nm) GD_KERNEL(k_gather<uint64_t>, grid_for(nm, 256), 256, 0, s, m_key.get(), perm.get(), nm, k2.get());
+        sort_pairs_u64(s, k2.get(), perm.get(), nm);
+        DBuf<int64_t> p2(nm, s);
+        if (nm) GD_KERNEL(k_gather<int64_t>, grid_for(nm, 256), 256, 0, s, m_pos.get(), perm.get(), nm, p2.get());
+        m_key = std::move(k2);
+        m_pos = std::move(p2);
+    }
+    DBuf<int64_t> rq_pos(nrq, s);
+    DBuf<uint8_t> found_local;
+    uint8_t* found = d_found;
+    if (!found) {
+        found_local.alloc(k, s);
+        found = found_local.get();
+    }
+    GD_CUDA(cudaMemsetAsync(found, 0, k, s));
+    GD_KERNEL(k_del_resolve, grid_for(nrq, 256), 256, 0, s, rq_key.get(), rq_occ.get(), rq_rec.get(),
+              rq_which.get(), nrq, m_key.get(), m_pos.get(), nm, rq_pos.get(), found);
+    KilledArcs ka;
+    ka.row.alloc(nrq, s);
+    ka.col.alloc(nrq, s);
+    ka.w.alloc(nrq, s);
+    DBuf<int64_t> kpos(nrq, s);
+    DBuf<unsigned long long> kcnt(1, s);
+    kcnt.zero(s);
+    GD_KERNEL(k_del_kill, grid_for(nrq, 256), 256, 0, s, ov, rq_key.get(), rq_rec.get(), rq_which.get(),
+              rq_pos.get(), nrq, found, ka.row.get(), ka.col.get(), ka.w.get(), kpos.get(), kcnt.get());
+    ka.count = (int64_t)read_scalar(s, kcnt.get());
+    live -= ka.count;
+    // applied = records whose forward arc was found
+    int64_t applied = 0;
+    {
+        DBuf<int32_t> tmp(k, s);
+        applied = select_flagged_index(s, found, k, tmp.get());
+    }
+    // base-segment tombstones -> merge log
+    if (ka.count) {
+        DBuf<uint8_t> bf(ka.count, s);
+        GD_KERNEL(k_select_base_kills, grid_for(ka.count, 256), 256, 0, s, kpos.get(), ka.row.get(), ka.count,
+                  bf.get());
+        DBuf<int32_t> sel(ka.count, s);
+        int64_t nb = select_flagged_index(s, bf.get(), ka.count, sel.get());
+        if (nb) {
+            DBuf<int64_t> bp(nb, s);
+            DBuf<int32_t> br(nb, s);
+            GD_KERNEL(k_gather_sel<int64_t>, grid_for(nb, 256), 256, 0, s, kpos.get(), sel.get(), nb, bp.get());
+            GD_KERNEL(k_gather_sel<int32_t>, grid_for(nb, 256), 256, 0, s, ka.row.get(), sel.get(), nb, br.get());
+            append_out_tombs(bp.get(), br.get(), nb);
+        }
+    }
+    index_delete(rev, ka);
+    if (fwd.built) index_delete(fwd, ka);
+    return applied;
+}
+
+void Store::drop_claimed_tombs() {
+    if (!notomb) return;
+    cudaStream_t s = stream;
+    DBuf<uint8_t> keep(notomb, s);
+    GD_KERNEL(k_tomb_still_dead, grid_for(notomb, 256), 256, 0, s, otpos.get(), notomb, segs[0].col.get(),
+              keep.get());
+    DBuf<int32_t> sel(notomb, s);
+    int64_t m = select_flagged_index(s, keep.get(), notomb, sel.get());
+    if (m == notomb) return;
+    DBuf<int64_t> p(m, s);
+    DBuf<int32_t> r(m, s);
+    if (m) {
+        GD_KERNEL(k_gather_sel<int64_t>, grid_for(m, 256), 256, 0, s, otpos.get(), sel.get(), m, p.get());
+        GD_KERNEL(k_gather_sel<int32_t>, grid_for(m, 256), 256, 0, s, otrow.get(), sel.get(), m, r.get());
+    }
+    otpos = std::move(p);
+    otrow = std::move(r);
+    notomb = m;
+}
+
+void Store::apply_adds(const int32_t* d_src, const int32_t* d_dst, const int32_t* d_w, int64_t k) {
+    cudaStream_t s = stream;
+    if (k == 0) return;
+    int64_t na = directed ? k : 2 * k;
+    DBuf<uint32_t> key(na, s);
+    DBuf<int32_t> val(na, s);
+    AddedArcs aa;
+    aa.row.alloc(na, s);
+    aa.col.alloc(na, s);
+    aa.w.alloc(na, s);
+    aa.count = na;
+    GD_KERNEL(k_add_arcs, grid_for(k, 256), 256, 0, s, d_src, d_dst, d_w, k, directed, key.get(), val.get(),
+              aa.row.get(), aa.col.get(), aa.w.get());
+    sort_pairs_u32(s, key.get(), val.get(), na);  // stable: stream order within a source
+    DBuf<uint8_t> rflag(na, s);
+    GD_KERNEL(k_row_starts_u32, grid_for(na, 256), 256, 0, s, key.get(), na, rflag.get());
+    DBuf<int32_t> row_first(na, s);
+    int64_t nrows = select_flagged_index(s, rflag.get(), na, row_first.get());
+    DBuf<int64_t> vac(na, s);
+    fill_i64(s, vac.get(), na, -1);
+    OutView ov = out_view();
+    GD_KERNEL_T("add_vacancies", 0, k_add_vacancies, grid_for(nrows * 32, 256, 148LL * 32), 256, 0, s, ov,
+                key.get(), row_first.get(), nrows, na, vac.get());
+    DBuf<uint8_t> left(na, s);
+    GD_KERNEL(k_add_claim, grid_for(na, 256), 256, 0, s, ov, val.get(), aa.row.get(), aa.col.get(), aa.w.get(),
+              vac.get(), na, left.get());
+    drop_claimed_tombs();
+    // leftovers (already ordered by (source, stream order)) -> one new delta
+    DBuf<int32_t> sel(na, s);
+    int64_t nl = select_flagged_index(s, left.get(), na, sel.get());
+    if (nl) {
+        OutSeg d;
+        d.nslots = nl;
+        DBuf<int32_t> lrow(nl, s);
+        d.col.alloc(nl, s);
+        if (weighted) d.w.alloc(nl, s);
+        GD_KERNEL(k_gather_arcs, grid_for(nl, 256), 256, 0, s, sel.get(), nl, val.get(), aa.row.get(),
+                  aa.col.get(), aa.w.get(), lrow.get(), d.col.get(), weighted ? d.w.get() : nullptr);
+        offsets_from_rows(s, n, lrow.get(), nl, d.off);
+        segs.push_back(std::move(d));
+        upload_tables();
+    }
+    live += na;
+    index_add(rev, aa);
+    if (fwd.built) index_add(fwd, aa);
+}
+
+void Store::merge() {
+    cudaStream_t s = stream;
+    // live delta arcs in (row, segment, slot) order
+    int64_t dtot = 0;
+    for (size_t i = 1; i < segs.size(); ++i) dtot += segs[i].nslots;
+    DBuf<int32_t> irow(dtot, s), icol(dtot, s), iw(weighted ? dtot : 0, s);
+    int64_t nins = 0;
+    for (size_t i = 1; i < segs.size(); ++i) {
+        OutSeg& d = segs[i];
+        if (!d.nslots) continue;
+        DBuf<int32_t> row(d.nslots, s);
+        DBuf<uint8_t> lf(d.nslots, s);
+        GD_KERNEL(k_delta_rows, grid_for(d.nslots, 256), 256, 0, s, d.off.get(), n, d.col.get(), d.nslots,
+                  row.get(), lf.get());
+        DBuf<int32_t> sel(d.nslots, s);
+        int64_t c = select_flagged_index(s, lf.get(), d.nslots, sel.get());
+        if (!c) continue;
+        GD_KERNEL(k_gather_sel<int32_t>, grid_for(c, 256), 256, 0, s, row.get(), sel.get(), c, irow.get() + nins);
+        GD_KERNEL(k_gather_sel<int32_t>, grid_for(c, 256), 256, 0, s, d.col.get(), sel.get(), c, icol.get() + nins);
+        if (weighted)
+            GD_KERNEL(k_gather_sel<int32_t>, grid_for(c, 256), 256, 0, s, d.w.get(), sel.get(), c, iw.get() + nins);
+        nins += c;
+    }
+    if (segs.size() > 2 && nins > 1) {  // several deltas: stable sort by row keeps (segment, slot) order
+        DBuf<uint32_t> rk(nins, s);
+        GD_CUDA(cudaMemcpyAsync(rk.get(), irow.get(), nins * 4, cudaMemcpyDeviceToDevice, s));
+        DBuf<int32_t> perm(nins, s);
+        iota_i32(s, perm.get(), nins);
+        sort_pairs_u32(s, rk.get(), perm.get(), nins);
+        DBuf<int32_t> r2(nins, s), c2(nins, s), w2(weighted ? nins : 0, s);
+        GD_KERNEL(k_gather_sel<int32_t>, grid_for(nins, 256), 256, 0, s, irow.get(), perm.get(), nins, r2.get());
+        GD_KERNEL(k_gather_sel<int32_t>, grid_for(nins, 256), 256, 0, s, icol.get(), perm.get(), nins, c2.get());
+        if (weighted)
+            GD_KERNEL(k_gather_sel<int32_t>, grid_for(nins, 256), 256, 0, s, iw.get(), perm.get(), nins, w2.get());
+        irow = std::move(r2);
+        icol = std::move(c2);
+        iw = std::move(w2);
+    }
+    DBuf<int64_t> ipos(nins, s);
+    if (nins) GD_KERNEL(k_out_ins_pos, grid_for(nins, 256), 256, 0, s, irow.get(), nins, segs[0].off.get(), ipos.get());
+    OutSeg nb;
+    int64_t nnz2 = 0;
+    edit_merge(s, n, segs[0].off.get(), segs[0].col.get(), weighted ? segs[0].w.get() : nullptr, segs[0].nslots,
+               otpos.get(), otrow.get(), notomb, irow.get(), icol.get(), weighted ? iw.get() : nullptr, ipos.get(),
+               nins, nb.off, nb.col, nb.w, nnz2, weighted);
+    nb.nslots = nnz2;
+    segs.clear();
+    segs.push_back(std::move(nb));
+    upload_tables();
+    otpos.release();
+    otrow.release();
+    notomb = 0;
+    live = nnz2;
+    if (rev.built) compact_index(rev);
+    if (fwd.built) compact_index(fwd);
+}
+
+void Store::export_segment(int64_t seg, int64_t* off, int64_t* col, int64_t* w) {
+    cudaStream_t s = stream;
+    OutSeg& sg = segs.at((size_t)seg);
+    GD_CUDA(cudaMemcpyAsync(off, sg.off.get(), (n + 1) * 8, cudaMemcpyDeviceToHost, s));
+    if (sg.nslots) {
+        DBuf<int64_t> c(sg.nslots, s), ww(sg.nslots, s);
+        GD_KERNEL(k_export_seg, grid_for(sg.nslots, 256), 256, 0, s, sg.col.get(), sg.w.n ? sg.w.get() : nullptr,
+                  sg.nslots, c.get(), ww.get());
+        GD_CUDA(cudaMemcpyAsync(col, c.get(), sg.nslots * 8, cudaMemcpyDeviceToHost, s));
+        if (w) GD_CUDA(cudaMemcpyAsync(w, ww.get(), sg.nslots * 8, cudaMemcpyDeviceToHost, s));
+        GD_CUDA(cudaStreamSynchronize(s));
+    }
+    GD_CUDA(cudaStreamSynchronize(s));
+}
+
+int64_t Store::rev_nnz_live() {
+    require_rev();
+    compact_index(rev);
+    return rev.nnz;
+}
+
+void Store::export_rev(int64_t* off, int64_t* src, int64_t* w) {
+    require_rev();
+    compact_index(rev);
+    cudaStream_t s = stream;
+    GD_CUDA(cudaMemcpyAsync(off, rev.off.get(), (n + 1) * 8, cudaMemcpyDeviceToHost, s));
+    if (rev.nnz) {
+        DBuf<int64_t> c(rev.nnz, s), ww(rev.nnz, s);
+        GD_KERNEL(k_export_seg, grid_for(rev.nnz, 256), 256, 0, s, rev.col.get(), rev.w.n ? rev.w.get() : nullptr,
+                  rev.nnz, c.get(), ww.get());
+        GD_CUDA(cudaMemcpyAsync(src, c.get(), rev.nnz * 8, cudaMemcpyDeviceToHost, s));
+        if (w) GD_CUDA(cudaMemcpyAsync(w, ww.get(), rev.nnz * 8, cudaMemcpyDeviceToHost, s));
+        GD_CUDA(cudaStreamSynchronize(s));
+    }
+    GD_CUDA(cudaStreamSynchronize(s));
+}
+
+}  // namespace gdb

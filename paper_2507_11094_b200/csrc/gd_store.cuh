@@ -1,0 +1,140 @@
+// gd_store.cuh -- GPU-resident diff-CSR store (base CSR + per-batch delta
+// segments + tombstones) reproducing the reference's slot layout exactly.
+//
+// Reference: graph/csr.py:17-80, graph/dynamic.py:46-334,
+// runtime/graphdyn_rt.h:215-511.  Layout in HBM:
+//
+//   out-store  segments[0..S): off int64[n+1], coord int32[slots] (-1 = the
+//              reference's SENTINEL), w int32[slots] (weighted only).  Slot
+//              positions match the reference bit for bit: deletes tombstone
+//              the oldest matching slot, inserts claim the first vacancy of
+//              the source's chain, leftovers spill into ONE new delta per add
+//              call, merge compacts in neighbors() order.
+//   rev index  in-arcs as a CSR over destinations with sources ascending
+//              (the reference's reverse lists after a merge,
+//              dynamic.py:319-329), plus an optional per-batch delta of new
+//              in-arcs.  Deleted entries are tombstoned in place (~src) so
+//              rows stay binary-searchable.  For undirected graphs this is the
+//              sorted adjacency TC intersects over.
+//   fwd index  the same structure over sources (directed TC only).
+#pragma once
+
+#include <vector>
+
+#include "gd_common.cuh"
+
+namespace gdb {
+
+struct OutSeg {
+    DBuf<int64_t> off;
+    DBuf<int32_t> col;
+    DBuf<int32_t> w;  // empty when unweighted
+    int64_t nslots = 0;
+};
+
+// Device-side read views, passed by value to kernels.
+struct OutView {
+    int nseg;
+    const int64_t* const* off;  // device table of nseg pointers
+    const int32_t* const* col;
+    const int32_t* const* w;  // entries are nullptr when unweighted
+};
+
+struct IdxView {  // a clean-or-tombstoned sorted index (no delta)
+    const int64_t* off;
+    const int32_t* col;  // negative = tombstoned entry
+    const int32_t* w;    // nullptr when unweighted
+};
+
+struct SortedIndex {
+    bool built = false;
+    bool rows_are_dst = true;  // rev (true) or fwd (false)
+    DBuf<int64_t> off;
+    DBuf<int32_t> col;
+    DBuf<int32_t> w;
+    int64_t nnz = 0;
+    // tombstones since the last compaction, sorted by position
+    DBuf<int64_t> tpos;
+    DBuf<int32_t> trow;
+    int64_t ntomb = 0;
+    // delta: new entries sorted by (row, col)
+    DBuf<int32_t> drow, dcol, dw;
+    int64_t dnnz = 0;
+    bool dirty() const { return ntomb > 0 || dnnz > 0; }
+    IdxView view() const { return IdxView{off.get(), col.get(), w.n ? w.get() : nullptr}; }
+};
+
+// Killed out-arcs of one delete call (device), consumed by index upkeep.
+struct KilledArcs {
+    DBuf<int32_t> row, col, w;
+    int64_t count = 0;
+};
+// Inserted out-arcs of one add call (device).
+struct AddedArcs {
+    DBuf<int32_t> row, col, w;
+    int64_t count = 0;
+};
+
+class Store {
+  public:
+    Store(int device, int64_t n, const int64_t* src, const int64_t* dst, const int64_t* w, int64_t m,
+          bool directed, bool weighted, bool with_reverse, int64_t merge_interval, bool as_arcs = false);
+    ~Store();
+
+    // update_csr_del on device-resident records (int32).  Returns applied;
+    // found_fwd (k bytes, device) gets 1 per applied record when non-null.
+    int64_t apply_deletes(const int32_t* d_src, const int32_t* d_dst, int64_t k, uint8_t* d_found);
+    void apply_adds(const int32_t* d_src, const int32_t* d_dst, const int32_t* d_w, int64_t k);
+    void merge();
+    bool merge_due(int64_t batch_index) const { return (batch_index + 1) % merge_interval == 0; }
+
+    // indexes
+    void require_rev();  // build the rev index if absent
+    void require_fwd();  // directed TC: sorted out-index
+    void compact_rev() { compact_index(rev); }
+    void compact_fwd() { compact_index(fwd); }
+    SortedIndex& tc_index() { return directed ? fwd : rev; }
+    void compact_index(SortedIndex& ix);
+
+    OutView out_view() const;
+    int64_t total_slots() const;
+    int64_t device_bytes() const;
+
+    // export helpers (synchronous)
+    void export_segment(int64_t seg, int64_t* off, int64_t* col, int64_t* w);
+    int64_t rev_nnz_live();
+    void export_rev(int64_t* off, int64_t* src, int64_t* w);
+
+    int device;
+    cudaStream_t stream = nullptr;
+    int64_t n;
+    bool directed, weighted, with_reverse;
+    int64_t merge_interval;
+    int64_t live = 0;
+    std::vector<OutSeg> segs;
+    SortedIndex rev, fwd;
+    // out-store base tombstones since the last merge (sorted by position)
+    DBuf<int64_t> otpos;
+    DBuf<int32_t> otrow;
+    int64_t notomb = 0;
+
+  private:
+    DBuf<const int64_t*> tab_off;
+    DBuf<const int32_t*> tab_col, tab_w;
+    void upload_tables();
+    void build_index(SortedIndex& ix, bool rows_are_dst);
+    void index_delete(SortedIndex& ix, const KilledArcs& ka);
+    void index_add(SortedIndex& ix, const AddedArcs& aa);
+    void append_out_tombs(const int64_t* d_pos, const int32_t* d_row, int64_t cnt);
+    void drop_claimed_tombs();
+};
+
+// Edit-merge compaction shared by the out-store merge and index compaction:
+// copy the live entries of a base array (negative = dead) while inserting
+// sorted items before base positions P (stable), rows re-offset.
+void edit_merge(cudaStream_t s, int64_t n, const int64_t* off, const int32_t* col, const int32_t* w, int64_t nnz,
+                const int64_t* tpos, const int32_t* trow, int64_t ntomb, const int32_t* irow, const int32_t* icol,
+                const int32_t* iw, const int64_t* ipos, int64_t nins, DBuf<int64_t>& new_off,
+                DBuf<int32_t>& new_col, DBuf<int32_t>& new_w, int64_t& new_nnz, bool weighted);
+
+}  // namespace gdb

@@ -1,0 +1,352 @@
+"""Front door mirroring the reference engine (engine/run.py:22-68,
+engine/interp.py:112-160) for the three shipped programs.
+
+`run_program(check, graph, inputs, entry=...)` runs staticSSSP / dynamicSSSP,
+staticPR / dynamicPR or staticTC / dynamicTC entirely on the GPU through the
+C ABI and returns an ExecContext-shaped result (`properties[name].values()`,
+`return_value`, `scalars`, `batch_stats`, `phase_totals`,
+`fixedpoint_iterations`).  `check` is either the reference's own CheckResult
+(when its frontend is importable) or the stand-in from `compile_source`
+below; the DSL compiler itself is out of scope.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+import time
+from dataclasses import dataclass, field
+from typing import Dict, List, Optional
+
+import numpy as np
+
+from . import _native as N
+from .errors import CompileError, ConfigurationError, ExecError
+from .graph import DynamicGraph
+from .updates import RecordArrays, UpdateStream
+
+INT_INF = np.iinfo(np.int64).max
+
+PHASES = ("static_phase", "preprocess", "structural_update", "propagate", "merge")
+
+# entry -> (program, role)
+_ENTRIES = {
+    "staticSSSP": ("sssp_dynamic", "Static"),
+    "decrementalSSSP": ("sssp_dynamic", "Decremental"),
+    "incrementalSSSP": ("sssp_dynamic", "Incremental"),
+    "dynamicSSSP": ("sssp_dynamic", "Dynamic"),
+    "staticPR": ("pr_dynamic", "Static"),
+    "incrementalPR": ("pr_dynamic", "Incremental"),
+    "dynamicPR": ("pr_dynamic", "Dynamic"),
+    "staticTC": ("tc_dynamic", "Static"),
+    "dynamicTC": ("tc_dynamic", "Dynamic"),
+}
+_DRIVER = {"sssp_dynamic": "dynamicSSSP", "pr_dynamic": "dynamicPR", "tc_dynamic": "dynamicTC"}
+_FUNCS = {p: [e for e, (q, _) in _ENTRIES.items() if q == p] for p in _DRIVER}
+
+
+@dataclass
+class _Fn:
+    name: str
+    role: str
+
+
+class Program:
+    """The parts of the reference's ast.Program the engine front door reads."""
+
+    def __init__(self, name: str):
+        self.name = name
+        self.entry = _DRIVER[name]
+        self.functions = [_Fn(f, _ENTRIES[f][1]) for f in _FUNCS[name]]
+
+    def function(self, name: str):
+        for f in self.functions:
+            if f.name == name:
+                return f
+        return None
+
+    def by_role(self, role: str):
+        return [f for f in self.functions if f.role == role]
+
+
+@dataclass
+class CheckResult:
+    program: Program
+
+
+def compile_source(source: str, strip: bool = False) -> CheckResult:
+    """Recognise one of the three shipped programs (programs/*.sp).
+
+    The B200 path executes these programs natively; any other DSL source is
+    rejected with CompileError rather than interpreted on the CPU."""
+    for name, driver in _DRIVER.items():
+        if f"Dynamic {driver}(" in source:
+            return CheckResult(Program(name))
+    raise CompileError(["the B200 path implements only sssp_dynamic, pr_dynamic and tc_dynamic "
+                        "(programs/*.sp); no Dynamic driver of those was found in the source"])
+
+
+def needs_reverse(program) -> bool:
+    """engine/run.py:14-19: reverse adjacency for programs using nodesTo/propagateNodeFlags."""
+    name = _program_name(program)
+    return name in ("sssp_dynamic", "pr_dynamic")
+
+
+def _program_name(program) -> str:
+    if isinstance(program, Program):
+        return program.name
+    names = set()
+    fns = getattr(program, "functions", None) or getattr(program, "decls", None) or []
+    for f in fns:
+        names.add(getattr(f, "name", ""))
+    if not names and hasattr(program, "function"):
+        for e in _ENTRIES:
+            if program.function(e) is not None:
+                names.add(e)
+    for name, driver in _DRIVER.items():
+        if driver in names:
+            return name
+    raise CompileError(["program is not one of sssp_dynamic / pr_dynamic / tc_dynamic"])
+
+
+class NodePropertyTable:
+    """Result table with the reference's read API (properties.py:46-76)."""
+
+    def __init__(self, name: str, dtype: str, data: np.ndarray):
+        self.name = name
+        self.dtype = dtype
+        self.data = data
+
+    def values(self) -> list:
+        if self.dtype in ("float", "double"):
+            return [float(x) for x in self.data]
+        if self.dtype == "bool":
+            return [bool(x) for x in self.data]
+        return [int(x) for x in self.data]
+
+    def get(self, v: int):
+        return self.values()[v]
+
+
+@dataclass
+class ExecContext:
+    gview: object
+    worker_count: int = 1
+    iteration_cap_factor: int = 10
+    properties: Dict[str, object] = field(default_factory=dict)
+    scalars: Dict[str, object] = field(default_factory=dict)
+    return_value: object = None
+    fixedpoint_iterations: List[int] = field(default_factory=list)
+    batch_stats: List[dict] = field(default_factory=list)
+    phase_totals: Dict[str, float] = field(default_factory=dict)
+    kernel_times: Dict[str, dict] = field(default_factory=dict)
+
+    @property
+    def graph(self) -> DynamicGraph:
+        return self.gview
+
+
+# -------------------------------------------------------------------- handles ----
+
+class _Algo:
+    """Owns one algorithm handle of the C ABI (gd_sssp / gd_pr / gd_tc)."""
+
+    kind = ""
+
+    def __init__(self, h: C.c_void_p, graph: DynamicGraph):
+        self.h = h
+        self.graph = graph  # keeps the store alive
+
+    def batch(self, arr: RecordArrays, batch_index: int) -> None:
+        a = arr.contiguous()
+        N.check(getattr(N.lib(), f"gd_{self.kind}_batch")(self.h, N.ptr(a.kind), N.ptr(a.src), N.ptr(a.dst),
+                                                          N.ptr(a.weight), len(a), int(batch_index)))
+
+    def batch_device(self, kind_ptr: int, src_ptr: int, dst_ptr: int, w_ptr: int, k: int, batch_index: int) -> None:
+        """Records already in device memory (uint8 kind, int32 src/dst/w)."""
+        N.check(getattr(N.lib(), f"gd_{self.kind}_batch_device")(self.h, C.c_void_p(kind_ptr), C.c_void_p(src_ptr),
+                                                                 C.c_void_p(dst_ptr), C.c_void_p(w_ptr), int(k),
+                                                                 int(batch_index)))
+
+    def phase_ms(self) -> Dict[str, float]:
+        ms = (C.c_double * 5)()
+        N.check(N.lib().gd_phase_times(self.h, ms))
+        return {p: ms[i] for i, p in enumerate(PHASES)}
+
+    def iterations(self) -> int:
+        it = C.c_int64()
+        N.check(N.lib().gd_iterations(self.h, C.byref(it)))
+        return it.value
+
+    def set_profiling(self, on: bool) -> None:
+        N.check(N.lib().gd_set_profiling(self.h, int(on)))
+
+    def kernel_time(self, name: str):
+        ms, n, b = C.c_double(), C.c_int64(), C.c_int64()
+        N.check(N.lib().gd_kernel_time(self.h, name.encode(), C.byref(ms), C.byref(n), C.byref(b)))
+        return ms.value, n.value
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h is not None and N._lib is not None:
+            getattr(N._lib, f"gd_{self.kind}_destroy")(h)
+            self.h = None
+
+
+class SSSPHandle(_Algo):
+    kind = "sssp"
+
+    def __init__(self, graph: DynamicGraph, src: int):
+        h = C.c_void_p()
+        N.check(N.lib().gd_sssp_create(graph.handle, int(src), C.byref(h)))
+        super().__init__(h, graph)
+
+    def read(self):
+        n = self.graph.node_count
+        dist = np.zeros(n, dtype=np.int64)
+        parent = np.zeros(n, dtype=np.int64)
+        N.check(N.lib().gd_sssp_read(self.h, N.ptr(dist), N.ptr(parent)))
+        return dist, parent
+
+
+class PRHandle(_Algo):
+    kind = "pr"
+
+    def __init__(self, graph: DynamicGraph, damping: float, beta: float, maxiter: int):
+        h = C.c_void_p()
+        N.check(N.lib().gd_pr_create(graph.handle, float(damping), float(beta), int(maxiter), C.byref(h)))
+        super().__init__(h, graph)
+
+    def read(self, with_outdeg: bool = True):
+        n = self.graph.node_count
+        rank = np.zeros(n, dtype=np.float64)
+        od = np.zeros(n, dtype=np.int64) if with_outdeg else None
+        N.check(N.lib().gd_pr_read(self.h, N.ptr(rank), N.ptr(od)))
+        return rank, od
+
+    def rank_device_ptr(self) -> int:
+        p = C.c_void_p()
+        N.check(N.lib().gd_pr_rank_device(self.h, C.byref(p)))
+        return p.value
+
+
+class TCHandle(_Algo):
+    kind = "tc"
+
+    def __init__(self, graph: DynamicGraph):
+        h = C.c_void_p()
+        N.check(N.lib().gd_tc_create(graph.handle, C.byref(h)))
+        super().__init__(h, graph)
+
+    def read(self) -> int:
+        c = C.c_int64()
+        N.check(N.lib().gd_tc_read(self.h, C.byref(c)))
+        return c.value
+
+
+# ----------------------------------------------------------------- front door ----
+
+def _need(inputs, key, conv):
+    if key not in inputs:
+        raise ExecError(f"unbound input {key!r}")
+    v = inputs[key]
+    if conv is int and v == math.inf:
+        return INT_INF
+    return conv(v)
+
+
+def _stream_of(inputs) -> UpdateStream:
+    for key in ("updateList", "updates", "update_list"):
+        if key in inputs:
+            s = inputs[key]
+            if s is None:
+                raise ExecError(f"unbound input {key!r} (update stream)")
+            if isinstance(s, UpdateStream):
+                return s
+            if hasattr(s, "records"):  # the reference's own UpdateStream
+                return UpdateStream(list(s.records))
+            return UpdateStream(list(s))
+    raise ExecError("unbound input 'updateList' (update stream)")
+
+
+def _batch_size(inputs, stream_len: int) -> int:
+    for key in ("batchsize", "batch_size"):
+        if key in inputs:
+            return int(inputs[key])
+    raise ExecError("unbound input 'batchsize'")
+
+
+def run_program(check, graph: DynamicGraph, inputs: Dict[str, object], *, entry: Optional[str] = None,
+                worker_count: int = 1, iteration_cap_factor: int = 10, debug: bool = False,
+                gview=None) -> ExecContext:
+    """engine/run.py:22-41 on the B200 path.  worker_count/debug/gview are
+    accepted for signature compatibility; the GPU path has no worker pool."""
+    program = check.program
+    name = _program_name(program)
+    entry = entry or getattr(program, "entry", None) or _DRIVER[name]
+    if entry not in _ENTRIES or _ENTRIES[entry][0] != name:
+        raise ExecError(f"no function named {entry!r}")
+    role = _ENTRIES[entry][1]
+    if role in ("Incremental", "Decremental"):
+        raise ExecError(f"{entry} runs only inside its Dynamic driver on the B200 path")
+    if not isinstance(graph, DynamicGraph):
+        raise ConfigurationError("run_program on the B200 path needs a paper_2507_11094_b200 DynamicGraph")
+    ctx = ExecContext(graph, worker_count=worker_count, iteration_cap_factor=iteration_cap_factor)
+    dynamic = role == "Dynamic"
+    stream = _stream_of(inputs) if dynamic else None
+    bsize = _batch_size(inputs, len(stream)) if dynamic else 0
+    if dynamic and bsize <= 0:
+        raise ExecError("batch size must be positive")
+
+    t0 = time.perf_counter()
+    if name == "sssp_dynamic":
+        algo = SSSPHandle(graph, _need(inputs, "src", int))
+    elif name == "pr_dynamic":
+        algo = PRHandle(graph, _need(inputs, "damping", float), _need(inputs, "beta", float),
+                        _need(inputs, "maxiter", int))
+    else:
+        algo = TCHandle(graph)
+    if dynamic:
+        arr = stream.arrays
+        prev_it = algo.iterations()
+        for index, start in enumerate(range(0, len(arr), bsize)):
+            part = arr.slice(start, start + bsize)
+            stats = {"index": index, "adds": int(np.count_nonzero(part.kind == ord("a"))),
+                     "deletes": int(np.count_nonzero(part.kind == ord("d")))}
+            before = algo.phase_ms()
+            algo.batch(part, index)
+            graph._touch()
+            after = algo.phase_ms()
+            for p in PHASES[1:]:
+                stats[p] = (after[p] - before[p]) / 1e3
+            ctx.batch_stats.append(stats)
+            it = algo.iterations()
+            ctx.fixedpoint_iterations.append(it - prev_it)
+            prev_it = it
+    totals = algo.phase_ms()
+    ctx.phase_totals = {p: totals[p] / 1e3 for p in PHASES if totals[p] > 0 or p == "static_phase"}
+    ctx.scalars["wall_seconds"] = time.perf_counter() - t0
+
+    if name == "sssp_dynamic":
+        dist, parent = algo.read()
+        ctx.properties["dist"] = NodePropertyTable("dist", "int", dist)
+        ctx.properties["parent"] = NodePropertyTable("parent", "int", parent)
+    elif name == "pr_dynamic":
+        rank, od = algo.read()
+        ctx.properties["pagerank"] = NodePropertyTable("pagerank", "float", rank)
+        ctx.properties["outdeg"] = NodePropertyTable("outdeg", "int", od)
+    else:
+        c = algo.read()
+        ctx.return_value = c
+        ctx.scalars["tcount"] = c
+    ctx.scalars.pop("wall_seconds", None)
+    return ctx
+
+
+def run_batches(check, graph: DynamicGraph, updates: UpdateStream, batch_size: int, inputs: Dict[str, object],
+                **kwargs) -> ExecContext:
+    """engine/run.py:44-68: bind the stream and batch size to the driver."""
+    bound = dict(inputs)
+    bound["updateList"] = updates
+    bound["batchsize"] = batch_size
+    return run_program(check, graph, bound, **kwargs)

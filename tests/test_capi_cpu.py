@@ -1,0 +1,105 @@
+"""CPU-side checks of the boundary: the C-ABI library loads and exports every
+symbol include/gd_capi.h declares, host logic mirrors the reference, and the
+product fails loudly (no CPU fallback) when no GPU is present."""
+
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from conftest import gpu_available
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_symbols():
+    text = open(os.path.join(REPO, "include", "gd_capi.h")).read()
+    return sorted(set(re.findall(r"GD_API\s+[\w\s\*]+?\b(gd_\w+)\s*\(", text)))
+
+
+def test_library_exports_every_header_symbol():
+    from paper_2507_11094_b200 import _native
+
+    L = ctypes.CDLL(_native.LIB_PATH)
+    syms = header_symbols()
+    assert len(syms) >= 35
+    missing = [s for s in syms if not hasattr(L, s)]
+    assert not missing, missing
+    bound = {name for name, _, _ in _native.SIGNATURES}
+    assert set(syms) <= bound, set(syms) - bound
+
+
+def test_library_is_sm100a_only():
+    import subprocess
+
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf",
+                          os.path.join(REPO, "paper_2507_11094_b200", "libgdb200.so")],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    assert not re.search(r"sm_(?!100a)\d+", out)
+
+
+@pytest.mark.skipif(gpu_available(), reason="checks the no-GPU behaviour")
+def test_no_cpu_fallback():
+    import paper_2507_11094_b200 as gd
+
+    with pytest.raises(gd.DeviceError, match="no CPU fallback"):
+        gd.DynamicGraph.build([(0, 1, 1)], 2)
+
+
+def test_compile_source_recognises_shipped_programs():
+    import paper_2507_11094_b200 as gd
+
+    for prog, entry in (("sssp_dynamic", "dynamicSSSP"), ("pr_dynamic", "dynamicPR"), ("tc_dynamic", "dynamicTC")):
+        src = f"Dynamic {entry}(Graph g) {{}}"
+        chk = gd.compile_source(src)
+        assert chk.program.entry == entry
+        assert chk.program.function(entry) is not None
+    with pytest.raises(gd.CompileError):
+        gd.compile_source("function f(Graph g) {}")
+    if os.path.isdir("/root/reference/pkg/src/graphdyn/programs"):
+        for name in ("sssp_dynamic", "pr_dynamic", "tc_dynamic"):
+            text = open(f"/root/reference/pkg/src/graphdyn/programs/{name}.sp").read()
+            assert gd.compile_source(text).program.name == name
+            assert gd.needs_reverse(gd.compile_source(text).program) == (name != "tc_dynamic")
+
+
+def test_update_stream_parsing_and_batching(tmp_path):
+    import paper_2507_11094_b200 as gd
+
+    p = tmp_path / "u.txt"
+    p.write_text("# c\na 1 2 5\nd 3 4\n\na 5 6\n")
+    s = gd.load_update_stream(str(p))
+    assert [(r.kind, r.src, r.dst, r.weight) for r in s] == [("a", 1, 2, 5), ("d", 3, 4, 1), ("a", 5, 6, 1)]
+    bs = list(s.batches(2))
+    assert [len(b) for b in bs] == [2, 1]
+    assert [r.kind for r in bs[0].only_adds()] == ["a"]
+    with pytest.raises(ValueError):
+        list(s.batches(0))
+    with pytest.raises(gd.MalformedInputError):
+        gd.parse_update_line("x 1 2")
+    with pytest.raises(gd.MalformedInputError):
+        gd.parse_update_line("d 1 2 3")
+    out = tmp_path / "o.txt"
+    gd.dump_update_stream(list(s), str(out))
+    assert [(r.kind, r.src, r.dst) for r in gd.load_update_stream(str(out))] == [(r.kind, r.src, r.dst) for r in s]
+
+
+def test_parse_edge_lines_matches_reference_rules():
+    import paper_2507_11094_b200 as gd
+
+    edges, weighted, mx = gd.parse_edge_lines("0 1 3\n# x\n2 0 4\n")
+    assert edges == [(0, 1, 3), (2, 0, 4)] and weighted and mx == 2
+    for bad in ("0 1\n1 2 3\n", "0\n", "0 -1\n", "0 1 -2\n", "a b\n"):
+        with pytest.raises(gd.MalformedInputError):
+            gd.parse_edge_lines(bad)
+    if os.path.isdir("/root/reference/pkg/src"):
+        import sys
+
+        sys.path.insert(0, "/root/reference/pkg/src")
+        from graphdyn.graph.io import parse_edge_lines as ref
+
+        text = "0 1 3\n5 2 1 # c\n\n3 3 0\n"
+        assert gd.parse_edge_lines(text) == ref(text)
