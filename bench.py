@@ -1,0 +1,421 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 dynamic-graph hot path (BASELINE.json).
+
+Default workload = BASELINE configs[1] (the metric's 1-GPU config): dynamic
+PageRank on R-MAT scale-22 (4,194,304 V, 2^26 distinct directed edges,
+unweighted), successive 1% ΔG batches (671,089 records: 50% deletes drawn
+from the edges, 50% adds from non-edges), d=0.85, beta=1e-3, maxiter=100,
+merge every batch (the reference default).  One step = one batch: OnDelete/
+OnAdd handlers, updateCSRDel/Add on the GPU diff-CSR store, merge, affected
+flood, incremental PageRank to convergence.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--workload pr|sssp|tc|sssp-grid]
+
+Under torchrun (N>1) every rank runs its own replica of the workload (weak
+scaling; vertex-range sharding is future work); timing is the
+max over ranks.  `--impl reference` times the reference's own emitted OpenMP
+driver (oracle/_ref/libgdref.so, compiled from /root/reference) on the host
+cores -- rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "per-ΔG-batch time & updated edges/sec for dyn SSSP/PR/TC at 1/2/4/8 B200"
+UNIT = "updated edges/s"
+
+WORKLOADS = {
+    # BASELINE configs[1]
+    "pr": dict(algo="pr", graph="rmat", scale=22, edges=1 << 26, percent=1.0, weighted=False, directed=True,
+               desc="dynamic PageRank, R-MAT scale-22 (4,194,304 V, 67,108,864 E), successive 1% batches"),
+    # BASELINE configs[0] (the reference's CPU-runnable case)
+    "sssp": dict(algo="sssp", graph="rmat", scale=16, edges=1_000_000, percent=5.0, weighted=True, directed=True,
+                 desc="dynamic SSSP, R-MAT scale-16 (65,536 V, 1M E, w 1-100), 5% batches"),
+    # BASELINE configs[2] at 1%
+    "tc": dict(algo="tc", graph="uniform", nodes=1 << 24, edges=256_000_000, percent=1.0, weighted=False,
+               directed=False, desc="dynamic TC, uniform 16,777,216 V / 256M undirected edges, 1% batches"),
+    # BASELINE configs[3]
+    "sssp-grid": dict(algo="sssp", graph="grid", rows=4899, cols=4899, percent=5.0, weighted=True, directed=True,
+                      desc="dynamic SSSP, 4899x4899 grid (24.0M V, 96M arcs), 5% batches, corner source"),
+}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def make_inputs(wl, batches, seed=22):
+    from paper_2507_11094_b200 import generate as G
+
+    t = time.time()
+    if wl["graph"] == "rmat":
+        s, d, w, n = G.rmat(wl["scale"], wl["edges"], seed=seed, weighted=wl["weighted"],
+                            undirected=not wl["directed"])
+    elif wl["graph"] == "uniform":
+        s, d, w, n = G.uniform(wl["nodes"], wl["edges"], seed=seed, weighted=wl["weighted"],
+                               undirected=not wl["directed"])
+    else:
+        s, d, w, n = G.grid(wl["rows"], wl["cols"], seed=seed)
+    kind, us, ud, uw, per = G.updates(s, d, n, percent=wl["percent"], batches=batches, seed=seed + 1,
+                                      undirected=not wl["directed"], max_weight=100 if wl["weighted"] else 1)
+    log(f"[bench] inputs: n={n} m={len(s)} records={len(kind)} batch={per} gen={time.time() - t:.1f}s "
+        f"({G.threads()} threads)")
+    return n, s, d, w, kind, us, ud, uw, per
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"], stdout=subprocess.PIPE,
+                                      stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        out, _ = self.p.communicate(timeout=10)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def load_peaks():
+    p = os.path.join(REPO, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as fh:
+            j = json.load(fh)
+        return float(j["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ------------------------------------------------------------------ reference ----
+
+def reference_run(wl, steps, threads, sample_batches=None):
+    """The reference's own dynamicPR/SSSP/TC (oracle/_ref) on the host cores.
+    Per-batch time = (T_k - T_0)/k as the reference's bench does (cli.py:436-442)."""
+    from oracle import oracle as O
+
+    k = steps if sample_batches is None else min(steps, sample_batches)
+    n, s, d, w, kind, us, ud, uw, per = make_inputs(wl, k)
+    total = min(len(kind), k * per)
+    t = time.time()
+    algo = wl["algo"]
+    _, times = O.ref_run(algo, n, s, d, w if wl["weighted"] else None, directed=wl["directed"],
+                         weighted=wl["weighted"], kind=kind[:total], us=us[:total], ud=ud[:total], uw=uw[:total],
+                         batch_size=per, threads=threads, sssp_src=0)
+    per_batch = (times[1] - times[0]) / k
+    used = 1 if algo == "tc" else threads
+    log(f"[reference] T0={times[0]:.2f}s Tk={times[1]:.2f}s k={k} per-batch={per_batch:.3f}s wall={time.time()-t:.1f}s")
+    return {"value": per / per_batch, "unit": UNIT, "cores": used, "kind": "reference",
+            "per_batch_s": per_batch,
+            "sample": (f"{wl['desc']}: the reference's emitted OpenMP driver "
+                       f"({algo}_dynamic_omp.cc + graphdyn_rt.h, g++ -O2 -fopenmp) on {k} successive batches of "
+                       f"{per} records, (T_k - T_0)/k per batch (cli.py:436-442); "
+                       f"{used} OpenMP thread(s){' (emitted TC crashes with >1 thread)' if algo == 'tc' else ''}")}
+
+
+# ------------------------------------------------------------------------ ours ----
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="pr")
+    ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-batches", type=int, default=1,
+                    help="bounded sample for the reference arm: at most this many batches")
+    args = ap.parse_args()
+    wl = WORKLOADS[args.workload]
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        if rank != 0:
+            return 0
+        threads = os.cpu_count() or 1
+        try:
+            cb = reference_run(wl, args.steps, threads, sample_batches=args.ref_batches)
+        except Exception as exc:  # noqa: BLE001
+            print(json.dumps({"impl": "reference", "unavailable": f"{type(exc).__name__}: {exc}"}))
+            return 0
+        line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": args.gpus,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": cb["per_batch_s"] * 1e3,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": _dtype(wl),
+                "data": "synthetic", "config": _config(wl, args, world),
+                "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+                "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line))
+        return 0
+
+    import torch
+
+    dist_on = world > 1
+    if dist_on:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    import paper_2507_11094_b200 as gd
+
+    e2e_steps = args.e2e_steps if args.e2e_steps is not None else max(1, min(args.steps, 5))
+    nb = args.warmup + args.steps + e2e_steps
+    n, s, d, w, kind, us, ud, uw, per = make_inputs(wl, nb, seed=22 + 1000 * rank)
+    records_per_step = per
+
+    t = time.time()
+    g = gd.DynamicGraph.from_arrays(n, s, d, w if wl["weighted"] else None, directed=wl["directed"],
+                                    weighted=wl["weighted"], with_reverse=wl["algo"] != "tc", device=local)
+    if wl["algo"] == "pr":
+        algo = gd.PRHandle(g, 0.85, 1e-3, 100)
+    elif wl["algo"] == "sssp":
+        algo = gd.SSSPHandle(g, 0)
+    else:
+        algo = gd.TCHandle(g)
+    torch.cuda.synchronize()
+    log(f"[bench] store + static pass: {time.time() - t:.1f}s; device bytes {g.device_bytes() / 2**30:.2f} GiB")
+
+    # records resident in HBM for the device-path steps (int32 ids, uint8 kind)
+    dk = torch.from_numpy(kind).to(f"cuda:{local}")
+    ds = torch.from_numpy(us.astype(np.int32)).to(f"cuda:{local}")
+    dd = torch.from_numpy(ud.astype(np.int32)).to(f"cuda:{local}")
+    dw = torch.from_numpy(uw.astype(np.int32)).to(f"cuda:{local}")
+
+    def dev_step(i):
+        a, b = i * per, min((i + 1) * per, len(kind))
+        algo.batch_device(dk.data_ptr() + a, ds.data_ptr() + 4 * a, dd.data_ptr() + 4 * a, dw.data_ptr() + 4 * a,
+                          b - a, i)
+        return b - a
+
+    stream = torch.cuda.ExternalStream(_graph_stream(g))
+    for i in range(args.warmup):
+        dev_step(i)
+    torch.cuda.synchronize()
+
+    # ---- timed region: K steps, inputs already in HBM --------------------------------
+    algo.set_profiling(True)
+    kstats = {}
+    clocks = Clocks(local)
+    if dist_on:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    launches0 = gd._native.lib().gd_kernel_launches()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    done = 0
+    for i in range(args.warmup, args.warmup + args.steps):
+        done += dev_step(i)
+        for name in KERNELS:
+            ms, nl, nb_ = algo.kernel_time(name)
+            if nl:
+                st = kstats.setdefault(name, [0.0, 0, 0])
+                st[0] += ms
+                st[1] += nl
+                st[2] += nb_
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    launches = gd._native.lib().gd_kernel_launches() - launches0
+    clk = clocks.stop()
+    elapsed_ms = ev0.elapsed_time(ev1)
+    if dist_on:
+        tt = torch.tensor([elapsed_ms], device=f"cuda:{local}")
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        elapsed_ms = float(tt.item())
+    algo.set_profiling(False)
+
+    # ---- e2e: host buffers through the public C-ABI call, H2D + D2H inside ----------
+    pin = {}
+    for nm, arr in (("kind", kind), ("src", us), ("dst", ud), ("w", uw)):
+        t_ = torch.from_numpy(np.ascontiguousarray(arr)).pin_memory()
+        pin[nm] = t_
+    out_pin = torch.empty(n, dtype=torch.float64 if wl["algo"] == "pr" else torch.int64).pin_memory()
+    e_start = args.warmup + args.steps
+    h2d = d2h = 0
+    if dist_on:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    e_done = 0
+    for i in range(e_start, e_start + e2e_steps):
+        a, b = i * per, min((i + 1) * per, len(kind))
+        k = b - a
+        if k <= 0:
+            break
+        h2d += k * (1 + 8 + 8 + 8)
+        tb0 = time.perf_counter()
+        _host_batch(gd, algo, pin, a, k, i)
+        tb1 = time.perf_counter()
+        d2h += _read_result(gd, algo, wl, out_pin, n)
+        tb2 = time.perf_counter()
+        log(f"[bench] e2e step {i}: batch {1e3 * (tb1 - tb0):.2f} ms, read {1e3 * (tb2 - tb1):.2f} ms")
+        e_done += k
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1)
+    if dist_on:
+        tt = torch.tensor([e2e_ms], device=f"cuda:{local}")
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        e2e_ms = float(tt.item())
+    e2e_value = (e_done * world) / (e2e_ms / 1e3) if e2e_ms > 0 else None
+
+    value = (done * world) / (elapsed_ms / 1e3)
+    peak, peak_kind = load_peaks()
+    dom = max(kstats.items(), key=lambda kv: kv[1][0]) if kstats else None
+    roof = None
+    if dom:
+        name, (ms, nl, nbytes) = dom
+        b_per_launch = nbytes / nl
+        avg_ms = ms / nl
+        ach = (b_per_launch / 1e9) / (avg_ms / 1e3) if b_per_launch else None
+        roof = {"bound": "hbm", "kernel": name, "achieved": ach, "peak": peak, "unit": "GB/s",
+                "frac": (ach / peak) if ach else None, "traffic": _ncu_traffic(name),
+                "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured" else
+                "fallback 6.65 TB/s (B200_PROFILING.md)",
+                "bytes_per_launch": b_per_launch, "avg_launch_ms": avg_ms, "launches": nl,
+                "share_of_step": ms / elapsed_ms if elapsed_ms else None}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cb = reference_run(wl, args.steps, os.cpu_count() or 1, sample_batches=args.ref_batches)
+            cpu = {k_: cb[k_] for k_ in ("value", "unit", "cores", "kind", "sample")}
+        except Exception as exc:  # noqa: BLE001
+            cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
+                   "sample": f"unavailable: {type(exc).__name__}: {exc}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": _dtype(wl), "data": "synthetic",
+            "config": _config(wl, args, world),
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d // max(e2e_steps, 1),
+                    "d2h_bytes_per_step": d2h // max(e2e_steps, 1), "steps": e2e_steps,
+                    "ms_per_step": e2e_ms / max(e2e_steps, 1)},
+            "gpu_launches": int(launches),
+            "roofline": roof,
+            "kernels": {k_: {"ms_total": v[0], "launches": v[1], "share": v[0] / elapsed_ms,
+                             "gbs": (v[2] / 1e9) / (v[0] / 1e3) if v[2] and v[0] else None}
+                        for k_, v in sorted(kstats.items(), key=lambda kv: -kv[1][0])},
+            "cpu_baseline": cpu,
+            "clocks": clk,
+            "records_per_step": records_per_step,
+        }
+        print(json.dumps(line))
+    if dist_on:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+KERNELS = ("pr_pull", "pr_pull_heavy", "pr_contrib", "merge_copy", "flood_hook", "flood_mark", "del_scan",
+           "add_vacancies", "tc_count", "sssp_relax", "sssp_walk", "sssp_pull", "sssp_parent")
+
+def _graph_stream(g):
+    import ctypes as C
+
+    from paper_2507_11094_b200 import _native as N
+
+    p = C.c_void_p()
+    N.check(N.lib().gd_graph_stream(g.handle, C.byref(p)))
+    return p.value
+
+
+def _host_batch(gd, algo, pin, a, k, i):
+    import ctypes as C
+
+    from paper_2507_11094_b200 import _native as N
+
+    fn = getattr(N.lib(), f"gd_{algo.kind}_batch")
+    N.check(fn(algo.h, C.c_void_p(pin["kind"].data_ptr() + a), C.c_void_p(pin["src"].data_ptr() + 8 * a),
+               C.c_void_p(pin["dst"].data_ptr() + 8 * a), C.c_void_p(pin["w"].data_ptr() + 8 * a), k, i))
+
+
+def _read_result(gd, algo, wl, out_pin, n):
+    import ctypes as C
+
+    from paper_2507_11094_b200 import _native as N
+
+    if wl["algo"] == "pr":
+        N.check(N.lib().gd_pr_read(algo.h, C.c_void_p(out_pin.data_ptr()), None))
+        return 8 * n
+    if wl["algo"] == "sssp":
+        N.check(N.lib().gd_sssp_read(algo.h, C.c_void_p(out_pin.data_ptr()), C.c_void_p(out_pin.data_ptr())))
+        return 16 * n
+    c = C.c_int64()
+    N.check(N.lib().gd_tc_read(algo.h, C.byref(c)))
+    return 8
+
+
+def _ncu_traffic(name):
+    p = os.path.join(REPO, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as fh:
+            return json.load(fh).get(name)
+    except Exception:
+        return None
+
+
+def _dtype(wl):
+    return {"pr": "f64", "sssp": "int64", "tc": "int64"}[wl["algo"]]
+
+
+def _config(wl, args, world):
+    c = {"workload": wl["desc"], "algo": wl["algo"], "batch_percent": wl["percent"], "merge_interval": 1,
+         "parallelism": "replicas" if world > 1 else "single-gpu",
+         "l2": "inputs larger than L2 (graph store >> 126 MB L2)"}
+    if wl["algo"] == "pr":
+        c.update({"damping": 0.85, "beta": 1e-3, "maxiter": 100})
+    return c
+
+
+if __name__ == "__main__":
+    sys.exit(main())

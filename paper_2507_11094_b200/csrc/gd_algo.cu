@@ -1,4 +1,6 @@
 // gd_algo.cu -- batch staging, validation, out-degrees and the weak-component flood.
+#include <algorithm>
+
 #include "gd_algo.cuh"
 
 namespace gdb {
@@ -218,31 +220,64 @@ __global__ void k_uf_init(int32_t* p, int64_t n) {
         p[i] = (int32_t)i;
 }
 
-// Rows are processed by 32-lane warps over the concatenated slot range of each
-// segment: every lane owns one slot, so reads are coalesced regardless of the
-// degree distribution.  The row of a slot comes from a per-warp search.
-__global__ void k_uf_hook(OutView ov, int64_t n, int32_t* p) {
-    const int lane = threadIdx.x & 31;
-    int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int sg = 0; sg < ov.nseg; ++sg) {
-        const int64_t* off = ov.off[sg];
-        const int32_t* col = ov.col[sg];
-        int64_t m = off[n];
-        for (int64_t base = warp * 32; base < m; base += nwarps * 32) {
-            int64_t i = base + lane;
-            int64_t last = min(base + 31, m - 1);
-            // rows of the first and last slot of the chunk bound every lane's search
-            int64_t r0 = 0, r1 = 0;
-            if (lane == 0) r0 = upper_bound_dev<int64_t>(off, 0, n + 1, base) - 1;
-            if (lane == 31) r1 = upper_bound_dev<int64_t>(off, 0, n + 1, last) - 1;
-            r0 = __shfl_sync(0xffffffffu, r0, 0);
-            r1 = __shfl_sync(0xffffffffu, r1, 31);
-            if (i >= m) continue;
+// Afforest-style connectivity (Sutton et al. 2018): link every vertex to its
+// first kSample live out-arcs, find the dominant component, then only the
+// vertices outside it process their remaining arcs -- in BOTH directions,
+// because an arc is stored at its source only.  Same components as linking
+// every arc, at a fraction of the arc reads (the giant component of an R-MAT
+// graph holds ~all non-isolated vertices).
+constexpr int kSample = 2;
+
+__global__ void k_aff_sample(OutView ov, int64_t n, int32_t* p) {
+    const int64_t* off = ov.off[0];
+    const int32_t* col = ov.col[0];
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+        int64_t a = off[v], b = off[v + 1];
+        int k = 0;
+        for (int64_t i = a; i < b && k < kSample; ++i) {
             int32_t c = col[i];
             if (c < 0) continue;
-            int32_t r = (int32_t)(upper_bound_dev<int64_t>(off, r0, r1 + 1, i) - 1);
-            if (r != c) uf_union(p, r, c);
+            ++k;
+            if (c != (int32_t)v) uf_union(p, (int32_t)v, c);
+        }
+    }
+}
+
+__global__ void k_uf_compress(int32_t* p, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        p[i] = uf_find(p, (int32_t)i);
+}
+
+__global__ void k_aff_gather(const int32_t* p, int64_t n, int32_t* out, int m) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x)
+        out[i] = p[(int64_t)((unsigned long long)i * 2654435761ULL % (unsigned long long)n)];
+}
+
+// Vertices outside the dominant component link the rest of their out-arcs
+// (base after the sampled ones, then every delta) and all their in-arcs.
+__global__ void k_aff_rest(OutView ov, IdxView in, int64_t n, int32_t giant, int32_t* p) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+        if (uf_find(p, (int32_t)v) == giant) continue;
+        for (int sg = 0; sg < ov.nseg; ++sg) {
+            const int64_t* off = ov.off[sg];
+            const int32_t* col = ov.col[sg];
+            int64_t a = off[v], b = off[v + 1];
+            int k = 0;
+            for (int64_t i = a; i < b; ++i) {
+                int32_t c = col[i];
+                if (c < 0) continue;
+                if (sg == 0 && k < kSample) {  // linked in the sampling pass
+                    ++k;
+                    continue;
+                }
+                if (c != (int32_t)v) uf_union(p, (int32_t)v, c);
+            }
+        }
+        if (in.off) {
+            for (int64_t e = in.off[v]; e < in.off[v + 1]; ++e) {
+                int32_t u = in.col[e];
+                if (u >= 0 && u != (int32_t)v) uf_union(p, (int32_t)v, u);
+            }
         }
     }
 }
@@ -267,13 +302,39 @@ int64_t flood_weak_components(Store& g, uint8_t* flags, KernelProf* prof) {
     cudaStream_t s = g.stream;
     int64_t n = g.n;
     if (n == 0) return 0;
+    // in-arcs are needed for directed graphs (interp.py:82-85 requires reverse)
+    IdxView in{nullptr, nullptr, nullptr};
+    if (g.directed) {
+        g.require_rev();
+        g.compact_rev();
+        in = g.rev.view();
+    }
     DBuf<int32_t> p(n, s);
     DBuf<uint8_t> seed(n, s);
     seed.zero(s);
+    OutView ov = g.out_view();
     GD_KERNEL(k_uf_init, grid_for(n, 256), 256, 0, s, p.get(), n);
-    int64_t slots = g.total_slots();
-    GD_KERNEL_T("flood_hook", 0, k_uf_hook, grid_for(std::max<int64_t>(slots, 1), 256), 256, 0, s, g.out_view(), n,
-                p.get());
+    GD_KERNEL_T("flood_sample", n * (8 + 4 * kSample), k_aff_sample, grid_for(n, 256), 256, 0, s, ov, n, p.get());
+    GD_KERNEL(k_uf_compress, grid_for(n, 256), 256, 0, s, p.get(), n);
+    constexpr int kProbe = 1024;
+    DBuf<int32_t> probe(kProbe, s);
+    GD_KERNEL(k_aff_gather, 4, 256, 0, s, p.get(), n, probe.get(), kProbe);
+    std::vector<int32_t> h(kProbe);
+    GD_CUDA(cudaMemcpyAsync(h.data(), probe.get(), kProbe * 4, cudaMemcpyDeviceToHost, s));
+    GD_CUDA(cudaStreamSynchronize(s));
+    std::sort(h.begin(), h.end());
+    int32_t giant = h[0];
+    int best = 0;
+    for (int i = 0; i < kProbe;) {
+        int j = i;
+        while (j < kProbe && h[j] == h[i]) ++j;
+        if (j - i > best) {
+            best = j - i;
+            giant = h[i];
+        }
+        i = j;
+    }
+    GD_KERNEL_T("flood_rest", 0, k_aff_rest, grid_for(n, 256), 256, 0, s, ov, in, n, giant, p.get());
     GD_KERNEL_T("flood_mark", 0, k_uf_compress_seed, grid_for(n, 256), 256, 0, s, p.get(), n, flags, seed.get());
     GD_KERNEL(k_uf_mark, grid_for(n, 256), 256, 0, s, p.get(), n, seed.get(), flags);
     return 1;

@@ -102,12 +102,20 @@ __host__ __device__ inline int64_t sat_add(int64_t a, int64_t b) {  // graphdyn_
 __host__ __device__ inline int32_t tomb(int32_t c) { return ~c; }
 __host__ __device__ inline int32_t untomb(int32_t c) { return c < 0 ? ~c : c; }
 
-// 64-bit key of a directed pair (row, col), both non-negative int32.
-__host__ __device__ inline uint64_t pair_key(int32_t r, int32_t c) {
-    return (static_cast<uint64_t>(static_cast<uint32_t>(r)) << 32) | static_cast<uint32_t>(c);
+// Key of a directed pair (row, col): row << sh | col with sh = bits(n - 1),
+// so radix sorts run over 2*sh bits only (44 for scale-22 instead of 64).
+__host__ __device__ inline uint64_t pair_key(int32_t r, int32_t c, int sh) {
+    return (static_cast<uint64_t>(static_cast<uint32_t>(r)) << sh) | static_cast<uint32_t>(c);
 }
-__host__ __device__ inline int32_t key_row(uint64_t k) { return static_cast<int32_t>(k >> 32); }
-__host__ __device__ inline int32_t key_col(uint64_t k) { return static_cast<int32_t>(k & 0xffffffffu); }
+__host__ __device__ inline int32_t key_row(uint64_t k, int sh) { return static_cast<int32_t>(k >> sh); }
+__host__ __device__ inline int32_t key_col(uint64_t k, int sh) {
+    return static_cast<int32_t>(k & ((1ULL << sh) - 1));
+}
+inline int bits_for(uint64_t v) {  // number of bits to represent v (>= 1)
+    int b = 1;
+    while (b < 64 && (v >> b)) ++b;
+    return b;
+}
 
 template <typename T>
 __device__ inline int64_t lower_bound_dev(const T* a, int64_t lo, int64_t hi, T x) {

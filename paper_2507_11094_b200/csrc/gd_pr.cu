@@ -162,6 +162,13 @@ __global__ void k_heavy_flags(const int32_t* list, int64_t m, const int64_t* off
     }
 }
 
+__global__ void k_list_degrees(const int32_t* list, int64_t m, const int64_t* off, int64_t* deg) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+        int32_t v = list[i];
+        deg[i] = off[v + 1] - off[v];
+    }
+}
+
 __global__ void k_gather_list(const int32_t* list, const int32_t* sel, int64_t m, int32_t* out) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
         out[i] = list[sel[i]];
@@ -210,6 +217,17 @@ void PR::set_lists(const int32_t* list, int64_t m) {
     if (nheavy) GD_KERNEL(k_gather_list, grid_for(nheavy, 256), 256, 0, s, list, sel.get(), nheavy, heavy.get());
     nlight = select_flagged_index(s, lf.get(), m, sel.get());
     if (nlight) GD_KERNEL(k_gather_list, grid_for(nlight, 256), 256, 0, s, list, sel.get(), nlight, light.get());
+    // in-arcs the pull reads (for the roofline's algorithmic bytes)
+    DBuf<int64_t> deg(std::max<int64_t>(nlight, nheavy), s);
+    ein_light = ein_heavy = 0;
+    if (nlight) {
+        GD_KERNEL(k_list_degrees, grid_for(nlight, 256), 256, 0, s, light.get(), nlight, g->rev.off.get(), deg.get());
+        ein_light = sum_i64(s, deg.get(), nlight);
+    }
+    if (nheavy) {
+        GD_KERNEL(k_list_degrees, grid_for(nheavy, 256), 256, 0, s, heavy.get(), nheavy, g->rev.off.get(), deg.get());
+        ein_heavy = sum_i64(s, deg.get(), nheavy);
+    }
 }
 
 // while (diff >= beta && iter < maxiter) { dangling; pull; commit }
@@ -231,11 +249,11 @@ void PR::power_loop() {
         if (nlight) {
             int64_t groups = nlight;
             unsigned grid = grid_for(groups * kGroup, kPullThreads, 148LL * 32);
-            GD_KERNEL_T("pr_pull", 0, k_pr_pull_light, grid, kPullThreads, 0, s, light.get(), nlight, ix,
+            GD_KERNEL_T("pr_pull", nlight * 24 + ein_light * 12, k_pr_pull_light, grid, kPullThreads, 0, s, light.get(), nlight, ix,
                         contrib.get(), rank.get(), scal.get(), base, damping, inv_n, rank_new.get(), scal.get() + 1);
         }
         if (nheavy)
-            GD_KERNEL_T("pr_pull_heavy", 0, k_pr_pull_heavy, (unsigned)std::min<int64_t>(nheavy, 148LL * 8),
+            GD_KERNEL_T("pr_pull_heavy", nheavy * 24 + ein_heavy * 12, k_pr_pull_heavy, (unsigned)std::min<int64_t>(nheavy, 148LL * 8),
                         kPullThreads, 0, s, heavy.get(), nheavy, ix, contrib.get(), rank.get(), scal.get(), base,
                         damping, inv_n, rank_new.get(), scal.get() + 1);
         if (nlight) GD_KERNEL(k_pr_commit, grid_for(nlight, 256), 256, 0, s, light.get(), nlight, rank_new.get(), rank.get());

@@ -13,6 +13,7 @@ struct PR : AlgoBase {
     DBuf<uint8_t> affected;
     DBuf<int32_t> light, heavy;
     int64_t nlight = 0, nheavy = 0;
+    int64_t ein_light = 0, ein_heavy = 0;  // in-arcs of the light / heavy lists
     int64_t last_sweeps = 0, last_affected = 0;
 
     PR(Store* st, double damping, double beta, int64_t maxiter);  // = staticPR

@@ -1,10 +1,14 @@
 // gd_store.cu -- the GPU diff-CSR store.  See gd_store.cuh for the layout.
 //
 // Batch application is sort + segmented-scan shaped: records are radix-sorted
-// by (src, dst), each source's chain is scanned ONCE by one warp against the
-// sorted requests of that source, and the j-th record of a pair resolves to
-// the j-th live occurrence of that pair in chain order -- the exact outcome
-// of the reference's sequential per-record scans (dynamic.py:208-286).
+// by (src, dst), each requested source's chain is scanned once (split into
+// 1024-slot work items so hub rows spread over many warps) against the sorted
+// requests of that source, and the j-th record of a pair resolves to the j-th
+// live occurrence of that pair in chain order -- the exact outcome of the
+// reference's sequential per-record scans (dynamic.py:208-286).
+//
+// Slot positions are global slot ids (gid): the concatenation of segments in
+// chain order (base first, then deltas), so sorting by gid is chain order.
 #include <algorithm>
 #include <cstring>
 
@@ -15,17 +19,22 @@ namespace gdb {
 
 namespace {
 
-constexpr int kChainShift = 40;  // chain position = seg << 40 | slot
-constexpr int64_t kSlotMask = (1LL << kChainShift) - 1;
+constexpr int kChunk = 1024;  // chain slots per delete-scan work item
+
+__device__ inline int seg_of(const int64_t* base, int nseg, int64_t gid) {
+    int s = 0;
+    while (s + 1 < nseg && base[s + 1] <= gid) ++s;
+    return s;
+}
 
 // ---------------------------------------------------------------- build ----
 
-__global__ void k_expand_edges(const int64_t* src, const int64_t* dst, const int64_t* w, int64_t m, bool directed,
+__global__ void k_expand_edges(const int64_t* src, const int64_t* dst, const int64_t* w, int64_t m, bool as_given,
                                uint32_t* key, int32_t* val, int32_t* adst, int32_t* aw) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
         int32_t s = (int32_t)src[i], d = (int32_t)dst[i];
         int32_t wi = w ? (int32_t)w[i] : 1;
-        if (directed) {
+        if (as_given) {
             key[i] = (uint32_t)s;
             val[i] = (int32_t)i;
             adst[i] = d;
@@ -43,8 +52,6 @@ __global__ void k_expand_edges(const int64_t* src, const int64_t* dst, const int
     }
 }
 
-// off[v] = number of sorted rows < v, via histogram + scan (rows need not be
-// sorted for the histogram).
 __global__ void k_hist_rows(const int32_t* rows, int64_t m, int64_t* cnt) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
         atomicAdd(reinterpret_cast<unsigned long long*>(&cnt[rows[i]]), 1ULL);
@@ -60,10 +67,10 @@ __global__ void k_gather(const T* in, const int32_t* idx, int64_t m, T* out) {
         out[i] = in[idx[i]];
 }
 
-__global__ void k_key_split(const uint64_t* key, int64_t m, int32_t* row, int32_t* col) {
+__global__ void k_key_split(const uint64_t* key, int64_t m, int sh, int32_t* row, int32_t* col) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
-        if (row) row[i] = key_row(key[i]);
-        if (col) col[i] = key_col(key[i]);
+        if (row) row[i] = key_row(key[i], sh);
+        if (col) col[i] = key_col(key[i], sh);
     }
 }
 
@@ -79,7 +86,7 @@ void offsets_from_rows(cudaStream_t s, int64_t n, const int32_t* rows, int64_t m
 
 // Directed: key (s,d).  Undirected: key (min,max) -- records of one unordered
 // pair consume occurrences of both arcs in stream order (dynamic.py:221-234).
-__global__ void k_del_keys(const int32_t* s, const int32_t* d, int64_t k, bool directed, uint64_t* key,
+__global__ void k_del_keys(const int32_t* s, const int32_t* d, int64_t k, bool directed, int sh, uint64_t* key,
                            int32_t* val) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < k; i += (int64_t)gridDim.x * blockDim.x) {
         int32_t a = s[i], b = d[i];
@@ -88,22 +95,23 @@ __global__ void k_del_keys(const int32_t* s, const int32_t* d, int64_t k, bool d
             a = b;
             b = t;
         }
-        key[i] = pair_key(a, b);
+        key[i] = pair_key(a, b, sh);
         val[i] = (int32_t)i;
     }
 }
 
 // Expand sorted records into directed requests (row, col, occurrence).
 __global__ void k_del_requests(const uint64_t* skey, const int32_t* srec, int64_t k, const int32_t* s,
-                               const int32_t* d, bool directed, uint64_t* rq_key, int32_t* rq_occ, int32_t* rq_rec,
-                               uint8_t* rq_which, int32_t* rq_ord) {
+                               const int32_t* d, bool directed, int sh, uint64_t* rq_key, int32_t* rq_occ,
+                               int32_t* rq_rec, uint8_t* rq_which, int32_t* rq_ord) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < k; i += (int64_t)gridDim.x * blockDim.x) {
         uint64_t key = skey[i];
-        int32_t j = (int32_t)(i - lower_bound_dev<uint64_t>(skey, 0, i, key));
+        int32_t j = 0;  // rank within the run of equal keys (runs are short)
+        for (int64_t p = i - 1; p >= 0 && skey[p] == key; --p) ++j;
         int32_t r = srec[i];
         int32_t a = s[r], b = d[r];
         if (directed) {
-            rq_key[i] = pair_key(a, b);
+            rq_key[i] = pair_key(a, b, sh);
             rq_occ[i] = j;
             rq_rec[i] = r;
             rq_which[i] = 0;
@@ -111,14 +119,14 @@ __global__ void k_del_requests(const uint64_t* skey, const int32_t* srec, int64_
         } else {
             int64_t o = 2 * i;
             if (a != b) {
-                rq_key[o] = pair_key(a, b);
+                rq_key[o] = pair_key(a, b, sh);
                 rq_occ[o] = j;
-                rq_key[o + 1] = pair_key(b, a);
+                rq_key[o + 1] = pair_key(b, a, sh);
                 rq_occ[o + 1] = j;
             } else {  // self-loop: two slots per record (dynamic.py:231-234)
-                rq_key[o] = pair_key(a, a);
+                rq_key[o] = pair_key(a, a, sh);
                 rq_occ[o] = 2 * j;
-                rq_key[o + 1] = pair_key(a, a);
+                rq_key[o + 1] = pair_key(a, a, sh);
                 rq_occ[o + 1] = 2 * j + 1;
             }
             rq_rec[o] = r;
@@ -132,41 +140,66 @@ __global__ void k_del_requests(const uint64_t* skey, const int32_t* srec, int64_
 }
 
 // first index of each row run in a (row,col)-sorted key array
-__global__ void k_row_starts(const uint64_t* key, int64_t m, uint8_t* flag) {
+__global__ void k_row_starts(const uint64_t* key, int64_t m, int sh, uint8_t* flag) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
-        flag[i] = (i == 0 || key_row(key[i]) != key_row(key[i - 1])) ? 1 : 0;
+        flag[i] = (i == 0 || key_row(key[i], sh) != key_row(key[i - 1], sh)) ? 1 : 0;
 }
 __global__ void k_row_starts_u32(const uint32_t* key, int64_t m, uint8_t* flag) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
         flag[i] = (i == 0 || key[i] != key[i - 1]) ? 1 : 0;
 }
 
-// One warp per requested source row: scan the chain (base, then deltas, in
-// slot order) once and emit every live slot whose column is requested.
-__global__ void k_del_scan(OutView ov, const int32_t* row_first, int64_t nrows, const uint64_t* rq_key,
-                           int64_t nrq, uint64_t* m_key, int64_t* m_pos, unsigned long long* m_cnt, int64_t cap) {
+// number of kChunk work items of every requested row (its whole chain)
+__global__ void k_row_chunks(OutView ov, const uint64_t* rq_key, const int32_t* row_first, int64_t nrows, int sh,
+                             int64_t* chunks) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nrows; i += (int64_t)gridDim.x * blockDim.x) {
+        int32_t row = key_row(rq_key[row_first[i]], sh);
+        int64_t len = 0;
+        for (int sg = 0; sg < ov.nseg; ++sg) len += ov.off[sg][row + 1] - ov.off[sg][row];
+        chunks[i] = len > 0 ? (len + kChunk - 1) / kChunk : 0;
+    }
+}
+
+// One warp per work item (row, 1024-slot chunk of its chain): every live slot
+// whose column is requested for that row is emitted as a match (key, gid).
+__global__ void __launch_bounds__(256) k_del_scan(OutView ov, const int32_t* row_first, const int64_t* coff,
+                                                  int64_t nrows, int64_t nwork, const uint64_t* rq_key, int64_t nrq,
+                                                  int sh, uint64_t* m_key, int64_t* m_gid, unsigned long long* m_cnt,
+                                                  int64_t cap) {
     const int lane = threadIdx.x & 31;
     int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t r = warp; r < nrows; r += nwarps) {
-        int64_t lo = row_first[r];
-        int64_t hi = (r + 1 < nrows) ? row_first[r + 1] : nrq;
-        int32_t row = key_row(rq_key[lo]);
-        uint64_t klo = pair_key(row, 0);
-        for (int sg = 0; sg < ov.nseg; ++sg) {
+    for (int64_t wk = warp; wk < nwork; wk += nwarps) {
+        int64_t i = upper_bound_dev<int64_t>(coff, 0, nrows, wk) - 1;
+        int64_t chunk = wk - coff[i];
+        int64_t lo = row_first[i];
+        int64_t hi = (i + 1 < nrows) ? row_first[i + 1] : nrq;
+        int32_t row = key_row(rq_key[lo], sh);
+        int64_t ncols = hi - lo;
+        int32_t c0 = key_col(rq_key[lo], sh);
+        int32_t c1 = ncols > 1 ? key_col(rq_key[lo + 1], sh) : -2;
+        int64_t p0 = chunk * kChunk, p1 = p0 + kChunk;
+        int64_t acc = 0;  // chain offset of the current segment's part of the row
+        for (int sg = 0; sg < ov.nseg && acc < p1; ++sg) {
             const int64_t* off = ov.off[sg];
             const int32_t* col = ov.col[sg];
-            int64_t a = off[row], b = off[row + 1];
-            for (int64_t base = a; base < b; base += 32) {
-                int64_t i = base + lane;
+            int64_t a = off[row], L = off[row + 1] - a;
+            int64_t s0 = max(p0, acc), s1 = min(p1, acc + L);
+            for (int64_t x0 = s0; x0 < s1; x0 += 32) {
+                int64_t x = x0 + lane;
                 bool hit = false;
                 int32_t c = -1;
-                if (i < b) {
-                    c = col[i];
+                int64_t idx = a + (x - acc);
+                if (x < s1) {
+                    c = col[idx];
                     if (c >= 0) {
-                        uint64_t want = klo | (uint32_t)c;
-                        int64_t p = lower_bound_dev<uint64_t>(rq_key, lo, hi, want);
-                        hit = (p < hi && rq_key[p] == want);
+                        if (ncols <= 2) {
+                            hit = (c == c0) || (c == c1);
+                        } else {
+                            uint64_t want = pair_key(row, c, sh);
+                            int64_t p = lower_bound_dev<uint64_t>(rq_key, lo, hi, want);
+                            hit = (p < hi && rq_key[p] == want);
+                        }
                     }
                 }
                 unsigned mask = __ballot_sync(0xffffffffu, hit);
@@ -177,26 +210,27 @@ __global__ void k_del_scan(OutView ov, const int32_t* row_first, int64_t nrows, 
                     if (hit) {
                         int64_t slot = (int64_t)basei + __popc(mask & ((1u << lane) - 1));
                         if (slot < cap) {
-                            m_key[slot] = klo | (uint32_t)c;
-                            m_pos[slot] = ((int64_t)sg << kChainShift) | i;
+                            m_key[slot] = pair_key(row, c, sh);
+                            m_gid[slot] = ov.base[sg] + idx;
                         }
                     }
                 }
             }
+            acc += L;
         }
     }
 }
 
-// Resolve each request against the (key, chain-pos)-sorted matches.
+// Resolve each request against the (key, gid)-sorted matches.
 __global__ void k_del_resolve(const uint64_t* rq_key, const int32_t* rq_occ, const int32_t* rq_rec,
-                              const uint8_t* rq_which, int64_t nrq, const uint64_t* m_key, const int64_t* m_pos,
+                              const uint8_t* rq_which, int64_t nrq, const uint64_t* m_key, const int64_t* m_gid,
                               int64_t nm, int64_t* rq_pos, uint8_t* found_fwd) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nrq; i += (int64_t)gridDim.x * blockDim.x) {
         uint64_t key = rq_key[i];
         int64_t lo = lower_bound_dev<uint64_t>(m_key, 0, nm, key);
-        int64_t hi = upper_bound_dev<uint64_t>(m_key, lo, nm, key);
         int64_t occ = rq_occ[i];
-        int64_t pos = (occ < hi - lo) ? m_pos[lo + occ] : -1;
+        int64_t pos = -1;
+        if (lo + occ < nm && m_key[lo + occ] == key) pos = m_gid[lo + occ];
         rq_pos[i] = pos;
         if (rq_which[i] == 0) found_fwd[rq_rec[i]] = pos >= 0 ? 1 : 0;
     }
@@ -205,24 +239,24 @@ __global__ void k_del_resolve(const uint64_t* rq_key, const int32_t* rq_occ, con
 // Tombstone the resolved slots.  A reverse-direction request only applies
 // when its record's forward arc was found (dynamic.py:221-229).
 __global__ void k_del_kill(OutView ov, const uint64_t* rq_key, const int32_t* rq_rec, const uint8_t* rq_which,
-                           const int64_t* rq_pos, int64_t nrq, const uint8_t* found_fwd, int32_t* k_row,
-                           int32_t* k_col, int32_t* k_w, int64_t* k_pos, unsigned long long* k_cnt) {
+                           const int64_t* rq_pos, int64_t nrq, const uint8_t* found_fwd, int sh, int32_t* k_row,
+                           int32_t* k_col, int32_t* k_w, int64_t* k_gid, unsigned long long* k_cnt) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nrq; i += (int64_t)gridDim.x * blockDim.x) {
-        int64_t pos = rq_pos[i];
-        if (pos < 0) continue;
+        int64_t gid = rq_pos[i];
+        if (gid < 0) continue;
         if (rq_which[i] == 1 && !found_fwd[rq_rec[i]]) continue;
-        int sg = (int)(pos >> kChainShift);
-        int64_t slot = pos & kSlotMask;
+        int sg = seg_of(ov.base, ov.nseg, gid);
+        int64_t slot = gid - ov.base[sg];
         int32_t* col = const_cast<int32_t*>(ov.col[sg]);
         const int32_t* w = ov.w[sg];
         int32_t c = col[slot];
         int32_t wt = w ? w[slot] : 1;
         col[slot] = kSentinel;
         unsigned long long o = atomicAdd(k_cnt, 1ULL);
-        k_row[o] = key_row(rq_key[i]);
+        k_row[o] = key_row(rq_key[i], sh);
         k_col[o] = c;
         k_w[o] = wt;
-        k_pos[o] = pos;
+        k_gid[o] = gid;
     }
 }
 
@@ -256,7 +290,7 @@ __global__ void k_add_arcs(const int32_t* s, const int32_t* d, const int32_t* w,
 // One warp per source row with inserts: list the first `want` vacancies of
 // the chain in slot order (ballot + prefix keeps the order).
 __global__ void k_add_vacancies(OutView ov, const uint32_t* skey, const int32_t* row_first, int64_t nrows,
-                                int64_t narcs, int64_t* vac_pos) {
+                                int64_t narcs, int64_t* vac_gid) {
     const int lane = threadIdx.x & 31;
     int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -275,7 +309,7 @@ __global__ void k_add_vacancies(OutView ov, const uint32_t* skey, const int32_t*
                 unsigned mask = __ballot_sync(0xffffffffu, vac);
                 if (vac) {
                     int64_t t = got + __popc(mask & ((1u << lane) - 1));
-                    if (t < want) vac_pos[lo + t] = ((int64_t)sg << kChainShift) | i;
+                    if (t < want) vac_gid[lo + t] = ov.base[sg] + i;
                 }
                 got += __popc(mask);
             }
@@ -283,18 +317,18 @@ __global__ void k_add_vacancies(OutView ov, const uint32_t* skey, const int32_t*
     }
 }
 
-__global__ void k_add_claim(OutView ov, const int32_t* sval, const int32_t* a_row, const int32_t* a_col,
-                            const int32_t* a_w, const int64_t* vac_pos, int64_t narcs, uint8_t* leftover) {
+__global__ void k_add_claim(OutView ov, const int32_t* sval, const int32_t* a_col, const int32_t* a_w,
+                            const int64_t* vac_gid, int64_t narcs, uint8_t* leftover) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < narcs; i += (int64_t)gridDim.x * blockDim.x) {
-        int64_t pos = vac_pos[i];
-        if (pos < 0) {
+        int64_t gid = vac_gid[i];
+        if (gid < 0) {
             leftover[i] = 1;
             continue;
         }
         leftover[i] = 0;
         int32_t a = sval[i];
-        int sg = (int)(pos >> kChainShift);
-        int64_t slot = pos & kSlotMask;
+        int sg = seg_of(ov.base, ov.nseg, gid);
+        int64_t slot = gid - ov.base[sg];
         const_cast<int32_t*>(ov.col[sg])[slot] = a_col[a];
         if (ov.w[sg]) const_cast<int32_t*>(ov.w[sg])[slot] = a_w[a];
     }
@@ -318,28 +352,30 @@ __global__ void k_tomb_still_dead(const int64_t* pos, int64_t m, const int32_t* 
 
 // ----------------------------------------------------- index maintenance ----
 
-// For each killed arc, the index entry (ix_row, ix_col, w) it maps to.
+// For each killed arc, the index entry (ix_row, ix_col) it maps to, and its
+// weight as a secondary sort key.
 __global__ void k_kill_to_index(const int32_t* k_row, const int32_t* k_col, const int32_t* k_w, int64_t m,
-                                bool rows_are_dst, uint64_t* key, int32_t* val, int32_t* wkey) {
+                                bool rows_are_dst, int sh, uint64_t* key, int32_t* val, uint32_t* wkey) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
         int32_t r = rows_are_dst ? k_col[i] : k_row[i];
         int32_t c = rows_are_dst ? k_row[i] : k_col[i];
-        key[i] = pair_key(r, c);
+        key[i] = pair_key(r, c, sh);
         val[i] = (int32_t)i;
-        wkey[i] = k_w[i];
+        wkey[i] = (uint32_t)k_w[i];
     }
 }
 
 // Items sorted by (key, w); the j-th item of an equal (key, w) run tombstones
 // the j-th live entry with that column and weight in the (clean) row.
-__global__ void k_index_kill(const uint64_t* key, const int32_t* wk, int64_t m, int64_t* off, int32_t* col,
-                             const int32_t* w, int64_t* t_pos, int32_t* t_row, unsigned long long* t_cnt) {
+__global__ void k_index_kill(const uint64_t* key, const int32_t* wk, int64_t m, int sh, const int64_t* off,
+                             int32_t* col, const int32_t* w, int64_t* t_pos, int32_t* t_row,
+                             unsigned long long* t_cnt) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
         uint64_t kk = key[i];
         int32_t wt = wk[i];
         int64_t j = 0;
         for (int64_t p = i - 1; p >= 0 && key[p] == kk && wk[p] == wt; --p) ++j;
-        int32_t r = key_row(kk), c = key_col(kk);
+        int32_t r = key_row(kk, sh), c = key_col(kk, sh);
         int64_t lo = col_lower(col, off[r], off[r + 1], c);
         int64_t hi = col_upper(col, lo, off[r + 1], c);
         for (int64_t e = lo; e < hi; ++e) {
@@ -358,12 +394,12 @@ __global__ void k_index_kill(const uint64_t* key, const int32_t* wk, int64_t m, 
     }
 }
 
-__global__ void k_added_to_index(const int32_t* a_row, const int32_t* a_col, int64_t m, bool rows_are_dst,
+__global__ void k_added_to_index(const int32_t* a_row, const int32_t* a_col, int64_t m, bool rows_are_dst, int sh,
                                   uint64_t* key, int32_t* val) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
         int32_t r = rows_are_dst ? a_col[i] : a_row[i];
         int32_t c = rows_are_dst ? a_row[i] : a_col[i];
-        key[i] = pair_key(r, c);
+        key[i] = pair_key(r, c, sh);
         val[i] = (int32_t)i;
     }
 }
@@ -383,7 +419,7 @@ __global__ void k_out_ins_pos(const int32_t* irow, int64_t m, const int64_t* off
         ipos[i] = off0[irow[i] + 1];
 }
 
-// row of every slot of a (small) delta segment, live flag
+// row of every slot of a segment + live flag
 __global__ void k_delta_rows(const int64_t* off, int64_t n, const int32_t* col, int64_t nslots, int32_t* row,
                              uint8_t* live) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nslots;
@@ -410,36 +446,65 @@ __global__ void k_add_offsets(const int64_t* off, const int64_t* shift, int64_t 
         out[i] = off[i] + shift[i];
 }
 
-constexpr int kTile = 2048;
 constexpr int kEditThreads = 256;
+constexpr int kPerThread = 8;
+constexpr int kTile = kEditThreads * kPerThread;  // 2048 entries per tile
 
-// Base entries: newpos(i) = i - #tombs(< i) + #inserts(P <= i).  Each CTA
-// owns a tile; it locates the tombs / inserts overlapping the tile once, so
-// per-entry searches run over the (usually empty) in-tile range.
+// Per tile: first tomb >= tile start, first insert with P > tile start - 1
+// (all tiles in parallel, instead of one searching thread per CTA).
+__global__ void k_tile_bounds(int64_t ntiles, const int64_t* tpos, int64_t ntomb, const int64_t* ipos, int64_t nins,
+                              int64_t* tb, int64_t* pj) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t <= ntiles; t += (int64_t)gridDim.x * blockDim.x) {
+        int64_t p = t * kTile;
+        tb[t] = lower_bound_dev<int64_t>(tpos, 0, ntomb, p);
+        pj[t] = upper_bound_dev<int64_t>(ipos, 0, nins, p - 1);
+    }
+}
+
+// Base entries: newpos(i) = i - #tombs(< i) + #inserts(P <= i).  Each thread
+// owns kPerThread consecutive entries: one bounded search for its first entry,
+// then the two counters only advance at the (sparse) tomb / insert positions.
 __global__ void __launch_bounds__(kEditThreads) k_edit_base(const int32_t* col, const int32_t* w, int64_t nnz,
-                                                            const int64_t* tpos, int64_t ntomb, const int64_t* ipos,
-                                                            int64_t nins, int32_t* ocol, int32_t* ow) {
-    __shared__ int64_t sh[4];
-    for (int64_t t0 = (int64_t)blockIdx.x * kTile; t0 < nnz; t0 += (int64_t)gridDim.x * kTile) {
-        int64_t t1 = min(t0 + (int64_t)kTile, nnz);
-        if (threadIdx.x == 0) {
-            sh[0] = lower_bound_dev<int64_t>(tpos, 0, ntomb, t0);
-            sh[1] = lower_bound_dev<int64_t>(tpos, sh[0], ntomb, t1);
-            sh[2] = upper_bound_dev<int64_t>(ipos, 0, nins, t0 - 1);  // #P <= t0-1
-            sh[3] = upper_bound_dev<int64_t>(ipos, sh[2], nins, t1 - 1);
+                                                            const int64_t* tpos, const int64_t* ipos,
+                                                            const int64_t* tb_tile, const int64_t* pj_tile,
+                                                            int64_t ntiles, int32_t* ocol, int32_t* ow) {
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        int64_t t0 = tile * kTile;
+        int64_t tb0 = tb_tile[tile], tb1 = tb_tile[tile + 1];
+        int64_t pj0 = pj_tile[tile], pj1 = pj_tile[tile + 1];
+        int64_t i0 = t0 + (int64_t)threadIdx.x * kPerThread;
+        if (i0 >= nnz) continue;
+        int64_t i1 = min(i0 + kPerThread, nnz);
+        int64_t tb = (tb0 == tb1) ? tb0 : lower_bound_dev<int64_t>(tpos, tb0, tb1, i0);
+        int64_t pj = (pj0 == pj1) ? pj0 : upper_bound_dev<int64_t>(ipos, pj0, pj1, i0 - 1);
+        int32_t v[kPerThread];
+        int32_t ww[kPerThread];
+        if (i1 - i0 == kPerThread) {  // 32-byte aligned (tiles and chunks are multiples of 8)
+            const int4* c4 = reinterpret_cast<const int4*>(col + i0);
+            int4 a = c4[0], b = c4[1];
+            v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+            if (w) {
+                const int4* w4 = reinterpret_cast<const int4*>(w + i0);
+                int4 x = w4[0], y = w4[1];
+                ww[0] = x.x; ww[1] = x.y; ww[2] = x.z; ww[3] = x.w; ww[4] = y.x; ww[5] = y.y; ww[6] = y.z; ww[7] = y.w;
+            }
+        } else {
+            for (int q = 0; q < kPerThread; ++q) {
+                v[q] = (i0 + q < i1) ? col[i0 + q] : -1;
+                ww[q] = (w && i0 + q < i1) ? w[i0 + q] : 0;
+            }
         }
-        __syncthreads();
-        int64_t tb0 = sh[0], tb1 = sh[1], pj0 = sh[2], pj1 = sh[3];
-        for (int64_t i = t0 + threadIdx.x; i < t1; i += blockDim.x) {
-            int32_t c = col[i];
-            if (c < 0) continue;
-            int64_t tb = (tb0 == tb1) ? tb0 : lower_bound_dev<int64_t>(tpos, tb0, tb1, i);
-            int64_t pj = (pj0 == pj1) ? pj0 : upper_bound_dev<int64_t>(ipos, pj0, pj1, i);
+#pragma unroll
+        for (int q = 0; q < kPerThread; ++q) {
+            int64_t i = i0 + q;
+            if (i >= i1) break;
+            while (tb < tb1 && tpos[tb] < i) ++tb;
+            while (pj < pj1 && ipos[pj] <= i) ++pj;
+            if (v[q] < 0) continue;
             int64_t np = i - tb + pj;
-            ocol[np] = c;
-            if (ow) ow[np] = w[i];
+            ocol[np] = v[q];
+            if (ow) ow[np] = ww[q];
         }
-        __syncthreads();
     }
 }
 
@@ -461,9 +526,15 @@ __global__ void k_export_seg(const int32_t* col, const int32_t* w, int64_t m, in
     }
 }
 
-__global__ void k_live_flags(const int32_t* col, int64_t m, uint8_t* f) {
+__global__ void k_select_base_kills(const int64_t* gid, int64_t m, int64_t base_slots, uint8_t* flag) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
-        f[i] = col[i] >= 0 ? 1 : 0;
+        flag[i] = gid[i] < base_slots ? 1 : 0;
+}
+
+template <typename T>
+__global__ void k_gather_sel(const T* in, const int32_t* sel, int64_t m, T* out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = in[sel[i]];
 }
 
 }  // namespace
@@ -487,9 +558,15 @@ void edit_merge(cudaStream_t s, int64_t n, const int64_t* off, const int32_t* co
     if (weighted) new_w.alloc(new_nnz, s);
     else new_w.release();
     if (nnz) {
-        unsigned g = (unsigned)std::min<int64_t>((nnz + kTile - 1) / kTile, 148LL * 16);
-        GD_KERNEL_T("merge_copy", 0, k_edit_base, g, kEditThreads, 0, s, col, weighted ? w : nullptr, nnz, tpos,
-                    ntomb, ipos, nins, new_col.get(), weighted ? new_w.get() : nullptr);
+        int64_t ntiles = (nnz + kTile - 1) / kTile;
+        DBuf<int64_t> tb(ntiles + 1, s), pj(ntiles + 1, s);
+        GD_KERNEL(k_tile_bounds, grid_for(ntiles + 1, 256), 256, 0, s, ntiles, tpos, ntomb, ipos, nins, tb.get(),
+                  pj.get());
+        unsigned g = (unsigned)std::min<int64_t>(ntiles, 148LL * 64);
+        // algorithmic bytes: every base entry read once, every surviving entry written once
+        GD_KERNEL_T("merge_copy", (nnz + (nnz - ntomb)) * (weighted ? 8 : 4), k_edit_base, g, kEditThreads, 0, s,
+                    col, weighted ? w : nullptr, nnz, tpos, ipos, tb.get(), pj.get(), ntiles, new_col.get(),
+                    weighted ? new_w.get() : nullptr);
     }
     if (nins)
         GD_KERNEL(k_edit_ins, grid_for(nins, 256), 256, 0, s, icol, iw, ipos, nins, tpos, ntomb, new_col.get(),
@@ -501,8 +578,15 @@ void edit_merge(cudaStream_t s, int64_t n, const int64_t* off, const int32_t* co
 Store::Store(int dev, int64_t n_, const int64_t* src, const int64_t* dst, const int64_t* w, int64_t m, bool dir,
              bool wtd, bool with_rev, int64_t mi, bool as_arcs)
     : device(dev), n(n_), directed(dir), weighted(wtd), with_reverse(with_rev), merge_interval(mi) {
+    sh = bits_for((uint64_t)std::max<int64_t>(n - 1, 1));
     GD_CUDA(cudaSetDevice(device));
     GD_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    // keep freed stream-ordered memory in the pool across syncs: per-batch
+    // temporaries are re-used instead of being unmapped and re-mapped
+    cudaMemPool_t pool;
+    GD_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t keep = UINT64_MAX;
+    GD_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
     cudaStream_t s = stream;
     bool expand = !directed && !as_arcs;
     int64_t na = expand ? 2 * m : m;
@@ -519,7 +603,7 @@ Store::Store(int dev, int64_t n_, const int64_t* src, const int64_t* dst, const 
         GD_KERNEL(k_expand_edges, grid_for(m, 256), 256, 0, s, hs.get(), hd.get(), w ? hw.get() : nullptr, m,
                   !expand, key.get(), val.get(), adst.get(), aw.get());
     // stable sort by source keeps insertion order within a source (dynamic.py:116)
-    sort_pairs_u32(s, key.get(), val.get(), na);
+    sort_pairs_u32(s, key.get(), val.get(), na, sh);
     OutSeg base;
     base.nslots = na;
     base.col.alloc(na, s);
@@ -551,26 +635,28 @@ Store::~Store() {
 }
 
 void Store::upload_tables() {
-    std::vector<const int64_t*> o;
-    std::vector<const int32_t*> c, w;
-    for (auto& sg : segs) {
-        o.push_back(sg.off.get());
-        c.push_back(sg.col.get());
-        w.push_back(sg.w.n ? sg.w.get() : nullptr);
-    }
     size_t k = segs.size();
-    tab_off.ensure(k, stream);
-    tab_col.ensure(k, stream);
-    tab_w.ensure(k, stream);
-    GD_CUDA(cudaMemcpyAsync(tab_off.get(), o.data(), k * sizeof(void*), cudaMemcpyHostToDevice, stream));
-    GD_CUDA(cudaMemcpyAsync(tab_col.get(), c.data(), k * sizeof(void*), cudaMemcpyHostToDevice, stream));
-    GD_CUDA(cudaMemcpyAsync(tab_w.get(), w.data(), k * sizeof(void*), cudaMemcpyHostToDevice, stream));
-    // the host vectors die at scope exit: make the copies complete first
-    GD_CUDA(cudaStreamSynchronize(stream));
+    // the previous copy may still be in flight: wait before reusing the host table
+    if (tab_k) GD_CUDA(cudaStreamSynchronize(stream));
+    h_tab.assign(4 * k, 0);
+    int64_t acc = 0;
+    for (size_t i = 0; i < k; ++i) {
+        h_tab[i] = reinterpret_cast<uintptr_t>(segs[i].off.get());
+        h_tab[k + i] = reinterpret_cast<uintptr_t>(segs[i].col.get());
+        h_tab[2 * k + i] = reinterpret_cast<uintptr_t>(segs[i].w.n ? segs[i].w.get() : nullptr);
+        h_tab[3 * k + i] = (uintptr_t)acc;
+        acc += segs[i].nslots;
+    }
+    tab.ensure(4 * k, stream);
+    GD_CUDA(cudaMemcpyAsync(tab.get(), h_tab.data(), 4 * k * sizeof(uintptr_t), cudaMemcpyHostToDevice, stream));
+    tab_k = k;
 }
 
 OutView Store::out_view() const {
-    return OutView{(int)segs.size(), tab_off.get(), tab_col.get(), tab_w.get()};
+    const uintptr_t* t = tab.get();
+    size_t k = tab_k;
+    return OutView{(int)k, reinterpret_cast<const int64_t* const*>(t), reinterpret_cast<const int32_t* const*>(t + k),
+                   reinterpret_cast<const int32_t* const*>(t + 2 * k), reinterpret_cast<const int64_t*>(t + 3 * k)};
 }
 
 int64_t Store::total_slots() const {
@@ -591,7 +677,6 @@ int64_t Store::device_bytes() const {
 void Store::build_index(SortedIndex& ix, bool rows_are_dst) {
     cudaStream_t s = stream;
     ix.rows_are_dst = rows_are_dst;
-    // gather live arcs (row, col, w) of every segment
     int64_t tot = total_slots();
     DBuf<uint64_t> key(tot, s);
     DBuf<int32_t> val(tot, s), wv(tot, s);
@@ -615,18 +700,18 @@ void Store::build_index(SortedIndex& ix, bool rows_are_dst) {
             GD_KERNEL(k_gather<int32_t>, grid_for(c, 256), 256, 0, s, sg.w.get(), sel.get(), c, tmp.w.get());
         else
             fill_i32(s, tmp.w.get(), c, 1);
-        GD_KERNEL(k_added_to_index, grid_for(c, 256), 256, 0, s, tmp.row.get(), tmp.col.get(), c, rows_are_dst,
+        GD_KERNEL(k_added_to_index, grid_for(c, 256), 256, 0, s, tmp.row.get(), tmp.col.get(), c, rows_are_dst, sh,
                   key.get() + m, val.get() + m);
         GD_CUDA(cudaMemcpyAsync(wv.get() + m, tmp.w.get(), c * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
         m += c;
     }
     // val = position in the concatenation (indexes wv); the key carries (row, col)
     iota_i32(s, val.get(), m);
-    sort_pairs_u64(s, key.get(), val.get(), m);
+    sort_pairs_u64(s, key.get(), val.get(), m, 2 * sh);
     ix.nnz = m;
     ix.col.alloc(m, s);
     DBuf<int32_t> rows(m, s);
-    if (m) GD_KERNEL(k_key_split, grid_for(m, 256), 256, 0, s, key.get(), m, rows.get(), ix.col.get());
+    if (m) GD_KERNEL(k_key_split, grid_for(m, 256), 256, 0, s, key.get(), m, sh, rows.get(), ix.col.get());
     if (weighted) {
         ix.w.alloc(m, s);
         if (m) GD_KERNEL(k_gather<int32_t>, grid_for(m, 256), 256, 0, s, wv.get(), val.get(), m, ix.w.get());
@@ -678,25 +763,22 @@ void Store::index_delete(SortedIndex& ix, const KilledArcs& ka) {
     cudaStream_t s = stream;
     int64_t m = ka.count;
     DBuf<uint64_t> key(m, s);
-    DBuf<int32_t> val(m, s), wk(m, s);
+    DBuf<int32_t> val(m, s);
+    DBuf<uint32_t> wkey(m, s);
     GD_KERNEL(k_kill_to_index, grid_for(m, 256), 256, 0, s, ka.row.get(), ka.col.get(), ka.w.get(), m,
-              ix.rows_are_dst, key.get(), val.get(), wk.get());
-    // order by (key, w): stable sort by w, then by key
-    {
-        DBuf<uint32_t> wkey(m, s);
-        GD_CUDA(cudaMemcpyAsync(wkey.get(), wk.get(), m * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
-        DBuf<int32_t> perm(m, s);
-        iota_i32(s, perm.get(), m);
-        sort_pairs_u32(s, wkey.get(), perm.get(), m);  // weights are >= 0 here
-        DBuf<uint64_t> k2(m, s);
-        GD_KERNEL(k_gather<uint64_t>, grid_for(m, 256), 256, 0, s, key.get(), perm.get(), m, k2.get());
-        sort_pairs_u64(s, k2.get(), perm.get(), m);
-        DBuf<int32_t> w2(m, s);
-        GD_KERNEL(k_gather<int32_t>, grid_for(m, 256), 256, 0, s, wk.get(), perm.get(), m, w2.get());
-        key = std::move(k2);
-        wk = std::move(w2);
+              ix.rows_are_dst, sh, key.get(), val.get(), wkey.get());
+    DBuf<uint64_t> k2(m, s);
+    DBuf<int32_t> w2(m, s);
+    if (weighted) {  // order by (key, w): stable sort by w, then by key
+        sort_pairs_u32(s, wkey.get(), val.get(), m);
+        GD_KERNEL(k_gather<uint64_t>, grid_for(m, 256), 256, 0, s, key.get(), val.get(), m, k2.get());
+        sort_pairs_u64(s, k2.get(), val.get(), m, 2 * sh);
+        GD_KERNEL(k_gather<int32_t>, grid_for(m, 256), 256, 0, s, ka.w.get(), val.get(), m, w2.get());
+    } else {
+        sort_pairs_u64(s, key.get(), val.get(), m, 2 * sh);
+        GD_CUDA(cudaMemcpyAsync(k2.get(), key.get(), m * 8, cudaMemcpyDeviceToDevice, s));
+        fill_i32(s, w2.get(), m, 1);
     }
-    // append to the index tomb log
     int64_t old = ix.ntomb;
     DBuf<int64_t> tpos(old + m, s);
     DBuf<int32_t> trow(old + m, s);
@@ -706,14 +788,14 @@ void Store::index_delete(SortedIndex& ix, const KilledArcs& ka) {
     }
     DBuf<unsigned long long> cnt(1, s);
     cnt.zero(s);
-    GD_KERNEL(k_index_kill, grid_for(m, 256), 256, 0, s, key.get(), wk.get(), m, ix.off.get(), ix.col.get(),
+    GD_KERNEL(k_index_kill, grid_for(m, 256), 256, 0, s, k2.get(), w2.get(), m, sh, ix.off.get(), ix.col.get(),
               ix.w.n ? ix.w.get() : nullptr, tpos.get() + old, trow.get() + old, cnt.get());
     int64_t killed = (int64_t)read_scalar(s, cnt.get());
     int64_t tot = old + killed;
     // keep the log sorted by position
     DBuf<uint64_t> pk(tot, s);
     GD_CUDA(cudaMemcpyAsync(pk.get(), tpos.get(), tot * 8, cudaMemcpyDeviceToDevice, s));
-    sort_pairs_u64(s, pk.get(), trow.get(), tot);
+    sort_pairs_u64(s, pk.get(), trow.get(), tot, bits_for((uint64_t)std::max<int64_t>(ix.nnz, 1)));
     GD_CUDA(cudaMemcpyAsync(tpos.get(), pk.get(), tot * 8, cudaMemcpyDeviceToDevice, s));
     ix.tpos = std::move(tpos);
     ix.trow = std::move(trow);
@@ -727,12 +809,12 @@ void Store::index_add(SortedIndex& ix, const AddedArcs& aa) {
     int64_t m = aa.count;
     DBuf<uint64_t> key(m, s);
     DBuf<int32_t> val(m, s);
-    GD_KERNEL(k_added_to_index, grid_for(m, 256), 256, 0, s, aa.row.get(), aa.col.get(), m, ix.rows_are_dst,
+    GD_KERNEL(k_added_to_index, grid_for(m, 256), 256, 0, s, aa.row.get(), aa.col.get(), m, ix.rows_are_dst, sh,
               key.get(), val.get());
-    sort_pairs_u64(s, key.get(), val.get(), m);
+    sort_pairs_u64(s, key.get(), val.get(), m, 2 * sh);
     ix.drow.alloc(m, s);
     ix.dcol.alloc(m, s);
-    GD_KERNEL(k_key_split, grid_for(m, 256), 256, 0, s, key.get(), m, ix.drow.get(), ix.dcol.get());
+    GD_KERNEL(k_key_split, grid_for(m, 256), 256, 0, s, key.get(), m, sh, ix.drow.get(), ix.dcol.get());
     if (weighted) {
         ix.dw.alloc(m, s);
         GD_KERNEL(k_gather<int32_t>, grid_for(m, 256), 256, 0, s, aa.w.get(), val.get(), m, ix.dw.get());
@@ -752,42 +834,31 @@ void Store::append_out_tombs(const int64_t* d_pos, const int32_t* d_row, int64_t
     }
     GD_CUDA(cudaMemcpyAsync(pk.get() + notomb, d_pos, cnt * 8, cudaMemcpyDeviceToDevice, s));
     GD_CUDA(cudaMemcpyAsync(rw.get() + notomb, d_row, cnt * 4, cudaMemcpyDeviceToDevice, s));
-    sort_pairs_u64(s, pk.get(), rw.get(), tot);
+    sort_pairs_u64(s, pk.get(), rw.get(), tot, bits_for((uint64_t)std::max<int64_t>(segs[0].nslots, 1)));
     otpos.alloc(tot, s);
     GD_CUDA(cudaMemcpyAsync(otpos.get(), pk.get(), tot * 8, cudaMemcpyDeviceToDevice, s));
     otrow = std::move(rw);
     notomb = tot;
 }
 
-namespace {
-__global__ void k_select_base_kills(const int64_t* pos, const int32_t* row, int64_t m, uint8_t* flag) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
-        flag[i] = (pos[i] >> kChainShift) == 0 ? 1 : 0;
-}
-template <typename T>
-__global__ void k_gather_sel(const T* in, const int32_t* sel, int64_t m, T* out) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
-        out[i] = in[sel[i]];
-}
-}  // namespace
-
 int64_t Store::apply_deletes(const int32_t* d_src, const int32_t* d_dst, int64_t k, uint8_t* d_found) {
     cudaStream_t s = stream;
     if (k == 0) return 0;
     if (rev.built) compact_index(rev);
     if (fwd.built) compact_index(fwd);
+    const int kb = 2 * sh;
     DBuf<uint64_t> skey(k, s);
     DBuf<int32_t> srec(k, s);
-    GD_KERNEL(k_del_keys, grid_for(k, 256), 256, 0, s, d_src, d_dst, k, directed, skey.get(), srec.get());
-    sort_pairs_u64(s, skey.get(), srec.get(), k);
+    GD_KERNEL(k_del_keys, grid_for(k, 256), 256, 0, s, d_src, d_dst, k, directed, sh, skey.get(), srec.get());
+    sort_pairs_u64(s, skey.get(), srec.get(), k, kb);
     int64_t nrq = directed ? k : 2 * k;
     DBuf<uint64_t> rq_key(nrq, s);
     DBuf<int32_t> rq_occ(nrq, s), rq_rec(nrq, s), rq_ord(nrq, s);
     DBuf<uint8_t> rq_which(nrq, s);
-    GD_KERNEL(k_del_requests, grid_for(k, 256), 256, 0, s, skey.get(), srec.get(), k, d_src, d_dst, directed,
+    GD_KERNEL(k_del_requests, grid_for(k, 256), 256, 0, s, skey.get(), srec.get(), k, d_src, d_dst, directed, sh,
               rq_key.get(), rq_occ.get(), rq_rec.get(), rq_which.get(), rq_ord.get());
     if (!directed) {  // order the requests by directed key (stable: occ order kept)
-        sort_pairs_u64(s, rq_key.get(), rq_ord.get(), nrq);
+        sort_pairs_u64(s, rq_key.get(), rq_ord.get(), nrq, kb);
         DBuf<int32_t> o2(nrq, s), r2(nrq, s);
         DBuf<uint8_t> w2(nrq, s);
         GD_KERNEL(k_gather_sel<int32_t>, grid_for(nrq, 256), 256, 0, s, rq_occ.get(), rq_ord.get(), nrq, o2.get());
@@ -798,42 +869,50 @@ int64_t Store::apply_deletes(const int32_t* d_src, const int32_t* d_dst, int64_t
         rq_rec = std::move(r2);
         rq_which = std::move(w2);
     }
-    // distinct source rows
+    // distinct source rows and their chain work items
     DBuf<uint8_t> rflag(nrq, s);
-    GD_KERNEL(k_row_starts, grid_for(nrq, 256), 256, 0, s, rq_key.get(), nrq, rflag.get());
+    GD_KERNEL(k_row_starts, grid_for(nrq, 256), 256, 0, s, rq_key.get(), nrq, sh, rflag.get());
     DBuf<int32_t> row_first(nrq, s);
     int64_t nrows = select_flagged_index(s, rflag.get(), nrq, row_first.get());
-    // scan chains, collect matches (retry once with the exact size on overflow)
     OutView ov = out_view();
+    DBuf<int64_t> chunks(nrows + 1, s), coff(nrows + 1, s);
+    GD_KERNEL(k_row_chunks, grid_for(nrows, 256), 256, 0, s, ov, rq_key.get(), row_first.get(), nrows, sh,
+              chunks.get());
+    GD_CUDA(cudaMemsetAsync(chunks.get() + nrows, 0, 8, s));
+    exclusive_scan_i64(s, chunks.get(), coff.get(), nrows + 1);
+    int64_t nwork = read_scalar(s, coff.get() + nrows);
+    // scan chains, collect matches (retry once with the exact size on overflow)
     int64_t cap = 2 * nrq + 1024;
     DBuf<uint64_t> m_key;
-    DBuf<int64_t> m_pos;
+    DBuf<int64_t> m_gid;
     DBuf<unsigned long long> m_cnt(1, s);
     int64_t nm = 0;
     for (int attempt = 0; attempt < 2; ++attempt) {
         m_key.alloc(cap, s);
-        m_pos.alloc(cap, s);
+        m_gid.alloc(cap, s);
         m_cnt.zero(s);
-        GD_KERNEL_T("del_scan", 0, k_del_scan, grid_for(nrows * 32, 256, 148LL * 32), 256, 0, s, ov,
-                    row_first.get(), nrows, rq_key.get(), nrq, m_key.get(), m_pos.get(), m_cnt.get(), cap);
+        if (nwork)
+            GD_KERNEL_T("del_scan", 0, k_del_scan, grid_for(nwork * 32, 256, 148LL * 32), 256, 0, s, ov,
+                        row_first.get(), coff.get(), nrows, nwork, rq_key.get(), nrq, sh, m_key.get(), m_gid.get(),
+                        m_cnt.get(), cap);
         nm = (int64_t)read_scalar(s, m_cnt.get());
         if (nm <= cap) break;
         cap = nm;
     }
-    // order matches by (key, chain position): LSD = sort by pos, then stable by key
-    {
+    // order matches by (key, gid): LSD = sort by gid, then stable by key
+    if (nm > 1) {
         DBuf<int32_t> perm(nm, s);
         iota_i32(s, perm.get(), nm);
         DBuf<uint64_t> pk(nm, s);
-        GD_CUDA(cudaMemcpyAsync(pk.get(), m_pos.get(), nm * 8, cudaMemcpyDeviceToDevice, s));
-        sort_pairs_u64(s, pk.get(), perm.get(), nm);
+        GD_CUDA(cudaMemcpyAsync(pk.get(), m_gid.get(), nm * 8, cudaMemcpyDeviceToDevice, s));
+        sort_pairs_u64(s, pk.get(), perm.get(), nm, bits_for((uint64_t)std::max<int64_t>(total_slots(), 1)));
         DBuf<uint64_t> k2(nm, s);
-        if (nm) GD_KERNEL(k_gather<uint64_t>, grid_for(nm, 256), 256, 0, s, m_key.get(), perm.get(), nm, k2.get());
-        sort_pairs_u64(s, k2.get(), perm.get(), nm);
+        GD_KERNEL(k_gather<uint64_t>, grid_for(nm, 256), 256, 0, s, m_key.get(), perm.get(), nm, k2.get());
+        sort_pairs_u64(s, k2.get(), perm.get(), nm, kb);
         DBuf<int64_t> p2(nm, s);
-        if (nm) GD_KERNEL(k_gather<int64_t>, grid_for(nm, 256), 256, 0, s, m_pos.get(), perm.get(), nm, p2.get());
+        GD_KERNEL(k_gather<int64_t>, grid_for(nm, 256), 256, 0, s, m_gid.get(), perm.get(), nm, p2.get());
         m_key = std::move(k2);
-        m_pos = std::move(p2);
+        m_gid = std::move(p2);
     }
     DBuf<int64_t> rq_pos(nrq, s);
     DBuf<uint8_t> found_local;
@@ -844,16 +923,16 @@ int64_t Store::apply_deletes(const int32_t* d_src, const int32_t* d_dst, int64_t
     }
     GD_CUDA(cudaMemsetAsync(found, 0, k, s));
     GD_KERNEL(k_del_resolve, grid_for(nrq, 256), 256, 0, s, rq_key.get(), rq_occ.get(), rq_rec.get(),
-              rq_which.get(), nrq, m_key.get(), m_pos.get(), nm, rq_pos.get(), found);
+              rq_which.get(), nrq, m_key.get(), m_gid.get(), nm, rq_pos.get(), found);
     KilledArcs ka;
     ka.row.alloc(nrq, s);
     ka.col.alloc(nrq, s);
     ka.w.alloc(nrq, s);
-    DBuf<int64_t> kpos(nrq, s);
+    DBuf<int64_t> kgid(nrq, s);
     DBuf<unsigned long long> kcnt(1, s);
     kcnt.zero(s);
     GD_KERNEL(k_del_kill, grid_for(nrq, 256), 256, 0, s, ov, rq_key.get(), rq_rec.get(), rq_which.get(),
-              rq_pos.get(), nrq, found, ka.row.get(), ka.col.get(), ka.w.get(), kpos.get(), kcnt.get());
+              rq_pos.get(), nrq, found, sh, ka.row.get(), ka.col.get(), ka.w.get(), kgid.get(), kcnt.get());
     ka.count = (int64_t)read_scalar(s, kcnt.get());
     live -= ka.count;
     // applied = records whose forward arc was found
@@ -862,17 +941,17 @@ int64_t Store::apply_deletes(const int32_t* d_src, const int32_t* d_dst, int64_t
         DBuf<int32_t> tmp(k, s);
         applied = select_flagged_index(s, found, k, tmp.get());
     }
-    // base-segment tombstones -> merge log
+    // base-segment tombstones (gid < base slots; gid == slot there) -> merge log
     if (ka.count) {
         DBuf<uint8_t> bf(ka.count, s);
-        GD_KERNEL(k_select_base_kills, grid_for(ka.count, 256), 256, 0, s, kpos.get(), ka.row.get(), ka.count,
+        GD_KERNEL(k_select_base_kills, grid_for(ka.count, 256), 256, 0, s, kgid.get(), ka.count, segs[0].nslots,
                   bf.get());
         DBuf<int32_t> sel(ka.count, s);
         int64_t nb = select_flagged_index(s, bf.get(), ka.count, sel.get());
         if (nb) {
             DBuf<int64_t> bp(nb, s);
             DBuf<int32_t> br(nb, s);
-            GD_KERNEL(k_gather_sel<int64_t>, grid_for(nb, 256), 256, 0, s, kpos.get(), sel.get(), nb, bp.get());
+            GD_KERNEL(k_gather_sel<int64_t>, grid_for(nb, 256), 256, 0, s, kgid.get(), sel.get(), nb, bp.get());
             GD_KERNEL(k_gather_sel<int32_t>, grid_for(nb, 256), 256, 0, s, ka.row.get(), sel.get(), nb, br.get());
             append_out_tombs(bp.get(), br.get(), nb);
         }
@@ -915,7 +994,7 @@ void Store::apply_adds(const int32_t* d_src, const int32_t* d_dst, const int32_t
     aa.count = na;
     GD_KERNEL(k_add_arcs, grid_for(k, 256), 256, 0, s, d_src, d_dst, d_w, k, directed, key.get(), val.get(),
               aa.row.get(), aa.col.get(), aa.w.get());
-    sort_pairs_u32(s, key.get(), val.get(), na);  // stable: stream order within a source
+    sort_pairs_u32(s, key.get(), val.get(), na, sh);  // stable: stream order within a source
     DBuf<uint8_t> rflag(na, s);
     GD_KERNEL(k_row_starts_u32, grid_for(na, 256), 256, 0, s, key.get(), na, rflag.get());
     DBuf<int32_t> row_first(na, s);
@@ -926,8 +1005,8 @@ void Store::apply_adds(const int32_t* d_src, const int32_t* d_dst, const int32_t
     GD_KERNEL_T("add_vacancies", 0, k_add_vacancies, grid_for(nrows * 32, 256, 148LL * 32), 256, 0, s, ov,
                 key.get(), row_first.get(), nrows, na, vac.get());
     DBuf<uint8_t> left(na, s);
-    GD_KERNEL(k_add_claim, grid_for(na, 256), 256, 0, s, ov, val.get(), aa.row.get(), aa.col.get(), aa.w.get(),
-              vac.get(), na, left.get());
+    GD_KERNEL(k_add_claim, grid_for(na, 256), 256, 0, s, ov, val.get(), aa.col.get(), aa.w.get(), vac.get(), na,
+              left.get());
     drop_claimed_tombs();
     // leftovers (already ordered by (source, stream order)) -> one new delta
     DBuf<int32_t> sel(na, s);
@@ -977,7 +1056,7 @@ void Store::merge() {
         GD_CUDA(cudaMemcpyAsync(rk.get(), irow.get(), nins * 4, cudaMemcpyDeviceToDevice, s));
         DBuf<int32_t> perm(nins, s);
         iota_i32(s, perm.get(), nins);
-        sort_pairs_u32(s, rk.get(), perm.get(), nins);
+        sort_pairs_u32(s, rk.get(), perm.get(), nins, sh);
         DBuf<int32_t> r2(nins, s), c2(nins, s), w2(weighted ? nins : 0, s);
         GD_KERNEL(k_gather_sel<int32_t>, grid_for(nins, 256), 256, 0, s, irow.get(), perm.get(), nins, r2.get());
         GD_KERNEL(k_gather_sel<int32_t>, grid_for(nins, 256), 256, 0, s, icol.get(), perm.get(), nins, c2.get());

@@ -38,6 +38,7 @@ struct OutView {
     const int64_t* const* off;  // device table of nseg pointers
     const int32_t* const* col;
     const int32_t* const* w;  // entries are nullptr when unweighted
+    const int64_t* base;      // global slot id of each segment's slot 0
 };
 
 struct IdxView {  // a clean-or-tombstoned sorted index (no delta)
@@ -108,6 +109,7 @@ class Store {
     int device;
     cudaStream_t stream = nullptr;
     int64_t n;
+    int sh = 1;  // pair keys: row << sh | col
     bool directed, weighted, with_reverse;
     int64_t merge_interval;
     int64_t live = 0;
@@ -119,8 +121,10 @@ class Store {
     int64_t notomb = 0;
 
   private:
-    DBuf<const int64_t*> tab_off;
-    DBuf<const int32_t*> tab_col, tab_w;
+    // segment table on the device: [off ptrs | col ptrs | w ptrs | bases]
+    DBuf<uintptr_t> tab;
+    std::vector<uintptr_t> h_tab;
+    size_t tab_k = 0;
     void upload_tables();
     void build_index(SortedIndex& ix, bool rows_are_dst);
     void index_delete(SortedIndex& ix, const KilledArcs& ka);

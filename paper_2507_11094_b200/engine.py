@@ -184,7 +184,7 @@ class _Algo:
     def kernel_time(self, name: str):
         ms, n, b = C.c_double(), C.c_int64(), C.c_int64()
         N.check(N.lib().gd_kernel_time(self.h, name.encode(), C.byref(ms), C.byref(n), C.byref(b)))
-        return ms.value, n.value
+        return ms.value, n.value, b.value
 
     def __del__(self):
         h = getattr(self, "h", None)
