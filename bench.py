@@ -78,45 +78,65 @@ def make_inputs(wl, batches, seed=22):
 
 
 class Clocks:
-    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+    """nvidia-smi sampling around the timed region (B200_PROFILING.md clocks
+    line); samples are time-stamped and filtered to the timed window."""
 
-    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+    Q = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
 
     def __init__(self, device):
         self.device = device
         self.p = None
+        self.window = None
 
     def start(self):
         try:
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
-                                       "--format=csv,noheader,nounits", "-lms", "100"], stdout=subprocess.PIPE,
+                                       "--format=csv,noheader,nounits", "-lms", "20"], stdout=subprocess.PIPE,
                                       stderr=subprocess.DEVNULL, text=True)
+            time.sleep(0.5)  # let the sampler come up before the timed region
         except OSError:
             self.p = None
+
+    def mark(self, t0, t1):
+        self.window = (t0, t1)
 
     def stop(self):
         if self.p is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.1)
         self.p.terminate()
         out, _ = self.p.communicate(timeout=10)
-        sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        import datetime
+
+        rows = []
         for line in out.strip().splitlines():
             f = [x.strip() for x in line.split(",")]
-            if len(f) < 8:
+            if len(f) < 9:
                 continue
             try:
-                sm.append(float(f[0]))
-                mx = float(f[1])
+                ts = datetime.datetime.strptime(f[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                rows.append((ts, float(f[1]), float(f[2]), f[5:9]))
             except ValueError:
                 continue
-            for nm, v in zip(names, f[4:8]):
+        t0, t1 = self.window or (0, float("inf"))
+        inside = [r for r in rows if t0 - 0.02 <= r[0] <= t1 + 0.02]
+        note = None
+        if not inside:  # region shorter than the sampling period: nearest samples
+            inside = sorted(rows, key=lambda r: abs(r[0] - (t0 + t1) / 2))[:3]
+            note = "timed region shorter than the sampling period; nearest samples"
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in inside:
+            for nm, v in zip(names, r[3]):
                 if v.lower().startswith("active"):
                     reasons.add(nm)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        d = {"sm_mhz": statistics.median([r[1] for r in inside]) if inside else None,
+             "sm_max_mhz": inside[0][2] if inside else None, "reasons": sorted(reasons), "samples": len(inside)}
+        if note:
+            d["note"] = note
+        return d
 
 
 def load_peaks():
@@ -241,10 +261,11 @@ def main():
     algo.set_profiling(True)
     kstats = {}
     clocks = Clocks(local)
+    clocks.start()
     if dist_on:
         torch.distributed.barrier()
     torch.cuda.synchronize()
-    clocks.start()
+    wall0 = time.time()
     launches0 = gd._native.lib().gd_kernel_launches()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
@@ -262,6 +283,7 @@ def main():
     ev1.record(stream)
     torch.cuda.synchronize()
     launches = gd._native.lib().gd_kernel_launches() - launches0
+    clocks.mark(wall0, time.time())
     clk = clocks.stop()
     elapsed_ms = ev0.elapsed_time(ev1)
     if dist_on:
@@ -356,7 +378,7 @@ def main():
     return 0
 
 
-KERNELS = ("pr_pull", "pr_pull_heavy", "pr_contrib", "merge_copy", "flood_hook", "flood_mark", "del_scan",
+KERNELS = ("pr_pull", "pr_contrib", "merge_copy", "flood_sample", "flood_rest", "flood_mark", "del_scan",
            "add_vacancies", "tc_count", "sssp_relax", "sssp_walk", "sssp_pull", "sssp_parent")
 
 def _graph_stream(g):

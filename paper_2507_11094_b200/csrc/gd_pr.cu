@@ -17,8 +17,6 @@ namespace gdb {
 namespace {
 
 constexpr int kPullThreads = 256;
-constexpr int kGroup = 8;          // lanes per light vertex
-constexpr int kHeavyDeg = 8 * 64;  // rows longer than this go to the block kernel
 constexpr int kRedBlocks = 148 * 4;
 
 __global__ void k_pr_init(double* rank, int64_t n, double v) {
@@ -66,37 +64,62 @@ __device__ inline double atomic_max_pos(double* a, double v) {  // v >= 0
     return __longlong_as_double(atomicMax(reinterpret_cast<long long*>(a), __double_as_longlong(v)));
 }
 
-// Light rows: a group of kGroup lanes per affected vertex pulls
-// sum(contrib[src]) over the in-arcs, then computes the new rank and |delta|
-// (pr_dynamic_omp.cc:75-98).
-__global__ void __launch_bounds__(kPullThreads) k_pr_pull_light(const int32_t* list, int64_t m, IdxView ix,
+// The pull for one affected vertex v (pr_dynamic_omp.cc:75-98):
+// incoming = sum(contrib[src]) over the in-arcs, new rank, |delta|.  Three
+// kernels by in-degree bin so lanes stay busy on a skewed (R-MAT) graph:
+// light rows (<= 32 in-arcs) get 8 lanes, medium rows (<= 4096) a warp, hub
+// rows a 512-thread block.  Every lane keeps 4 loads in flight (column ids
+// first, then the contrib gathers) to cover L2 latency.  Reductions are in a
+// fixed order, so results are deterministic run to run.
+constexpr int kLightMax = 32;
+constexpr int kMediumMax = 4096;
+constexpr int kHubThreads = 512;
+constexpr int kILP = 4;
+
+template <int G>
+__device__ inline double row_sum(const int32_t* __restrict__ col, int64_t a, int64_t b, int lane,
+                                 const double* __restrict__ contrib) {
+    double acc = 0.0;
+    for (int64_t e0 = a + lane; e0 < b; e0 += G * kILP) {
+        int32_t u[kILP];
+#pragma unroll
+        for (int q = 0; q < kILP; ++q) {
+            int64_t e = e0 + q * G;
+            u[q] = e < b ? __ldcs(&col[e]) : -1;  // streamed once per sweep
+        }
+        double c[kILP];
+#pragma unroll
+        for (int q = 0; q < kILP; ++q) c[q] = u[q] >= 0 ? __ldg(&contrib[u[q]]) : 0.0;
+#pragma unroll
+        for (int q = 0; q < kILP; ++q) acc += c[q];
+    }
+    return acc;
+}
+
+template <int G>
+__global__ void __launch_bounds__(kPullThreads) k_pr_pull_group(const int32_t* list, int64_t m, IdxView ix,
                                                                   const double* contrib, const double* rank,
                                                                   const double* dangling, double base,
                                                                   double damping, double inv_n, double* rank_new,
                                                                   double* diff) {
-    const int lane = threadIdx.x & (kGroup - 1);
-    const int gw = (threadIdx.x & 31) / kGroup;  // group within the warp
-    constexpr int kPerWarp = 32 / kGroup;
+    const int lane = threadIdx.x & (G - 1);
+    const int gw = (threadIdx.x & 31) / G;
+    constexpr int kPer = 32 / G;
     int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const double dn = *dangling * inv_n;
     double dmax = 0.0;
-    for (int64_t t0 = warp * kPerWarp; t0 < m; t0 += nwarps * kPerWarp) {  // warp-uniform trip count
+    for (int64_t t0 = warp * kPer; t0 < m; t0 += nwarps * kPer) {  // warp-uniform trip count
         int64_t t = t0 + gw;
         bool valid = t < m;
         int32_t v = valid ? list[t] : 0;
         int64_t a = valid ? ix.off[v] : 0, b = valid ? ix.off[v + 1] : 0;
-        double acc = 0.0;
-        for (int64_t e = a + lane; e < b; e += kGroup) {
-            int32_t u = ix.col[e];
-            if (u >= 0) acc += __ldg(&contrib[u]);
-        }
+        double acc = row_sum<G>(ix.col, a, b, lane, contrib);
 #pragma unroll
-        for (int o = kGroup / 2; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o, kGroup);
+        for (int o = G / 2; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o, G);
         if (valid && lane == 0) {
             double nr = base + damping * (acc + dn);
-            double dl = fabs(nr - rank[v]);
-            dmax = fmax(dmax, dl);
+            dmax = fmax(dmax, fabs(nr - rank[v]));
             rank_new[v] = nr;
         }
     }
@@ -104,29 +127,22 @@ __global__ void __launch_bounds__(kPullThreads) k_pr_pull_light(const int32_t* l
     if ((threadIdx.x & 31) == 0 && dmax > 0.0) atomic_max_pos(diff, dmax);
 }
 
-// Heavy rows: one block per vertex.
-__global__ void __launch_bounds__(kPullThreads) k_pr_pull_heavy(const int32_t* list, int64_t m, IdxView ix,
-                                                                  const double* contrib, const double* rank,
-                                                                  const double* dangling, double base,
-                                                                  double damping, double inv_n, double* rank_new,
-                                                                  double* diff) {
-    __shared__ double sh[kPullThreads / 32];
+__global__ void __launch_bounds__(kHubThreads) k_pr_pull_hub(const int32_t* list, int64_t m, IdxView ix,
+                                                              const double* contrib, const double* rank,
+                                                              const double* dangling, double base, double damping,
+                                                              double inv_n, double* rank_new, double* diff) {
+    __shared__ double sh[kHubThreads / 32];
     const double dn = *dangling * inv_n;
     for (int64_t t = blockIdx.x; t < m; t += gridDim.x) {
         int32_t v = list[t];
-        int64_t a = ix.off[v], b = ix.off[v + 1];
-        double acc = 0.0;
-        for (int64_t e = a + threadIdx.x; e < b; e += blockDim.x) {
-            int32_t u = ix.col[e];
-            if (u >= 0) acc += __ldg(&contrib[u]);
-        }
+        double acc = row_sum<kHubThreads>(ix.col, ix.off[v], ix.off[v + 1], threadIdx.x, contrib);
         for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
         if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
         __syncthreads();
         if (threadIdx.x == 0) {
-            double s = 0.0;
-            for (int w = 0; w < kPullThreads / 32; ++w) s += sh[w];
-            double nr = base + damping * (s + dn);
+            double sum = 0.0;
+            for (int w = 0; w < kHubThreads / 32; ++w) sum += sh[w];
+            double nr = base + damping * (sum + dn);
             double dl = fabs(nr - rank[v]);
             if (dl > 0.0) atomic_max_pos(diff, dl);
             rank_new[v] = nr;
@@ -153,19 +169,18 @@ __global__ void k_pr_onupdate(const int32_t* s, const int32_t* d, int64_t k, int
     }
 }
 
-__global__ void k_heavy_flags(const int32_t* list, int64_t m, const int64_t* off, uint8_t* heavy, uint8_t* light) {
+// in-arcs of each bin (for the roofline's algorithmic bytes)
+__global__ void k_bin_arcs(const int32_t* list, int64_t m, const int64_t* off, unsigned long long* sums) {
+    unsigned long long a[3] = {0, 0, 0};
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
         int32_t v = list[i];
-        bool h = (off[v + 1] - off[v]) > kHeavyDeg;
-        heavy[i] = h;
-        light[i] = !h;
+        int64_t d = off[v + 1] - off[v];
+        a[d <= kLightMax ? 0 : (d <= kMediumMax ? 1 : 2)] += (unsigned long long)d;
     }
-}
-
-__global__ void k_list_degrees(const int32_t* list, int64_t m, const int64_t* off, int64_t* deg) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
-        int32_t v = list[i];
-        deg[i] = off[v + 1] - off[v];
+    for (int k = 0; k < 3; ++k) {
+        unsigned long long x = a[k];
+        for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+        if ((threadIdx.x & 31) == 0 && x) atomicAdd(&sums[k], x);
     }
 }
 
@@ -206,28 +221,25 @@ PR::PR(Store* st, double d, double b, int64_t mi) : AlgoBase(ALGO_PR, st), dampi
 void PR::set_lists(const int32_t* list, int64_t m) {
     cudaStream_t s = stream();
     g->compact_rev();
-    light.alloc(m, s);
-    heavy.alloc(m, s);
-    nlight = nheavy = 0;
+    for (auto* l : {&bins[0], &bins[1], &bins[2]}) l->ensure(std::max<int64_t>(m, 1), s);
+    nbin[0] = nbin[1] = nbin[2] = 0;
+    ebin[0] = ebin[1] = ebin[2] = 0;
     if (!m) return;
-    DBuf<uint8_t> hf(m, s), lf(m, s);
-    GD_KERNEL(k_heavy_flags, grid_for(m, 256), 256, 0, s, list, m, g->rev.off.get(), hf.get(), lf.get());
-    DBuf<int32_t> sel(m, s);
-    nheavy = select_flagged_index(s, hf.get(), m, sel.get());
-    if (nheavy) GD_KERNEL(k_gather_list, grid_for(nheavy, 256), 256, 0, s, list, sel.get(), nheavy, heavy.get());
-    nlight = select_flagged_index(s, lf.get(), m, sel.get());
-    if (nlight) GD_KERNEL(k_gather_list, grid_for(nlight, 256), 256, 0, s, list, sel.get(), nlight, light.get());
-    // in-arcs the pull reads (for the roofline's algorithmic bytes)
-    DBuf<int64_t> deg(std::max<int64_t>(nlight, nheavy), s);
-    ein_light = ein_heavy = 0;
-    if (nlight) {
-        GD_KERNEL(k_list_degrees, grid_for(nlight, 256), 256, 0, s, light.get(), nlight, g->rev.off.get(), deg.get());
-        ein_light = sum_i64(s, deg.get(), nlight);
-    }
-    if (nheavy) {
-        GD_KERNEL(k_list_degrees, grid_for(nheavy, 256), 256, 0, s, heavy.get(), nheavy, g->rev.off.get(), deg.get());
-        ein_heavy = sum_i64(s, deg.get(), nheavy);
-    }
+    DBuf<int> cnt(2, s);
+    DBuf<unsigned long long> sums(3, s);
+    sums.zero(s);
+    partition3_by_degree(s, list, m, g->rev.off.get(), kLightMax, kMediumMax, bins[0].get(), bins[1].get(),
+                         bins[2].get(), cnt.get());
+    GD_KERNEL(k_bin_arcs, grid_for(m, 256, 148LL * 8), 256, 0, s, list, m, g->rev.off.get(), sums.get());
+    int hc[2];
+    unsigned long long hs[3];
+    GD_CUDA(cudaMemcpyAsync(hc, cnt.get(), sizeof hc, cudaMemcpyDeviceToHost, s));
+    GD_CUDA(cudaMemcpyAsync(hs, sums.get(), sizeof hs, cudaMemcpyDeviceToHost, s));
+    GD_CUDA(cudaStreamSynchronize(s));
+    nbin[0] = hc[0];
+    nbin[1] = hc[1];
+    nbin[2] = m - hc[0] - hc[1];
+    for (int k = 0; k < 3; ++k) ebin[k] = (int64_t)hs[k];
 }
 
 // while (diff >= beta && iter < maxiter) { dangling; pull; commit }
@@ -246,18 +258,26 @@ void PR::power_loop() {
                     contrib.get(), partial.get());
         GD_KERNEL(k_sum_partials, 1, 1024, 0, s, partial.get(), kRedBlocks, scal.get());
         GD_CUDA(cudaMemsetAsync(scal.get() + 1, 0, sizeof(double), s));
-        if (nlight) {
-            int64_t groups = nlight;
-            unsigned grid = grid_for(groups * kGroup, kPullThreads, 148LL * 32);
-            GD_KERNEL_T("pr_pull", nlight * 24 + ein_light * 12, k_pr_pull_light, grid, kPullThreads, 0, s, light.get(), nlight, ix,
-                        contrib.get(), rank.get(), scal.get(), base, damping, inv_n, rank_new.get(), scal.get() + 1);
-        }
-        if (nheavy)
-            GD_KERNEL_T("pr_pull_heavy", nheavy * 24 + ein_heavy * 12, k_pr_pull_heavy, (unsigned)std::min<int64_t>(nheavy, 148LL * 8),
-                        kPullThreads, 0, s, heavy.get(), nheavy, ix, contrib.get(), rank.get(), scal.get(), base,
-                        damping, inv_n, rank_new.get(), scal.get() + 1);
-        if (nlight) GD_KERNEL(k_pr_commit, grid_for(nlight, 256), 256, 0, s, light.get(), nlight, rank_new.get(), rank.get());
-        if (nheavy) GD_KERNEL(k_pr_commit, grid_for(nheavy, 256), 256, 0, s, heavy.get(), nheavy, rank_new.get(), rank.get());
+        // algorithmic bytes: |A| (off + 2 f64) + E_in(A) (idx + f64)
+        if (nbin[0])
+            GD_KERNEL_T("pr_pull", nbin[0] * 24 + ebin[0] * 12, k_pr_pull_group<8>,
+                        grid_for(((nbin[0] + 3) / 4) * 32, kPullThreads, 148LL * 32), kPullThreads, 0, s,
+                        bins[0].get(), nbin[0], ix, contrib.get(), rank.get(), scal.get(), base, damping, inv_n,
+                        rank_new.get(), scal.get() + 1);
+        if (nbin[1])
+            GD_KERNEL_T("pr_pull", nbin[1] * 24 + ebin[1] * 12, k_pr_pull_group<32>,
+                        grid_for(nbin[1] * 32, kPullThreads, 148LL * 32), kPullThreads, 0, s, bins[1].get(),
+                        nbin[1], ix, contrib.get(), rank.get(), scal.get(), base, damping, inv_n, rank_new.get(),
+                        scal.get() + 1);
+        if (nbin[2])
+            GD_KERNEL_T("pr_pull", nbin[2] * 24 + ebin[2] * 12, k_pr_pull_hub,
+                        (unsigned)std::min<int64_t>(nbin[2], 148LL * 4), kHubThreads, 0, s, bins[2].get(), nbin[2],
+                        ix, contrib.get(), rank.get(), scal.get(), base, damping, inv_n, rank_new.get(),
+                        scal.get() + 1);
+        for (int k = 0; k < 3; ++k)
+            if (nbin[k])
+                GD_KERNEL(k_pr_commit, grid_for(nbin[k], 256), 256, 0, s, bins[k].get(), nbin[k], rank_new.get(),
+                          rank.get());
         diff = read_scalar(s, scal.get() + 1);
         ++iter;
     }

@@ -11,9 +11,9 @@ struct PR : AlgoBase {
     DBuf<double> rank, rank_new, contrib, partial, scal;
     DBuf<int32_t> outdeg;  // maintained per record (misses included), int32 on device
     DBuf<uint8_t> affected;
-    DBuf<int32_t> light, heavy;
-    int64_t nlight = 0, nheavy = 0;
-    int64_t ein_light = 0, ein_heavy = 0;  // in-arcs of the light / heavy lists
+    DBuf<int32_t> bins[3];            // affected vertices by in-degree: light / medium / hub
+    int64_t nbin[3] = {0, 0, 0};
+    int64_t ebin[3] = {0, 0, 0};      // in-arcs per bin (roofline bytes)
     int64_t last_sweeps = 0, last_affected = 0;
 
     PR(Store* st, double damping, double beta, int64_t maxiter);  // = staticPR

@@ -104,6 +104,28 @@ int64_t select_flagged_index(cudaStream_t s, const uint8_t* flags, int64_t n, in
     return read_scalar(s, cnt.get());
 }
 
+namespace {
+struct DegAtMost {
+    const int64_t* off;
+    int64_t t;
+    __device__ bool operator()(const int32_t& v) const { return off[v + 1] - off[v] <= t; }
+};
+}  // namespace
+
+void partition3_by_degree(cudaStream_t s, const int32_t* list, int64_t m, const int64_t* off, int64_t t1,
+                          int64_t t2, int32_t* out1, int32_t* out2, int32_t* out3, int* d_counts) {
+    if (m <= 0) {
+        GD_CUDA(cudaMemsetAsync(d_counts, 0, 2 * sizeof(int), s));
+        return;
+    }
+    size_t bytes = 0;
+    DegAtMost a{off, t1}, b{off, t2};
+    GD_CUDA(cub::DevicePartition::If(nullptr, bytes, list, out1, out2, out3, d_counts, (int)m, a, b, s));
+    Temp t(bytes, s);
+    GD_CUDA(cub::DevicePartition::If(t.p, bytes, list, out1, out2, out3, d_counts, (int)m, a, b, s));
+    count_library_launch();
+}
+
 __global__ void k_iota_i32(int32_t* a, int64_t n) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         a[i] = static_cast<int32_t>(i);

@@ -149,24 +149,120 @@ __global__ void k_row_starts_u32(const uint32_t* key, int64_t m, uint8_t* flag) 
         flag[i] = (i == 0 || key[i] != key[i - 1]) ? 1 : 0;
 }
 
-// number of kChunk work items of every requested row (its whole chain)
+// Rows are scanned in two parts: the first kHead chain slots of every
+// requested row by an 8-lane group (k_del_scan_head: one group per row, no
+// work-item search), and the rest of long rows in kChunk pieces, one warp
+// each (k_del_scan_tail).  chunks[i] = tail work items of row i; the longest
+// chain length sizes the chain-offset field of the match sort key.
+constexpr int kHead = 256;
+constexpr int kScanWarps = 8;
+constexpr int kBitmapWords = 1024;  // 32 Kbit per warp
+
 __global__ void k_row_chunks(OutView ov, const uint64_t* rq_key, const int32_t* row_first, int64_t nrows, int sh,
-                             int64_t* chunks) {
+                             int64_t* chunks, unsigned long long* maxlen) {
+    unsigned long long mx = 0;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nrows; i += (int64_t)gridDim.x * blockDim.x) {
         int32_t row = key_row(rq_key[row_first[i]], sh);
         int64_t len = 0;
         for (int sg = 0; sg < ov.nseg; ++sg) len += ov.off[sg][row + 1] - ov.off[sg][row];
-        chunks[i] = len > 0 ? (len + kChunk - 1) / kChunk : 0;
+        chunks[i] = len > kHead ? (len - kHead + kChunk - 1) / kChunk : 0;
+        mx = max(mx, (unsigned long long)len);
+    }
+    for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0 && mx) atomicMax(maxlen, mx);
+}
+
+__global__ void k_widen(const int32_t* a, int64_t m, uint64_t* o) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+        o[i] = (uint64_t)(uint32_t)a[i];
+}
+
+// Matches go out as (sort key, gid) with sort key = pair key << rb | chain
+// offset of the slot within its row, so ONE radix sort orders them by (pair,
+// chain order): the j-th match of a pair is the pair's j-th live occurrence.
+struct MatchOut {
+    uint64_t* key;
+    int32_t* gid;
+    unsigned long long* cnt;
+    int64_t cap;
+    int rb;
+};
+
+__device__ inline void emit_matches(const MatchOut& mo, bool hit, int32_t row, int32_t c, int sh, int64_t chain,
+                                    int64_t gid) {
+    unsigned mask = __ballot_sync(0xffffffffu, hit);
+    if (!mask) return;
+    const int lane = threadIdx.x & 31;
+    unsigned long long basei = 0;
+    if (lane == 0) basei = atomicAdd(mo.cnt, (unsigned long long)__popc(mask));
+    basei = __shfl_sync(0xffffffffu, basei, 0);
+    if (hit) {
+        int64_t slot = (int64_t)basei + __popc(mask & ((1u << lane) - 1));
+        if (slot < mo.cap) {
+            mo.key[slot] = (pair_key(row, c, sh) << mo.rb) | (uint64_t)chain;
+            mo.gid[slot] = (int32_t)gid;
+        }
     }
 }
 
-// One warp per work item (row, 1024-slot chunk of its chain): every live slot
-// whose column is requested for that row is emitted as a match (key, gid).
-__global__ void __launch_bounds__(256) k_del_scan(OutView ov, const int32_t* row_first, const int64_t* coff,
-                                                  int64_t nrows, int64_t nwork, const uint64_t* rq_key, int64_t nrq,
-                                                  int sh, uint64_t* m_key, int64_t* m_gid, unsigned long long* m_cnt,
-                                                  int64_t cap) {
+__device__ inline bool requested(const uint64_t* rq_key, int64_t lo, int64_t hi, int32_t row, int32_t c, int sh,
+                                 int32_t c0, int32_t c1, const uint32_t* bm) {
+    if (hi - lo <= 2) return c == c0 || c == c1;
+    if (bm) {
+        uint32_t h = (uint32_t)c & (kBitmapWords * 32 - 1);
+        if (!(bm[h >> 5] & (1u << (h & 31)))) return false;
+    }
+    uint64_t want = pair_key(row, c, sh);
+    int64_t p = lower_bound_dev<uint64_t>(rq_key, lo, hi, want);
+    return p < hi && rq_key[p] == want;
+}
+
+// head: one 8-lane group per requested row, chain slots [0, kHead)
+__global__ void __launch_bounds__(256) k_del_scan_head(OutView ov, const int32_t* row_first, int64_t nrows,
+                                                       const uint64_t* rq_key, int64_t nrq, int sh, MatchOut mo) {
+    constexpr int G = 8, kPer = 32 / G;
+    const int gl = threadIdx.x & (G - 1), gw = (threadIdx.x & 31) / G;
+    int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t t0 = warp * kPer; t0 < nrows; t0 += nwarps * kPer) {
+        int64_t i = t0 + gw;
+        bool valid = i < nrows;
+        int64_t lo = valid ? row_first[i] : 0;
+        int64_t hi = valid ? ((i + 1 < nrows) ? row_first[i + 1] : nrq) : 0;
+        int32_t row = valid ? key_row(rq_key[lo], sh) : 0;
+        int32_t c0 = valid ? key_col(rq_key[lo], sh) : -2;
+        int32_t c1 = (valid && hi - lo > 1) ? key_col(rq_key[lo + 1], sh) : -2;
+        int64_t acc = 0;
+        for (int sg = 0; sg < ov.nseg; ++sg) {  // nseg is uniform: the loop stays warp-uniform
+            int64_t a = valid ? ov.off[sg][row] : 0;
+            int64_t L = valid ? ov.off[sg][row + 1] - a : 0;
+            int64_t len = max(min(acc + L, (int64_t)kHead) - acc, (int64_t)0);
+            int64_t wlen = len;
+            for (int o = G; o < 32; o <<= 1) wlen = max(wlen, (int64_t)__shfl_xor_sync(0xffffffffu, wlen, o));
+            const int32_t* col = ov.col[sg];
+            for (int64_t x0 = 0; x0 < wlen; x0 += G) {
+                int64_t x = x0 + gl;
+                bool hit = false;
+                int32_t c = -1;
+                if (x < len) {
+                    c = col[a + x];
+                    if (c >= 0) hit = requested(rq_key, lo, hi, row, c, sh, c0, c1, nullptr);
+                }
+                emit_matches(mo, hit, row, c, sh, acc + x, ov.base[sg] + a + x);
+            }
+            acc += L;
+        }
+    }
+}
+
+// tail: one warp per kChunk piece of a long row beyond its head
+__global__ void __launch_bounds__(kScanWarps * 32) k_del_scan_tail(OutView ov, const int32_t* row_first,
+                                                                   const int64_t* coff, int64_t nrows, int64_t nwork,
+                                                                   const uint64_t* rq_key, int64_t nrq, int sh,
+                                                                   MatchOut mo) {
+    __shared__ uint32_t bitmap[kScanWarps][kBitmapWords];
     const int lane = threadIdx.x & 31;
+    uint32_t* bm = bitmap[threadIdx.x >> 5];
     int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t wk = warp; wk < nwork; wk += nwarps) {
@@ -178,8 +274,18 @@ __global__ void __launch_bounds__(256) k_del_scan(OutView ov, const int32_t* row
         int64_t ncols = hi - lo;
         int32_t c0 = key_col(rq_key[lo], sh);
         int32_t c1 = ncols > 1 ? key_col(rq_key[lo + 1], sh) : -2;
-        int64_t p0 = chunk * kChunk, p1 = p0 + kChunk;
-        int64_t acc = 0;  // chain offset of the current segment's part of the row
+        bool use_bm = ncols > 2;
+        if (use_bm) {
+            for (int q = lane; q < kBitmapWords; q += 32) bm[q] = 0;
+            __syncwarp();
+            for (int64_t e = lo + lane; e < hi; e += 32) {
+                uint32_t c = (uint32_t)key_col(rq_key[e], sh) & (kBitmapWords * 32 - 1);
+                atomicOr(&bm[c >> 5], 1u << (c & 31));
+            }
+            __syncwarp();
+        }
+        int64_t p0 = kHead + chunk * kChunk, p1 = p0 + kChunk;
+        int64_t acc = 0;
         for (int sg = 0; sg < ov.nseg && acc < p1; ++sg) {
             const int64_t* off = ov.off[sg];
             const int32_t* col = ov.col[sg];
@@ -192,45 +298,26 @@ __global__ void __launch_bounds__(256) k_del_scan(OutView ov, const int32_t* row
                 int64_t idx = a + (x - acc);
                 if (x < s1) {
                     c = col[idx];
-                    if (c >= 0) {
-                        if (ncols <= 2) {
-                            hit = (c == c0) || (c == c1);
-                        } else {
-                            uint64_t want = pair_key(row, c, sh);
-                            int64_t p = lower_bound_dev<uint64_t>(rq_key, lo, hi, want);
-                            hit = (p < hi && rq_key[p] == want);
-                        }
-                    }
+                    if (c >= 0) hit = requested(rq_key, lo, hi, row, c, sh, c0, c1, use_bm ? bm : nullptr);
                 }
-                unsigned mask = __ballot_sync(0xffffffffu, hit);
-                if (mask) {
-                    unsigned long long basei = 0;
-                    if (lane == 0) basei = atomicAdd(m_cnt, (unsigned long long)__popc(mask));
-                    basei = __shfl_sync(0xffffffffu, basei, 0);
-                    if (hit) {
-                        int64_t slot = (int64_t)basei + __popc(mask & ((1u << lane) - 1));
-                        if (slot < cap) {
-                            m_key[slot] = pair_key(row, c, sh);
-                            m_gid[slot] = ov.base[sg] + idx;
-                        }
-                    }
-                }
+                emit_matches(mo, hit, row, c, sh, x, ov.base[sg] + idx);
             }
             acc += L;
         }
+        __syncwarp();
     }
 }
 
 // Resolve each request against the (key, gid)-sorted matches.
 __global__ void k_del_resolve(const uint64_t* rq_key, const int32_t* rq_occ, const int32_t* rq_rec,
-                              const uint8_t* rq_which, int64_t nrq, const uint64_t* m_key, const int64_t* m_gid,
-                              int64_t nm, int64_t* rq_pos, uint8_t* found_fwd) {
+                              const uint8_t* rq_which, int64_t nrq, const uint64_t* m_key, const int32_t* m_gid,
+                              int64_t nm, int rb, int64_t* rq_pos, uint8_t* found_fwd) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nrq; i += (int64_t)gridDim.x * blockDim.x) {
         uint64_t key = rq_key[i];
-        int64_t lo = lower_bound_dev<uint64_t>(m_key, 0, nm, key);
+        int64_t lo = lower_bound_dev<uint64_t>(m_key, 0, nm, key << rb);
         int64_t occ = rq_occ[i];
         int64_t pos = -1;
-        if (lo + occ < nm && m_key[lo + occ] == key) pos = m_gid[lo + occ];
+        if (lo + occ < nm && (m_key[lo + occ] >> rb) == key) pos = m_gid[lo + occ];
         rq_pos[i] = pos;
         if (rq_which[i] == 0) found_fwd[rq_rec[i]] = pos >= 0 ? 1 : 0;
     }
@@ -366,7 +453,10 @@ __global__ void k_kill_to_index(const int32_t* k_row, const int32_t* k_col, cons
 }
 
 // Items sorted by (key, w); the j-th item of an equal (key, w) run tombstones
-// the j-th live entry with that column and weight in the (clean) row.
+// the j-th live entry with that column and weight in the (clean) row.  Each
+// item writes its own slot of the tomb log (-1 when nothing matched); for
+// unweighted graphs the positions come out ascending (items and entries share
+// the (row, col) order), so no sort is needed there.
 __global__ void k_index_kill(const uint64_t* key, const int32_t* wk, int64_t m, int sh, const int64_t* off,
                              int32_t* col, const int32_t* w, int64_t* t_pos, int32_t* t_row,
                              unsigned long long* t_cnt) {
@@ -384,14 +474,19 @@ __global__ void k_index_kill(const uint64_t* key, const int32_t* wk, int64_t m, 
             if (w && w[e] != wt) continue;
             if (j == 0) {
                 col[e] = tomb(v);
-                unsigned long long o = atomicAdd(t_cnt, 1ULL);
-                t_pos[o] = e;
-                t_row[o] = r;
+                t_pos[i] = e;
+                t_row[i] = r;
+                atomicAdd(t_cnt, 1ULL);
                 break;
             }
             --j;
         }
     }
+}
+
+__global__ void k_nonneg_flags(const int64_t* a, int64_t m, uint8_t* f) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+        f[i] = a[i] >= 0 ? 1 : 0;
 }
 
 __global__ void k_added_to_index(const int32_t* a_row, const int32_t* a_col, int64_t m, bool rows_are_dst, int sh,
@@ -461,49 +556,81 @@ __global__ void k_tile_bounds(int64_t ntiles, const int64_t* tpos, int64_t ntomb
     }
 }
 
-// Base entries: newpos(i) = i - #tombs(< i) + #inserts(P <= i).  Each thread
-// owns kPerThread consecutive entries: one bounded search for its first entry,
-// then the two counters only advance at the (sparse) tomb / insert positions.
+// Base entries: newpos(i) = i - #tombs(< i) + #inserts(P <= i).  Each warp
+// owns a 256-entry window, lane-strided so every load and store instruction
+// covers 32 consecutive entries.  The window's few tomb / insert events are
+// dropped into a shared delta array (-1 after a tomb, +1 at an insert point)
+// whose warp-scanned prefix is each entry's shift -- no per-entry search.
+constexpr int kWin = kTile / (kEditThreads / 32);  // 256
+
 __global__ void __launch_bounds__(kEditThreads) k_edit_base(const int32_t* col, const int32_t* w, int64_t nnz,
                                                             const int64_t* tpos, const int64_t* ipos,
                                                             const int64_t* tb_tile, const int64_t* pj_tile,
                                                             int64_t ntiles, int32_t* ocol, int32_t* ow) {
+    __shared__ int dsh[kEditThreads / 32][kWin + 1];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int* d = dsh[wid];
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        int64_t t0 = tile * kTile;
+        int64_t ws = tile * kTile + (int64_t)wid * kWin;
+        if (ws >= nnz) continue;  // warp-uniform
+        int64_t we = min(ws + kWin, nnz);
         int64_t tb0 = tb_tile[tile], tb1 = tb_tile[tile + 1];
         int64_t pj0 = pj_tile[tile], pj1 = pj_tile[tile + 1];
-        int64_t i0 = t0 + (int64_t)threadIdx.x * kPerThread;
-        if (i0 >= nnz) continue;
-        int64_t i1 = min(i0 + kPerThread, nnz);
-        int64_t tb = (tb0 == tb1) ? tb0 : lower_bound_dev<int64_t>(tpos, tb0, tb1, i0);
-        int64_t pj = (pj0 == pj1) ? pj0 : upper_bound_dev<int64_t>(ipos, pj0, pj1, i0 - 1);
-        int32_t v[kPerThread];
-        int32_t ww[kPerThread];
-        if (i1 - i0 == kPerThread) {  // 32-byte aligned (tiles and chunks are multiples of 8)
-            const int4* c4 = reinterpret_cast<const int4*>(col + i0);
-            int4 a = c4[0], b = c4[1];
-            v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
-            if (w) {
-                const int4* w4 = reinterpret_cast<const int4*>(w + i0);
-                int4 x = w4[0], y = w4[1];
-                ww[0] = x.x; ww[1] = x.y; ww[2] = x.z; ww[3] = x.w; ww[4] = y.x; ww[5] = y.y; ww[6] = y.z; ww[7] = y.w;
+        int64_t tbw = tb0, tbe = tb0, pjw = pj0, pje = pj0;
+        if (tb0 != tb1 || pj0 != pj1) {
+            if (lane == 0) {
+                tbw = lower_bound_dev<int64_t>(tpos, tb0, tb1, ws);
+                tbe = lower_bound_dev<int64_t>(tpos, tbw, tb1, we);
+            } else if (lane == 1) {
+                pjw = upper_bound_dev<int64_t>(ipos, pj0, pj1, ws - 1);
+                pje = upper_bound_dev<int64_t>(ipos, pjw, pj1, we - 1);
             }
+            tbw = __shfl_sync(0xffffffffu, tbw, 0);
+            tbe = __shfl_sync(0xffffffffu, tbe, 0);
+            pjw = __shfl_sync(0xffffffffu, pjw, 1);
+            pje = __shfl_sync(0xffffffffu, pje, 1);
+        }
+        const bool events = (tbe > tbw) || (pje > pjw);
+        int sc[kWin / 32];
+        if (events) {
+            for (int q = lane; q <= kWin; q += 32) d[q] = 0;
+            __syncwarp();
+            for (int64_t k = tbw + lane; k < tbe; k += 32) atomicAdd(&d[tpos[k] - ws + 1], -1);
+            for (int64_t k = pjw + lane; k < pje; k += 32) atomicAdd(&d[ipos[k] - ws], 1);
+            __syncwarp();
+            int carry = 0;
+#pragma unroll
+            for (int q = 0; q < kWin / 32; ++q) {
+                int x = d[q * 32 + lane];
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    int y = __shfl_up_sync(0xffffffffu, x, o);
+                    if (lane >= o) x += y;
+                }
+                x += carry;
+                sc[q] = x;
+                carry = __shfl_sync(0xffffffffu, x, 31);
+            }
+            __syncwarp();
         } else {
-            for (int q = 0; q < kPerThread; ++q) {
-                v[q] = (i0 + q < i1) ? col[i0 + q] : -1;
-                ww[q] = (w && i0 + q < i1) ? w[i0 + q] : 0;
-            }
+#pragma unroll
+            for (int q = 0; q < kWin / 32; ++q) sc[q] = 0;
+        }
+        const int64_t shift0 = pjw - tbw;
+        int32_t v[kWin / 32];
+        int32_t wv[kWin / 32];
+#pragma unroll
+        for (int q = 0; q < kWin / 32; ++q) {
+            int64_t i = ws + q * 32 + lane;
+            v[q] = i < we ? __ldcs(&col[i]) : -1;
+            wv[q] = (w && i < we) ? __ldcs(&w[i]) : 0;
         }
 #pragma unroll
-        for (int q = 0; q < kPerThread; ++q) {
-            int64_t i = i0 + q;
-            if (i >= i1) break;
-            while (tb < tb1 && tpos[tb] < i) ++tb;
-            while (pj < pj1 && ipos[pj] <= i) ++pj;
+        for (int q = 0; q < kWin / 32; ++q) {
             if (v[q] < 0) continue;
-            int64_t np = i - tb + pj;
-            ocol[np] = v[q];
-            if (ow) ow[np] = ww[q];
+            int64_t np = ws + q * 32 + lane + shift0 + sc[q];
+            __stcs(&ocol[np], v[q]);
+            if (ow) __stcs(&ow[np], wv[q]);
         }
     }
 }
@@ -788,15 +915,36 @@ void Store::index_delete(SortedIndex& ix, const KilledArcs& ka) {
     }
     DBuf<unsigned long long> cnt(1, s);
     cnt.zero(s);
+    fill_i64(s, tpos.get() + old, m, -1);
     GD_KERNEL(k_index_kill, grid_for(m, 256), 256, 0, s, k2.get(), w2.get(), m, sh, ix.off.get(), ix.col.get(),
               ix.w.n ? ix.w.get() : nullptr, tpos.get() + old, trow.get() + old, cnt.get());
     int64_t killed = (int64_t)read_scalar(s, cnt.get());
+    if (killed < m) {  // drop the unmatched (-1) slots, order kept
+        DBuf<uint8_t> f(m, s);
+        GD_KERNEL(k_nonneg_flags, grid_for(m, 256), 256, 0, s, tpos.get() + old, m, f.get());
+        DBuf<int32_t> sel(m, s);
+        select_flagged_index(s, f.get(), m, sel.get());
+        DBuf<int64_t> p2(std::max<int64_t>(killed, 1), s);
+        DBuf<int32_t> r2(std::max<int64_t>(killed, 1), s);
+        if (killed) {
+            GD_KERNEL(k_gather_sel<int64_t>, grid_for(killed, 256), 256, 0, s, tpos.get() + old, sel.get(), killed,
+                      p2.get());
+            GD_KERNEL(k_gather_sel<int32_t>, grid_for(killed, 256), 256, 0, s, trow.get() + old, sel.get(), killed,
+                      r2.get());
+            GD_CUDA(cudaMemcpyAsync(tpos.get() + old, p2.get(), killed * 8, cudaMemcpyDeviceToDevice, s));
+            GD_CUDA(cudaMemcpyAsync(trow.get() + old, r2.get(), killed * 4, cudaMemcpyDeviceToDevice, s));
+        }
+    }
     int64_t tot = old + killed;
-    // keep the log sorted by position
-    DBuf<uint64_t> pk(tot, s);
-    GD_CUDA(cudaMemcpyAsync(pk.get(), tpos.get(), tot * 8, cudaMemcpyDeviceToDevice, s));
-    sort_pairs_u64(s, pk.get(), trow.get(), tot, bits_for((uint64_t)std::max<int64_t>(ix.nnz, 1)));
-    GD_CUDA(cudaMemcpyAsync(tpos.get(), pk.get(), tot * 8, cudaMemcpyDeviceToDevice, s));
+    // Unweighted: items and entries share the (row, col) order, so the log is
+    // already ascending.  Weighted: parallel arcs of one pair sit in the index
+    // in arrival order, not weight order -- sort.  An older log: sort the union.
+    if (killed && (old || weighted)) {
+        DBuf<uint64_t> pk(tot, s);
+        GD_CUDA(cudaMemcpyAsync(pk.get(), tpos.get(), tot * 8, cudaMemcpyDeviceToDevice, s));
+        sort_pairs_u64(s, pk.get(), trow.get(), tot, bits_for((uint64_t)std::max<int64_t>(ix.nnz, 1)));
+        GD_CUDA(cudaMemcpyAsync(tpos.get(), pk.get(), tot * 8, cudaMemcpyDeviceToDevice, s));
+    }
     ix.tpos = std::move(tpos);
     ix.trow = std::move(trow);
     ix.ntomb = tot;
@@ -876,43 +1024,58 @@ int64_t Store::apply_deletes(const int32_t* d_src, const int32_t* d_dst, int64_t
     int64_t nrows = select_flagged_index(s, rflag.get(), nrq, row_first.get());
     OutView ov = out_view();
     DBuf<int64_t> chunks(nrows + 1, s), coff(nrows + 1, s);
+    DBuf<unsigned long long> maxlen(1, s);
+    maxlen.zero(s);
     GD_KERNEL(k_row_chunks, grid_for(nrows, 256), 256, 0, s, ov, rq_key.get(), row_first.get(), nrows, sh,
-              chunks.get());
+              chunks.get(), maxlen.get());
     GD_CUDA(cudaMemsetAsync(chunks.get() + nrows, 0, 8, s));
     exclusive_scan_i64(s, chunks.get(), coff.get(), nrows + 1);
-    int64_t nwork = read_scalar(s, coff.get() + nrows);
+    int64_t hv[2];
+    GD_CUDA(cudaMemcpyAsync(&hv[0], coff.get() + nrows, 8, cudaMemcpyDeviceToHost, s));
+    GD_CUDA(cudaMemcpyAsync(&hv[1], maxlen.get(), 8, cudaMemcpyDeviceToHost, s));
+    GD_CUDA(cudaStreamSynchronize(s));
+    int64_t nwork = hv[0];
+    int rb = bits_for((uint64_t)std::max<int64_t>(hv[1], 1));
+    const bool one_sort = kb + rb <= 64;  // (pair, chain offset) fits one 64-bit key
+    if (!one_sort) rb = 0;
     // scan chains, collect matches (retry once with the exact size on overflow)
     int64_t cap = 2 * nrq + 1024;
     DBuf<uint64_t> m_key;
-    DBuf<int64_t> m_gid;
+    DBuf<int32_t> m_gid;
     DBuf<unsigned long long> m_cnt(1, s);
     int64_t nm = 0;
     for (int attempt = 0; attempt < 2; ++attempt) {
         m_key.alloc(cap, s);
         m_gid.alloc(cap, s);
         m_cnt.zero(s);
+        MatchOut mo{m_key.get(), m_gid.get(), m_cnt.get(), cap, rb};
+        GD_KERNEL_T("del_scan", 0, k_del_scan_head, grid_for(((nrows + 3) / 4) * 32, 256, 148LL * 32), 256, 0, s,
+                    ov, row_first.get(), nrows, rq_key.get(), nrq, sh, mo);
         if (nwork)
-            GD_KERNEL_T("del_scan", 0, k_del_scan, grid_for(nwork * 32, 256, 148LL * 32), 256, 0, s, ov,
-                        row_first.get(), coff.get(), nrows, nwork, rq_key.get(), nrq, sh, m_key.get(), m_gid.get(),
-                        m_cnt.get(), cap);
+            GD_KERNEL_T("del_scan", 0, k_del_scan_tail, grid_for(nwork * 32, kScanWarps * 32, 148LL * 16),
+                        kScanWarps * 32, 0, s, ov, row_first.get(), coff.get(), nrows, nwork, rq_key.get(), nrq, sh,
+                        mo);
         nm = (int64_t)read_scalar(s, m_cnt.get());
         if (nm <= cap) break;
         cap = nm;
     }
-    // order matches by (key, gid): LSD = sort by gid, then stable by key
     if (nm > 1) {
-        DBuf<int32_t> perm(nm, s);
-        iota_i32(s, perm.get(), nm);
-        DBuf<uint64_t> pk(nm, s);
-        GD_CUDA(cudaMemcpyAsync(pk.get(), m_gid.get(), nm * 8, cudaMemcpyDeviceToDevice, s));
-        sort_pairs_u64(s, pk.get(), perm.get(), nm, bits_for((uint64_t)std::max<int64_t>(total_slots(), 1)));
-        DBuf<uint64_t> k2(nm, s);
-        GD_KERNEL(k_gather<uint64_t>, grid_for(nm, 256), 256, 0, s, m_key.get(), perm.get(), nm, k2.get());
-        sort_pairs_u64(s, k2.get(), perm.get(), nm, kb);
-        DBuf<int64_t> p2(nm, s);
-        GD_KERNEL(k_gather<int64_t>, grid_for(nm, 256), 256, 0, s, m_gid.get(), perm.get(), nm, p2.get());
-        m_key = std::move(k2);
-        m_gid = std::move(p2);
+        if (one_sort) {
+            sort_pairs_u64(s, m_key.get(), m_gid.get(), nm, kb + rb);
+        } else {  // LSD: by gid, then stable by pair key
+            DBuf<uint64_t> gk(nm, s);
+            DBuf<int32_t> perm(nm, s);
+            GD_KERNEL(k_widen, grid_for(nm, 256), 256, 0, s, m_gid.get(), nm, gk.get());
+            iota_i32(s, perm.get(), nm);
+            sort_pairs_u64(s, gk.get(), perm.get(), nm, 32);
+            DBuf<uint64_t> k2(nm, s);
+            GD_KERNEL(k_gather<uint64_t>, grid_for(nm, 256), 256, 0, s, m_key.get(), perm.get(), nm, k2.get());
+            sort_pairs_u64(s, k2.get(), perm.get(), nm, kb);
+            DBuf<int32_t> g2(nm, s);
+            GD_KERNEL(k_gather<int32_t>, grid_for(nm, 256), 256, 0, s, m_gid.get(), perm.get(), nm, g2.get());
+            m_key = std::move(k2);
+            m_gid = std::move(g2);
+        }
     }
     DBuf<int64_t> rq_pos(nrq, s);
     DBuf<uint8_t> found_local;
@@ -923,7 +1086,7 @@ int64_t Store::apply_deletes(const int32_t* d_src, const int32_t* d_dst, int64_t
     }
     GD_CUDA(cudaMemsetAsync(found, 0, k, s));
     GD_KERNEL(k_del_resolve, grid_for(nrq, 256), 256, 0, s, rq_key.get(), rq_occ.get(), rq_rec.get(),
-              rq_which.get(), nrq, m_key.get(), m_gid.get(), nm, rq_pos.get(), found);
+              rq_which.get(), nrq, m_key.get(), m_gid.get(), nm, rb, rq_pos.get(), found);
     KilledArcs ka;
     ka.row.alloc(nrq, s);
     ka.col.alloc(nrq, s);
