@@ -233,13 +233,14 @@ __global__ void k_aff_sample(OutView ov, int64_t n, int32_t* p) {
     const int32_t* col = ov.col[0];
     for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
         int64_t a = off[v], b = off[v + 1];
-        int k = 0;
-        for (int64_t i = a; i < b && k < kSample; ++i) {
-            int32_t c = col[i];
-            if (c < 0) continue;
-            ++k;
-            if (c != (int32_t)v) uf_union(p, (int32_t)v, c);
-        }
+        // the first kSample slots, loaded together (a tombstone among them
+        // just means fewer samples: the rest pass links every arc anyway)
+        int32_t c[kSample];
+#pragma unroll
+        for (int k = 0; k < kSample; ++k) c[k] = a + k < b ? col[a + k] : -1;
+#pragma unroll
+        for (int k = 0; k < kSample; ++k)
+            if (c[k] >= 0 && c[k] != (int32_t)v) uf_union(p, (int32_t)v, c[k]);
     }
 }
 
@@ -262,15 +263,9 @@ __global__ void k_aff_rest(OutView ov, IdxView in, int64_t n, int32_t giant, int
             const int64_t* off = ov.off[sg];
             const int32_t* col = ov.col[sg];
             int64_t a = off[v], b = off[v + 1];
-            int k = 0;
-            for (int64_t i = a; i < b; ++i) {
+            for (int64_t i = (sg == 0 ? a + kSample : a); i < b; ++i) {  // base slots < kSample: sampled
                 int32_t c = col[i];
-                if (c < 0) continue;
-                if (sg == 0 && k < kSample) {  // linked in the sampling pass
-                    ++k;
-                    continue;
-                }
-                if (c != (int32_t)v) uf_union(p, (int32_t)v, c);
+                if (c >= 0 && c != (int32_t)v) uf_union(p, (int32_t)v, c);
             }
         }
         if (in.off) {

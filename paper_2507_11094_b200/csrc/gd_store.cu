@@ -20,6 +20,7 @@ namespace gdb {
 namespace {
 
 constexpr int kChunk = 1024;  // chain slots per delete-scan work item
+constexpr int kScanILP = 4;    // loads in flight per lane in the chain scans
 
 __device__ inline int seg_of(const int64_t* base, int nseg, int64_t gid) {
     int s = 0;
@@ -240,15 +241,19 @@ __global__ void __launch_bounds__(256) k_del_scan_head(OutView ov, const int32_t
             int64_t wlen = len;
             for (int o = G; o < 32; o <<= 1) wlen = max(wlen, (int64_t)__shfl_xor_sync(0xffffffffu, wlen, o));
             const int32_t* col = ov.col[sg];
-            for (int64_t x0 = 0; x0 < wlen; x0 += G) {
-                int64_t x = x0 + gl;
-                bool hit = false;
-                int32_t c = -1;
-                if (x < len) {
-                    c = col[a + x];
-                    if (c >= 0) hit = requested(rq_key, lo, hi, row, c, sh, c0, c1, nullptr);
+            for (int64_t x0 = 0; x0 < wlen; x0 += G * kScanILP) {
+                int32_t cv[kScanILP];
+#pragma unroll
+                for (int u = 0; u < kScanILP; ++u) {  // all loads first: kScanILP in flight per lane
+                    int64_t x = x0 + u * G + gl;
+                    cv[u] = x < len ? col[a + x] : -1;
                 }
-                emit_matches(mo, hit, row, c, sh, acc + x, ov.base[sg] + a + x);
+#pragma unroll
+                for (int u = 0; u < kScanILP; ++u) {
+                    int64_t x = x0 + u * G + gl;
+                    bool hit = cv[u] >= 0 && requested(rq_key, lo, hi, row, cv[u], sh, c0, c1, nullptr);
+                    emit_matches(mo, hit, row, cv[u], sh, acc + x, ov.base[sg] + a + x);
+                }
             }
             acc += L;
         }
@@ -291,16 +296,19 @@ __global__ void __launch_bounds__(kScanWarps * 32) k_del_scan_tail(OutView ov, c
             const int32_t* col = ov.col[sg];
             int64_t a = off[row], L = off[row + 1] - a;
             int64_t s0 = max(p0, acc), s1 = min(p1, acc + L);
-            for (int64_t x0 = s0; x0 < s1; x0 += 32) {
-                int64_t x = x0 + lane;
-                bool hit = false;
-                int32_t c = -1;
-                int64_t idx = a + (x - acc);
-                if (x < s1) {
-                    c = col[idx];
-                    if (c >= 0) hit = requested(rq_key, lo, hi, row, c, sh, c0, c1, use_bm ? bm : nullptr);
+            for (int64_t x0 = s0; x0 < s1; x0 += 32 * kScanILP) {
+                int32_t cv[kScanILP];
+#pragma unroll
+                for (int u = 0; u < kScanILP; ++u) {  // all loads first: kScanILP in flight per lane
+                    int64_t x = x0 + u * 32 + lane;
+                    cv[u] = x < s1 ? col[a + (x - acc)] : -1;
                 }
-                emit_matches(mo, hit, row, c, sh, x, ov.base[sg] + idx);
+#pragma unroll
+                for (int u = 0; u < kScanILP; ++u) {
+                    int64_t x = x0 + u * 32 + lane;
+                    bool hit = cv[u] >= 0 && requested(rq_key, lo, hi, row, cv[u], sh, c0, c1, use_bm ? bm : nullptr);
+                    emit_matches(mo, hit, row, cv[u], sh, x, ov.base[sg] + a + (x - acc));
+                }
             }
             acc += L;
         }
@@ -390,15 +398,24 @@ __global__ void k_add_vacancies(OutView ov, const uint32_t* skey, const int32_t*
             const int64_t* off = ov.off[sg];
             const int32_t* col = ov.col[sg];
             int64_t a = off[row], b = off[row + 1];
-            for (int64_t base = a; base < b && got < want; base += 32) {
-                int64_t i = base + lane;
-                bool vac = (i < b) && col[i] < 0;
-                unsigned mask = __ballot_sync(0xffffffffu, vac);
-                if (vac) {
-                    int64_t t = got + __popc(mask & ((1u << lane) - 1));
-                    if (t < want) vac_gid[lo + t] = ov.base[sg] + i;
+            for (int64_t base = a; base < b && got < want; base += 32 * kScanILP) {
+                int32_t cv[kScanILP];
+#pragma unroll
+                for (int u = 0; u < kScanILP; ++u) {
+                    int64_t i = base + u * 32 + lane;
+                    cv[u] = i < b ? col[i] : 0;
                 }
-                got += __popc(mask);
+#pragma unroll
+                for (int u = 0; u < kScanILP; ++u) {
+                    int64_t i = base + u * 32 + lane;
+                    bool vac = (i < b) && cv[u] < 0;
+                    unsigned mask = __ballot_sync(0xffffffffu, vac);
+                    if (vac) {
+                        int64_t t = got + __popc(mask & ((1u << lane) - 1));
+                        if (t < want) vac_gid[lo + t] = ov.base[sg] + i;
+                    }
+                    got += __popc(mask);
+                }
             }
         }
     }
