@@ -260,13 +260,13 @@ void PR::power_loop() {
         GD_CUDA(cudaMemsetAsync(scal.get() + 1, 0, sizeof(double), s));
         // algorithmic bytes: |A| (off + 2 f64) + E_in(A) (idx + f64)
         if (nbin[0])
-            GD_KERNEL_T("pr_pull", nbin[0] * 24 + ebin[0] * 12, k_pr_pull_group<8>,
-                        grid_for(((nbin[0] + 3) / 4) * 32, kPullThreads, 148LL * 32), kPullThreads, 0, s,
+            GD_KERNEL_T("pr_pull", nbin[0] * 24 + ebin[0] * 12, k_pr_pull_group<2>,
+                        grid_for(((nbin[0] + 15) / 16) * 32, kPullThreads, 148LL * 32), kPullThreads, 0, s,
                         bins[0].get(), nbin[0], ix, contrib.get(), rank.get(), scal.get(), base, damping, inv_n,
                         rank_new.get(), scal.get() + 1);
         if (nbin[1])
-            GD_KERNEL_T("pr_pull", nbin[1] * 24 + ebin[1] * 12, k_pr_pull_group<32>,
-                        grid_for(nbin[1] * 32, kPullThreads, 148LL * 32), kPullThreads, 0, s, bins[1].get(),
+            GD_KERNEL_T("pr_pull", nbin[1] * 24 + ebin[1] * 12, k_pr_pull_group<16>,
+                        grid_for(((nbin[1] + 1) / 2) * 32, kPullThreads, 148LL * 32), kPullThreads, 0, s, bins[1].get(),
                         nbin[1], ix, contrib.get(), rank.get(), scal.get(), base, damping, inv_n, rank_new.get(),
                         scal.get() + 1);
         if (nbin[2])
