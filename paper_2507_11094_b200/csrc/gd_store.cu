@@ -178,44 +178,52 @@ __global__ void k_widen(const int32_t* a, int64_t m, uint64_t* o) {
         o[i] = (uint64_t)(uint32_t)a[i];
 }
 
-// Matches go out as (sort key, gid) with sort key = pair key << rb | chain
-// offset of the slot within its row, so ONE radix sort orders them by (pair,
-// chain order): the j-th match of a pair is the pair's j-th live occurrence.
+// A hit on a pair with ONE delete request takes the pair's first live
+// occurrence in chain order: atomicMin of the global slot id (gid order is
+// chain order).  Pairs with several requests (parallel arcs deleted together)
+// go to an overflow list keyed (pair << rb | chain offset) whose single radix
+// sort gives the j-th occurrence for the j-th request.
 struct MatchOut {
-    uint64_t* key;
-    int32_t* gid;
-    unsigned long long* cnt;
+    unsigned long long* sel;  // per request: min gid (pairs with one request)
+    const uint8_t* single;    // per request: its key has exactly one request
+    uint64_t* okey;
+    int32_t* ogid;
+    unsigned long long* ocnt;
     int64_t cap;
     int rb;
 };
 
-__device__ inline void emit_matches(const MatchOut& mo, bool hit, int32_t row, int32_t c, int sh, int64_t chain,
+__device__ inline void emit_matches(const MatchOut& mo, int64_t p, int32_t row, int32_t c, int sh, int64_t chain,
                                     int64_t gid) {
-    unsigned mask = __ballot_sync(0xffffffffu, hit);
+    bool multi = p >= 0 && !mo.single[p];
+    if (p >= 0 && !multi) atomicMin(&mo.sel[p], (unsigned long long)gid);
+    unsigned mask = __ballot_sync(0xffffffffu, multi);
     if (!mask) return;
     const int lane = threadIdx.x & 31;
     unsigned long long basei = 0;
-    if (lane == 0) basei = atomicAdd(mo.cnt, (unsigned long long)__popc(mask));
+    if (lane == 0) basei = atomicAdd(mo.ocnt, (unsigned long long)__popc(mask));
     basei = __shfl_sync(0xffffffffu, basei, 0);
-    if (hit) {
+    if (multi) {
         int64_t slot = (int64_t)basei + __popc(mask & ((1u << lane) - 1));
         if (slot < mo.cap) {
-            mo.key[slot] = (pair_key(row, c, sh) << mo.rb) | (uint64_t)chain;
-            mo.gid[slot] = (int32_t)gid;
+            mo.okey[slot] = (pair_key(row, c, sh) << mo.rb) | (uint64_t)chain;
+            mo.ogid[slot] = (int32_t)gid;
         }
     }
 }
 
-__device__ inline bool requested(const uint64_t* rq_key, int64_t lo, int64_t hi, int32_t row, int32_t c, int sh,
-                                 int32_t c0, int32_t c1, const uint32_t* bm) {
-    if (hi - lo <= 2) return c == c0 || c == c1;
+// index of the first request for (row, c), or -1
+__device__ inline int64_t requested(const uint64_t* rq_key, int64_t lo, int64_t hi, int32_t row, int32_t c, int sh,
+                                    int32_t c0, int32_t c1, const uint32_t* bm) {
+    if (c < 0) return -1;
+    if (hi - lo <= 2) return c == c0 ? lo : (c == c1 ? lo + 1 : -1);
     if (bm) {
         uint32_t h = (uint32_t)c & (kBitmapWords * 32 - 1);
-        if (!(bm[h >> 5] & (1u << (h & 31)))) return false;
+        if (!(bm[h >> 5] & (1u << (h & 31)))) return -1;
     }
     uint64_t want = pair_key(row, c, sh);
     int64_t p = lower_bound_dev<uint64_t>(rq_key, lo, hi, want);
-    return p < hi && rq_key[p] == want;
+    return (p < hi && rq_key[p] == want) ? p : -1;
 }
 
 // head: one 8-lane group per requested row, chain slots [0, kHead)
@@ -251,8 +259,8 @@ __global__ void __launch_bounds__(256) k_del_scan_head(OutView ov, const int32_t
 #pragma unroll
                 for (int u = 0; u < kScanILP; ++u) {
                     int64_t x = x0 + u * G + gl;
-                    bool hit = cv[u] >= 0 && requested(rq_key, lo, hi, row, cv[u], sh, c0, c1, nullptr);
-                    emit_matches(mo, hit, row, cv[u], sh, acc + x, ov.base[sg] + a + x);
+                    int64_t hp = requested(rq_key, lo, hi, row, cv[u], sh, c0, c1, nullptr);
+                    emit_matches(mo, hp, row, cv[u], sh, acc + x, ov.base[sg] + a + x);
                 }
             }
             acc += L;
@@ -306,8 +314,8 @@ __global__ void __launch_bounds__(kScanWarps * 32) k_del_scan_tail(OutView ov, c
 #pragma unroll
                 for (int u = 0; u < kScanILP; ++u) {
                     int64_t x = x0 + u * 32 + lane;
-                    bool hit = cv[u] >= 0 && requested(rq_key, lo, hi, row, cv[u], sh, c0, c1, use_bm ? bm : nullptr);
-                    emit_matches(mo, hit, row, cv[u], sh, x, ov.base[sg] + a + (x - acc));
+                    int64_t hp = requested(rq_key, lo, hi, row, cv[u], sh, c0, c1, use_bm ? bm : nullptr);
+                    emit_matches(mo, hp, row, cv[u], sh, x, ov.base[sg] + a + (x - acc));
                 }
             }
             acc += L;
@@ -316,43 +324,59 @@ __global__ void __launch_bounds__(kScanWarps * 32) k_del_scan_tail(OutView ov, c
     }
 }
 
-// Resolve each request against the (key, gid)-sorted matches.
+__global__ void k_single_flags(const uint64_t* key, int64_t m, uint8_t* single) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+        single[i] = (i == 0 || key[i - 1] != key[i]) && (i + 1 == m || key[i + 1] != key[i]);
+}
+
+// Resolve each request: single-request pairs from the atomicMin slot, the
+// others against the (pair, chain)-sorted overflow matches.
 __global__ void k_del_resolve(const uint64_t* rq_key, const int32_t* rq_occ, const int32_t* rq_rec,
-                              const uint8_t* rq_which, int64_t nrq, const uint64_t* m_key, const int32_t* m_gid,
-                              int64_t nm, int rb, int64_t* rq_pos, uint8_t* found_fwd) {
+                              const uint8_t* rq_which, const uint8_t* single, const unsigned long long* sel,
+                              int64_t nrq, const uint64_t* m_key, const int32_t* m_gid, int64_t nm, int rb,
+                              int64_t* rq_pos, uint8_t* found_fwd, unsigned long long* applied) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nrq; i += (int64_t)gridDim.x * blockDim.x) {
-        uint64_t key = rq_key[i];
-        int64_t lo = lower_bound_dev<uint64_t>(m_key, 0, nm, key << rb);
-        int64_t occ = rq_occ[i];
         int64_t pos = -1;
-        if (lo + occ < nm && (m_key[lo + occ] >> rb) == key) pos = m_gid[lo + occ];
+        if (single[i]) {
+            if (sel[i] != ~0ULL) pos = (int64_t)sel[i];
+        } else {
+            uint64_t key = rq_key[i];
+            int64_t lo = lower_bound_dev<uint64_t>(m_key, 0, nm, key << rb);
+            int64_t occ = rq_occ[i];
+            if (lo + occ < nm && (m_key[lo + occ] >> rb) == key) pos = m_gid[lo + occ];
+        }
         rq_pos[i] = pos;
-        if (rq_which[i] == 0) found_fwd[rq_rec[i]] = pos >= 0 ? 1 : 0;
+        if (rq_which[i] == 0) {
+            found_fwd[rq_rec[i]] = pos >= 0 ? 1 : 0;
+            if (pos >= 0) atomicAdd(applied, 1ULL);
+        }
     }
 }
 
 // Tombstone the resolved slots.  A reverse-direction request only applies
-// when its record's forward arc was found (dynamic.py:221-229).
+// when its record's forward arc was found (dynamic.py:221-229).  Output slot i
+// belongs to request i (gid -1 = nothing killed).
 __global__ void k_del_kill(OutView ov, const uint64_t* rq_key, const int32_t* rq_rec, const uint8_t* rq_which,
                            const int64_t* rq_pos, int64_t nrq, const uint8_t* found_fwd, int sh, int32_t* k_row,
                            int32_t* k_col, int32_t* k_w, int64_t* k_gid, unsigned long long* k_cnt) {
+    unsigned long long killed = 0;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nrq; i += (int64_t)gridDim.x * blockDim.x) {
         int64_t gid = rq_pos[i];
+        if (gid >= 0 && rq_which[i] == 1 && !found_fwd[rq_rec[i]]) gid = -1;
+        k_gid[i] = gid;
         if (gid < 0) continue;
-        if (rq_which[i] == 1 && !found_fwd[rq_rec[i]]) continue;
         int sg = seg_of(ov.base, ov.nseg, gid);
         int64_t slot = gid - ov.base[sg];
         int32_t* col = const_cast<int32_t*>(ov.col[sg]);
         const int32_t* w = ov.w[sg];
-        int32_t c = col[slot];
-        int32_t wt = w ? w[slot] : 1;
+        k_row[i] = key_row(rq_key[i], sh);
+        k_col[i] = col[slot];
+        k_w[i] = w ? w[slot] : 1;
         col[slot] = kSentinel;
-        unsigned long long o = atomicAdd(k_cnt, 1ULL);
-        k_row[o] = key_row(rq_key[i], sh);
-        k_col[o] = c;
-        k_w[o] = wt;
-        k_gid[o] = gid;
+        ++killed;
     }
+    for (int o = 16; o; o >>= 1) killed += __shfl_xor_sync(0xffffffffu, killed, o);
+    if ((threadIdx.x & 31) == 0 && killed) atomicAdd(k_cnt, killed);
 }
 
 // ---------------------------------------------------------------- adds -----
@@ -449,61 +473,33 @@ __global__ void k_gather_arcs(const int32_t* sel, int64_t m, const int32_t* sval
     }
 }
 
-__global__ void k_tomb_still_dead(const int64_t* pos, int64_t m, const int32_t* col0, uint8_t* keep) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
-        keep[i] = col0[pos[i]] < 0 ? 1 : 0;
-}
 
 // ----------------------------------------------------- index maintenance ----
 
-// For each killed arc, the index entry (ix_row, ix_col) it maps to, and its
-// weight as a secondary sort key.
-__global__ void k_kill_to_index(const int32_t* k_row, const int32_t* k_col, const int32_t* k_w, int64_t m,
-                                bool rows_are_dst, int sh, uint64_t* key, int32_t* val, uint32_t* wkey) {
+// Each killed arc tombstones one live index entry with the same column and
+// weight, claimed by CAS so parallel arcs take distinct entries.  Log slot i
+// belongs to killed arc i (-1 when there was none).
+__global__ void k_index_claim(const int32_t* k_row, const int32_t* k_col, const int32_t* k_w, const int64_t* k_gid,
+                              int64_t m, bool rows_are_dst, const int64_t* off, int32_t* col, const int32_t* w,
+                              int64_t* t_pos, int32_t* t_row) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+        t_pos[i] = -1;
+        if (k_gid[i] < 0) continue;
         int32_t r = rows_are_dst ? k_col[i] : k_row[i];
         int32_t c = rows_are_dst ? k_row[i] : k_col[i];
-        key[i] = pair_key(r, c, sh);
-        val[i] = (int32_t)i;
-        wkey[i] = (uint32_t)k_w[i];
-    }
-}
-
-// Items sorted by (key, w); the j-th item of an equal (key, w) run tombstones
-// the j-th live entry with that column and weight in the (clean) row.  Each
-// item writes its own slot of the tomb log (-1 when nothing matched); for
-// unweighted graphs the positions come out ascending (items and entries share
-// the (row, col) order), so no sort is needed there.
-__global__ void k_index_kill(const uint64_t* key, const int32_t* wk, int64_t m, int sh, const int64_t* off,
-                             int32_t* col, const int32_t* w, int64_t* t_pos, int32_t* t_row,
-                             unsigned long long* t_cnt) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
-        uint64_t kk = key[i];
-        int32_t wt = wk[i];
-        int64_t j = 0;
-        for (int64_t p = i - 1; p >= 0 && key[p] == kk && wk[p] == wt; --p) ++j;
-        int32_t r = key_row(kk, sh), c = key_col(kk, sh);
+        int32_t wt = k_w[i];
         int64_t lo = col_lower(col, off[r], off[r + 1], c);
         int64_t hi = col_upper(col, lo, off[r + 1], c);
         for (int64_t e = lo; e < hi; ++e) {
-            int32_t v = col[e];
-            if (v < 0) continue;
+            if (col[e] != c) continue;  // tombstoned (~c)
             if (w && w[e] != wt) continue;
-            if (j == 0) {
-                col[e] = tomb(v);
+            if (atomicCAS(&col[e], c, tomb(c)) == c) {
                 t_pos[i] = e;
                 t_row[i] = r;
-                atomicAdd(t_cnt, 1ULL);
                 break;
             }
-            --j;
         }
     }
-}
-
-__global__ void k_nonneg_flags(const int64_t* a, int64_t m, uint8_t* f) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
-        f[i] = a[i] >= 0 ? 1 : 0;
 }
 
 __global__ void k_added_to_index(const int32_t* a_row, const int32_t* a_col, int64_t m, bool rows_are_dst, int sh,
@@ -543,14 +539,28 @@ __global__ void k_delta_rows(const int64_t* off, int64_t n, const int32_t* col, 
 
 // --------------------------------------------------------- edit merge -----
 
-__global__ void k_shift_hist(const int32_t* trow, int64_t ntomb, const int32_t* irow, int64_t nins, int64_t* cnt) {
-    int64_t tot = ntomb + nins;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
-        if (i < ntomb)
-            atomicAdd(reinterpret_cast<unsigned long long*>(&cnt[trow[i]]), (unsigned long long)(-1LL));
-        else
-            atomicAdd(reinterpret_cast<unsigned long long*>(&cnt[irow[i - ntomb]]), 1ULL);
+constexpr int kEditThreads = 256;
+constexpr int kWin = 256;                                 // entries per warp window
+constexpr int kTile = kWin * (kEditThreads / 32);         // 2048 entries per CTA tile
+
+// Dead entries per 256-entry window and per row, from an UNORDERED tomb log.  With
+// dedupe (the out-store), a slot logged twice (deleted, claimed, deleted
+// again between merges) counts once: the first visit flips -1 to -2.
+__global__ void k_tomb_hist(const int64_t* tpos, const int32_t* trow, int64_t ntomb, int32_t* col, int64_t nnz,
+                            bool dedupe, unsigned long long* tile_dead, int64_t* row_shift) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ntomb; i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t p = tpos[i];
+        if (p < 0 || p >= nnz) continue;
+        bool dead = dedupe ? atomicCAS(&col[p], kSentinel, kSentinel - 1) == kSentinel : col[p] < 0;
+        if (!dead) continue;
+        atomicAdd(&tile_dead[p / kWin], 1ULL);
+        atomicAdd(reinterpret_cast<unsigned long long*>(&row_shift[trow[i]]), (unsigned long long)(-1LL));
     }
+}
+
+__global__ void k_ins_hist(const int32_t* irow, int64_t nins, int64_t* row_shift) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nins; i += (int64_t)gridDim.x * blockDim.x)
+        atomicAdd(reinterpret_cast<unsigned long long*>(&row_shift[irow[i]]), 1ULL);
 }
 
 __global__ void k_add_offsets(const int64_t* off, const int64_t* shift, int64_t n1, int64_t* out) {
@@ -558,105 +568,95 @@ __global__ void k_add_offsets(const int64_t* off, const int64_t* shift, int64_t 
         out[i] = off[i] + shift[i];
 }
 
-constexpr int kEditThreads = 256;
-constexpr int kPerThread = 8;
-constexpr int kTile = kEditThreads * kPerThread;  // 2048 entries per tile
-
-// Per tile: first tomb >= tile start, first insert with P > tile start - 1
-// (all tiles in parallel, instead of one searching thread per CTA).
-__global__ void k_tile_bounds(int64_t ntiles, const int64_t* tpos, int64_t ntomb, const int64_t* ipos, int64_t nins,
-                              int64_t* tb, int64_t* pj) {
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t <= ntiles; t += (int64_t)gridDim.x * blockDim.x) {
-        int64_t p = t * kTile;
-        tb[t] = lower_bound_dev<int64_t>(tpos, 0, ntomb, p);
-        pj[t] = upper_bound_dev<int64_t>(ipos, 0, nins, p - 1);
-    }
+// inserts with P < tile start, per tile (insertion points are sorted)
+__global__ void k_tile_ins(int64_t ntiles, const int64_t* ipos, int64_t nins, int64_t* pj) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t <= ntiles; t += (int64_t)gridDim.x * blockDim.x)
+        pj[t] = lower_bound_dev<int64_t>(ipos, 0, nins, t * kTile);
 }
 
-// Base entries: newpos(i) = i - #tombs(< i) + #inserts(P <= i).  Each warp
-// owns a 256-entry window, lane-strided so every load and store instruction
-// covers 32 consecutive entries.  The window's few tomb / insert events are
-// dropped into a shared delta array (-1 after a tomb, +1 at an insert point)
-// whose warp-scanned prefix is each entry's shift -- no per-entry search.
-constexpr int kWin = kTile / (kEditThreads / 32);  // 256
-
-__global__ void __launch_bounds__(kEditThreads) k_edit_base(const int32_t* col, const int32_t* w, int64_t nnz,
-                                                            const int64_t* tpos, const int64_t* ipos,
-                                                            const int64_t* tb_tile, const int64_t* pj_tile,
-                                                            int64_t ntiles, int32_t* ocol, int32_t* ow) {
-    __shared__ int dsh[kEditThreads / 32][kWin + 1];
+// newpos(i) = i - #dead(< i) + #inserts(P <= i).  A CTA takes a 2048-entry
+// tile, each warp a 256-entry window, lane-strided (every load / store
+// instruction covers 32 consecutive entries).  Dead entries are exactly the
+// negative ones, so #dead is the window's base (scan of the per-window tomb
+// histogram) plus a ballot/popc prefix; warps never wait on each other.  The
+// window's few insertion points are counted per entry and their entries
+// written here too.
+__global__ void __launch_bounds__(kEditThreads) k_edit_base(const int32_t* __restrict__ col,
+                                                            const int32_t* __restrict__ w, int64_t nnz,
+                                                            const int64_t* dead_win, const int64_t* ipos,
+                                                            const int64_t* pj_tile, const int32_t* icol,
+                                                            const int32_t* iw, int64_t ntiles,
+                                                            int32_t* __restrict__ ocol, int32_t* __restrict__ ow) {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    int* d = dsh[wid];
+    const unsigned lt = (1u << lane) - 1;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        int64_t ws = tile * kTile + (int64_t)wid * kWin;
-        if (ws >= nnz) continue;  // warp-uniform
-        int64_t we = min(ws + kWin, nnz);
-        int64_t tb0 = tb_tile[tile], tb1 = tb_tile[tile + 1];
-        int64_t pj0 = pj_tile[tile], pj1 = pj_tile[tile + 1];
-        int64_t tbw = tb0, tbe = tb0, pjw = pj0, pje = pj0;
-        if (tb0 != tb1 || pj0 != pj1) {
-            if (lane == 0) {
-                tbw = lower_bound_dev<int64_t>(tpos, tb0, tb1, ws);
-                tbe = lower_bound_dev<int64_t>(tpos, tbw, tb1, we);
-            } else if (lane == 1) {
-                pjw = upper_bound_dev<int64_t>(ipos, pj0, pj1, ws - 1);
-                pje = upper_bound_dev<int64_t>(ipos, pjw, pj1, we - 1);
-            }
-            tbw = __shfl_sync(0xffffffffu, tbw, 0);
-            tbe = __shfl_sync(0xffffffffu, tbe, 0);
-            pjw = __shfl_sync(0xffffffffu, pjw, 1);
-            pje = __shfl_sync(0xffffffffu, pje, 1);
-        }
-        const bool events = (tbe > tbw) || (pje > pjw);
-        int sc[kWin / 32];
-        if (events) {
-            for (int q = lane; q <= kWin; q += 32) d[q] = 0;
-            __syncwarp();
-            for (int64_t k = tbw + lane; k < tbe; k += 32) atomicAdd(&d[tpos[k] - ws + 1], -1);
-            for (int64_t k = pjw + lane; k < pje; k += 32) atomicAdd(&d[ipos[k] - ws], 1);
-            __syncwarp();
-            int carry = 0;
-#pragma unroll
-            for (int q = 0; q < kWin / 32; ++q) {
-                int x = d[q * 32 + lane];
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    int y = __shfl_up_sync(0xffffffffu, x, o);
-                    if (lane >= o) x += y;
-                }
-                x += carry;
-                sc[q] = x;
-                carry = __shfl_sync(0xffffffffu, x, 31);
-            }
-            __syncwarp();
-        } else {
-#pragma unroll
-            for (int q = 0; q < kWin / 32; ++q) sc[q] = 0;
-        }
-        const int64_t shift0 = pjw - tbw;
-        int32_t v[kWin / 32];
-        int32_t wv[kWin / 32];
+        const int64_t ws = tile * kTile + (int64_t)wid * kWin;
+        const int64_t we = min(ws + kWin, nnz);
+        int32_t v[kWin / 32], wv[kWin / 32];
+        unsigned m[kWin / 32];
+        if (ws >= nnz) continue;  // warp-uniform: no block-level sync in this kernel
+        int wd = 0;
 #pragma unroll
         for (int q = 0; q < kWin / 32; ++q) {
             int64_t i = ws + q * 32 + lane;
-            v[q] = i < we ? __ldcs(&col[i]) : -1;
-            wv[q] = (w && i < we) ? __ldcs(&w[i]) : 0;
+            bool in = i < we;
+            v[q] = in ? __ldcs(&col[i]) : 0;
+            wv[q] = (w && in) ? __ldcs(&w[i]) : 0;
         }
 #pragma unroll
         for (int q = 0; q < kWin / 32; ++q) {
-            if (v[q] < 0) continue;
-            int64_t np = ws + q * 32 + lane + shift0 + sc[q];
-            __stcs(&ocol[np], v[q]);
-            if (ow) __stcs(&ow[np], wv[q]);
+            int64_t i = ws + q * 32 + lane;
+            m[q] = __ballot_sync(0xffffffffu, i < we && v[q] < 0);
+            wd += __popc(m[q]);
+        }
+        (void)wd;
+        const int64_t dead0 = dead_win[ws / kWin];
+        const int64_t pj0 = pj_tile[tile], pj1 = pj_tile[tile + 1];
+        int64_t pjw = pj0, pje = pj0;
+        if (pj0 != pj1) {
+            pjw = lower_bound_dev<int64_t>(ipos, pj0, pj1, ws);
+            pje = lower_bound_dev<int64_t>(ipos, pjw, pj1, we);
+        }
+        const int64_t nins = pje - pjw;
+        const int64_t my_ins = lane < nins ? ipos[pjw + lane] : INT64_MAX;
+        int64_t dead_before = dead0;
+#pragma unroll
+        for (int q = 0; q < kWin / 32; ++q) {
+            int64_t i = ws + q * 32 + lane;
+            int64_t ins = pjw;
+            if (nins > 32) {
+                ins = upper_bound_dev<int64_t>(ipos, pjw, pje, i);
+            } else {
+                for (int k = 0; k < nins; ++k) ins += __shfl_sync(0xffffffffu, my_ins, k) <= i;
+            }
+            if (i < we && v[q] >= 0) {
+                int64_t np = i - (dead_before + __popc(m[q] & lt)) + ins;
+                __stcs(&ocol[np], v[q]);
+                if (ow) __stcs(&ow[np], wv[q]);
+            }
+            dead_before += __popc(m[q]);
+        }
+        for (int64_t j = pjw + lane; j < pje; j += 32) {  // this window's inserted entries
+            int64_t P = ipos[j];
+            int64_t o = P - ws;
+            int qq = (int)(o >> 5), r = (int)(o & 31);
+            int64_t dead = dead0;
+#pragma unroll
+            for (int q = 0; q < kWin / 32; ++q)
+                dead += q < qq ? __popc(m[q]) : (q == qq ? __popc(m[q] & ((1u << r) - 1)) : 0);
+            int64_t np = P - dead + j;
+            ocol[np] = icol[j];
+            if (ow) ow[np] = iw ? iw[j] : 1;
         }
     }
 }
 
-__global__ void k_edit_ins(const int32_t* icol, const int32_t* iw, const int64_t* ipos, int64_t nins,
-                           const int64_t* tpos, int64_t ntomb, int32_t* ocol, int32_t* ow) {
+// insertions at the very end of the base (P == nnz)
+__global__ void k_edit_tail(const int64_t* ipos, int64_t nins, int64_t nnz, const int64_t* dead_total,
+                            const int32_t* icol, const int32_t* iw, int32_t* ocol, int32_t* ow) {
     for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < nins; j += (int64_t)gridDim.x * blockDim.x) {
-        int64_t p = ipos[j];
-        int64_t np = p - lower_bound_dev<int64_t>(tpos, 0, ntomb, p) + j;
+        if (ipos[j] < nnz) continue;
+        int64_t np = nnz - *dead_total + j;
         ocol[np] = icol[j];
         if (ow) ow[np] = iw ? iw[j] : 1;
     }
@@ -670,10 +670,6 @@ __global__ void k_export_seg(const int32_t* col, const int32_t* w, int64_t m, in
     }
 }
 
-__global__ void k_select_base_kills(const int64_t* gid, int64_t m, int64_t base_slots, uint8_t* flag) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
-        flag[i] = gid[i] < base_slots ? 1 : 0;
-}
 
 template <typename T>
 __global__ void k_gather_sel(const T* in, const int32_t* sel, int64_t m, T* out) {
@@ -685,36 +681,41 @@ __global__ void k_gather_sel(const T* in, const int32_t* sel, int64_t m, T* out)
 
 // ==========================================================================
 
-void edit_merge(cudaStream_t s, int64_t n, const int64_t* off, const int32_t* col, const int32_t* w, int64_t nnz,
-                const int64_t* tpos, const int32_t* trow, int64_t ntomb, const int32_t* irow, const int32_t* icol,
-                const int32_t* iw, const int64_t* ipos, int64_t nins, DBuf<int64_t>& new_off,
+void edit_merge(cudaStream_t s, int64_t n, const int64_t* off, int32_t* col, const int32_t* w, int64_t nnz,
+                const int64_t* tpos, const int32_t* trow, int64_t ntomb, bool dedupe, const int32_t* irow,
+                const int32_t* icol, const int32_t* iw, const int64_t* ipos, int64_t nins, DBuf<int64_t>& new_off,
                 DBuf<int32_t>& new_col, DBuf<int32_t>& new_w, int64_t& new_nnz, bool weighted) {
-    new_nnz = nnz - ntomb + nins;
-    DBuf<int64_t> cnt(n + 1, s);
-    cnt.zero(s);
-    if (ntomb + nins)
-        GD_KERNEL(k_shift_hist, grid_for(ntomb + nins, 256), 256, 0, s, trow, ntomb, irow, nins, cnt.get());
-    DBuf<int64_t> shift(n + 1, s);
-    exclusive_scan_i64(s, cnt.get(), shift.get(), n + 1);
+    const int64_t ntiles = (nnz + kTile - 1) / kTile;
+    const int64_t nwin = (nnz + kWin - 1) / kWin;
+    DBuf<int64_t> shift_cnt(n + 1, s), dead_cnt(nwin + 1, s);
+    shift_cnt.zero(s);
+    dead_cnt.zero(s);
+    if (ntomb)
+        GD_KERNEL(k_tomb_hist, grid_for(ntomb, 256), 256, 0, s, tpos, trow, ntomb, col, nnz, dedupe,
+                  reinterpret_cast<unsigned long long*>(dead_cnt.get()), shift_cnt.get());
+    if (nins) GD_KERNEL(k_ins_hist, grid_for(nins, 256), 256, 0, s, irow, nins, shift_cnt.get());
+    DBuf<int64_t> shift(n + 1, s), dead_win(nwin + 1, s);
+    exclusive_scan_i64(s, shift_cnt.get(), shift.get(), n + 1);
+    exclusive_scan_i64(s, dead_cnt.get(), dead_win.get(), nwin + 1);
+    int64_t dead_total = read_scalar(s, dead_win.get() + nwin);  // sizes the new arrays
+    new_nnz = nnz - dead_total + nins;
     new_off.alloc(n + 1, s);
     GD_KERNEL(k_add_offsets, grid_for(n + 1, 256), 256, 0, s, off, shift.get(), n + 1, new_off.get());
     new_col.alloc(new_nnz, s);
     if (weighted) new_w.alloc(new_nnz, s);
     else new_w.release();
-    if (nnz) {
-        int64_t ntiles = (nnz + kTile - 1) / kTile;
-        DBuf<int64_t> tb(ntiles + 1, s), pj(ntiles + 1, s);
-        GD_KERNEL(k_tile_bounds, grid_for(ntiles + 1, 256), 256, 0, s, ntiles, tpos, ntomb, ipos, nins, tb.get(),
-                  pj.get());
+    if (ntiles) {
+        DBuf<int64_t> pj(ntiles + 1, s);
+        GD_KERNEL(k_tile_ins, grid_for(ntiles + 1, 256), 256, 0, s, ntiles, ipos, nins, pj.get());
         unsigned g = (unsigned)std::min<int64_t>(ntiles, 148LL * 64);
         // algorithmic bytes: every base entry read once, every surviving entry written once
-        GD_KERNEL_T("merge_copy", (nnz + (nnz - ntomb)) * (weighted ? 8 : 4), k_edit_base, g, kEditThreads, 0, s,
-                    col, weighted ? w : nullptr, nnz, tpos, ipos, tb.get(), pj.get(), ntiles, new_col.get(),
-                    weighted ? new_w.get() : nullptr);
+        GD_KERNEL_T("merge_copy", (nnz + (nnz - dead_total)) * (weighted ? 8 : 4), k_edit_base, g, kEditThreads, 0,
+                    s, col, weighted ? w : nullptr, nnz, dead_win.get(), ipos, pj.get(), icol, iw, ntiles,
+                    new_col.get(), weighted ? new_w.get() : nullptr);
     }
     if (nins)
-        GD_KERNEL(k_edit_ins, grid_for(nins, 256), 256, 0, s, icol, iw, ipos, nins, tpos, ntomb, new_col.get(),
-                  weighted ? new_w.get() : nullptr);
+        GD_KERNEL(k_edit_tail, grid_for(nins, 256), 256, 0, s, ipos, nins, nnz, dead_win.get() + nwin, icol, iw,
+                  new_col.get(), weighted ? new_w.get() : nullptr);
 }
 
 // ==========================================================================
@@ -887,8 +888,8 @@ void Store::compact_index(SortedIndex& ix) {
     DBuf<int32_t> ncol, nw;
     int64_t nnz2 = 0;
     edit_merge(s, n, ix.off.get(), ix.col.get(), ix.w.n ? ix.w.get() : nullptr, ix.nnz, ix.tpos.get(),
-               ix.trow.get(), ix.ntomb, ix.drow.get(), ix.dcol.get(), ix.dw.n ? ix.dw.get() : nullptr, ipos.get(),
-               ix.dnnz, noff, ncol, nw, nnz2, weighted);
+               ix.trow.get(), ix.ntomb, false, ix.drow.get(), ix.dcol.get(), ix.dw.n ? ix.dw.get() : nullptr,
+               ipos.get(), ix.dnnz, noff, ncol, nw, nnz2, weighted);
     ix.off = std::move(noff);
     ix.col = std::move(ncol);
     ix.w = std::move(nw);
@@ -905,24 +906,7 @@ void Store::compact_index(SortedIndex& ix) {
 void Store::index_delete(SortedIndex& ix, const KilledArcs& ka) {
     if (!ix.built || ka.count == 0) return;
     cudaStream_t s = stream;
-    int64_t m = ka.count;
-    DBuf<uint64_t> key(m, s);
-    DBuf<int32_t> val(m, s);
-    DBuf<uint32_t> wkey(m, s);
-    GD_KERNEL(k_kill_to_index, grid_for(m, 256), 256, 0, s, ka.row.get(), ka.col.get(), ka.w.get(), m,
-              ix.rows_are_dst, sh, key.get(), val.get(), wkey.get());
-    DBuf<uint64_t> k2(m, s);
-    DBuf<int32_t> w2(m, s);
-    if (weighted) {  // order by (key, w): stable sort by w, then by key
-        sort_pairs_u32(s, wkey.get(), val.get(), m);
-        GD_KERNEL(k_gather<uint64_t>, grid_for(m, 256), 256, 0, s, key.get(), val.get(), m, k2.get());
-        sort_pairs_u64(s, k2.get(), val.get(), m, 2 * sh);
-        GD_KERNEL(k_gather<int32_t>, grid_for(m, 256), 256, 0, s, ka.w.get(), val.get(), m, w2.get());
-    } else {
-        sort_pairs_u64(s, key.get(), val.get(), m, 2 * sh);
-        GD_CUDA(cudaMemcpyAsync(k2.get(), key.get(), m * 8, cudaMemcpyDeviceToDevice, s));
-        fill_i32(s, w2.get(), m, 1);
-    }
+    int64_t m = ka.count;  // slots (one per request; gid -1 = none)
     int64_t old = ix.ntomb;
     DBuf<int64_t> tpos(old + m, s);
     DBuf<int32_t> trow(old + m, s);
@@ -930,41 +914,12 @@ void Store::index_delete(SortedIndex& ix, const KilledArcs& ka) {
         GD_CUDA(cudaMemcpyAsync(tpos.get(), ix.tpos.get(), old * 8, cudaMemcpyDeviceToDevice, s));
         GD_CUDA(cudaMemcpyAsync(trow.get(), ix.trow.get(), old * 4, cudaMemcpyDeviceToDevice, s));
     }
-    DBuf<unsigned long long> cnt(1, s);
-    cnt.zero(s);
-    fill_i64(s, tpos.get() + old, m, -1);
-    GD_KERNEL(k_index_kill, grid_for(m, 256), 256, 0, s, k2.get(), w2.get(), m, sh, ix.off.get(), ix.col.get(),
-              ix.w.n ? ix.w.get() : nullptr, tpos.get() + old, trow.get() + old, cnt.get());
-    int64_t killed = (int64_t)read_scalar(s, cnt.get());
-    if (killed < m) {  // drop the unmatched (-1) slots, order kept
-        DBuf<uint8_t> f(m, s);
-        GD_KERNEL(k_nonneg_flags, grid_for(m, 256), 256, 0, s, tpos.get() + old, m, f.get());
-        DBuf<int32_t> sel(m, s);
-        select_flagged_index(s, f.get(), m, sel.get());
-        DBuf<int64_t> p2(std::max<int64_t>(killed, 1), s);
-        DBuf<int32_t> r2(std::max<int64_t>(killed, 1), s);
-        if (killed) {
-            GD_KERNEL(k_gather_sel<int64_t>, grid_for(killed, 256), 256, 0, s, tpos.get() + old, sel.get(), killed,
-                      p2.get());
-            GD_KERNEL(k_gather_sel<int32_t>, grid_for(killed, 256), 256, 0, s, trow.get() + old, sel.get(), killed,
-                      r2.get());
-            GD_CUDA(cudaMemcpyAsync(tpos.get() + old, p2.get(), killed * 8, cudaMemcpyDeviceToDevice, s));
-            GD_CUDA(cudaMemcpyAsync(trow.get() + old, r2.get(), killed * 4, cudaMemcpyDeviceToDevice, s));
-        }
-    }
-    int64_t tot = old + killed;
-    // Unweighted: items and entries share the (row, col) order, so the log is
-    // already ascending.  Weighted: parallel arcs of one pair sit in the index
-    // in arrival order, not weight order -- sort.  An older log: sort the union.
-    if (killed && (old || weighted)) {
-        DBuf<uint64_t> pk(tot, s);
-        GD_CUDA(cudaMemcpyAsync(pk.get(), tpos.get(), tot * 8, cudaMemcpyDeviceToDevice, s));
-        sort_pairs_u64(s, pk.get(), trow.get(), tot, bits_for((uint64_t)std::max<int64_t>(ix.nnz, 1)));
-        GD_CUDA(cudaMemcpyAsync(tpos.get(), pk.get(), tot * 8, cudaMemcpyDeviceToDevice, s));
-    }
+    GD_KERNEL(k_index_claim, grid_for(m, 256), 256, 0, s, ka.row.get(), ka.col.get(), ka.w.get(), ka.gid.get(), m,
+              ix.rows_are_dst, ix.off.get(), ix.col.get(), ix.w.n ? ix.w.get() : nullptr, tpos.get() + old,
+              trow.get() + old);
     ix.tpos = std::move(tpos);
     ix.trow = std::move(trow);
-    ix.ntomb = tot;
+    ix.ntomb = old + m;
 }
 
 void Store::index_add(SortedIndex& ix, const AddedArcs& aa) {
@@ -991,18 +946,16 @@ void Store::append_out_tombs(const int64_t* d_pos, const int32_t* d_row, int64_t
     if (!cnt) return;
     cudaStream_t s = stream;
     int64_t tot = notomb + cnt;
-    DBuf<uint64_t> pk(tot, s);
-    DBuf<int32_t> rw(tot, s);
+    DBuf<int64_t> p(tot, s);
+    DBuf<int32_t> r(tot, s);
     if (notomb) {
-        GD_CUDA(cudaMemcpyAsync(pk.get(), otpos.get(), notomb * 8, cudaMemcpyDeviceToDevice, s));
-        GD_CUDA(cudaMemcpyAsync(rw.get(), otrow.get(), notomb * 4, cudaMemcpyDeviceToDevice, s));
+        GD_CUDA(cudaMemcpyAsync(p.get(), otpos.get(), notomb * 8, cudaMemcpyDeviceToDevice, s));
+        GD_CUDA(cudaMemcpyAsync(r.get(), otrow.get(), notomb * 4, cudaMemcpyDeviceToDevice, s));
     }
-    GD_CUDA(cudaMemcpyAsync(pk.get() + notomb, d_pos, cnt * 8, cudaMemcpyDeviceToDevice, s));
-    GD_CUDA(cudaMemcpyAsync(rw.get() + notomb, d_row, cnt * 4, cudaMemcpyDeviceToDevice, s));
-    sort_pairs_u64(s, pk.get(), rw.get(), tot, bits_for((uint64_t)std::max<int64_t>(segs[0].nslots, 1)));
-    otpos.alloc(tot, s);
-    GD_CUDA(cudaMemcpyAsync(otpos.get(), pk.get(), tot * 8, cudaMemcpyDeviceToDevice, s));
-    otrow = std::move(rw);
+    GD_CUDA(cudaMemcpyAsync(p.get() + notomb, d_pos, cnt * 8, cudaMemcpyDeviceToDevice, s));
+    GD_CUDA(cudaMemcpyAsync(r.get() + notomb, d_row, cnt * 4, cudaMemcpyDeviceToDevice, s));
+    otpos = std::move(p);
+    otrow = std::move(r);
     notomb = tot;
 }
 
@@ -1055,8 +1008,13 @@ int64_t Store::apply_deletes(const int32_t* d_src, const int32_t* d_dst, int64_t
     int rb = bits_for((uint64_t)std::max<int64_t>(hv[1], 1));
     const bool one_sort = kb + rb <= 64;  // (pair, chain offset) fits one 64-bit key
     if (!one_sort) rb = 0;
-    // scan chains, collect matches (retry once with the exact size on overflow)
-    int64_t cap = 2 * nrq + 1024;
+    // single-request pairs resolve by atomicMin; the rest collect overflow
+    // matches (retry once with the exact size on overflow)
+    DBuf<uint8_t> single(nrq, s);
+    GD_KERNEL(k_single_flags, grid_for(nrq, 256), 256, 0, s, rq_key.get(), nrq, single.get());
+    DBuf<unsigned long long> sel(nrq, s);
+    GD_CUDA(cudaMemsetAsync(sel.get(), 0xff, nrq * 8, s));
+    int64_t cap = 1024;
     DBuf<uint64_t> m_key;
     DBuf<int32_t> m_gid;
     DBuf<unsigned long long> m_cnt(1, s);
@@ -1065,7 +1023,8 @@ int64_t Store::apply_deletes(const int32_t* d_src, const int32_t* d_dst, int64_t
         m_key.alloc(cap, s);
         m_gid.alloc(cap, s);
         m_cnt.zero(s);
-        MatchOut mo{m_key.get(), m_gid.get(), m_cnt.get(), cap, rb};
+        if (attempt) GD_CUDA(cudaMemsetAsync(sel.get(), 0xff, nrq * 8, s));
+        MatchOut mo{sel.get(), single.get(), m_key.get(), m_gid.get(), m_cnt.get(), cap, rb};
         GD_KERNEL_T("del_scan", 0, k_del_scan_head, grid_for(((nrows + 3) / 4) * 32, 256, 148LL * 32), 256, 0, s,
                     ov, row_first.get(), nrows, rq_key.get(), nrq, sh, mo);
         if (nwork)
@@ -1102,63 +1061,29 @@ int64_t Store::apply_deletes(const int32_t* d_src, const int32_t* d_dst, int64_t
         found = found_local.get();
     }
     GD_CUDA(cudaMemsetAsync(found, 0, k, s));
+    DBuf<unsigned long long> counts(2, s);  // [0] applied records, [1] killed slots
+    counts.zero(s);
     GD_KERNEL(k_del_resolve, grid_for(nrq, 256), 256, 0, s, rq_key.get(), rq_occ.get(), rq_rec.get(),
-              rq_which.get(), nrq, m_key.get(), m_gid.get(), nm, rb, rq_pos.get(), found);
+              rq_which.get(), single.get(), sel.get(), nrq, m_key.get(), m_gid.get(), nm, rb, rq_pos.get(), found,
+              counts.get());
     KilledArcs ka;
     ka.row.alloc(nrq, s);
     ka.col.alloc(nrq, s);
     ka.w.alloc(nrq, s);
-    DBuf<int64_t> kgid(nrq, s);
-    DBuf<unsigned long long> kcnt(1, s);
-    kcnt.zero(s);
+    ka.gid.alloc(nrq, s);
+    ka.count = nrq;
     GD_KERNEL(k_del_kill, grid_for(nrq, 256), 256, 0, s, ov, rq_key.get(), rq_rec.get(), rq_which.get(),
-              rq_pos.get(), nrq, found, sh, ka.row.get(), ka.col.get(), ka.w.get(), kgid.get(), kcnt.get());
-    ka.count = (int64_t)read_scalar(s, kcnt.get());
-    live -= ka.count;
-    // applied = records whose forward arc was found
-    int64_t applied = 0;
-    {
-        DBuf<int32_t> tmp(k, s);
-        applied = select_flagged_index(s, found, k, tmp.get());
-    }
-    // base-segment tombstones (gid < base slots; gid == slot there) -> merge log
-    if (ka.count) {
-        DBuf<uint8_t> bf(ka.count, s);
-        GD_KERNEL(k_select_base_kills, grid_for(ka.count, 256), 256, 0, s, kgid.get(), ka.count, segs[0].nslots,
-                  bf.get());
-        DBuf<int32_t> sel(ka.count, s);
-        int64_t nb = select_flagged_index(s, bf.get(), ka.count, sel.get());
-        if (nb) {
-            DBuf<int64_t> bp(nb, s);
-            DBuf<int32_t> br(nb, s);
-            GD_KERNEL(k_gather_sel<int64_t>, grid_for(nb, 256), 256, 0, s, kgid.get(), sel.get(), nb, bp.get());
-            GD_KERNEL(k_gather_sel<int32_t>, grid_for(nb, 256), 256, 0, s, ka.row.get(), sel.get(), nb, br.get());
-            append_out_tombs(bp.get(), br.get(), nb);
-        }
-    }
+              rq_pos.get(), nrq, found, sh, ka.row.get(), ka.col.get(), ka.w.get(), ka.gid.get(), counts.get() + 1);
+    // the tomb logs take every slot (gid -1 = none; delta-segment gids are
+    // ignored by the merge), unordered: no select, no sort
+    append_out_tombs(ka.gid.get(), ka.row.get(), nrq);
     index_delete(rev, ka);
     if (fwd.built) index_delete(fwd, ka);
-    return applied;
-}
-
-void Store::drop_claimed_tombs() {
-    if (!notomb) return;
-    cudaStream_t s = stream;
-    DBuf<uint8_t> keep(notomb, s);
-    GD_KERNEL(k_tomb_still_dead, grid_for(notomb, 256), 256, 0, s, otpos.get(), notomb, segs[0].col.get(),
-              keep.get());
-    DBuf<int32_t> sel(notomb, s);
-    int64_t m = select_flagged_index(s, keep.get(), notomb, sel.get());
-    if (m == notomb) return;
-    DBuf<int64_t> p(m, s);
-    DBuf<int32_t> r(m, s);
-    if (m) {
-        GD_KERNEL(k_gather_sel<int64_t>, grid_for(m, 256), 256, 0, s, otpos.get(), sel.get(), m, p.get());
-        GD_KERNEL(k_gather_sel<int32_t>, grid_for(m, 256), 256, 0, s, otrow.get(), sel.get(), m, r.get());
-    }
-    otpos = std::move(p);
-    otrow = std::move(r);
-    notomb = m;
+    unsigned long long hc[2];
+    GD_CUDA(cudaMemcpyAsync(hc, counts.get(), sizeof hc, cudaMemcpyDeviceToHost, s));
+    GD_CUDA(cudaStreamSynchronize(s));
+    live -= (int64_t)hc[1];
+    return (int64_t)hc[0];
 }
 
 void Store::apply_adds(const int32_t* d_src, const int32_t* d_dst, const int32_t* d_w, int64_t k) {
@@ -1187,7 +1112,6 @@ void Store::apply_adds(const int32_t* d_src, const int32_t* d_dst, const int32_t
     DBuf<uint8_t> left(na, s);
     GD_KERNEL(k_add_claim, grid_for(na, 256), 256, 0, s, ov, val.get(), aa.col.get(), aa.w.get(), vac.get(), na,
               left.get());
-    drop_claimed_tombs();
     // leftovers (already ordered by (source, stream order)) -> one new delta
     DBuf<int32_t> sel(na, s);
     int64_t nl = select_flagged_index(s, left.get(), na, sel.get());
@@ -1251,8 +1175,8 @@ void Store::merge() {
     OutSeg nb;
     int64_t nnz2 = 0;
     edit_merge(s, n, segs[0].off.get(), segs[0].col.get(), weighted ? segs[0].w.get() : nullptr, segs[0].nslots,
-               otpos.get(), otrow.get(), notomb, irow.get(), icol.get(), weighted ? iw.get() : nullptr, ipos.get(),
-               nins, nb.off, nb.col, nb.w, nnz2, weighted);
+               otpos.get(), otrow.get(), notomb, true, irow.get(), icol.get(), weighted ? iw.get() : nullptr,
+               ipos.get(), nins, nb.off, nb.col, nb.w, nnz2, weighted);
     nb.nslots = nnz2;
     segs.clear();
     segs.push_back(std::move(nb));

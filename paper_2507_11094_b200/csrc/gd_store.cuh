@@ -54,7 +54,7 @@ struct SortedIndex {
     DBuf<int32_t> col;
     DBuf<int32_t> w;
     int64_t nnz = 0;
-    // tombstones since the last compaction, sorted by position
+    // tombstones since the last compaction (unordered; -1 = unused slot)
     DBuf<int64_t> tpos;
     DBuf<int32_t> trow;
     int64_t ntomb = 0;
@@ -65,9 +65,11 @@ struct SortedIndex {
     IdxView view() const { return IdxView{off.get(), col.get(), w.n ? w.get() : nullptr}; }
 };
 
-// Killed out-arcs of one delete call (device), consumed by index upkeep.
+// Killed out-arcs of one delete call (device), one slot per request
+// (gid -1 = nothing killed), consumed by index upkeep and the tomb log.
 struct KilledArcs {
     DBuf<int32_t> row, col, w;
+    DBuf<int64_t> gid;
     int64_t count = 0;
 };
 // Inserted out-arcs of one add call (device).
@@ -115,7 +117,8 @@ class Store {
     int64_t live = 0;
     std::vector<OutSeg> segs;
     SortedIndex rev, fwd;
-    // out-store base tombstones since the last merge (sorted by position)
+    // out-store tombstones since the last merge (unordered global slot ids;
+    // -1 and delta-segment ids are ignored by the merge)
     DBuf<int64_t> otpos;
     DBuf<int32_t> otrow;
     int64_t notomb = 0;
@@ -130,15 +133,16 @@ class Store {
     void index_delete(SortedIndex& ix, const KilledArcs& ka);
     void index_add(SortedIndex& ix, const AddedArcs& aa);
     void append_out_tombs(const int64_t* d_pos, const int32_t* d_row, int64_t cnt);
-    void drop_claimed_tombs();
 };
 
 // Edit-merge compaction shared by the out-store merge and index compaction:
 // copy the live entries of a base array (negative = dead) while inserting
 // sorted items before base positions P (stable), rows re-offset.
-void edit_merge(cudaStream_t s, int64_t n, const int64_t* off, const int32_t* col, const int32_t* w, int64_t nnz,
-                const int64_t* tpos, const int32_t* trow, int64_t ntomb, const int32_t* irow, const int32_t* icol,
-                const int32_t* iw, const int64_t* ipos, int64_t nins, DBuf<int64_t>& new_off,
+// Dead entries are the negative ones, found via an unordered tomb log
+// (dedupe: the out-store may log a slot twice).
+void edit_merge(cudaStream_t s, int64_t n, const int64_t* off, int32_t* col, const int32_t* w, int64_t nnz,
+                const int64_t* tpos, const int32_t* trow, int64_t ntomb, bool dedupe, const int32_t* irow,
+                const int32_t* icol, const int32_t* iw, const int64_t* ipos, int64_t nins, DBuf<int64_t>& new_off,
                 DBuf<int32_t>& new_col, DBuf<int32_t>& new_w, int64_t& new_nnz, bool weighted);
 
 }  // namespace gdb
