@@ -56,27 +56,26 @@ __global__ void k_gather_i32(const int32_t* in, const int32_t* sel, int64_t m, i
 
 }  // namespace
 
-void AlgoBase::split(DevBatch& b, const uint8_t* isdel_isadd, const int32_t* s, const int32_t* d, const int32_t* w,
-                     int64_t k) {
+// Split validated records by kind in stream order.  `hdr` already holds
+// [err, bad index, kdel, kadd] on the host (one sync for all of them).
+void AlgoBase::split(DevBatch& b, const int32_t* sel_del, const int32_t* sel_add, const int32_t* s, const int32_t* d,
+                     const int32_t* w, int64_t kdel, int64_t kadd) {
     cudaStream_t st = stream();
-    const uint8_t* isdel = isdel_isadd;
-    const uint8_t* isadd = isdel_isadd + k;
-    DBuf<int32_t> sel(k, st);
-    b.kdel = select_flagged_index(st, isdel, k, sel.get());
+    b.kdel = kdel;
+    b.kadd = kadd;
     b.ds.alloc(b.kdel, st);
     b.dd.alloc(b.kdel, st);
     if (b.kdel) {
-        GD_KERNEL(k_gather_i32, grid_for(b.kdel, 256), 256, 0, st, s, sel.get(), b.kdel, b.ds.get());
-        GD_KERNEL(k_gather_i32, grid_for(b.kdel, 256), 256, 0, st, d, sel.get(), b.kdel, b.dd.get());
+        GD_KERNEL(k_gather_i32, grid_for(b.kdel, 256), 256, 0, st, s, sel_del, b.kdel, b.ds.get());
+        GD_KERNEL(k_gather_i32, grid_for(b.kdel, 256), 256, 0, st, d, sel_del, b.kdel, b.dd.get());
     }
-    b.kadd = select_flagged_index(st, isadd, k, sel.get());
     b.as.alloc(b.kadd, st);
     b.ad.alloc(b.kadd, st);
     b.aw.alloc(b.kadd, st);
     if (b.kadd) {
-        GD_KERNEL(k_gather_i32, grid_for(b.kadd, 256), 256, 0, st, s, sel.get(), b.kadd, b.as.get());
-        GD_KERNEL(k_gather_i32, grid_for(b.kadd, 256), 256, 0, st, d, sel.get(), b.kadd, b.ad.get());
-        if (w) GD_KERNEL(k_gather_i32, grid_for(b.kadd, 256), 256, 0, st, w, sel.get(), b.kadd, b.aw.get());
+        GD_KERNEL(k_gather_i32, grid_for(b.kadd, 256), 256, 0, st, s, sel_add, b.kadd, b.as.get());
+        GD_KERNEL(k_gather_i32, grid_for(b.kadd, 256), 256, 0, st, d, sel_add, b.kadd, b.ad.get());
+        if (w) GD_KERNEL(k_gather_i32, grid_for(b.kadd, 256), 256, 0, st, w, sel_add, b.kadd, b.aw.get());
         else fill_i32(st, b.aw.get(), b.kadd, 1);
     }
 }
@@ -109,19 +108,25 @@ void AlgoBase::stage_host(DevBatch& b, const uint8_t* kind, const int64_t* src, 
     GD_CUDA(cudaMemcpyAsync(k_stage.get(), kind, k, cudaMemcpyHostToDevice, st));
     DBuf<int32_t> s(k, st), d(k, st), ww(k, st);
     DBuf<uint8_t> flags(2 * k, st);
-    DBuf<int> err(1, st);
-    DBuf<unsigned long long> bad(1, st);
-    err.zero(st);
-    GD_CUDA(cudaMemsetAsync(bad.get(), 0xff, sizeof(unsigned long long), st));
+    DBuf<int64_t> hdr(4, st);  // err, bad index, kdel, kadd
+    GD_CUDA(cudaMemsetAsync(hdr.get(), 0, 8, st));
+    GD_CUDA(cudaMemsetAsync(hdr.get() + 1, 0xff, 8, st));
     GD_KERNEL(k_stage_host, grid_for(k, 256), 256, 0, st, k_stage.get(), h_stage.get(), h_stage.get() + k,
               w ? h_stage.get() + 2 * k : nullptr, k, g->n, s.get(), d.get(), ww.get(), flags.get(),
-              flags.get() + k, err.get(), bad.get());
-    int e = read_scalar(st, err.get());
+              flags.get() + k, reinterpret_cast<int*>(hdr.get()),
+              reinterpret_cast<unsigned long long*>(hdr.get() + 1));
+    DBuf<int32_t> sel_del(k, st), sel_add(k, st);
+    select_flagged_index_async(st, flags.get(), k, sel_del.get(), hdr.get() + 2);
+    select_flagged_index_async(st, flags.get() + k, k, sel_add.get(), hdr.get() + 3);
+    int64_t h[4];
+    GD_CUDA(cudaMemcpyAsync(h, hdr.get(), sizeof h, cudaMemcpyDeviceToHost, st));
+    GD_CUDA(cudaStreamSynchronize(st));
+    int e = (int)(h[0] & 0xffffffff);
     if (e) {
-        unsigned long long i = read_scalar(st, bad.get());
+        unsigned long long i = (unsigned long long)h[1];
         raise_validation(e, i, g->n, (char)kind[i], src[i], dst[i]);
     }
-    split(b, flags.get(), s.get(), d.get(), ww.get(), k);
+    split(b, sel_del.get(), sel_add.get(), s.get(), d.get(), ww.get(), h[2], h[3]);
 }
 
 void AlgoBase::stage_device(DevBatch& b, const uint8_t* kind, const int32_t* src, const int32_t* dst,
@@ -132,19 +137,24 @@ void AlgoBase::stage_device(DevBatch& b, const uint8_t* kind, const int32_t* src
         return;
     }
     DBuf<uint8_t> flags(2 * k, st);
-    DBuf<int> err(1, st);
-    DBuf<unsigned long long> bad(1, st);
-    err.zero(st);
-    GD_CUDA(cudaMemsetAsync(bad.get(), 0xff, sizeof(unsigned long long), st));
+    DBuf<int64_t> hdr(4, st);  // err, bad index, kdel, kadd
+    GD_CUDA(cudaMemsetAsync(hdr.get(), 0, 8, st));
+    GD_CUDA(cudaMemsetAsync(hdr.get() + 1, 0xff, 8, st));
     GD_KERNEL(k_stage_dev, grid_for(k, 256), 256, 0, st, kind, src, dst, k, g->n, flags.get(), flags.get() + k,
-              err.get(), bad.get());
-    int e = read_scalar(st, err.get());
+              reinterpret_cast<int*>(hdr.get()), reinterpret_cast<unsigned long long*>(hdr.get() + 1));
+    DBuf<int32_t> sel_del(k, st), sel_add(k, st);
+    select_flagged_index_async(st, flags.get(), k, sel_del.get(), hdr.get() + 2);
+    select_flagged_index_async(st, flags.get() + k, k, sel_add.get(), hdr.get() + 3);
+    int64_t h[4];
+    GD_CUDA(cudaMemcpyAsync(h, hdr.get(), sizeof h, cudaMemcpyDeviceToHost, st));
+    GD_CUDA(cudaStreamSynchronize(st));
+    int e = (int)(h[0] & 0xffffffff);
     if (e) {
-        unsigned long long i = read_scalar(st, bad.get());
+        unsigned long long i = (unsigned long long)h[1];
         raise_validation(e, i, g->n, (char)read_scalar(st, kind + i), read_scalar(st, src + i),
                          read_scalar(st, dst + i));
     }
-    split(b, flags.get(), src, dst, w, k);
+    split(b, sel_del.get(), sel_add.get(), src, dst, w, h[2], h[3]);
 }
 
 // ---------------------------------------------------------------- degrees ---

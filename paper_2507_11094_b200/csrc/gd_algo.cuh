@@ -41,7 +41,8 @@ struct AlgoBase {
                       int64_t k);
 
   private:
-    void split(DevBatch& b, const uint8_t* kind, const int32_t* s, const int32_t* d, const int32_t* w, int64_t k);
+    void split(DevBatch& b, const int32_t* sel_del, const int32_t* sel_add, const int32_t* s, const int32_t* d,
+               const int32_t* w, int64_t kdel, int64_t kadd);
     DBuf<int64_t> h_stage;  // reusable device staging for host uploads
     DBuf<uint8_t> k_stage;
 };

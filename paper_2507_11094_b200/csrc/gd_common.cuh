@@ -163,6 +163,8 @@ void inclusive_scan_i64(cudaStream_t s, const int64_t* in, int64_t* out, int64_t
 int64_t sum_i64(cudaStream_t s, const int64_t* in, int64_t n);  // synchronous result
 // Compact indices i in [0, n) with flags[i] != 0 into out (ordered); returns count (sync).
 int64_t select_flagged_index(cudaStream_t s, const uint8_t* flags, int64_t n, int32_t* out);
+// Same, count left in device memory (no sync).
+void select_flagged_index_async(cudaStream_t s, const uint8_t* flags, int64_t n, int32_t* out, int64_t* d_count);
 // Stable 3-way split of a vertex list by row length (off[v+1]-off[v]):
 // <= t1, <= t2, rest (rest in reverse order).  d_counts[0..1] = sizes of the
 // first two parts (device; asynchronous).

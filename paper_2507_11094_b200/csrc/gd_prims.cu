@@ -126,6 +126,19 @@ void partition3_by_degree(cudaStream_t s, const int32_t* list, int64_t m, const 
     count_library_launch();
 }
 
+void select_flagged_index_async(cudaStream_t s, const uint8_t* flags, int64_t n, int32_t* out, int64_t* d_count) {
+    if (n <= 0) {
+        GD_CUDA(cudaMemsetAsync(d_count, 0, sizeof(int64_t), s));
+        return;
+    }
+    thrust::counting_iterator<int32_t> it(0);
+    size_t bytes = 0;
+    GD_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, it, flags, out, d_count, n, s));
+    Temp t(bytes, s);
+    GD_CUDA(cub::DeviceSelect::Flagged(t.p, bytes, it, flags, out, d_count, n, s));
+    count_library_launch();
+}
+
 __global__ void k_iota_i32(int32_t* a, int64_t n) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         a[i] = static_cast<int32_t>(i);

@@ -203,7 +203,10 @@ __global__ void k_on_add(const int32_t* s, const int32_t* d, const int32_t* w, i
                          int64_t* dist, uint8_t* seed) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < k; i += (int64_t)gridDim.x * blockDim.x) {
         int32_t t = d[i];
-        int64_t c = sat_add(dist[s[i]], weighted ? (int64_t)w[i] : 1);
+        // the record's own weight, as the reference's OnAdd reads e.weight of
+        // the batch record (interp.py:624-629), weighted graph or not
+        int64_t c = sat_add(dist[s[i]], (int64_t)w[i]);
+        (void)weighted;
         if (c < dist[t]) {
             long long old = atomicMin(reinterpret_cast<long long*>(&dist[t]), (long long)c);
             if (c < old) seed[t] = 1;

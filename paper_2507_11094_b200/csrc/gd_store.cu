@@ -159,9 +159,10 @@ constexpr int kHead = 256;
 constexpr int kScanWarps = 8;
 constexpr int kBitmapWords = 1024;  // 32 Kbit per warp
 
-__global__ void k_row_chunks(OutView ov, const uint64_t* rq_key, const int32_t* row_first, int64_t nrows, int sh,
-                             int64_t* chunks, unsigned long long* maxlen) {
+__global__ void k_row_chunks(OutView ov, const uint64_t* rq_key, const int32_t* row_first, const int64_t* d_nrows,
+                             int sh, int64_t* chunks, unsigned long long* maxlen) {
     unsigned long long mx = 0;
+    const int64_t nrows = *d_nrows;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nrows; i += (int64_t)gridDim.x * blockDim.x) {
         int32_t row = key_row(rq_key[row_first[i]], sh);
         int64_t len = 0;
@@ -408,9 +409,10 @@ __global__ void k_add_arcs(const int32_t* s, const int32_t* d, const int32_t* w,
 
 // One warp per source row with inserts: list the first `want` vacancies of
 // the chain in slot order (ballot + prefix keeps the order).
-__global__ void k_add_vacancies(OutView ov, const uint32_t* skey, const int32_t* row_first, int64_t nrows,
+__global__ void k_add_vacancies(OutView ov, const uint32_t* skey, const int32_t* row_first, const int64_t* d_nrows,
                                 int64_t narcs, int64_t* vac_gid) {
     const int lane = threadIdx.x & 31;
+    const int64_t nrows = *d_nrows;
     int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t r = warp; r < nrows; r += nwarps) {
@@ -779,21 +781,45 @@ Store::~Store() {
     }
 }
 
+namespace {
+constexpr int kTabMax = 16;
+struct SegTable {
+    uintptr_t v[4 * kTabMax];
+};
+__global__ void k_set_table(SegTable t, int k, uintptr_t* tab) {
+    for (int i = threadIdx.x; i < 4 * k; i += blockDim.x) tab[i] = t.v[(i / k) * kTabMax + (i % k)];
+}
+}  // namespace
+
 void Store::upload_tables() {
     size_t k = segs.size();
-    // the previous copy may still be in flight: wait before reusing the host table
-    if (tab_k) GD_CUDA(cudaStreamSynchronize(stream));
-    h_tab.assign(4 * k, 0);
-    int64_t acc = 0;
-    for (size_t i = 0; i < k; ++i) {
-        h_tab[i] = reinterpret_cast<uintptr_t>(segs[i].off.get());
-        h_tab[k + i] = reinterpret_cast<uintptr_t>(segs[i].col.get());
-        h_tab[2 * k + i] = reinterpret_cast<uintptr_t>(segs[i].w.n ? segs[i].w.get() : nullptr);
-        h_tab[3 * k + i] = (uintptr_t)acc;
-        acc += segs[i].nslots;
-    }
     tab.ensure(4 * k, stream);
-    GD_CUDA(cudaMemcpyAsync(tab.get(), h_tab.data(), 4 * k * sizeof(uintptr_t), cudaMemcpyHostToDevice, stream));
+    if (k <= (size_t)kTabMax) {  // by value through a kernel: no host buffer to keep alive
+        SegTable t{};
+        int64_t acc = 0;
+        for (size_t i = 0; i < k; ++i) {
+            t.v[i] = reinterpret_cast<uintptr_t>(segs[i].off.get());
+            t.v[kTabMax + i] = reinterpret_cast<uintptr_t>(segs[i].col.get());
+            t.v[2 * kTabMax + i] = reinterpret_cast<uintptr_t>(segs[i].w.n ? segs[i].w.get() : nullptr);
+            t.v[3 * kTabMax + i] = (uintptr_t)acc;
+            acc += segs[i].nslots;
+        }
+        GD_KERNEL(k_set_table, 1, 64, 0, stream, t, (int)k, tab.get());
+    } else {
+        // the previous copy may still be in flight: wait before reusing the host table
+        GD_CUDA(cudaStreamSynchronize(stream));
+        h_tab.assign(4 * k, 0);
+        int64_t acc = 0;
+        for (size_t i = 0; i < k; ++i) {
+            h_tab[i] = reinterpret_cast<uintptr_t>(segs[i].off.get());
+            h_tab[k + i] = reinterpret_cast<uintptr_t>(segs[i].col.get());
+            h_tab[2 * k + i] = reinterpret_cast<uintptr_t>(segs[i].w.n ? segs[i].w.get() : nullptr);
+            h_tab[3 * k + i] = (uintptr_t)acc;
+            acc += segs[i].nslots;
+        }
+        GD_CUDA(cudaMemcpyAsync(tab.get(), h_tab.data(), 4 * k * sizeof(uintptr_t), cudaMemcpyHostToDevice,
+                                stream));
+    }
     tab_k = k;
 }
 
@@ -964,6 +990,7 @@ int64_t Store::apply_deletes(const int32_t* d_src, const int32_t* d_dst, int64_t
     if (k == 0) return 0;
     if (rev.built) compact_index(rev);
     if (fwd.built) compact_index(fwd);
+    first_clean_delta = segs.size();  // deltas made before this delete may now hold tombstones
     const int kb = 2 * sh;
     DBuf<uint64_t> skey(k, s);
     DBuf<int32_t> srec(k, s);
@@ -991,19 +1018,23 @@ int64_t Store::apply_deletes(const int32_t* d_src, const int32_t* d_dst, int64_t
     DBuf<uint8_t> rflag(nrq, s);
     GD_KERNEL(k_row_starts, grid_for(nrq, 256), 256, 0, s, rq_key.get(), nrq, sh, rflag.get());
     DBuf<int32_t> row_first(nrq, s);
-    int64_t nrows = select_flagged_index(s, rflag.get(), nrq, row_first.get());
+    DBuf<int64_t> hdr(3, s);  // nrows, work items, longest chain
+    select_flagged_index_async(s, rflag.get(), nrq, row_first.get(), hdr.get());
     OutView ov = out_view();
-    DBuf<int64_t> chunks(nrows + 1, s), coff(nrows + 1, s);
+    DBuf<int64_t> chunks(nrq + 1, s), coff(nrq + 1, s);
     DBuf<unsigned long long> maxlen(1, s);
     maxlen.zero(s);
-    GD_KERNEL(k_row_chunks, grid_for(nrows, 256), 256, 0, s, ov, rq_key.get(), row_first.get(), nrows, sh,
+    chunks.zero(s);
+    GD_KERNEL(k_row_chunks, grid_for(nrq, 256), 256, 0, s, ov, rq_key.get(), row_first.get(), hdr.get(), sh,
               chunks.get(), maxlen.get());
-    GD_CUDA(cudaMemsetAsync(chunks.get() + nrows, 0, 8, s));
-    exclusive_scan_i64(s, chunks.get(), coff.get(), nrows + 1);
-    int64_t hv[2];
-    GD_CUDA(cudaMemcpyAsync(&hv[0], coff.get() + nrows, 8, cudaMemcpyDeviceToHost, s));
-    GD_CUDA(cudaMemcpyAsync(&hv[1], maxlen.get(), 8, cudaMemcpyDeviceToHost, s));
+    exclusive_scan_i64(s, chunks.get(), coff.get(), nrq + 1);
+    GD_CUDA(cudaMemcpyAsync(hdr.get() + 1, coff.get() + nrq, 8, cudaMemcpyDeviceToDevice, s));
+    GD_CUDA(cudaMemcpyAsync(hdr.get() + 2, maxlen.get(), 8, cudaMemcpyDeviceToDevice, s));
+    int64_t hv3[3];
+    GD_CUDA(cudaMemcpyAsync(hv3, hdr.get(), sizeof hv3, cudaMemcpyDeviceToHost, s));
     GD_CUDA(cudaStreamSynchronize(s));
+    const int64_t nrows = hv3[0];
+    int64_t hv[2] = {hv3[1], hv3[2]};
     int64_t nwork = hv[0];
     int rb = bits_for((uint64_t)std::max<int64_t>(hv[1], 1));
     const bool one_sort = kb + rb <= 64;  // (pair, chain offset) fits one 64-bit key
@@ -1103,12 +1134,13 @@ void Store::apply_adds(const int32_t* d_src, const int32_t* d_dst, const int32_t
     DBuf<uint8_t> rflag(na, s);
     GD_KERNEL(k_row_starts_u32, grid_for(na, 256), 256, 0, s, key.get(), na, rflag.get());
     DBuf<int32_t> row_first(na, s);
-    int64_t nrows = select_flagged_index(s, rflag.get(), na, row_first.get());
+    DBuf<int64_t> d_nrows(1, s);
+    select_flagged_index_async(s, rflag.get(), na, row_first.get(), d_nrows.get());
     DBuf<int64_t> vac(na, s);
     fill_i64(s, vac.get(), na, -1);
     OutView ov = out_view();
-    GD_KERNEL_T("add_vacancies", 0, k_add_vacancies, grid_for(nrows * 32, 256, 148LL * 32), 256, 0, s, ov,
-                key.get(), row_first.get(), nrows, na, vac.get());
+    GD_KERNEL_T("add_vacancies", 0, k_add_vacancies, grid_for(na * 32, 256, 148LL * 32), 256, 0, s, ov, key.get(),
+                row_first.get(), d_nrows.get(), na, vac.get());
     DBuf<uint8_t> left(na, s);
     GD_KERNEL(k_add_claim, grid_for(na, 256), 256, 0, s, ov, val.get(), aa.col.get(), aa.w.get(), vac.get(), na,
               left.get());
@@ -1146,6 +1178,14 @@ void Store::merge() {
         DBuf<uint8_t> lf(d.nslots, s);
         GD_KERNEL(k_delta_rows, grid_for(d.nslots, 256), 256, 0, s, d.off.get(), n, d.col.get(), d.nslots,
                   row.get(), lf.get());
+        if (i >= first_clean_delta) {  // no delete phase since it was made: every slot is live
+            GD_CUDA(cudaMemcpyAsync(irow.get() + nins, row.get(), d.nslots * 4, cudaMemcpyDeviceToDevice, s));
+            GD_CUDA(cudaMemcpyAsync(icol.get() + nins, d.col.get(), d.nslots * 4, cudaMemcpyDeviceToDevice, s));
+            if (weighted)
+                GD_CUDA(cudaMemcpyAsync(iw.get() + nins, d.w.get(), d.nslots * 4, cudaMemcpyDeviceToDevice, s));
+            nins += d.nslots;
+            continue;
+        }
         DBuf<int32_t> sel(d.nslots, s);
         int64_t c = select_flagged_index(s, lf.get(), d.nslots, sel.get());
         if (!c) continue;
@@ -1185,6 +1225,7 @@ void Store::merge() {
     otrow.release();
     notomb = 0;
     live = nnz2;
+    first_clean_delta = 1;
     if (rev.built) compact_index(rev);
     if (fwd.built) compact_index(fwd);
 }

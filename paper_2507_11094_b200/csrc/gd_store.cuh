@@ -122,6 +122,7 @@ class Store {
     DBuf<int64_t> otpos;
     DBuf<int32_t> otrow;
     int64_t notomb = 0;
+    size_t first_clean_delta = 1;  // deltas from this index on have seen no delete phase
 
   private:
     // segment table on the device: [off ptrs | col ptrs | w ptrs | bases]
