@@ -1,0 +1,143 @@
+"""Parity at BASELINE sizes.
+
+* configs[0] (SSSP, R-MAT-16, 1M edges, one 5% batch) and a 1% batch of
+  configs[1] (PR, R-MAT-22, 2^26 edges) are checked against the reference's
+  OWN emitted OpenMP drivers (oracle/_ref/libgdref.so, built from
+  /root/reference) on identical inputs: SSSP dist + parent exact, PR max-abs
+  <= 1e-6.
+* Size-independent properties where the reference cannot run in minutes:
+  dynamic == static on the final graph (SSSP distances and a valid
+  shortest-path tree; triangle counts on simple graphs).
+"""
+
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+INF = np.iinfo(np.int64).max
+
+
+@pytest.fixture(scope="module")
+def gd():
+    import paper_2507_11094_b200 as gd
+
+    return gd
+
+
+def ref_available():
+    from oracle import oracle as O
+
+    return O.ref_available()
+
+
+def final_edges(g):
+    """Live arcs of a store in neighbors() order (export)."""
+    rows, cols, wts = [], [], []
+    for seg in g.segments():
+        cnt = np.diff(seg.offsets)
+        r = np.repeat(np.arange(g.node_count, dtype=np.int64), cnt)
+        live = seg.coordinates != np.iinfo(np.int64).max
+        rows.append(r[live])
+        cols.append(seg.coordinates[live])
+        wts.append(seg.weights[live] if seg.weights is not None else np.ones(int(live.sum()), np.int64))
+    return np.concatenate(rows), np.concatenate(cols), np.concatenate(wts)
+
+
+def tree_valid(dist, parent, src, s, d, w):
+    """Every reachable v != src has a parent arc closing its distance."""
+    key = s * (1 << 32) + d
+    order = np.argsort(key, kind="stable")
+    ks, ws = key[order], w[order]
+    reach = (dist < INF) & (np.arange(len(dist)) != src)
+    assert np.all(parent[~reach] == -1)
+    v = np.flatnonzero(reach)
+    p = parent[v]
+    assert np.all(p >= 0)
+    q = p * (1 << 32) + v
+    lo = np.searchsorted(ks, q, side="left")
+    hi = np.searchsorted(ks, q, side="right")
+    ok = np.zeros(len(v), dtype=bool)
+    for j in range(int((hi - lo).max()) if len(v) else 0):  # parallel arcs: any weight may close it
+        idx = np.minimum(lo + j, len(ks) - 1)
+        ok |= (lo + j < hi) & (dist[p] + ws[idx] == dist[v])
+    assert ok.all()
+
+
+@pytest.mark.skipif(not ref_available(), reason="oracle/_ref not built (needs /root/reference at build time)")
+def test_c1_sssp_matches_reference_emitted_openmp(gd):
+    """BASELINE configs[0]: R-MAT-16, 1M edges, w 1-100, one 5% batch, src 0."""
+    from oracle import oracle as O
+    from paper_2507_11094_b200 import generate as G
+
+    s, d, w, n = G.rmat(16, 1_000_000, seed=16, weighted=True, max_weight=100)
+    kind, us, ud, uw, per = G.updates(s, d, n, percent=5, batches=1, seed=17, max_weight=100)
+    (rd, rp), _ = O.ref_run("sssp", n, s, d, w, weighted=True, kind=kind, us=us, ud=ud, uw=uw, batch_size=per,
+                            threads=os.cpu_count() or 1, skip_t0=True)
+    g = gd.DynamicGraph.from_arrays(n, s, d, w, weighted=True, with_reverse=True)
+    ctx = gd.run_batches(gd.compile_source("Dynamic dynamicSSSP("), g, gd.UpdateStream.from_arrays(kind, us, ud, uw),
+                         per, {"src": 0})
+    np.testing.assert_array_equal(ctx.properties["dist"].values(), rd)
+    np.testing.assert_array_equal(ctx.properties["parent"].values(), rp)
+
+
+@pytest.mark.slow
+@pytest.mark.skipif(not ref_available(), reason="oracle/_ref not built")
+def test_c2_pagerank_batch_matches_reference_emitted_openmp(gd):
+    """BASELINE configs[1] graph (R-MAT-22, 2^26 edges), one 1% batch."""
+    from oracle import oracle as O
+    from paper_2507_11094_b200 import generate as G
+
+    s, d, w, n = G.rmat(22, 1 << 26, seed=22)
+    kind, us, ud, uw, per = G.updates(s, d, n, percent=1, batches=1, seed=23)
+    for beta in (1e-3,):
+        ref, _ = O.ref_run("pr", n, s, d, None, kind=kind, us=us, ud=ud, uw=uw, batch_size=per,
+                           threads=os.cpu_count() or 1, beta=beta, skip_t0=True)
+        g = gd.DynamicGraph.from_arrays(n, s, d, with_reverse=True)
+        ctx = gd.run_batches(gd.compile_source("Dynamic dynamicPR("), g,
+                             gd.UpdateStream.from_arrays(kind, us, ud, uw), per,
+                             {"damping": 0.85, "beta": beta, "maxiter": 100})
+        got = ctx.properties["pagerank"].data
+        err = np.abs(got - ref)
+        assert err.max() <= 1e-6, err.max()
+        rel = err[ref > 0] / ref[ref > 0]
+        print(f"PR C2 beta={beta}: max-abs {err.max():.3e}, max-rel {rel.max():.3e}")
+
+
+@pytest.mark.parametrize("graph,scale,pct,nbatch", [("rmat", 18, 5, 4), ("grid", 300, 5, 3)])
+def test_sssp_dynamic_equals_static_on_final_graph(gd, graph, scale, pct, nbatch):
+    from paper_2507_11094_b200 import generate as G
+
+    if graph == "rmat":
+        s, d, w, n = G.rmat(scale, 16 << scale, seed=scale, weighted=True, max_weight=100)
+    else:
+        s, d, w, n = G.grid(scale, scale, seed=5)
+    kind, us, ud, uw, per = G.updates(s, d, n, percent=pct, batches=nbatch, seed=9, max_weight=100)
+    g = gd.DynamicGraph.from_arrays(n, s, d, w, weighted=True, with_reverse=True)
+    ctx = gd.run_batches(gd.compile_source("Dynamic dynamicSSSP("), g, gd.UpdateStream.from_arrays(kind, us, ud, uw),
+                         per, {"src": 0})
+    dist = np.asarray(ctx.properties["dist"].data)
+    parent = np.asarray(ctx.properties["parent"].data)
+    fs, fd, fw = final_edges(g)
+    g2 = gd.DynamicGraph.from_arrays(n, fs, fd, fw, weighted=True, with_reverse=True)
+    st = gd.run_program(gd.compile_source("Dynamic dynamicSSSP("), g2, {"src": 0}, entry="staticSSSP")
+    np.testing.assert_array_equal(dist, st.properties["dist"].data)
+    tree_valid(dist, parent, 0, fs, fd, fw)
+
+
+@pytest.mark.parametrize("n,m,pct", [(1 << 18, 4_000_000, 5), (1 << 20, 16_000_000, 1)])
+def test_tc_dynamic_equals_static_on_final_graph(gd, n, m, pct):
+    from paper_2507_11094_b200 import generate as G
+
+    s, d, _, n = G.uniform(n, m, seed=3, undirected=True)
+    kind, us, ud, uw, per = G.updates(s, d, n, percent=pct, batches=2, seed=4, undirected=True)
+    g = gd.DynamicGraph.from_arrays(n, s, d, directed=False)
+    ctx = gd.run_batches(gd.compile_source("Dynamic dynamicTC("), g, gd.UpdateStream.from_arrays(kind, us, ud, uw),
+                         per, {})
+    fs, fd, fw = final_edges(g)
+    keep = fs < fd  # each undirected edge once
+    g2 = gd.DynamicGraph.from_arrays(n, fs[keep], fd[keep], directed=False)
+    st = gd.run_program(gd.compile_source("Dynamic dynamicTC("), g2, {}, entry="staticTC")
+    assert ctx.return_value == st.return_value
