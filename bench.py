@@ -12,9 +12,11 @@ flood, incremental PageRank to convergence.
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                   [--workload pr|sssp|tc|sssp-grid]
 
-Under torchrun (N>1) every rank runs its own replica of the workload (weak
-scaling; vertex-range sharding is future work); timing is the
-max over ranks.  `--impl reference` times the reference's own emitted OpenMP
+Under torchrun (N>1): PR and TC run ONE job over all GPUs -- every rank
+holds a replica of the store and applies every batch, PR pulls only its
+destination range and all-gathers the rank vector over NCCL each sweep, TC
+counts a 1/N slice of the records and all-reduces (strong scaling); SSSP
+runs independent replicas (weak scaling).  Timing is the max over ranks.  `--impl reference` times the reference's own emitted OpenMP
 driver (oracle/_ref/libgdref.so, compiled from /root/reference) on the host
 cores -- rank 0 only.
 """
@@ -216,11 +218,11 @@ def main():
     import torch
 
     dist_on = world > 1
+    torch.cuda.set_device(local)
     if dist_on:
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    torch.cuda.set_device(local)
     import paper_2507_11094_b200 as gd
 
     e2e_steps = args.e2e_steps if args.e2e_steps is not None else max(1, min(args.steps, 5))
@@ -239,6 +241,12 @@ def main():
         algo = gd.TCHandle(g)
     torch.cuda.synchronize()
     log(f"[bench] store + static pass: {time.time() - t:.1f}s; device bytes {g.device_bytes() / 2**30:.2f} GiB")
+    sharded = dist_on and wl["algo"] in ("pr", "tc")
+    if sharded:  # vertex-range PR pull + NCCL all-gather / record-sliced TC + all-reduce
+        from paper_2507_11094_b200.dist import Communicator
+
+        comm = Communicator.from_torch_distributed(local)
+        comm.attach(algo)
 
     # records resident in HBM for the device-path steps (int32 ids, uint8 kind)
     dk = torch.from_numpy(kind).to(f"cuda:{local}")
@@ -327,9 +335,11 @@ def main():
         tt = torch.tensor([e2e_ms], device=f"cuda:{local}")
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
         e2e_ms = float(tt.item())
-    e2e_value = (e_done * world) / (e2e_ms / 1e3) if e2e_ms > 0 else None
+    e2e_value = (e_done * (1 if (dist_on and wl["algo"] in ("pr", "tc")) else world)) / (e2e_ms / 1e3) \
+        if e2e_ms > 0 else None
 
-    value = (done * world) / (elapsed_ms / 1e3)
+    shards = dist_on and wl["algo"] in ("pr", "tc")  # one job over all GPUs vs independent replicas
+    value = (done * (1 if shards else world)) / (elapsed_ms / 1e3)
     peak, peak_kind = load_peaks()
     dom = max(kstats.items(), key=lambda kv: kv[1][0]) if kstats else None
     roof = None
@@ -358,8 +368,8 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": _dtype(wl), "data": "synthetic",
-            "config": _config(wl, args, world),
+            "scaling": "strong" if shards else "weak", "vs_baseline": None, "dtype": _dtype(wl),
+            "data": "synthetic", "config": _config(wl, args, world),
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d // max(e2e_steps, 1),
                     "d2h_bytes_per_step": d2h // max(e2e_steps, 1), "steps": e2e_steps,
                     "ms_per_step": e2e_ms / max(e2e_steps, 1)},
@@ -432,7 +442,10 @@ def _dtype(wl):
 
 def _config(wl, args, world):
     c = {"workload": wl["desc"], "algo": wl["algo"], "batch_percent": wl["percent"], "merge_interval": 1,
-         "parallelism": "replicas" if world > 1 else "single-gpu",
+         "parallelism": ("single-gpu" if world == 1 else
+                         "replicated store, PR pull by dst range + NCCL all-gather" if wl["algo"] == "pr" else
+                         "replicated store, TC record slices + NCCL all-reduce" if wl["algo"] == "tc" else
+                         "replicas"),
          "l2": "inputs larger than L2 (graph store >> 126 MB L2)"}
     if wl["algo"] == "pr":
         c.update({"damping": 0.85, "beta": 1e-3, "maxiter": 100})

@@ -58,6 +58,7 @@ typedef struct gd_graph gd_graph;
 typedef struct gd_sssp gd_sssp;
 typedef struct gd_pr gd_pr;
 typedef struct gd_tc gd_tc;
+typedef struct gd_comm gd_comm;
 
 /* Last error message of the calling thread ("" when none). */
 GD_API const char* gd_last_error(void);
@@ -143,6 +144,20 @@ GD_API int gd_tc_batch_device(gd_tc* t, const uint8_t* kind, const int32_t* src,
                        int64_t k, int64_t batch_index);
 GD_API int gd_tc_read(gd_tc* t, int64_t* count);
 GD_API int gd_tc_destroy(gd_tc* t);
+
+/* ---- multi-GPU (one process per GPU).  NCCL is loaded on
+ *      first use.  Rank 0 makes the id, the caller broadcasts the 128 bytes
+ *      (e.g. torch.distributed), every rank creates its communicator.  Stores
+ *      are replicas (each rank applies every batch); a PR handle with a comm
+ *      pulls only its destination range and all-gathers the rank vector each
+ *      sweep (all-reduce max of the residual); a TC handle counts a 1/world
+ *      slice of each phase's records and all-reduces the count delta.  The
+ *      reference has no multi-process path (partition.py simulates one). */
+GD_API int gd_comm_unique_id(uint8_t id[128]);
+GD_API int gd_comm_create(int world, int rank, const uint8_t id[128], int device, gd_comm** out);
+GD_API int gd_comm_destroy(gd_comm* c);
+GD_API int gd_pr_set_comm(gd_pr* p, gd_comm* c);
+GD_API int gd_tc_set_comm(gd_tc* t, gd_comm* c);
 
 /* ---- reporting (ExecContext.phase_totals / fixedpoint_iterations,
  *      engine/interp.py:112-145); h is any gd_sssp* / gd_pr* / gd_tc* ---- */

@@ -62,6 +62,11 @@ SIGNATURES = [
     ("gd_tc_batch_device", C.c_int, [vp, vp, vp, vp, vp, i64, i64]),
     ("gd_tc_read", C.c_int, [vp, i64p]),
     ("gd_tc_destroy", C.c_int, [vp]),
+    ("gd_comm_unique_id", C.c_int, [vp]),
+    ("gd_comm_create", C.c_int, [C.c_int, C.c_int, vp, C.c_int, C.POINTER(vp)]),
+    ("gd_comm_destroy", C.c_int, [vp]),
+    ("gd_pr_set_comm", C.c_int, [vp, vp]),
+    ("gd_tc_set_comm", C.c_int, [vp, vp]),
     ("gd_phase_times", C.c_int, [vp, f64p]),
     ("gd_iterations", C.c_int, [vp, i64p]),
     ("gd_kernel_time", C.c_int, [vp, C.c_char_p, f64p, i64p, i64p]),

@@ -23,6 +23,9 @@ struct gd_pr {
 struct gd_tc {
     gdb::TC* a;
 };
+struct gd_comm {
+    gdb::Comm* c;
+};
 
 namespace gdb {
 
@@ -450,6 +453,41 @@ int gd_tc_destroy(gd_tc* t) {
         delete t->a;
         delete t;
     });
+}
+
+int gd_comm_unique_id(uint8_t id[128]) {
+    return guard([&] { gdb::comm_unique_id(id); });
+}
+int gd_comm_create(int world, int rank, const uint8_t id[128], int device, gd_comm** out) {
+    return guard([&] {
+        if (!out) throw gdb::GdError(GD_ERR_CONTRACT, "null output handle");
+        auto* h = new gd_comm{nullptr};
+        try {
+            h->c = gdb::comm_create(world, rank, id, device);
+        } catch (...) {
+            delete h;
+            throw;
+        }
+        *out = h;
+    });
+}
+int gd_comm_destroy(gd_comm* c) {
+    if (!c) return ok();
+    return guard([&] {
+        gdb::comm_destroy(c->c);
+        delete c;
+    });
+}
+int gd_pr_set_comm(gd_pr* p, gd_comm* c) {
+    if (!p) return null_handle();
+    return guard([&] {
+        GD_CUDA(cudaSetDevice(p->a->g->device));
+        p->a->set_comm(c ? c->c : nullptr);
+    });
+}
+int gd_tc_set_comm(gd_tc* t, gd_comm* c) {
+    if (!t) return null_handle();
+    return guard([&] { t->a->comm = c ? c->c : nullptr; });
 }
 
 int gd_phase_times(const void* h, double ms[5]) {

@@ -218,9 +218,44 @@ PR::PR(Store* st, double d, double b, int64_t mi) : AlgoBase(ALGO_PR, st), dampi
     prof.flush();
 }
 
+namespace {
+__global__ void k_range_bounds(const int32_t* list, int64_t m, int32_t lo, int32_t hi, int64_t* out) {
+    if (threadIdx.x == 0) out[0] = lower_bound_dev<int32_t>(list, 0, m, lo);
+    if (threadIdx.x == 1) out[1] = lower_bound_dev<int32_t>(list, 0, m, hi);
+}
+}  // namespace
+
+void PR::set_comm(Comm* c) {
+    cudaStream_t s = stream();
+    int64_t n = g->n;
+    comm = c;
+    if (!c) return;
+    // rank / rank_new padded to chunk * world for the in-place all-gather
+    int64_t npad = std::max<int64_t>(c->chunk(n) * c->world, 1);
+    DBuf<double> r2(npad, s), n2(npad, s);
+    r2.zero(s);
+    n2.zero(s);
+    if (n) {
+        GD_CUDA(cudaMemcpyAsync(r2.get(), rank.get(), n * 8, cudaMemcpyDeviceToDevice, s));
+        GD_CUDA(cudaMemcpyAsync(n2.get(), rank_new.get(), n * 8, cudaMemcpyDeviceToDevice, s));
+    }
+    rank = std::move(r2);
+    rank_new = std::move(n2);
+    GD_CUDA(cudaStreamSynchronize(s));
+}
+
 void PR::set_lists(const int32_t* list, int64_t m) {
     cudaStream_t s = stream();
     g->compact_rev();
+    if (comm && m) {  // the list is ascending: keep the owned destination range
+        DBuf<int64_t> b(2, s);
+        GD_KERNEL(k_range_bounds, 1, 32, 0, s, list, m, (int32_t)comm->lo(g->n), (int32_t)comm->hi(g->n), b.get());
+        int64_t hb[2];
+        GD_CUDA(cudaMemcpyAsync(hb, b.get(), sizeof hb, cudaMemcpyDeviceToHost, s));
+        GD_CUDA(cudaStreamSynchronize(s));
+        list += hb[0];
+        m = hb[1] - hb[0];
+    }
     for (auto* l : {&bins[0], &bins[1], &bins[2]}) l->ensure(std::max<int64_t>(m, 1), s);
     nbin[0] = nbin[1] = nbin[2] = 0;
     ebin[0] = ebin[1] = ebin[2] = 0;
@@ -278,6 +313,10 @@ void PR::power_loop() {
             if (nbin[k])
                 GD_KERNEL(k_pr_commit, grid_for(nbin[k], 256), 256, 0, s, bins[k].get(), nbin[k], rank_new.get(),
                           rank.get());
+        if (comm) {  // every rank gets every owned range; the residual is the max over ranks
+            comm->allgather_f64(rank.get(), comm->chunk(n), s);
+            comm->allreduce_max_f64(scal.get() + 1, 1, s);
+        }
         diff = read_scalar(s, scal.get() + 1);
         ++iter;
     }

@@ -2,6 +2,7 @@
 #pragma once
 
 #include "gd_algo.cuh"
+#include "gd_comm.cuh"
 
 namespace gdb {
 
@@ -16,7 +17,10 @@ struct PR : AlgoBase {
     int64_t ebin[3] = {0, 0, 0};      // in-arcs per bin (roofline bytes)
     int64_t last_sweeps = 0, last_affected = 0;
 
+    Comm* comm = nullptr;  // set: pull only the owned destination range, all-gather ranks
+
     PR(Store* st, double damping, double beta, int64_t maxiter);  // = staticPR
+    void set_comm(Comm* c);
     void batch(DevBatch& b, int64_t batch_index);                 // one Batch body
     void read(double* rank, int64_t* outdeg);
 

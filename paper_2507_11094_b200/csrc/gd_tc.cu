@@ -108,8 +108,13 @@ int64_t TC::count_records(const int32_t* s, const int32_t* d, int64_t k) {
     sort_keys_u64(st, R.get(), k);
     DBuf<unsigned long long> tot(1, st);
     tot.zero(st);
-    GD_KERNEL_T("tc_count", 0, k_tc_count, grid_for(k * 32, kThreads, 148LL * 64), kThreads, 0, st, s, d, k, ix.view(),
-                g->n, reinterpret_cast<const int64_t*>(R.get()), k, tot.get());
+    // ranks are over ALL records of the phase; the counted slice is this rank's
+    int64_t a = comm ? k * comm->rank / comm->world : 0;
+    int64_t b = comm ? k * (comm->rank + 1) / comm->world : k;
+    if (b > a)
+        GD_KERNEL_T("tc_count", 0, k_tc_count, grid_for((b - a) * 32, kThreads, 148LL * 64), kThreads, 0, st, s + a,
+                    d + a, b - a, ix.view(), g->n, reinterpret_cast<const int64_t*>(R.get()), k, tot.get());
+    if (comm) comm->allreduce_sum_i64(reinterpret_cast<int64_t*>(tot.get()), 1, st);
     return (int64_t)read_scalar(st, tot.get());
 }
 

@@ -156,6 +156,7 @@ class _Algo:
     def __init__(self, h: C.c_void_p, graph: DynamicGraph):
         self.h = h
         self.graph = graph  # keeps the store alive
+        self.comm = None
 
     def batch(self, arr: RecordArrays, batch_index: int) -> None:
         a = arr.contiguous()

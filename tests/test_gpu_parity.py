@@ -234,3 +234,33 @@ def test_empty_and_edge_cases(gd):
                          gd.DynamicGraph.build([(0, 2, 5)], 3, weighted=True, with_reverse=True), {"src": 0},
                          entry="staticSSSP")
     assert ctx.properties["dist"].values() == [0, np.iinfo(np.int64).max, 5]
+
+
+def test_comm_single_rank_sharded_paths_match(gd):
+    """The NCCL code path (1 rank: all-gather / all-reduce are identities)."""
+    from paper_2507_11094_b200.dist import Communicator, unique_id
+
+    rng = np.random.default_rng(21)
+    n = 4096
+    src, dst, _ = rmat(12, 8 * n, rng, weighted=False)
+    kind, us, ud, uw = updates(rng, n, src, dst, 2000, distinct_deletes=True)
+    comm = Communicator(1, 0, unique_id(), 0)
+    outs = []
+    for use in (False, True):
+        g = gd.DynamicGraph.from_arrays(n, src, dst, with_reverse=True)
+        pr = gd.PRHandle(g, 0.85, 1e-10, 100)
+        if use:
+            comm.attach(pr)
+        for bi, st in enumerate(range(0, 2000, 500)):
+            pr.batch(gd.RecordArrays(kind[st:st + 500], us[st:st + 500], ud[st:st + 500], uw[st:st + 500]), bi)
+        outs.append(pr.read()[0])
+    np.testing.assert_allclose(outs[0], outs[1], rtol=0, atol=1e-15)
+    cnt = []
+    for use in (False, True):
+        g = gd.DynamicGraph.from_arrays(n, src, dst, directed=False)
+        tc = gd.TCHandle(g)
+        if use:
+            comm.attach(tc)
+        tc.batch(gd.RecordArrays(kind, us, ud, uw), 0)
+        cnt.append(tc.read())
+    assert cnt[0] == cnt[1]
