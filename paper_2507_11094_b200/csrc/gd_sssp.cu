@@ -51,118 +51,465 @@ __device__ inline bool claim(int32_t* stamp, int32_t v, int32_t round) { return 
         bool valid = _t < (M);
 #define GROUP_LOOP_END }
 
-__global__ void k_init(int64_t* dist, int32_t* parent, int32_t* stamp, int64_t n) {
+__global__ void k_init(int64_t* dist, int32_t* parent, int32_t* stamp, int32_t* hstamp, int64_t n) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         dist[i] = kInf;
         parent[i] = -1;
         stamp[i] = 0;
+        hstamp[i] = 0;
     }
 }
 
 __global__ void k_set_i64(int64_t* a, int64_t i, int64_t v) { a[i] = v; }
 
-// push relaxation of one frontier round (sssp_dynamic.sp:15-21,110-117)
-__global__ void __launch_bounds__(kThreads) k_relax(const int32_t* fq, int64_t m, OutView ov, int64_t* dist,
-                                                    int32_t* stamp, int32_t round, int32_t* nq,
-                                                    unsigned long long* ncnt, uint8_t* touched) {
-    GROUP_LOOP_BEGIN(m)
-    int32_t v = valid ? fq[_t] : 0;
-    int64_t dv = valid ? dist[v] : kInf;
-    if (dv < kInf) {
-        for (int sg = 0; sg < ov.nseg; ++sg) {
-            const int64_t* off = ov.off[sg];
-            const int32_t* col = ov.col[sg];
-            const int32_t* w = ov.w[sg];
-            int64_t a = off[v], b = off[v + 1];
-            for (int64_t e = a + lane; e < b; e += kG) {
-                int32_t t = col[e];
-                if (t < 0) continue;
-                int64_t c = sat_add(dv, w ? (int64_t)w[e] : 1);
-                if (c < dist[t]) {
-                    long long old = atomicMin(reinterpret_cast<long long*>(&dist[t]), (long long)c);
-                    if (c < old) {
-                        if (touched) touched[t] = 1;
-                        if (claim(stamp, t, round)) enqueue(nq, ncnt, t);
-                    }
+// ---------------------------------------------------------------------------
+// Frontier fixpoints.  One whole fixpoint runs in one cooperative launch: a
+// grid barrier per round instead of a kernel boundary + host read-back of the
+// queue size.  High-diameter graphs (configs[3], grid) take thousands of
+// rounds per batch, so the per-round cost is the batch latency.
+//
+// Round bodies (sssp_dynamic.sp):
+//   RELAX  push Min(dist[t], dist[v] + w) over out-arcs       (:15-21,110-117)
+//   WALK   invalidate tree children parent[t] == v            (:45-63)
+//   PULL   stale v pulls Min over live in-arcs; if it dropped,
+//          re-queue its stale out-neighbours                  (:68-86)
+// A group of kG lanes takes one queued vertex.  A vertex whose scan exceeds
+// kHeavy arcs (R-MAT hubs: 10^4 arcs would serialise a group for ~1 ms) is
+// instead cut into kPiece-arc pieces appended to a piece list, and the next
+// round spreads the pieces over all warps.  Deferring a vertex's scan by one
+// round leaves every fixpoint unchanged: relaxation is monotone (the piece
+// re-reads dist[v]), the walk's descendant set and the pull's Bellman-Ford
+// limit do not depend on the schedule.
+//
+// Queues and piece lists are double-buffered; their counters are triple-
+// buffered so one barrier per round suffices: round `it` reads slot it%3,
+// appends to slot (it+1)%3 and clears slot (it+2)%3, which every thread last
+// read before the previous barrier.  Slot s = cnt[3s .. 3s+2] = {queue, out
+// pieces, in pieces}.  ctr[0] = last round id used for stamps, ctr[1] +=
+// rounds run, ctr[2] = 1 when the round cap (interp.py:141) is hit.
+// ---------------------------------------------------------------------------
+enum { FP_RELAX = 0, FP_WALK = 1, FP_PULL = 2 };
+
+constexpr int kHeavy = 256;  // arcs a group scans inline
+constexpr int kPiece = 128;  // arcs per piece (one warp, 4 per lane)
+constexpr int64_t kNearFarMinRounds = 256;  // static-pass rounds below which near-far is off
+
+struct FpArgs {
+    OutView ov;
+    IdxView ix;
+    int64_t* dist;
+    int32_t* parent;
+    uint8_t* flags;  // relax: touched (nullable); walk: stale (written); pull: stale (read)
+    int32_t* stamp;   // queue de-duplication per round
+    int32_t* hstamp;  // out-piece de-duplication per round
+    const int32_t* seeds;  // round 0 input, never written
+    int32_t* q[2];
+    int64_t* ho[2];  // out-scan pieces
+    int64_t* hi[2];  // in-pull pieces (PULL)
+    unsigned long long* cnt;  // [9]
+    long long* ctr;           // [6]
+    int64_t cap;
+    // near-far (RELAX, delta > 0): relaxations landing at >= theta wait in a
+    // far pile (3 rotating buffers, counters fcnt/fmin) until the near queue
+    // drains; then a split round raises theta by delta and moves the pile's
+    // entries below it to the queue.  Same fixpoint, far fewer re-relaxations
+    // on high-diameter weighted graphs.
+    int64_t delta;
+    int32_t* far[3];
+    unsigned long long* fcnt;  // [3]
+    long long* fmin;           // [3] lower bound of the pile's distances
+    int32_t* infar;            // 1 while a vertex sits in the pile
+};
+
+struct Round {
+    int32_t id;
+    int64_t theta;
+    int32_t* fout;
+    unsigned long long* ffcnt;
+    long long* ffmin;
+    int32_t* qout;
+    unsigned long long* qcnt;
+    int64_t* hoout;
+    unsigned long long* hocnt;
+    int64_t* hiout;
+    unsigned long long* hicnt;
+};
+
+__device__ __forceinline__ int64_t piece_key(int32_t v, int sg, int64_t k) {
+    return ((int64_t)v << 32) | ((int64_t)sg << 27) | k;
+}
+__device__ __forceinline__ void piece_decode(int64_t key, int32_t& v, int& sg, int64_t& k) {
+    v = (int32_t)(key >> 32);
+    sg = (int)((key >> 27) & 31);
+    k = key & ((1LL << 27) - 1);
+}
+
+template <int W>
+__device__ __forceinline__ unsigned group_mask() {
+    return W == 32 ? 0xffffffffu : (((1u << W) - 1) << ((threadIdx.x & 31) & ~(W - 1)));
+}
+
+// per-arc action of an out-scan; `pre` is the target's word loaded ahead
+template <int MODE>
+__device__ __forceinline__ int64_t out_pre(const FpArgs& a, int32_t t) {
+    if (t < 0) return 0;
+    if (MODE == FP_RELAX) return a.dist[t];
+    if (MODE == FP_WALK) return a.parent[t];
+    return a.flags[t];
+}
+
+template <int MODE>
+__device__ __forceinline__ void out_act(const FpArgs& a, const Round& r, int32_t v, int64_t dv, int32_t t, int32_t w,
+                                        int64_t pre) {
+    if (t < 0) return;
+    if (MODE == FP_RELAX) {
+        int64_t c = sat_add(dv, (int64_t)w);
+        if (c < pre) {
+            long long old = atomicMin(reinterpret_cast<long long*>(&a.dist[t]), (long long)c);
+            if (c < old) {
+                if (a.flags) a.flags[t] = 1;
+                if (c < r.theta) {
+                    if (claim(a.stamp, t, r.id)) enqueue(r.qout, r.qcnt, t);
+                } else {
+                    // one hot word: read first, the pile's floor rarely drops
+                    // (L1 bypassed: the slot is reset to INF between uses)
+                    if (c < __ldcg(r.ffmin)) atomicMin(r.ffmin, (long long)c);
+                    if (atomicExch(&a.infar[t], 1) == 0) enqueue(r.fout, r.ffcnt, t);
                 }
             }
         }
-    }
-    GROUP_LOOP_END
-}
-
-// descend the parent tree from invalidated nodes (sssp_dynamic.sp:45-63)
-__global__ void __launch_bounds__(kThreads) k_walk(const int32_t* fq, int64_t m, OutView ov, int64_t* dist,
-                                                   int32_t* parent, uint8_t* stale, int32_t* stamp, int32_t round,
-                                                   int32_t* nq, unsigned long long* ncnt) {
-    GROUP_LOOP_BEGIN(m)
-    if (valid) {
-        int32_t v = fq[_t];
-        for (int sg = 0; sg < ov.nseg; ++sg) {
-            const int64_t* off = ov.off[sg];
-            const int32_t* col = ov.col[sg];
-            int64_t a = off[v], b = off[v + 1];
-            for (int64_t e = a + lane; e < b; e += kG) {
-                int32_t t = col[e];
-                if (t < 0) continue;
-                if (parent[t] == v) {
-                    dist[t] = kInf;
-                    parent[t] = -1;
-                    stale[t] = 1;
-                    if (claim(stamp, t, round)) enqueue(nq, ncnt, t);
-                }
-            }
+    } else if (MODE == FP_WALK) {
+        if (pre == v) {
+            a.dist[t] = kInf;
+            a.parent[t] = -1;
+            a.flags[t] = 1;
+            if (claim(a.stamp, t, r.id)) enqueue(r.qout, r.qcnt, t);
         }
+    } else {
+        if (pre && claim(a.stamp, t, r.id)) enqueue(r.qout, r.qcnt, t);
     }
-    GROUP_LOOP_END
 }
 
-// stale nodes pull Min(dist[v], dist[u] + w) over live in-arcs; a node whose
-// distance dropped re-queues its stale out-neighbours (sssp_dynamic.sp:68-86)
-__global__ void __launch_bounds__(kThreads) k_pull(const int32_t* fq, int64_t m, IdxView ix, OutView ov,
-                                                   int64_t* dist, const uint8_t* stale, int32_t* stamp,
-                                                   int32_t round, int32_t* nq, unsigned long long* ncnt) {
-    GROUP_LOOP_BEGIN(m)
-    int32_t v = valid ? fq[_t] : 0;
+// arcs [e0, e1) of segment sg, lanes strided by W, 4 arcs in flight per lane
+template <int MODE, int W>
+__device__ __forceinline__ void out_scan(const FpArgs& a, const Round& r, int32_t v, int64_t dv, int sg, int64_t e0,
+                                         int64_t e1, int lane) {
+    const int32_t* col = a.ov.col[sg];
+    const int32_t* wt = MODE == FP_RELAX ? a.ov.w[sg] : nullptr;
+    int64_t e = e0 + lane;
+    for (; e + 3 * W < e1; e += 4 * W) {
+        int32_t t[4], w[4];
+        int64_t pre[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) t[j] = col[e + j * W];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) w[j] = wt ? wt[e + j * W] : 1;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) pre[j] = out_pre<MODE>(a, t[j]);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) out_act<MODE>(a, r, v, dv, t[j], w[j], pre[j]);
+    }
+    for (; e < e1; e += W) {
+        int32_t t = col[e];
+        int32_t w = wt ? wt[e] : 1;
+        out_act<MODE>(a, r, v, dv, t, w, out_pre<MODE>(a, t));
+    }
+}
+
+// visit v's out-arcs with a converged group of W lanes: inline when short,
+// else (once per round per vertex) as pieces for the next round
+template <int MODE, int W>
+__device__ __forceinline__ void out_visit(const FpArgs& a, const Round& r, int32_t v, int64_t dv, int lane) {
+    const unsigned gm = group_mask<W>();
+    const int leader = (threadIdx.x & 31) & ~(W - 1);
+    int64_t deg = 0;
+    for (int sg = 0; sg < a.ov.nseg; ++sg) deg += a.ov.off[sg][v + 1] - a.ov.off[sg][v];
+    if (deg <= kHeavy) {
+        for (int sg = 0; sg < a.ov.nseg; ++sg)
+            out_scan<MODE, W>(a, r, v, dv, sg, a.ov.off[sg][v], a.ov.off[sg][v + 1], lane);
+        return;
+    }
+    int64_t np = 0;
+    for (int sg = 0; sg < a.ov.nseg; ++sg) np += (a.ov.off[sg][v + 1] - a.ov.off[sg][v] + kPiece - 1) / kPiece;
+    unsigned long long base = 0;
+    if (lane == 0 && claim(a.hstamp, v, r.id)) base = atomicAdd(r.hocnt, (unsigned long long)np) + 1;
+    base = __shfl_sync(gm, base, leader);
+    if (!base) return;
+    base -= 1;
+    for (int sg = 0; sg < a.ov.nseg; ++sg) {
+        int64_t ns = (a.ov.off[sg][v + 1] - a.ov.off[sg][v] + kPiece - 1) / kPiece;
+        for (int64_t k = lane; k < ns; k += W) r.hoout[base + k] = piece_key(v, sg, k);
+        base += ns;
+    }
+}
+
+// min over in-arcs [e0, e1) of sat(dist[u] + w), lanes strided by W
+template <int W>
+__device__ __forceinline__ int64_t in_min(const FpArgs& a, int64_t e0, int64_t e1, int lane) {
     int64_t best = kInf;
+    int64_t e = e0 + lane;
+    for (; e + 3 * W < e1; e += 4 * W) {
+        int32_t u[4];
+        int64_t c[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) u[j] = a.ix.col[e + j * W];
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            c[j] = u[j] < 0 ? kInf : sat_add(a.dist[u[j]], a.ix.w ? (int64_t)a.ix.w[e + j * W] : 1);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) best = c[j] < best ? c[j] : best;
+    }
+    for (; e < e1; e += W) {
+        int32_t u = a.ix.col[e];
+        if (u < 0) continue;
+        int64_t c = sat_add(a.dist[u], a.ix.w ? (int64_t)a.ix.w[e] : 1);
+        best = c < best ? c : best;
+    }
+    const unsigned gm = group_mask<W>();
+#pragma unroll
+    for (int o = W / 2; o; o >>= 1) {
+        long long x = __shfl_xor_sync(gm, (long long)best, o, W);
+        best = x < best ? x : best;
+    }
+    return best;
+}
+
+// lower dist[v] to best; true (on every lane of the group) when it dropped
+template <int W>
+__device__ __forceinline__ bool lower(const FpArgs& a, int32_t v, int64_t best, int lane) {
+    bool changed = false;
+    if (lane == 0 && best < a.dist[v]) {
+        long long old = atomicMin(reinterpret_cast<long long*>(&a.dist[v]), (long long)best);
+        changed = best < old;
+    }
+    return __shfl_sync(group_mask<W>(), changed, (threadIdx.x & 31) & ~(W - 1));
+}
+
+template <int MODE>
+__device__ __forceinline__ void fp_round(const FpArgs& a, const Round& r, const int32_t* qin, int64_t m,
+                                         const int64_t* hoin, int64_t mo, const int64_t* hiin, int64_t mi) {
+    const int wl = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    // pieces deferred by the previous round: one warp per piece
+    for (int64_t p = warp; p < mo; p += nwarps) {
+        int32_t v;
+        int sg;
+        int64_t k;
+        piece_decode(hoin[p], v, sg, k);
+        int64_t s0 = a.ov.off[sg][v], s1 = a.ov.off[sg][v + 1];
+        int64_t e0 = s0 + k * kPiece, e1 = min(e0 + kPiece, s1);
+        int64_t dv = MODE == FP_RELAX ? a.dist[v] : 0;
+        if (MODE != FP_RELAX || dv < kInf) out_scan<MODE, 32>(a, r, v, dv, sg, e0, e1, wl);
+    }
+    if (MODE == FP_PULL) {
+        for (int64_t p = warp; p < mi; p += nwarps) {
+            int32_t v;
+            int sg;
+            int64_t k;
+            piece_decode(hiin[p], v, sg, k);
+            int64_t s0 = a.ix.off[v], s1 = a.ix.off[v + 1];
+            int64_t e0 = s0 + k * kPiece, e1 = min(e0 + kPiece, s1);
+            int64_t best = in_min<32>(a, e0, e1, wl);
+            if (lower<32>(a, v, best, wl)) out_visit<MODE, 32>(a, r, v, 0, wl);
+        }
+    }
+    // the queue: one group of kG lanes per vertex
+    GROUP_LOOP_BEGIN(m)
+    (void)gw;
     if (valid) {
-        int64_t a = ix.off[v], b = ix.off[v + 1];
-        for (int64_t e = a + lane; e < b; e += kG) {
+        int32_t v = qin[_t];
+        if (MODE == FP_RELAX) {
+            int64_t dv = a.dist[v];
+            if (dv < kInf) out_visit<MODE, kG>(a, r, v, dv, lane);
+        } else if (MODE == FP_WALK) {
+            out_visit<MODE, kG>(a, r, v, 0, lane);
+        } else {
+            int64_t s0 = a.ix.off[v], s1 = a.ix.off[v + 1];
+            if (s1 - s0 > kHeavy) {
+                int64_t np = (s1 - s0 + kPiece - 1) / kPiece;
+                unsigned long long base = 0;
+                if (lane == 0) base = atomicAdd(r.hicnt, (unsigned long long)np);
+                base = __shfl_sync(group_mask<kG>(), base, (threadIdx.x & 31) & ~(kG - 1));
+                for (int64_t k = lane; k < np; k += kG) r.hiout[base + k] = piece_key(v, 0, k);
+            } else {
+                int64_t best = in_min<kG>(a, s0, s1, lane);
+                if (lower<kG>(a, v, best, lane)) out_visit<MODE, kG>(a, r, v, 0, lane);
+            }
+        }
+    }
+    GROUP_LOOP_END
+}
+
+// near-far split: pile entries below theta join the queue, the rest move to
+// the next pile
+__device__ __forceinline__ void split_round(const FpArgs& a, const Round& r, const int32_t* src, int64_t F) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < F; i += (int64_t)gridDim.x * blockDim.x) {
+        int32_t v = src[i];
+        int64_t d = a.dist[v];
+        if (d == kInf) {  // unreached seed: re-enters when relaxed
+            a.infar[v] = 0;
+        } else if (d < r.theta) {
+            a.infar[v] = 0;
+            if (claim(a.stamp, v, r.id)) enqueue(r.qout, r.qcnt, v);
+        } else {
+            a.infar[v] = 1;
+            if (d < __ldcg(r.ffmin)) atomicMin(r.ffmin, (long long)d);
+            enqueue(r.fout, r.ffcnt, v);
+        }
+    }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kThreads) k_fixpoint(FpArgs a) {
+    cg::grid_group grid = cg::this_grid();
+    const bool leader = grid.thread_rank() == 0;
+    const int32_t round0 = (int32_t)a.ctr[0];
+    const bool nf = MODE == FP_RELAX && a.delta > 0;
+    int64_t theta = kInf;  // every relaxation is near unless near-far
+    if (nf) theta = 0;
+    int nsplit = 0;  // pile = far[nsplit % 3]
+    int64_t it = 0;
+    for (;; ++it) {
+        const volatile unsigned long long* c = a.cnt + 3 * (it % 3);
+        int64_t m = (int64_t)c[0];
+        const int64_t mo = (int64_t)c[1], mi = (int64_t)c[2];
+        const int p = nsplit % 3;
+        int64_t F = 0;
+        bool split = false;
+        if (nf && it == 0) {  // the seeds are split like a pile
+            F = m;
+            m = 0;
+            split = true;
+        } else if (nf && (m | mo | mi) == 0) {
+            F = (int64_t)((const volatile unsigned long long*)a.fcnt)[p];
+            split = true;
+        }
+        if ((m | mo | mi | F) == 0) break;
+        if (it >= a.cap) {
+            if (leader) a.ctr[2] = 1;
+            break;
+        }
+        if (split) {
+            int64_t lo = ((const volatile long long*)a.fmin)[p];
+            theta = max(sat_add(theta, a.delta), sat_add(lo, a.delta));
+        }
+        if (leader) {
+            unsigned long long* z = a.cnt + 3 * ((it + 2) % 3);
+            z[0] = z[1] = z[2] = 0;
+            if (split) {
+                a.fcnt[(p + 2) % 3] = 0;
+                a.fmin[(p + 2) % 3] = kInf;
+                a.ctr[5] += 1;
+            }
+            a.ctr[3] += m;  // queue entries processed (diagnostics)
+            a.ctr[4] += mo + mi;
+        }
+        const int nx = (it + 1) & 1;
+        unsigned long long* cn = a.cnt + 3 * ((it + 1) % 3);
+        const int fo = split ? (p + 1) % 3 : p;
+        Round r{round0 + (int32_t)it + 1, theta, a.far[fo], a.fcnt + fo, a.fmin + fo,
+                a.q[nx], cn, a.ho[nx], cn + 1, a.hi[nx], cn + 2};
+        if (split) split_round(a, r, it == 0 ? a.seeds : a.far[p], F);
+        else fp_round<MODE>(a, r, it == 0 ? a.seeds : a.q[it & 1], m, a.ho[it & 1], mo, a.hi[it & 1], mi);
+        grid.sync();
+        if (split) ++nsplit;
+    }
+    // it > 0: a barrier separates every thread's read of ctr[0] from this write
+    if (leader && it > 0) {
+        a.ctr[0] = round0 + it;
+        a.ctr[1] += it;
+    }
+}
+
+// decrementalSSSP's pull fixpoint (sssp_dynamic.sp:68-86) as one pull sweep
+// over the stale list plus a near-far push from it: after the walk the
+// non-stale distances are exact (their tree paths survive the deletes), so
+// both reach the same least fixpoint over the stale set.  Vertices with more
+// than kHeavy in-arcs go to `heavy` and are pulled by a whole CTA.
+__global__ void __launch_bounds__(kThreads) k_pull_once(const int32_t* list, const int64_t* d_m, IdxView ix,
+                                                        int64_t* dist, int32_t* heavy, unsigned long long* nheavy) {
+    const int64_t m = *d_m;
+    FpArgs a;
+    a.ix = ix;
+    a.dist = dist;
+    GROUP_LOOP_BEGIN(m)
+    (void)gw;
+    if (valid) {
+        int32_t v = list[_t];
+        int64_t s0 = ix.off[v], s1 = ix.off[v + 1];
+        if (s1 - s0 > kHeavy) {
+            if (lane == 0) heavy[atomicAdd(nheavy, 1ULL)] = v;
+        } else {
+            int64_t best = in_min<kG>(a, s0, s1, lane);
+            if (lane == 0 && best < dist[v]) atomicMin(reinterpret_cast<long long*>(&dist[v]), (long long)best);
+        }
+    }
+    GROUP_LOOP_END
+}
+
+__global__ void __launch_bounds__(kThreads) k_pull_heavy(const int32_t* heavy, const unsigned long long* nheavy,
+                                                         IdxView ix, int64_t* dist) {
+    __shared__ long long part[kThreads / 32];
+    const int64_t nh = (int64_t)*nheavy;
+    for (int64_t h = blockIdx.x; h < nh; h += gridDim.x) {
+        int32_t v = heavy[h];
+        int64_t best = kInf;
+#pragma unroll 4
+        for (int64_t e = ix.off[v] + threadIdx.x; e < ix.off[v + 1]; e += kThreads) {
             int32_t u = ix.col[e];
             if (u < 0) continue;
             int64_t c = sat_add(dist[u], ix.w ? (int64_t)ix.w[e] : 1);
             best = c < best ? c : best;
         }
-    }
 #pragma unroll
-    for (int o = kG / 2; o; o >>= 1) {
-        long long x = __shfl_xor_sync(0xffffffffu, (long long)best, o, kG);
-        best = x < best ? x : best;
-    }
-    bool changed = false;
-    if (valid && lane == 0 && best < dist[v]) {
-        long long old = atomicMin(reinterpret_cast<long long*>(&dist[v]), (long long)best);
-        changed = best < old;
-    }
-    changed = __shfl_sync(0xffffffffu, changed, (threadIdx.x & 31) & ~(kG - 1));
-    if (changed) {
-        for (int sg = 0; sg < ov.nseg; ++sg) {
-            const int64_t* off = ov.off[sg];
-            const int32_t* col = ov.col[sg];
-            int64_t a = off[v], b = off[v + 1];
-            for (int64_t e = a + lane; e < b; e += kG) {
-                int32_t t = col[e];
-                if (t < 0) continue;
-                if (stale[t] && claim(stamp, t, round)) enqueue(nq, ncnt, t);
-            }
+        for (int o = 16; o; o >>= 1) {
+            long long x = __shfl_xor_sync(0xffffffffu, (long long)best, o);
+            best = x < best ? x : best;
         }
+        if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = best;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int j = 1; j < kThreads / 32; ++j) best = part[j] < best ? part[j] : best;
+            if (best < dist[v]) atomicMin(reinterpret_cast<long long*>(&dist[v]), (long long)best);
+        }
+        __syncthreads();
     }
-    GROUP_LOOP_END
+}
+
+__global__ void k_wsum(const int32_t* col, const int32_t* w, int64_t ns, unsigned long long* acc) {
+    unsigned long long sum = 0, cnt = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ns; i += (int64_t)gridDim.x * blockDim.x)
+        if (col[i] >= 0) {
+            sum += (unsigned long long)max(w[i], 0);
+            ++cnt;
+        }
+    for (int o = 16; o; o >>= 1) {
+        sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    }
+    if ((threadIdx.x & 31) == 0 && cnt) {
+        atomicAdd(&acc[0], sum);
+        atomicAdd(&acc[1], cnt);
+    }
+}
+
+__global__ void k_fp_prep(unsigned long long* cnt, const int64_t* d_n, int64_t n, unsigned long long* fcnt,
+                          long long* fmin) {
+    cnt[0] = (unsigned long long)(d_n ? *d_n : n);
+    for (int i = 1; i < 6; ++i) cnt[i] = 0;
+    if (fcnt) {
+        fcnt[0] = fcnt[1] = fcnt[2] = 0;
+        fmin[0] = 0;  // a lower bound for the seeds
+        fmin[1] = fmin[2] = kInf;
+    }
 }
 
 // parent = min-id in-neighbour u with dist[u] + w == dist[v] (sssp_dynamic.sp:23-34)
-__global__ void __launch_bounds__(kThreads) k_fix_parent(const int32_t* list, int64_t m, IdxView ix,
-                                                         const int64_t* dist, int32_t* parent, int32_t src) {
+__global__ void __launch_bounds__(kThreads) k_fix_parent(const int32_t* list, const int64_t* d_m, int64_t m,
+                                                         IdxView ix, const int64_t* dist, int32_t* parent,
+                                                         int32_t src) {
+    if (d_m) m = *d_m;
     GROUP_LOOP_BEGIN(m)
     int32_t v = valid ? (list ? list[_t] : (int32_t)_t) : 0;
     int64_t dv = valid ? dist[v] : kInf;
@@ -221,6 +568,24 @@ __global__ void k_read_parent(const int32_t* p, int64_t n, int64_t* out) {
 
 inline unsigned group_grid(int64_t m) { return grid_for(((m + kPerWarp - 1) / kPerWarp) * 32, kThreads, 148LL * 32); }
 
+// co-resident grid for the cooperative fixpoint: <= 4 CTAs per SM keeps the
+// barrier cheap while leaving 32 warps per SM for latency hiding
+template <int MODE>
+unsigned coop_grid() {
+    static unsigned g = 0;
+    if (!g) {
+        int dev = 0, sms = 0, nb = 0;
+        GD_CUDA(cudaGetDevice(&dev));
+        GD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        GD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_fixpoint<MODE>, kThreads, 0));
+        if (nb < 1) throw GdError(GD_ERR_CUDA, "fixpoint kernel cannot be resident");
+        int per = 4;
+        if (const char* e = getenv("GD_FP_CTAS_PER_SM")) per = std::max(1, atoi(e));
+        g = (unsigned)(sms * std::min(nb, per));
+    }
+    return g;
+}
+
 }  // namespace
 
 SSSP::SSSP(Store* st, int64_t s) : AlgoBase(ALGO_SSSP, st), src((int32_t)s) {
@@ -232,94 +597,118 @@ SSSP::SSSP(Store* st, int64_t s) : AlgoBase(ALGO_SSSP, st), src((int32_t)s) {
     dist.alloc(n, cs);
     parent.alloc(n, cs);
     stamp.alloc(n, cs);
+    hstamp.alloc(n, cs);
     fa.alloc(n, cs);
     fb.alloc(n, cs);
     fr.init(n, cs);
+    ctr.alloc(6, cs);
+    fcnt.alloc(3, cs);
+    fmin.alloc(3, cs);
+    infar.alloc(n, cs);
+    infar.zero(cs);
+    for (int j = 0; j < 3; ++j) far[j].alloc(std::max<int64_t>(n, 1), cs);
+    // near-far bucket width: 3x the mean live arc weight (unweighted graphs
+    // relax level by level already)
+    if (g->weighted && !g->segs.empty() && g->segs[0].nslots) {
+        DBuf<unsigned long long> acc(2, cs);
+        acc.zero(cs);
+        GD_KERNEL(k_wsum, grid_for(g->segs[0].nslots, 256, 148 * 8), 256, 0, cs, g->segs[0].col.get(),
+                  g->segs[0].w.get(), g->segs[0].nslots, acc.get());
+        unsigned long long h[2];
+        GD_CUDA(cudaMemcpyAsync(h, acc.get(), sizeof(h), cudaMemcpyDeviceToHost, cs));
+        GD_CUDA(cudaStreamSynchronize(cs));
+        if (h[1]) delta = std::max<int64_t>(1, (int64_t)(3 * h[0] / h[1]));
+    }
+    if (const char* e = getenv("GD_SSSP_DELTA")) delta = atoll(e);
+    ctr.zero(cs);
+    dcount.alloc(1, cs);
     ProfScope ps(&prof);
     timer.begin(PH_STATIC);
-    GD_KERNEL(k_init, grid_for(n, 256), 256, 0, cs, dist.get(), parent.get(), stamp.get(), n);
+    GD_KERNEL(k_init, grid_for(n, 256), 256, 0, cs, dist.get(), parent.get(), stamp.get(), hstamp.get(), n);
     GD_KERNEL(k_set_i64, 1, 1, 0, cs, dist.get(), (int64_t)src, (int64_t)0);
     int32_t seed = src;
     DBuf<int32_t> sq(1, cs);
     GD_CUDA(cudaMemcpyAsync(sq.get(), &seed, 4, cudaMemcpyHostToDevice, cs));
-    relax_push(sq.get(), 1, nullptr);
-    fix_parents(nullptr, n);
+    fixpoint(FP_RELAX, sq.get(), nullptr, 1, nullptr);
+    fix_parents(nullptr, nullptr, n);
+    finish();
+    // low-diameter graphs (R-MAT: tens of rounds) gain nothing from buckets
+    // and pay their extra rounds; keep near-far for the deep ones (grids)
+    if (!getenv("GD_SSSP_DELTA") && iterations < kNearFarMinRounds) delta = 0;
     timer.end_all();
     prof.flush();
 }
 
-void SSSP::check_cap(int64_t it) {
-    if (it >= cap_factor * std::max<int64_t>(g->n, 1)) throw GdError(GD_ERR_DIVERGED, "fixed point diverged");
-}
-
-int64_t SSSP::relax_push(const int32_t* seeds, int64_t nseeds, uint8_t* touched) {
+void SSSP::fixpoint(int mode, const int32_t* seeds, const int64_t* d_nseeds, int64_t nseeds, uint8_t* flags) {
     cudaStream_t s = stream();
-    OutView ov = g->out_view();
-    if (nseeds == 0) return 0;
-    GD_CUDA(cudaMemcpyAsync(fr.q[0].get(), seeds, nseeds * 4, cudaMemcpyDeviceToDevice, s));
-    int cur = 0;
-    int64_t m = nseeds, it = 0;
-    while (m > 0) {
-        check_cap(it);
-        ++round;
-        GD_CUDA(cudaMemsetAsync(fr.cnt.get(), 0, sizeof(unsigned long long), s));
-        GD_KERNEL_T("sssp_relax", 0, k_relax, group_grid(m), kThreads, 0, s, fr.q[cur].get(), m, ov, dist.get(),
-                    stamp.get(), round, fr.q[1 - cur].get(), fr.cnt.get(), touched);
-        m = (int64_t)read_scalar(s, fr.cnt.get());
-        cur = 1 - cur;
-        ++it;
+    if (!d_nseeds && nseeds == 0) return;
+    const bool nf = mode == FP_RELAX && delta > 0;
+    GD_KERNEL(k_fp_prep, 1, 1, 0, s, fr.cnt.get(), d_nseeds, nseeds, nf ? fcnt.get() : nullptr,
+              nf ? fmin.get() : nullptr);
+    FpArgs a;
+    a.delta = nf ? delta : 0;
+    for (int j = 0; j < 3; ++j) a.far[j] = nf ? far[j].get() : nullptr;
+    a.fcnt = fcnt.get();
+    a.fmin = fmin.get();
+    a.infar = infar.get();
+    a.ov = g->out_view();
+    a.ix = g->rev.view();
+    a.dist = dist.get();
+    a.parent = parent.get();
+    a.flags = flags;
+    a.stamp = stamp.get();
+    a.seeds = seeds;
+    a.q[0] = fr.q[0].get();
+    a.q[1] = fr.q[1].get();
+    // piece lists: every vertex is cut at most once per round; a vertex with
+    // d > kHeavy arcs spread over nseg segments yields <= d/kPiece + nseg pieces
+    int64_t S = g->total_slots(), R = mode == FP_PULL ? g->rev.nnz : 0;
+    int64_t capo = S / kPiece + (int64_t)a.ov.nseg * (S / kHeavy + 1) + 64;
+    int64_t capi = R / kPiece + R / kHeavy + 64;
+    for (int j = 0; j < 2; ++j) {
+        ho[j].ensure(capo, s);
+        hi[j].ensure(capi, s);
+        a.ho[j] = ho[j].get();
+        a.hi[j] = hi[j].get();
     }
-    iterations += it;
-    return it;
+    a.hstamp = hstamp.get();
+    a.cnt = fr.cnt.get();
+    a.ctr = ctr.get();
+    a.cap = cap_factor * std::max<int64_t>(g->n, 1);
+    void* args[] = {&a};
+    static const char* names[] = {"sssp_relax", "sssp_walk", "sssp_pull"};
+    const void* fn = mode == FP_RELAX  ? (const void*)k_fixpoint<FP_RELAX>
+                     : mode == FP_WALK ? (const void*)k_fixpoint<FP_WALK>
+                                       : (const void*)k_fixpoint<FP_PULL>;
+    unsigned grid = mode == FP_RELAX ? coop_grid<FP_RELAX>() : mode == FP_WALK ? coop_grid<FP_WALK>()
+                                                                               : coop_grid<FP_PULL>();
+    int pi = prof_begin(names[mode], 0, s);
+    GD_CUDA(cudaLaunchCooperativeKernel(fn, grid, kThreads, args, 0, s));
+    count_launch();
+    prof_end(pi, s);
 }
 
-int64_t SSSP::walk(const int32_t* seeds, int64_t nseeds, uint8_t* stale) {
-    cudaStream_t s = stream();
-    OutView ov = g->out_view();
-    if (nseeds == 0) return 0;
-    GD_CUDA(cudaMemcpyAsync(fr.q[0].get(), seeds, nseeds * 4, cudaMemcpyDeviceToDevice, s));
-    int cur = 0;
-    int64_t m = nseeds, it = 0;
-    while (m > 0) {
-        check_cap(it);
-        ++round;
-        GD_CUDA(cudaMemsetAsync(fr.cnt.get(), 0, sizeof(unsigned long long), s));
-        GD_KERNEL_T("sssp_walk", 0, k_walk, group_grid(m), kThreads, 0, s, fr.q[cur].get(), m, ov, dist.get(),
-                    parent.get(), stale, stamp.get(), round, fr.q[1 - cur].get(), fr.cnt.get());
-        m = (int64_t)read_scalar(s, fr.cnt.get());
-        cur = 1 - cur;
-        ++it;
-    }
-    iterations += it;
-    return it;
-}
-
-int64_t SSSP::pull(const int32_t* list, int64_t nstale, const uint8_t* stale) {
-    cudaStream_t s = stream();
-    OutView ov = g->out_view();
-    IdxView ix = g->rev.view();
-    if (nstale == 0) return 0;
-    GD_CUDA(cudaMemcpyAsync(fr.q[0].get(), list, nstale * 4, cudaMemcpyDeviceToDevice, s));
-    int cur = 0;
-    int64_t m = nstale, it = 0;
-    while (m > 0) {
-        check_cap(it);
-        ++round;
-        GD_CUDA(cudaMemsetAsync(fr.cnt.get(), 0, sizeof(unsigned long long), s));
-        GD_KERNEL_T("sssp_pull", 0, k_pull, group_grid(m), kThreads, 0, s, fr.q[cur].get(), m, ix, ov, dist.get(),
-                    stale, stamp.get(), round, fr.q[1 - cur].get(), fr.cnt.get());
-        m = (int64_t)read_scalar(s, fr.cnt.get());
-        cur = 1 - cur;
-        ++it;
-    }
-    iterations += it;
-    return it;
-}
-
-void SSSP::fix_parents(const int32_t* list, int64_t m) {
+void SSSP::fix_parents(const int32_t* list, const int64_t* d_m, int64_t m) {
     if (m == 0) return;
-    GD_KERNEL_T("sssp_parent", 0, k_fix_parent, group_grid(m), kThreads, 0, stream(), list, m, g->rev.view(),
+    GD_KERNEL_T("sssp_parent", 0, k_fix_parent, group_grid(m), kThreads, 0, stream(), list, d_m, m, g->rev.view(),
                 dist.get(), parent.get(), src);
+}
+
+// one read-back per batch: total rounds and the divergence flag
+void SSSP::finish() {
+    long long h[6];
+    GD_CUDA(cudaMemcpyAsync(h, ctr.get(), sizeof(h), cudaMemcpyDeviceToHost, stream()));
+    GD_CUDA(cudaStreamSynchronize(stream()));
+    static const bool dbg = getenv("GD_SSSP_DEBUG") != nullptr;
+    if (dbg)
+        fprintf(stderr, "[sssp] rounds %lld (+%lld) visits %lld pieces %lld splits %lld\n", h[1], h[1] - iterations,
+                h[3], h[4], h[5]);
+    iterations = h[1];
+    if (h[2]) {  // abandoned piles leave in-far marks behind
+        infar.zero(stream());
+        GD_CUDA(cudaMemsetAsync(ctr.get() + 2, 0, sizeof(long long), stream()));
+        throw GdError(GD_ERR_DIVERGED, "fixed point diverged");
+    }
 }
 
 void SSSP::batch(DevBatch& b, int64_t batch_index) {
@@ -330,6 +719,7 @@ void SSSP::batch(DevBatch& b, int64_t batch_index) {
     uint8_t* seed_del = fa.get();  // activeOnDelete, then stale
     uint8_t* seed_add = fb.get();  // activeOnAdd, then touched
     DBuf<int32_t> list(std::max<int64_t>(n, 1), s);
+    int64_t* nlist = dcount.get();
 
     timer.begin(PH_PRE);
     fa.zero(s);
@@ -342,12 +732,23 @@ void SSSP::batch(DevBatch& b, int64_t batch_index) {
     // decrementalSSSP (sssp_dynamic.sp:37-99); stale starts as the seeds
     timer.begin(PH_PROP);
     GD_KERNEL(k_set_i64, 1, 1, 0, s, dist.get(), (int64_t)src, (int64_t)0);
-    int64_t nseed = select_flagged_index(s, seed_del, n, list.get());
-    walk(list.get(), nseed, seed_del);
+    select_flagged_index_async(s, seed_del, n, list.get(), nlist);
+    fixpoint(FP_WALK, list.get(), nlist, 0, seed_del);
     GD_KERNEL(k_set_i64, 1, 1, 0, s, dist.get(), (int64_t)src, (int64_t)0);
-    int64_t nstale = select_flagged_index(s, seed_del, n, list.get());
-    pull(list.get(), nstale, seed_del);
-    fix_parents(list.get(), nstale);
+    select_flagged_index_async(s, seed_del, n, list.get(), nlist);
+    if (delta > 0) {  // one pull sweep + near-far push (same fixpoint, see k_pull_once)
+        IdxView ix = g->rev.view();
+        heavy.ensure(g->rev.nnz / kHeavy + 64, s);
+        GD_CUDA(cudaMemsetAsync(fr.cnt.get() + 9, 0, sizeof(unsigned long long), s));
+        GD_KERNEL_T("sssp_pull", 0, k_pull_once, group_grid(n), kThreads, 0, s, list.get(), nlist, ix, dist.get(),
+                    heavy.get(), fr.cnt.get() + 9);
+        GD_KERNEL_T("sssp_pull", 0, k_pull_heavy, 148 * 4, kThreads, 0, s, heavy.get(), fr.cnt.get() + 9, ix,
+                    dist.get());
+        fixpoint(FP_RELAX, list.get(), nlist, 0, nullptr);
+    } else {
+        fixpoint(FP_PULL, list.get(), nlist, 0, seed_del);
+    }
+    fix_parents(list.get(), nlist, n);
 
     timer.begin(PH_PRE);
     if (b.kadd) GD_KERNEL(k_on_add, grid_for(b.kadd, 256), 256, 0, s, b.as.get(), b.ad.get(), b.aw.get(), b.kadd,
@@ -363,10 +764,11 @@ void SSSP::batch(DevBatch& b, int64_t batch_index) {
 
     // incrementalSSSP (sssp_dynamic.sp:101-130); touched starts as the seeds
     timer.begin(PH_PROP);
-    int64_t nadd = select_flagged_index(s, seed_add, n, list.get());
-    relax_push(list.get(), nadd, seed_add);
-    int64_t ntouched = select_flagged_index(s, seed_add, n, list.get());
-    fix_parents(list.get(), ntouched);
+    select_flagged_index_async(s, seed_add, n, list.get(), nlist);
+    fixpoint(FP_RELAX, list.get(), nlist, 0, seed_add);
+    select_flagged_index_async(s, seed_add, n, list.get(), nlist);
+    fix_parents(list.get(), nlist, n);
+    finish();
     timer.end_all();
     prof.flush();
 }

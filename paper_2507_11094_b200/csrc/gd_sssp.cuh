@@ -11,20 +11,30 @@ struct SSSP : AlgoBase {
     DBuf<int64_t> dist;       // int64, INF = INT64_MAX (reference type)
     DBuf<int32_t> parent;     // -1 = none
     DBuf<int32_t> stamp;      // frontier de-duplication (round id)
+    DBuf<int32_t> hstamp;     // hub-piece de-duplication (round id)
+    DBuf<int64_t> ho[2], hi[2];  // hub pieces (out-scans, in-pulls), double-buffered
     DBuf<uint8_t> fa, fb;     // per-node flags (stale / touched / seeds)
     Frontier fr;
-    int32_t round = 0;
+    DBuf<long long> ctr;   // [last stamp round, total rounds, diverged, visits, pieces, splits]
+    int64_t delta = 0;     // near-far bucket width for RELAX (0 = plain frontier)
+    DBuf<int32_t> far[3];  // near-far piles
+    DBuf<unsigned long long> fcnt;
+    DBuf<long long> fmin;
+    DBuf<int32_t> infar;
+    DBuf<int32_t> heavy;   // stale vertices with > kHeavy in-arcs (pull sweep)
+    DBuf<int64_t> dcount;  // device-side list sizes (no host read-back per fixpoint)
 
     SSSP(Store* st, int64_t src);  // = staticSSSP
     void batch(DevBatch& b, int64_t batch_index);
     void read(int64_t* dist, int64_t* parent);
 
   private:
-    int64_t relax_push(const int32_t* seeds, int64_t nseeds, uint8_t* touched);  // push fixpoint
-    int64_t walk(const int32_t* seeds, int64_t nseeds, uint8_t* stale);
-    int64_t pull(const int32_t* stale_list, int64_t nstale, const uint8_t* stale);
-    void fix_parents(const int32_t* list, int64_t m);  // list == nullptr: every node
-    void check_cap(int64_t it);
+    // one cooperative launch per fixpoint (relax / walk / pull); the seed count
+    // is read from d_nseeds on the device when given, else nseeds
+    void fixpoint(int mode, const int32_t* seeds, const int64_t* d_nseeds, int64_t nseeds, uint8_t* flags);
+    // list == nullptr: every node; d_m (device) overrides m, which bounds the grid
+    void fix_parents(const int32_t* list, const int64_t* d_m, int64_t m);
+    void finish();
 };
 
 }  // namespace gdb
