@@ -141,3 +141,26 @@ def test_tc_dynamic_equals_static_on_final_graph(gd, n, m, pct):
     g2 = gd.DynamicGraph.from_arrays(n, fs[keep], fd[keep], directed=False)
     st = gd.run_program(gd.compile_source("Dynamic dynamicTC("), g2, {}, entry="staticTC")
     assert ctx.return_value == st.return_value
+
+
+@pytest.mark.parametrize("graph", ["rmat", "grid"])
+@pytest.mark.parametrize("delta", ["0", "7", "100", "5000"])
+def test_sssp_near_far_width_does_not_change_results(gd, graph, delta, monkeypatch):
+    """The near-far bucket width (GD_SSSP_DELTA; 0 = plain frontier) and the
+    decremental sweep+push it enables must reproduce the reference oracle."""
+    from oracle import oracle as O
+    from paper_2507_11094_b200 import generate as G
+
+    if graph == "rmat":
+        s, d, w, n = G.rmat(12, 40_000, seed=3, weighted=True, max_weight=100)
+    else:
+        s, d, w, n = G.grid(60, 60, seed=3)
+    kind, us, ud, uw, per = G.updates(s, d, n, percent=10, batches=3, seed=4, max_weight=100)
+    monkeypatch.setenv("GD_SSSP_DELTA", delta)
+    g = gd.DynamicGraph.from_arrays(n, s, d, w, weighted=True, with_reverse=True)
+    ctx = gd.run_batches(gd.compile_source("Dynamic dynamicSSSP("), g, gd.UpdateStream.from_arrays(kind, us, ud, uw),
+                         per, {"src": 0})
+    og = O.OracleGraph(n, s, d, w, directed=True, weighted=True, with_reverse=True)
+    want_d, want_p = O.OracleSSSP(og, 0).run_stream(kind, us, ud, uw, per).read()
+    np.testing.assert_array_equal(ctx.properties["dist"].values(), want_d)
+    np.testing.assert_array_equal(ctx.properties["parent"].values(), want_p)
