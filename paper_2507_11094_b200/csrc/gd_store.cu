@@ -571,85 +571,101 @@ __global__ void k_add_offsets(const int64_t* off, const int64_t* shift, int64_t 
 }
 
 // inserts with P < tile start, per tile (insertion points are sorted)
-__global__ void k_tile_ins(int64_t ntiles, const int64_t* ipos, int64_t nins, int64_t* pj) {
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t <= ntiles; t += (int64_t)gridDim.x * blockDim.x)
-        pj[t] = lower_bound_dev<int64_t>(ipos, 0, nins, t * kTile);
+__global__ void k_win_ins(int64_t nwin, const int64_t* ipos, int64_t nins, int64_t* pj) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t <= nwin; t += (int64_t)gridDim.x * blockDim.x)
+        pj[t] = lower_bound_dev<int64_t>(ipos, 0, nins, t * kWin);
 }
 
-// newpos(i) = i - #dead(< i) + #inserts(P <= i).  A CTA takes a 2048-entry
-// tile, each warp a 256-entry window, lane-strided (every load / store
-// instruction covers 32 consecutive entries).  Dead entries are exactly the
-// negative ones, so #dead is the window's base (scan of the per-window tomb
-// histogram) plus a ballot/popc prefix; warps never wait on each other.  The
-// window's few insertion points are counted per entry and their entries
-// written here too.
+// newpos(i) = i - #dead(< i) + #inserts(P <= i).  One warp per 256-entry
+// window, lane-strided (every load / store instruction covers 32 consecutive
+// entries).  Dead entries are exactly the negative ones, so #dead is the
+// window's base (scan of the per-window tomb histogram) plus a ballot/popc
+// prefix; warps never wait on each other.  The window's insertion range
+// comes from a per-window table, so the entries, the dead base and the range
+// are loaded together and only the insertion positions depend on them.  All
+// per-entry arithmetic is 32-bit and relative to the window: the 64-bit
+// output base ws - dead + ins is formed once per window.
+template <bool FULL>
+__device__ __forceinline__ void edit_window(const int32_t* __restrict__ col, const int32_t* __restrict__ w,
+                                            int64_t nnz, int64_t win, const int64_t* __restrict__ dead_win,
+                                            const int64_t* __restrict__ ipos, const int64_t* __restrict__ pj_win,
+                                            const int32_t* __restrict__ icol, const int32_t* __restrict__ iw,
+                                            int32_t* __restrict__ ocol, int32_t* __restrict__ ow) {
+    constexpr int Q = kWin / 32;
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1;
+    const int64_t ws = win * kWin;
+    const int lim = FULL ? kWin : (int)(nnz - ws);
+    const int32_t* cb = col + ws;
+    const int32_t* wb = w ? w + ws : nullptr;
+    int32_t v[Q], wv[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+        const int o = q * 32 + lane;
+        const bool in = FULL || o < lim;
+        v[q] = in ? __ldcs(&cb[o]) : 0;
+        wv[q] = (wb && in) ? __ldcs(&wb[o]) : 0;
+    }
+    const int64_t dead0 = dead_win[win];
+    const int64_t pjw = pj_win[win], pje = pj_win[win + 1];
+    const int nins = (int)(pje - pjw);
+    int my_ins = INT_MAX;
+    int32_t my_icol = 0, my_iw = 1;
+    if (lane < nins) {
+        my_ins = (int)(ipos[pjw + lane] - ws);
+        my_icol = icol[pjw + lane];
+        if (iw) my_iw = iw[pjw + lane];
+    }
+    unsigned m[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) m[q] = __ballot_sync(0xffffffffu, (FULL || q * 32 + lane < lim) && v[q] < 0);
+    const int64_t obase = ws - dead0 + pjw;  // newpos of window entry 0, before local shifts
+    int32_t* oc = ocol + obase;
+    int32_t* owb = ow ? ow + obase : nullptr;
+    int dead = 0;
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+        const int o = q * 32 + lane;
+        int ins = 0;
+        if (nins > 32) {
+            ins = (int)(upper_bound_dev<int64_t>(ipos, pjw, pje, ws + o) - pjw);
+        } else {
+            for (int k = 0; k < nins; ++k) ins += __shfl_sync(0xffffffffu, my_ins, k) <= o;
+        }
+        if ((FULL || o < lim) && v[q] >= 0) {
+            const int np = o - (dead + __popc(m[q] & lt)) + ins;
+            __stcs(&oc[np], v[q]);
+            if (owb) __stcs(&owb[np], wv[q]);
+        }
+        dead += __popc(m[q]);
+    }
+    for (int j = lane; j < nins; j += 32) {  // this window's inserted entries
+        const int P = j < 32 ? my_ins : (int)(ipos[pjw + j] - ws);
+        const int32_t ic = j < 32 ? my_icol : icol[pjw + j];
+        const int32_t iwv = j < 32 ? my_iw : (iw ? iw[pjw + j] : 1);
+        const int qq = P >> 5, r = P & 31;
+        int d = 0;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) d += q < qq ? __popc(m[q]) : (q == qq ? __popc(m[q] & ((1u << r) - 1)) : 0);
+        const int np = P - d + j;
+        oc[np] = ic;
+        if (owb) owb[np] = iwv;
+    }
+}
+
 __global__ void __launch_bounds__(kEditThreads) k_edit_base(const int32_t* __restrict__ col,
                                                             const int32_t* __restrict__ w, int64_t nnz,
-                                                            const int64_t* dead_win, const int64_t* ipos,
-                                                            const int64_t* pj_tile, const int32_t* icol,
-                                                            const int32_t* iw, int64_t ntiles,
+                                                            const int64_t* __restrict__ dead_win,
+                                                            const int64_t* __restrict__ ipos,
+                                                            const int64_t* __restrict__ pj_win,
+                                                            const int32_t* __restrict__ icol,
+                                                            const int32_t* __restrict__ iw, int64_t nwin,
                                                             int32_t* __restrict__ ocol, int32_t* __restrict__ ow) {
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const unsigned lt = (1u << lane) - 1;
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const int64_t ws = tile * kTile + (int64_t)wid * kWin;
-        const int64_t we = min(ws + kWin, nnz);
-        int32_t v[kWin / 32], wv[kWin / 32];
-        unsigned m[kWin / 32];
-        if (ws >= nnz) continue;  // warp-uniform: no block-level sync in this kernel
-        int wd = 0;
-#pragma unroll
-        for (int q = 0; q < kWin / 32; ++q) {
-            int64_t i = ws + q * 32 + lane;
-            bool in = i < we;
-            v[q] = in ? __ldcs(&col[i]) : 0;
-            wv[q] = (w && in) ? __ldcs(&w[i]) : 0;
-        }
-#pragma unroll
-        for (int q = 0; q < kWin / 32; ++q) {
-            int64_t i = ws + q * 32 + lane;
-            m[q] = __ballot_sync(0xffffffffu, i < we && v[q] < 0);
-            wd += __popc(m[q]);
-        }
-        (void)wd;
-        const int64_t dead0 = dead_win[ws / kWin];
-        const int64_t pj0 = pj_tile[tile], pj1 = pj_tile[tile + 1];
-        int64_t pjw = pj0, pje = pj0;
-        if (pj0 != pj1) {
-            pjw = lower_bound_dev<int64_t>(ipos, pj0, pj1, ws);
-            pje = lower_bound_dev<int64_t>(ipos, pjw, pj1, we);
-        }
-        const int64_t nins = pje - pjw;
-        const int64_t my_ins = lane < nins ? ipos[pjw + lane] : INT64_MAX;
-        int64_t dead_before = dead0;
-#pragma unroll
-        for (int q = 0; q < kWin / 32; ++q) {
-            int64_t i = ws + q * 32 + lane;
-            int64_t ins = pjw;
-            if (nins > 32) {
-                ins = upper_bound_dev<int64_t>(ipos, pjw, pje, i);
-            } else {
-                for (int k = 0; k < nins; ++k) ins += __shfl_sync(0xffffffffu, my_ins, k) <= i;
-            }
-            if (i < we && v[q] >= 0) {
-                int64_t np = i - (dead_before + __popc(m[q] & lt)) + ins;
-                __stcs(&ocol[np], v[q]);
-                if (ow) __stcs(&ow[np], wv[q]);
-            }
-            dead_before += __popc(m[q]);
-        }
-        for (int64_t j = pjw + lane; j < pje; j += 32) {  // this window's inserted entries
-            int64_t P = ipos[j];
-            int64_t o = P - ws;
-            int qq = (int)(o >> 5), r = (int)(o & 31);
-            int64_t dead = dead0;
-#pragma unroll
-            for (int q = 0; q < kWin / 32; ++q)
-                dead += q < qq ? __popc(m[q]) : (q == qq ? __popc(m[q] & ((1u << r) - 1)) : 0);
-            int64_t np = P - dead + j;
-            ocol[np] = icol[j];
-            if (ow) ow[np] = iw ? iw[j] : 1;
-        }
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t nfull = nnz / kWin;
+    for (int64_t win = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; win < nwin; win += nwarps) {
+        if (win < nfull) edit_window<true>(col, w, nnz, win, dead_win, ipos, pj_win, icol, iw, ocol, ow);
+        else edit_window<false>(col, w, nnz, win, dead_win, ipos, pj_win, icol, iw, ocol, ow);
     }
 }
 
@@ -707,12 +723,12 @@ void edit_merge(cudaStream_t s, int64_t n, const int64_t* off, int32_t* col, con
     if (weighted) new_w.alloc(new_nnz, s);
     else new_w.release();
     if (ntiles) {
-        DBuf<int64_t> pj(ntiles + 1, s);
-        GD_KERNEL(k_tile_ins, grid_for(ntiles + 1, 256), 256, 0, s, ntiles, ipos, nins, pj.get());
+        DBuf<int64_t> pj(nwin + 1, s);
+        GD_KERNEL(k_win_ins, grid_for(nwin + 1, 256), 256, 0, s, nwin, ipos, nins, pj.get());
         unsigned g = (unsigned)std::min<int64_t>(ntiles, 148LL * 64);
         // algorithmic bytes: every base entry read once, every surviving entry written once
         GD_KERNEL_T("merge_copy", (nnz + (nnz - dead_total)) * (weighted ? 8 : 4), k_edit_base, g, kEditThreads, 0,
-                    s, col, weighted ? w : nullptr, nnz, dead_win.get(), ipos, pj.get(), icol, iw, ntiles,
+                    s, col, weighted ? w : nullptr, nnz, dead_win.get(), ipos, pj.get(), icol, iw, nwin,
                     new_col.get(), weighted ? new_w.get() : nullptr);
     }
     if (nins)
