@@ -288,15 +288,12 @@ def main():
     done = 0
     for i in range(args.warmup, args.warmup + args.steps):
         done += dev_step(i)
-        for name in KERNELS:
-            ms, nl, nb_ = algo.kernel_time(name)
-            if nl:
-                st = kstats.setdefault(name, [0.0, 0, 0])
-                st[0] += ms
-                st[1] += nl
-                st[2] += nb_
     ev1.record(stream)
     torch.cuda.synchronize()
+    for name in KERNELS:  # summed over the timed steps by the library
+        ms, nl, nb_ = algo.kernel_time(name, total=True)
+        if nl:
+            kstats[name] = [ms, nl, nb_]
     launches = gd._native.lib().gd_kernel_launches() - launches0
     clocks.mark(wall0, time.time())
     clk = clocks.stop()

@@ -167,7 +167,11 @@ GD_API int gd_iterations(const void* h, int64_t* total_iterations);
  * name = "pr_pull" | "tc_count" | "sssp_relax" | "merge" ...; ms summed over
  * the batch's launches of that kernel, launches = how many. */
 GD_API int gd_kernel_time(const void* h, const char* name, double* ms, int64_t* launches, int64_t* bytes);
-/* enable per-kernel event timing (off by default: it adds event records) */
+/* the same, summed over every batch since profiling was last switched on
+ * (one query after a timed loop instead of one per batch) */
+GD_API int gd_kernel_time_total(const void* h, const char* name, double* ms, int64_t* launches, int64_t* bytes);
+/* enable per-kernel event timing (off by default: it adds event records);
+ * switching it on clears the running totals */
 GD_API int gd_set_profiling(const void* h, int on);
 
 #ifdef __cplusplus

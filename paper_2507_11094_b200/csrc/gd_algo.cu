@@ -264,9 +264,29 @@ __global__ void k_aff_gather(const int32_t* p, int64_t n, int32_t* out, int m) {
         out[i] = p[(int64_t)((unsigned long long)i * 2654435761ULL % (unsigned long long)n)];
 }
 
+// the most frequent root among the probe samples (one CTA; ties -> smaller
+// root, as the host version chose the first of the sorted runs)
+__global__ void k_aff_giant(const int32_t* probe, int m, int32_t* giant) {
+    __shared__ int32_t sv[1024];
+    __shared__ unsigned long long best;
+    for (int i = threadIdx.x; i < m; i += blockDim.x) sv[i] = probe[i];
+    if (threadIdx.x == 0) best = ~0ULL;
+    __syncthreads();
+    for (int i = threadIdx.x; i < m; i += blockDim.x) {
+        int c = 0;
+        for (int j = 0; j < m; ++j) c += sv[j] == sv[i];
+        // max count first, then the smaller root: minimise (~count, root)
+        unsigned long long key = ((unsigned long long)(0xffffffffu - (unsigned)c) << 32) | (unsigned)sv[i];
+        atomicMin(&best, key);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) *giant = (int32_t)(best & 0xffffffffu);
+}
+
 // Vertices outside the dominant component link the rest of their out-arcs
 // (base after the sampled ones, then every delta) and all their in-arcs.
-__global__ void k_aff_rest(OutView ov, IdxView in, int64_t n, int32_t giant, int32_t* p) {
+__global__ void k_aff_rest(OutView ov, IdxView in, int64_t n, const int32_t* giant_p, int32_t* p) {
+    const int32_t giant = *giant_p;
     for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
         if (uf_find(p, (int32_t)v) == giant) continue;
         for (int sg = 0; sg < ov.nseg; ++sg) {
@@ -324,22 +344,9 @@ int64_t flood_weak_components(Store& g, uint8_t* flags, KernelProf* prof) {
     constexpr int kProbe = 1024;
     DBuf<int32_t> probe(kProbe, s);
     GD_KERNEL(k_aff_gather, 4, 256, 0, s, p.get(), n, probe.get(), kProbe);
-    std::vector<int32_t> h(kProbe);
-    GD_CUDA(cudaMemcpyAsync(h.data(), probe.get(), kProbe * 4, cudaMemcpyDeviceToHost, s));
-    GD_CUDA(cudaStreamSynchronize(s));
-    std::sort(h.begin(), h.end());
-    int32_t giant = h[0];
-    int best = 0;
-    for (int i = 0; i < kProbe;) {
-        int j = i;
-        while (j < kProbe && h[j] == h[i]) ++j;
-        if (j - i > best) {
-            best = j - i;
-            giant = h[i];
-        }
-        i = j;
-    }
-    GD_KERNEL_T("flood_rest", 0, k_aff_rest, grid_for(n, 256), 256, 0, s, ov, in, n, giant, p.get());
+    DBuf<int32_t> giant(1, s);
+    GD_KERNEL(k_aff_giant, 1, 1024, 0, s, probe.get(), kProbe, giant.get());
+    GD_KERNEL_T("flood_rest", 0, k_aff_rest, grid_for(n, 256), 256, 0, s, ov, in, n, giant.get(), p.get());
     GD_KERNEL_T("flood_mark", 0, k_uf_compress_seed, grid_for(n, 256), 256, 0, s, p.get(), n, flags, seed.get());
     GD_KERNEL(k_uf_mark, grid_for(n, 256), 256, 0, s, p.get(), n, seed.get(), flags);
     return 1;

@@ -39,12 +39,16 @@ thread_local KernelProf* tl_prof = nullptr;
 int prof_begin(const char* name, int64_t bytes, cudaStream_t s) {
     KernelProf* p = tl_prof;
     if (!p || !p->on) return -1;
-    KernelProf::Rec r{name, nullptr, nullptr, bytes};
+    KernelProf::Rec r{name, nullptr, nullptr, bytes, -1};
     GD_CUDA(cudaEventCreate(&r.a));
     GD_CUDA(cudaEventCreate(&r.b));
     GD_CUDA(cudaEventRecord(r.a, s));
     p->pending.push_back(r);
     return (int)p->pending.size() - 1;
+}
+
+void prof_tag(int idx, int64_t tag) {
+    if (idx >= 0 && tl_prof) tl_prof->pending[(size_t)idx].tag = tag;
 }
 
 void prof_end(int idx, cudaStream_t s) {
@@ -56,16 +60,21 @@ void prof_end(int idx, cudaStream_t s) {
 void KernelProf::flush() {
     for (auto& r : pending) {
         GD_CUDA(cudaEventSynchronize(r.b));
-        float ms = 0;
-        GD_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
-        KernelStat& k = last[r.name];
-        k.ms += ms;
-        k.launches += 1;
-        k.bytes += r.bytes;
+        if (r.tag < 0 || r.tag < sweep_limit) {
+            float ms = 0;
+            GD_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
+            int64_t bytes = r.bytes;
+            for (KernelStat* k : {&last[r.name], &total[r.name]}) {
+                k->ms += ms;
+                k->launches += 1;
+                k->bytes += bytes;
+            }
+        }
         cudaEventDestroy(r.a);
         cudaEventDestroy(r.b);
     }
     pending.clear();
+    sweep_limit = INT64_MAX;
 }
 
 KernelProf::~KernelProf() {
@@ -519,9 +528,22 @@ int gd_kernel_time(const void* h, const char* name, double* ms, int64_t* launche
     return ok();
 }
 
+int gd_kernel_time_total(const void* h, const char* name, double* ms, int64_t* launches, int64_t* bytes) {
+    if (!h) return null_handle();
+    gdb::AlgoBase* a = algo_of(h);
+    auto it = a->prof.total.find(name);
+    bool hit = it != a->prof.total.end();
+    *ms = hit ? it->second.ms : 0;
+    *launches = hit ? it->second.launches : 0;
+    if (bytes) *bytes = hit ? it->second.bytes : 0;
+    return ok();
+}
+
 int gd_set_profiling(const void* h, int on) {
     if (!h) return null_handle();
-    algo_of(h)->prof.on = on != 0;
+    gdb::KernelProf& p = algo_of(h)->prof;
+    if (on && !p.on) p.total.clear();
+    p.on = on != 0;
     return ok();
 }
 

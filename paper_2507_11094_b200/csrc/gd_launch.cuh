@@ -30,9 +30,12 @@ struct KernelProf {
         const char* name;
         cudaEvent_t a, b;
         int64_t bytes;
+        int64_t tag;  // >= 0: queued sweep index; dropped when >= sweep_limit
     };
     std::vector<Rec> pending;
-    std::map<std::string, KernelStat> last;  // stats of the last flushed call
+    int64_t sweep_limit = INT64_MAX;  // sweeps that actually ran (the rest were device no-ops)
+    std::map<std::string, KernelStat> last;   // stats of the last flushed call
+    std::map<std::string, KernelStat> total;  // since profiling was switched on
     void reset_last() { last.clear(); }
     void flush();  // sync on the recorded events and fold them into `last`
     ~KernelProf();
@@ -47,6 +50,9 @@ struct ProfScope {
 };
 
 int prof_begin(const char* name, int64_t bytes, cudaStream_t s);
+// marks a recorded launch as part of queued sweep `tag` (dropped at flush
+// when the sweep turned out to be a device no-op)
+void prof_tag(int idx, int64_t tag);
 void prof_end(int idx, cudaStream_t s);
 
 }  // namespace gdb

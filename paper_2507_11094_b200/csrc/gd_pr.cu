@@ -26,8 +26,15 @@ __global__ void k_pr_init(double* rank, int64_t n, double v) {
 
 // contrib[u] = rank[u] / outdeg[u]; per-block partial of the dangling sum
 // (outdeg == 0) -- pr_dynamic_omp.cc:68-73.
+// Device control block of the sweep loop (no host round trip per sweep):
+// ctl[0..2] bin sizes, ctl[3..5] in-arcs per bin, ctl[6] done, ctl[7] sweeps.
+// Sweeps are enqueued ahead; once ctl[6] is set, the queued ones return at
+// their first instruction.
+enum { C_NBIN = 0, C_EBIN = 3, C_DONE = 6, C_SWEEPS = 7, C_LEN = 8 };
+
 __global__ void __launch_bounds__(256) k_pr_contrib(const double* rank, const int32_t* outdeg, int64_t n,
-                                                    double* contrib, double* partial) {
+                                                    double* contrib, double* partial, const int64_t* ctl) {
+    if (ctl && ctl[C_DONE]) return;
     double acc = 0.0;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         double r = rank[i];
@@ -46,8 +53,10 @@ __global__ void __launch_bounds__(256) k_pr_contrib(const double* rank, const in
     }
 }
 
-// deterministic final sum of the partials (fixed order)
-__global__ void k_sum_partials(const double* partial, int np, double* out) {
+// deterministic final sum of the partials (fixed order); clears the sweep's
+// residual
+__global__ void k_sum_partials(const double* partial, int np, double* out, const int64_t* ctl) {
+    if (ctl && ctl[C_DONE]) return;
     __shared__ double sh[1024];
     double t = 0.0;
     for (int i = threadIdx.x; i < np; i += blockDim.x) t += partial[i];
@@ -57,7 +66,10 @@ __global__ void k_sum_partials(const double* partial, int np, double* out) {
         if ((int)threadIdx.x < s) sh[threadIdx.x] += sh[threadIdx.x + s];
         __syncthreads();
     }
-    if (threadIdx.x == 0) *out = sh[0];
+    if (threadIdx.x == 0) {
+        out[0] = sh[0];
+        out[1] = 0.0;
+    }
 }
 
 __device__ inline double atomic_max_pos(double* a, double v) {  // v >= 0
@@ -97,11 +109,13 @@ __device__ inline double row_sum(const int32_t* __restrict__ col, int64_t a, int
 }
 
 template <int G>
-__global__ void __launch_bounds__(kPullThreads) k_pr_pull_group(const int32_t* list, int64_t m, IdxView ix,
-                                                                  const double* contrib, const double* rank,
-                                                                  const double* dangling, double base,
-                                                                  double damping, double inv_n, double* rank_new,
-                                                                  double* diff) {
+__global__ void __launch_bounds__(kPullThreads) k_pr_pull_group(const int32_t* list, const int64_t* ctl, int bin,
+                                                                  IdxView ix, const double* contrib,
+                                                                  const double* rank, const double* dangling,
+                                                                  double base, double damping, double inv_n,
+                                                                  double* rank_new, double* diff) {
+    if (ctl[C_DONE]) return;
+    const int64_t m = ctl[C_NBIN + bin];
     const int lane = threadIdx.x & (G - 1);
     const int gw = (threadIdx.x & 31) / G;
     constexpr int kPer = 32 / G;
@@ -127,10 +141,12 @@ __global__ void __launch_bounds__(kPullThreads) k_pr_pull_group(const int32_t* l
     if ((threadIdx.x & 31) == 0 && dmax > 0.0) atomic_max_pos(diff, dmax);
 }
 
-__global__ void __launch_bounds__(kHubThreads) k_pr_pull_hub(const int32_t* list, int64_t m, IdxView ix,
+__global__ void __launch_bounds__(kHubThreads) k_pr_pull_hub(const int32_t* list, const int64_t* ctl, IdxView ix,
                                                               const double* contrib, const double* rank,
                                                               const double* dangling, double base, double damping,
                                                               double inv_n, double* rank_new, double* diff) {
+    if (ctl[C_DONE]) return;
+    const int64_t m = ctl[C_NBIN + 2];
     __shared__ double sh[kHubThreads / 32];
     const double dn = *dangling * inv_n;
     for (int64_t t = blockIdx.x; t < m; t += gridDim.x) {
@@ -151,11 +167,23 @@ __global__ void __launch_bounds__(kHubThreads) k_pr_pull_hub(const int32_t* list
     }
 }
 
-__global__ void k_pr_commit(const int32_t* list, int64_t m, const double* rank_new, double* rank) {
+// Jacobi commit of all three bins
+__global__ void k_pr_commit(const int32_t* b0, const int32_t* b1, const int32_t* b2, const int64_t* ctl,
+                            const double* rank_new, double* rank) {
+    if (ctl[C_DONE]) return;
+    const int64_t n0 = ctl[C_NBIN], n1 = ctl[C_NBIN + 1], m = n0 + n1 + ctl[C_NBIN + 2];
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
-        int32_t v = list[i];
+        int32_t v = i < n0 ? b0[i] : (i < n0 + n1 ? b1[i - n0] : b2[i - n0 - n1]);
         rank[v] = rank_new[v];
     }
+}
+
+// while (diff >= beta && iter < maxiter): decide on the device whether the
+// next queued sweep runs
+__global__ void k_pr_check(int64_t* ctl, const double* diff, double beta, int64_t maxiter) {
+    if (ctl[C_DONE]) return;
+    int64_t it = ++ctl[C_SWEEPS];
+    if (!(*diff >= beta && it < maxiter)) ctl[C_DONE] = 1;
 }
 
 // OnDelete / OnAdd handlers (pr_dynamic.sp:87-97): mark both endpoints,
@@ -169,24 +197,63 @@ __global__ void k_pr_onupdate(const int32_t* s, const int32_t* d, int64_t k, int
     }
 }
 
-// in-arcs of each bin (for the roofline's algorithmic bytes)
-__global__ void k_bin_arcs(const int32_t* list, int64_t m, const int64_t* off, unsigned long long* sums) {
-    unsigned long long a[3] = {0, 0, 0};
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
-        int32_t v = list[i];
-        int64_t d = off[v + 1] - off[v];
-        a[d <= kLightMax ? 0 : (d <= kMediumMax ? 1 : 2)] += (unsigned long long)d;
-    }
-    for (int k = 0; k < 3; ++k) {
-        unsigned long long x = a[k];
-        for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-        if ((threadIdx.x & 31) == 0 && x) atomicAdd(&sums[k], x);
-    }
-}
+// affected vertices of [lo, hi) into the three in-degree bins, plus the
+// in-arcs per bin.  A CTA stages a 2048-vertex chunk's bin entries in shared
+// memory and claims each bin's output range with one atomic, so the three
+// global counters see a few thousand atomics, not one per warp.  Bin order
+// does not matter: every vertex's sum is computed on its own, in a fixed
+// order.  flags == nullptr: every vertex (staticPR).
+constexpr int kBinThreads = 256;
+constexpr int kBinChunk = 2048;
 
-__global__ void k_gather_list(const int32_t* list, const int32_t* sel, int64_t m, int32_t* out) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
-        out[i] = list[sel[i]];
+__global__ void __launch_bounds__(kBinThreads) k_pr_bin(const uint8_t* flags, int64_t lo, int64_t hi,
+                                                        const int64_t* off, int32_t* b0, int32_t* b1, int32_t* b2,
+                                                        int64_t* ctl) {
+    __shared__ int32_t stage[3][kBinChunk];
+    __shared__ int cnt[3];
+    __shared__ unsigned long long gbase[3];
+    const int lane = threadIdx.x & 31;
+    unsigned long long e[3] = {0, 0, 0};
+    for (int64_t c0 = lo + (int64_t)blockIdx.x * kBinChunk; c0 < hi; c0 += (int64_t)gridDim.x * kBinChunk) {
+        if (threadIdx.x < 3) cnt[threadIdx.x] = 0;
+        __syncthreads();
+#pragma unroll 2
+        for (int j = threadIdx.x; j < kBinChunk; j += kBinThreads) {
+            int64_t v = c0 + j;
+            bool in = v < hi && (!flags || flags[v]);
+            int64_t d = in ? off[v + 1] - off[v] : 0;
+            int b = d <= kLightMax ? 0 : (d <= kMediumMax ? 1 : 2);
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                unsigned mk = __ballot_sync(0xffffffffu, in && b == k);
+                if (!mk) continue;
+                int base = 0;
+                if (lane == 0) base = atomicAdd(&cnt[k], __popc(mk));
+                base = __shfl_sync(0xffffffffu, base, 0);
+                if (in && b == k) {
+                    stage[k][base + __popc(mk & ((1u << lane) - 1))] = (int32_t)v;
+                    e[k] += (unsigned long long)d;
+                }
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x < 3 && cnt[threadIdx.x])
+            gbase[threadIdx.x] = atomicAdd(reinterpret_cast<unsigned long long*>(&ctl[C_NBIN + threadIdx.x]),
+                                           (unsigned long long)cnt[threadIdx.x]);
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            int32_t* out = k == 0 ? b0 : (k == 1 ? b1 : b2);
+            for (int j = threadIdx.x; j < cnt[k]; j += kBinThreads) out[gbase[k] + j] = stage[k][j];
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        unsigned long long x = e[k];
+        for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+        if (lane == 0 && x) atomicAdd(reinterpret_cast<unsigned long long*>(&ctl[C_EBIN + k]), x);
+    }
 }
 
 }  // namespace
@@ -203,27 +270,18 @@ PR::PR(Store* st, double d, double b, int64_t mi) : AlgoBase(ALGO_PR, st), dampi
     affected.alloc(std::max<int64_t>(n, 1), s);
     partial.alloc(kRedBlocks, s);
     scal.alloc(2, s);  // [0] dangling, [1] diff
+    ctl.alloc(C_LEN, s);
+    for (auto* l : {&bins[0], &bins[1], &bins[2]}) l->alloc(std::max<int64_t>(n, 1), s);
     ProfScope ps(&prof);
     timer.begin(PH_STATIC);
     if (n) {
         GD_KERNEL(k_pr_init, grid_for(n, 256), 256, 0, s, rank.get(), n, 1.0 / (double)n);
         out_degrees(*g, outdeg.get());
     }
-    // staticPR: every node participates
-    DBuf<int32_t> all(n, s);
-    iota_i32(s, all.get(), n);
-    set_lists(all.get(), n);
-    power_loop();
+    recompute(nullptr);  // staticPR: every node participates
     timer.end_all();
     prof.flush();
 }
-
-namespace {
-__global__ void k_range_bounds(const int32_t* list, int64_t m, int32_t lo, int32_t hi, int64_t* out) {
-    if (threadIdx.x == 0) out[0] = lower_bound_dev<int32_t>(list, 0, m, lo);
-    if (threadIdx.x == 1) out[1] = lower_bound_dev<int32_t>(list, 0, m, hi);
-}
-}  // namespace
 
 void PR::set_comm(Comm* c) {
     cudaStream_t s = stream();
@@ -244,89 +302,101 @@ void PR::set_comm(Comm* c) {
     GD_CUDA(cudaStreamSynchronize(s));
 }
 
-void PR::set_lists(const int32_t* list, int64_t m) {
+// One sweep (pr_dynamic_omp.cc:66-99): dangling mass + contrib over all V,
+// the pull over the affected bins, the Jacobi commit, then (multi-GPU) the
+// rank all-gather and the residual max, and the device-side loop test.
+void PR::sweep(int64_t tag) {
     cudaStream_t s = stream();
-    g->compact_rev();
-    if (comm && m) {  // the list is ascending: keep the owned destination range
-        DBuf<int64_t> b(2, s);
-        GD_KERNEL(k_range_bounds, 1, 32, 0, s, list, m, (int32_t)comm->lo(g->n), (int32_t)comm->hi(g->n), b.get());
-        int64_t hb[2];
-        GD_CUDA(cudaMemcpyAsync(hb, b.get(), sizeof hb, cudaMemcpyDeviceToHost, s));
-        GD_CUDA(cudaStreamSynchronize(s));
-        list += hb[0];
-        m = hb[1] - hb[0];
-    }
-    for (auto* l : {&bins[0], &bins[1], &bins[2]}) l->ensure(std::max<int64_t>(m, 1), s);
-    nbin[0] = nbin[1] = nbin[2] = 0;
-    ebin[0] = ebin[1] = ebin[2] = 0;
-    if (!m) return;
-    DBuf<int> cnt(2, s);
-    DBuf<unsigned long long> sums(3, s);
-    sums.zero(s);
-    partition3_by_degree(s, list, m, g->rev.off.get(), kLightMax, kMediumMax, bins[0].get(), bins[1].get(),
-                         bins[2].get(), cnt.get());
-    GD_KERNEL(k_bin_arcs, grid_for(m, 256, 148LL * 8), 256, 0, s, list, m, g->rev.off.get(), sums.get());
-    int hc[2];
-    unsigned long long hs[3];
-    GD_CUDA(cudaMemcpyAsync(hc, cnt.get(), sizeof hc, cudaMemcpyDeviceToHost, s));
-    GD_CUDA(cudaMemcpyAsync(hs, sums.get(), sizeof hs, cudaMemcpyDeviceToHost, s));
-    GD_CUDA(cudaStreamSynchronize(s));
-    nbin[0] = hc[0];
-    nbin[1] = hc[1];
-    nbin[2] = m - hc[0] - hc[1];
-    for (int k = 0; k < 3; ++k) ebin[k] = (int64_t)hs[k];
-}
-
-// while (diff >= beta && iter < maxiter) { dangling; pull; commit }
-void PR::power_loop() {
-    cudaStream_t s = stream();
-    int64_t n = g->n;
-    if (n == 0) return;
+    const int64_t n = g->n;
     IdxView ix = g->rev.view();
     const double base = (1.0 - damping) / (double)n;
     const double inv_n = 1.0 / (double)n;
-    int64_t iter = 0;
-    double diff = beta + 1.0;
-    last_sweeps = 0;
-    while (diff >= beta && iter < maxiter) {
-        GD_KERNEL_T("pr_contrib", n * 20, k_pr_contrib, kRedBlocks, 256, 0, s, rank.get(), outdeg.get(), n,
-                    contrib.get(), partial.get());
-        GD_KERNEL(k_sum_partials, 1, 1024, 0, s, partial.get(), kRedBlocks, scal.get());
-        GD_CUDA(cudaMemsetAsync(scal.get() + 1, 0, sizeof(double), s));
-        // algorithmic bytes: |A| (off + 2 f64) + E_in(A) (idx + f64)
-        if (nbin[0])
-            GD_KERNEL_T("pr_pull", nbin[0] * 24 + ebin[0] * 12, k_pr_pull_group<2>,
-                        grid_for(((nbin[0] + 15) / 16) * 32, kPullThreads, 148LL * 32), kPullThreads, 0, s,
-                        bins[0].get(), nbin[0], ix, contrib.get(), rank.get(), scal.get(), base, damping, inv_n,
-                        rank_new.get(), scal.get() + 1);
-        if (nbin[1])
-            GD_KERNEL_T("pr_pull", nbin[1] * 24 + ebin[1] * 12, k_pr_pull_group<16>,
-                        grid_for(((nbin[1] + 1) / 2) * 32, kPullThreads, 148LL * 32), kPullThreads, 0, s, bins[1].get(),
-                        nbin[1], ix, contrib.get(), rank.get(), scal.get(), base, damping, inv_n, rank_new.get(),
-                        scal.get() + 1);
-        if (nbin[2])
-            GD_KERNEL_T("pr_pull", nbin[2] * 24 + ebin[2] * 12, k_pr_pull_hub,
-                        (unsigned)std::min<int64_t>(nbin[2], 148LL * 4), kHubThreads, 0, s, bins[2].get(), nbin[2],
-                        ix, contrib.get(), rank.get(), scal.get(), base, damping, inv_n, rank_new.get(),
-                        scal.get() + 1);
-        for (int k = 0; k < 3; ++k)
-            if (nbin[k])
-                GD_KERNEL(k_pr_commit, grid_for(nbin[k], 256), 256, 0, s, bins[k].get(), nbin[k], rank_new.get(),
-                          rank.get());
-        if (comm) {  // every rank gets every owned range; the residual is the max over ranks
-            comm->allgather_f64(rank.get(), comm->chunk(n), s);
-            comm->allreduce_max_f64(scal.get() + 1, 1, s);
-        }
-        diff = read_scalar(s, scal.get() + 1);
-        ++iter;
+    int64_t* c = ctl.get();
+    int pc = prof_begin("pr_contrib", n * 20, s);
+    prof_tag(pc, tag);
+    k_pr_contrib<<<kRedBlocks, 256, 0, s>>>(rank.get(), outdeg.get(), n, contrib.get(), partial.get(), c);
+    count_launch();
+    GD_LAUNCH_CHECK();
+    prof_end(pc, s);
+    GD_KERNEL(k_sum_partials, 1, 1024, 0, s, partial.get(), kRedBlocks, scal.get(), c);
+    // algorithmic bytes: |A| (off + 2 f64) + E_in(A) (idx + f64), filled in from the bin
+    // counts once the loop has read them back
+    int pi = prof_begin("pr_pull", 0, s);
+    prof_tag(pi, tag);
+    pull_recs.push_back({pi, 0});
+    k_pr_pull_group<2><<<148 * 16, kPullThreads, 0, s>>>(bins[0].get(), c, 0, ix, contrib.get(), rank.get(),
+                                                         scal.get(), base, damping, inv_n, rank_new.get(),
+                                                         scal.get() + 1);
+    count_launch();
+    GD_LAUNCH_CHECK();
+    prof_end(pi, s);
+    pi = prof_begin("pr_pull", 0, s);
+    prof_tag(pi, tag);
+    pull_recs.push_back({pi, 1});
+    k_pr_pull_group<16><<<148 * 16, kPullThreads, 0, s>>>(bins[1].get(), c, 1, ix, contrib.get(), rank.get(),
+                                                          scal.get(), base, damping, inv_n, rank_new.get(),
+                                                          scal.get() + 1);
+    count_launch();
+    GD_LAUNCH_CHECK();
+    prof_end(pi, s);
+    pi = prof_begin("pr_pull", 0, s);
+    prof_tag(pi, tag);
+    pull_recs.push_back({pi, 2});
+    k_pr_pull_hub<<<148 * 2, kHubThreads, 0, s>>>(bins[2].get(), c, ix, contrib.get(), rank.get(), scal.get(), base,
+                                                  damping, inv_n, rank_new.get(), scal.get() + 1);
+    count_launch();
+    GD_LAUNCH_CHECK();
+    prof_end(pi, s);
+    GD_KERNEL(k_pr_commit, 148 * 8, 256, 0, s, bins[0].get(), bins[1].get(), bins[2].get(), c, rank_new.get(),
+              rank.get());
+    if (comm) {  // every rank gets every owned range; the residual is the max over ranks
+        comm->allgather_f64(rank.get(), comm->chunk(n), s);
+        comm->allreduce_max_f64(scal.get() + 1, 1, s);
     }
-    last_sweeps = iter;
-    iterations += iter;
+    GD_KERNEL(k_pr_check, 1, 1, 0, s, c, scal.get() + 1, beta, maxiter);
+}
+
+// Bin the affected vertices (flags == nullptr: all) of this rank's range
+// and run the sweep loop.  Sweeps are queued `ahead` at a time and the
+// device-side test turns the surplus into no-ops, so the host reads the loop
+// state once per group instead of once per sweep.
+void PR::recompute(const uint8_t* flags) {
+    cudaStream_t s = stream();
+    const int64_t n = g->n;
+    last_sweeps = 0;
+    if (n == 0) return;
+    g->compact_rev();
+    GD_CUDA(cudaMemsetAsync(ctl.get(), 0, C_LEN * sizeof(int64_t), s));
+    if (maxiter <= 0) return;
+    const int64_t lo = comm ? comm->lo(n) : 0, hi = comm ? comm->hi(n) : n;
+    if (hi > lo)
+        GD_KERNEL(k_pr_bin, (unsigned)std::min<int64_t>((hi - lo + kBinChunk - 1) / kBinChunk, 148LL * 8),
+                  kBinThreads, 0, s, flags, lo, hi, g->rev.off.get(), bins[0].get(), bins[1].get(), bins[2].get(),
+                  ctl.get());
+    int64_t done = 0, sweeps = 0;
+    int64_t hctl[C_LEN];
+    pull_recs.clear();
+    while (!done) {
+        const int64_t ahead = std::max<int64_t>(2, std::min<int64_t>(ahead_hint, 16));
+        for (int64_t k = 0; k < ahead; ++k) sweep(sweeps + k);
+        GD_CUDA(cudaMemcpyAsync(hctl, ctl.get(), sizeof hctl, cudaMemcpyDeviceToHost, s));
+        GD_CUDA(cudaStreamSynchronize(s));
+        done = hctl[C_DONE];
+        sweeps = hctl[C_SWEEPS];
+    }
+    ahead_hint = sweeps;  // sweep counts are stable batch to batch: usually one read-back
+    last_sweeps = sweeps;
+    iterations += sweeps;
+    prof.sweep_limit = sweeps;  // queued no-op sweeps are not launches of the path
+    for (auto& pr : pull_recs)
+        if (pr.first >= 0) prof.pending[(size_t)pr.first].bytes = 24 * hctl[C_NBIN + pr.second] + 12 * hctl[C_EBIN + pr.second];
+    int64_t a = 0;
+    for (int k = 0; k < 3; ++k) a += hctl[C_NBIN + k];
+    last_affected = flags ? a : n;
 }
 
 void PR::batch(DevBatch& b, int64_t batch_index) {
     cudaStream_t s = stream();
-    int64_t n = g->n;
     ProfScope ps(&prof);
     prof.reset_last();
     timer.begin(PH_PRE);
@@ -346,11 +416,7 @@ void PR::batch(DevBatch& b, int64_t batch_index) {
     }
     timer.begin(PH_PROP);
     flood_weak_components(*g, affected.get(), &prof);
-    DBuf<int32_t> list(std::max<int64_t>(n, 1), s);
-    int64_t m = select_flagged_index(s, affected.get(), n, list.get());
-    last_affected = m;
-    set_lists(list.get(), m);
-    power_loop();
+    recompute(affected.get());
     timer.end_all();
     prof.flush();
 }

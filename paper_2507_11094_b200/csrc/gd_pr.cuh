@@ -1,6 +1,9 @@
 // gd_pr.cuh -- dynamic PageRank state (programs/pr_dynamic.sp).
 #pragma once
 
+#include <utility>
+#include <vector>
+
 #include "gd_algo.cuh"
 #include "gd_comm.cuh"
 
@@ -13,9 +16,10 @@ struct PR : AlgoBase {
     DBuf<int32_t> outdeg;  // maintained per record (misses included), int32 on device
     DBuf<uint8_t> affected;
     DBuf<int32_t> bins[3];            // affected vertices by in-degree: light / medium / hub
-    int64_t nbin[3] = {0, 0, 0};
-    int64_t ebin[3] = {0, 0, 0};      // in-arcs per bin (roofline bytes)
+    DBuf<int64_t> ctl;                // device loop state: bin sizes, bin in-arcs, done, sweeps
+    int64_t ahead_hint = 4;           // sweeps to queue per read-back (last batch's count + 1)
     int64_t last_sweeps = 0, last_affected = 0;
+    std::vector<std::pair<int, int>> pull_recs;  // (profiler record, bin) of the queued pull launches
 
     Comm* comm = nullptr;  // set: pull only the owned destination range, all-gather ranks
 
@@ -25,8 +29,8 @@ struct PR : AlgoBase {
     void read(double* rank, int64_t* outdeg);
 
   private:
-    void set_lists(const int32_t* list, int64_t m);
-    void power_loop();
+    void recompute(const uint8_t* flags);  // bin + sweep loop; flags == nullptr: all vertices
+    void sweep(int64_t tag);
 };
 
 }  // namespace gdb

@@ -182,9 +182,12 @@ class _Algo:
     def set_profiling(self, on: bool) -> None:
         N.check(N.lib().gd_set_profiling(self.h, int(on)))
 
-    def kernel_time(self, name: str):
+    def kernel_time(self, name: str, total: bool = False):
+        """(ms, launches, algorithmic bytes) of `name` in the last batch, or
+        summed since profiling was switched on (total=True)."""
         ms, n, b = C.c_double(), C.c_int64(), C.c_int64()
-        N.check(N.lib().gd_kernel_time(self.h, name.encode(), C.byref(ms), C.byref(n), C.byref(b)))
+        fn = N.lib().gd_kernel_time_total if total else N.lib().gd_kernel_time
+        N.check(fn(self.h, name.encode(), C.byref(ms), C.byref(n), C.byref(b)))
         return ms.value, n.value, b.value
 
     def __del__(self):
