@@ -119,8 +119,7 @@ void AlgoBase::stage_host(DevBatch& b, const uint8_t* kind, const int64_t* src, 
     select_flagged_index_async(st, flags.get(), k, sel_del.get(), hdr.get() + 2);
     select_flagged_index_async(st, flags.get() + k, k, sel_add.get(), hdr.get() + 3);
     int64_t h[4];
-    GD_CUDA(cudaMemcpyAsync(h, hdr.get(), sizeof h, cudaMemcpyDeviceToHost, st));
-    GD_CUDA(cudaStreamSynchronize(st));
+    read_small(st, h, hdr.get(), sizeof h);
     int e = (int)(h[0] & 0xffffffff);
     if (e) {
         unsigned long long i = (unsigned long long)h[1];
@@ -146,8 +145,7 @@ void AlgoBase::stage_device(DevBatch& b, const uint8_t* kind, const int32_t* src
     select_flagged_index_async(st, flags.get(), k, sel_del.get(), hdr.get() + 2);
     select_flagged_index_async(st, flags.get() + k, k, sel_add.get(), hdr.get() + 3);
     int64_t h[4];
-    GD_CUDA(cudaMemcpyAsync(h, hdr.get(), sizeof h, cudaMemcpyDeviceToHost, st));
-    GD_CUDA(cudaStreamSynchronize(st));
+    read_small(st, h, hdr.get(), sizeof h);
     int e = (int)(h[0] & 0xffffffff);
     if (e) {
         unsigned long long i = (unsigned long long)h[1];

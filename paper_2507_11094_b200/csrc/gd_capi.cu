@@ -247,7 +247,7 @@ int gd_graph_apply_deletes(gd_graph* g, const int64_t* src, const int64_t* dst, 
         check_ids(src, dst, k, st.n);
         HostIds h = upload_ids(st.stream, src, dst, nullptr, k);
         gdb::DBuf<uint8_t> found(k, st.stream);
-        int64_t a = st.apply_deletes(h.s.get(), h.d.get(), k, found.get());
+        int64_t a = st.apply_deletes(h.s.get(), h.d.get(), k, found.get(), true);
         if (miss_flags && k) {
             GD_CUDA(cudaMemcpyAsync(miss_flags, found.get(), k, cudaMemcpyDeviceToHost, st.stream));
             GD_CUDA(cudaStreamSynchronize(st.stream));
@@ -283,7 +283,7 @@ int gd_graph_merge(gd_graph* g) {
 int gd_graph_stats(gd_graph* g, int64_t* live, int64_t* nseg, int64_t* slots) {
     if (!g) return null_handle();
     return guard([&] {
-        if (live) *live = g->st->live;
+        if (live) *live = g->st->live_count();
         if (nseg) *nseg = (int64_t)g->st->segs.size();
         if (slots) *slots = g->st->total_slots();
     });

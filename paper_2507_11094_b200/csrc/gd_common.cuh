@@ -173,11 +173,15 @@ void partition3_by_degree(cudaStream_t s, const int32_t* list, int64_t m, const 
 void iota_i32(cudaStream_t s, int32_t* a, int64_t n);
 void fill_i64(cudaStream_t s, int64_t* a, int64_t n, int64_t v);
 void fill_i32(cudaStream_t s, int32_t* a, int64_t n, int32_t v);
+// Small device -> host reads (counts, flags) through a per-thread pinned
+// staging buffer: a pageable destination costs an extra staged copy and
+// several microseconds of latency at every such sync point.
+void read_small(cudaStream_t s, void* host, const void* dev, size_t bytes);
+
 template <typename T>
 inline T read_scalar(cudaStream_t s, const T* dptr) {
     T h{};
-    GD_CUDA(cudaMemcpyAsync(&h, dptr, sizeof(T), cudaMemcpyDeviceToHost, s));
-    GD_CUDA(cudaStreamSynchronize(s));
+    read_small(s, &h, dptr, sizeof(T));
     return h;
 }
 

@@ -379,8 +379,7 @@ void PR::recompute(const uint8_t* flags) {
     while (!done) {
         const int64_t ahead = std::max<int64_t>(2, std::min<int64_t>(ahead_hint, 16));
         for (int64_t k = 0; k < ahead; ++k) sweep(sweeps + k);
-        GD_CUDA(cudaMemcpyAsync(hctl, ctl.get(), sizeof hctl, cudaMemcpyDeviceToHost, s));
-        GD_CUDA(cudaStreamSynchronize(s));
+        read_small(s, hctl, ctl.get(), sizeof hctl);
         done = hctl[C_DONE];
         sweeps = hctl[C_SWEEPS];
     }

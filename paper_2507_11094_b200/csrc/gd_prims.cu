@@ -1,3 +1,4 @@
+#include <cstring>
 // gd_prims.cu -- device-wide sort / scan / select primitives (CUB, stream-ordered).
 #include <cub/cub.cuh>
 #include <thrust/iterator/counting_iterator.h>
@@ -79,6 +80,20 @@ void inclusive_scan_i64(cudaStream_t s, const int64_t* in, int64_t* out, int64_t
     Temp t(bytes, s);
     GD_CUDA(cub::DeviceScan::InclusiveSum(t.p, bytes, in, out, n, s));
     count_library_launch();
+}
+
+void read_small(cudaStream_t s, void* host, const void* dev, size_t bytes) {
+    constexpr size_t kCap = 4096;
+    static thread_local void* pin = nullptr;
+    if (bytes > kCap) {
+        GD_CUDA(cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, s));
+        GD_CUDA(cudaStreamSynchronize(s));
+        return;
+    }
+    if (!pin) GD_CUDA(cudaMallocHost(&pin, kCap));
+    GD_CUDA(cudaMemcpyAsync(pin, dev, bytes, cudaMemcpyDeviceToHost, s));
+    GD_CUDA(cudaStreamSynchronize(s));
+    memcpy(host, pin, bytes);
 }
 
 int64_t sum_i64(cudaStream_t s, const int64_t* in, int64_t n) {

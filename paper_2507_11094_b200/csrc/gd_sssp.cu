@@ -615,8 +615,7 @@ SSSP::SSSP(Store* st, int64_t s) : AlgoBase(ALGO_SSSP, st), src((int32_t)s) {
         GD_KERNEL(k_wsum, grid_for(g->segs[0].nslots, 256, 148 * 8), 256, 0, cs, g->segs[0].col.get(),
                   g->segs[0].w.get(), g->segs[0].nslots, acc.get());
         unsigned long long h[2];
-        GD_CUDA(cudaMemcpyAsync(h, acc.get(), sizeof(h), cudaMemcpyDeviceToHost, cs));
-        GD_CUDA(cudaStreamSynchronize(cs));
+        read_small(cs, h, acc.get(), sizeof(h));
         if (h[1]) delta = std::max<int64_t>(1, (int64_t)(3 * h[0] / h[1]));
     }
     if (const char* e = getenv("GD_SSSP_DELTA")) delta = atoll(e);
@@ -697,8 +696,7 @@ void SSSP::fix_parents(const int32_t* list, const int64_t* d_m, int64_t m) {
 // one read-back per batch: total rounds and the divergence flag
 void SSSP::finish() {
     long long h[6];
-    GD_CUDA(cudaMemcpyAsync(h, ctr.get(), sizeof(h), cudaMemcpyDeviceToHost, stream()));
-    GD_CUDA(cudaStreamSynchronize(stream()));
+    read_small(stream(), h, ctr.get(), sizeof(h));
     static const bool dbg = getenv("GD_SSSP_DEBUG") != nullptr;
     if (dbg)
         fprintf(stderr, "[sssp] rounds %lld (+%lld) visits %lld pieces %lld splits %lld\n", h[1], h[1] - iterations,

@@ -187,11 +187,11 @@ __global__ void k_widen(const int32_t* a, int64_t m, uint64_t* o) {
 struct MatchOut {
     unsigned long long* sel;  // per request: min gid (pairs with one request)
     const uint8_t* single;    // per request: its key has exactly one request
-    uint64_t* okey;
+    uint64_t* okey;           // overflow matches: pair key, chain offset, gid
+    int64_t* ochain;
     int32_t* ogid;
     unsigned long long* ocnt;
     int64_t cap;
-    int rb;
 };
 
 __device__ inline void emit_matches(const MatchOut& mo, int64_t p, int32_t row, int32_t c, int sh, int64_t chain,
@@ -207,7 +207,8 @@ __device__ inline void emit_matches(const MatchOut& mo, int64_t p, int32_t row, 
     if (multi) {
         int64_t slot = (int64_t)basei + __popc(mask & ((1u << lane) - 1));
         if (slot < mo.cap) {
-            mo.okey[slot] = (pair_key(row, c, sh) << mo.rb) | (uint64_t)chain;
+            mo.okey[slot] = pair_key(row, c, sh);
+            mo.ochain[slot] = chain;
             mo.ogid[slot] = (int32_t)gid;
         }
     }
@@ -228,9 +229,10 @@ __device__ inline int64_t requested(const uint64_t* rq_key, int64_t lo, int64_t 
 }
 
 // head: one 8-lane group per requested row, chain slots [0, kHead)
-__global__ void __launch_bounds__(256) k_del_scan_head(OutView ov, const int32_t* row_first, int64_t nrows,
+__global__ void __launch_bounds__(256) k_del_scan_head(OutView ov, const int32_t* row_first, const int64_t* d_nrows,
                                                        const uint64_t* rq_key, int64_t nrq, int sh, MatchOut mo) {
     constexpr int G = 8, kPer = 32 / G;
+    const int64_t nrows = *d_nrows;
     const int gl = threadIdx.x & (G - 1), gw = (threadIdx.x & 31) / G;
     int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -271,9 +273,10 @@ __global__ void __launch_bounds__(256) k_del_scan_head(OutView ov, const int32_t
 
 // tail: one warp per kChunk piece of a long row beyond its head
 __global__ void __launch_bounds__(kScanWarps * 32) k_del_scan_tail(OutView ov, const int32_t* row_first,
-                                                                   const int64_t* coff, int64_t nrows, int64_t nwork,
+                                                                   const int64_t* coff, const int64_t* hdr,
                                                                    const uint64_t* rq_key, int64_t nrq, int sh,
                                                                    MatchOut mo) {
+    const int64_t nrows = hdr[0], nwork = hdr[1];
     __shared__ uint32_t bitmap[kScanWarps][kBitmapWords];
     const int lane = threadIdx.x & 31;
     uint32_t* bm = bitmap[threadIdx.x >> 5];
@@ -328,6 +331,12 @@ __global__ void __launch_bounds__(kScanWarps * 32) k_del_scan_tail(OutView ov, c
 __global__ void k_single_flags(const uint64_t* key, int64_t m, uint8_t* single) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
         single[i] = (i == 0 || key[i - 1] != key[i]) && (i + 1 == m || key[i + 1] != key[i]);
+}
+
+// (pair << rb | chain offset): one radix key for the (pair, chain) order
+__global__ void k_overflow_keys(uint64_t* key, const int64_t* chain, int64_t nm, int rb) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nm; i += (int64_t)gridDim.x * blockDim.x)
+        key[i] = (key[i] << rb) | (uint64_t)chain[i];
 }
 
 // Resolve each request: single-request pairs from the atomicMin slot, the
@@ -784,6 +793,8 @@ Store::Store(int dev, int64_t n_, const int64_t* src, const int64_t* dst, const 
     }
     segs.push_back(std::move(base));
     live = na;
+    dcounts.alloc(2, s);
+    dcounts.zero(s);
     upload_tables();
     if (with_reverse) build_index(rev, true);
     GD_CUDA(cudaStreamSynchronize(s));
@@ -1001,7 +1012,8 @@ void Store::append_out_tombs(const int64_t* d_pos, const int32_t* d_row, int64_t
     notomb = tot;
 }
 
-int64_t Store::apply_deletes(const int32_t* d_src, const int32_t* d_dst, int64_t k, uint8_t* d_found) {
+int64_t Store::apply_deletes(const int32_t* d_src, const int32_t* d_dst, int64_t k, uint8_t* d_found,
+                             bool want_count) {
     cudaStream_t s = stream;
     if (k == 0) return 0;
     if (rev.built) compact_index(rev);
@@ -1034,7 +1046,7 @@ int64_t Store::apply_deletes(const int32_t* d_src, const int32_t* d_dst, int64_t
     DBuf<uint8_t> rflag(nrq, s);
     GD_KERNEL(k_row_starts, grid_for(nrq, 256), 256, 0, s, rq_key.get(), nrq, sh, rflag.get());
     DBuf<int32_t> row_first(nrq, s);
-    DBuf<int64_t> hdr(3, s);  // nrows, work items, longest chain
+    DBuf<int64_t> hdr(4, s);  // nrows, work items, longest chain, overflow matches
     select_flagged_index_async(s, rflag.get(), nrq, row_first.get(), hdr.get());
     OutView ov = out_view();
     DBuf<int64_t> chunks(nrq + 1, s), coff(nrq + 1, s);
@@ -1046,59 +1058,57 @@ int64_t Store::apply_deletes(const int32_t* d_src, const int32_t* d_dst, int64_t
     exclusive_scan_i64(s, chunks.get(), coff.get(), nrq + 1);
     GD_CUDA(cudaMemcpyAsync(hdr.get() + 1, coff.get() + nrq, 8, cudaMemcpyDeviceToDevice, s));
     GD_CUDA(cudaMemcpyAsync(hdr.get() + 2, maxlen.get(), 8, cudaMemcpyDeviceToDevice, s));
-    int64_t hv3[3];
-    GD_CUDA(cudaMemcpyAsync(hv3, hdr.get(), sizeof hv3, cudaMemcpyDeviceToHost, s));
-    GD_CUDA(cudaStreamSynchronize(s));
-    const int64_t nrows = hv3[0];
-    int64_t hv[2] = {hv3[1], hv3[2]};
-    int64_t nwork = hv[0];
-    int rb = bits_for((uint64_t)std::max<int64_t>(hv[1], 1));
-    const bool one_sort = kb + rb <= 64;  // (pair, chain offset) fits one 64-bit key
-    if (!one_sort) rb = 0;
     // single-request pairs resolve by atomicMin; the rest collect overflow
-    // matches (retry once with the exact size on overflow)
+    // matches (retry once with the exact size on overflow).  Row and work
+    // counts stay on the device: the one read-back is the overflow size
+    // together with the longest chain.
     DBuf<uint8_t> single(nrq, s);
     GD_KERNEL(k_single_flags, grid_for(nrq, 256), 256, 0, s, rq_key.get(), nrq, single.get());
     DBuf<unsigned long long> sel(nrq, s);
     GD_CUDA(cudaMemsetAsync(sel.get(), 0xff, nrq * 8, s));
     int64_t cap = 1024;
     DBuf<uint64_t> m_key;
+    DBuf<int64_t> m_chain;
     DBuf<int32_t> m_gid;
-    DBuf<unsigned long long> m_cnt(1, s);
-    int64_t nm = 0;
+    int64_t nm = 0, maxchain = 0;
     for (int attempt = 0; attempt < 2; ++attempt) {
         m_key.alloc(cap, s);
+        m_chain.alloc(cap, s);
         m_gid.alloc(cap, s);
-        m_cnt.zero(s);
+        GD_CUDA(cudaMemsetAsync(hdr.get() + 3, 0, 8, s));
         if (attempt) GD_CUDA(cudaMemsetAsync(sel.get(), 0xff, nrq * 8, s));
-        MatchOut mo{sel.get(), single.get(), m_key.get(), m_gid.get(), m_cnt.get(), cap, rb};
-        GD_KERNEL_T("del_scan", 0, k_del_scan_head, grid_for(((nrows + 3) / 4) * 32, 256, 148LL * 32), 256, 0, s,
-                    ov, row_first.get(), nrows, rq_key.get(), nrq, sh, mo);
-        if (nwork)
-            GD_KERNEL_T("del_scan", 0, k_del_scan_tail, grid_for(nwork * 32, kScanWarps * 32, 148LL * 16),
-                        kScanWarps * 32, 0, s, ov, row_first.get(), coff.get(), nrows, nwork, rq_key.get(), nrq, sh,
-                        mo);
-        nm = (int64_t)read_scalar(s, m_cnt.get());
+        MatchOut mo{sel.get(), single.get(), m_key.get(), m_chain.get(), m_gid.get(),
+                    reinterpret_cast<unsigned long long*>(hdr.get() + 3), cap};
+        GD_KERNEL_T("del_scan", 0, k_del_scan_head, grid_for(((nrq + 3) / 4) * 32, 256, 148LL * 32), 256, 0, s, ov,
+                    row_first.get(), hdr.get(), rq_key.get(), nrq, sh, mo);
+        GD_KERNEL_T("del_scan", 0, k_del_scan_tail, 148 * 16, kScanWarps * 32, 0, s, ov, row_first.get(),
+                    coff.get(), hdr.get(), rq_key.get(), nrq, sh, mo);
+        int64_t h2[2];
+        read_small(s, h2, hdr.get() + 2, sizeof h2);
+        maxchain = h2[0];
+        nm = h2[1];
         if (nm <= cap) break;
         cap = nm;
     }
-    if (nm > 1) {
-        if (one_sort) {
-            sort_pairs_u64(s, m_key.get(), m_gid.get(), nm, kb + rb);
-        } else {  // LSD: by gid, then stable by pair key
-            DBuf<uint64_t> gk(nm, s);
-            DBuf<int32_t> perm(nm, s);
-            GD_KERNEL(k_widen, grid_for(nm, 256), 256, 0, s, m_gid.get(), nm, gk.get());
-            iota_i32(s, perm.get(), nm);
-            sort_pairs_u64(s, gk.get(), perm.get(), nm, 32);
-            DBuf<uint64_t> k2(nm, s);
-            GD_KERNEL(k_gather<uint64_t>, grid_for(nm, 256), 256, 0, s, m_key.get(), perm.get(), nm, k2.get());
-            sort_pairs_u64(s, k2.get(), perm.get(), nm, kb);
-            DBuf<int32_t> g2(nm, s);
-            GD_KERNEL(k_gather<int32_t>, grid_for(nm, 256), 256, 0, s, m_gid.get(), perm.get(), nm, g2.get());
-            m_key = std::move(k2);
-            m_gid = std::move(g2);
-        }
+    int rb = bits_for((uint64_t)std::max<int64_t>(maxchain, 1));
+    const bool one_sort = kb + rb <= 64;  // (pair, chain offset) fits one 64-bit key
+    if (!one_sort) rb = 0;
+    if (nm >= 1 && one_sort) {
+        GD_KERNEL(k_overflow_keys, grid_for(nm, 256), 256, 0, s, m_key.get(), m_chain.get(), nm, rb);
+        if (nm > 1) sort_pairs_u64(s, m_key.get(), m_gid.get(), nm, kb + rb);
+    } else if (nm > 1) {  // LSD: by gid (= chain order), then stable by pair key
+        DBuf<uint64_t> gk(nm, s);
+        DBuf<int32_t> perm(nm, s);
+        GD_KERNEL(k_widen, grid_for(nm, 256), 256, 0, s, m_gid.get(), nm, gk.get());
+        iota_i32(s, perm.get(), nm);
+        sort_pairs_u64(s, gk.get(), perm.get(), nm, 32);
+        DBuf<uint64_t> k2(nm, s);
+        GD_KERNEL(k_gather<uint64_t>, grid_for(nm, 256), 256, 0, s, m_key.get(), perm.get(), nm, k2.get());
+        sort_pairs_u64(s, k2.get(), perm.get(), nm, kb);
+        DBuf<int32_t> g2(nm, s);
+        GD_KERNEL(k_gather<int32_t>, grid_for(nm, 256), 256, 0, s, m_gid.get(), perm.get(), nm, g2.get());
+        m_key = std::move(k2);
+        m_gid = std::move(g2);
     }
     DBuf<int64_t> rq_pos(nrq, s);
     DBuf<uint8_t> found_local;
@@ -1108,11 +1118,13 @@ int64_t Store::apply_deletes(const int32_t* d_src, const int32_t* d_dst, int64_t
         found = found_local.get();
     }
     GD_CUDA(cudaMemsetAsync(found, 0, k, s));
-    DBuf<unsigned long long> counts(2, s);  // [0] applied records, [1] killed slots
-    counts.zero(s);
+    // [0] applied records of this call, [1] killed slots since `live` was last
+    // brought up to date (read lazily: live_count())
+    GD_CUDA(cudaMemsetAsync(dcounts.get(), 0, sizeof(unsigned long long), s));
+    unsigned long long* counts = dcounts.get();
     GD_KERNEL(k_del_resolve, grid_for(nrq, 256), 256, 0, s, rq_key.get(), rq_occ.get(), rq_rec.get(),
               rq_which.get(), single.get(), sel.get(), nrq, m_key.get(), m_gid.get(), nm, rb, rq_pos.get(), found,
-              counts.get());
+              counts);
     KilledArcs ka;
     ka.row.alloc(nrq, s);
     ka.col.alloc(nrq, s);
@@ -1120,17 +1132,24 @@ int64_t Store::apply_deletes(const int32_t* d_src, const int32_t* d_dst, int64_t
     ka.gid.alloc(nrq, s);
     ka.count = nrq;
     GD_KERNEL(k_del_kill, grid_for(nrq, 256), 256, 0, s, ov, rq_key.get(), rq_rec.get(), rq_which.get(),
-              rq_pos.get(), nrq, found, sh, ka.row.get(), ka.col.get(), ka.w.get(), ka.gid.get(), counts.get() + 1);
+              rq_pos.get(), nrq, found, sh, ka.row.get(), ka.col.get(), ka.w.get(), ka.gid.get(), counts + 1);
     // the tomb logs take every slot (gid -1 = none; delta-segment gids are
     // ignored by the merge), unordered: no select, no sort
     append_out_tombs(ka.gid.get(), ka.row.get(), nrq);
     index_delete(rev, ka);
     if (fwd.built) index_delete(fwd, ka);
-    unsigned long long hc[2];
-    GD_CUDA(cudaMemcpyAsync(hc, counts.get(), sizeof hc, cudaMemcpyDeviceToHost, s));
-    GD_CUDA(cudaStreamSynchronize(s));
-    live -= (int64_t)hc[1];
-    return (int64_t)hc[0];
+    if (!want_count) return -1;
+    unsigned long long applied = 0;
+    read_small(s, &applied, counts, sizeof applied);
+    return (int64_t)applied;
+}
+
+int64_t Store::live_count() {
+    unsigned long long killed = 0;
+    read_small(stream, &killed, dcounts.get() + 1, sizeof killed);
+    GD_CUDA(cudaMemsetAsync(dcounts.get() + 1, 0, sizeof killed, stream));
+    live -= (int64_t)killed;
+    return live;
 }
 
 void Store::apply_adds(const int32_t* d_src, const int32_t* d_dst, const int32_t* d_w, int64_t k) {
@@ -1240,7 +1259,8 @@ void Store::merge() {
     otpos.release();
     otrow.release();
     notomb = 0;
-    live = nnz2;
+    live = nnz2;  // exact: pending kills are folded in
+    GD_CUDA(cudaMemsetAsync(dcounts.get() + 1, 0, sizeof(unsigned long long), s));
     first_clean_delta = 1;
     if (rev.built) compact_index(rev);
     if (fwd.built) compact_index(fwd);

@@ -86,7 +86,9 @@ class Store {
 
     // update_csr_del on device-resident records (int32).  Returns applied;
     // found_fwd (k bytes, device) gets 1 per applied record when non-null.
-    int64_t apply_deletes(const int32_t* d_src, const int32_t* d_dst, int64_t k, uint8_t* d_found);
+    // returns the applied record count when want_count (one sync), else -1
+    int64_t apply_deletes(const int32_t* d_src, const int32_t* d_dst, int64_t k, uint8_t* d_found,
+                          bool want_count = false);
     void apply_adds(const int32_t* d_src, const int32_t* d_dst, const int32_t* d_w, int64_t k);
     void merge();
     bool merge_due(int64_t batch_index) const { return (batch_index + 1) % merge_interval == 0; }
@@ -114,7 +116,9 @@ class Store {
     int sh = 1;  // pair keys: row << sh | col
     bool directed, weighted, with_reverse;
     int64_t merge_interval;
-    int64_t live = 0;
+    int64_t live = 0;                // host view; kills pending in dcounts[1]
+    DBuf<unsigned long long> dcounts;  // [applied records of the last delete call, killed slots not yet in live]
+    int64_t live_count();              // live arcs (reads the pending kills)
     std::vector<OutSeg> segs;
     SortedIndex rev, fwd;
     // out-store tombstones since the last merge (unordered global slot ids;
