@@ -65,10 +65,32 @@ def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
 
+GEN = "fast"  # --gen: "fast" (parallel counter-based RNG) or "python" (the reference's own recipes and seeds)
+
+
 def make_inputs(wl, batches, seed=22):
     from paper_2507_11094_b200 import generate as G
 
     t = time.time()
+    if GEN == "python" and wl["graph"] in ("rmat", "uniform"):
+        # generate.py's rmat_graph / uniform_random_graph / generate_updates,
+        # draw for draw (seed-compatible); one stream of batches x percent,
+        # cut into batches of ceil(percent% of m) as the reference's bench does
+        und = not wl["directed"]
+        mw = 100 if wl["weighted"] else 10
+        if wl["graph"] == "rmat":
+            s, d, w, n = G.py_rmat_graph(wl["scale"], wl["edges"], seed=seed, weighted=wl["weighted"], max_weight=mw,
+                                         undirected=und)
+        else:
+            n = wl["nodes"]
+            s, d, w = G.py_uniform_random_graph(n, wl["edges"], seed=seed, weighted=wl["weighted"], max_weight=mw,
+                                                undirected=und)
+        per = math.ceil(wl["percent"] / 100.0 * len(s))
+        kind, us, ud, uw = G.py_generate_updates(s, d, w, n, min(100.0, wl["percent"] * batches), seed=seed + 1,
+                                                 undirected=und)
+        log(f"[bench] inputs (reference generators, seed {seed}): n={n} m={len(s)} records={len(kind)} batch={per} "
+            f"gen={time.time() - t:.1f}s")
+        return n, s, d, w, kind, us, ud, uw, per
     if wl["graph"] == "rmat":
         s, d, w, n = G.rmat(wl["scale"], wl["edges"], seed=seed, weighted=wl["weighted"],
                             undirected=not wl["directed"])
@@ -195,10 +217,14 @@ def main():
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="pr")
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--gen", choices=("fast", "python"), default="fast",
+                    help="input generator: fast (parallel) or python (the reference's generate.py, seed-compatible)")
     ap.add_argument("--ref-batches", type=int, default=1,
                     help="bounded sample for the reference arm: at most this many batches")
     args = ap.parse_args()
     wl = WORKLOADS[args.workload]
+    global GEN
+    GEN = args.gen
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -450,7 +476,9 @@ def _config(wl, args, world):
                          "replicated store, PR pull by dst range + NCCL all-gather" if wl["algo"] == "pr" else
                          "replicated store, TC record slices + NCCL all-reduce" if wl["algo"] == "tc" else
                          "replicas"),
-         "l2": "inputs larger than L2 (graph store >> 126 MB L2)"}
+         "l2": "inputs larger than L2 (graph store >> 126 MB L2)",
+         "generator": ("reference generate.py recipes, seed-compatible" if GEN == "python" and wl["graph"] != "grid"
+                       else "parallel counter-based RNG, reference recipes")}
     if wl["algo"] == "pr":
         c.update({"damping": 0.85, "beta": 1e-3, "maxiter": 100})
     return c

@@ -33,6 +33,14 @@ def _L():
         L.gdgen_updates.restype = i64
         L.gdgen_updates.argtypes = [vp, vp, i64, i64, i64, i64, i64, C.c_uint64, C.c_int, i64, vp, vp, vp, vp]
         L.gdgen_threads.restype = C.c_int
+        L.gdgen_py_rmat.restype = i64
+        L.gdgen_py_rmat.argtypes = [C.c_int, i64, C.c_uint64, C.c_int, i64, C.c_double, C.c_double, C.c_double,
+                                    C.c_int, vp, vp, vp]
+        L.gdgen_py_uniform.restype = i64
+        L.gdgen_py_uniform.argtypes = [i64, i64, C.c_uint64, C.c_int, i64, C.c_int, C.c_int, vp, vp, vp]
+        L.gdgen_py_updates.restype = i64
+        L.gdgen_py_updates.argtypes = [vp, vp, vp, i64, i64, C.c_double, C.c_uint64, C.c_double, C.c_int, vp, vp, vp,
+                                       vp]
         _lib = L
     return _lib
 
@@ -94,3 +102,64 @@ def updates(src, dst, n: int, *, percent: float, batches: int = 1, seed: int, ad
                             _p(us), _p(ud), _p(uw))
     k = n_del + na
     return kind[:k], us[:k], ud[:k], uw[:k], per
+
+
+# ---------------------------------------------------------------------------
+# Seed-compatible generators: the reference's own recipes (generate.py:15-161)
+# drawn from a native restatement of Python's random.Random, so the same seed
+# gives the same edges / stream as the reference (checked against it in
+# tests/test_pyrand_cpu.py).  Sequential; ~50-100x faster than the Python.
+
+
+def _seed(seed: int) -> int:
+    seed = abs(int(seed))
+    if seed >= 1 << 64:
+        raise ValueError("seed-compatible generators take seeds below 2**64")
+    return seed
+
+
+def py_rmat_graph(node_count_log2: int, edge_count: int, *, seed: int, weighted: bool = False, max_weight: int = 10,
+                  a: float = 0.57, b: float = 0.19, c: float = 0.19, undirected: bool = False):
+    """generate.rmat_graph: (src, dst, w, node_count) as int64 arrays."""
+    m = max(int(edge_count), 0)
+    src = np.empty(m, dtype=np.int64)
+    dst = np.empty(m, dtype=np.int64)
+    w = np.empty(m, dtype=np.int64)
+    got = _L().gdgen_py_rmat(node_count_log2, m, _seed(seed), int(weighted), max_weight, a, b, c, int(undirected),
+                             _p(src), _p(dst), _p(w))
+    return src[:got], dst[:got], w[:got], 1 << node_count_log2
+
+
+def py_uniform_random_graph(node_count: int, edge_count: int, *, seed: int, weighted: bool = False,
+                            max_weight: int = 10, connected: bool = False, undirected: bool = False):
+    """generate.uniform_random_graph: (src, dst, w) as int64 arrays."""
+    cap = max(int(edge_count), 0) + (node_count if connected else 0)
+    src = np.empty(cap, dtype=np.int64)
+    dst = np.empty(cap, dtype=np.int64)
+    w = np.empty(cap, dtype=np.int64)
+    got = _L().gdgen_py_uniform(node_count, max(int(edge_count), 0), _seed(seed), int(weighted), max_weight,
+                                int(connected), int(undirected), _p(src), _p(dst), _p(w))
+    return src[:got], dst[:got], w[:got]
+
+
+def py_generate_updates(src, dst, w, node_count: int, percent: float, *, seed: int, add_fraction: float = 0.5,
+                        undirected: bool = False):
+    """generate.generate_updates: (kind uint8 'a'/'d', src, dst, w) in the
+    reference's stream order."""
+    from .errors import ContractViolation
+
+    if not (0.0 < percent <= 100.0):
+        raise ContractViolation(f"percent must lie in (0, 100], got {percent}")
+    if not (0.0 <= add_fraction <= 1.0):
+        raise ContractViolation(f"add_fraction must lie in [0, 1], got {add_fraction}")
+    s = np.ascontiguousarray(src, dtype=np.int64)
+    d = np.ascontiguousarray(dst, dtype=np.int64)
+    ww = np.ascontiguousarray(w if w is not None else np.ones(len(s)), dtype=np.int64)
+    cap = math.ceil(percent / 100.0 * len(s)) + 1
+    kind = np.empty(cap, dtype=np.uint8)
+    us = np.empty(cap, dtype=np.int64)
+    ud = np.empty(cap, dtype=np.int64)
+    uw = np.empty(cap, dtype=np.int64)
+    k = _L().gdgen_py_updates(_p(s), _p(d), _p(ww), len(s), node_count, float(percent), _seed(seed),
+                              float(add_fraction), int(undirected), _p(kind), _p(us), _p(ud), _p(uw))
+    return kind[:k], us[:k], ud[:k], uw[:k]
