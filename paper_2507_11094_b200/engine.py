@@ -344,6 +344,11 @@ def run_program(check, graph: DynamicGraph, inputs: Dict[str, object], *, entry:
         ctx.return_value = c
         ctx.scalars["tcount"] = c
     ctx.scalars.pop("wall_seconds", None)
+    # bound scalar inputs are program scalars too (interp.py binds them into
+    # ctx.scalars): batchsize, src, damping, beta, maxiter
+    for key in ("batchsize", "batch_size", "src", "damping", "beta", "maxiter"):
+        if key in inputs and isinstance(inputs[key], (bool, int, float, np.integer, np.floating)):
+            ctx.scalars.setdefault(key, inputs[key].item() if isinstance(inputs[key], np.generic) else inputs[key])
     return ctx
 
 

@@ -1,0 +1,141 @@
+"""The graphdyn-compatible CLI on the GPU, against the reference CLI's own
+outputs for the same commands (tests/golden/make_cli_golden.py): SSSP
+dist/parent CSVs byte-identical, PR within 1e-9, TC counts exact; plus the
+reference's test_cli.py scenarios (exit codes, static mode == oracle, bench
+equivalence, manifests)."""
+
+import csv
+import json
+import os
+
+import numpy as np
+import pytest
+
+from paper_2507_11094_b200.cli import EXIT_OK, EXIT_RUNTIME, EXIT_USAGE, main
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+GOLD = os.path.join(HERE, "golden", "cli")
+PROGS = os.path.join(HERE, "programs")
+
+
+def g(name):
+    return os.path.join(GOLD, name)
+
+
+def values(path):
+    with open(path, newline="") as fh:
+        rows = list(csv.reader(fh))
+    return {int(n): v for n, v in rows[1:]}
+
+
+def scalars(path):
+    with open(path, newline="") as fh:
+        return {k: v for k, v in list(csv.reader(fh))[1:]}
+
+
+def test_dynamic_run_writes_results_and_manifest(tmp_path):
+    out = tmp_path / "out"
+    rc = main(["run", os.path.join(PROGS, "sssp_dynamic.sp"), g("scenario.txt"), "--updates",
+               g("scenario_updates.txt"), "--batch", "1000", "--src", "0", "--out", str(out)])
+    assert rc == EXIT_OK
+    assert [int(values(out / "dist.csv")[v]) for v in range(6)] == [0, 30, 20, 40, 44, 50]
+    for f in ("dist.csv", "parent.csv"):
+        assert (out / f).read_bytes() == open(g(f"run_sssp/{f}"), "rb").read()
+    m = json.loads((out / "manifest.json").read_text())
+    assert m["seed"] == 0 and "graph" in m["input_digests"]
+    assert m["run"]["batch_count"] == 1 and "static_phase" in m["run"]["phase_seconds"]
+    assert scalars(out / "scalars.csv") == scalars(g("run_sssp/scalars.csv"))
+
+
+def test_sssp_run_matches_reference_cli(tmp_path):
+    out = tmp_path / "o"
+    assert main(["run", os.path.join(PROGS, "sssp_dynamic.sp"), g("g40.txt"), "--updates", g("gen_g40.txt"),
+                 "--batch", "5", "--src", "3", "--out", str(out)]) == EXIT_OK
+    for f in ("dist.csv", "parent.csv"):
+        assert (out / f).read_bytes() == open(g(f"run_sssp_g40/{f}"), "rb").read()
+
+
+def test_pr_run_matches_reference_cli(tmp_path):
+    out = tmp_path / "o"
+    assert main(["run", "pr", g("rmat9.txt"), "--updates", g("gen_rmat9.txt"), "--batch", "40",
+                 "--out", str(out)]) == EXIT_OK
+    got, want = values(out / "pagerank.csv"), values(g("run_pr_rmat9/pagerank.csv"))
+    assert got.keys() == want.keys()
+    err = max(abs(float(got[k]) - float(want[k])) for k in want)
+    assert err <= 1e-9, err
+    assert (out / "outdeg.csv").read_bytes() == open(g("run_pr_rmat9/outdeg.csv"), "rb").read()
+    assert scalars(out / "scalars.csv") == scalars(g("run_pr_rmat9/scalars.csv"))
+
+
+def test_tc_run_and_oracle_match_reference_cli(tmp_path):
+    out = tmp_path / "o"
+    assert main(["run", os.path.join(PROGS, "tc_dynamic.sp"), g("g60u.txt"), "--undirected", "--updates",
+                 g("gen_g60u.txt"), "--batch", "20", "--out", str(out)]) == EXIT_OK
+    want = scalars(g("run_tc_g60u/scalars.csv"))
+    got = scalars(out / "scalars.csv")
+    assert got["tcount"] == want["tcount"] and got["return"] == want["return"]
+    o2 = tmp_path / "or"
+    assert main(["oracle", "tc", g("g60u.txt"), "--undirected", "--updates", g("gen_g60u.txt"),
+                 "--out", str(o2)]) == EXIT_OK
+    assert (o2 / "scalars.csv").read_bytes() == open(g("oracle_tc/scalars.csv"), "rb").read()
+
+
+def test_sssp_oracle_matches_reference_cli(tmp_path):
+    out = tmp_path / "o"
+    assert main(["oracle", "sssp", g("g40.txt"), "--updates", g("gen_g40.txt"), "--src", "3",
+                 "--out", str(out)]) == EXIT_OK
+    assert (out / "dist.csv").read_bytes() == open(g("oracle_sssp/dist.csv"), "rb").read()
+
+
+def test_static_mode_equals_oracle_on_updated_graph(tmp_path):
+    out1, out2 = tmp_path / "s", tmp_path / "o"
+    assert main(["run", os.path.join(PROGS, "sssp_dynamic.sp"), g("scenario.txt"), "--mode", "static",
+                 "--updates", g("scenario_updates.txt"), "--src", "0", "--out", str(out1)]) == EXIT_OK
+    assert main(["oracle", "sssp", g("scenario.txt"), "--updates", g("scenario_updates.txt"), "--src", "0",
+                 "--out", str(out2)]) == EXIT_OK
+    assert values(out1 / "dist.csv") == values(out2 / "dist.csv")
+
+
+def test_missing_src_is_usage_error(tmp_path):
+    rc = main(["run", os.path.join(PROGS, "sssp_dynamic.sp"), g("scenario.txt"), "--updates",
+               g("scenario_updates.txt"), "--out", str(tmp_path / "x")])
+    assert rc == EXIT_USAGE
+
+
+def test_runtime_error_exit_code(tmp_path):
+    u = tmp_path / "bad.txt"
+    u.write_text("a 0 99\n")
+    rc = main(["run", os.path.join(PROGS, "sssp_dynamic.sp"), g("scenario.txt"), "--updates", str(u), "--src", "0",
+               "--out", str(tmp_path / "x")])
+    assert rc == EXIT_RUNTIME
+
+
+def test_bench_produces_table_and_equivalence(tmp_path):
+    out = tmp_path / "bench"
+    rc = main(["bench", os.path.join(PROGS, "sssp_dynamic.sp"), g("g40.txt"), "--percents", "5,20", "--src", "0",
+               "--seed", "9", "--out", str(out)])
+    assert rc == EXIT_OK
+    with open(out / "bench.csv", newline="") as fh:
+        rows = list(csv.DictReader(fh))
+    assert [float(r["percent"]) for r in rows] == [5.0, 20.0]
+    assert all(r["equivalent"] == "True" for r in rows)
+    for prog, extra in (("pr", []), ("tc", ["--undirected"])):
+        graph = g("rmat9.txt") if prog == "pr" else g("g60u.txt")
+        assert main(["bench", prog, graph, *extra, "--percents", "10", "--seed", "2",
+                     "--out", str(tmp_path / prog)]) == EXIT_OK
+
+
+def test_binary_inputs_give_the_text_results(tmp_path):
+    from paper_2507_11094_b200 import io as gio
+
+    edges = np.loadtxt(g("g40.txt"), dtype=np.int64)
+    gio.save_edges_binary(str(tmp_path / "g.bin"), 40, edges[:, 0], edges[:, 1], edges[:, 2])
+    assert main(["gen-updates", g("g40.txt"), "--percent", "10", "--seed", "42", "--binary",
+                 "--out", str(tmp_path / "u.bin")]) == EXIT_OK
+    out = tmp_path / "o"
+    assert main(["run", "sssp", str(tmp_path / "g.bin"), "--updates", str(tmp_path / "u.bin"), "--batch", "5",
+                 "--src", "3", "--out", str(out)]) == EXIT_OK
+    for f in ("dist.csv", "parent.csv"):
+        assert (out / f).read_bytes() == open(g(f"run_sssp_g40/{f}"), "rb").read()
