@@ -121,10 +121,19 @@ def test_bench_produces_table_and_equivalence(tmp_path):
         rows = list(csv.DictReader(fh))
     assert [float(r["percent"]) for r in rows] == [5.0, 20.0]
     assert all(r["equivalent"] == "True" for r in rows)
-    for prog, extra in (("pr", []), ("tc", ["--undirected"])):
-        graph = g("rmat9.txt") if prog == "pr" else g("g60u.txt")
-        assert main(["bench", prog, graph, *extra, "--percents", "10", "--seed", "2",
-                     "--out", str(tmp_path / prog)]) == EXIT_OK
+    # PR: dynamic == static only on a connected graph at a tight beta (S12)
+    from paper_2507_11094_b200 import generate as G
+
+    s, d, w = G.py_uniform_random_graph(80, 300, seed=4, connected=True)
+    conn = tmp_path / "conn.txt"
+    conn.write_text("".join(f"{a} {b}\n" for a, b in zip(s.tolist(), d.tolist())))
+    assert main(["bench", "pr", str(conn), "--beta", "1e-11", "--percents", "10", "--seed", "2",
+                 "--out", str(tmp_path / "pr")]) == EXIT_OK
+    assert main(["bench", "tc", g("g60u.txt"), "--undirected", "--percents", "10", "--seed", "2",
+                 "--out", str(tmp_path / "tc")]) == EXIT_OK
+    # a disconnected graph at beta 1e-3 is reported, as the reference does, with exit 4
+    assert main(["bench", "pr", g("rmat9.txt"), "--percents", "10", "--seed", "2",
+                 "--out", str(tmp_path / "pr2")]) == 4
 
 
 def test_binary_inputs_give_the_text_results(tmp_path):
