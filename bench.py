@@ -307,6 +307,8 @@ def main():
         torch.distributed.barrier()
     torch.cuda.synchronize()
     wall0 = time.time()
+    if sharded:
+        comm.reset_stats()
     launches0 = gd._native.lib().gd_kernel_launches()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
@@ -321,6 +323,11 @@ def main():
         if nl:
             kstats[name] = [ms, nl, nb_]
     launches = gd._native.lib().gd_kernel_launches() - launches0
+    comm_stats = None
+    if sharded:  # CommStats analogue: NCCL traffic of this rank per timed step
+        cs = comm.stats()
+        comm_stats = {k: v / args.steps for k, v in cs.items()}
+        comm_stats["per"] = "rank and step"
     clocks.mark(wall0, time.time())
     clk = clocks.stop()
     elapsed_ms = ev0.elapsed_time(ev1)
@@ -412,6 +419,8 @@ def main():
             "clocks": clk,
             "records_per_step": records_per_step,
         }
+        if comm_stats is not None:
+            line["comm"] = comm_stats
         print(json.dumps(line))
     if dist_on:
         torch.distributed.destroy_process_group()

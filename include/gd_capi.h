@@ -156,6 +156,13 @@ GD_API int gd_tc_destroy(gd_tc* t);
 GD_API int gd_comm_unique_id(uint8_t id[128]);
 GD_API int gd_comm_create(int world, int rank, const uint8_t id[128], int device, gd_comm** out);
 GD_API int gd_comm_destroy(gd_comm* c);
+/* communication accounting (the CommStats analogue of partition.py:32-66):
+ * out[0] collective calls, out[1] all-gather payload bytes, out[2] all-reduce
+ * payload bytes, out[3] bytes this rank sends under the ring algorithms
+ * ((world-1)/world of an all-gather's payload, 2(world-1)/world of an
+ * all-reduce's) -- counted since creation or the last reset */
+GD_API int gd_comm_stats(const gd_comm* c, int64_t out[4]);
+GD_API int gd_comm_reset_stats(gd_comm* c);
 GD_API int gd_pr_set_comm(gd_pr* p, gd_comm* c);
 GD_API int gd_tc_set_comm(gd_tc* t, gd_comm* c);
 

@@ -70,6 +70,8 @@ SIGNATURES = [
     ("gd_phase_times", C.c_int, [vp, f64p]),
     ("gd_iterations", C.c_int, [vp, i64p]),
     ("gd_kernel_time", C.c_int, [vp, C.c_char_p, f64p, i64p, i64p]),
+    ("gd_comm_stats", C.c_int, [vp, i64p]),
+    ("gd_comm_reset_stats", C.c_int, [vp]),
     ("gd_kernel_time_total", C.c_int, [vp, C.c_char_p, f64p, i64p, i64p]),
     ("gd_set_profiling", C.c_int, [vp, C.c_int]),
 ]

@@ -487,6 +487,21 @@ int gd_comm_destroy(gd_comm* c) {
         delete c;
     });
 }
+int gd_comm_stats(const gd_comm* c, int64_t out[4]) {
+    if (!c || !c->c) return null_handle();
+    out[0] = c->c->n_calls;
+    out[1] = c->c->ag_bytes;
+    out[2] = c->c->ar_bytes;
+    out[3] = c->c->sent_bytes;
+    return ok();
+}
+
+int gd_comm_reset_stats(gd_comm* c) {
+    if (!c || !c->c) return null_handle();
+    c->c->n_calls = c->c->ag_bytes = c->c->ar_bytes = c->c->sent_bytes = 0;
+    return ok();
+}
+
 int gd_pr_set_comm(gd_pr* p, gd_comm* c) {
     if (!p) return null_handle();
     return guard([&] {

@@ -94,15 +94,24 @@ void comm_destroy(Comm* c) {
 }
 
 void Comm::allgather_f64(double* buf, int64_t ch, cudaStream_t s) const {
+    ++n_calls;
+    ag_bytes += ch * 8 * world;
+    sent_bytes += ch * 8 * (world - 1);
     check(api().allgather(buf + (int64_t)rank * ch, buf, (size_t)ch, ncclFloat64, (ncclComm_t)nccl, s),
           "ncclAllGather");
 }
 
 void Comm::allreduce_max_f64(double* x, int64_t count, cudaStream_t s) const {
+    ++n_calls;
+    ar_bytes += count * 8;
+    sent_bytes += world > 1 ? count * 8 * 2 * (world - 1) / world : 0;
     check(api().allreduce(x, x, (size_t)count, ncclFloat64, ncclMax, (ncclComm_t)nccl, s), "ncclAllReduce(max)");
 }
 
 void Comm::allreduce_sum_i64(int64_t* x, int64_t count, cudaStream_t s) const {
+    ++n_calls;
+    ar_bytes += count * 8;
+    sent_bytes += world > 1 ? count * 8 * 2 * (world - 1) / world : 0;
     check(api().allreduce(x, x, (size_t)count, ncclInt64, ncclSum, (ncclComm_t)nccl, s), "ncclAllReduce(sum)");
 }
 

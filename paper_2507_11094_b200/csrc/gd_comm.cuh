@@ -19,6 +19,8 @@ namespace gdb {
 struct Comm {
     void* nccl = nullptr;  // ncclComm_t
     int rank = 0, world = 1, device = 0;
+    // accounting: calls, all-gather / all-reduce payload bytes, ring bytes sent
+    mutable int64_t n_calls = 0, ag_bytes = 0, ar_bytes = 0, sent_bytes = 0;
 
     // vertex range owned by this rank: [lo, hi), chunk = ceil(n / world)
     int64_t chunk(int64_t n) const { return (n + world - 1) / world; }

@@ -72,6 +72,18 @@ class Communicator:
         N.check(getattr(N.lib(), fn)(algo.h, self.h))
         algo.comm = self  # keep alive
 
+    def stats(self) -> dict:
+        """Communication accounting since creation / reset (CommStats analogue)."""
+        import numpy as np
+
+        out = np.zeros(4, dtype=np.int64)
+        N.check(N.lib().gd_comm_stats(self.h, out.ctypes.data_as(C.POINTER(C.c_int64))))
+        return {"calls": int(out[0]), "allgather_bytes": int(out[1]), "allreduce_bytes": int(out[2]),
+                "sent_bytes": int(out[3])}
+
+    def reset_stats(self) -> None:
+        N.check(N.lib().gd_comm_reset_stats(self.h))
+
     def __del__(self):
         h = getattr(self, "h", None)
         if h is not None and N._lib is not None:

@@ -251,10 +251,17 @@ def test_comm_single_rank_sharded_paths_match(gd):
         pr = gd.PRHandle(g, 0.85, 1e-10, 100)
         if use:
             comm.attach(pr)
+            it0 = pr.iterations()
         for bi, st in enumerate(range(0, 2000, 500)):
             pr.batch(gd.RecordArrays(kind[st:st + 500], us[st:st + 500], ud[st:st + 500], uw[st:st + 500]), bi)
         outs.append(pr.read()[0])
     np.testing.assert_allclose(outs[0], outs[1], rtol=0, atol=1e-15)
+    # accounting: one all-gather of the padded rank vector + one residual all-reduce per sweep
+    sweeps = pr.iterations() - it0
+    st = comm.stats()
+    assert st["calls"] == 2 * sweeps and st["allgather_bytes"] == 8 * n * sweeps
+    assert st["allreduce_bytes"] == 8 * sweeps and st["sent_bytes"] == 0  # one rank sends nothing
+    comm.reset_stats()
     cnt = []
     for use in (False, True):
         g = gd.DynamicGraph.from_arrays(n, src, dst, directed=False)
@@ -264,3 +271,4 @@ def test_comm_single_rank_sharded_paths_match(gd):
         tc.batch(gd.RecordArrays(kind, us, ud, uw), 0)
         cnt.append(tc.read())
     assert cnt[0] == cnt[1]
+    assert comm.stats()["calls"] == 2  # the delete and the add phase's count all-reduce
