@@ -217,6 +217,9 @@ def main():
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="pr")
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--static", action="store_true",
+                    help="also time the static alternative per batch: apply the batch, merge, recompute from scratch "
+                         "(staticSSSP / staticPR / staticTC), on up to 3 batches")
     ap.add_argument("--gen", choices=("fast", "python"), default="fast",
                     help="input generator: fast (parallel) or python (the reference's generate.py, seed-compatible)")
     ap.add_argument("--ref-batches", type=int, default=1,
@@ -375,6 +378,8 @@ def main():
     e2e_value = (e_done * (1 if (dist_on and wl["algo"] in ("pr", "tc")) else world)) / (e2e_ms / 1e3) \
         if e2e_ms > 0 else None
 
+    static = _static_compare(gd, torch, wl, args, local, n, s, d, w, kind, us, ud, uw, per) if args.static else None
+
     shards = dist_on and wl["algo"] in ("pr", "tc")  # one job over all GPUs vs independent replicas
     value = (done * (1 if shards else world)) / (elapsed_ms / 1e3)
     peak, peak_kind = load_peaks()
@@ -421,10 +426,49 @@ def main():
         }
         if comm_stats is not None:
             line["comm"] = comm_stats
+        if static is not None:
+            static["dynamic_speedup"] = static["ms_per_step"] / (elapsed_ms / args.steps)
+            line["static"] = static
         print(json.dumps(line))
     if dist_on:
         torch.distributed.destroy_process_group()
     return 0
+
+
+def _static_compare(gd, torch, wl, args, local, n, s, d, w, kind, us, ud, uw, per):
+    """The static alternative the reference's `bench` compares against
+    (cli.py:396-491): per batch, apply it to the store, merge, and run the
+    static entry from scratch.  Same batches as the dynamic timed steps."""
+    from paper_2507_11094_b200.updates import RecordArrays, UpdateBatch
+
+    g2 = gd.DynamicGraph.from_arrays(n, s, d, w if wl["weighted"] else None, directed=wl["directed"],
+                                     weighted=wl["weighted"], with_reverse=wl["algo"] != "tc", device=local)
+    stream = torch.cuda.ExternalStream(_graph_stream(g2))
+    k = min(args.steps, 3)
+    times = []
+    for i in range(args.warmup, args.warmup + k):
+        a, b = i * per, min((i + 1) * per, len(kind))
+        part = RecordArrays(kind[a:b], us[a:b], ud[a:b], uw[a:b])
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        batch = UpdateBatch(arrays=part)
+        g2.update_csr_del(batch.only_deletes())
+        g2.update_csr_add(batch.only_adds())
+        g2.merge_deltas()
+        if wl["algo"] == "pr":
+            h = gd.PRHandle(g2, 0.85, 1e-3, 100)
+        elif wl["algo"] == "sssp":
+            h = gd.SSSPHandle(g2, 0)
+        else:
+            h = gd.TCHandle(g2)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        times.append(e0.elapsed_time(e1))
+        del h
+    ms = sum(times) / len(times)
+    return {"ms_per_step": ms, "value": per / (ms / 1e3), "unit": UNIT, "steps": k,
+            "what": "apply batch + merge + static recompute from scratch (the reference bench's static column)"}
 
 
 KERNELS = ("pr_pull", "pr_contrib", "merge_copy", "flood_sample", "flood_rest", "flood_mark", "del_scan",
