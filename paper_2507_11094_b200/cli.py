@@ -151,18 +151,16 @@ def _is_binary(path: str, magic: bytes) -> bool:
 
 def _read_edges(path: str):
     """(src, dst, w, weighted, max_id, node_count_hint, directed_hint)."""
-    from .io import _EDGE_MAGIC, load_edges_binary, parse_edge_lines
+    from .io import _EDGE_MAGIC, load_edges_binary
 
     if _is_binary(path, _EDGE_MAGIC):
         n, s, d, w, directed = load_edges_binary(path)
         return (np.asarray(s), np.asarray(d), None if w is None else np.asarray(w), w is not None,
                 int(max(s.max(), d.max())) if len(s) else -1, n, directed)
-    with open(path, "r", encoding="utf-8") as fh:
-        edges, weighted, max_id = parse_edge_lines(fh.read(), path=path)
-    s = np.array([e[0] for e in edges], dtype=np.int64)
-    d = np.array([e[1] for e in edges], dtype=np.int64)
-    w = np.array([e[2] for e in edges], dtype=np.int64)
-    return s, d, (w if weighted else None), weighted, max_id, None, None
+    from .io import read_edge_file
+
+    s, d, w, weighted, max_id = read_edge_file(path)
+    return s, d, w, weighted, max_id, None, None
 
 
 def _load_graph(path: str, *, directed: bool, nodes: Optional[int], merge_interval: int, with_reverse: bool,

@@ -41,8 +41,43 @@ def _L():
         L.gdgen_py_updates.restype = i64
         L.gdgen_py_updates.argtypes = [vp, vp, vp, i64, i64, C.c_double, C.c_uint64, C.c_double, C.c_int, vp, vp, vp,
                                        vp]
+        L.gdgen_parse_file.restype = vp
+        L.gdgen_parse_file.argtypes = [C.c_char_p, C.c_int, C.POINTER(i64), C.POINTER(C.c_int), C.POINTER(i64),
+                                       C.POINTER(i64), C.c_char_p, C.c_int]
+        L.gdgen_parsed_copy.restype = None
+        L.gdgen_parsed_copy.argtypes = [vp, vp, vp, vp, vp]
+        L.gdgen_parsed_free.restype = None
+        L.gdgen_parsed_free.argtypes = [vp]
         _lib = L
     return _lib
+
+
+def parse_text_file(path: str, updates: bool):
+    """Native parallel parse of an edge (updates=False) or update file:
+    returns (kind or None, src, dst, w, weighted, max_id); raises
+    MalformedInputError with the first bad line, as the Python loops do."""
+    from .errors import MalformedInputError
+
+    L = _L()
+    cnt, wtd, mx, eline = C.c_int64(), C.c_int(), C.c_int64(), C.c_int64()
+    msg = C.create_string_buffer(512)
+    h = L.gdgen_parse_file(os.fsencode(path), int(updates), C.byref(cnt), C.byref(wtd), C.byref(mx),
+                           C.byref(eline), msg, 512)
+    try:
+        if eline.value >= 0:
+            text = msg.value.decode(errors="replace")
+            if eline.value == 0:
+                raise OSError(f"{path}: {text}")
+            raise MalformedInputError(text, path=path, line=int(eline.value))
+        k = cnt.value
+        kind = np.empty(k, dtype=np.uint8) if updates else None
+        src = np.empty(k, dtype=np.int64)
+        dst = np.empty(k, dtype=np.int64)
+        w = np.empty(k, dtype=np.int64)
+        L.gdgen_parsed_copy(h, None if kind is None else _p(kind), _p(src), _p(dst), _p(w))
+        return kind, src, dst, w, bool(wtd.value), int(mx.value)
+    finally:
+        L.gdgen_parsed_free(h)
 
 
 def _p(a):
