@@ -30,7 +30,7 @@ __global__ void k_pr_init(double* rank, int64_t n, double v) {
 // ctl[0..2] bin sizes, ctl[3..5] in-arcs per bin, ctl[6] done, ctl[7] sweeps.
 // Sweeps are enqueued ahead; once ctl[6] is set, the queued ones return at
 // their first instruction.
-enum { C_NBIN = 0, C_EBIN = 3, C_DONE = 6, C_SWEEPS = 7, C_LEN = 8 };
+enum { C_NBIN = 0, C_EBIN = 3, C_DONE = 6, C_SWEEPS = 7, C_WORK = 8, C_LEN = 9 };
 
 __global__ void __launch_bounds__(256) k_pr_contrib(const double* rank, const int32_t* outdeg, int64_t n,
                                                     double* contrib, double* partial, const int64_t* ctl) {
@@ -55,7 +55,7 @@ __global__ void __launch_bounds__(256) k_pr_contrib(const double* rank, const in
 
 // deterministic final sum of the partials (fixed order); clears the sweep's
 // residual
-__global__ void k_sum_partials(const double* partial, int np, double* out, const int64_t* ctl) {
+__global__ void k_sum_partials(const double* partial, int np, double* out, int64_t* ctl) {
     if (ctl && ctl[C_DONE]) return;
     __shared__ double sh[1024];
     double t = 0.0;
@@ -69,6 +69,7 @@ __global__ void k_sum_partials(const double* partial, int np, double* out, const
     if (threadIdx.x == 0) {
         out[0] = sh[0];
         out[1] = 0.0;
+        if (ctl) ctl[C_WORK] = 0;  // the fused pull's work counter
     }
 }
 
@@ -165,6 +166,79 @@ __global__ void __launch_bounds__(kHubThreads) k_pr_pull_hub(const int32_t* list
         }
         __syncthreads();
     }
+}
+
+// All three bins in one launch: CTAs take work units from one counter, hubs
+// first (a whole CTA per hub row), then 16 medium rows (16 lanes each), then
+// 128 light rows (2 lanes each).  The serial bin launches left the latency-
+// bound hub tail and the L1-bound medium bin unoverlapped; here they share the
+// GPU.  Each row's sum keeps a fixed lane/order assignment: deterministic.
+constexpr int kFusedThreads = 256;
+
+__global__ void __launch_bounds__(kFusedThreads) k_pr_pull_fused(const int32_t* light, const int32_t* med,
+                                                                 const int32_t* hub, int64_t* ctl, IdxView ix,
+                                                                 const double* contrib, const double* rank,
+                                                                 const double* dangling, double base, double damping,
+                                                                 double inv_n, double* rank_new, double* diff) {
+    if (ctl[C_DONE]) return;
+    __shared__ long long unit_s;
+    __shared__ double red[kFusedThreads / 32];
+    const int64_t nl = ctl[C_NBIN], nm = ctl[C_NBIN + 1], nh = ctl[C_NBIN + 2];
+    const int64_t uh = nh, um = (nm + 15) / 16, ul = (nl + 127) / 128, total = uh + um + ul;
+    const double dn = *dangling * inv_n;
+    const int tid = threadIdx.x, lane = tid & 31;
+    double dmax = 0.0;
+    while (true) {
+        if (tid == 0) unit_s = (long long)atomicAdd(reinterpret_cast<unsigned long long*>(&ctl[C_WORK]), 1ULL);
+        __syncthreads();
+        const int64_t u = unit_s;
+        __syncthreads();
+        if (u >= total) break;
+        if (u < uh) {  // one hub row per CTA
+            int32_t v = hub[u];
+            double acc = row_sum<kFusedThreads>(ix.col, ix.off[v], ix.off[v + 1], tid, contrib);
+            for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            if (lane == 0) red[tid >> 5] = acc;
+            __syncthreads();
+            if (tid == 0) {
+                double sum = 0.0;
+                for (int w = 0; w < kFusedThreads / 32; ++w) sum += red[w];
+                double nr = base + damping * (sum + dn);
+                dmax = fmax(dmax, fabs(nr - rank[v]));
+                rank_new[v] = nr;
+            }
+            __syncthreads();
+        } else if (u < uh + um) {  // 16 medium rows, 16 lanes each
+            const int64_t t = (u - uh) * 16 + (tid >> 4);
+            const int gl = tid & 15;
+            bool valid = t < nm;
+            int32_t v = valid ? med[t] : 0;
+            int64_t a = valid ? ix.off[v] : 0, b = valid ? ix.off[v + 1] : 0;
+            double acc = row_sum<16>(ix.col, a, b, gl, contrib);
+#pragma unroll
+            for (int o = 8; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o, 16);
+            if (valid && gl == 0) {
+                double nr = base + damping * (acc + dn);
+                dmax = fmax(dmax, fabs(nr - rank[v]));
+                rank_new[v] = nr;
+            }
+        } else {  // 128 light rows, 2 lanes each
+            const int64_t t = (u - uh - um) * 128 + (tid >> 1);
+            const int gl = tid & 1;
+            bool valid = t < nl;
+            int32_t v = valid ? light[t] : 0;
+            int64_t a = valid ? ix.off[v] : 0, b = valid ? ix.off[v + 1] : 0;
+            double acc = row_sum<2>(ix.col, a, b, gl, contrib);
+            acc += __shfl_xor_sync(0xffffffffu, acc, 1, 2);
+            if (valid && gl == 0) {
+                double nr = base + damping * (acc + dn);
+                dmax = fmax(dmax, fabs(nr - rank[v]));
+                rank_new[v] = nr;
+            }
+        }
+    }
+    for (int o = 16; o; o >>= 1) dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+    if (lane == 0 && dmax > 0.0) atomic_max_pos(diff, dmax);
 }
 
 // Jacobi commit of all three bins
@@ -321,6 +395,18 @@ void PR::sweep(int64_t tag) {
     GD_KERNEL(k_sum_partials, 1, 1024, 0, s, partial.get(), kRedBlocks, scal.get(), c);
     // algorithmic bytes: |A| (off + 2 f64) + E_in(A) (idx + f64), filled in from the bin
     // counts once the loop has read them back
+    static const bool split = getenv("GD_PR_SPLIT_BINS") != nullptr;
+    if (!split) {
+        int pi = prof_begin("pr_pull", 0, s);
+        prof_tag(pi, tag);
+        pull_recs.push_back({pi, -1});
+        k_pr_pull_fused<<<148 * 8, kFusedThreads, 0, s>>>(bins[0].get(), bins[1].get(), bins[2].get(), c, ix,
+                                                          contrib.get(), rank.get(), scal.get(), base, damping,
+                                                          inv_n, rank_new.get(), scal.get() + 1);
+        count_launch();
+        GD_LAUNCH_CHECK();
+        prof_end(pi, s);
+    } else {
     int pi = prof_begin("pr_pull", 0, s);
     prof_tag(pi, tag);
     pull_recs.push_back({pi, 0});
@@ -347,6 +433,7 @@ void PR::sweep(int64_t tag) {
     count_launch();
     GD_LAUNCH_CHECK();
     prof_end(pi, s);
+    }
     GD_KERNEL(k_pr_commit, 148 * 8, 256, 0, s, bins[0].get(), bins[1].get(), bins[2].get(), c, rank_new.get(),
               rank.get());
     if (comm) {  // every rank gets every owned range; the residual is the max over ranks
@@ -389,8 +476,16 @@ void PR::recompute(const uint8_t* flags) {
     last_sweeps = sweeps;
     iterations += sweeps;
     prof.sweep_limit = sweeps;  // queued no-op sweeps are not launches of the path
-    for (auto& pr : pull_recs)
-        if (pr.first >= 0) prof.pending[(size_t)pr.first].bytes = 24 * hctl[C_NBIN + pr.second] + 12 * hctl[C_EBIN + pr.second];
+    for (auto& pr : pull_recs) {
+        if (pr.first < 0) continue;
+        int64_t nb = 0, eb = 0;  // bin -1: all three
+        for (int k = 0; k < 3; ++k)
+            if (pr.second < 0 || pr.second == k) {
+                nb += hctl[C_NBIN + k];
+                eb += hctl[C_EBIN + k];
+            }
+        prof.pending[(size_t)pr.first].bytes = 24 * nb + 12 * eb;
+    }
     int64_t a = 0;
     for (int k = 0; k < 3; ++k) a += hctl[C_NBIN + k];
     last_affected = flags ? a : n;
