@@ -51,6 +51,15 @@ WORKLOADS = {
     "tc": dict(algo="tc", graph="uniform", nodes=1 << 24, edges=256_000_000, percent=1.0, weighted=False,
                directed=False, desc="dynamic TC, uniform 16,777,216 V / 256M undirected edges, 1% batches"),
     # BASELINE configs[3]
+    # north_star target: R-MAT scale-24 (16.8M V, 2^28 edges), 1-20% batches
+    "pr-rmat24": dict(algo="pr", graph="rmat", scale=24, edges=1 << 28, percent=1.0, weighted=False, directed=True,
+                      desc="dynamic PageRank, R-MAT scale-24 (16,777,216 V, 268,435,456 E), 1% batches"),
+    "sssp-rmat24": dict(algo="sssp", graph="rmat", scale=24, edges=1 << 28, percent=1.0, weighted=True,
+                        directed=True,
+                        desc="dynamic SSSP, R-MAT scale-24 (16,777,216 V, 268,435,456 E, w 1-100), 1% batches"),
+    "tc-rmat24": dict(algo="tc", graph="rmat", scale=24, edges=1 << 28, percent=1.0, weighted=False,
+                      directed=False,
+                      desc="dynamic TC, undirected R-MAT scale-24 (16,777,216 V, 268,435,456 edges), 1% batches"),
     # The reference's fixedPoint sweeps all V per round and needs ~rows+cols
     # rounds, so its CPU time grows ~side^3: its arm runs a 600x600 sample
     # of the same family (per-record rate overstates the full-size reference).
@@ -217,6 +226,7 @@ def main():
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="pr")
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--percent", type=float, default=None, help="override the workload's batch percentage")
     ap.add_argument("--static", action="store_true",
                     help="also time the static alternative per batch: apply the batch, merge, recompute from scratch "
                          "(staticSSSP / staticPR / staticTC), on up to 3 batches")
@@ -225,7 +235,10 @@ def main():
     ap.add_argument("--ref-batches", type=int, default=1,
                     help="bounded sample for the reference arm: at most this many batches")
     args = ap.parse_args()
-    wl = WORKLOADS[args.workload]
+    wl = dict(WORKLOADS[args.workload])
+    if args.percent is not None:
+        wl["percent"] = args.percent
+        wl["desc"] = wl["desc"].rsplit(",", 1)[0] + f", {args.percent:g}% batches"
     global GEN
     GEN = args.gen
 

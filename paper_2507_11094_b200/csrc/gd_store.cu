@@ -594,7 +594,7 @@ __global__ void k_win_ins(int64_t nwin, const int64_t* ipos, int64_t nins, int64
 // are loaded together and only the insertion positions depend on them.  All
 // per-entry arithmetic is 32-bit and relative to the window: the 64-bit
 // output base ws - dead + ins is formed once per window.
-template <bool FULL>
+template <bool FULL, bool WEIGHTED>
 __device__ __forceinline__ void edit_window(const int32_t* __restrict__ col, const int32_t* __restrict__ w,
                                             int64_t nnz, int64_t win, const int64_t* __restrict__ dead_win,
                                             const int64_t* __restrict__ ipos, const int64_t* __restrict__ pj_win,
@@ -606,31 +606,43 @@ __device__ __forceinline__ void edit_window(const int32_t* __restrict__ col, con
     const int64_t ws = win * kWin;
     const int lim = FULL ? kWin : (int)(nnz - ws);
     const int32_t* cb = col + ws;
-    const int32_t* wb = w ? w + ws : nullptr;
     int32_t v[Q], wv[Q];
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
         const int o = q * 32 + lane;
         const bool in = FULL || o < lim;
-        v[q] = in ? __ldcs(&cb[o]) : 0;
-        wv[q] = (wb && in) ? __ldcs(&wb[o]) : 0;
+        v[q] = in ? __ldcs(&cb[o]) : -1;
+        if (WEIGHTED) wv[q] = in ? __ldcs(&w[ws + o]) : 0;
     }
     const int64_t dead0 = dead_win[win];
     const int64_t pjw = pj_win[win], pje = pj_win[win + 1];
     const int nins = (int)(pje - pjw);
+    unsigned m[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) m[q] = __ballot_sync(0xffffffffu, v[q] < 0);  // out-of-range entries read as -1
+    const int64_t obase = ws - dead0 + pjw;  // newpos of window entry 0, before local shifts
+    int32_t* oc = ocol + obase;
+    int32_t* owb = WEIGHTED ? ow + obase : nullptr;
+    if (nins == 0) {  // the common window: only the dead shift
+        int dead = 0;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            const int np = q * 32 + lane - (dead + __popc(m[q] & lt));
+            if (v[q] >= 0) {
+                __stcs(&oc[np], v[q]);
+                if (WEIGHTED) __stcs(&owb[np], wv[q]);
+            }
+            dead += __popc(m[q]);
+        }
+        return;
+    }
     int my_ins = INT_MAX;
     int32_t my_icol = 0, my_iw = 1;
     if (lane < nins) {
         my_ins = (int)(ipos[pjw + lane] - ws);
         my_icol = icol[pjw + lane];
-        if (iw) my_iw = iw[pjw + lane];
+        if (WEIGHTED && iw) my_iw = iw[pjw + lane];
     }
-    unsigned m[Q];
-#pragma unroll
-    for (int q = 0; q < Q; ++q) m[q] = __ballot_sync(0xffffffffu, (FULL || q * 32 + lane < lim) && v[q] < 0);
-    const int64_t obase = ws - dead0 + pjw;  // newpos of window entry 0, before local shifts
-    int32_t* oc = ocol + obase;
-    int32_t* owb = ow ? ow + obase : nullptr;
     int dead = 0;
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
@@ -641,10 +653,10 @@ __device__ __forceinline__ void edit_window(const int32_t* __restrict__ col, con
         } else {
             for (int k = 0; k < nins; ++k) ins += __shfl_sync(0xffffffffu, my_ins, k) <= o;
         }
-        if ((FULL || o < lim) && v[q] >= 0) {
+        if (v[q] >= 0) {
             const int np = o - (dead + __popc(m[q] & lt)) + ins;
             __stcs(&oc[np], v[q]);
-            if (owb) __stcs(&owb[np], wv[q]);
+            if (WEIGHTED) __stcs(&owb[np], wv[q]);
         }
         dead += __popc(m[q]);
     }
@@ -658,10 +670,11 @@ __device__ __forceinline__ void edit_window(const int32_t* __restrict__ col, con
         for (int q = 0; q < Q; ++q) d += q < qq ? __popc(m[q]) : (q == qq ? __popc(m[q] & ((1u << r) - 1)) : 0);
         const int np = P - d + j;
         oc[np] = ic;
-        if (owb) owb[np] = iwv;
+        if (WEIGHTED) owb[np] = iwv;
     }
 }
 
+template <bool WEIGHTED>
 __global__ void __launch_bounds__(kEditThreads) k_edit_base(const int32_t* __restrict__ col,
                                                             const int32_t* __restrict__ w, int64_t nnz,
                                                             const int64_t* __restrict__ dead_win,
@@ -673,8 +686,8 @@ __global__ void __launch_bounds__(kEditThreads) k_edit_base(const int32_t* __res
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const int64_t nfull = nnz / kWin;
     for (int64_t win = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; win < nwin; win += nwarps) {
-        if (win < nfull) edit_window<true>(col, w, nnz, win, dead_win, ipos, pj_win, icol, iw, ocol, ow);
-        else edit_window<false>(col, w, nnz, win, dead_win, ipos, pj_win, icol, iw, ocol, ow);
+        if (win < nfull) edit_window<true, WEIGHTED>(col, w, nnz, win, dead_win, ipos, pj_win, icol, iw, ocol, ow);
+        else edit_window<false, WEIGHTED>(col, w, nnz, win, dead_win, ipos, pj_win, icol, iw, ocol, ow);
     }
 }
 
@@ -736,9 +749,13 @@ void edit_merge(cudaStream_t s, int64_t n, const int64_t* off, int32_t* col, con
         GD_KERNEL(k_win_ins, grid_for(nwin + 1, 256), 256, 0, s, nwin, ipos, nins, pj.get());
         unsigned g = (unsigned)std::min<int64_t>(ntiles, 148LL * 64);
         // algorithmic bytes: every base entry read once, every surviving entry written once
-        GD_KERNEL_T("merge_copy", (nnz + (nnz - dead_total)) * (weighted ? 8 : 4), k_edit_base, g, kEditThreads, 0,
-                    s, col, weighted ? w : nullptr, nnz, dead_win.get(), ipos, pj.get(), icol, iw, nwin,
-                    new_col.get(), weighted ? new_w.get() : nullptr);
+        if (weighted)
+            GD_KERNEL_T("merge_copy", (nnz + (nnz - dead_total)) * 8, k_edit_base<true>, g, kEditThreads, 0, s, col,
+                        w, nnz, dead_win.get(), ipos, pj.get(), icol, iw, nwin, new_col.get(), new_w.get());
+        else
+            GD_KERNEL_T("merge_copy", (nnz + (nnz - dead_total)) * 4, k_edit_base<false>, g, kEditThreads, 0, s,
+                        col, nullptr, nnz, dead_win.get(), ipos, pj.get(), icol, nullptr, nwin, new_col.get(),
+                        nullptr);
     }
     if (nins)
         GD_KERNEL(k_edit_tail, grid_for(nins, 256), 256, 0, s, ipos, nins, nnz, dead_win.get() + nwin, icol, iw,
