@@ -157,7 +157,7 @@ __global__ void k_row_starts_u32(const uint32_t* key, int64_t m, uint8_t* flag) 
 // chain length sizes the chain-offset field of the match sort key.
 constexpr int kHead = 256;
 constexpr int kScanWarps = 8;
-constexpr int kBitmapWords = 1024;  // 32 Kbit per warp
+constexpr int kBitmapWords = 1024;  // 32 Kbit per warp (a filter: hits are confirmed by binary search)
 
 __global__ void k_row_chunks(OutView ov, const uint64_t* rq_key, const int32_t* row_first, const int64_t* d_nrows,
                              int sh, int64_t* chunks, unsigned long long* maxlen) {
@@ -216,9 +216,10 @@ __device__ inline void emit_matches(const MatchOut& mo, int64_t p, int32_t row, 
 
 // index of the first request for (row, c), or -1
 __device__ inline int64_t requested(const uint64_t* rq_key, int64_t lo, int64_t hi, int32_t row, int32_t c, int sh,
-                                    int32_t c0, int32_t c1, const uint32_t* bm) {
+                                    int32_t c0, int32_t c1, const uint32_t* bm, uint64_t filt = ~0ULL) {
     if (c < 0) return -1;
     if (hi - lo <= 2) return c == c0 ? lo : (c == c1 ? lo + 1 : -1);
+    if (!((filt >> (c & 63)) & 1)) return -1;
     if (bm) {
         uint32_t h = (uint32_t)c & (kBitmapWords * 32 - 1);
         if (!(bm[h >> 5] & (1u << (h & 31)))) return -1;
@@ -244,6 +245,13 @@ __global__ void __launch_bounds__(256) k_del_scan_head(OutView ov, const int32_t
         int32_t row = valid ? key_row(rq_key[lo], sh) : 0;
         int32_t c0 = valid ? key_col(rq_key[lo], sh) : -2;
         int32_t c1 = (valid && hi - lo > 1) ? key_col(rq_key[lo + 1], sh) : -2;
+        // rows with more requests: a 64-bit filter of the requested columns
+        // (c & 63) keeps most slots off the binary search
+        uint64_t filt = 0;
+        if (valid && hi - lo > 2)
+            for (int64_t e = lo + gl; e < hi; e += G) filt |= 1ULL << (key_col(rq_key[e], sh) & 63);
+#pragma unroll
+        for (int o = 1; o < G; o <<= 1) filt |= __shfl_xor_sync(0xffffffffu, filt, o, G);
         int64_t acc = 0;
         for (int sg = 0; sg < ov.nseg; ++sg) {  // nseg is uniform: the loop stays warp-uniform
             int64_t a = valid ? ov.off[sg][row] : 0;
@@ -262,7 +270,7 @@ __global__ void __launch_bounds__(256) k_del_scan_head(OutView ov, const int32_t
 #pragma unroll
                 for (int u = 0; u < kScanILP; ++u) {
                     int64_t x = x0 + u * G + gl;
-                    int64_t hp = requested(rq_key, lo, hi, row, cv[u], sh, c0, c1, nullptr);
+                    int64_t hp = requested(rq_key, lo, hi, row, cv[u], sh, c0, c1, nullptr, filt);
                     emit_matches(mo, hp, row, cv[u], sh, acc + x, ov.base[sg] + a + x);
                 }
             }
@@ -271,28 +279,39 @@ __global__ void __launch_bounds__(256) k_del_scan_head(OutView ov, const int32_t
     }
 }
 
-// tail: one warp per kChunk piece of a long row beyond its head
+// work item -> row of the tail pieces (rows write their own ranges)
+__global__ void k_chunk_rows(const int64_t* coff, const int64_t* hdr, int32_t* wrow) {
+    const int64_t nrows = hdr[0];
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nrows; i += (int64_t)gridDim.x * blockDim.x)
+        for (int64_t j = coff[i]; j < coff[i + 1]; ++j) wrow[j] = (int32_t)i;
+}
+
+// tail: one warp per kChunk piece of a long row beyond its head; the piece's
+// row comes from a table (no search), and a warp that meets the same row
+// again keeps its request bitmap.
 __global__ void __launch_bounds__(kScanWarps * 32) k_del_scan_tail(OutView ov, const int32_t* row_first,
-                                                                   const int64_t* coff, const int64_t* hdr,
-                                                                   const uint64_t* rq_key, int64_t nrq, int sh,
-                                                                   MatchOut mo) {
+                                                                   const int64_t* coff, const int32_t* wrow,
+                                                                   const int64_t* hdr, const uint64_t* rq_key,
+                                                                   int64_t nrq, int sh, MatchOut mo) {
     const int64_t nrows = hdr[0], nwork = hdr[1];
     __shared__ uint32_t bitmap[kScanWarps][kBitmapWords];
     const int lane = threadIdx.x & 31;
     uint32_t* bm = bitmap[threadIdx.x >> 5];
-    int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    int64_t cur = -1;  // row whose bitmap is in bm
     for (int64_t wk = warp; wk < nwork; wk += nwarps) {
-        int64_t i = upper_bound_dev<int64_t>(coff, 0, nrows, wk) - 1;
-        int64_t chunk = wk - coff[i];
-        int64_t lo = row_first[i];
-        int64_t hi = (i + 1 < nrows) ? row_first[i + 1] : nrq;
-        int32_t row = key_row(rq_key[lo], sh);
-        int64_t ncols = hi - lo;
-        int32_t c0 = key_col(rq_key[lo], sh);
-        int32_t c1 = ncols > 1 ? key_col(rq_key[lo + 1], sh) : -2;
-        bool use_bm = ncols > 2;
-        if (use_bm) {
+        const int64_t i = wrow[wk];
+        const int64_t chunk = wk - coff[i];
+        const int64_t lo = row_first[i];
+        const int64_t hi = (i + 1 < nrows) ? row_first[i + 1] : nrq;
+        const int32_t row = key_row(rq_key[lo], sh);
+        const int64_t ncols = hi - lo;
+        const int32_t c0 = key_col(rq_key[lo], sh);
+        const int32_t c1 = ncols > 1 ? key_col(rq_key[lo + 1], sh) : -2;
+        const bool use_bm = ncols > 2;
+        if (use_bm && i != cur) {
+            __syncwarp();
             for (int q = lane; q < kBitmapWords; q += 32) bm[q] = 0;
             __syncwarp();
             for (int64_t e = lo + lane; e < hi; e += 32) {
@@ -300,6 +319,7 @@ __global__ void __launch_bounds__(kScanWarps * 32) k_del_scan_tail(OutView ov, c
                 atomicOr(&bm[c >> 5], 1u << (c & 31));
             }
             __syncwarp();
+            cur = i;
         }
         int64_t p0 = kHead + chunk * kChunk, p1 = p0 + kChunk;
         int64_t acc = 0;
@@ -324,7 +344,6 @@ __global__ void __launch_bounds__(kScanWarps * 32) k_del_scan_tail(OutView ov, c
             }
             acc += L;
         }
-        __syncwarp();
     }
 }
 
@@ -1075,6 +1094,9 @@ int64_t Store::apply_deletes(const int32_t* d_src, const int32_t* d_dst, int64_t
     exclusive_scan_i64(s, chunks.get(), coff.get(), nrq + 1);
     GD_CUDA(cudaMemcpyAsync(hdr.get() + 1, coff.get() + nrq, 8, cudaMemcpyDeviceToDevice, s));
     GD_CUDA(cudaMemcpyAsync(hdr.get() + 2, maxlen.get(), 8, cudaMemcpyDeviceToDevice, s));
+    // tail pieces: at most one per kChunk slots of the requested rows
+    DBuf<int32_t> wrow(total_slots() / kChunk + nrq + 1, s);
+    GD_KERNEL(k_chunk_rows, grid_for(nrq, 256), 256, 0, s, coff.get(), hdr.get(), wrow.get());
     // single-request pairs resolve by atomicMin; the rest collect overflow
     // matches (retry once with the exact size on overflow).  Row and work
     // counts stay on the device: the one read-back is the overflow size
@@ -1099,7 +1121,7 @@ int64_t Store::apply_deletes(const int32_t* d_src, const int32_t* d_dst, int64_t
         GD_KERNEL_T("del_scan", 0, k_del_scan_head, grid_for(((nrq + 3) / 4) * 32, 256, 148LL * 32), 256, 0, s, ov,
                     row_first.get(), hdr.get(), rq_key.get(), nrq, sh, mo);
         GD_KERNEL_T("del_scan", 0, k_del_scan_tail, 148 * 16, kScanWarps * 32, 0, s, ov, row_first.get(),
-                    coff.get(), hdr.get(), rq_key.get(), nrq, sh, mo);
+                    coff.get(), wrow.get(), hdr.get(), rq_key.get(), nrq, sh, mo);
         int64_t h2[2];
         read_small(s, h2, hdr.get() + 2, sizeof h2);
         maxchain = h2[0];
