@@ -122,6 +122,11 @@ GD_API int gd_sssp_batch(gd_sssp* s, const uint8_t* kind, const int64_t* src, co
 GD_API int gd_sssp_batch_device(gd_sssp* s, const uint8_t* kind, const int32_t* src, const int32_t* dst,
                          const int32_t* w, int64_t k, int64_t batch_index);
 GD_API int gd_sssp_read(gd_sssp* s, int64_t* dist, int64_t* parent);
+/* asynchronous variant: the state is snapshotted on the device at once and
+ * copied to the (ideally pinned) host buffers on a side stream that overlaps
+ * the next batch; the buffers are valid after gd_wait(s).  No reference
+ * counterpart: ctx.properties are read after the run (interp.py:112-160). */
+GD_API int gd_sssp_read_async(gd_sssp* s, int64_t* dist, int64_t* parent);
 GD_API int gd_sssp_destroy(gd_sssp* s);
 
 /* ---- dynamic PageRank: programs/pr_dynamic.sp:7-102 --------------------- */
@@ -132,6 +137,7 @@ GD_API int gd_pr_batch_device(gd_pr* p, const uint8_t* kind, const int32_t* src,
                        int64_t k, int64_t batch_index);
 /* pagerank[n] (float64); outdeg[n] nullable (the maintained int64 outdeg) */
 GD_API int gd_pr_read(gd_pr* p, double* rank, int64_t* outdeg);
+GD_API int gd_pr_read_async(gd_pr* p, double* rank); /* as gd_sssp_read_async */
 /* device pointer to the float64 rank vector (valid until the next call) */
 GD_API int gd_pr_rank_device(gd_pr* p, const double** rank);
 GD_API int gd_pr_destroy(gd_pr* p);
@@ -169,6 +175,8 @@ GD_API int gd_tc_set_comm(gd_tc* t, gd_comm* c);
 /* ---- reporting (ExecContext.phase_totals / fixedpoint_iterations,
  *      engine/interp.py:112-145); h is any gd_sssp* / gd_pr* / gd_tc* ---- */
 GD_API int gd_phase_times(const void* h, double ms[5]);
+/* block until the handle's asynchronous reads have landed in host memory */
+GD_API int gd_wait(const void* h);
 GD_API int gd_iterations(const void* h, int64_t* total_iterations);
 /* per-kernel device time of the last batch for roofline reporting:
  * name = "pr_pull" | "tc_count" | "sssp_relax" | "merge" ...; ms summed over

@@ -71,6 +71,9 @@ SIGNATURES = [
     ("gd_iterations", C.c_int, [vp, i64p]),
     ("gd_kernel_time", C.c_int, [vp, C.c_char_p, f64p, i64p, i64p]),
     ("gd_comm_stats", C.c_int, [vp, i64p]),
+    ("gd_sssp_read_async", C.c_int, [vp, vp, vp]),
+    ("gd_pr_read_async", C.c_int, [vp, vp]),
+    ("gd_wait", C.c_int, [vp]),
     ("gd_comm_reset_stats", C.c_int, [vp]),
     ("gd_kernel_time_total", C.c_int, [vp, C.c_char_p, f64p, i64p, i64p]),
     ("gd_set_profiling", C.c_int, [vp, C.c_int]),

@@ -93,6 +93,42 @@ static void raise_validation(int err, unsigned long long idx, int64_t n, char ki
                                            ": weight outside the int32 range of the B200 layout");
 }
 
+void AlgoBase::copy_out_async(void* host, const void* dev, size_t bytes, int slot) {
+    cudaStream_t st = stream();
+    if (!copy_stream) {
+        GD_CUDA(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
+        for (int k = 0; k < 2; ++k) {
+            GD_CUDA(cudaEventCreateWithFlags(&ev_ready[k], cudaEventDisableTiming));
+            GD_CUDA(cudaEventCreateWithFlags(&ev_copied[k], cudaEventDisableTiming));
+            GD_CUDA(cudaEventRecord(ev_copied[k], copy_stream));
+        }
+    }
+    if (!bytes) return;
+    // the snapshot buffer may still feed the previous read of this slot
+    GD_CUDA(cudaStreamWaitEvent(st, ev_copied[slot], 0));
+    snap[slot].ensure(bytes, st);
+    GD_CUDA(cudaMemcpyAsync(snap[slot].get(), dev, bytes, cudaMemcpyDeviceToDevice, st));
+    GD_CUDA(cudaEventRecord(ev_ready[slot], st));
+    GD_CUDA(cudaStreamWaitEvent(copy_stream, ev_ready[slot], 0));
+    GD_CUDA(cudaMemcpyAsync(host, snap[slot].get(), bytes, cudaMemcpyDeviceToHost, copy_stream));
+    GD_CUDA(cudaEventRecord(ev_copied[slot], copy_stream));
+}
+
+void AlgoBase::wait_copies() {
+    if (copy_stream) GD_CUDA(cudaStreamSynchronize(copy_stream));
+}
+
+AlgoBase::~AlgoBase() {
+    if (copy_stream) {
+        cudaStreamSynchronize(copy_stream);
+        for (int k = 0; k < 2; ++k) {
+            cudaEventDestroy(ev_ready[k]);
+            cudaEventDestroy(ev_copied[k]);
+        }
+        cudaStreamDestroy(copy_stream);
+    }
+}
+
 void AlgoBase::stage_host(DevBatch& b, const uint8_t* kind, const int64_t* src, const int64_t* dst,
                           const int64_t* w, int64_t k) {
     cudaStream_t st = stream();

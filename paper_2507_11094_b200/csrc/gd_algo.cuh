@@ -29,7 +29,6 @@ struct AlgoBase {
     KernelProf prof;
     int64_t iterations = 0;  // fixedPoint / while iterations, summed
     explicit AlgoBase(int k, Store* st) : kind(k), g(st) { timer.s = st->stream; }
-    virtual ~AlgoBase() = default;
     cudaStream_t stream() const { return g->stream; }
 
     // Stage host records (int64, 'a'/'d'), validate like _validate_batch
@@ -40,11 +39,23 @@ struct AlgoBase {
     void stage_device(DevBatch& b, const uint8_t* kind, const int32_t* src, const int32_t* dst, const int32_t* w,
                       int64_t k);
 
+    // Asynchronous result read-back: `snap` bytes are copied on the handle's
+    // stream into a device snapshot (so the next batch may overwrite the
+    // state at once), then to `host` on a side copy stream that overlaps the
+    // next batch.  host is valid after wait_copies() (pinned memory for a
+    // real overlap).
+    void copy_out_async(void* host, const void* dev, size_t bytes, int slot);
+    void wait_copies();
+    virtual ~AlgoBase();
+
   private:
     void split(DevBatch& b, const int32_t* sel_del, const int32_t* sel_add, const int32_t* s, const int32_t* d,
                const int32_t* w, int64_t kdel, int64_t kadd);
     DBuf<int64_t> h_stage;  // reusable device staging for host uploads
     DBuf<uint8_t> k_stage;
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t ev_ready[2] = {nullptr, nullptr}, ev_copied[2] = {nullptr, nullptr};
+    DBuf<uint8_t> snap[2];
 };
 
 // ---- frontier queue ----------------------------------------------------------

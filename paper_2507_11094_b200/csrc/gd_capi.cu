@@ -397,6 +397,17 @@ int gd_sssp_read(gd_sssp* s, int64_t* dist, int64_t* parent) {
         s->a->read(dist, parent);
     });
 }
+int gd_sssp_read_async(gd_sssp* s, int64_t* dist, int64_t* parent) {
+    if (!s) return null_handle();
+    return guard([&] {
+        GD_CUDA(cudaSetDevice(s->a->g->device));
+        s->a->read_async(dist, parent);
+    });
+}
+int gd_wait(const void* h) {
+    if (!h) return null_handle();
+    return guard([&] { algo_of(h)->wait_copies(); });
+}
 int gd_sssp_destroy(gd_sssp* s) {
     if (!s) return ok();
     return guard([&] {
@@ -423,6 +434,13 @@ int gd_pr_read(gd_pr* p, double* rank, int64_t* outdeg) {
     return guard([&] {
         GD_CUDA(cudaSetDevice(p->a->g->device));
         p->a->read(rank, outdeg);
+    });
+}
+int gd_pr_read_async(gd_pr* p, double* rank) {
+    if (!p) return null_handle();
+    return guard([&] {
+        GD_CUDA(cudaSetDevice(p->a->g->device));
+        p->a->copy_out_async(rank, p->a->rank.get(), (size_t)p->a->g->n * 8, 0);
     });
 }
 int gd_pr_rank_device(gd_pr* p, const double** rank) {

@@ -771,6 +771,18 @@ void SSSP::batch(DevBatch& b, int64_t batch_index) {
     prof.flush();
 }
 
+void SSSP::read_async(int64_t* h_dist, int64_t* h_parent) {
+    cudaStream_t s = stream();
+    int64_t n = g->n;
+    if (!n) return;
+    copy_out_async(h_dist, dist.get(), (size_t)n * 8, 0);
+    if (h_parent) {
+        parent64.ensure(n, s);
+        GD_KERNEL(k_read_parent, grid_for(n, 256), 256, 0, s, parent.get(), n, parent64.get());
+        copy_out_async(h_parent, parent64.get(), (size_t)n * 8, 1);
+    }
+}
+
 void SSSP::read(int64_t* h_dist, int64_t* h_parent) {
     cudaStream_t s = stream();
     int64_t n = g->n;

@@ -21,12 +21,14 @@ struct SSSP : AlgoBase {
     DBuf<unsigned long long> fcnt;
     DBuf<long long> fmin;
     DBuf<int32_t> infar;
-    DBuf<int32_t> heavy;   // stale vertices with > kHeavy in-arcs (pull sweep)
+    DBuf<int32_t> heavy;
+    DBuf<int64_t> parent64;  // int64 widening of parent for the async read   // stale vertices with > kHeavy in-arcs (pull sweep)
     DBuf<int64_t> dcount;  // device-side list sizes (no host read-back per fixpoint)
 
     SSSP(Store* st, int64_t src);  // = staticSSSP
     void batch(DevBatch& b, int64_t batch_index);
     void read(int64_t* dist, int64_t* parent);
+    void read_async(int64_t* dist, int64_t* parent);  // see AlgoBase::copy_out_async
 
   private:
     // one cooperative launch per fixpoint (relax / walk / pull); the seed count

@@ -179,6 +179,10 @@ class _Algo:
         N.check(N.lib().gd_iterations(self.h, C.byref(it)))
         return it.value
 
+    def wait(self) -> None:
+        """Block until read_async copies have landed (gd_wait)."""
+        N.check(N.lib().gd_wait(self.h))
+
     def set_profiling(self, on: bool) -> None:
         N.check(N.lib().gd_set_profiling(self.h, int(on)))
 
@@ -212,6 +216,14 @@ class SSSPHandle(_Algo):
         N.check(N.lib().gd_sssp_read(self.h, N.ptr(dist), N.ptr(parent)))
         return dist, parent
 
+    def read_async(self, dist_out: np.ndarray, parent_out: Optional[np.ndarray] = None) -> None:
+        """Asynchronous read (gd_sssp_read_async); valid after wait()."""
+        n = self.graph.node_count
+        for a in (dist_out, parent_out):
+            if a is not None and (a.dtype != np.int64 or a.size < n):
+                raise ValueError("outputs must be int64[node_count]")
+        N.check(N.lib().gd_sssp_read_async(self.h, N.ptr(dist_out), N.ptr(parent_out)))
+
 
 class PRHandle(_Algo):
     kind = "pr"
@@ -227,6 +239,13 @@ class PRHandle(_Algo):
         od = np.zeros(n, dtype=np.int64) if with_outdeg else None
         N.check(N.lib().gd_pr_read(self.h, N.ptr(rank), N.ptr(od)))
         return rank, od
+
+    def read_async(self, rank_out: np.ndarray) -> None:
+        """Snapshot the ranks now, copy them to rank_out (float64[n], pinned
+        for overlap) behind the next batch; valid after wait()."""
+        if rank_out.dtype != np.float64 or rank_out.size < self.graph.node_count:
+            raise ValueError("rank_out must be float64[node_count]")
+        N.check(N.lib().gd_pr_read_async(self.h, N.ptr(rank_out)))
 
     def rank_device_ptr(self) -> int:
         p = C.c_void_p()

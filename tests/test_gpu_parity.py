@@ -272,3 +272,32 @@ def test_comm_single_rank_sharded_paths_match(gd):
         cnt.append(tc.read())
     assert cnt[0] == cnt[1]
     assert comm.stats()["calls"] == 2  # the delete and the add phase's count all-reduce
+
+
+def test_async_reads_snapshot_the_state_at_the_call(gd):
+    """read_async snapshots on the device: a batch issued before wait() must
+    not leak into the buffers; wait() then yields exactly the read() result."""
+    rng = np.random.default_rng(5)
+    n = 3000
+    src, dst, w = rmat(11, 8 * n, rng, weighted=True)
+    n = 1 << 11
+    kind, us, ud, uw = updates(rng, n, src, dst, 1200, distinct_deletes=True)
+    g = gd.DynamicGraph.from_arrays(n, src, dst, w, weighted=True, with_reverse=True)
+    sp = gd.SSSPHandle(g, 0)
+    g2 = gd.DynamicGraph.from_arrays(n, src, dst, with_reverse=True)
+    pr = gd.PRHandle(g2, 0.85, 1e-10, 100)
+    d_out, p_out = np.zeros(n, np.int64), np.zeros(n, np.int64)
+    r_out = np.zeros(n, np.float64)
+    for bi, st in enumerate(range(0, 1200, 400)):
+        d_want, p_want = sp.read()
+        r_want = pr.read()[0]
+        sp.read_async(d_out, p_out)
+        pr.read_async(r_out)
+        part = gd.RecordArrays(kind[st:st + 400], us[st:st + 400], ud[st:st + 400], uw[st:st + 400])
+        sp.batch(part, bi)  # overwrites dist / parent / rank while the copies may be in flight
+        pr.batch(part, bi)
+        sp.wait()
+        pr.wait()
+        np.testing.assert_array_equal(d_out, d_want)
+        np.testing.assert_array_equal(p_out, p_want)
+        np.testing.assert_array_equal(r_out, r_want)
