@@ -136,6 +136,9 @@ void AlgoBase::stage_host(DevBatch& b, const uint8_t* kind, const int64_t* src, 
         b.kdel = b.kadd = 0;
         return;
     }
+    // record weights only matter to a weighted store or to SSSP's OnAdd
+    // (which reads the record's own weight); skip their upload otherwise
+    if (!g->weighted && this->kind != ALGO_SSSP) w = nullptr;
     h_stage.ensure(3 * k, st);
     k_stage.ensure(k, st);
     GD_CUDA(cudaMemcpyAsync(h_stage.get(), src, k * 8, cudaMemcpyHostToDevice, st));
