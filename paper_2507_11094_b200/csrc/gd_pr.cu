@@ -466,7 +466,7 @@ void PR::recompute(const uint8_t* flags) {
     while (!done) {
         // multi-GPU: one sweep at a time -- a queued no-op sweep would still
         // move the rank vector through its all-gather
-        const int64_t ahead = comm ? 1 : std::max<int64_t>(2, std::min<int64_t>(ahead_hint, 16));
+        const int64_t ahead = comm ? 1 : std::max<int64_t>(1, std::min<int64_t>(ahead_hint, 16));
         for (int64_t k = 0; k < ahead; ++k) sweep(sweeps + k);
         read_small(s, hctl, ctl.get(), sizeof hctl);
         done = hctl[C_DONE];

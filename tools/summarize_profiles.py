@@ -49,6 +49,10 @@ with open(os.path.join(out, "ncu_full_summary.csv"), "w", newline="") as fh:
     w = csv.writer(fh)
     w.writerow([h[i] + (f" [{units[i]}]" if units[i] else "") for i in idx])
     for row in d:
+        dur = float(row[h.index("gpu__time_duration.sum")]) * {"usecond": 1, "msecond": 1e3, "nsecond": 1e-3}.get(
+            units[h.index("gpu__time_duration.sum")], 1)
+        if dur < 10:  # a queued PR sweep that the device turned into a no-op
+            continue
         w.writerow([row[i] for i in idx])
         name = row[h.index("Kernel Name")]
         scale = {"Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "byte": 1}
