@@ -378,11 +378,11 @@ int64_t flood_weak_components(Store& g, uint8_t* flags, KernelProf* prof) {
     GD_KERNEL(k_uf_init, grid_for(n, 256), 256, 0, s, p.get(), n);
     GD_KERNEL_T("flood_sample", n * (8 + 4 * kSample), k_aff_sample, grid_for(n, 256), 256, 0, s, ov, n, p.get());
     GD_KERNEL(k_uf_compress, grid_for(n, 256), 256, 0, s, p.get(), n);
-    constexpr int kProbe = 1024;
+    constexpr int kProbe = 256;  // the giant component holds ~all non-isolated vertices
     DBuf<int32_t> probe(kProbe, s);
     GD_KERNEL(k_aff_gather, 4, 256, 0, s, p.get(), n, probe.get(), kProbe);
     DBuf<int32_t> giant(1, s);
-    GD_KERNEL(k_aff_giant, 1, 1024, 0, s, probe.get(), kProbe, giant.get());
+    GD_KERNEL(k_aff_giant, 1, kProbe, 0, s, probe.get(), kProbe, giant.get());
     GD_KERNEL_T("flood_rest", 0, k_aff_rest, grid_for(n, 256), 256, 0, s, ov, in, n, giant.get(), p.get());
     GD_KERNEL_T("flood_mark", 0, k_uf_compress_seed, grid_for(n, 256), 256, 0, s, p.get(), n, flags, seed.get());
     GD_KERNEL(k_uf_mark, grid_for(n, 256), 256, 0, s, p.get(), n, seed.get(), flags);

@@ -262,12 +262,15 @@ __global__ void k_pr_check(int64_t* ctl, const double* diff, double beta, int64_
 
 // OnDelete / OnAdd handlers (pr_dynamic.sp:87-97): mark both endpoints,
 // outdeg[src] -= 1 (deletes, misses included) / += 1 (adds).
-__global__ void k_pr_onupdate(const int32_t* s, const int32_t* d, int64_t k, int32_t delta, uint8_t* affected,
-                              int32_t* outdeg) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < k; i += (int64_t)gridDim.x * blockDim.x) {
-        affected[s[i]] = 1;
-        affected[d[i]] = 1;
-        atomicAdd(&outdeg[s[i]], delta);
+__global__ void k_pr_onupdate(const int32_t* ds, const int32_t* dd, int64_t kdel, const int32_t* as,
+                              const int32_t* ad, int64_t kadd, uint8_t* affected, int32_t* outdeg) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < kdel + kadd;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const bool del = i < kdel;
+        const int32_t s = del ? ds[i] : as[i - kdel], d = del ? dd[i] : ad[i - kdel];
+        affected[s] = 1;
+        affected[d] = 1;
+        atomicAdd(&outdeg[s], del ? -1 : 1);
     }
 }
 
@@ -497,10 +500,11 @@ void PR::batch(DevBatch& b, int64_t batch_index) {
     prof.reset_last();
     timer.begin(PH_PRE);
     affected.zero(s);
-    if (b.kdel) GD_KERNEL(k_pr_onupdate, grid_for(b.kdel, 256), 256, 0, s, b.ds.get(), b.dd.get(), b.kdel, -1,
-                          affected.get(), outdeg.get());
-    if (b.kadd) GD_KERNEL(k_pr_onupdate, grid_for(b.kadd, 256), 256, 0, s, b.as.get(), b.ad.get(), b.kadd, 1,
-                          affected.get(), outdeg.get());
+    // OnDelete then OnAdd (pr_dynamic.sp:87-97); both only mark and count, so
+    // one launch covers the two record lists
+    if (b.kdel + b.kadd)
+        GD_KERNEL(k_pr_onupdate, grid_for(b.kdel + b.kadd, 256), 256, 0, s, b.ds.get(), b.dd.get(), b.kdel,
+                  b.as.get(), b.ad.get(), b.kadd, affected.get(), outdeg.get());
     timer.begin(PH_STRUCT);
     g->apply_deletes(b.ds.get(), b.dd.get(), b.kdel, nullptr);
     g->apply_adds(b.as.get(), b.ad.get(), b.aw.get(), b.kadd);
