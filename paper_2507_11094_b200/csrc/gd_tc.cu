@@ -29,9 +29,27 @@ __device__ inline bool in_sorted(const int64_t* R, int64_t nr, int64_t x) {
     return p < nr && R[p] == x;
 }
 
-__global__ void k_ranks(const int32_t* s, const int32_t* d, int64_t k, int64_t n, uint64_t* r) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < k; i += (int64_t)gridDim.x * blockDim.x)
-        r[i] = (uint64_t)pair_rank(s[i], d[i], n);
+// Membership filter of the batch pair ranks: one bit per hashed rank, ~16
+// bits per record, so a common neighbour's (u,w) / (v,w) is almost always
+// cleared by one load instead of a binary search over R.
+__device__ inline uint64_t rank_hash(int64_t r) {
+    uint64_t x = (uint64_t)r * 0x9E3779B97F4A7C15ULL;
+    return x ^ (x >> 29);
+}
+
+__global__ void k_ranks(const int32_t* s, const int32_t* d, int64_t k, int64_t n, uint64_t* r, uint32_t* filt,
+                        uint64_t fmask) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < k; i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t rk = pair_rank(s[i], d[i], n);
+        r[i] = (uint64_t)rk;
+        uint64_t h = rank_hash(rk) & fmask;
+        atomicOr(&filt[h >> 5], 1u << (h & 31));
+    }
+}
+
+__device__ inline bool maybe_in(const uint32_t* filt, uint64_t fmask, int64_t r) {
+    uint64_t h = rank_hash(r) & fmask;
+    return (filt[h >> 5] >> (h & 31)) & 1;
 }
 
 // count of x in the sorted clean row [a, b)
@@ -41,30 +59,123 @@ __device__ inline int64_t mult_in(const int32_t* col, int64_t a, int64_t b, int3
     return upper_bound_dev<int32_t>(col, lo, b, x) - lo;
 }
 
-// one warp per batch record
-__global__ void __launch_bounds__(kThreads) k_tc_count(const int32_t* s, const int32_t* d, int64_t k, IdxView ix,
-                                                       int64_t n, const int64_t* R, int64_t nr,
+// ---------------------------------------------------------------------------
+// Per-record counting, load-balanced.  A record (u,v) walks the row of its
+// endpoint S with fewer arcs and looks each neighbour w up in the row of the
+// other endpoint L.  The walk is cut into kWalkChunk-arc work items (a hub-
+// hub record on R-MAT is 10^5 arcs: one warp would serialise it), and the
+// lookup is a bit test when L is a hub of this phase (degree >= kBmDeg):
+// the phase builds one n-bit bitmap per hub, up to a memory budget, from
+// its sorted row, and clears it afterwards.  A bit hit on a hub whose row
+// holds parallel arcs falls back to the binary search for the
+// multiplicity.  Counts are integers, so chunk partials add up exactly.
+// ---------------------------------------------------------------------------
+constexpr int kWalkChunk = 1024;
+constexpr int64_t kBmDeg = 1024;
+constexpr int64_t kBmBudget = 8LL << 30;  // bytes of hub bitmaps per phase
+
+struct TcRec {
+    int32_t* L;
+    int32_t* S;
+    int64_t* nch;    // work items of the record (then exclusive-scanned in place)
+};
+
+__global__ void k_tc_prep(const int32_t* s, const int32_t* d, int64_t k, IdxView ix, TcRec r, uint8_t* hubmark,
+                          unsigned long long* bytes) {
+    unsigned long long acc = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < k; i += (int64_t)gridDim.x * blockDim.x) {
+        int32_t u = s[i], v = d[i];
+        int64_t du = ix.off[u + 1] - ix.off[u], dv = ix.off[v + 1] - ix.off[v];
+        // walk the shorter row (ties: u, as the one-warp kernel did)
+        bool walk_u = du <= dv;
+        int32_t L = walk_u ? v : u, S = walk_u ? u : v;
+        int64_t dS = walk_u ? du : dv, dL = walk_u ? dv : du;
+        r.L[i] = L;
+        r.S[i] = S;
+        r.nch[i] = (dS + kWalkChunk - 1) / kWalkChunk;
+        if (dL >= kBmDeg) hubmark[L] = 1;
+        acc += 32 + 4 * (unsigned long long)(du + dv);  // 2*2*off + (deg u + deg v)*idx
+    }
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0 && acc) atomicAdd(bytes, acc);
+}
+
+__global__ void k_tc_chunk_table(const int64_t* choff, int64_t k, int32_t* rec_of) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < k; i += (int64_t)gridDim.x * blockDim.x)
+        for (int64_t c = choff[i]; c < choff[i + 1]; ++c) rec_of[c] = (int32_t)i;
+}
+
+__global__ void k_tc_hub_slots(const int32_t* hubs, const int64_t* nhub, int64_t hmax, int32_t* slot) {
+    const int64_t m = min(*nhub, hmax);
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < m; j += (int64_t)gridDim.x * blockDim.x)
+        slot[hubs[j]] = (int32_t)j;
+}
+
+// set (clear = false) or clear the bits of each budgeted hub's row; marks
+// hubs whose sorted row holds a repeated neighbour (parallel arcs)
+__global__ void k_tc_bitmaps(const int32_t* hubs, const int64_t* nhub, int64_t hmax, IdxView ix, int64_t words,
+                             uint32_t* bm, uint8_t* multi, bool clear) {
+    const int64_t m = min(*nhub, hmax);
+    for (int64_t j = blockIdx.x; j < m; j += gridDim.x) {
+        const int32_t h = hubs[j];
+        uint32_t* b = bm + j * words;
+        const int64_t a = ix.off[h], e = ix.off[h + 1];
+        bool dup = false;
+        for (int64_t q = a + threadIdx.x; q < e; q += blockDim.x) {
+            int32_t w = ix.col[q];
+            if (w < 0) continue;
+            if (clear) {
+                b[w >> 5] = 0;
+            } else {
+                atomicOr(&b[w >> 5], 1u << (w & 31));
+                dup |= q + 1 < e && ix.col[q + 1] == w;
+            }
+        }
+        if (!clear && __syncthreads_or(dup) && threadIdx.x == 0) multi[j] = 1;
+        if (clear && threadIdx.x == 0) multi[j] = 0;
+    }
+}
+
+__global__ void k_tc_reset(const int32_t* hubs, const int64_t* nhub, uint8_t* hubmark, int32_t* slot) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < *nhub; j += (int64_t)gridDim.x * blockDim.x) {
+        hubmark[hubs[j]] = 0;
+        slot[hubs[j]] = -1;
+    }
+}
+
+// one warp per work item: kWalkChunk arcs of S's row against L
+__global__ void __launch_bounds__(kThreads) k_tc_count(const int32_t* s, const int32_t* d, TcRec r,
+                                                       const int32_t* rec_of, const int64_t* nwork, IdxView ix,
+                                                       int64_t n, const int64_t* R, int64_t nr, const int32_t* slot,
+                                                       const uint32_t* bm, int64_t words, const uint8_t* multi,
+                                                       const uint32_t* filt, uint64_t fmask,
                                                        unsigned long long* total) {
     const int lane = threadIdx.x & 31;
-    int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t nw = *nwork;
     int64_t acc = 0;
-    for (int64_t i = warp; i < k; i += nwarps) {
-        int32_t u = s[i], v = d[i];
-        int64_t r = pair_rank(u, v, n);
-        int64_t ua = ix.off[u], ub = ix.off[u + 1];
-        int64_t va = ix.off[v], vb = ix.off[v + 1];
-        // walk the shorter row, search the longer
-        bool walk_u = (ub - ua) <= (vb - va);
-        int64_t wa = walk_u ? ua : va, wb = walk_u ? ub : vb;
-        int64_t sa = walk_u ? va : ua, sb = walk_u ? vb : ub;
+    for (int64_t c = warp; c < nw; c += nwarps) {
+        const int32_t i = rec_of[c];
+        const int32_t u = s[i], v = d[i];
+        const int64_t rk = pair_rank(u, v, n);
+        const int32_t L = r.L[i], S = r.S[i];
+        const int64_t j = c - r.nch[i];  // nch holds the exclusive scan here
+        const int64_t wa = ix.off[S] + j * kWalkChunk, wb = min(wa + kWalkChunk, ix.off[S + 1]);
+        const int64_t la = ix.off[L], lb = ix.off[L + 1];
+        const int32_t hs = slot[L];
+        const uint32_t* b = hs >= 0 ? bm + (int64_t)hs * words : nullptr;
+        const bool mult = hs >= 0 && multi[hs];
         for (int64_t e = wa + lane; e < wb; e += 32) {
             int32_t w = ix.col[e];
-            if (w == v) continue;
-            int64_t m = mult_in(ix.col, sa, sb, w);
+            if (w < 0 || w == v) continue;
+            int64_t m;
+            if (b) m = (b[w >> 5] >> (w & 31)) & 1 ? (mult ? mult_in(ix.col, la, lb, w) : 1) : 0;
+            else m = mult_in(ix.col, la, lb, w);
             if (!m) continue;
             int64_t ru = pair_rank(u, w, n), rv = pair_rank(v, w, n);
-            bool skip = (ru < r && in_sorted(R, nr, ru)) || (rv < r && in_sorted(R, nr, rv));
+            bool skip = (ru < rk && maybe_in(filt, fmask, ru) && in_sorted(R, nr, ru)) ||
+                        (rv < rk && maybe_in(filt, fmask, rv) && in_sorted(R, nr, rv));
             if (!skip) acc += m;
         }
     }
@@ -103,19 +214,84 @@ int64_t TC::count_records(const int32_t* s, const int32_t* d, int64_t k) {
     cudaStream_t st = stream();
     SortedIndex& ix = g->tc_index();
     g->compact_index(ix);
+    const int64_t n = g->n;
     DBuf<uint64_t> R(k, st);
-    GD_KERNEL(k_ranks, grid_for(k, 256), 256, 0, st, s, d, k, g->n, R.get());
+    int fbits = 10;  // filter of 2^fbits bits, >= 16 per record
+    while (fbits < 34 && (int64_t(1) << fbits) < 16 * k) ++fbits;
+    DBuf<uint32_t> filt((size_t(1) << fbits) / 32, st);
+    filt.zero(st);
+    const uint64_t fmask = (uint64_t(1) << fbits) - 1;
+    GD_KERNEL(k_ranks, grid_for(k, 256), 256, 0, st, s, d, k, n, R.get(), filt.get(), fmask);
     sort_keys_u64(st, R.get(), k);
-    DBuf<unsigned long long> tot(1, st);
-    tot.zero(st);
+    DBuf<unsigned long long> ctr(2, st);  // [0] count delta, [1] algorithmic bytes
+    ctr.zero(st);
     // ranks are over ALL records of the phase; the counted slice is this rank's
-    int64_t a = comm ? k * comm->rank / comm->world : 0;
-    int64_t b = comm ? k * (comm->rank + 1) / comm->world : k;
-    if (b > a)
-        GD_KERNEL_T("tc_count", 0, k_tc_count, grid_for((b - a) * 32, kThreads, 148LL * 64), kThreads, 0, st, s + a,
-                    d + a, b - a, ix.view(), g->n, reinterpret_cast<const int64_t*>(R.get()), k, tot.get());
-    if (comm) comm->allreduce_sum_i64(reinterpret_cast<int64_t*>(tot.get()), 1, st);
-    return (int64_t)read_scalar(st, tot.get());
+    const int64_t a = comm ? k * comm->rank / comm->world : 0;
+    const int64_t b = comm ? k * (comm->rank + 1) / comm->world : k;
+    const int64_t m = b - a;
+    if (m > 0) {
+        if (hubmark.n < (size_t)n) {
+            hubmark.alloc(n, st);
+            hubmark.zero(st);
+            hub_slot.alloc(n, st);
+            fill_i32(st, hub_slot.get(), n, -1);
+        }
+        DBuf<int32_t> L(m, st), S(m, st);
+        DBuf<int64_t> nch(m + 1, st), choff(m + 1, st);
+        GD_CUDA(cudaMemsetAsync(nch.get() + m, 0, sizeof(int64_t), st));
+        TcRec rr{L.get(), S.get(), nch.get()};
+        GD_KERNEL(k_tc_prep, grid_for(m, 256), 256, 0, st, s + a, d + a, m, ix.view(), rr, hubmark.get(),
+                  ctr.get() + 1);
+        exclusive_scan_i64(st, nch.get(), choff.get(), m + 1);
+        rr.nch = choff.get();
+        // hubs of this phase: L endpoints with >= kBmDeg arcs
+        DBuf<int32_t> hubs(n, st);
+        DBuf<int64_t> cnt2(2, st);  // [work items, hubs] for one read-back
+        GD_CUDA(cudaMemcpyAsync(cnt2.get(), choff.get() + m, sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
+        select_flagged_index_async(st, hubmark.get(), n, hubs.get(), cnt2.get() + 1);
+        int64_t hc[2];
+        read_small(st, hc, cnt2.get(), sizeof hc);
+        const int64_t nwork = hc[0], nhubs = hc[1];
+        // work items: exact count (records may share a long S row)
+        DBuf<int32_t> rec_of(std::max<int64_t>(nwork, 1), st);
+        GD_KERNEL(k_tc_chunk_table, grid_for(m, 256), 256, 0, st, choff.get(), m, rec_of.get());
+        // bitmaps for as many hubs as the budget allows (grow-only; every
+        // phase leaves them clean)
+        const int64_t words = (n + 31) / 32;
+        const int64_t hmax = std::min<int64_t>(nhubs, kBmBudget / (words * 4));
+        if (hmax > 0 && bm.n < (size_t)(hmax * words)) {
+            bm.alloc((size_t)(hmax * words), st);
+            GD_CUDA(cudaMemsetAsync(bm.get(), 0, bm.n * 4, st));
+            bm_multi.alloc(hmax, st);
+            bm_multi.zero(st);
+        }
+        const int64_t* nhub = cnt2.get() + 1;
+        if (hmax > 0) {
+            GD_KERNEL(k_tc_hub_slots, grid_for(hmax, 256), 256, 0, st, hubs.get(), nhub, hmax, hub_slot.get());
+            GD_KERNEL(k_tc_bitmaps, 148 * 4, 256, 0, st, hubs.get(), nhub, hmax, ix.view(), words, bm.get(),
+                      bm_multi.get(), false);
+        }
+        int pi = prof_begin("tc_count", 0, st);
+        k_tc_count<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((nwork + 7) / 8, 148 * 16)), kThreads, 0,
+                     st>>>(s + a, d + a, rr, rec_of.get(), choff.get() + m, ix.view(), n,
+                                                 reinterpret_cast<const int64_t*>(R.get()), k, hub_slot.get(),
+                                                 bm.get(), words, bm_multi.get(), filt.get(), fmask, ctr.get());
+        count_launch();
+        GD_LAUNCH_CHECK();
+        prof_end(pi, st);
+        if (hmax > 0)
+            GD_KERNEL(k_tc_bitmaps, 148 * 4, 256, 0, st, hubs.get(), nhub, hmax, ix.view(), words, bm.get(),
+                      bm_multi.get(), true);
+        if (nhubs > 0)
+            GD_KERNEL(k_tc_reset, grid_for(nhubs, 256), 256, 0, st, hubs.get(), nhub, hubmark.get(), hub_slot.get());
+        if (pi >= 0) count_rec.push_back(pi);
+    }
+    if (comm) comm->allreduce_sum_i64(reinterpret_cast<int64_t*>(ctr.get()), 1, st);
+    unsigned long long h[2];
+    read_small(st, h, ctr.get(), sizeof h);
+    for (int pi : count_rec) prof.pending[(size_t)pi].bytes = (int64_t)h[1];
+    count_rec.clear();
+    return (int64_t)h[0];
 }
 
 TC::TC(Store* st) : AlgoBase(ALGO_TC, st) {

@@ -1,6 +1,8 @@
 // gd_tc.cuh -- dynamic triangle counting state (programs/tc_dynamic.sp).
 #pragma once
 
+#include <vector>
+
 #include "gd_algo.cuh"
 #include "gd_comm.cuh"
 
@@ -9,6 +11,11 @@ namespace gdb {
 struct TC : AlgoBase {
     int64_t count = 0;
     Comm* comm = nullptr;  // set: count a contiguous 1/world slice of the records, all-reduce
+    // hub bitmaps of the counting phases (see gd_tc.cu); kept clean between phases
+    DBuf<uint8_t> hubmark, bm_multi;
+    DBuf<int32_t> hub_slot;
+    DBuf<uint32_t> bm;
+    std::vector<int> count_rec;
     explicit TC(Store* st);  // = staticTC
     void batch(DevBatch& b, int64_t batch_index);
 

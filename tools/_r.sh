@@ -1,3 +1,3 @@
-bash tools/gpu_launches.sh > gpurun_out/launches.log 2>&1; echo "launches rc=$?"; tail -2 gpurun_out/launches.log
-KREGEX='k_pr_pull_fused|k_edit_base|k_del_scan|k_pr_contrib|k_aff_sample' NCU_SKIP=4 NCU_COUNT=12 bash tools/gpu_ncu_full.sh > gpurun_out/full.log 2>&1; echo "full rc=$?"; tail -2 gpurun_out/full.log
-timeout 900 python bench.py > gpurun_out/bench_default.json 2> gpurun_out/bench_default.err; echo "bench rc=$?"; cat gpurun_out/bench_default.json | head -c 300
+timeout 900 python -m pytest tests -m gpu -x -q --timeout 300 -p no:cacheprovider -k "tc or TC or smoke or golden" 2>&1 | tail -1
+for wl in tc-rmat24 tc; do timeout 900 python bench.py --workload $wl --steps 5 --warmup 3 --e2e-steps 3 --no-cpu-baseline > gpurun_out/tcx.json 2> gpurun_out/tcx.err; python -c "
+import json; j=json.load(open('gpurun_out/tcx.json')); print('$wl', j['ms_per_step'], j['e2e']['ms_per_step'], j['roofline']['kernel'], j['roofline']['frac'], {k: (round(v['ms_total']/j['steps'],2), v['gbs']) for k,v in j['kernels'].items()})"; done
