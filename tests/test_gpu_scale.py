@@ -144,8 +144,8 @@ def test_tc_dynamic_equals_static_on_final_graph(gd, n, m, pct):
 
 
 @pytest.mark.parametrize("graph", ["rmat", "grid"])
-@pytest.mark.parametrize("delta", ["0", "7", "100", "5000"])
-def test_sssp_near_far_width_does_not_change_results(gd, graph, delta, monkeypatch):
+@pytest.mark.parametrize("delta,decr", [("0", "1"), ("0", "0"), ("7", "1"), ("100", "1"), ("5000", "1")])
+def test_sssp_near_far_width_does_not_change_results(gd, graph, delta, decr, monkeypatch):
     """The near-far bucket width (GD_SSSP_DELTA; 0 = plain frontier) and the
     decremental sweep+push it enables must reproduce the reference oracle."""
     from oracle import oracle as O
@@ -157,6 +157,7 @@ def test_sssp_near_far_width_does_not_change_results(gd, graph, delta, monkeypat
         s, d, w, n = G.grid(60, 60, seed=3)
     kind, us, ud, uw, per = G.updates(s, d, n, percent=10, batches=3, seed=4, max_weight=100)
     monkeypatch.setenv("GD_SSSP_DELTA", delta)
+    monkeypatch.setenv("GD_SSSP_DECR", decr)  # 0: the pull fixpoint instead of sweep + push
     g = gd.DynamicGraph.from_arrays(n, s, d, w, weighted=True, with_reverse=True)
     ctx = gd.run_batches(gd.compile_source("Dynamic dynamicSSSP("), g, gd.UpdateStream.from_arrays(kind, us, ud, uw),
                          per, {"src": 0})

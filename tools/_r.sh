@@ -1,3 +1,4 @@
-timeout 900 python -m pytest tests -m gpu -x -q --timeout 300 -p no:cacheprovider -k "tc or TC or smoke or golden" 2>&1 | tail -1
-for wl in tc-rmat24 tc; do timeout 900 python bench.py --workload $wl --steps 5 --warmup 3 --e2e-steps 3 --no-cpu-baseline > gpurun_out/tcx.json 2> gpurun_out/tcx.err; python -c "
-import json; j=json.load(open('gpurun_out/tcx.json')); print('$wl', j['ms_per_step'], j['e2e']['ms_per_step'], j['roofline']['kernel'], j['roofline']['frac'], {k: (round(v['ms_total']/j['steps'],2), v['gbs']) for k,v in j['kernels'].items()})"; done
+for dm in 0 1; do for p in 1 10 20; do GD_SSSP_DECR=$dm timeout 900 python bench.py --workload sssp-rmat24 --percent $p --steps 4 --warmup 2 --e2e-steps 2 --no-cpu-baseline > gpurun_out/s.json 2> gpurun_out/s.err; python -c "
+import json; j=json.load(open('gpurun_out/s.json')); print('decr=$dm p=$p', round(j['ms_per_step'],2), {k: round(v['ms_total']/j['steps'],2) for k,v in j['kernels'].items()})"; done
+GD_SSSP_DECR=$dm timeout 900 python bench.py --workload sssp --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/s.json 2> gpurun_out/s.err; python -c "
+import json; j=json.load(open('gpurun_out/s.json')); print('decr=$dm C1', round(j['ms_per_step'],3))"; done
