@@ -61,12 +61,12 @@ struct AlgoBase {
 // ---- frontier queue ----------------------------------------------------------
 struct Frontier {
     DBuf<int32_t> q[2];
-    DBuf<unsigned long long> cnt;  // [10]: 3 counter slots + scratch
+    DBuf<unsigned long long> cnt;  // [11]: 3 counter slots + scratch
     int cur = 0;
     void init(int64_t n, cudaStream_t s) {
         q[0].ensure(n + 1, s);
         q[1].ensure(n + 1, s);
-        cnt.ensure(10, s);
+        cnt.ensure(11, s);
     }
 };
 

@@ -508,15 +508,17 @@ __global__ void k_fp_prep(unsigned long long* cnt, const int64_t* d_n, int64_t n
 // parent = min-id in-neighbour u with dist[u] + w == dist[v] (sssp_dynamic.sp:23-34)
 __global__ void __launch_bounds__(kThreads) k_fix_parent(const int32_t* list, const int64_t* d_m, int64_t m,
                                                          IdxView ix, const int64_t* dist, int32_t* parent,
-                                                         int32_t src) {
+                                                         int32_t src, int32_t* heavy, unsigned long long* nheavy) {
     if (d_m) m = *d_m;
     GROUP_LOOP_BEGIN(m)
     int32_t v = valid ? (list ? list[_t] : (int32_t)_t) : 0;
     int64_t dv = valid ? dist[v] : kInf;
     bool act = valid && v != src && dv < kInf;
     int32_t best = INT_MAX;
-    if (act) {
-        int64_t a = ix.off[v], b = ix.off[v + 1];
+    const int64_t a = act ? ix.off[v] : 0, b = act ? ix.off[v + 1] : 0;
+    const bool hv = heavy && b - a > kHeavy;  // group-uniform: a whole CTA takes it below
+    if (hv && lane == 0) heavy[atomicAdd(nheavy, 1ULL)] = v;
+    if (act && !hv) {
         for (int64_t e = a + lane; e < b; e += kG) {
             int32_t u = ix.col[e];
             if (u < 0) continue;
@@ -528,8 +530,33 @@ __global__ void __launch_bounds__(kThreads) k_fix_parent(const int32_t* list, co
         int32_t x = __shfl_xor_sync(0xffffffffu, best, o, kG);
         best = x < best ? x : best;
     }
-    if (act && lane == 0) parent[v] = best == INT_MAX ? -1 : best;
+    if (act && !hv && lane == 0) parent[v] = best == INT_MAX ? -1 : best;
     GROUP_LOOP_END
+}
+
+// the parent fix-up of vertices with more than kHeavy in-arcs: one CTA each
+__global__ void __launch_bounds__(kThreads) k_fix_parent_heavy(const int32_t* heavy, const unsigned long long* nheavy,
+                                                               IdxView ix, const int64_t* dist, int32_t* parent) {
+    __shared__ int32_t part[kThreads / 32];
+    const int64_t nh = (int64_t)*nheavy;
+    for (int64_t h = blockIdx.x; h < nh; h += gridDim.x) {
+        const int32_t v = heavy[h];
+        const int64_t dv = dist[v];
+        int32_t best = INT_MAX;
+        for (int64_t e = ix.off[v] + threadIdx.x; e < ix.off[v + 1]; e += kThreads) {
+            int32_t u = ix.col[e];
+            if (u < 0) continue;
+            if (sat_add(dist[u], ix.w ? (int64_t)ix.w[e] : 1) == dv && u < best) best = u;
+        }
+        for (int o = 16; o; o >>= 1) best = min(best, __shfl_xor_sync(0xffffffffu, best, o));
+        if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = best;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int j = 1; j < kThreads / 32; ++j) best = min(best, part[j]);
+            parent[v] = best == INT_MAX ? -1 : best;
+        }
+        __syncthreads();
+    }
 }
 
 // OnDelete (sssp_dynamic.sp:139-146): a tree-edge deletion invalidates dst
@@ -689,8 +716,15 @@ void SSSP::fixpoint(int mode, const int32_t* seeds, const int64_t* d_nseeds, int
 
 void SSSP::fix_parents(const int32_t* list, const int64_t* d_m, int64_t m) {
     if (m == 0) return;
-    GD_KERNEL_T("sssp_parent", 0, k_fix_parent, group_grid(m), kThreads, 0, stream(), list, d_m, m, g->rev.view(),
-                dist.get(), parent.get(), src);
+    cudaStream_t s = stream();
+    IdxView ix = g->rev.view();
+    heavy.ensure(g->rev.nnz / kHeavy + 64, s);
+    unsigned long long* nh = fr.cnt.get() + 10;
+    GD_CUDA(cudaMemsetAsync(nh, 0, sizeof(unsigned long long), s));
+    GD_KERNEL_T("sssp_parent", 0, k_fix_parent, group_grid(m), kThreads, 0, s, list, d_m, m, ix, dist.get(),
+                parent.get(), src, heavy.get(), nh);
+    GD_KERNEL_T("sssp_parent", 0, k_fix_parent_heavy, 148 * 4, kThreads, 0, s, heavy.get(), nh, ix, dist.get(),
+                parent.get());
 }
 
 // one read-back per batch: total rounds and the divergence flag
