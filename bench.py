@@ -60,6 +60,23 @@ WORKLOADS = {
     "tc-rmat24": dict(algo="tc", graph="rmat", scale=24, edges=1 << 28, percent=1.0, weighted=False,
                       directed=False,
                       desc="dynamic TC, undirected R-MAT scale-24 (16,777,216 V, 268,435,456 edges), 1% batches"),
+    # BASELINE configs[4] (C5) on one GPU: R-MAT scale-26, 2^30 edges.  The
+    # reference arm cannot run it in bounded time (its per-batch cost grows
+    # with E and the store alone needs ~50 GB of host RAM), so it times the
+    # scale-22 sample of the same recipe; its per-record rate overstates the
+    # full-size reference.
+    "pr-c5": dict(algo="pr", graph="rmat", scale=26, edges=1 << 30, percent=1.0, weighted=False, directed=True,
+                  desc="dynamic PageRank, R-MAT scale-26 (67,108,864 V, 1,073,741,824 E), 1% batches",
+                  ref_sample=dict(scale=22, edges=1 << 26,
+                                  desc="dynamic PageRank, R-MAT scale-22 sample (4.2M V, 67M E), 1% batches")),
+    "sssp-c5": dict(algo="sssp", graph="rmat", scale=26, edges=1 << 30, percent=1.0, weighted=True, directed=True,
+                    desc="dynamic SSSP, R-MAT scale-26 (67,108,864 V, 1,073,741,824 E, w 1-100), 1% batches",
+                    ref_sample=dict(scale=22, edges=1 << 26,
+                                    desc="dynamic SSSP, R-MAT scale-22 sample (4.2M V, 67M E), 1% batches")),
+    "tc-c5": dict(algo="tc", graph="rmat", scale=26, edges=1 << 30, percent=1.0, weighted=False, directed=False,
+                  desc="dynamic TC, undirected R-MAT scale-26 (67,108,864 V, 1,073,741,824 edges), 1% batches",
+                  ref_sample=dict(scale=20, edges=1 << 24,
+                                  desc="dynamic TC, undirected R-MAT scale-20 sample (1M V, 16.8M edges), 1% batches")),
     # The reference's fixedPoint sweeps all V per round and needs ~rows+cols
     # rounds, so its CPU time grows ~side^3: its arm runs a 600x600 sample
     # of the same family (per-record rate overstates the full-size reference).

@@ -348,7 +348,9 @@ __global__ void k_uf_compress_seed(int32_t* p, int64_t n, const uint8_t* flags, 
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         int32_t r = uf_find(p, (int32_t)i);
         p[i] = r;
-        if (flags[i]) root_has_seed[r] = 1;
+        // read before writing: ~all flagged vertices share the giant's root,
+        // and a million stores to one address serialise in L2
+        if (flags[i] && !root_has_seed[r]) root_has_seed[r] = 1;
     }
 }
 

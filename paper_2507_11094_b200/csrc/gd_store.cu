@@ -230,7 +230,7 @@ __device__ inline int64_t requested(const uint64_t* rq_key, int64_t lo, int64_t 
 }
 
 // head: one 8-lane group per requested row, chain slots [0, kHead)
-__global__ void __launch_bounds__(256) k_del_scan_head(OutView ov, const int32_t* row_first, const int64_t* d_nrows,
+__global__ void __launch_bounds__(256, 4) k_del_scan_head(OutView ov, const int32_t* row_first, const int64_t* d_nrows,
                                                        const uint64_t* rq_key, int64_t nrq, int sh, MatchOut mo) {
     constexpr int G = 8, kPer = 32 / G;
     const int64_t nrows = *d_nrows;
@@ -267,11 +267,19 @@ __global__ void __launch_bounds__(256) k_del_scan_head(OutView ov, const int32_t
                     int64_t x = x0 + u * G + gl;
                     cv[u] = x < len ? col[a + x] : -1;
                 }
+                int64_t hp[kScanILP];
+                bool any = false;
 #pragma unroll
                 for (int u = 0; u < kScanILP; ++u) {
-                    int64_t x = x0 + u * G + gl;
-                    int64_t hp = requested(rq_key, lo, hi, row, cv[u], sh, c0, c1, nullptr, filt);
-                    emit_matches(mo, hp, row, cv[u], sh, acc + x, ov.base[sg] + a + x);
+                    hp[u] = requested(rq_key, lo, hi, row, cv[u], sh, c0, c1, nullptr, filt);
+                    any |= hp[u] >= 0;
+                }
+                if (__any_sync(0xffffffffu, any)) {  // hits are rare: one vote per ILP batch
+#pragma unroll
+                    for (int u = 0; u < kScanILP; ++u) {
+                        int64_t x = x0 + u * G + gl;
+                        emit_matches(mo, hp[u], row, cv[u], sh, acc + x, ov.base[sg] + a + x);
+                    }
                 }
             }
             acc += L;
@@ -289,7 +297,7 @@ __global__ void k_chunk_rows(const int64_t* coff, const int64_t* hdr, int32_t* w
 // tail: one warp per kChunk piece of a long row beyond its head; the piece's
 // row comes from a table (no search), and a warp that meets the same row
 // again keeps its request bitmap.
-__global__ void __launch_bounds__(kScanWarps * 32) k_del_scan_tail(OutView ov, const int32_t* row_first,
+__global__ void __launch_bounds__(kScanWarps * 32, 4) k_del_scan_tail(OutView ov, const int32_t* row_first,
                                                                    const int64_t* coff, const int32_t* wrow,
                                                                    const int64_t* hdr, const uint64_t* rq_key,
                                                                    int64_t nrq, int sh, MatchOut mo) {
@@ -335,11 +343,19 @@ __global__ void __launch_bounds__(kScanWarps * 32) k_del_scan_tail(OutView ov, c
                     int64_t x = x0 + u * 32 + lane;
                     cv[u] = x < s1 ? col[a + (x - acc)] : -1;
                 }
+                int64_t hp[kScanILP];
+                bool any = false;
 #pragma unroll
                 for (int u = 0; u < kScanILP; ++u) {
-                    int64_t x = x0 + u * 32 + lane;
-                    int64_t hp = requested(rq_key, lo, hi, row, cv[u], sh, c0, c1, use_bm ? bm : nullptr);
-                    emit_matches(mo, hp, row, cv[u], sh, x, ov.base[sg] + a + (x - acc));
+                    hp[u] = requested(rq_key, lo, hi, row, cv[u], sh, c0, c1, use_bm ? bm : nullptr);
+                    any |= hp[u] >= 0;
+                }
+                if (__any_sync(0xffffffffu, any)) {
+#pragma unroll
+                    for (int u = 0; u < kScanILP; ++u) {
+                        int64_t x = x0 + u * 32 + lane;
+                        emit_matches(mo, hp[u], row, cv[u], sh, x, ov.base[sg] + a + (x - acc));
+                    }
                 }
             }
             acc += L;
