@@ -48,18 +48,28 @@ WORKLOADS = {
     "sssp": dict(algo="sssp", graph="rmat", scale=16, edges=1_000_000, percent=5.0, weighted=True, directed=True,
                  desc="dynamic SSSP, R-MAT scale-16 (65,536 V, 1M E, w 1-100), 5% batches"),
     # BASELINE configs[2] at 1%
+    # (the reference's emitted TC runs single-threaded -- it crashes with more,
+    # so its arm times a 1M-vertex sample of the recipe)
     "tc": dict(algo="tc", graph="uniform", nodes=1 << 24, edges=256_000_000, percent=1.0, weighted=False,
-               directed=False, desc="dynamic TC, uniform 16,777,216 V / 256M undirected edges, 1% batches"),
+               directed=False, desc="dynamic TC, uniform 16,777,216 V / 256M undirected edges, 1% batches",
+               ref_sample=dict(nodes=1 << 20, edges=1 << 24,
+                               desc="dynamic TC, uniform 1,048,576 V / 16.8M undirected edges sample, 1% batches")),
     # BASELINE configs[3]
     # north_star target: R-MAT scale-24 (16.8M V, 2^28 edges), 1-20% batches
     "pr-rmat24": dict(algo="pr", graph="rmat", scale=24, edges=1 << 28, percent=1.0, weighted=False, directed=True,
-                      desc="dynamic PageRank, R-MAT scale-24 (16,777,216 V, 268,435,456 E), 1% batches"),
+                      desc="dynamic PageRank, R-MAT scale-24 (16,777,216 V, 268,435,456 E), 1% batches",
+                      ref_sample=dict(scale=22, edges=1 << 26,
+                                      desc="dynamic PageRank, R-MAT scale-22 sample (4.2M V, 67M E), 1% batches")),
     "sssp-rmat24": dict(algo="sssp", graph="rmat", scale=24, edges=1 << 28, percent=1.0, weighted=True,
                         directed=True,
-                        desc="dynamic SSSP, R-MAT scale-24 (16,777,216 V, 268,435,456 E, w 1-100), 1% batches"),
+                        desc="dynamic SSSP, R-MAT scale-24 (16,777,216 V, 268,435,456 E, w 1-100), 1% batches",
+                        ref_sample=dict(scale=22, edges=1 << 26,
+                                        desc="dynamic SSSP, R-MAT scale-22 sample (4.2M V, 67M E), 1% batches")),
     "tc-rmat24": dict(algo="tc", graph="rmat", scale=24, edges=1 << 28, percent=1.0, weighted=False,
                       directed=False,
-                      desc="dynamic TC, undirected R-MAT scale-24 (16,777,216 V, 268,435,456 edges), 1% batches"),
+                      desc="dynamic TC, undirected R-MAT scale-24 (16,777,216 V, 268,435,456 edges), 1% batches",
+                      ref_sample=dict(scale=16, edges=1 << 20,
+                                      desc="dynamic TC, undirected R-MAT scale-16 sample (65K V, 1M edges), 1% batches")),
     # BASELINE configs[4] (C5) on one GPU: R-MAT scale-26, 2^30 edges.  The
     # reference arm cannot run it in bounded time (its per-batch cost grows
     # with E and the store alone needs ~50 GB of host RAM), so it times the
@@ -75,8 +85,8 @@ WORKLOADS = {
                                     desc="dynamic SSSP, R-MAT scale-22 sample (4.2M V, 67M E), 1% batches")),
     "tc-c5": dict(algo="tc", graph="rmat", scale=26, edges=1 << 30, percent=1.0, weighted=False, directed=False,
                   desc="dynamic TC, undirected R-MAT scale-26 (67,108,864 V, 1,073,741,824 edges), 1% batches",
-                  ref_sample=dict(scale=20, edges=1 << 24,
-                                  desc="dynamic TC, undirected R-MAT scale-20 sample (1M V, 16.8M edges), 1% batches")),
+                  ref_sample=dict(scale=16, edges=1 << 20,
+                                  desc="dynamic TC, undirected R-MAT scale-16 sample (65K V, 1M edges), 1% batches")),
     # The reference's fixedPoint sweeps all V per round and needs ~rows+cols
     # rounds, so its CPU time grows ~side^3: its arm runs a 600x600 sample
     # of the same family (per-record rate overstates the full-size reference).
@@ -244,6 +254,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--percent", type=float, default=None, help="override the workload's batch percentage")
+    ap.add_argument("--force-dist", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--static", action="store_true",
                     help="also time the static alternative per batch: apply the batch, merge, recompute from scratch "
                          "(staticSSSP / staticPR / staticTC), on up to 3 batches")
@@ -283,7 +294,9 @@ def main():
 
     import torch
 
-    dist_on = world > 1
+    # --force-dist: take the N>1 code path (process group, NCCL communicator,
+    # sharded PR / TC) at world size 1, to exercise it on a single GPU
+    dist_on = world > 1 or args.force_dist
     torch.cuda.set_device(local)
     if dist_on:
         import torch.distributed as dist
@@ -514,7 +527,7 @@ def _static_compare(gd, torch, wl, args, local, n, s, d, w, kind, us, ud, uw, pe
             "what": "apply batch + merge + static recompute from scratch (the reference bench's static column)"}
 
 
-KERNELS = ("pr_pull", "pr_contrib", "merge_copy", "flood_sample", "flood_rest", "flood_mark", "del_scan",
+KERNELS = ("pr_pull", "pr_contrib", "tc_bitmap", "merge_copy", "flood_sample", "flood_rest", "flood_mark", "del_scan",
            "add_vacancies", "tc_count", "sssp_relax", "sssp_walk", "sssp_pull", "sssp_parent")
 
 def _graph_stream(g):

@@ -268,8 +268,8 @@ __global__ void k_pr_onupdate(const int32_t* ds, const int32_t* dd, int64_t kdel
          i += (int64_t)gridDim.x * blockDim.x) {
         const bool del = i < kdel;
         const int32_t s = del ? ds[i] : as[i - kdel], d = del ? dd[i] : ad[i - kdel];
-        if (!affected[s]) affected[s] = 1;  // hubs recur: skip the redundant stores
-        if (!affected[d]) affected[d] = 1;
+        affected[s] = 1;
+        affected[d] = 1;
         atomicAdd(&outdeg[s], del ? -1 : 1);
     }
 }

@@ -268,8 +268,8 @@ int64_t TC::count_records(const int32_t* s, const int32_t* d, int64_t k) {
         const int64_t* nhub = cnt2.get() + 1;
         if (hmax > 0) {
             GD_KERNEL(k_tc_hub_slots, grid_for(hmax, 256), 256, 0, st, hubs.get(), nhub, hmax, hub_slot.get());
-            GD_KERNEL(k_tc_bitmaps, 148 * 4, 256, 0, st, hubs.get(), nhub, hmax, ix.view(), words, bm.get(),
-                      bm_multi.get(), false);
+            GD_KERNEL_T("tc_bitmap", 0, k_tc_bitmaps, 148 * 4, 256, 0, st, hubs.get(), nhub, hmax, ix.view(), words,
+                        bm.get(), bm_multi.get(), false);
         }
         int pi = prof_begin("tc_count", 0, st);
         k_tc_count<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((nwork + 7) / 8, 148 * 16)), kThreads, 0,
@@ -280,8 +280,8 @@ int64_t TC::count_records(const int32_t* s, const int32_t* d, int64_t k) {
         GD_LAUNCH_CHECK();
         prof_end(pi, st);
         if (hmax > 0)
-            GD_KERNEL(k_tc_bitmaps, 148 * 4, 256, 0, st, hubs.get(), nhub, hmax, ix.view(), words, bm.get(),
-                      bm_multi.get(), true);
+            GD_KERNEL_T("tc_bitmap", 0, k_tc_bitmaps, 148 * 4, 256, 0, st, hubs.get(), nhub, hmax, ix.view(), words,
+                        bm.get(), bm_multi.get(), true);
         if (nhubs > 0)
             GD_KERNEL(k_tc_reset, grid_for(nhubs, 256), 256, 0, st, hubs.get(), nhub, hubmark.get(), hub_slot.get());
         if (pi >= 0) count_rec.push_back(pi);
