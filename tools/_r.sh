@@ -1,5 +1,7 @@
-timeout 900 python -m pytest tests -m gpu -x -q --timeout 300 -p no:cacheprovider -k "tc or TC or smoke or golden or comm" 2>&1 | tail -1
-for p in 1 10; do timeout 900 python bench.py --workload tc-rmat24 --percent $p --steps 3 --warmup 2 --e2e-steps 2 --no-cpu-baseline > gpurun_out/t.json 2> gpurun_out/t.err; python -c "
-import json; j=json.load(open('gpurun_out/t.json')); print('tc24 $p%', j['ms_per_step'], {k: round(v['ms_total']/j['steps'],2) for k,v in j['kernels'].items()})"; done
-timeout 900 python bench.py --workload tc --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/t.json 2> gpurun_out/t.err; python -c "
-import json; j=json.load(open('gpurun_out/t.json')); print('C3', j['ms_per_step'], {k: round(v['ms_total']/j['steps'],2) for k,v in j['kernels'].items()})"
+free -g | head -2
+timeout 1500 python bench.py --workload pr-c5 --steps 3 --warmup 2 --e2e-steps 2 --no-cpu-baseline > gpurun_out/c5pr.json 2> gpurun_out/c5pr.err; echo "pr-c5 rc=$?"; tail -4 gpurun_out/c5pr.err
+python -c "
+import json; j=json.load(open('gpurun_out/c5pr.json')); print(j['ms_per_step'], j['value'], j['e2e']['ms_per_step'], j['roofline']['kernel'], j['roofline']['frac'], {k: round(v['ms_total']/j['steps'],2) for k,v in j['kernels'].items()})"
+timeout 1500 python bench.py --workload sssp-c5 --steps 3 --warmup 2 --e2e-steps 2 --no-cpu-baseline > gpurun_out/c5sssp.json 2> gpurun_out/c5sssp.err; echo "sssp-c5 rc=$?"; tail -4 gpurun_out/c5sssp.err
+python -c "
+import json; j=json.load(open('gpurun_out/c5sssp.json')); print(j['ms_per_step'], j['value'], j['e2e']['ms_per_step'], j['roofline']['kernel'], {k: round(v['ms_total']/j['steps'],2) for k,v in j['kernels'].items()})"
