@@ -306,7 +306,10 @@ def main():
 
     e2e_steps = args.e2e_steps if args.e2e_steps is not None else max(1, min(args.steps, 10))
     nb = args.warmup + args.steps + 1 + e2e_steps  # +1: the untimed e2e warm-up step
-    n, s, d, w, kind, us, ud, uw, per = make_inputs(wl, nb, seed=22 + 1000 * rank)
+    # sharded PR / TC: every rank holds a replica of ONE job's store, so all
+    # ranks build the same graph and stream; SSSP replicas each get their own
+    one_job = dist_on and wl["algo"] in ("pr", "tc")
+    n, s, d, w, kind, us, ud, uw, per = make_inputs(wl, nb, seed=22 if one_job else 22 + 1000 * rank)
     records_per_step = per
 
     t = time.time()
