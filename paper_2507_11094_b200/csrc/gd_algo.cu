@@ -325,6 +325,14 @@ __global__ void k_aff_giant(const int32_t* probe, int m, int32_t* giant) {
 __global__ void k_aff_rest(OutView ov, IdxView in, int64_t n, const int32_t* giant_p, int32_t* p) {
     const int32_t giant = *giant_p;
     for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+        // the root test and the arc counts load together; isolated vertices
+        // (42% of R-MAT V) and sampled-only ones stop here
+        const int32_t pv = p[v];
+        const int64_t b0 = ov.off[0][v], e0 = ov.off[0][v + 1];
+        const int64_t ia = in.off ? in.off[v] : 0, ib = in.off ? in.off[v + 1] : 0;
+        int64_t more = (e0 - b0 > kSample ? 1 : 0) + (ib - ia);
+        for (int sg = 1; sg < ov.nseg; ++sg) more += ov.off[sg][v + 1] - ov.off[sg][v];
+        if (more == 0 || pv == giant) continue;
         if (uf_find(p, (int32_t)v) == giant) continue;
         for (int sg = 0; sg < ov.nseg; ++sg) {
             const int64_t* off = ov.off[sg];
