@@ -23,7 +23,7 @@ __global__ void k_stage_host(const uint8_t* kind, const int64_t* s64, const int6
         if (kd == 'a' && (wt < INT32_MIN || wt > INT32_MAX)) e |= kBadWeight;
         if (e) {
             atomicOr(err, e);
-            atomicMin(bad_index, (unsigned long long)i);
+            atomicMax(bad_index, ~(unsigned long long)i);  // the first bad record, zero-initialised
         }
         s[i] = (int32_t)a;
         d[i] = (int32_t)b;
@@ -42,7 +42,7 @@ __global__ void k_stage_dev(const uint8_t* kind, const int32_t* s, const int32_t
         if (s[i] < 0 || s[i] >= n || d[i] < 0 || d[i] >= n) e |= kBadNode;
         if (e) {
             atomicOr(err, e);
-            atomicMin(bad_index, (unsigned long long)i);
+            atomicMax(bad_index, ~(unsigned long long)i);  // the first bad record, zero-initialised
         }
         isdel[i] = kd == 'd';
         isadd[i] = kd == 'a';
@@ -148,8 +148,7 @@ void AlgoBase::stage_host(DevBatch& b, const uint8_t* kind, const int64_t* src, 
     DBuf<int32_t> s(k, st), d(k, st), ww(k, st);
     DBuf<uint8_t> flags(2 * k, st);
     DBuf<int64_t> hdr(4, st);  // err, bad index, kdel, kadd
-    GD_CUDA(cudaMemsetAsync(hdr.get(), 0, 8, st));
-    GD_CUDA(cudaMemsetAsync(hdr.get() + 1, 0xff, 8, st));
+    GD_CUDA(cudaMemsetAsync(hdr.get(), 0, 16, st));
     GD_KERNEL(k_stage_host, grid_for(k, 256), 256, 0, st, k_stage.get(), h_stage.get(), h_stage.get() + k,
               w ? h_stage.get() + 2 * k : nullptr, k, g->n, s.get(), d.get(), ww.get(), flags.get(),
               flags.get() + k, reinterpret_cast<int*>(hdr.get()),
@@ -161,7 +160,7 @@ void AlgoBase::stage_host(DevBatch& b, const uint8_t* kind, const int64_t* src, 
     read_small(st, h, hdr.get(), sizeof h);
     int e = (int)(h[0] & 0xffffffff);
     if (e) {
-        unsigned long long i = (unsigned long long)h[1];
+        unsigned long long i = ~(unsigned long long)h[1];
         raise_validation(e, i, g->n, (char)kind[i], src[i], dst[i]);
     }
     split(b, sel_del.get(), sel_add.get(), s.get(), d.get(), ww.get(), h[2], h[3]);
@@ -176,8 +175,7 @@ void AlgoBase::stage_device(DevBatch& b, const uint8_t* kind, const int32_t* src
     }
     DBuf<uint8_t> flags(2 * k, st);
     DBuf<int64_t> hdr(4, st);  // err, bad index, kdel, kadd
-    GD_CUDA(cudaMemsetAsync(hdr.get(), 0, 8, st));
-    GD_CUDA(cudaMemsetAsync(hdr.get() + 1, 0xff, 8, st));
+    GD_CUDA(cudaMemsetAsync(hdr.get(), 0, 16, st));
     GD_KERNEL(k_stage_dev, grid_for(k, 256), 256, 0, st, kind, src, dst, k, g->n, flags.get(), flags.get() + k,
               reinterpret_cast<int*>(hdr.get()), reinterpret_cast<unsigned long long*>(hdr.get() + 1));
     DBuf<int32_t> sel_del(k, st), sel_add(k, st);
@@ -187,7 +185,7 @@ void AlgoBase::stage_device(DevBatch& b, const uint8_t* kind, const int32_t* src
     read_small(st, h, hdr.get(), sizeof h);
     int e = (int)(h[0] & 0xffffffff);
     if (e) {
-        unsigned long long i = (unsigned long long)h[1];
+        unsigned long long i = ~(unsigned long long)h[1];
         raise_validation(e, i, g->n, (char)read_scalar(st, kind + i), read_scalar(st, src + i),
                          read_scalar(st, dst + i));
     }
@@ -262,9 +260,11 @@ __device__ inline void uf_union(int32_t* p, int32_t a, int32_t b) {
     }
 }
 
-__global__ void k_uf_init(int32_t* p, int64_t n) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+__global__ void k_uf_init(int32_t* p, int64_t n, uint8_t* root_has_seed) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         p[i] = (int32_t)i;
+        root_has_seed[i] = 0;
+    }
 }
 
 // Afforest-style connectivity (Sutton et al. 2018): link every vertex to its
@@ -382,10 +382,9 @@ int64_t flood_weak_components(Store& g, uint8_t* flags, KernelProf* prof) {
         in = g.rev.view();
     }
     DBuf<int32_t> p(n, s);
-    DBuf<uint8_t> seed(n, s);
-    seed.zero(s);
+    DBuf<uint8_t> seed(n, s);  // zeroed by k_uf_init
     OutView ov = g.out_view();
-    GD_KERNEL(k_uf_init, grid_for(n, 256), 256, 0, s, p.get(), n);
+    GD_KERNEL(k_uf_init, grid_for(n, 256), 256, 0, s, p.get(), n, seed.get());
     GD_KERNEL_T("flood_sample", n * (8 + 4 * kSample), k_aff_sample, grid_for(n, 256), 256, 0, s, ov, n, p.get());
     GD_KERNEL(k_uf_compress, grid_for(n, 256), 256, 0, s, p.get(), n);
     constexpr int kProbe = 256;  // the giant component holds ~all non-isolated vertices

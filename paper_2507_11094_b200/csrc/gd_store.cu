@@ -160,10 +160,14 @@ constexpr int kScanWarps = 8;
 constexpr int kBitmapWords = 1024;  // 32 Kbit per warp (a filter: hits are confirmed by binary search)
 
 __global__ void k_row_chunks(OutView ov, const uint64_t* rq_key, const int32_t* row_first, const int64_t* d_nrows,
-                             int sh, int64_t* chunks, unsigned long long* maxlen) {
+                             int64_t cap, int sh, int64_t* chunks, unsigned long long* maxlen) {
     unsigned long long mx = 0;
     const int64_t nrows = *d_nrows;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nrows; i += (int64_t)gridDim.x * blockDim.x) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cap; i += (int64_t)gridDim.x * blockDim.x) {
+        if (i >= nrows) {  // the tail of the scan input (no separate memset)
+            chunks[i] = 0;
+            continue;
+        }
         int32_t row = key_row(rq_key[row_first[i]], sh);
         int64_t len = 0;
         for (int sg = 0; sg < ov.nseg; ++sg) len += ov.off[sg][row + 1] - ov.off[sg][row];
@@ -363,9 +367,11 @@ __global__ void __launch_bounds__(kScanWarps * 32, 4) k_del_scan_tail(OutView ov
     }
 }
 
-__global__ void k_single_flags(const uint64_t* key, int64_t m, uint8_t* single) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+__global__ void k_single_flags(const uint64_t* key, int64_t m, uint8_t* single, unsigned long long* sel) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
         single[i] = (i == 0 || key[i - 1] != key[i]) && (i + 1 == m || key[i + 1] != key[i]);
+        sel[i] = ~0ULL;  // atomicMin target of the single-request pairs
+    }
 }
 
 // (pair << rb | chain offset): one radix key for the (pair, chain) order
@@ -762,16 +768,17 @@ void edit_merge(cudaStream_t s, int64_t n, const int64_t* off, int32_t* col, con
                 DBuf<int32_t>& new_col, DBuf<int32_t>& new_w, int64_t& new_nnz, bool weighted) {
     const int64_t ntiles = (nnz + kTile - 1) / kTile;
     const int64_t nwin = (nnz + kWin - 1) / kWin;
-    DBuf<int64_t> shift_cnt(n + 1, s), dead_cnt(nwin + 1, s);
-    shift_cnt.zero(s);
-    dead_cnt.zero(s);
+    DBuf<int64_t> counts(n + 1 + nwin + 1, s);  // per-row shifts, then per-window deaths: one memset
+    counts.zero(s);
+    int64_t* shift_cnt_p = counts.get();
+    int64_t* dead_cnt_p = counts.get() + n + 1;
     if (ntomb)
         GD_KERNEL(k_tomb_hist, grid_for(ntomb, 256), 256, 0, s, tpos, trow, ntomb, col, nnz, dedupe,
-                  reinterpret_cast<unsigned long long*>(dead_cnt.get()), shift_cnt.get());
-    if (nins) GD_KERNEL(k_ins_hist, grid_for(nins, 256), 256, 0, s, irow, nins, shift_cnt.get());
+                  reinterpret_cast<unsigned long long*>(dead_cnt_p), shift_cnt_p);
+    if (nins) GD_KERNEL(k_ins_hist, grid_for(nins, 256), 256, 0, s, irow, nins, shift_cnt_p);
     DBuf<int64_t> shift(n + 1, s), dead_win(nwin + 1, s);
-    exclusive_scan_i64(s, shift_cnt.get(), shift.get(), n + 1);
-    exclusive_scan_i64(s, dead_cnt.get(), dead_win.get(), nwin + 1);
+    exclusive_scan_i64(s, shift_cnt_p, shift.get(), n + 1);
+    exclusive_scan_i64(s, dead_cnt_p, dead_win.get(), nwin + 1);
     int64_t dead_total = read_scalar(s, dead_win.get() + nwin);  // sizes the new arrays
     new_nnz = nnz - dead_total + nins;
     new_off.alloc(n + 1, s);
@@ -1099,17 +1106,14 @@ int64_t Store::apply_deletes(const int32_t* d_src, const int32_t* d_dst, int64_t
     GD_KERNEL(k_row_starts, grid_for(nrq, 256), 256, 0, s, rq_key.get(), nrq, sh, rflag.get());
     DBuf<int32_t> row_first(nrq, s);
     DBuf<int64_t> hdr(4, s);  // nrows, work items, longest chain, overflow matches
+    GD_CUDA(cudaMemsetAsync(hdr.get(), 0, 4 * sizeof(int64_t), s));
     select_flagged_index_async(s, rflag.get(), nrq, row_first.get(), hdr.get());
     OutView ov = out_view();
     DBuf<int64_t> chunks(nrq + 1, s), coff(nrq + 1, s);
-    DBuf<unsigned long long> maxlen(1, s);
-    maxlen.zero(s);
-    chunks.zero(s);
-    GD_KERNEL(k_row_chunks, grid_for(nrq, 256), 256, 0, s, ov, rq_key.get(), row_first.get(), hdr.get(), sh,
-              chunks.get(), maxlen.get());
+    GD_KERNEL(k_row_chunks, grid_for(nrq + 1, 256), 256, 0, s, ov, rq_key.get(), row_first.get(), hdr.get(), nrq + 1,
+              sh, chunks.get(), reinterpret_cast<unsigned long long*>(hdr.get() + 2));
     exclusive_scan_i64(s, chunks.get(), coff.get(), nrq + 1);
     GD_CUDA(cudaMemcpyAsync(hdr.get() + 1, coff.get() + nrq, 8, cudaMemcpyDeviceToDevice, s));
-    GD_CUDA(cudaMemcpyAsync(hdr.get() + 2, maxlen.get(), 8, cudaMemcpyDeviceToDevice, s));
     // tail pieces: at most one per kChunk slots of the requested rows
     DBuf<int32_t> wrow(total_slots() / kChunk + nrq + 1, s);
     GD_KERNEL(k_chunk_rows, grid_for(nrq, 256), 256, 0, s, coff.get(), hdr.get(), wrow.get());
@@ -1118,9 +1122,8 @@ int64_t Store::apply_deletes(const int32_t* d_src, const int32_t* d_dst, int64_t
     // counts stay on the device: the one read-back is the overflow size
     // together with the longest chain.
     DBuf<uint8_t> single(nrq, s);
-    GD_KERNEL(k_single_flags, grid_for(nrq, 256), 256, 0, s, rq_key.get(), nrq, single.get());
     DBuf<unsigned long long> sel(nrq, s);
-    GD_CUDA(cudaMemsetAsync(sel.get(), 0xff, nrq * 8, s));
+    GD_KERNEL(k_single_flags, grid_for(nrq, 256), 256, 0, s, rq_key.get(), nrq, single.get(), sel.get());
     int64_t cap = 1024;
     DBuf<uint64_t> m_key;
     DBuf<int64_t> m_chain;
@@ -1130,8 +1133,10 @@ int64_t Store::apply_deletes(const int32_t* d_src, const int32_t* d_dst, int64_t
         m_key.alloc(cap, s);
         m_chain.alloc(cap, s);
         m_gid.alloc(cap, s);
-        GD_CUDA(cudaMemsetAsync(hdr.get() + 3, 0, 8, s));
-        if (attempt) GD_CUDA(cudaMemsetAsync(sel.get(), 0xff, nrq * 8, s));
+        if (attempt) {  // overflow retry: start the match collection over
+            GD_CUDA(cudaMemsetAsync(hdr.get() + 3, 0, 8, s));
+            GD_CUDA(cudaMemsetAsync(sel.get(), 0xff, nrq * 8, s));
+        }
         MatchOut mo{sel.get(), single.get(), m_key.get(), m_chain.get(), m_gid.get(),
                     reinterpret_cast<unsigned long long*>(hdr.get() + 3), cap};
         GD_KERNEL_T("del_scan", 0, k_del_scan_head, grid_for(((nrq + 3) / 4) * 32, 256, 148LL * 32), 256, 0, s, ov,
@@ -1172,7 +1177,7 @@ int64_t Store::apply_deletes(const int32_t* d_src, const int32_t* d_dst, int64_t
         found_local.alloc(k, s);
         found = found_local.get();
     }
-    GD_CUDA(cudaMemsetAsync(found, 0, k, s));
+    // every record's forward request writes its found flag (k_del_resolve): no memset
     // [0] applied records of this call, [1] killed slots since `live` was last
     // brought up to date (read lazily: live_count())
     GD_CUDA(cudaMemsetAsync(dcounts.get(), 0, sizeof(unsigned long long), s));
