@@ -762,46 +762,64 @@ __global__ void k_gather_sel(const T* in, const int32_t* sel, int64_t m, T* out)
 
 // ==========================================================================
 
+// Two-phase edit merge: plan() builds the per-row shifts and per-window
+// death counts (device only), apply() sizes and writes the merged arrays once
+// the host knows the death total.  Store::merge plans the out-store and the
+// in-index first and reads both totals with ONE read-back.
+void edit_plan(cudaStream_t s, EditJob& j) {
+    j.nwin = (j.nnz + kWin - 1) / kWin;
+    j.counts.alloc(j.n + 1 + j.nwin + 1, s);  // per-row shifts, then per-window deaths: one memset
+    j.counts.zero(s);
+    int64_t* shift_cnt = j.counts.get();
+    int64_t* dead_cnt = j.counts.get() + j.n + 1;
+    if (j.ntomb)
+        GD_KERNEL(k_tomb_hist, grid_for(j.ntomb, 256), 256, 0, s, j.tpos, j.trow, j.ntomb, j.col, j.nnz, j.dedupe,
+                  reinterpret_cast<unsigned long long*>(dead_cnt), shift_cnt);
+    if (j.nins) GD_KERNEL(k_ins_hist, grid_for(j.nins, 256), 256, 0, s, j.irow, j.nins, shift_cnt);
+    j.shift.alloc(j.n + 1, s);
+    j.dead_win.alloc(j.nwin + 1, s);
+    exclusive_scan_i64(s, shift_cnt, j.shift.get(), j.n + 1);
+    exclusive_scan_i64(s, dead_cnt, j.dead_win.get(), j.nwin + 1);
+}
+
+void edit_apply(cudaStream_t s, EditJob& j, int64_t dead_total, DBuf<int64_t>& new_off, DBuf<int32_t>& new_col,
+                DBuf<int32_t>& new_w, int64_t& new_nnz) {
+    const int64_t n = j.n, nnz = j.nnz, nwin = j.nwin, nins = j.nins;
+    const int64_t ntiles = (nnz + kTile - 1) / kTile;
+    new_nnz = nnz - dead_total + nins;
+    new_off.alloc(n + 1, s);
+    GD_KERNEL(k_add_offsets, grid_for(n + 1, 256), 256, 0, s, j.off, j.shift.get(), n + 1, new_off.get());
+    new_col.alloc(new_nnz, s);
+    if (j.weighted) new_w.alloc(new_nnz, s);
+    else new_w.release();
+    if (ntiles) {
+        DBuf<int64_t> pj(nwin + 1, s);
+        GD_KERNEL(k_win_ins, grid_for(nwin + 1, 256), 256, 0, s, nwin, j.ipos, nins, pj.get());
+        unsigned g = (unsigned)std::min<int64_t>(ntiles, 148LL * 64);
+        // algorithmic bytes: every base entry read once, every surviving entry written once
+        if (j.weighted)
+            GD_KERNEL_T("merge_copy", (nnz + (nnz - dead_total)) * 8, k_edit_base<true>, g, kEditThreads, 0, s, j.col,
+                        j.w, nnz, j.dead_win.get(), j.ipos, pj.get(), j.icol, j.iw, nwin, new_col.get(), new_w.get());
+        else
+            GD_KERNEL_T("merge_copy", (nnz + (nnz - dead_total)) * 4, k_edit_base<false>, g, kEditThreads, 0, s,
+                        j.col, nullptr, nnz, j.dead_win.get(), j.ipos, pj.get(), j.icol, nullptr, nwin, new_col.get(),
+                        nullptr);
+    }
+    if (nins)
+        GD_KERNEL(k_edit_tail, grid_for(nins, 256), 256, 0, s, j.ipos, nins, nnz, j.dead_win.get() + nwin, j.icol,
+                  j.iw, new_col.get(), j.weighted ? new_w.get() : nullptr);
+    j.counts.release();
+    j.shift.release();
+}
+
 void edit_merge(cudaStream_t s, int64_t n, const int64_t* off, int32_t* col, const int32_t* w, int64_t nnz,
                 const int64_t* tpos, const int32_t* trow, int64_t ntomb, bool dedupe, const int32_t* irow,
                 const int32_t* icol, const int32_t* iw, const int64_t* ipos, int64_t nins, DBuf<int64_t>& new_off,
                 DBuf<int32_t>& new_col, DBuf<int32_t>& new_w, int64_t& new_nnz, bool weighted) {
-    const int64_t ntiles = (nnz + kTile - 1) / kTile;
-    const int64_t nwin = (nnz + kWin - 1) / kWin;
-    DBuf<int64_t> counts(n + 1 + nwin + 1, s);  // per-row shifts, then per-window deaths: one memset
-    counts.zero(s);
-    int64_t* shift_cnt_p = counts.get();
-    int64_t* dead_cnt_p = counts.get() + n + 1;
-    if (ntomb)
-        GD_KERNEL(k_tomb_hist, grid_for(ntomb, 256), 256, 0, s, tpos, trow, ntomb, col, nnz, dedupe,
-                  reinterpret_cast<unsigned long long*>(dead_cnt_p), shift_cnt_p);
-    if (nins) GD_KERNEL(k_ins_hist, grid_for(nins, 256), 256, 0, s, irow, nins, shift_cnt_p);
-    DBuf<int64_t> shift(n + 1, s), dead_win(nwin + 1, s);
-    exclusive_scan_i64(s, shift_cnt_p, shift.get(), n + 1);
-    exclusive_scan_i64(s, dead_cnt_p, dead_win.get(), nwin + 1);
-    int64_t dead_total = read_scalar(s, dead_win.get() + nwin);  // sizes the new arrays
-    new_nnz = nnz - dead_total + nins;
-    new_off.alloc(n + 1, s);
-    GD_KERNEL(k_add_offsets, grid_for(n + 1, 256), 256, 0, s, off, shift.get(), n + 1, new_off.get());
-    new_col.alloc(new_nnz, s);
-    if (weighted) new_w.alloc(new_nnz, s);
-    else new_w.release();
-    if (ntiles) {
-        DBuf<int64_t> pj(nwin + 1, s);
-        GD_KERNEL(k_win_ins, grid_for(nwin + 1, 256), 256, 0, s, nwin, ipos, nins, pj.get());
-        unsigned g = (unsigned)std::min<int64_t>(ntiles, 148LL * 64);
-        // algorithmic bytes: every base entry read once, every surviving entry written once
-        if (weighted)
-            GD_KERNEL_T("merge_copy", (nnz + (nnz - dead_total)) * 8, k_edit_base<true>, g, kEditThreads, 0, s, col,
-                        w, nnz, dead_win.get(), ipos, pj.get(), icol, iw, nwin, new_col.get(), new_w.get());
-        else
-            GD_KERNEL_T("merge_copy", (nnz + (nnz - dead_total)) * 4, k_edit_base<false>, g, kEditThreads, 0, s,
-                        col, nullptr, nnz, dead_win.get(), ipos, pj.get(), icol, nullptr, nwin, new_col.get(),
-                        nullptr);
-    }
-    if (nins)
-        GD_KERNEL(k_edit_tail, grid_for(nins, 256), 256, 0, s, ipos, nins, nnz, dead_win.get() + nwin, icol, iw,
-                  new_col.get(), weighted ? new_w.get() : nullptr);
+    EditJob j{n, off, col, w, nnz, tpos, trow, ntomb, dedupe, irow, icol, iw, ipos, nins, weighted};
+    edit_plan(s, j);
+    int64_t dead_total = read_scalar(s, j.dead_win.get() + j.nwin);  // sizes the new arrays
+    edit_apply(s, j, dead_total, new_off, new_col, new_w, new_nnz);
 }
 
 // ==========================================================================
@@ -989,19 +1007,24 @@ void Store::require_fwd() {
 }
 
 // Fold tombstones and the delta into a clean index.
-void Store::compact_index(SortedIndex& ix) {
-    if (!ix.built || !ix.dirty()) return;
+// index compaction as a plan (k_index_ins_pos + histograms) and a finish
+void Store::index_plan(SortedIndex& ix, EditJob& j, DBuf<int64_t>& ipos) {
     cudaStream_t s = stream;
-    DBuf<int64_t> ipos(ix.dnnz, s);
+    ipos.alloc(ix.dnnz, s);
     if (ix.dnnz)
         GD_KERNEL(k_index_ins_pos, grid_for(ix.dnnz, 256), 256, 0, s, ix.drow.get(), ix.dcol.get(), ix.dnnz,
                   ix.off.get(), ix.col.get(), ipos.get());
+    j = EditJob{n, ix.off.get(), ix.col.get(), ix.w.n ? ix.w.get() : nullptr, ix.nnz, ix.tpos.get(), ix.trow.get(),
+                ix.ntomb, false, ix.drow.get(), ix.dcol.get(), ix.dw.n ? ix.dw.get() : nullptr, ipos.get(), ix.dnnz,
+                weighted};
+    edit_plan(s, j);
+}
+
+void Store::index_finish(SortedIndex& ix, EditJob& j, int64_t dead_total) {
     DBuf<int64_t> noff;
     DBuf<int32_t> ncol, nw;
     int64_t nnz2 = 0;
-    edit_merge(s, n, ix.off.get(), ix.col.get(), ix.w.n ? ix.w.get() : nullptr, ix.nnz, ix.tpos.get(),
-               ix.trow.get(), ix.ntomb, false, ix.drow.get(), ix.dcol.get(), ix.dw.n ? ix.dw.get() : nullptr,
-               ipos.get(), ix.dnnz, noff, ncol, nw, nnz2, weighted);
+    edit_apply(stream, j, dead_total, noff, ncol, nw, nnz2);
     ix.off = std::move(noff);
     ix.col = std::move(ncol);
     ix.w = std::move(nw);
@@ -1013,6 +1036,14 @@ void Store::compact_index(SortedIndex& ix) {
     ix.drow.release();
     ix.dcol.release();
     ix.dw.release();
+}
+
+void Store::compact_index(SortedIndex& ix) {
+    if (!ix.built || !ix.dirty()) return;
+    EditJob j;
+    DBuf<int64_t> ipos;
+    index_plan(ix, j, ipos);
+    index_finish(ix, j, read_scalar(stream, j.dead_win.get() + j.nwin));
 }
 
 void Store::index_delete(SortedIndex& ix, const KilledArcs& ka) {
@@ -1307,11 +1338,26 @@ void Store::merge() {
     }
     DBuf<int64_t> ipos(nins, s);
     if (nins) GD_KERNEL(k_out_ins_pos, grid_for(nins, 256), 256, 0, s, irow.get(), nins, segs[0].off.get(), ipos.get());
+    // plan the out-store merge and the in-index compaction, then ONE read-back
+    // of both death totals sizes both outputs
+    EditJob jo{n, segs[0].off.get(), segs[0].col.get(), weighted ? segs[0].w.get() : nullptr, segs[0].nslots,
+               otpos.get(), otrow.get(), notomb, true, irow.get(), icol.get(), weighted ? iw.get() : nullptr,
+               ipos.get(), nins, weighted};
+    edit_plan(s, jo);
+    const bool rev_dirty = rev.built && rev.dirty();
+    EditJob jr;
+    DBuf<int64_t> rpos;
+    if (rev_dirty) index_plan(rev, jr, rpos);
+    DBuf<int64_t> totals(2, s);
+    GD_CUDA(cudaMemcpyAsync(totals.get(), jo.dead_win.get() + jo.nwin, 8, cudaMemcpyDeviceToDevice, s));
+    if (rev_dirty)
+        GD_CUDA(cudaMemcpyAsync(totals.get() + 1, jr.dead_win.get() + jr.nwin, 8, cudaMemcpyDeviceToDevice, s));
+    int64_t ht[2] = {0, 0};
+    read_small(s, ht, totals.get(), rev_dirty ? 16 : 8);
     OutSeg nb;
     int64_t nnz2 = 0;
-    edit_merge(s, n, segs[0].off.get(), segs[0].col.get(), weighted ? segs[0].w.get() : nullptr, segs[0].nslots,
-               otpos.get(), otrow.get(), notomb, true, irow.get(), icol.get(), weighted ? iw.get() : nullptr,
-               ipos.get(), nins, nb.off, nb.col, nb.w, nnz2, weighted);
+    edit_apply(s, jo, ht[0], nb.off, nb.col, nb.w, nnz2);
+    if (rev_dirty) index_finish(rev, jr, ht[1]);
     nb.nslots = nnz2;
     segs.clear();
     segs.push_back(std::move(nb));

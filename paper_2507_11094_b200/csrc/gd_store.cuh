@@ -33,6 +33,8 @@ struct OutSeg {
 };
 
 // Device-side read views, passed by value to kernels.
+struct EditJob;  // gd_store.cu: a two-phase edit merge
+
 struct OutView {
     int nseg;
     const int64_t* const* off;  // device table of nseg pointers
@@ -97,6 +99,8 @@ class Store {
     void require_rev();  // build the rev index if absent
     void require_fwd();  // directed TC: sorted out-index
     void compact_rev() { compact_index(rev); }
+    void index_plan(SortedIndex& ix, EditJob& j, DBuf<int64_t>& ipos);
+    void index_finish(SortedIndex& ix, EditJob& j, int64_t dead_total);
     void compact_fwd() { compact_index(fwd); }
     SortedIndex& tc_index() { return directed ? fwd : rev; }
     void compact_index(SortedIndex& ix);
@@ -145,6 +149,29 @@ class Store {
 // sorted items before base positions P (stable), rows re-offset.
 // Dead entries are the negative ones, found via an unordered tomb log
 // (dedupe: the out-store may log a slot twice).
+// an edit merge split in two (see gd_store.cu): inputs, then the plan's buffers
+struct EditJob {
+    int64_t n = 0;
+    const int64_t* off = nullptr;
+    int32_t* col = nullptr;
+    const int32_t* w = nullptr;
+    int64_t nnz = 0;
+    const int64_t* tpos = nullptr;
+    const int32_t* trow = nullptr;
+    int64_t ntomb = 0;
+    bool dedupe = false;
+    const int32_t* irow = nullptr;
+    const int32_t* icol = nullptr;
+    const int32_t* iw = nullptr;
+    const int64_t* ipos = nullptr;
+    int64_t nins = 0;
+    bool weighted = false;
+    int64_t nwin = 0;
+    DBuf<int64_t> counts, shift, dead_win;
+};
+void edit_plan(cudaStream_t s, EditJob& j);
+void edit_apply(cudaStream_t s, EditJob& j, int64_t dead_total, DBuf<int64_t>& new_off, DBuf<int32_t>& new_col,
+                DBuf<int32_t>& new_w, int64_t& new_nnz);
 void edit_merge(cudaStream_t s, int64_t n, const int64_t* off, int32_t* col, const int32_t* w, int64_t nnz,
                 const int64_t* tpos, const int32_t* trow, int64_t ntomb, bool dedupe, const int32_t* irow,
                 const int32_t* icol, const int32_t* iw, const int64_t* ipos, int64_t nins, DBuf<int64_t>& new_off,
