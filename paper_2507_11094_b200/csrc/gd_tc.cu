@@ -100,6 +100,18 @@ __global__ void k_tc_prep(const int32_t* s, const int32_t* d, int64_t k, IdxView
     if ((threadIdx.x & 31) == 0 && acc) atomicAdd(bytes, acc);
 }
 
+__global__ void k_tc_lkeys(const int32_t* L, int64_t m, uint32_t* key, int32_t* perm) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+        key[i] = (uint32_t)L[i];
+        perm[i] = (int32_t)i;
+    }
+}
+
+__global__ void k_tc_perm_nch(const int32_t* perm, const int64_t* nch, int64_t m, int64_t* out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= m; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = i < m ? nch[perm[i]] : 0;
+}
+
 __global__ void k_tc_chunk_table(const int64_t* choff, int64_t k, int32_t* rec_of) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < k; i += (int64_t)gridDim.x * blockDim.x)
         for (int64_t c = choff[i]; c < choff[i + 1]; ++c) rec_of[c] = (int32_t)i;
@@ -145,7 +157,8 @@ __global__ void k_tc_reset(const int32_t* hubs, const int64_t* nhub, uint8_t* hu
 
 // one warp per work item: kWalkChunk arcs of S's row against L
 __global__ void __launch_bounds__(kThreads) k_tc_count(const int32_t* s, const int32_t* d, TcRec r,
-                                                       const int32_t* rec_of, const int64_t* nwork, IdxView ix,
+                                                       const int32_t* perm, const int32_t* rec_of,
+                                                       const int64_t* nwork, IdxView ix,
                                                        int64_t n, const int64_t* R, int64_t nr, const int32_t* slot,
                                                        const uint32_t* bm, int64_t words, const uint8_t* multi,
                                                        const uint32_t* filt, uint64_t fmask,
@@ -156,11 +169,12 @@ __global__ void __launch_bounds__(kThreads) k_tc_count(const int32_t* s, const i
     const int64_t nw = *nwork;
     int64_t acc = 0;
     for (int64_t c = warp; c < nw; c += nwarps) {
-        const int32_t i = rec_of[c];
+        const int32_t ip = rec_of[c];  // position in L order
+        const int32_t i = perm ? perm[ip] : ip;
         const int32_t u = s[i], v = d[i];
         const int64_t rk = pair_rank(u, v, n);
         const int32_t L = r.L[i], S = r.S[i];
-        const int64_t j = c - r.nch[i];  // nch holds the exclusive scan here
+        const int64_t j = c - r.nch[ip];  // nch holds the exclusive scan in L order here
         const int64_t wa = ix.off[S] + j * kWalkChunk, wb = min(wa + kWalkChunk, ix.off[S + 1]);
         const int64_t la = ix.off[L], lb = ix.off[L + 1];
         const int32_t hs = slot[L];
@@ -242,16 +256,30 @@ int64_t TC::count_records(const int32_t* s, const int32_t* d, int64_t k) {
         TcRec rr{L.get(), S.get(), nch.get()};
         GD_KERNEL(k_tc_prep, grid_for(m, 256), 256, 0, st, s + a, d + a, m, ix.view(), rr, hubmark.get(),
                   ctr.get() + 1);
+        // hubs of this phase (L endpoints with >= kBmDeg arcs) and the work
+        // item total, read back together
         exclusive_scan_i64(st, nch.get(), choff.get(), m + 1);
-        rr.nch = choff.get();
-        // hubs of this phase: L endpoints with >= kBmDeg arcs
         DBuf<int32_t> hubs(n, st);
-        DBuf<int64_t> cnt2(2, st);  // [work items, hubs] for one read-back
+        DBuf<int64_t> cnt2(2, st);
         GD_CUDA(cudaMemcpyAsync(cnt2.get(), choff.get() + m, sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
         select_flagged_index_async(st, hubmark.get(), n, hubs.get(), cnt2.get() + 1);
         int64_t hc[2];
         read_small(st, hc, cnt2.get(), sizeof hc);
         const int64_t nwork = hc[0], nhubs = hc[1];
+        // with hub rows in play, work items go in L order: warps running side
+        // by side (grid-stride neighbours) meet the same long rows and share
+        // their L2 lines; without hubs the record order stands
+        DBuf<int32_t> perm;
+        if (nhubs > 0) {
+            DBuf<uint32_t> lkey(m, st);
+            perm.alloc(m, st);
+            GD_KERNEL(k_tc_lkeys, grid_for(m, 256), 256, 0, st, L.get(), m, lkey.get(), perm.get());
+            sort_pairs_u32(st, lkey.get(), perm.get(), m, bits_for((uint64_t)std::max<int64_t>(n - 1, 1)));
+            DBuf<int64_t> nchp(m + 1, st);
+            GD_KERNEL(k_tc_perm_nch, grid_for(m + 1, 256), 256, 0, st, perm.get(), nch.get(), m, nchp.get());
+            exclusive_scan_i64(st, nchp.get(), choff.get(), m + 1);
+        }
+        rr.nch = choff.get();
         // work items: exact count (records may share a long S row)
         DBuf<int32_t> rec_of(std::max<int64_t>(nwork, 1), st);
         GD_KERNEL(k_tc_chunk_table, grid_for(m, 256), 256, 0, st, choff.get(), m, rec_of.get());
@@ -273,7 +301,7 @@ int64_t TC::count_records(const int32_t* s, const int32_t* d, int64_t k) {
         }
         int pi = prof_begin("tc_count", 0, st);
         k_tc_count<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((nwork + 7) / 8, 148 * 16)), kThreads, 0,
-                     st>>>(s + a, d + a, rr, rec_of.get(), choff.get() + m, ix.view(), n,
+                     st>>>(s + a, d + a, rr, nhubs > 0 ? perm.get() : nullptr, rec_of.get(), choff.get() + m, ix.view(), n,
                                                  reinterpret_cast<const int64_t*>(R.get()), k, hub_slot.get(),
                                                  bm.get(), words, bm_multi.get(), filt.get(), fmask, ctr.get());
         count_launch();
