@@ -81,7 +81,7 @@ struct TcRec {
 };
 
 __global__ void k_tc_prep(const int32_t* s, const int32_t* d, int64_t k, IdxView ix, TcRec r, uint8_t* hubmark,
-                          unsigned long long* bytes) {
+                          uint8_t* isshort, unsigned long long* bytes) {
     unsigned long long acc = 0;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < k; i += (int64_t)gridDim.x * blockDim.x) {
         int32_t u = s[i], v = d[i];
@@ -92,7 +92,9 @@ __global__ void k_tc_prep(const int32_t* s, const int32_t* d, int64_t k, IdxView
         int64_t dS = walk_u ? du : dv, dL = walk_u ? dv : du;
         r.L[i] = L;
         r.S[i] = S;
-        r.nch[i] = (dS + kWalkChunk - 1) / kWalkChunk;
+        const bool sh = dS <= 64;  // kShortWalk: a sub-warp group takes it whole
+        isshort[i] = sh;
+        r.nch[i] = sh ? 0 : (dS + kWalkChunk - 1) / kWalkChunk;
         if (dL >= kBmDeg) hubmark[L] = 1;
         acc += 32 + 4 * (unsigned long long)(du + dv);  // 2*2*off + (deg u + deg v)*idx
     }
@@ -155,7 +157,35 @@ __global__ void k_tc_reset(const int32_t* hubs, const int64_t* nhub, uint8_t* hu
     }
 }
 
-// one warp per work item: kWalkChunk arcs of S's row against L
+// count of one record's walk slice [wa, wb) of S's row against L, lanes
+// strided by W
+template <int W>
+__device__ __forceinline__ int64_t tc_walk(const IdxView& ix, int32_t u, int32_t v, int32_t L, int64_t wa, int64_t wb,
+                                           int lane, int64_t n, const int64_t* R, int64_t nr, const int32_t* slot,
+                                           const uint32_t* bm, int64_t words, const uint8_t* multi,
+                                           const uint32_t* filt, uint64_t fmask) {
+    const int64_t rk = pair_rank(u, v, n);
+    const int64_t la = ix.off[L], lb = ix.off[L + 1];
+    const int32_t hs = slot[L];
+    const uint32_t* b = hs >= 0 ? bm + (int64_t)hs * words : nullptr;
+    const bool mult = hs >= 0 && multi[hs];
+    int64_t acc = 0;
+    for (int64_t e = wa + lane; e < wb; e += W) {
+        int32_t w = ix.col[e];
+        if (w < 0 || w == v) continue;
+        int64_t m;
+        if (b) m = (b[w >> 5] >> (w & 31)) & 1 ? (mult ? mult_in(ix.col, la, lb, w) : 1) : 0;
+        else m = mult_in(ix.col, la, lb, w);
+        if (!m) continue;
+        int64_t ru = pair_rank(u, w, n), rv = pair_rank(v, w, n);
+        bool skip = (ru < rk && maybe_in(filt, fmask, ru) && in_sorted(R, nr, ru)) ||
+                    (rv < rk && maybe_in(filt, fmask, rv) && in_sorted(R, nr, rv));
+        if (!skip) acc += m;
+    }
+    return acc;
+}
+
+// long records: one warp per work item, kWalkChunk arcs of S's row
 __global__ void __launch_bounds__(kThreads) k_tc_count(const int32_t* s, const int32_t* d, TcRec r,
                                                        const int32_t* perm, const int32_t* rec_of,
                                                        const int64_t* nwork, IdxView ix,
@@ -171,30 +201,43 @@ __global__ void __launch_bounds__(kThreads) k_tc_count(const int32_t* s, const i
     for (int64_t c = warp; c < nw; c += nwarps) {
         const int32_t ip = rec_of[c];  // position in L order
         const int32_t i = perm ? perm[ip] : ip;
-        const int32_t u = s[i], v = d[i];
-        const int64_t rk = pair_rank(u, v, n);
-        const int32_t L = r.L[i], S = r.S[i];
+        const int32_t S = r.S[i];
         const int64_t j = c - r.nch[ip];  // nch holds the exclusive scan in L order here
         const int64_t wa = ix.off[S] + j * kWalkChunk, wb = min(wa + kWalkChunk, ix.off[S + 1]);
-        const int64_t la = ix.off[L], lb = ix.off[L + 1];
-        const int32_t hs = slot[L];
-        const uint32_t* b = hs >= 0 ? bm + (int64_t)hs * words : nullptr;
-        const bool mult = hs >= 0 && multi[hs];
-        for (int64_t e = wa + lane; e < wb; e += 32) {
-            int32_t w = ix.col[e];
-            if (w < 0 || w == v) continue;
-            int64_t m;
-            if (b) m = (b[w >> 5] >> (w & 31)) & 1 ? (mult ? mult_in(ix.col, la, lb, w) : 1) : 0;
-            else m = mult_in(ix.col, la, lb, w);
-            if (!m) continue;
-            int64_t ru = pair_rank(u, w, n), rv = pair_rank(v, w, n);
-            bool skip = (ru < rk && maybe_in(filt, fmask, ru) && in_sorted(R, nr, ru)) ||
-                        (rv < rk && maybe_in(filt, fmask, rv) && in_sorted(R, nr, rv));
-            if (!skip) acc += m;
-        }
+        acc += tc_walk<32>(ix, s[i], d[i], r.L[i], wa, wb, lane, n, R, nr, slot, bm, words, multi, filt, fmask);
     }
     for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if (lane == 0 && acc) atomicAdd(total, (unsigned long long)acc);
+}
+
+// short records (walk <= kShortWalk arcs): 8 lanes each, 4 records per warp
+// in flight instead of one latency chain per warp
+constexpr int kShortWalk = 64;
+constexpr int kShortG = 8;
+
+__global__ void __launch_bounds__(kThreads) k_tc_count_short(const int32_t* s, const int32_t* d, TcRec r,
+                                                             const int32_t* list, const int64_t* nlist, IdxView ix,
+                                                             int64_t n, const int64_t* R, int64_t nr,
+                                                             const int32_t* slot, const uint32_t* bm, int64_t words,
+                                                             const uint8_t* multi, const uint32_t* filt,
+                                                             uint64_t fmask, unsigned long long* total) {
+    const int gl = threadIdx.x & (kShortG - 1), gw = (threadIdx.x & 31) / kShortG;
+    constexpr int kPer = 32 / kShortG;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t m = *nlist;
+    int64_t acc = 0;
+    for (int64_t t0 = warp * kPer; t0 < m; t0 += nwarps * kPer) {
+        const int64_t t = t0 + gw;
+        if (t < m) {
+            const int32_t i = list[t];
+            const int32_t S = r.S[i];
+            acc += tc_walk<kShortG>(ix, s[i], d[i], r.L[i], ix.off[S], ix.off[S + 1], gl, n, R, nr, slot, bm, words,
+                                    multi, filt, fmask);
+        }
+    }
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0 && acc) atomicAdd(total, (unsigned long long)acc);
 }
 
 // staticTC (tc_dynamic.sp:7-19): sum over arcs (v,a), a > v, and arcs (a,b),
@@ -254,8 +297,12 @@ int64_t TC::count_records(const int32_t* s, const int32_t* d, int64_t k) {
         DBuf<int64_t> nch(m + 1, st), choff(m + 1, st);
         GD_CUDA(cudaMemsetAsync(nch.get() + m, 0, sizeof(int64_t), st));
         TcRec rr{L.get(), S.get(), nch.get()};
+        DBuf<uint8_t> isshort(m, st);
         GD_KERNEL(k_tc_prep, grid_for(m, 256), 256, 0, st, s + a, d + a, m, ix.view(), rr, hubmark.get(),
-                  ctr.get() + 1);
+                  isshort.get(), ctr.get() + 1);
+        DBuf<int32_t> shortl(m, st);
+        DBuf<int64_t> nshort(1, st);
+        select_flagged_index_async(st, isshort.get(), m, shortl.get(), nshort.get());
         // hubs of this phase (L endpoints with >= kBmDeg arcs) and the work
         // item total, read back together
         exclusive_scan_i64(st, nch.get(), choff.get(), m + 1);
@@ -304,6 +351,12 @@ int64_t TC::count_records(const int32_t* s, const int32_t* d, int64_t k) {
                      st>>>(s + a, d + a, rr, nhubs > 0 ? perm.get() : nullptr, rec_of.get(), choff.get() + m, ix.view(), n,
                                                  reinterpret_cast<const int64_t*>(R.get()), k, hub_slot.get(),
                                                  bm.get(), words, bm_multi.get(), filt.get(), fmask, ctr.get());
+        count_launch();
+        GD_LAUNCH_CHECK();
+        k_tc_count_short<<<148 * 16, kThreads, 0, st>>>(s + a, d + a, rr, shortl.get(), nshort.get(), ix.view(), n,
+                                                        reinterpret_cast<const int64_t*>(R.get()), k, hub_slot.get(),
+                                                        bm.get(), words, bm_multi.get(), filt.get(), fmask,
+                                                        ctr.get());
         count_launch();
         GD_LAUNCH_CHECK();
         prof_end(pi, st);
