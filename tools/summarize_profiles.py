@@ -19,7 +19,7 @@ hdr, data = rows[hi], rows[hi + 1:]
 ki, vi = hdr.index("Kernel Name"), hdr.index("Metric Value")
 seq = [(r[ki], float(r[vi].replace(",", ""))) for r in data]
 first = next(i for i, (k, _) in enumerate(seq) if "k_pr_onupdate" in k)
-nb = sum(1 for k, _ in seq if "k_pr_onupdate" in k) // 2
+nb = sum(1 for k, _ in seq if "k_pr_onupdate" in k)  # one OnDelete/OnAdd launch per batch
 tot, cnt = collections.defaultdict(float), collections.Counter()
 for k, v in seq[first:]:
     name = k.split("(")[0].replace("gdb::<unnamed>::", "").replace("void ", "")
