@@ -165,3 +165,38 @@ def test_sssp_near_far_width_does_not_change_results(gd, graph, delta, decr, mon
     want_d, want_p = O.OracleSSSP(og, 0).run_stream(kind, us, ud, uw, per).read()
     np.testing.assert_array_equal(ctx.properties["dist"].values(), want_d)
     np.testing.assert_array_equal(ctx.properties["parent"].values(), want_p)
+
+
+@pytest.mark.parametrize("dup", [False, True])
+def test_tc_hub_bitmaps_and_work_items_match_oracle(gd, dup):
+    """Hub rows (>= 1024 arcs: bitmap lookups, L-ordered work items, walks cut
+    into 1024-arc items) and, with dup, parallel arcs on the hub rows (the
+    bitmap hit falls back to the multiplicity search)."""
+    from oracle import oracle as O
+
+    rng = np.random.default_rng(31 + dup)
+    n = 6000
+    hubs = np.array([0, 1, 2])
+    src = [np.repeat(hubs, 2500), rng.integers(0, n, 30000)]
+    dst = [rng.integers(3, n, 7500), rng.integers(0, n, 30000)]
+    src.append(np.array([0, 1, 0]))  # hub-hub edges: long walks on both sides
+    dst.append(np.array([1, 2, 2]))
+    if dup:  # parallel copies of some hub arcs
+        src.append(np.repeat(hubs, 300))
+        dst.append(np.concatenate([d[:300] for d in np.split(dst[0], 3)]))
+    s, d = np.concatenate(src), np.concatenate(dst)
+    keep = s != d
+    s, d = s[keep], d[keep]
+    k = 4000
+    kind = np.where(rng.random(k) < 0.5, ord("d"), ord("a")).astype(np.uint8)
+    pick = rng.integers(0, len(s), k)
+    us = np.where(kind == ord("d"), s[pick], np.where(rng.random(k) < 0.3, rng.choice(hubs, k),
+                                                        rng.integers(0, n, k)))
+    ud = np.where(kind == ord("d"), d[pick], rng.integers(0, n, k))
+    uw = np.ones(k, np.int64)
+    for bs in (500, 4000):
+        g = gd.DynamicGraph.from_arrays(n, s, d, directed=False)
+        ctx = gd.run_batches(gd.compile_source("Dynamic dynamicTC("), g,
+                             gd.UpdateStream.from_arrays(kind, us, ud, uw), bs, {})
+        og = O.OracleGraph(n, s, d, directed=False)
+        assert ctx.return_value == O.OracleTC(og).run_stream(kind, us, ud, uw, bs).read()
