@@ -322,32 +322,52 @@ __global__ void k_aff_giant(const int32_t* probe, int m, int32_t* giant) {
 
 // Vertices outside the dominant component link the rest of their out-arcs
 // (base after the sampled ones, then every delta) and all their in-arcs.
+// rows with more than kRestWarp remaining arcs go to a warp each
+constexpr int64_t kRestWarp = 64;
+
+__device__ inline void aff_link_row(OutView ov, IdxView in, int32_t v, int32_t* p, int lane, int stride) {
+    for (int sg = 0; sg < ov.nseg; ++sg) {
+        const int64_t* off = ov.off[sg];
+        const int32_t* col = ov.col[sg];
+        int64_t a = off[v], b = off[v + 1];
+        for (int64_t i = (sg == 0 ? a + kSample : a) + lane; i < b; i += stride) {  // base slots < kSample: sampled
+            int32_t c = col[i];
+            if (c >= 0 && c != v) uf_union(p, v, c);
+        }
+    }
+    if (in.off) {
+        for (int64_t e = in.off[v] + lane; e < in.off[v + 1]; e += stride) {
+            int32_t u = in.col[e];
+            if (u >= 0 && u != v) uf_union(p, v, u);
+        }
+    }
+}
+
 __global__ void k_aff_rest(OutView ov, IdxView in, int64_t n, const int32_t* giant_p, int32_t* p) {
     const int32_t giant = *giant_p;
-    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
-        // the root test and the arc counts load together; isolated vertices
-        // (42% of R-MAT V) and sampled-only ones stop here
-        const int32_t pv = p[v];
-        const int64_t b0 = ov.off[0][v], e0 = ov.off[0][v + 1];
-        const int64_t ia = in.off ? in.off[v] : 0, ib = in.off ? in.off[v + 1] : 0;
-        int64_t more = (e0 - b0 > kSample ? 1 : 0) + (ib - ia);
-        for (int sg = 1; sg < ov.nseg; ++sg) more += ov.off[sg][v + 1] - ov.off[sg][v];
-        if (more == 0 || pv == giant) continue;
-        if (uf_find(p, (int32_t)v) == giant) continue;
-        for (int sg = 0; sg < ov.nseg; ++sg) {
-            const int64_t* off = ov.off[sg];
-            const int32_t* col = ov.col[sg];
-            int64_t a = off[v], b = off[v + 1];
-            for (int64_t i = (sg == 0 ? a + kSample : a); i < b; ++i) {  // base slots < kSample: sampled
-                int32_t c = col[i];
-                if (c >= 0 && c != (int32_t)v) uf_union(p, (int32_t)v, c);
-            }
+    const int lane = threadIdx.x & 31;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    // 32 consecutive vertices per warp step: the loop stays warp-uniform so
+    // that a hub outside the giant can be linked by the whole warp
+    for (int64_t v0 = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; v0 < n; v0 += nwarps * 32) {
+        const int64_t v = v0 + lane;
+        bool need = false;
+        int64_t more = 0;
+        if (v < n) {
+            // the root test and the arc counts load together; isolated
+            // vertices (42% of R-MAT V) and sampled-only ones stop here
+            const int32_t pv = p[v];
+            const int64_t b0 = ov.off[0][v], e0 = ov.off[0][v + 1];
+            const int64_t ia = in.off ? in.off[v] : 0, ib = in.off ? in.off[v + 1] : 0;
+            more = max(e0 - b0 - kSample, (int64_t)0) + (ib - ia);
+            for (int sg = 1; sg < ov.nseg; ++sg) more += ov.off[sg][v + 1] - ov.off[sg][v];
+            need = more > 0 && pv != giant && uf_find(p, (int32_t)v) != giant;
         }
-        if (in.off) {
-            for (int64_t e = in.off[v]; e < in.off[v + 1]; ++e) {
-                int32_t u = in.col[e];
-                if (u >= 0 && u != (int32_t)v) uf_union(p, (int32_t)v, u);
-            }
+        const bool heavy = need && more > kRestWarp;
+        if (need && !heavy) aff_link_row(ov, in, (int32_t)v, p, 0, 1);
+        for (unsigned hm = __ballot_sync(0xffffffffu, heavy); hm; hm &= hm - 1) {  // a hub: the whole warp
+            const int32_t hv = __shfl_sync(0xffffffffu, (int32_t)v, __ffs(hm) - 1);
+            aff_link_row(ov, in, hv, p, lane, 32);
         }
     }
 }

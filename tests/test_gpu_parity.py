@@ -201,6 +201,27 @@ def test_propagate_flags_matches_bfs(gd):
         np.testing.assert_array_equal(g.propagate_flags(seeds), want)
 
 
+def test_propagate_flags_with_hubs_outside_the_giant(gd):
+    """Two large stars (in- and out-arcs), no dominating component: the
+    union-find's rest pass must link a hub that is not in the sampled giant
+    (warp-cooperative path) and the flags must match the BFS oracle."""
+    from oracle import oracle as O
+
+    n = 12000
+    leaves_a = np.arange(10, 5010)
+    leaves_b = np.arange(5010, 11000)
+    src = np.concatenate([np.full(len(leaves_a), 3), leaves_b, np.array([11000, 11001])])
+    dst = np.concatenate([leaves_a, np.full(len(leaves_b), 7), np.array([11001, 11002])])
+    for seeds_at in ([4000], [6000], [11002], [4000, 11002]):
+        seeds = np.zeros(n, np.uint8)
+        seeds[seeds_at] = 1
+        for directed in (True, False):
+            g = gd.DynamicGraph.from_arrays(n, src, dst, directed=directed, with_reverse=True)
+            og = O.OracleGraph(n, src, dst, directed=directed, with_reverse=True)
+            want, _ = og.propagate_flags(seeds)
+            np.testing.assert_array_equal(g.propagate_flags(seeds), want)
+
+
 def test_errors_map_to_reference_exceptions(gd):
     g = gd.DynamicGraph.build([(0, 1, 30), (0, 2, 20)], 3, weighted=True, with_reverse=True)
     with pytest.raises(gd.ExecError, match="99"):
