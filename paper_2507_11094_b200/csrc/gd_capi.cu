@@ -39,9 +39,7 @@ thread_local KernelProf* tl_prof = nullptr;
 int prof_begin(const char* name, int64_t bytes, cudaStream_t s) {
     KernelProf* p = tl_prof;
     if (!p || !p->on) return -1;
-    KernelProf::Rec r{name, nullptr, nullptr, bytes, -1};
-    GD_CUDA(cudaEventCreate(&r.a));
-    GD_CUDA(cudaEventCreate(&r.b));
+    KernelProf::Rec r{name, p->event(), p->event(), bytes, -1, p->seq, false};  // pooled events
     GD_CUDA(cudaEventRecord(r.a, s));
     p->pending.push_back(r);
     return (int)p->pending.size() - 1;
@@ -57,24 +55,45 @@ void prof_end(int idx, cudaStream_t s) {
     GD_CUDA(cudaEventRecord(p->pending[(size_t)idx].b, s));
 }
 
+void KernelProf::reset_last() {
+    if (pending.size() > 4096) flush();
+    ++seq;
+    last.clear();
+}
+
+void KernelProf::drop_sweeps_from(int64_t limit) {
+    for (auto& r : pending)
+        if (r.seq == seq && r.tag >= limit) r.drop = true;
+}
+
 void KernelProf::flush() {
     for (auto& r : pending) {
-        GD_CUDA(cudaEventSynchronize(r.b));
-        if (r.tag < 0 || r.tag < sweep_limit) {
+        if (!r.drop) {
+            GD_CUDA(cudaEventSynchronize(r.b));
             float ms = 0;
             GD_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
-            int64_t bytes = r.bytes;
-            for (KernelStat* k : {&last[r.name], &total[r.name]}) {
+            for (KernelStat* k : {&total[r.name], r.seq == seq ? &last[r.name] : nullptr}) {
+                if (!k) continue;
                 k->ms += ms;
                 k->launches += 1;
-                k->bytes += bytes;
+                k->bytes += r.bytes;
             }
         }
-        cudaEventDestroy(r.a);
-        cudaEventDestroy(r.b);
+        pool.push_back(r.a);
+        pool.push_back(r.b);
     }
     pending.clear();
-    sweep_limit = INT64_MAX;
+}
+
+cudaEvent_t KernelProf::event() {
+    if (!pool.empty()) {
+        cudaEvent_t e = pool.back();
+        pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    GD_CUDA(cudaEventCreate(&e));
+    return e;
 }
 
 KernelProf::~KernelProf() {
@@ -82,6 +101,7 @@ KernelProf::~KernelProf() {
         cudaEventDestroy(r.a);
         cudaEventDestroy(r.b);
     }
+    for (auto e : pool) cudaEventDestroy(e);
 }
 
 }  // namespace gdb
@@ -548,6 +568,7 @@ int gd_iterations(const void* h, int64_t* it) {
 int gd_kernel_time(const void* h, const char* name, double* ms, int64_t* launches, int64_t* bytes) {
     if (!h) return null_handle();
     gdb::AlgoBase* a = algo_of(h);
+    a->prof.flush();
     auto it = a->prof.last.find(name);
     if (it == a->prof.last.end()) {
         *ms = 0;
@@ -564,6 +585,7 @@ int gd_kernel_time(const void* h, const char* name, double* ms, int64_t* launche
 int gd_kernel_time_total(const void* h, const char* name, double* ms, int64_t* launches, int64_t* bytes) {
     if (!h) return null_handle();
     gdb::AlgoBase* a = algo_of(h);
+    a->prof.flush();
     auto it = a->prof.total.find(name);
     bool hit = it != a->prof.total.end();
     *ms = hit ? it->second.ms : 0;
@@ -575,7 +597,10 @@ int gd_kernel_time_total(const void* h, const char* name, double* ms, int64_t* l
 int gd_set_profiling(const void* h, int on) {
     if (!h) return null_handle();
     gdb::KernelProf& p = algo_of(h)->prof;
-    if (on && !p.on) p.total.clear();
+    if (on && !p.on) {
+        p.flush();
+        p.total.clear();
+    }
     p.on = on != 0;
     return ok();
 }

@@ -191,21 +191,29 @@ enum Phase { PH_STATIC = 0, PH_PRE = 1, PH_STRUCT = 2, PH_PROP = 3, PH_MERGE = 4
 
 struct PhaseTimer {
     cudaStream_t s = nullptr;
-    std::vector<cudaEvent_t> evs;
+    std::vector<cudaEvent_t> evs, pool;  // pool: recycled events (no create/destroy per phase)
     std::vector<int> phases;
     double total_ms[PH_COUNT] = {0, 0, 0, 0, 0};
     int open = -1;
-    void begin(int ph) {
+    cudaEvent_t event() {
+        if (!pool.empty()) {
+            cudaEvent_t e = pool.back();
+            pool.pop_back();
+            return e;
+        }
         cudaEvent_t e;
         GD_CUDA(cudaEventCreate(&e));
+        return e;
+    }
+    void begin(int ph) {
+        cudaEvent_t e = event();
         GD_CUDA(cudaEventRecord(e, s));
         evs.push_back(e);
         phases.push_back(ph);
     }
     // Called at a sync point: turn consecutive event pairs into phase times.
     void end_all() {
-        cudaEvent_t e;
-        GD_CUDA(cudaEventCreate(&e));
+        cudaEvent_t e = event();
         GD_CUDA(cudaEventRecord(e, s));
         evs.push_back(e);
         phases.push_back(-1);
@@ -215,12 +223,13 @@ struct PhaseTimer {
             GD_CUDA(cudaEventElapsedTime(&ms, evs[i], evs[i + 1]));
             if (phases[i] >= 0) total_ms[phases[i]] += ms;
         }
-        for (auto ev : evs) cudaEventDestroy(ev);
+        pool.insert(pool.end(), evs.begin(), evs.end());
         evs.clear();
         phases.clear();
     }
     ~PhaseTimer() {
         for (auto ev : evs) cudaEventDestroy(ev);
+        for (auto ev : pool) cudaEventDestroy(ev);
     }
 };
 

@@ -30,14 +30,22 @@ struct KernelProf {
         const char* name;
         cudaEvent_t a, b;
         int64_t bytes;
-        int64_t tag;  // >= 0: queued sweep index; dropped when >= sweep_limit
+        int64_t tag;    // >= 0: queued sweep index (see drop_sweeps_from)
+        int64_t seq;    // the batch (reset_last call) it belongs to
+        bool drop;      // a queued sweep that ran as a device no-op
     };
+    // Records are folded lazily -- when stats are queried, or at a batch
+    // start once many are pending -- so a timed loop pays only for the event
+    // records themselves, not for syncs and elapsed-time queries per batch.
     std::vector<Rec> pending;
-    int64_t sweep_limit = INT64_MAX;  // sweeps that actually ran (the rest were device no-ops)
-    std::map<std::string, KernelStat> last;   // stats of the last flushed call
+    int64_t seq = 0;
+    std::map<std::string, KernelStat> last;   // stats of the latest batch
     std::map<std::string, KernelStat> total;  // since profiling was switched on
-    void reset_last() { last.clear(); }
-    void flush();  // sync on the recorded events and fold them into `last`
+    void reset_last();                        // a batch starts
+    void flush();                             // fold the pending records
+    void drop_sweeps_from(int64_t limit);     // this batch's records of queued sweeps >= limit
+    std::vector<cudaEvent_t> pool;            // recycled events
+    cudaEvent_t event();
     ~KernelProf();
 };
 

@@ -357,7 +357,6 @@ PR::PR(Store* st, double d, double b, int64_t mi) : AlgoBase(ALGO_PR, st), dampi
     }
     recompute(nullptr);  // staticPR: every node participates
     timer.end_all();
-    prof.flush();
 }
 
 void PR::set_comm(Comm* c) {
@@ -478,7 +477,7 @@ void PR::recompute(const uint8_t* flags) {
     ahead_hint = sweeps;  // sweep counts are stable batch to batch: usually one read-back
     last_sweeps = sweeps;
     iterations += sweeps;
-    prof.sweep_limit = sweeps;  // queued no-op sweeps are not launches of the path
+    prof.drop_sweeps_from(sweeps);  // queued no-op sweeps are not launches of the path
     for (auto& pr : pull_recs) {
         if (pr.first < 0) continue;
         int64_t nb = 0, eb = 0;  // bin -1: all three
@@ -518,7 +517,6 @@ void PR::batch(DevBatch& b, int64_t batch_index) {
     flood_weak_components(*g, affected.get(), &prof);
     recompute(affected.get());
     timer.end_all();
-    prof.flush();
 }
 
 void PR::read(double* h_rank, int64_t* h_outdeg) {

@@ -662,7 +662,6 @@ SSSP::SSSP(Store* st, int64_t s) : AlgoBase(ALGO_SSSP, st), src((int32_t)s) {
     // and pay their extra rounds; keep near-far for the deep ones (grids)
     if (!getenv("GD_SSSP_DELTA") && iterations < kNearFarMinRounds) delta = 0;
     timer.end_all();
-    prof.flush();
 }
 
 void SSSP::fixpoint(int mode, const int32_t* seeds, const int64_t* d_nseeds, int64_t nseeds, uint8_t* flags) {
@@ -806,7 +805,6 @@ void SSSP::batch(DevBatch& b, int64_t batch_index) {
     fix_parents(list.get(), nlist, n);
     finish();
     timer.end_all();
-    prof.flush();
 }
 
 void SSSP::read_async(int64_t* h_dist, int64_t* h_parent) {

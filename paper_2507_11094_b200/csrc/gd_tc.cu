@@ -390,7 +390,6 @@ TC::TC(Store* st) : AlgoBase(ALGO_TC, st) {
                     ix.view(), g->n, tot.get());
     count = (int64_t)read_scalar(s, tot.get());
     timer.end_all();
-    prof.flush();
 }
 
 void TC::batch(DevBatch& b, int64_t batch_index) {
@@ -410,7 +409,6 @@ void TC::batch(DevBatch& b, int64_t batch_index) {
     timer.begin(PH_PRE);
     count += count_records(b.as.get(), b.ad.get(), b.kadd);
     timer.end_all();
-    prof.flush();
 }
 
 }  // namespace gdb
