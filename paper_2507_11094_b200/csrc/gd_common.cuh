@@ -39,7 +39,15 @@ struct GdError : std::runtime_error {
 
 #define GD_LAUNCH_CHECK() GD_CUDA(cudaGetLastError())
 
-// Stream-ordered device buffer (cudaMallocAsync pool); freed on the stream.
+// Stream-ordered device memory with a per-stream cache of freed blocks in
+// size classes (2^k in 8 steps).  A batch allocates and frees ~100 temporaries;
+// cudaMallocAsync / cudaFreeAsync for each cost host time that the GPU then
+// waits on.  A block is reused only on the stream it was freed on, so stream
+// order protects it.
+void* dev_alloc(size_t bytes, cudaStream_t s);
+void dev_free(void* p, size_t bytes, cudaStream_t s);
+void dev_cache_release(cudaStream_t s, bool all = false);  // return a stream's cached blocks (before destroying it)
+
 template <typename T>
 struct DBuf {
     T* p = nullptr;
@@ -69,14 +77,14 @@ struct DBuf {
         release();
         s = st;
         n = count;
-        if (count) GD_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), st));
+        if (count) p = static_cast<T*>(dev_alloc(count * sizeof(T), st));
     }
     // grow-only reuse: keeps the allocation when large enough
     void ensure(size_t count, cudaStream_t st) {
         if (count > n || p == nullptr) alloc(count ? count : 1, st);
     }
     void release() {
-        if (p) cudaFreeAsync(p, s);
+        if (p) dev_free(p, n * sizeof(T), s);
         p = nullptr;
         n = 0;
     }

@@ -1,3 +1,6 @@
+#include <vector>
+#include <mutex>
+#include <map>
 #include <cstring>
 // gd_prims.cu -- device-wide sort / scan / select primitives (CUB, stream-ordered).
 #include <cub/cub.cuh>
@@ -14,10 +17,10 @@ struct Temp {
     size_t bytes = 0;
     cudaStream_t s;
     Temp(size_t b, cudaStream_t st) : bytes(b), s(st) {
-        if (b) GD_CUDA(cudaMallocAsync(&p, b, st));
+        if (b) p = dev_alloc(b, st);
     }
     ~Temp() {
-        if (p) cudaFreeAsync(p, s);
+        if (p) dev_free(p, bytes, s);
     }
 };
 }  // namespace
@@ -80,6 +83,78 @@ void inclusive_scan_i64(cudaStream_t s, const int64_t* in, int64_t* out, int64_t
     Temp t(bytes, s);
     GD_CUDA(cub::DeviceScan::InclusiveSum(t.p, bytes, in, out, n, s));
     count_library_launch();
+}
+
+namespace {
+struct DevCache {
+    std::mutex mu;
+    std::map<std::pair<cudaStream_t, size_t>, std::vector<void*>> free;
+};
+DevCache& dev_cache() {
+    static DevCache* c = new DevCache;  // never destroyed: blocks outlive static teardown order
+    return *c;
+}
+size_t size_class(size_t bytes) {
+    if (bytes <= 4096) return 4096;
+    size_t k = 63 - __builtin_clzll(bytes - 1);  // 2^k < bytes <= 2^(k+1)
+    size_t step = (size_t(1) << k) / 8;
+    return ((bytes + step - 1) / step) * step;
+}
+}  // namespace
+
+// Blocks up to kCacheMax are cached per (stream, size class) so the per-batch
+// temporaries skip the pool's host-side bookkeeping; a block is only handed
+// out again on the stream it was freed on, so stream order keeps it safe.
+// Larger blocks (the store's arrays) go straight to the stream-ordered pool at
+// their exact size.
+constexpr size_t kCacheMax = size_t(64) << 20;
+
+void* dev_alloc(size_t bytes, cudaStream_t s) {
+    const bool cached = bytes <= kCacheMax;
+    const size_t c = cached ? size_class(bytes) : bytes;
+    DevCache& dc = dev_cache();
+    if (cached) {
+        std::lock_guard<std::mutex> lk(dc.mu);
+        auto it = dc.free.find({s, c});
+        if (it != dc.free.end() && !it->second.empty()) {
+            void* p = it->second.back();
+            it->second.pop_back();
+            return p;
+        }
+    }
+    void* p = nullptr;
+    cudaError_t e = cudaMallocAsync(&p, c, s);
+    if (e == cudaErrorMemoryAllocation) {  // hand every cached block back to the pool, retry once
+        cudaGetLastError();
+        dev_cache_release(nullptr, true);
+        GD_CUDA(cudaDeviceSynchronize());
+        e = cudaMallocAsync(&p, c, s);
+    }
+    GD_CUDA(e);
+    return p;
+}
+
+void dev_free(void* p, size_t bytes, cudaStream_t s) {
+    if (bytes > kCacheMax) {
+        GD_CUDA(cudaFreeAsync(p, s));
+        return;
+    }
+    DevCache& dc = dev_cache();
+    std::lock_guard<std::mutex> lk(dc.mu);
+    dc.free[{s, size_class(bytes)}].push_back(p);
+}
+
+void dev_cache_release(cudaStream_t s, bool all) {
+    DevCache& dc = dev_cache();
+    std::lock_guard<std::mutex> lk(dc.mu);
+    for (auto it = dc.free.begin(); it != dc.free.end();) {
+        if (all || it->first.first == s) {
+            for (void* p : it->second) cudaFreeAsync(p, it->first.first);
+            it = dc.free.erase(it);
+        } else {
+            ++it;
+        }
+    }
 }
 
 void read_small(cudaStream_t s, void* host, const void* dev, size_t bytes) {

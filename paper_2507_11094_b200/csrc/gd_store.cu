@@ -881,7 +881,17 @@ Store::~Store() {
     if (stream) {
         cudaSetDevice(device);
         segs.clear();
+        rev = SortedIndex();
+        fwd = SortedIndex();
+        dcounts.release();
+        otpos.release();
+        otrow.release();
+        tab.release();
         cudaStreamSynchronize(stream);
+        dev_cache_release(stream);  // the stream's cached blocks go back to the pool
+        cudaStreamSynchronize(stream);
+        cudaStreamDestroy(stream);
+        stream = nullptr;
     }
 }
 
