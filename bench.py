@@ -530,7 +530,7 @@ def _static_compare(gd, torch, wl, args, local, n, s, d, w, kind, us, ud, uw, pe
             "what": "apply batch + merge + static recompute from scratch (the reference bench's static column)"}
 
 
-KERNELS = ("pr_pull", "pr_contrib", "tc_bitmap", "merge_copy", "flood_sample", "flood_rest", "flood_mark", "del_scan",
+KERNELS = ("pr_pull", "pr_contrib", "tc_bitmap", "merge_copy", "flood_sample", "flood_rest", "flood_mark", "del_scan_head", "del_scan_tail",
            "add_vacancies", "tc_count", "sssp_relax", "sssp_walk", "sssp_pull", "sssp_parent")
 
 def _graph_stream(g):

@@ -49,6 +49,10 @@ void prof_tag(int idx, int64_t tag) {
     if (idx >= 0 && tl_prof) tl_prof->pending[(size_t)idx].tag = tag;
 }
 
+void prof_set_bytes(int idx, int64_t bytes) {
+    if (idx >= 0 && tl_prof) tl_prof->pending[(size_t)idx].bytes = bytes;
+}
+
 void prof_end(int idx, cudaStream_t s) {
     KernelProf* p = tl_prof;
     if (idx < 0 || !p) return;

@@ -62,6 +62,8 @@ int prof_begin(const char* name, int64_t bytes, cudaStream_t s);
 // when the sweep turned out to be a device no-op)
 void prof_tag(int idx, int64_t tag);
 void prof_end(int idx, cudaStream_t s);
+// algorithmic bytes of a recorded launch, when known only after it ran
+void prof_set_bytes(int idx, int64_t bytes);
 
 }  // namespace gdb
 

@@ -30,7 +30,7 @@ __global__ void k_pr_init(double* rank, int64_t n, double v) {
 // ctl[0..2] bin sizes, ctl[3..5] in-arcs per bin, ctl[6] done, ctl[7] sweeps.
 // Sweeps are enqueued ahead; once ctl[6] is set, the queued ones return at
 // their first instruction.
-enum { C_NBIN = 0, C_EBIN = 3, C_DONE = 6, C_SWEEPS = 7, C_WORK = 8, C_LEN = 9 };
+enum { C_NBIN = 0, C_EBIN = 3, C_DONE = 6, C_SWEEPS = 7, C_WORK = 8, C_WORK2 = 9, C_LEN = 10 };
 
 __global__ void __launch_bounds__(256) k_pr_contrib(const double* rank, const int32_t* outdeg, int64_t n,
                                                     double* contrib, double* partial, const int64_t* ctl) {
@@ -69,7 +69,10 @@ __global__ void k_sum_partials(const double* partial, int np, double* out, int64
     if (threadIdx.x == 0) {
         out[0] = sh[0];
         out[1] = 0.0;
-        if (ctl) ctl[C_WORK] = 0;  // the fused pull's work counter
+        if (ctl) {  // the fused pull's work counters
+            ctl[C_WORK] = 0;
+            ctl[C_WORK2] = 0;
+        }
     }
 }
 
@@ -81,13 +84,16 @@ __device__ inline double atomic_max_pos(double* a, double v) {  // v >= 0
 // incoming = sum(contrib[src]) over the in-arcs, new rank, |delta|.  Three
 // kernels by in-degree bin so lanes stay busy on a skewed (R-MAT) graph:
 // light rows (<= 32 in-arcs) get 8 lanes, medium rows (<= 4096) a warp, hub
-// rows a 512-thread block.  Every lane keeps 4 loads in flight (column ids
+// rows a 512-thread block.  Every lane keeps 8 loads in flight (column ids
 // first, then the contrib gathers) to cover L2 latency.  Reductions are in a
 // fixed order, so results are deterministic run to run.
 constexpr int kLightMax = 32;
 constexpr int kMediumMax = 4096;
 constexpr int kHubThreads = 512;
-constexpr int kILP = 4;
+#ifndef GD_PR_ILP
+#define GD_PR_ILP 8
+#endif
+constexpr int kILP = GD_PR_ILP;
 
 template <int G>
 __device__ inline double row_sum(const int32_t* __restrict__ col, int64_t a, int64_t b, int lane,
@@ -168,12 +174,24 @@ __global__ void __launch_bounds__(kHubThreads) k_pr_pull_hub(const int32_t* list
     }
 }
 
-// All three bins in one launch: CTAs take work units from one counter, hubs
-// first (a whole CTA per hub row), then 16 medium rows (16 lanes each), then
-// 128 light rows (2 lanes each).  The serial bin launches left the latency-
+// All three bins in one launch: CTAs take hub rows from one counter (a whole
+// CTA per hub row), then each warp takes units of 12 medium rows (16 lanes
+// each) or 96 light rows (2 lanes each) from a second one.  The serial bin launches left the latency-
 // bound hub tail and the L1-bound medium bin unoverlapped; here they share the
 // GPU.  Each row's sum keeps a fixed lane/order assignment: deterministic.
 constexpr int kFusedThreads = 256;
+#ifndef GD_PR_MED_UNIT
+#define GD_PR_MED_UNIT 12
+#endif
+#ifndef GD_PR_LIGHT_UNIT
+#define GD_PR_LIGHT_UNIT 96
+#endif
+#ifndef GD_PR_LG
+#define GD_PR_LG 2
+#endif
+constexpr int kMedUnit = GD_PR_MED_UNIT;
+constexpr int kLightUnit = GD_PR_LIGHT_UNIT;
+constexpr int kLG = GD_PR_LG;  // lanes per light row
 
 __global__ void __launch_bounds__(kFusedThreads) k_pr_pull_fused(const int32_t* light, const int32_t* med,
                                                                  const int32_t* hub, int64_t* ctl, IdxView ix,
@@ -184,56 +202,73 @@ __global__ void __launch_bounds__(kFusedThreads) k_pr_pull_fused(const int32_t* 
     __shared__ long long unit_s;
     __shared__ double red[kFusedThreads / 32];
     const int64_t nl = ctl[C_NBIN], nm = ctl[C_NBIN + 1], nh = ctl[C_NBIN + 2];
-    const int64_t uh = nh, um = (nm + 15) / 16, ul = (nl + 127) / 128, total = uh + um + ul;
     const double dn = *dangling * inv_n;
     const int tid = threadIdx.x, lane = tid & 31;
     double dmax = 0.0;
+    // phase 1: hub rows, a whole CTA each
     while (true) {
         if (tid == 0) unit_s = (long long)atomicAdd(reinterpret_cast<unsigned long long*>(&ctl[C_WORK]), 1ULL);
         __syncthreads();
         const int64_t u = unit_s;
         __syncthreads();
+        if (u >= nh) break;
+        int32_t v = hub[u];
+        double acc = row_sum<kFusedThreads>(ix.col, ix.off[v], ix.off[v + 1], tid, contrib);
+        for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) red[tid >> 5] = acc;
+        __syncthreads();
+        if (tid == 0) {
+            double sum = 0.0;
+            for (int w = 0; w < kFusedThreads / 32; ++w) sum += red[w];
+            double nr = base + damping * (sum + dn);
+            dmax = fmax(dmax, fabs(nr - rank[v]));
+            rank_new[v] = nr;
+        }
+        __syncthreads();
+    }
+    // phase 2: warps claim units on their own -- medium rows range from 33 to
+    // 4096 in-arcs, and a CTA-wide claim made 8 warps wait for the longest
+    // row at a barrier.  A unit is 12 medium rows (16 lanes each, 2 at a time)
+    // or 96 light rows (2 lanes each, 16 at a time).
+    const int64_t um = (nm + kMedUnit - 1) / kMedUnit, ul = (nl + kLightUnit - 1) / kLightUnit, total = um + ul;
+    while (true) {
+        unsigned long long w = 0;
+        if (lane == 0) w = atomicAdd(reinterpret_cast<unsigned long long*>(&ctl[C_WORK2]), 1ULL);
+        const int64_t u = (int64_t)__shfl_sync(0xffffffffu, w, 0);
         if (u >= total) break;
-        if (u < uh) {  // one hub row per CTA
-            int32_t v = hub[u];
-            double acc = row_sum<kFusedThreads>(ix.col, ix.off[v], ix.off[v + 1], tid, contrib);
-            for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-            if (lane == 0) red[tid >> 5] = acc;
-            __syncthreads();
-            if (tid == 0) {
-                double sum = 0.0;
-                for (int w = 0; w < kFusedThreads / 32; ++w) sum += red[w];
-                double nr = base + damping * (sum + dn);
-                dmax = fmax(dmax, fabs(nr - rank[v]));
-                rank_new[v] = nr;
-            }
-            __syncthreads();
-        } else if (u < uh + um) {  // 16 medium rows, 16 lanes each
-            const int64_t t = (u - uh) * 16 + (tid >> 4);
-            const int gl = tid & 15;
-            bool valid = t < nm;
-            int32_t v = valid ? med[t] : 0;
-            int64_t a = valid ? ix.off[v] : 0, b = valid ? ix.off[v + 1] : 0;
-            double acc = row_sum<16>(ix.col, a, b, gl, contrib);
+        if (u < um) {
+            const int gl = lane & 15;
+#pragma unroll 1
+            for (int r = 0; r < kMedUnit; r += 2) {
+                const int64_t t = u * kMedUnit + r + (lane >> 4);
+                bool valid = t < nm;
+                int32_t v = valid ? med[t] : 0;
+                int64_t a = valid ? ix.off[v] : 0, b = valid ? ix.off[v + 1] : 0;
+                double acc = row_sum<16>(ix.col, a, b, gl, contrib);
 #pragma unroll
-            for (int o = 8; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o, 16);
-            if (valid && gl == 0) {
-                double nr = base + damping * (acc + dn);
-                dmax = fmax(dmax, fabs(nr - rank[v]));
-                rank_new[v] = nr;
+                for (int o = 8; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o, 16);
+                if (valid && gl == 0) {
+                    double nr = base + damping * (acc + dn);
+                    dmax = fmax(dmax, fabs(nr - rank[v]));
+                    rank_new[v] = nr;
+                }
             }
-        } else {  // 128 light rows, 2 lanes each
-            const int64_t t = (u - uh - um) * 128 + (tid >> 1);
-            const int gl = tid & 1;
-            bool valid = t < nl;
-            int32_t v = valid ? light[t] : 0;
-            int64_t a = valid ? ix.off[v] : 0, b = valid ? ix.off[v + 1] : 0;
-            double acc = row_sum<2>(ix.col, a, b, gl, contrib);
-            acc += __shfl_xor_sync(0xffffffffu, acc, 1, 2);
-            if (valid && gl == 0) {
-                double nr = base + damping * (acc + dn);
-                dmax = fmax(dmax, fabs(nr - rank[v]));
-                rank_new[v] = nr;
+        } else {
+            const int gl = lane & (kLG - 1);
+#pragma unroll 1
+            for (int r = 0; r < kLightUnit; r += 32 / kLG) {
+                const int64_t t = (u - um) * kLightUnit + r + lane / kLG;
+                bool valid = t < nl;
+                int32_t v = valid ? light[t] : 0;
+                int64_t a = valid ? ix.off[v] : 0, b = valid ? ix.off[v + 1] : 0;
+                double acc = row_sum<kLG>(ix.col, a, b, gl, contrib);
+#pragma unroll
+                for (int o = kLG / 2; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o, kLG);
+                if (valid && gl == 0) {
+                    double nr = base + damping * (acc + dn);
+                    dmax = fmax(dmax, fabs(nr - rank[v]));
+                    rank_new[v] = nr;
+                }
             }
         }
     }

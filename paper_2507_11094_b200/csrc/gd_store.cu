@@ -160,8 +160,9 @@ constexpr int kScanWarps = 8;
 constexpr int kBitmapWords = 1024;  // 32 Kbit per warp (a filter: hits are confirmed by binary search)
 
 __global__ void k_row_chunks(OutView ov, const uint64_t* rq_key, const int32_t* row_first, const int64_t* d_nrows,
-                             int64_t cap, int sh, int64_t* chunks, unsigned long long* maxlen) {
-    unsigned long long mx = 0;
+                             int64_t cap, int sh, int64_t* chunks, unsigned long long* maxlen,
+                             unsigned long long* scanned) {
+    unsigned long long mx = 0, sh_head = 0, sh_tail = 0;
     const int64_t nrows = *d_nrows;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cap; i += (int64_t)gridDim.x * blockDim.x) {
         if (i >= nrows) {  // the tail of the scan input (no separate memset)
@@ -173,9 +174,19 @@ __global__ void k_row_chunks(OutView ov, const uint64_t* rq_key, const int32_t* 
         for (int sg = 0; sg < ov.nseg; ++sg) len += ov.off[sg][row + 1] - ov.off[sg][row];
         chunks[i] = len > kHead ? (len - kHead + kChunk - 1) / kChunk : 0;
         mx = max(mx, (unsigned long long)len);
+        sh_head += (unsigned long long)min(len, (int64_t)kHead);
+        sh_tail += (unsigned long long)max(len - (int64_t)kHead, (int64_t)0);
     }
-    for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    if ((threadIdx.x & 31) == 0 && mx) atomicMax(maxlen, mx);
+    for (int o = 16; o; o >>= 1) {
+        mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        sh_head += __shfl_xor_sync(0xffffffffu, sh_head, o);
+        sh_tail += __shfl_xor_sync(0xffffffffu, sh_tail, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (mx) atomicMax(maxlen, mx);
+        if (sh_head) atomicAdd(&scanned[0], sh_head);  // chain slots the head / tail kernels read
+        if (sh_tail) atomicAdd(&scanned[1], sh_tail);
+    }
 }
 
 __global__ void k_widen(const int32_t* a, int64_t m, uint64_t* o) {
@@ -1146,13 +1157,15 @@ int64_t Store::apply_deletes(const int32_t* d_src, const int32_t* d_dst, int64_t
     DBuf<uint8_t> rflag(nrq, s);
     GD_KERNEL(k_row_starts, grid_for(nrq, 256), 256, 0, s, rq_key.get(), nrq, sh, rflag.get());
     DBuf<int32_t> row_first(nrq, s);
-    DBuf<int64_t> hdr(4, s);  // nrows, work items, longest chain, overflow matches
-    GD_CUDA(cudaMemsetAsync(hdr.get(), 0, 4 * sizeof(int64_t), s));
+    // nrows, work items, longest chain, overflow matches, head / tail slots scanned
+    DBuf<int64_t> hdr(6, s);
+    GD_CUDA(cudaMemsetAsync(hdr.get(), 0, 6 * sizeof(int64_t), s));
     select_flagged_index_async(s, rflag.get(), nrq, row_first.get(), hdr.get());
     OutView ov = out_view();
     DBuf<int64_t> chunks(nrq + 1, s), coff(nrq + 1, s);
     GD_KERNEL(k_row_chunks, grid_for(nrq + 1, 256), 256, 0, s, ov, rq_key.get(), row_first.get(), hdr.get(), nrq + 1,
-              sh, chunks.get(), reinterpret_cast<unsigned long long*>(hdr.get() + 2));
+              sh, chunks.get(), reinterpret_cast<unsigned long long*>(hdr.get() + 2),
+              reinterpret_cast<unsigned long long*>(hdr.get() + 4));
     exclusive_scan_i64(s, chunks.get(), coff.get(), nrq + 1);
     GD_CUDA(cudaMemcpyAsync(hdr.get() + 1, coff.get() + nrq, 8, cudaMemcpyDeviceToDevice, s));
     // tail pieces: at most one per kChunk slots of the requested rows
@@ -1180,14 +1193,26 @@ int64_t Store::apply_deletes(const int32_t* d_src, const int32_t* d_dst, int64_t
         }
         MatchOut mo{sel.get(), single.get(), m_key.get(), m_chain.get(), m_gid.get(),
                     reinterpret_cast<unsigned long long*>(hdr.get() + 3), cap};
-        GD_KERNEL_T("del_scan", 0, k_del_scan_head, grid_for(((nrq + 3) / 4) * 32, 256, 148LL * 32), 256, 0, s, ov,
-                    row_first.get(), hdr.get(), rq_key.get(), nrq, sh, mo);
-        GD_KERNEL_T("del_scan", 0, k_del_scan_tail, 148 * 16, kScanWarps * 32, 0, s, ov, row_first.get(),
-                    coff.get(), wrow.get(), hdr.get(), rq_key.get(), nrq, sh, mo);
-        int64_t h2[2];
-        read_small(s, h2, hdr.get() + 2, sizeof h2);
-        maxchain = h2[0];
-        nm = h2[1];
+        const int ph = prof_begin("del_scan_head", 0, s);
+        k_del_scan_head<<<grid_for(((nrq + 3) / 4) * 32, 256, 148LL * 32), 256, 0, s>>>(ov, row_first.get(), hdr.get(),
+                                                                                    rq_key.get(), nrq, sh, mo);
+        count_launch();
+        GD_LAUNCH_CHECK();
+        prof_end(ph, s);
+        const int pt = prof_begin("del_scan_tail", 0, s);
+        k_del_scan_tail<<<148 * 16, kScanWarps * 32, 0, s>>>(ov, row_first.get(), coff.get(), wrow.get(), hdr.get(),
+                                                             rq_key.get(), nrq, sh, mo);
+        count_launch();
+        GD_LAUNCH_CHECK();
+        prof_end(pt, s);
+        int64_t h6[6];
+        read_small(s, h6, hdr.get(), sizeof h6);
+        maxchain = h6[2];
+        nm = h6[3];
+        // algorithmic bytes: the chain slots each kernel reads
+        // (idx), the request keys, and the row offsets of every segment
+        prof_set_bytes(ph, 4 * h6[4] + 8 * nrq + 16 * (int64_t)ov.nseg * h6[0]);
+        prof_set_bytes(pt, 4 * h6[5] + 8 * h6[1]);
         if (nm <= cap) break;
         cap = nm;
     }

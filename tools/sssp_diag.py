@@ -32,6 +32,6 @@ for i in range(nb):
     h.batch_device(dk.data_ptr() + a, ds.data_ptr() + 4 * a, dd.data_ptr() + 4 * a, dw.data_ptr() + 4 * a, b - a, i)
     torch.cuda.synchronize()
     el = time.perf_counter() - t
-    ks = {k: h.kernel_time(k) for k in ("sssp_walk", "sssp_pull", "sssp_relax", "sssp_parent", "del_scan", "merge_copy")}
+    ks = {k: h.kernel_time(k) for k in ("sssp_walk", "sssp_pull", "sssp_relax", "sssp_parent", "del_scan_head", "del_scan_tail", "merge_copy")}
     print(f"batch {i}: {el*1e3:.2f} ms rounds={h.iterations()-it0} phases={ {k: round(v, 3) for k, v in h.phase_ms().items()} }")
     print("   ", {k: round(v[0], 3) for k, v in ks.items() if v[1]})

@@ -59,7 +59,7 @@ with open(os.path.join(out, "ncu_full_summary.csv"), "w", newline="") as fh:
         rd = float(row[h.index("dram__bytes_read.sum")]) * scale[units[h.index("dram__bytes_read.sum")]]
         wr = float(row[h.index("dram__bytes_write.sum")]) * scale[units[h.index("dram__bytes_write.sum")]]
         key = ("pr_pull" if "k_pr_pull" in name else "merge_copy" if "k_edit_base" in name else
-               "del_scan" if "k_del_scan" in name else "pr_contrib" if "k_pr_contrib" in name else
+               "del_scan_head" if "k_del_scan_head" in name else "del_scan_tail" if "k_del_scan_tail" in name else "pr_contrib" if "k_pr_contrib" in name else
                "flood_sample" if "k_aff_sample" in name else name)
         traffic[key].append(rd + wr)
 json.dump({k: sum(v) / len(v) for k, v in traffic.items()}, open(os.path.join("profiles", "ncu_traffic.json"), "w"),
