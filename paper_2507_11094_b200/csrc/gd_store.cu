@@ -231,12 +231,11 @@ __device__ inline void emit_matches(const MatchOut& mo, int64_t p, int32_t row, 
 
 // index of the first request for (row, c), or -1
 __device__ inline int64_t requested(const uint64_t* rq_key, int64_t lo, int64_t hi, int32_t row, int32_t c, int sh,
-                                    int32_t c0, int32_t c1, const uint32_t* bm, uint64_t filt = ~0ULL) {
+                                    int32_t c0, int32_t c1, const uint32_t* bm, uint32_t bmask) {
     if (c < 0) return -1;
     if (hi - lo <= 2) return c == c0 ? lo : (c == c1 ? lo + 1 : -1);
-    if (!((filt >> (c & 63)) & 1)) return -1;
     if (bm) {
-        uint32_t h = (uint32_t)c & (kBitmapWords * 32 - 1);
+        uint32_t h = (uint32_t)c & bmask;
         if (!(bm[h >> 5] & (1u << (h & 31)))) return -1;
     }
     uint64_t want = pair_key(row, c, sh);
@@ -245,11 +244,15 @@ __device__ inline int64_t requested(const uint64_t* rq_key, int64_t lo, int64_t 
 }
 
 // head: one 8-lane group per requested row, chain slots [0, kHead)
+constexpr int kHeadWords = 32;  // a 1024-bit request filter per group (shared memory)
+
 __global__ void __launch_bounds__(256, 4) k_del_scan_head(OutView ov, const int32_t* row_first, const int64_t* d_nrows,
                                                        const uint64_t* rq_key, int64_t nrq, int sh, MatchOut mo) {
     constexpr int G = 8, kPer = 32 / G;
+    __shared__ uint32_t hbm[256 / G][kHeadWords];
     const int64_t nrows = *d_nrows;
     const int gl = threadIdx.x & (G - 1), gw = (threadIdx.x & 31) / G;
+    uint32_t* gbm = hbm[threadIdx.x / G];
     int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t t0 = warp * kPer; t0 < nrows; t0 += nwarps * kPer) {
@@ -260,13 +263,21 @@ __global__ void __launch_bounds__(256, 4) k_del_scan_head(OutView ov, const int3
         int32_t row = valid ? key_row(rq_key[lo], sh) : 0;
         int32_t c0 = valid ? key_col(rq_key[lo], sh) : -2;
         int32_t c1 = (valid && hi - lo > 1) ? key_col(rq_key[lo + 1], sh) : -2;
-        // rows with more requests: a 64-bit filter of the requested columns
-        // (c & 63) keeps most slots off the binary search
-        uint64_t filt = 0;
-        if (valid && hi - lo > 2)
-            for (int64_t e = lo + gl; e < hi; e += G) filt |= 1ULL << (key_col(rq_key[e], sh) & 63);
-#pragma unroll
-        for (int o = 1; o < G; o <<= 1) filt |= __shfl_xor_sync(0xffffffffu, filt, o, G);
+        // rows with more requests: a 1024-bit filter of the requested columns
+        // keeps most slots off the binary search (R-MAT hubs draw dozens of
+        // requests, which saturated the 64-bit register filter used before)
+        const bool many = valid && hi - lo > 2;
+        __syncwarp();  // the group's previous row is done with the filter
+        if (many)
+            for (int q = gl; q < kHeadWords; q += G) gbm[q] = 0;
+        __syncwarp();
+        if (many)
+            for (int64_t e = lo + gl; e < hi; e += G) {
+                uint32_t c = (uint32_t)key_col(rq_key[e], sh) & (kHeadWords * 32 - 1);
+                atomicOr(&gbm[c >> 5], 1u << (c & 31));
+            }
+        __syncwarp();
+        const uint32_t* fbm = many ? gbm : nullptr;
         int64_t acc = 0;
         for (int sg = 0; sg < ov.nseg; ++sg) {  // nseg is uniform: the loop stays warp-uniform
             int64_t a = valid ? ov.off[sg][row] : 0;
@@ -286,7 +297,7 @@ __global__ void __launch_bounds__(256, 4) k_del_scan_head(OutView ov, const int3
                 bool any = false;
 #pragma unroll
                 for (int u = 0; u < kScanILP; ++u) {
-                    hp[u] = requested(rq_key, lo, hi, row, cv[u], sh, c0, c1, nullptr, filt);
+                    hp[u] = requested(rq_key, lo, hi, row, cv[u], sh, c0, c1, fbm, kHeadWords * 32 - 1);
                     any |= hp[u] >= 0;
                 }
                 if (__any_sync(0xffffffffu, any)) {  // hits are rare: one vote per ILP batch
@@ -362,7 +373,8 @@ __global__ void __launch_bounds__(kScanWarps * 32, 4) k_del_scan_tail(OutView ov
                 bool any = false;
 #pragma unroll
                 for (int u = 0; u < kScanILP; ++u) {
-                    hp[u] = requested(rq_key, lo, hi, row, cv[u], sh, c0, c1, use_bm ? bm : nullptr);
+                    hp[u] = requested(rq_key, lo, hi, row, cv[u], sh, c0, c1, use_bm ? bm : nullptr,
+                                      kBitmapWords * 32 - 1);
                     any |= hp[u] >= 0;
                 }
                 if (__any_sync(0xffffffffu, any)) {

@@ -6,7 +6,7 @@ show() {
   python -c "
 import json,sys
 j=json.loads(sys.stdin.read()); k=j['kernels']; s=j['steps']
-print('$1', round(j['ms_per_step'],3), round(j['e2e']['ms_per_step'],3), ' '.join(f'{n}={v[\"ms_total\"]/s:.3f}' for n,v in list(k.items())[:8]))"
+print('$1', round(j['ms_per_step'],3), round(j['e2e']['ms_per_step'],3), ' '.join(f'{n}={v[\"ms_total\"]/s:.3f}' for n,v in list(k.items())[:6]))"
 }
 for i in 1 2 3; do
   timeout 600 python bench.py --no-cpu-baseline --steps 20 ${BENCH_ARGS} 2>/dev/null | show B
