@@ -450,7 +450,7 @@ def main():
         avg_ms = ms / nl
         ach = (b_per_launch / 1e9) / (avg_ms / 1e3) if b_per_launch else None
         roof = {"bound": "hbm", "kernel": name, "achieved": ach, "peak": peak, "unit": "GB/s",
-                "frac": (ach / peak) if ach else None, "traffic": _ncu_traffic(name),
+                "frac": (ach / peak) if ach else None, "traffic": _ncu_traffic(args.workload, name),
                 "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured" else
                 "fallback 6.65 TB/s (B200_PROFILING.md)",
                 "bytes_per_launch": b_per_launch, "avg_launch_ms": avg_ms, "launches": nl,
@@ -572,11 +572,14 @@ def _read_result(gd, algo, wl, out_pin, n):
     return 8
 
 
-def _ncu_traffic(name):
+def _ncu_traffic(workload, name):
+    """Per-launch DRAM bytes of `name` from the committed `ncu --set full`
+    capture of this workload (tools/summarize_profiles.py), else None."""
     p = os.path.join(REPO, "profiles", "ncu_traffic.json")
     try:
         with open(p) as fh:
-            return json.load(fh).get(name)
+            t = json.load(fh)
+        return t.get(f"{workload}/{name}", t.get(name) if workload == "pr" else None)
     except Exception:
         return None
 
