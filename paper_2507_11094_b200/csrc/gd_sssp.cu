@@ -108,6 +108,9 @@ struct FpArgs {
     int64_t* hi[2];  // in-pull pieces (PULL)
     unsigned long long* cnt;  // [9]
     long long* ctr;           // [6]
+    // algorithmic bytes of this launch (profiling only, else null): every
+    // thread sums its own loads and adds them once at exit
+    long long* acc;
     int64_t cap;
     // near-far (RELAX, delta > 0): relaxations landing at >= theta wait in a
     // far pile (3 rotating buffers, counters fcnt/fmin) until the near queue
@@ -193,10 +196,14 @@ __device__ __forceinline__ void out_act(const FpArgs& a, const Round& r, int32_t
 // arcs [e0, e1) of segment sg, lanes strided by W, 4 arcs in flight per lane
 template <int MODE, int W>
 __device__ __forceinline__ void out_scan(const FpArgs& a, const Round& r, int32_t v, int64_t dv, int sg, int64_t e0,
-                                         int64_t e1, int lane) {
+                                         int64_t e1, int lane, int64_t& nb) {
     const int32_t* col = a.ov.col[sg];
     const int32_t* wt = MODE == FP_RELAX ? a.ov.w[sg] : nullptr;
+    // per slot: col, then weight + dist (relax), parent (walk) or flag (pull)
+    // (tombstoned slots counted in full: an upper bound of <= 2x on them)
+    const int64_t ba = 4 + (MODE == FP_RELAX ? (wt ? 12 : 8) : MODE == FP_WALK ? 4 : 1);
     int64_t e = e0 + lane;
+    if (e < e1) nb += ba * ((e1 - e + W - 1) / W);
     for (; e + 3 * W < e1; e += 4 * W) {
         int32_t t[4], w[4];
         int64_t pre[4];
@@ -219,14 +226,16 @@ __device__ __forceinline__ void out_scan(const FpArgs& a, const Round& r, int32_
 // visit v's out-arcs with a converged group of W lanes: inline when short,
 // else (once per round per vertex) as pieces for the next round
 template <int MODE, int W>
-__device__ __forceinline__ void out_visit(const FpArgs& a, const Round& r, int32_t v, int64_t dv, int lane) {
+__device__ __forceinline__ void out_visit(const FpArgs& a, const Round& r, int32_t v, int64_t dv, int lane,
+                                          int64_t& nb) {
     const unsigned gm = group_mask<W>();
     const int leader = (threadIdx.x & 31) & ~(W - 1);
     int64_t deg = 0;
     for (int sg = 0; sg < a.ov.nseg; ++sg) deg += a.ov.off[sg][v + 1] - a.ov.off[sg][v];
+    if (lane == 0) nb += 16 * a.ov.nseg;
     if (deg <= kHeavy) {
         for (int sg = 0; sg < a.ov.nseg; ++sg)
-            out_scan<MODE, W>(a, r, v, dv, sg, a.ov.off[sg][v], a.ov.off[sg][v + 1], lane);
+            out_scan<MODE, W>(a, r, v, dv, sg, a.ov.off[sg][v], a.ov.off[sg][v + 1], lane, nb);
         return;
     }
     int64_t np = 0;
@@ -239,15 +248,17 @@ __device__ __forceinline__ void out_visit(const FpArgs& a, const Round& r, int32
     for (int sg = 0; sg < a.ov.nseg; ++sg) {
         int64_t ns = (a.ov.off[sg][v + 1] - a.ov.off[sg][v] + kPiece - 1) / kPiece;
         for (int64_t k = lane; k < ns; k += W) r.hoout[base + k] = piece_key(v, sg, k);
+        if (lane == 0) nb += 8 * ns;
         base += ns;
     }
 }
 
 // min over in-arcs [e0, e1) of sat(dist[u] + w), lanes strided by W
 template <int W>
-__device__ __forceinline__ int64_t in_min(const FpArgs& a, int64_t e0, int64_t e1, int lane) {
+__device__ __forceinline__ int64_t in_min(const FpArgs& a, int64_t e0, int64_t e1, int lane, int64_t& nb) {
     int64_t best = kInf;
     int64_t e = e0 + lane;
+    if (e < e1) nb += (a.ix.w ? 16 : 12) * ((e1 - e + W - 1) / W);  // per slot: col, weight, dist[u]
     for (; e + 3 * W < e1; e += 4 * W) {
         int32_t u[4];
         int64_t c[4];
@@ -287,7 +298,8 @@ __device__ __forceinline__ bool lower(const FpArgs& a, int32_t v, int64_t best, 
 
 template <int MODE>
 __device__ __forceinline__ void fp_round(const FpArgs& a, const Round& r, const int32_t* qin, int64_t m,
-                                         const int64_t* hoin, int64_t mo, const int64_t* hiin, int64_t mi) {
+                                         const int64_t* hoin, int64_t mo, const int64_t* hiin, int64_t mi,
+                                         int64_t& nb) {
     const int wl = threadIdx.x & 31;
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -300,7 +312,8 @@ __device__ __forceinline__ void fp_round(const FpArgs& a, const Round& r, const 
         int64_t s0 = a.ov.off[sg][v], s1 = a.ov.off[sg][v + 1];
         int64_t e0 = s0 + k * kPiece, e1 = min(e0 + kPiece, s1);
         int64_t dv = MODE == FP_RELAX ? a.dist[v] : 0;
-        if (MODE != FP_RELAX || dv < kInf) out_scan<MODE, 32>(a, r, v, dv, sg, e0, e1, wl);
+        if (wl == 0) nb += 8 + 16 + (MODE == FP_RELAX ? 8 : 0);  // key, offsets, dist[v]
+        if (MODE != FP_RELAX || dv < kInf) out_scan<MODE, 32>(a, r, v, dv, sg, e0, e1, wl, nb);
     }
     if (MODE == FP_PULL) {
         for (int64_t p = warp; p < mi; p += nwarps) {
@@ -310,8 +323,9 @@ __device__ __forceinline__ void fp_round(const FpArgs& a, const Round& r, const 
             piece_decode(hiin[p], v, sg, k);
             int64_t s0 = a.ix.off[v], s1 = a.ix.off[v + 1];
             int64_t e0 = s0 + k * kPiece, e1 = min(e0 + kPiece, s1);
-            int64_t best = in_min<32>(a, e0, e1, wl);
-            if (lower<32>(a, v, best, wl)) out_visit<MODE, 32>(a, r, v, 0, wl);
+            if (wl == 0) nb += 8 + 16 + 8;  // key, offsets, dist[v]
+            int64_t best = in_min<32>(a, e0, e1, wl, nb);
+            if (lower<32>(a, v, best, wl)) out_visit<MODE, 32>(a, r, v, 0, wl, nb);
         }
     }
     // the queue: one group of kG lanes per vertex
@@ -319,13 +333,15 @@ __device__ __forceinline__ void fp_round(const FpArgs& a, const Round& r, const 
     (void)gw;
     if (valid) {
         int32_t v = qin[_t];
+        if (lane == 0) nb += 4 + (MODE == FP_RELAX ? 8 : 0);  // queue entry, dist[v]
         if (MODE == FP_RELAX) {
             int64_t dv = a.dist[v];
-            if (dv < kInf) out_visit<MODE, kG>(a, r, v, dv, lane);
+            if (dv < kInf) out_visit<MODE, kG>(a, r, v, dv, lane, nb);
         } else if (MODE == FP_WALK) {
-            out_visit<MODE, kG>(a, r, v, 0, lane);
+            out_visit<MODE, kG>(a, r, v, 0, lane, nb);
         } else {
             int64_t s0 = a.ix.off[v], s1 = a.ix.off[v + 1];
+            if (lane == 0) nb += 16 + 8;  // in-offsets, dist[v]
             if (s1 - s0 > kHeavy) {
                 int64_t np = (s1 - s0 + kPiece - 1) / kPiece;
                 unsigned long long base = 0;
@@ -333,8 +349,8 @@ __device__ __forceinline__ void fp_round(const FpArgs& a, const Round& r, const 
                 base = __shfl_sync(group_mask<kG>(), base, (threadIdx.x & 31) & ~(kG - 1));
                 for (int64_t k = lane; k < np; k += kG) r.hiout[base + k] = piece_key(v, 0, k);
             } else {
-                int64_t best = in_min<kG>(a, s0, s1, lane);
-                if (lower<kG>(a, v, best, lane)) out_visit<MODE, kG>(a, r, v, 0, lane);
+                int64_t best = in_min<kG>(a, s0, s1, lane, nb);
+                if (lower<kG>(a, v, best, lane)) out_visit<MODE, kG>(a, r, v, 0, lane, nb);
             }
         }
     }
@@ -343,9 +359,11 @@ __device__ __forceinline__ void fp_round(const FpArgs& a, const Round& r, const 
 
 // near-far split: pile entries below theta join the queue, the rest move to
 // the next pile
-__device__ __forceinline__ void split_round(const FpArgs& a, const Round& r, const int32_t* src, int64_t F) {
+__device__ __forceinline__ void split_round(const FpArgs& a, const Round& r, const int32_t* src, int64_t F,
+                                            int64_t& nb) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < F; i += (int64_t)gridDim.x * blockDim.x) {
         int32_t v = src[i];
+        nb += 4 + 8;  // pile entry, dist[v]
         int64_t d = a.dist[v];
         if (d == kInf) {  // unreached seed: re-enters when relaxed
             a.infar[v] = 0;
@@ -361,7 +379,7 @@ __device__ __forceinline__ void split_round(const FpArgs& a, const Round& r, con
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(kThreads) k_fixpoint(FpArgs a) {
+__global__ void __launch_bounds__(kThreads, 4) k_fixpoint(FpArgs a) {
     cg::grid_group grid = cg::this_grid();
     const bool leader = grid.thread_rank() == 0;
     const int32_t round0 = (int32_t)a.ctr[0];
@@ -369,6 +387,7 @@ __global__ void __launch_bounds__(kThreads) k_fixpoint(FpArgs a) {
     int64_t theta = kInf;  // every relaxation is near unless near-far
     if (nf) theta = 0;
     int nsplit = 0;  // pile = far[nsplit % 3]
+    int64_t nb = 0;  // this thread's algorithmic bytes (a.acc only)
     int64_t it = 0;
     for (;; ++it) {
         const volatile unsigned long long* c = a.cnt + 3 * (it % 3);
@@ -410,8 +429,8 @@ __global__ void __launch_bounds__(kThreads) k_fixpoint(FpArgs a) {
         const int fo = split ? (p + 1) % 3 : p;
         Round r{round0 + (int32_t)it + 1, theta, a.far[fo], a.fcnt + fo, a.fmin + fo,
                 a.q[nx], cn, a.ho[nx], cn + 1, a.hi[nx], cn + 2};
-        if (split) split_round(a, r, it == 0 ? a.seeds : a.far[p], F);
-        else fp_round<MODE>(a, r, it == 0 ? a.seeds : a.q[it & 1], m, a.ho[it & 1], mo, a.hi[it & 1], mi);
+        if (split) split_round(a, r, it == 0 ? a.seeds : a.far[p], F, nb);
+        else fp_round<MODE>(a, r, it == 0 ? a.seeds : a.q[it & 1], m, a.ho[it & 1], mo, a.hi[it & 1], mi, nb);
         grid.sync();
         if (split) ++nsplit;
     }
@@ -419,6 +438,11 @@ __global__ void __launch_bounds__(kThreads) k_fixpoint(FpArgs a) {
     if (leader && it > 0) {
         a.ctr[0] = round0 + it;
         a.ctr[1] += it;
+    }
+    if (a.acc) {
+        for (int o = 16; o; o >>= 1) nb += __shfl_xor_sync(0xffffffffu, nb, o);
+        if ((threadIdx.x & 31) == 0 && nb) atomicAdd(reinterpret_cast<unsigned long long*>(a.acc),
+                                                     (unsigned long long)nb);
     }
 }
 
@@ -441,7 +465,8 @@ __global__ void __launch_bounds__(kThreads) k_pull_once(const int32_t* list, con
         if (s1 - s0 > kHeavy) {
             if (lane == 0) heavy[atomicAdd(nheavy, 1ULL)] = v;
         } else {
-            int64_t best = in_min<kG>(a, s0, s1, lane);
+            int64_t nb = 0;  // unused here
+            int64_t best = in_min<kG>(a, s0, s1, lane, nb);
             if (lane == 0 && best < dist[v]) atomicMin(reinterpret_cast<long long*>(&dist[v]), (long long)best);
         }
     }
@@ -628,7 +653,7 @@ SSSP::SSSP(Store* st, int64_t s) : AlgoBase(ALGO_SSSP, st), src((int32_t)s) {
     fa.alloc(n, cs);
     fb.alloc(n, cs);
     fr.init(n, cs);
-    ctr.alloc(6, cs);
+    ctr.alloc(6 + kFpSlots, cs);
     fcnt.alloc(3, cs);
     fmin.alloc(3, cs);
     infar.alloc(n, cs);
@@ -708,6 +733,13 @@ void SSSP::fixpoint(int mode, const int32_t* seeds, const int64_t* d_nseeds, int
     unsigned grid = mode == FP_RELAX ? coop_grid<FP_RELAX>() : mode == FP_WALK ? coop_grid<FP_WALK>()
                                                                                : coop_grid<FP_PULL>();
     int pi = prof_begin(names[mode], 0, s);
+    // profiled launches sum their algorithmic bytes into a slot that
+    // finish() reads with the round counters (no extra read-back)
+    a.acc = nullptr;
+    if (pi >= 0 && nfp < kFpSlots) {
+        a.acc = ctr.get() + 6 + nfp;
+        fp_prof[nfp++] = pi;
+    }
     GD_CUDA(cudaLaunchCooperativeKernel(fn, grid, kThreads, args, 0, s));
     count_launch();
     prof_end(pi, s);
@@ -728,8 +760,13 @@ void SSSP::fix_parents(const int32_t* list, const int64_t* d_m, int64_t m) {
 
 // one read-back per batch: total rounds and the divergence flag
 void SSSP::finish() {
-    long long h[6];
-    read_small(stream(), h, ctr.get(), sizeof(h));
+    long long h[6 + kFpSlots];
+    read_small(stream(), h, ctr.get(), (6 + nfp) * sizeof(long long));
+    if (nfp) {
+        for (int j = 0; j < nfp; ++j) prof_set_bytes(fp_prof[j], h[6 + j]);
+        GD_CUDA(cudaMemsetAsync(ctr.get() + 6, 0, nfp * sizeof(long long), stream()));
+        nfp = 0;
+    }
     static const bool dbg = getenv("GD_SSSP_DEBUG") != nullptr;
     if (dbg)
         fprintf(stderr, "[sssp] rounds %lld (+%lld) visits %lld pieces %lld splits %lld\n", h[1], h[1] - iterations,

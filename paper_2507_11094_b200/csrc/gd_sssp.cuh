@@ -15,7 +15,12 @@ struct SSSP : AlgoBase {
     DBuf<int64_t> ho[2], hi[2];  // hub pieces (out-scans, in-pulls), double-buffered
     DBuf<uint8_t> fa, fb;     // per-node flags (stale / touched / seeds)
     Frontier fr;
-    DBuf<long long> ctr;   // [last stamp round, total rounds, diverged, visits, pieces, splits]
+    // [last stamp round, total rounds, diverged, visits, pieces, splits,
+    //  kFpSlots x algorithmic bytes of the profiled fixpoint launches]
+    DBuf<long long> ctr;
+    static constexpr int kFpSlots = 8;
+    int nfp = 0;               // profiled fixpoint launches since finish()
+    int fp_prof[kFpSlots];     // their profiler record indices
     int64_t delta = 0;     // near-far bucket width for RELAX (0 = plain frontier)
     DBuf<int32_t> far[3];  // near-far piles
     DBuf<unsigned long long> fcnt;

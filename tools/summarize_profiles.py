@@ -56,7 +56,7 @@ def full_summary(tag, rep):
       w = csv.writer(fh)
       w.writerow([h[i] + (f" [{units[i]}]" if units[i] else "") for i in idx])
       for row in d:
-          dur = float(row[h.index("gpu__time_duration.sum")]) * {"usecond": 1, "msecond": 1e3, "nsecond": 1e-3}.get(
+          dur = float(row[h.index("gpu__time_duration.sum")]) * {"usecond": 1, "us": 1, "msecond": 1e3, "ms": 1e3, "nsecond": 1e-3, "ns": 1e-3}.get(
               units[h.index("gpu__time_duration.sum")], 1)
           if dur < 10:  # a queued PR sweep that the device turned into a no-op
               continue
