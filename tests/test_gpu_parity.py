@@ -322,3 +322,33 @@ def test_async_reads_snapshot_the_state_at_the_call(gd):
         np.testing.assert_array_equal(d_out, d_want)
         np.testing.assert_array_equal(p_out, p_want)
         np.testing.assert_array_equal(r_out, r_want)
+
+
+def test_sssp_fixpoints_count_their_bytes(gd):
+    """Profiled fixpoint launches report algorithmic bytes (DESIGN.md §3,
+    k_fixpoint row); profiling does not change the results."""
+    from paper_2507_11094_b200.updates import RecordArrays
+    from oracle import oracle as O
+
+    n = 64
+    src = np.arange(n - 1, dtype=np.int64)  # a chain 0 -> 1 -> ... -> 63
+    dst = src + 1
+    w = np.full(n - 1, 3, dtype=np.int64)
+    g = gd.DynamicGraph.from_arrays(n, src, dst, w, weighted=True, with_reverse=True, merge_interval=1)
+    h = gd.SSSPHandle(g, 0)
+    h.set_profiling(True)
+    kind = np.array([ord("d"), ord("a")], dtype=np.uint8)
+    us, ud, uw = np.array([0, 0]), np.array([1, 40]), np.array([1, 5])
+    h.batch(RecordArrays(kind, us, ud, uw), 0)
+    ms, nl, b = h.kernel_time("sssp_walk")
+    assert nl == 1
+    # the walk visits the 63 invalidated vertices 1..63: at least a queue
+    # entry and one offset pair each, and 62 of them scan one slot (col + parent)
+    assert b >= 63 * (4 + 16) + 62 * 8
+    ms, nl, b = h.kernel_time("sssp_relax")
+    assert nl >= 1 and b > 0
+    og = O.OracleGraph(n, src, dst, w, weighted=True, with_reverse=True, merge_interval=1)
+    dist, parent = O.OracleSSSP(og, 0).run_stream(kind, us, ud, uw, 2).read()
+    got_d, got_p = h.read()
+    np.testing.assert_array_equal(got_d, dist)
+    np.testing.assert_array_equal(got_p, parent)
