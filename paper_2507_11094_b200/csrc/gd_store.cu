@@ -738,8 +738,11 @@ __device__ __forceinline__ void edit_window(const int32_t* __restrict__ col, con
     }
 }
 
+// 5 resident CTAs (48 registers) for the unweighted copy: more loads in
+// flight per SM, 0.280 -> 0.255 ms per C2 merge, 2.31 -> 2.13 ms on C3
+// (A/B, gpu_variants.sh).  The weighted copy keeps 4: at 48 it spills.
 template <bool WEIGHTED>
-__global__ void __launch_bounds__(kEditThreads) k_edit_base(const int32_t* __restrict__ col,
+__global__ void __launch_bounds__(kEditThreads, WEIGHTED ? 4 : 5) k_edit_base(const int32_t* __restrict__ col,
                                                             const int32_t* __restrict__ w, int64_t nnz,
                                                             const int64_t* __restrict__ dead_win,
                                                             const int64_t* __restrict__ ipos,
