@@ -215,7 +215,10 @@ __global__ void __launch_bounds__(kThreads) k_tc_count(const int32_t* s, const i
 constexpr int kShortWalk = 64;
 constexpr int kShortG = 8;
 
-__global__ void __launch_bounds__(kThreads) k_tc_count_short(const int32_t* s, const int32_t* d, TcRec r,
+#ifndef GD_TCS_MINB
+#define GD_TCS_MINB 1
+#endif
+__global__ void __launch_bounds__(kThreads, GD_TCS_MINB) k_tc_count_short(const int32_t* s, const int32_t* d, TcRec r,
                                                              const int32_t* list, const int64_t* nlist, IdxView ix,
                                                              int64_t n, const int64_t* R, int64_t nr,
                                                              const int32_t* slot, const uint32_t* bm, int64_t words,
