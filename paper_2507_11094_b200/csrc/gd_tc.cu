@@ -215,8 +215,11 @@ __global__ void __launch_bounds__(kThreads) k_tc_count(const int32_t* s, const i
 constexpr int kShortWalk = 64;
 constexpr int kShortG = 8;
 
+// 8 resident CTAs (32 registers, a 40-byte spill): the random neighbour
+// lookups want warps in flight more than registers; C3 tc_count 1.10 ->
+// 0.88 ms per batch (A/B, gpu_variants.sh)
 #ifndef GD_TCS_MINB
-#define GD_TCS_MINB 1
+#define GD_TCS_MINB 8
 #endif
 __global__ void __launch_bounds__(kThreads, GD_TCS_MINB) k_tc_count_short(const int32_t* s, const int32_t* d, TcRec r,
                                                              const int32_t* list, const int64_t* nlist, IdxView ix,
