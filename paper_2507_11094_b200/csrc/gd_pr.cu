@@ -193,7 +193,12 @@ constexpr int kMedUnit = GD_PR_MED_UNIT;
 constexpr int kLightUnit = GD_PR_LIGHT_UNIT;
 constexpr int kLG = GD_PR_LG;  // lanes per light row
 
-__global__ void __launch_bounds__(kFusedThreads) k_pr_pull_fused(const int32_t* light, const int32_t* med,
+#ifdef GD_PULL_MINB
+__global__ void __launch_bounds__(kFusedThreads, GD_PULL_MINB) k_pr_pull_fused(
+#else
+__global__ void __launch_bounds__(kFusedThreads) k_pr_pull_fused(
+#endif
+const int32_t* light, const int32_t* med,
                                                                  const int32_t* hub, int64_t* ctl, IdxView ix,
                                                                  const double* contrib, const double* rank,
                                                                  const double* dangling, double base, double damping,
