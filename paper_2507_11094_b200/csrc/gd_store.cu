@@ -246,7 +246,10 @@ __device__ inline int64_t requested(const uint64_t* rq_key, int64_t lo, int64_t 
 // head: one 8-lane group per requested row, chain slots [0, kHead)
 constexpr int kHeadWords = 32;  // a 1024-bit request filter per group (shared memory)
 
-__global__ void __launch_bounds__(256, 4) k_del_scan_head(OutView ov, const int32_t* row_first, const int64_t* d_nrows,
+#ifndef GD_SCAN_MINB
+#define GD_SCAN_MINB 4
+#endif
+__global__ void __launch_bounds__(256, GD_SCAN_MINB) k_del_scan_head(OutView ov, const int32_t* row_first, const int64_t* d_nrows,
                                                        const uint64_t* rq_key, int64_t nrq, int sh, MatchOut mo) {
     constexpr int G = 8, kPer = 32 / G;
     __shared__ uint32_t hbm[256 / G][kHeadWords];
@@ -323,7 +326,7 @@ __global__ void k_chunk_rows(const int64_t* coff, const int64_t* hdr, int32_t* w
 // tail: one warp per kChunk piece of a long row beyond its head; the piece's
 // row comes from a table (no search), and a warp that meets the same row
 // again keeps its request bitmap.
-__global__ void __launch_bounds__(kScanWarps * 32, 4) k_del_scan_tail(OutView ov, const int32_t* row_first,
+__global__ void __launch_bounds__(kScanWarps * 32, GD_SCAN_MINB) k_del_scan_tail(OutView ov, const int32_t* row_first,
                                                                    const int64_t* coff, const int32_t* wrow,
                                                                    const int64_t* hdr, const uint64_t* rq_key,
                                                                    int64_t nrq, int sh, MatchOut mo) {
