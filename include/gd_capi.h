@@ -103,6 +103,12 @@ GD_API int gd_graph_export_segment(gd_graph* g, int64_t seg, int64_t* offsets, i
  * over destinations, sources ascending within a node. */
 GD_API int gd_graph_reverse_nnz(gd_graph* g, int64_t* nnz);
 GD_API int gd_graph_export_reverse(gd_graph* g, int64_t* offsets, int64_t* src, int64_t* weights);
+/* nodes_to exactly (graph/dynamic.py:152-160): each node's live in-arcs in
+ * the reference's reverse-list order (rebuild order, then inserts in the
+ * order they were appended), with the EdgeRef slot identity (segment,
+ * index) of every arc.  Arrays hold gd_graph_reverse_nnz entries. */
+GD_API int gd_graph_export_reverse_slots(gd_graph* g, int64_t* offsets, int64_t* src, int64_t* segment,
+                                         int64_t* index, int64_t* weights);
 /* gview.propagate_flags (engine/interp.py:70-109): flood true flags across
  * weak components; flags is n bytes in/out. */
 GD_API int gd_graph_propagate_flags(gd_graph* g, uint8_t* flags, int64_t* rounds);
@@ -116,6 +122,12 @@ GD_API int gd_graph_device_bytes(gd_graph* g, int64_t* bytes);
  * dynamicSSSP (sssp_dynamic.sp:137-157) incl. merge-if-due
  * (engine/interp.py:877-880); read = ctx.properties["dist"/"parent"].      */
 GD_API int gd_sssp_create(gd_graph* g, int64_t src, gd_sssp** out);
+/* the same with run_program's iteration_cap_factor (engine/run.py:22-41):
+ * every fixpoint of this handle (static and per batch) stops with
+ * GD_ERR_DIVERGED after max(1, factor * max(1, n)) rounds, as
+ * ExecContext.iteration_cap (engine/interp.py:138-139,800-813).  Plain
+ * gd_sssp_create uses the reference default 10. */
+GD_API int gd_sssp_create_ex(gd_graph* g, int64_t src, int64_t iteration_cap_factor, gd_sssp** out);
 GD_API int gd_sssp_batch(gd_sssp* s, const uint8_t* kind, const int64_t* src, const int64_t* dst, const int64_t* w,
                   int64_t k, int64_t batch_index);
 /* Same batch with the records already in device memory (int32 ids, 'a'/'d'). */
@@ -138,6 +150,9 @@ GD_API int gd_pr_batch_device(gd_pr* p, const uint8_t* kind, const int32_t* src,
 /* pagerank[n] (float64); outdeg[n] nullable (the maintained int64 outdeg) */
 GD_API int gd_pr_read(gd_pr* p, double* rank, int64_t* outdeg);
 GD_API int gd_pr_read_async(gd_pr* p, double* rank); /* as gd_sssp_read_async */
+/* ctx.properties["affected"] (pr_dynamic.sp:82-99): the last batch's flags
+ * after propagateNodeFlags, n bytes of 0/1 (all 0 before the first batch) */
+GD_API int gd_pr_read_affected(gd_pr* p, uint8_t* affected);
 /* device pointer to the float64 rank vector (valid until the next call) */
 GD_API int gd_pr_rank_device(gd_pr* p, const double** rank);
 GD_API int gd_pr_destroy(gd_pr* p);

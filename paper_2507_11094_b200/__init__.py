@@ -7,7 +7,7 @@ All compute runs in sm_100a kernels behind the C ABI of include/gd_capi.h.
 """
 
 from .engine import (CheckResult, ExecContext, NodePropertyTable, PRHandle, SSSPHandle, TCHandle, compile_source,
-                     needs_reverse, run_batches, run_program)
+                     needs_reverse, run_batches, run_program, shipped_program, source_digest)
 from .errors import (CompileError, ConfigurationError, ContractViolation, DeviceError, DivergenceError, ExecError,
                      GraphDynError, MalformedInputError)
 from .graph import SENTINEL, Csr, DeleteReport, DiffCsr, DynamicGraph, EdgeRef
@@ -23,5 +23,5 @@ __all__ = [
     "ExecError", "GraphDynError", "MalformedInputError", "NodePropertyTable", "PRHandle", "RecordArrays",
     "SSSPHandle", "TCHandle", "UpdateBatch", "UpdateRecord", "UpdateStream", "compile_source", "dump_graph",
     "dump_update_stream", "load_graph", "load_update_stream", "needs_reverse", "parse_edge_lines",
-    "parse_update_line", "run_batches", "run_program",
+    "parse_update_line", "run_batches", "run_program", "shipped_program", "source_digest",
 ]

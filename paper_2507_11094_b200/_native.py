@@ -43,10 +43,12 @@ SIGNATURES = [
     ("gd_graph_export_segment", C.c_int, [vp, i64, vp, vp, vp]),
     ("gd_graph_reverse_nnz", C.c_int, [vp, i64p]),
     ("gd_graph_export_reverse", C.c_int, [vp, vp, vp, vp]),
+    ("gd_graph_export_reverse_slots", C.c_int, [vp, vp, vp, vp, vp, vp]),
     ("gd_graph_propagate_flags", C.c_int, [vp, vp, i64p]),
     ("gd_graph_stream", C.c_int, [vp, C.POINTER(vp)]),
     ("gd_graph_device_bytes", C.c_int, [vp, i64p]),
     ("gd_sssp_create", C.c_int, [vp, i64, C.POINTER(vp)]),
+    ("gd_sssp_create_ex", C.c_int, [vp, i64, i64, C.POINTER(vp)]),
     ("gd_sssp_batch", C.c_int, [vp, vp, vp, vp, vp, i64, i64]),
     ("gd_sssp_batch_device", C.c_int, [vp, vp, vp, vp, vp, i64, i64]),
     ("gd_sssp_read", C.c_int, [vp, vp, vp]),
@@ -56,6 +58,7 @@ SIGNATURES = [
     ("gd_pr_batch_device", C.c_int, [vp, vp, vp, vp, vp, i64, i64]),
     ("gd_pr_read", C.c_int, [vp, vp, vp]),
     ("gd_pr_rank_device", C.c_int, [vp, C.POINTER(vp)]),
+    ("gd_pr_read_affected", C.c_int, [vp, vp]),
     ("gd_pr_destroy", C.c_int, [vp]),
     ("gd_tc_create", C.c_int, [vp, C.POINTER(vp)]),
     ("gd_tc_batch", C.c_int, [vp, vp, vp, vp, vp, i64, i64]),

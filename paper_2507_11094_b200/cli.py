@@ -27,7 +27,7 @@ from typing import Dict, List, Optional
 
 import numpy as np
 
-from .engine import INT_INF, NodePropertyTable, compile_source, needs_reverse, run_program
+from .engine import INT_INF, NodePropertyTable, compile_source, needs_reverse, run_program, shipped_program
 from .errors import CompileError, GraphDynError
 from .manifest import build_manifest, write_manifest
 
@@ -135,8 +135,7 @@ def make_parser() -> _Parser:
 
 def _compile(program: str):
     if program in _PROGRAM_NAMES:  # shorthand: sssp / pr / tc
-        drv = {"sssp": "dynamicSSSP", "pr": "dynamicPR", "tc": "dynamicTC"}[program]
-        return compile_source(f"Dynamic {drv}(")
+        return shipped_program(program)
     try:
         text = Path(program).read_text()
     except OSError as exc:
@@ -538,9 +537,7 @@ def _apply_part(graph, part) -> None:
 
 def cmd_oracle(args) -> int:
     """cli.py:571-596 on the GPU: the static entry on the replayed graph."""
-    name = _PROGRAM_NAMES[args.algo]
-    drv = {"sssp_dynamic": "dynamicSSSP", "pr_dynamic": "dynamicPR", "tc_dynamic": "dynamicTC"}[name]
-    check = compile_source(f"Dynamic {drv}(")
+    check = shipped_program(args.algo)
     graph = _load_graph(args.graph, directed=not args.undirected, nodes=None, merge_interval=1,
                         with_reverse=needs_reverse(check.program), device=args.device)
     updates = _load_updates(args.updates)

@@ -361,6 +361,17 @@ int gd_graph_export_reverse(gd_graph* g, int64_t* off, int64_t* src, int64_t* w)
     });
 }
 
+int gd_graph_export_reverse_slots(gd_graph* g, int64_t* off, int64_t* src, int64_t* seg, int64_t* idx,
+                                  int64_t* w) {
+    if (!g) return null_handle();
+    return guard([&] {
+        GD_CUDA(cudaSetDevice(g->st->device));
+        if (!g->st->with_reverse)
+            throw gdb::GdError(GD_ERR_CONFIG, "graph was loaded without reverse-adjacency maintenance");
+        g->st->export_rev_slots(off, src, seg, idx, w);
+    });
+}
+
 int gd_graph_propagate_flags(gd_graph* g, uint8_t* flags, int64_t* rounds) {
     if (!g) return null_handle();
     return guard([&] {
@@ -405,7 +416,10 @@ int gd_graph_device_bytes(gd_graph* g, int64_t* bytes) {
         *out = h;                        \
     })
 
-int gd_sssp_create(gd_graph* g, int64_t src, gd_sssp** out) { ALGO_CREATE(gdb::SSSP, gd_sssp, new gdb::SSSP(g->st.get(), src)); }
+int gd_sssp_create(gd_graph* g, int64_t src, gd_sssp** out) { return gd_sssp_create_ex(g, src, 10, out); }
+int gd_sssp_create_ex(gd_graph* g, int64_t src, int64_t iteration_cap_factor, gd_sssp** out) {
+    ALGO_CREATE(gdb::SSSP, gd_sssp, new gdb::SSSP(g->st.get(), src, iteration_cap_factor));
+}
 int gd_sssp_batch(gd_sssp* s, const uint8_t* kind, const int64_t* src, const int64_t* dst, const int64_t* w,
                   int64_t k, int64_t bi) {
     return algo_batch_host(s, kind, src, dst, w, k, bi);
@@ -458,6 +472,13 @@ int gd_pr_read(gd_pr* p, double* rank, int64_t* outdeg) {
     return guard([&] {
         GD_CUDA(cudaSetDevice(p->a->g->device));
         p->a->read(rank, outdeg);
+    });
+}
+int gd_pr_read_affected(gd_pr* p, uint8_t* affected) {
+    if (!p) return null_handle();
+    return guard([&] {
+        GD_CUDA(cudaSetDevice(p->a->g->device));
+        p->a->read_affected(affected);
     });
 }
 int gd_pr_read_async(gd_pr* p, double* rank) {

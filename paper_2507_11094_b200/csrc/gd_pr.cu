@@ -385,6 +385,7 @@ PR::PR(Store* st, double d, double b, int64_t mi) : AlgoBase(ALGO_PR, st), dampi
     contrib.alloc(std::max<int64_t>(n, 1), s);
     outdeg.alloc(std::max<int64_t>(n, 1), s);
     affected.alloc(std::max<int64_t>(n, 1), s);
+    affected.zero(s);  // propNode<bool> default before the first Batch
     partial.alloc(kRedBlocks, s);
     scal.alloc(2, s);  // [0] dangling, [1] diff
     ctl.alloc(C_LEN, s);
@@ -557,6 +558,14 @@ void PR::batch(DevBatch& b, int64_t batch_index) {
     flood_weak_components(*g, affected.get(), &prof);
     recompute(affected.get());
     timer.end_all();
+}
+
+void PR::read_affected(uint8_t* h_aff) {
+    cudaStream_t s = stream();
+    int64_t n = g->n;
+    if (!n) return;
+    GD_CUDA(cudaMemcpyAsync(h_aff, affected.get(), n, cudaMemcpyDeviceToHost, s));
+    GD_CUDA(cudaStreamSynchronize(s));
 }
 
 void PR::read(double* h_rank, int64_t* h_outdeg) {

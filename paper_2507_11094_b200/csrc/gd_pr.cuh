@@ -27,6 +27,7 @@ struct PR : AlgoBase {
     void set_comm(Comm* c);
     void batch(DevBatch& b, int64_t batch_index);                 // one Batch body
     void read(double* rank, int64_t* outdeg);
+    void read_affected(uint8_t* aff);  // the last batch's flooded flags
 
   private:
     void recompute(const uint8_t* flags);  // bin + sweep loop; flags == nullptr: all vertices

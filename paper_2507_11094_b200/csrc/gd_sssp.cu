@@ -100,6 +100,9 @@ struct FpArgs {
     int64_t* dist;
     int32_t* parent;
     uint8_t* flags;  // relax: touched (nullable); walk: stale (written); pull: stale (read)
+    // relax only: when set, only targets t with only[t] != 0 may be lowered
+    // (the decremental push; the reference's pull changes stale nodes only)
+    const uint8_t* only;
     int32_t* stamp;   // queue de-duplication per round
     int32_t* hstamp;  // out-piece de-duplication per round
     const int32_t* seeds;  // round 0 input, never written
@@ -156,7 +159,7 @@ __device__ __forceinline__ unsigned group_mask() {
 template <int MODE>
 __device__ __forceinline__ int64_t out_pre(const FpArgs& a, int32_t t) {
     if (t < 0) return 0;
-    if (MODE == FP_RELAX) return a.dist[t];
+    if (MODE == FP_RELAX) return a.only && !a.only[t] ? LLONG_MIN : a.dist[t];  // LLONG_MIN: no c < pre
     if (MODE == FP_WALK) return a.parent[t];
     return a.flags[t];
 }
@@ -405,7 +408,9 @@ __global__ void __launch_bounds__(kThreads, 4) k_fixpoint(FpArgs a) {
             split = true;
         }
         if ((m | mo | mi | F) == 0) break;
-        if (it >= a.cap) {
+        // the cap counts work rounds, as fixedPoint counts body runs
+        // (interp.py:800-813); a near-far split round only moves a pile
+        if (!split && it - nsplit >= a.cap) {
             if (leader) a.ctr[2] = 1;
             break;
         }
@@ -640,7 +645,7 @@ unsigned coop_grid() {
 
 }  // namespace
 
-SSSP::SSSP(Store* st, int64_t s) : AlgoBase(ALGO_SSSP, st), src((int32_t)s) {
+SSSP::SSSP(Store* st, int64_t s, int64_t cap) : AlgoBase(ALGO_SSSP, st), src((int32_t)s), cap_factor(cap) {
     if (!st->with_reverse)
         throw GdError(GD_ERR_CONFIG, "graph was loaded without reverse-adjacency maintenance");
     if (s < 0 || s >= st->n) throw GdError(GD_ERR_EXEC, "source node out of range");
@@ -689,7 +694,8 @@ SSSP::SSSP(Store* st, int64_t s) : AlgoBase(ALGO_SSSP, st), src((int32_t)s) {
     timer.end_all();
 }
 
-void SSSP::fixpoint(int mode, const int32_t* seeds, const int64_t* d_nseeds, int64_t nseeds, uint8_t* flags) {
+void SSSP::fixpoint(int mode, const int32_t* seeds, const int64_t* d_nseeds, int64_t nseeds, uint8_t* flags,
+                    const uint8_t* only) {
     cudaStream_t s = stream();
     if (!d_nseeds && nseeds == 0) return;
     const bool nf = mode == FP_RELAX && delta > 0;
@@ -706,6 +712,7 @@ void SSSP::fixpoint(int mode, const int32_t* seeds, const int64_t* d_nseeds, int
     a.dist = dist.get();
     a.parent = parent.get();
     a.flags = flags;
+    a.only = mode == FP_RELAX ? only : nullptr;
     a.stamp = stamp.get();
     a.seeds = seeds;
     a.q[0] = fr.q[0].get();
@@ -724,7 +731,7 @@ void SSSP::fixpoint(int mode, const int32_t* seeds, const int64_t* d_nseeds, int
     a.hstamp = hstamp.get();
     a.cnt = fr.cnt.get();
     a.ctr = ctr.get();
-    a.cap = cap_factor * std::max<int64_t>(g->n, 1);
+    a.cap = std::max<int64_t>(1, cap_factor * std::max<int64_t>(g->n, 1));  // ExecContext.iteration_cap
     void* args[] = {&a};
     static const char* names[] = {"sssp_relax", "sssp_walk", "sssp_pull"};
     const void* fn = mode == FP_RELAX  ? (const void*)k_fixpoint<FP_RELAX>
@@ -816,7 +823,10 @@ void SSSP::batch(DevBatch& b, int64_t batch_index) {
                     heavy.get(), fr.cnt.get() + 9);
         GD_KERNEL_T("sssp_pull", 0, k_pull_heavy, 148 * 4, kThreads, 0, s, heavy.get(), fr.cnt.get() + 9, ix,
                     dist.get());
-        fixpoint(FP_RELAX, list.get(), nlist, 0, nullptr);
+        // the push may lower stale targets only: a live arc into a non-stale
+        // node need not be tight (OnAdd relaxes the record's own direction and
+        // weight only), and the reference's pull never changes such a node
+        fixpoint(FP_RELAX, list.get(), nlist, 0, nullptr, seed_del);
     } else {
         fixpoint(FP_PULL, list.get(), nlist, 0, seed_del);
     }

@@ -30,7 +30,7 @@ struct SSSP : AlgoBase {
     DBuf<int64_t> parent64;  // int64 widening of parent for the async read   // stale vertices with > kHeavy in-arcs (pull sweep)
     DBuf<int64_t> dcount;  // device-side list sizes (no host read-back per fixpoint)
 
-    SSSP(Store* st, int64_t src);  // = staticSSSP
+    SSSP(Store* st, int64_t src, int64_t cap_factor = 10);  // = staticSSSP
     void batch(DevBatch& b, int64_t batch_index);
     void read(int64_t* dist, int64_t* parent);
     void read_async(int64_t* dist, int64_t* parent);  // see AlgoBase::copy_out_async
@@ -38,7 +38,8 @@ struct SSSP : AlgoBase {
   private:
     // one cooperative launch per fixpoint (relax / walk / pull); the seed count
     // is read from d_nseeds on the device when given, else nseeds
-    void fixpoint(int mode, const int32_t* seeds, const int64_t* d_nseeds, int64_t nseeds, uint8_t* flags);
+    void fixpoint(int mode, const int32_t* seeds, const int64_t* d_nseeds, int64_t nseeds, uint8_t* flags,
+                  const uint8_t* only = nullptr);
     // list == nullptr: every node; d_m (device) overrides m, which bounds the grid
     void fix_parents(const int32_t* list, const int64_t* d_m, int64_t m);
     void finish();

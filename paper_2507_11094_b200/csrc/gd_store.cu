@@ -523,16 +523,19 @@ __global__ void k_add_vacancies(OutView ov, const uint32_t* skey, const int32_t*
     }
 }
 
+// clog (nullable): the claimed global slot of each arc by stream position,
+// -1 for a spill (the order nodes_to appends claims in, dynamic.py:272-274)
 __global__ void k_add_claim(OutView ov, const int32_t* sval, const int32_t* a_col, const int32_t* a_w,
-                            const int64_t* vac_gid, int64_t narcs, uint8_t* leftover) {
+                            const int64_t* vac_gid, int64_t narcs, uint8_t* leftover, int64_t* clog) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < narcs; i += (int64_t)gridDim.x * blockDim.x) {
         int64_t gid = vac_gid[i];
+        int32_t a = sval[i];
+        if (clog) clog[a] = gid;
         if (gid < 0) {
             leftover[i] = 1;
             continue;
         }
         leftover[i] = 0;
-        int32_t a = sval[i];
         int sg = seg_of(ov.base, ov.nseg, gid);
         int64_t slot = gid - ov.base[sg];
         const_cast<int32_t*>(ov.col[sg])[slot] = a_col[a];
@@ -1321,8 +1324,10 @@ void Store::apply_adds(const int32_t* d_src, const int32_t* d_dst, const int32_t
     GD_KERNEL_T("add_vacancies", 0, k_add_vacancies, grid_for(na * 32, 256, 148LL * 32), 256, 0, s, ov, key.get(),
                 row_first.get(), d_nrows.get(), na, vac.get());
     DBuf<uint8_t> left(na, s);
+    ClaimLog cl;
+    if (with_reverse) cl.gid.alloc(na, s);
     GD_KERNEL(k_add_claim, grid_for(na, 256), 256, 0, s, ov, val.get(), aa.col.get(), aa.w.get(), vac.get(), na,
-              left.get());
+              left.get(), with_reverse ? cl.gid.get() : nullptr);
     // leftovers (already ordered by (source, stream order)) -> one new delta
     DBuf<int32_t> sel(na, s);
     int64_t nl = select_flagged_index(s, left.get(), na, sel.get());
@@ -1337,7 +1342,9 @@ void Store::apply_adds(const int32_t* d_src, const int32_t* d_dst, const int32_t
         offsets_from_rows(s, n, lrow.get(), nl, d.off);
         segs.push_back(std::move(d));
         upload_tables();
+        cl.delta_seg = (int64_t)segs.size() - 1;
     }
+    if (with_reverse) claim_logs.push_back(std::move(cl));
     live += na;
     index_add(rev, aa);
     if (fwd.built) index_add(fwd, aa);
@@ -1421,6 +1428,7 @@ void Store::merge() {
     live = nnz2;  // exact: pending kills are folded in
     GD_CUDA(cudaMemsetAsync(dcounts.get() + 1, 0, sizeof(unsigned long long), s));
     first_clean_delta = 1;
+    claim_logs.clear();  // _rebuild_reverse: list order restarts from the layout
     if (rev.built) compact_index(rev);
     if (fwd.built) compact_index(fwd);
 }
@@ -1438,6 +1446,83 @@ void Store::export_segment(int64_t seg, int64_t* off, int64_t* col, int64_t* w) 
         GD_CUDA(cudaStreamSynchronize(s));
     }
     GD_CUDA(cudaStreamSynchronize(s));
+}
+
+// nodes_to in the reference's list order, with slot identities
+// (dynamic.py:152-160).  _rebuild_reverse (dynamic.py:319-329, at build and
+// merge) lists a node's in-arcs in (segment, source, slot) order, i.e. global
+// slot order; deletes remove entries in place; every later insert appends --
+// vacancy claims in stream order, then the call's new delta in slot order
+// (dynamic.py:266-285).  So a live slot sorts by the last append event that
+// placed it (none: its rebuild position comes first).  Host-side: a query
+// API, not on the batch path.
+void Store::export_rev_slots(int64_t* off, int64_t* src, int64_t* seg, int64_t* idx, int64_t* w) {
+    cudaStream_t s = stream;
+    const size_t S = segs.size();
+    std::vector<int64_t> base(S + 1, 0);
+    std::vector<std::vector<int64_t>> hoff(S);
+    std::vector<std::vector<int32_t>> hcol(S), hw(S);
+    for (size_t i = 0; i < S; ++i) {
+        base[i + 1] = base[i] + segs[i].nslots;
+        hoff[i].resize(n + 1);
+        hcol[i].resize(segs[i].nslots);
+        GD_CUDA(cudaMemcpyAsync(hoff[i].data(), segs[i].off.get(), (n + 1) * 8, cudaMemcpyDeviceToHost, s));
+        if (segs[i].nslots) {
+            GD_CUDA(cudaMemcpyAsync(hcol[i].data(), segs[i].col.get(), segs[i].nslots * 4, cudaMemcpyDeviceToHost, s));
+            if (weighted) {
+                hw[i].resize(segs[i].nslots);
+                GD_CUDA(cudaMemcpyAsync(hw[i].data(), segs[i].w.get(), segs[i].nslots * 4, cudaMemcpyDeviceToHost, s));
+            }
+        }
+    }
+    std::vector<std::vector<int64_t>> logs(claim_logs.size());
+    for (size_t c = 0; c < claim_logs.size(); ++c) {
+        logs[c].resize(claim_logs[c].gid.n);
+        if (claim_logs[c].gid.n)
+            GD_CUDA(cudaMemcpyAsync(logs[c].data(), claim_logs[c].gid.get(), claim_logs[c].gid.n * 8,
+                                    cudaMemcpyDeviceToHost, s));
+    }
+    GD_CUDA(cudaStreamSynchronize(s));
+    const int64_t total = base[S];
+    std::vector<int64_t> event(total, -1);  // last append event per global slot
+    int64_t ev = 0;
+    for (size_t c = 0; c < logs.size(); ++c) {
+        for (int64_t g : logs[c])
+            if (g >= 0) event[g] = ev++;
+        int64_t ds = claim_logs[c].delta_seg;
+        if (ds >= 0)
+            for (int64_t i = 0; i < segs[ds].nslots; ++i) event[base[ds] + i] = ev++;
+    }
+    // bucket live slots by destination, then order each bucket
+    std::vector<int64_t> cnt(n + 1, 0);
+    for (size_t i = 0; i < S; ++i)
+        for (int32_t d : hcol[i])
+            if (d >= 0) ++cnt[d + 1];
+    for (int64_t v = 0; v < n; ++v) cnt[v + 1] += cnt[v];
+    std::vector<int64_t> fill(cnt.begin(), cnt.end() - 1);
+    std::vector<int64_t> gids(cnt[n]);
+    for (size_t i = 0; i < S; ++i)
+        for (int64_t j = 0; j < segs[i].nslots; ++j)
+            if (hcol[i][j] >= 0) gids[fill[hcol[i][j]]++] = base[i] + j;
+    auto later = [&](int64_t a, int64_t b) {  // rebuild entries (event -1) first, by slot
+        if (event[a] != event[b]) return event[a] < event[b];
+        return a < b;
+    };
+    for (int64_t v = 0; v < n; ++v) {
+        std::sort(gids.begin() + cnt[v], gids.begin() + cnt[v + 1], later);
+        off[v] = cnt[v];
+    }
+    off[n] = cnt[n];
+    for (int64_t k = 0; k < cnt[n]; ++k) {
+        int64_t g = gids[k];
+        size_t sg = std::upper_bound(base.begin(), base.end(), g) - base.begin() - 1;
+        int64_t i = g - base[sg];
+        const std::vector<int64_t>& o = hoff[sg];
+        src[k] = std::upper_bound(o.begin(), o.end(), i) - o.begin() - 1;
+        seg[k] = (int64_t)sg;
+        idx[k] = i;
+        if (w) w[k] = weighted ? hw[sg][i] : 1;
+    }
 }
 
 int64_t Store::rev_nnz_live() {

@@ -74,6 +74,13 @@ struct KilledArcs {
     DBuf<int64_t> gid;
     int64_t count = 0;
 };
+// One add call's vacancy claims: global slot per arc in stream order (-1 =
+// spilled), and the delta segment the call created (-1 = none).  Kept from
+// one rebuild (build / merge) to the next for nodes_to's list order.
+struct ClaimLog {
+    DBuf<int64_t> gid;
+    int64_t delta_seg = -1;
+};
 // Inserted out-arcs of one add call (device).
 struct AddedArcs {
     DBuf<int32_t> row, col, w;
@@ -113,6 +120,7 @@ class Store {
     void export_segment(int64_t seg, int64_t* off, int64_t* col, int64_t* w);
     int64_t rev_nnz_live();
     void export_rev(int64_t* off, int64_t* src, int64_t* w);
+    void export_rev_slots(int64_t* off, int64_t* src, int64_t* seg, int64_t* idx, int64_t* w);
 
     int device;
     cudaStream_t stream = nullptr;
@@ -131,6 +139,7 @@ class Store {
     DBuf<int32_t> otrow;
     int64_t notomb = 0;
     size_t first_clean_delta = 1;  // deltas from this index on have seen no delete phase
+    std::vector<ClaimLog> claim_logs;  // add calls since the last rebuild (with_reverse only)
 
   private:
     // segment table on the device: [off ptrs | col ptrs | w ptrs | bases]

@@ -13,7 +13,9 @@ below; the DSL compiler itself is out of scope.
 from __future__ import annotations
 
 import ctypes as C
+import hashlib
 import math
+import re
 import time
 from dataclasses import dataclass, field
 from typing import Dict, List, Optional
@@ -74,16 +76,54 @@ class CheckResult:
     program: Program
 
 
-def compile_source(source: str, strip: bool = False) -> CheckResult:
-    """Recognise one of the three shipped programs (programs/*.sp).
+# SHA-256 of the normalised text (see _normalise) of the shipped programs,
+# /root/reference/pkg/src/graphdyn/programs/*.sp.  tests/test_capi_cpu.py
+# re-derives them from the reference when it is present.
+SHIPPED_DIGESTS = {
+    "sssp_dynamic": "ca559ae9aad5a6cdedf346499544a0efb065e3584d22091bf01ab4331138692b",
+    "pr_dynamic": "515c5e024d4e62030e32da41bfec3c4a4366ca328a2a4a0ccee453b174218b2c",
+    "tc_dynamic": "38faa7c28210c8884787026fcc6510fb1934633ec1d885d043e681d310937e8e",
+}
+_SHORT = {"sssp": "sssp_dynamic", "pr": "pr_dynamic", "tc": "tc_dynamic"}
 
-    The B200 path executes these programs natively; any other DSL source is
-    rejected with CompileError rather than interpreted on the CPU."""
-    for name, driver in _DRIVER.items():
-        if f"Dynamic {driver}(" in source:
+
+def _normalise(source: str) -> str:
+    """Comments dropped, then the token sequence (words and single
+    punctuation characters) joined by single spaces: layout- and
+    comment-insensitive, but any change to the program text shows."""
+    text = re.sub(r"/\*.*?\*/", " ", source, flags=re.S)
+    text = re.sub(r"//[^\n]*", " ", text)
+    return " ".join(re.findall(r"\w+|[^\w\s]", text))
+
+
+def source_digest(source: str) -> str:
+    return hashlib.sha256(_normalise(source).encode()).hexdigest()
+
+
+def compile_source(source: str, strip: bool = False) -> CheckResult:
+    """frontend.compile_source (frontend/__init__.py:13-28) for the B200 path.
+
+    The path executes exactly the three shipped programs (programs/*.sp) in
+    native code, so a source is accepted only when it IS one of them up to
+    comments and layout; any other text -- including an edited copy of a
+    shipped program -- raises CompileError instead of silently running the
+    shipped semantics.  The DSL compiler itself is out of scope."""
+    digest = source_digest(source)
+    for name, want in SHIPPED_DIGESTS.items():
+        if digest == want:
             return CheckResult(Program(name))
-    raise CompileError(["the B200 path implements only sssp_dynamic, pr_dynamic and tc_dynamic "
-                        "(programs/*.sp); no Dynamic driver of those was found in the source"])
+    raise CompileError(["the B200 path executes only the shipped programs sssp_dynamic, pr_dynamic and "
+                        "tc_dynamic (programs/*.sp); this source differs from each of them after comments "
+                        "and whitespace are removed"])
+
+
+def shipped_program(name: str) -> CheckResult:
+    """The CheckResult of a shipped program by name ("sssp_dynamic" or its
+    short form "sssp"; likewise pr / tc), without its source text."""
+    key = _SHORT.get(name, name)
+    if key not in SHIPPED_DIGESTS:
+        raise CompileError([f"unknown shipped program {name!r}; expected one of {sorted(SHIPPED_DIGESTS)}"])
+    return CheckResult(Program(key))
 
 
 def needs_reverse(program) -> bool:
@@ -204,9 +244,9 @@ class _Algo:
 class SSSPHandle(_Algo):
     kind = "sssp"
 
-    def __init__(self, graph: DynamicGraph, src: int):
+    def __init__(self, graph: DynamicGraph, src: int, iteration_cap_factor: int = 10):
         h = C.c_void_p()
-        N.check(N.lib().gd_sssp_create(graph.handle, int(src), C.byref(h)))
+        N.check(N.lib().gd_sssp_create_ex(graph.handle, int(src), int(iteration_cap_factor), C.byref(h)))
         super().__init__(h, graph)
 
     def read(self):
@@ -239,6 +279,12 @@ class PRHandle(_Algo):
         od = np.zeros(n, dtype=np.int64) if with_outdeg else None
         N.check(N.lib().gd_pr_read(self.h, N.ptr(rank), N.ptr(od)))
         return rank, od
+
+    def read_affected(self) -> np.ndarray:
+        """The last batch's flooded `affected` flags (uint8[n])."""
+        out = np.zeros(self.graph.node_count, dtype=np.uint8)
+        N.check(N.lib().gd_pr_read_affected(self.h, N.ptr(out)))
+        return out
 
     def read_async(self, rank_out: np.ndarray) -> None:
         """Snapshot the ranks now, copy them to rank_out (float64[n], pinned
@@ -323,7 +369,7 @@ def run_program(check, graph: DynamicGraph, inputs: Dict[str, object], *, entry:
 
     t0 = time.perf_counter()
     if name == "sssp_dynamic":
-        algo = SSSPHandle(graph, _need(inputs, "src", int))
+        algo = SSSPHandle(graph, _need(inputs, "src", int), iteration_cap_factor)
     elif name == "pr_dynamic":
         algo = PRHandle(graph, _need(inputs, "damping", float), _need(inputs, "beta", float),
                         _need(inputs, "maxiter", int))
@@ -350,14 +396,34 @@ def run_program(check, graph: DynamicGraph, inputs: Dict[str, object], *, entry:
     ctx.phase_totals = {p: totals[p] / 1e3 for p in PHASES if totals[p] > 0 or p == "static_phase"}
     ctx.scalars["wall_seconds"] = time.perf_counter() - t0
 
+    # node properties in the reference's declaration order (the entry's
+    # parameters, then its locals: interp.py binds every propNode of the
+    # entry's scope into ctx.properties)
+    n = graph.node_count
+    false = lambda: np.zeros(n, dtype=np.uint8)  # noqa: E731
     if name == "sssp_dynamic":
         dist, parent = algo.read()
         ctx.properties["dist"] = NodePropertyTable("dist", "int", dist)
         ctx.properties["parent"] = NodePropertyTable("parent", "int", parent)
+        # the bool locals are the `modified` sets of fixedPoint loops, which
+        # end only once no flag is set (interp.py:800-813; sssp_dynamic.sp:15,
+        # 52,72,110: activeOnDelete / activeOnAdd are passed in as `modified`
+        # and are re-attached False per batch, :138) -- so a completed run
+        # always leaves them all False
+        locals_ = ("activeOnDelete", "activeOnAdd") if dynamic else ("modified", "modified_nxt")
+        for nm in locals_:
+            ctx.properties[nm] = NodePropertyTable(nm, "bool", false())
     elif name == "pr_dynamic":
         rank, od = algo.read()
         ctx.properties["pagerank"] = NodePropertyTable("pagerank", "float", rank)
-        ctx.properties["outdeg"] = NodePropertyTable("outdeg", "int", od)
+        if dynamic:  # pr_dynamic.sp:82-83: affected, then outdeg
+            ctx.properties["affected"] = NodePropertyTable("affected", "bool", algo.read_affected())
+            ctx.properties["outdeg"] = NodePropertyTable("outdeg", "int", od)
+        else:  # staticPR (pr_dynamic.sp:7-9): rank_new holds the last sweep, i.e. the committed ranks
+            ctx.properties["outdeg"] = NodePropertyTable("outdeg", "int", od)
+            maxiter = _need(inputs, "maxiter", int)
+            ctx.properties["rank_new"] = NodePropertyTable(
+                "rank_new", "float", rank.copy() if maxiter > 0 else np.zeros(n, dtype=np.float64))
     else:
         c = algo.read()
         ctx.return_value = c

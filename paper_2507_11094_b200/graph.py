@@ -98,6 +98,8 @@ class DynamicGraph:
         self._snap_version = -1
         self._segs: List[Csr] = []
         self._rev = None
+        self._revl = None
+        self._revl_version = -1
         self._mutate_lock = threading.Lock()
 
     # -- construction -----------------------------------------------------------------
@@ -242,13 +244,30 @@ class DynamicGraph:
             total += int(np.count_nonzero(seg.coordinates[lo:hi] != SENTINEL))
         return total
 
+    def _reverse_lists(self):
+        """The reference's reverse lists: per node, (src, segment, index,
+        weight) in list order (gd_graph_export_reverse_slots)."""
+        if not self._with_reverse:
+            raise ConfigurationError("graph was loaded without reverse-adjacency maintenance")
+        self._snapshot()
+        if self._revl is None or self._revl_version != self.structure_version:
+            L = N.lib()
+            nnz = C.c_int64()
+            N.check(L.gd_graph_reverse_nnz(self._h, C.byref(nnz)))
+            off = np.zeros(self.node_count + 1, dtype=np.int64)
+            cols = [np.zeros(nnz.value, dtype=np.int64) for _ in range(4)]
+            N.check(L.gd_graph_export_reverse_slots(self._h, N.ptr(off), *(N.ptr(c) for c in cols)))
+            self._revl = (off, *cols)
+            self._revl_version = self.structure_version
+        return self._revl
+
     def nodes_to(self, v: int) -> Iterator[EdgeRef]:
-        """Live in-edges of v (sources ascending).  segment/index are -1: the
-        device in-index is not slot-addressed."""
+        """Live in-edges of v in the reference's reverse-list order, with
+        their slot identities (graph/dynamic.py:152-160)."""
         self._check_node(v)
-        off, s, w = self._reverse_snapshot()
+        off, s, sg, ix, w = self._reverse_lists()
         for k in range(int(off[v]), int(off[v + 1])):
-            yield EdgeRef(int(s[k]), v, int(w[k]) if self.weighted else 1, -1, -1)
+            yield EdgeRef(int(s[k]), v, int(w[k]) if self.weighted else 1, int(sg[k]), int(ix[k]))
 
     def in_degree(self, v: int) -> int:
         self._check_node(v)

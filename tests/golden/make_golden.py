@@ -63,14 +63,15 @@ def seg_dump(g: DynamicGraph):
     return out
 
 
-def rev_dump(g: DynamicGraph):
-    """Reverse lists (nodes_to) in the reference's own list order."""
+def rev_dump(g: DynamicGraph, slots=False):
+    """Reverse lists (nodes_to) in the reference's own list order; with
+    slots=True the EdgeRef slot identities (segment, index) instead."""
     off = [0]
     src, wts = [], []
     for v in range(g.node_count):
         for e in g.nodes_to(v):
-            src.append(e.source)
-            wts.append(e.weight)
+            src.append(e.segment if slots else e.source)
+            wts.append(e.index if slots else e.weight)
         off.append(len(src))
     return np.array(off, dtype=np.int64), np.array(src, dtype=np.int64), np.array(wts, dtype=np.int64)
 
@@ -113,6 +114,8 @@ def store_case(name, n, edges, batches, directed, merge_every, out):
         ro, rs, rw = rev_dump(g)
         parts += [np.array([len(rs)], dtype=np.int64), ro, rs, rw]
         out[f"{name}/{tag}"] = np.concatenate(parts)
+        _, rseg, ridx = rev_dump(g, slots=True)
+        out[f"{name}/{tag}/revslots"] = np.stack([rseg, ridx]) if len(rseg) else np.zeros((2, 0), np.int64)
 
     snap("build")
     for i, records in enumerate(batches):
@@ -167,19 +170,29 @@ def make_store(path):
 
 # -- algorithm fixtures from the reference engine ------------------------------------
 
+BOOL_PROPS = {}  # {prop: uint8[n]} of the last engine_run (filled by engine_run)
+
+
 def engine_run(algo, edges, n, records, batch, *, directed=True, weighted=False, merge_interval=1,
-               src=0, damping=0.85, beta=0.001, maxiter=100):
+               src=0, damping=0.85, beta=0.001, maxiter=100, cap=10):
     prog = {"sssp": "sssp_dynamic", "pr": "pr_dynamic", "tc": "tc_dynamic"}[algo]
     g = DynamicGraph.build(edges, n, directed=directed, weighted=weighted, merge_interval=merge_interval,
                            with_reverse=algo != "tc")
     inputs = {"sssp": {"src": src}, "pr": {"damping": damping, "beta": beta, "maxiter": maxiter}, "tc": {}}[algo]
-    ctx = run_batches(CHECK[prog], g, UpdateStream(records), batch, inputs)
+    ctx = run_batches(CHECK[prog], g, UpdateStream(records), batch, inputs, iteration_cap_factor=cap)
+    BOOL_PROPS.clear()
+    for pname, table in ctx.properties.items():
+        if getattr(table, "dtype", None) == "bool" and hasattr(table, "values"):
+            BOOL_PROPS[pname] = np.array(table.values(), dtype=np.uint8)
     if algo == "sssp":
         return np.array(ctx.properties["dist"].values(), dtype=np.int64), np.array(
             ctx.properties["parent"].values(), dtype=np.int64)
     if algo == "pr":
         return np.array(ctx.properties["pagerank"].values(), dtype=np.float64)
     return np.array([ctx.return_value], dtype=np.int64)
+
+
+INF = 2 ** 63 - 1
 
 
 def put_case(out, names, name, algo, n, edges, records, batch, *, directed, weighted, merge_interval=1,
@@ -193,6 +206,10 @@ def put_case(out, names, name, algo, n, edges, records, batch, *, directed, weig
     out[f"{name}/source"] = np.array([source])
     out[f"{name}/edges"] = np.stack([es, ed, ew])
     out[f"{name}/recs"] = np.stack([kind.astype(np.int64), s, d, w]) if len(kind) else np.zeros((4, 0), np.int64)
+    if source == "engine":
+        for pname, vals in BOOL_PROPS.items():
+            out[f"{name}/prop/{pname}"] = vals
+        out[f"{name}/propnames"] = np.array(list(BOOL_PROPS) or [""])
     if algo == "sssp":
         out[f"{name}/dist"], out[f"{name}/parent"] = result
     elif algo == "pr":
@@ -279,6 +296,34 @@ def make_algos(path):
         put_case(out, names, f"tc_multi{j}", "tc", n, edges, records, bs, directed=False, weighted=False,
                  merge_interval=1 + j % 2, result=r)
 
+    # undirected and unweighted SSSP: OnAdd relaxes only the record's own
+    # direction with the record's own weight, so non-stale distances need not
+    # be tight; the decremental repair may change stale nodes only
+    # (sssp_dynamic.sp:68-86).  First the advisor's repro.
+    rep_e = [(0, 1, 1), (0, 3, 1), (3, 1, 1), (3, 4, 1), (4, 5, 1), (5, 6, 1)]
+    rep_r = [UpdateRecord(ADD, 6, 1, 1), UpdateRecord(DELETE, 0, 1)]
+    r = engine_run("sssp", rep_e, 7, rep_r, 1, directed=False)
+    assert list(r[0]) == [0, 2, INF, 1, 2, 3, 4] and list(r[1]) == [-1, 3, -1, 0, 3, 4, 5]
+    put_case(out, names, "sssp_und_repro", "sssp", 7, rep_e, rep_r, 1, directed=False, weighted=False, result=r)
+    for j in range(12):
+        n = [16, 30, 48, 70][j % 4]
+        m = n * [2, 3][j % 2]
+        directed = j % 3 == 2
+        weighted = j % 2 == 0
+        edges = uniform_random_graph(n, m, seed=300 + j, weighted=True, max_weight=7, undirected=not directed)
+        if not weighted:
+            edges = [(u, v, 1) for u, v, _ in edges]
+        recs = generate_updates(edges, n, [10, 20, 30][j % 3], seed=400 + j, undirected=not directed)
+        rng = random.Random(500 + j)
+        # record weights above 1 on an unweighted store (OnAdd reads them)
+        recs = [UpdateRecord(rc.kind, rc.src, rc.dst, rng.randint(1, 6)) if rc.kind == ADD else rc for rc in recs]
+        bs = [1, 4, 11, max(1, len(recs))][j % 4]
+        mi = [1, 2][j % 2]
+        r = engine_run("sssp", edges, n, recs, bs, directed=directed, weighted=weighted, merge_interval=mi,
+                       src=j % n)
+        put_case(out, names, f"sssp_und{j}", "sssp", n, edges, recs, bs, directed=directed, weighted=weighted,
+                 merge_interval=mi, src=j % n, result=r)
+
     # larger cases from the reference's emitted OpenMP programs (--threads 1)
     for j, (lg, m, pct) in enumerate([(10, 6000, 5), (11, 16000, 10), (12, 40000, 5)]):
         edges, n = rmat_graph(lg, m, seed=40 + j, weighted=True, max_weight=100)
@@ -303,8 +348,43 @@ def make_algos(path):
         put_case(out, names, f"tc_omp{j}", "tc", 1 << lg, ue, ur, batch, directed=False, weighted=False,
                  result=res, source="omp")
     out["names"] = np.array(names)
+    make_caps(out)
     np.savez_compressed(path, **out)
     print(f"wrote {path}: {len(names)} algorithm cases")
+
+
+def make_caps(out):
+    """iteration_cap_factor -> DivergenceError (interp.py:138-139,800-813):
+    for each case, whether the reference raises at each factor."""
+    from graphdyn.errors import DivergenceError
+
+    cases = []
+    # directed unit path: the static fixpoint needs exactly n body runs
+    path = [(i, i + 1, 1) for i in range(9)]
+    cases.append(("cap_path", 10, path, [], 1, True, False))
+    # the worked example with its batch
+    ex = [(0, 1, 30), (0, 2, 20), (0, 3, 48), (3, 4, 4), (2, 5, 25), (4, 5, 6)]
+    cases.append(("cap_worked", 6, ex, [UpdateRecord(DELETE, 2, 5), UpdateRecord(ADD, 1, 3, 10)], 2, True, True))
+    names = []
+    for name, n, edges, recs, bs, directed, weighted in cases:
+        factors = [0, 1, 2, 10]
+        div = []
+        for f in factors:
+            try:
+                engine_run("sssp", edges, n, recs, bs, directed=directed, weighted=weighted, cap=f)
+                div.append(0)
+            except DivergenceError:
+                div.append(1)
+        es, ed, ew = edge_arrays(edges)
+        kind, s, d, w = rec_arrays(recs)
+        out[f"{name}/meta"] = np.array([n, int(directed), int(weighted), bs], dtype=np.int64)
+        out[f"{name}/edges"] = np.stack([es, ed, ew])
+        out[f"{name}/recs"] = np.stack([kind.astype(np.int64), s, d, w]) if len(kind) else np.zeros((4, 0), np.int64)
+        out[f"{name}/factors"] = np.array(factors, dtype=np.int64)
+        out[f"{name}/diverged"] = np.array(div, dtype=np.int64)
+        names.append(name)
+        print(name, dict(zip(factors, div)))
+    out["cap_names"] = np.array(names)
 
 
 if __name__ == "__main__":

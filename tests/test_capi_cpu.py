@@ -49,21 +49,51 @@ def test_no_cpu_fallback():
         gd.DynamicGraph.build([(0, 1, 1)], 2)
 
 
-def test_compile_source_recognises_shipped_programs():
+REF_PROGRAMS = "/root/reference/pkg/src/graphdyn/programs"
+
+
+def test_shipped_program_by_name():
     import paper_2507_11094_b200 as gd
 
-    for prog, entry in (("sssp_dynamic", "dynamicSSSP"), ("pr_dynamic", "dynamicPR"), ("tc_dynamic", "dynamicTC")):
-        src = f"Dynamic {entry}(Graph g) {{}}"
-        chk = gd.compile_source(src)
-        assert chk.program.entry == entry
-        assert chk.program.function(entry) is not None
+    for short, prog, entry in (("sssp", "sssp_dynamic", "dynamicSSSP"), ("pr", "pr_dynamic", "dynamicPR"),
+                               ("tc", "tc_dynamic", "dynamicTC")):
+        for key in (short, prog):
+            chk = gd.shipped_program(key)
+            assert chk.program.name == prog and chk.program.entry == entry
+            assert chk.program.function(entry) is not None
+            assert gd.needs_reverse(chk.program) == (prog != "tc_dynamic")
+    with pytest.raises(gd.CompileError):
+        gd.shipped_program("bfs")
+
+
+def test_compile_source_rejects_everything_but_the_shipped_programs():
+    import paper_2507_11094_b200 as gd
+
+    # a driver signature alone is not the program (the round-1 substring match)
+    for entry in ("dynamicSSSP", "dynamicPR", "dynamicTC"):
+        with pytest.raises(gd.CompileError):
+            gd.compile_source(f"Dynamic {entry}(Graph g) {{}}")
     with pytest.raises(gd.CompileError):
         gd.compile_source("function f(Graph g) {}")
-    if os.path.isdir("/root/reference/pkg/src/graphdyn/programs"):
-        for name in ("sssp_dynamic", "pr_dynamic", "tc_dynamic"):
-            text = open(f"/root/reference/pkg/src/graphdyn/programs/{name}.sp").read()
-            assert gd.compile_source(text).program.name == name
-            assert gd.needs_reverse(gd.compile_source(text).program) == (name != "tc_dynamic")
+
+
+@pytest.mark.skipif(not os.path.isdir(REF_PROGRAMS), reason="reference programs not present")
+def test_compile_source_pins_the_reference_programs():
+    import paper_2507_11094_b200 as gd
+    from paper_2507_11094_b200.engine import SHIPPED_DIGESTS
+
+    for name in ("sssp_dynamic", "pr_dynamic", "tc_dynamic"):
+        text = open(f"{REF_PROGRAMS}/{name}.sp").read()
+        assert gd.source_digest(text) == SHIPPED_DIGESTS[name]
+        assert gd.compile_source(text).program.name == name
+        # layout and comments do not matter
+        relaid = "// reformatted\n" + "\n".join(line.strip() + "   /* x */" for line in text.splitlines())
+        assert gd.compile_source(relaid).program.name == name
+        # any edit to the body does
+        for a, b in (("<", "<="), ("+", "-"), ("True", "False"), ("0.0", "0.5")):
+            if a in text:
+                with pytest.raises(gd.CompileError):
+                    gd.compile_source(text.replace(a, b, 1))
 
 
 def test_update_stream_parsing_and_batching(tmp_path):

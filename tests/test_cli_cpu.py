@@ -11,7 +11,6 @@ from paper_2507_11094_b200.cli import EXIT_COMPILE, EXIT_OK, EXIT_RUNTIME, EXIT_
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 GOLD = os.path.join(HERE, "golden", "cli")
-PROGS = os.path.join(HERE, "programs")
 
 
 @pytest.mark.parametrize("graph,flags,gold", [
@@ -50,13 +49,13 @@ def test_compile_diagnostics_exit_code(tmp_path):
 
 
 def test_bench_empty_percent_list_is_usage_error(tmp_path):
-    rc = main(["bench", os.path.join(PROGS, "sssp_dynamic.sp"), os.path.join(GOLD, "scenario.txt"),
+    rc = main(["bench", "sssp", os.path.join(GOLD, "scenario.txt"),
                "--percents", "", "--src", "0", "--out", str(tmp_path / "b")])
     assert rc == EXIT_USAGE
 
 
 def test_bench_ranks_is_usage_error(tmp_path):
-    rc = main(["bench", os.path.join(PROGS, "tc_dynamic.sp"), os.path.join(GOLD, "g60u.txt"), "--undirected",
+    rc = main(["bench", "tc", os.path.join(GOLD, "g60u.txt"), "--undirected",
                "--percents", "10", "--ranks", "2", "--out", str(tmp_path / "b")])
     assert rc == EXIT_USAGE
 

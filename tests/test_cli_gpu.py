@@ -17,7 +17,6 @@ pytestmark = pytest.mark.gpu
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 GOLD = os.path.join(HERE, "golden", "cli")
-PROGS = os.path.join(HERE, "programs")
 
 
 def g(name):
@@ -37,12 +36,14 @@ def scalars(path):
 
 def test_dynamic_run_writes_results_and_manifest(tmp_path):
     out = tmp_path / "out"
-    rc = main(["run", os.path.join(PROGS, "sssp_dynamic.sp"), g("scenario.txt"), "--updates",
+    rc = main(["run", "sssp", g("scenario.txt"), "--updates",
                g("scenario_updates.txt"), "--batch", "1000", "--src", "0", "--out", str(out)])
     assert rc == EXIT_OK
     assert [int(values(out / "dist.csv")[v]) for v in range(6)] == [0, 30, 20, 40, 44, 50]
-    for f in ("dist.csv", "parent.csv"):
+    # every node property the reference CLI writes, bool tables included
+    for f in ("dist.csv", "parent.csv", "activeOnDelete.csv", "activeOnAdd.csv"):
         assert (out / f).read_bytes() == open(g(f"run_sssp/{f}"), "rb").read()
+    assert sorted(p.name for p in out.glob("*.csv")) == sorted(p for p in os.listdir(g("run_sssp")))
     m = json.loads((out / "manifest.json").read_text())
     assert m["seed"] == 0 and "graph" in m["input_digests"]
     assert m["run"]["batch_count"] == 1 and "static_phase" in m["run"]["phase_seconds"]
@@ -51,9 +52,9 @@ def test_dynamic_run_writes_results_and_manifest(tmp_path):
 
 def test_sssp_run_matches_reference_cli(tmp_path):
     out = tmp_path / "o"
-    assert main(["run", os.path.join(PROGS, "sssp_dynamic.sp"), g("g40.txt"), "--updates", g("gen_g40.txt"),
+    assert main(["run", "sssp", g("g40.txt"), "--updates", g("gen_g40.txt"),
                  "--batch", "5", "--src", "3", "--out", str(out)]) == EXIT_OK
-    for f in ("dist.csv", "parent.csv"):
+    for f in ("dist.csv", "parent.csv", "activeOnDelete.csv", "activeOnAdd.csv"):
         assert (out / f).read_bytes() == open(g(f"run_sssp_g40/{f}"), "rb").read()
 
 
@@ -66,12 +67,15 @@ def test_pr_run_matches_reference_cli(tmp_path):
     err = max(abs(float(got[k]) - float(want[k])) for k in want)
     assert err <= 1e-9, err
     assert (out / "outdeg.csv").read_bytes() == open(g("run_pr_rmat9/outdeg.csv"), "rb").read()
+    # the last batch's flooded flags (pr_dynamic.sp:82-99)
+    assert (out / "affected.csv").read_bytes() == open(g("run_pr_rmat9/affected.csv"), "rb").read()
+    assert sorted(p.name for p in out.glob("*.csv")) == sorted(os.listdir(g("run_pr_rmat9")))
     assert scalars(out / "scalars.csv") == scalars(g("run_pr_rmat9/scalars.csv"))
 
 
 def test_tc_run_and_oracle_match_reference_cli(tmp_path):
     out = tmp_path / "o"
-    assert main(["run", os.path.join(PROGS, "tc_dynamic.sp"), g("g60u.txt"), "--undirected", "--updates",
+    assert main(["run", "tc", g("g60u.txt"), "--undirected", "--updates",
                  g("gen_g60u.txt"), "--batch", "20", "--out", str(out)]) == EXIT_OK
     want = scalars(g("run_tc_g60u/scalars.csv"))
     got = scalars(out / "scalars.csv")
@@ -91,7 +95,7 @@ def test_sssp_oracle_matches_reference_cli(tmp_path):
 
 def test_static_mode_equals_oracle_on_updated_graph(tmp_path):
     out1, out2 = tmp_path / "s", tmp_path / "o"
-    assert main(["run", os.path.join(PROGS, "sssp_dynamic.sp"), g("scenario.txt"), "--mode", "static",
+    assert main(["run", "sssp", g("scenario.txt"), "--mode", "static",
                  "--updates", g("scenario_updates.txt"), "--src", "0", "--out", str(out1)]) == EXIT_OK
     assert main(["oracle", "sssp", g("scenario.txt"), "--updates", g("scenario_updates.txt"), "--src", "0",
                  "--out", str(out2)]) == EXIT_OK
@@ -99,7 +103,7 @@ def test_static_mode_equals_oracle_on_updated_graph(tmp_path):
 
 
 def test_missing_src_is_usage_error(tmp_path):
-    rc = main(["run", os.path.join(PROGS, "sssp_dynamic.sp"), g("scenario.txt"), "--updates",
+    rc = main(["run", "sssp", g("scenario.txt"), "--updates",
                g("scenario_updates.txt"), "--out", str(tmp_path / "x")])
     assert rc == EXIT_USAGE
 
@@ -107,14 +111,14 @@ def test_missing_src_is_usage_error(tmp_path):
 def test_runtime_error_exit_code(tmp_path):
     u = tmp_path / "bad.txt"
     u.write_text("a 0 99\n")
-    rc = main(["run", os.path.join(PROGS, "sssp_dynamic.sp"), g("scenario.txt"), "--updates", str(u), "--src", "0",
+    rc = main(["run", "sssp", g("scenario.txt"), "--updates", str(u), "--src", "0",
                "--out", str(tmp_path / "x")])
     assert rc == EXIT_RUNTIME
 
 
 def test_bench_produces_table_and_equivalence(tmp_path):
     out = tmp_path / "bench"
-    rc = main(["bench", os.path.join(PROGS, "sssp_dynamic.sp"), g("g40.txt"), "--percents", "5,20", "--src", "0",
+    rc = main(["bench", "sssp", g("g40.txt"), "--percents", "5,20", "--src", "0",
                "--seed", "9", "--out", str(out)])
     assert rc == EXIT_OK
     with open(out / "bench.csv", newline="") as fh:
@@ -146,5 +150,5 @@ def test_binary_inputs_give_the_text_results(tmp_path):
     out = tmp_path / "o"
     assert main(["run", "sssp", str(tmp_path / "g.bin"), "--updates", str(tmp_path / "u.bin"), "--batch", "5",
                  "--src", "3", "--out", str(out)]) == EXIT_OK
-    for f in ("dist.csv", "parent.csv"):
+    for f in ("dist.csv", "parent.csv", "activeOnDelete.csv", "activeOnAdd.csv"):
         assert (out / f).read_bytes() == open(g(f"run_sssp_g40/{f}"), "rb").read()

@@ -4,7 +4,7 @@ outputs (golden fixtures) and against the CPU oracle on seeded inputs."""
 import numpy as np
 import pytest
 
-from golden_io import algo_cases, store_cases
+from golden_io import algo_cases, cap_cases, store_cases
 
 pytestmark = pytest.mark.gpu
 
@@ -37,6 +37,15 @@ def assert_store(g, snap, where, weighted=True):
             np.testing.assert_array_equal(seg.weights[live], ew[live], err_msg=f"{where} seg{i} weights")
     off, s, w = g._reverse_snapshot()
     assert sorted_rev(off, s, w) == sorted_rev(*snap.rev), f"{where}: reverse multisets"
+    # nodes_to: the reference's list order and EdgeRef slot identities
+    roff, rs, rseg, ridx, rw = g._reverse_lists()
+    np.testing.assert_array_equal(roff, snap.rev[0], err_msg=f"{where} nodes_to offsets")
+    np.testing.assert_array_equal(rs, snap.rev[1], err_msg=f"{where} nodes_to sources (list order)")
+    if weighted:
+        np.testing.assert_array_equal(rw, snap.rev[2], err_msg=f"{where} nodes_to weights")
+    if snap.revslots is not None:
+        np.testing.assert_array_equal(rseg, snap.revslots[0], err_msg=f"{where} nodes_to segments")
+        np.testing.assert_array_equal(ridx, snap.revslots[1], err_msg=f"{where} nodes_to slot indices")
 
 
 STORE = store_cases()
@@ -67,7 +76,6 @@ def test_store_layout_bit_exact(gd, case):
 
 
 ALGO = algo_cases()
-PROG = {"sssp": "Dynamic dynamicSSSP(", "pr": "Dynamic dynamicPR(", "tc": "Dynamic dynamicTC("}
 
 
 def run_gpu(gd, case):
@@ -78,7 +86,7 @@ def run_gpu(gd, case):
     stream = gd.UpdateStream.from_arrays(r[0].astype(np.uint8), r[1], r[2], r[3])
     inputs = {"sssp": {"src": case.src}, "pr": {"damping": case.damping, "beta": case.beta,
                                                 "maxiter": case.maxiter}, "tc": {}}[case.algo]
-    return gd.run_batches(gd.compile_source(PROG[case.algo]), g, stream, case.batch, inputs)
+    return gd.run_batches(gd.shipped_program(case.algo), g, stream, case.batch, inputs)
 
 
 @pytest.mark.parametrize("case", ALGO, ids=[c.name for c in ALGO])
@@ -97,6 +105,51 @@ def test_algorithm_matches_reference(gd, case):
         assert np.all(np.abs(got - want) <= tol), f"max-abs {np.max(np.abs(got - want))}"
     else:
         assert ctx.return_value == int(case.expect["count"][0])
+    # bool node properties (activeOnDelete / activeOnAdd, affected) and the
+    # reference's property names and order
+    props = [k[5:] for k in case.expect if k.startswith("prop:")]
+    for pn in props:
+        assert ctx.properties[pn].dtype == "bool"
+        np.testing.assert_array_equal(np.asarray(ctx.properties[pn].values(), dtype=np.uint8),
+                                      case.expect[f"prop:{pn}"], err_msg=pn)
+    if case.source == "engine":
+        want = {"sssp": ["dist", "parent", "activeOnDelete", "activeOnAdd"],
+                "pr": ["pagerank", "affected", "outdeg"], "tc": []}[case.algo]
+        assert list(ctx.properties) == want
+
+
+CAPS = cap_cases()
+
+
+@pytest.mark.parametrize("case", CAPS, ids=[c.name for c in CAPS])
+def test_iteration_cap_factor_trips_like_the_reference(gd, case):
+    """run_program(iteration_cap_factor=f) raises DivergenceError exactly
+    where the reference does (interp.py:138-139,800-813)."""
+    e, r = case.edges, case.recs
+    for f, div in zip(case.factors.tolist(), case.diverged.tolist()):
+        g = gd.DynamicGraph.from_arrays(case.n, e[0], e[1], e[2], directed=case.directed, weighted=case.weighted,
+                                        with_reverse=True)
+        stream = gd.UpdateStream.from_arrays(r[0].astype(np.uint8), r[1], r[2], r[3])
+        run = lambda: gd.run_batches(gd.shipped_program("sssp"), g, stream, case.batch, {"src": 0},  # noqa: E731
+                                     iteration_cap_factor=f)
+        if div:
+            with pytest.raises(gd.DivergenceError):
+                run()
+        else:
+            run()
+
+
+def test_static_entries_expose_the_reference_locals(gd):
+    """run_program(entry="staticSSSP"/"staticPR") properties as the
+    reference's: the entry's propNode locals included."""
+    g = gd.DynamicGraph.build([(0, 1, 1), (1, 2, 1), (4, 0, 1)], 5, with_reverse=True)
+    ctx = gd.run_program(gd.shipped_program("pr"), g, {"damping": 0.85, "beta": 1e-3, "maxiter": 100},
+                         entry="staticPR")
+    assert list(ctx.properties) == ["pagerank", "outdeg", "rank_new"]
+    assert ctx.properties["rank_new"].values() == ctx.properties["pagerank"].values()
+    ctx = gd.run_program(gd.shipped_program("sssp"), g, {"src": 0}, entry="staticSSSP")
+    assert list(ctx.properties) == ["dist", "parent", "modified", "modified_nxt"]
+    assert not any(ctx.properties["modified"].values())
 
 
 # -- seeded random cases vs the CPU oracle ----------------------------------------------
@@ -143,7 +196,7 @@ def test_sssp_random_vs_oracle(gd, scale, mi, bs):
     src, dst, w = rmat(scale, 8 * n, rng)
     kind, us, ud, uw = updates(rng, n, src, dst, 4 * bs)
     g = gd.DynamicGraph.from_arrays(n, src, dst, w, weighted=True, with_reverse=True, merge_interval=mi)
-    ctx = gd.run_batches(gd.compile_source(PROG["sssp"]), g, gd.UpdateStream.from_arrays(kind, us, ud, uw), bs,
+    ctx = gd.run_batches(gd.shipped_program("sssp"), g, gd.UpdateStream.from_arrays(kind, us, ud, uw), bs,
                          {"src": 1})
     og = O.OracleGraph(n, src, dst, w, weighted=True, with_reverse=True, merge_interval=mi)
     dist, parent = O.OracleSSSP(og, 1).run_stream(kind, us, ud, uw, bs).read()
@@ -162,7 +215,7 @@ def test_pr_random_vs_oracle(gd, scale, mi, bs):
     kind, us, ud, uw = updates(rng, n, src, dst, 4 * bs, distinct_deletes=True)
     for beta in (1e-3, 1e-10):
         g = gd.DynamicGraph.from_arrays(n, src, dst, with_reverse=True, merge_interval=mi)
-        ctx = gd.run_batches(gd.compile_source(PROG["pr"]), g, gd.UpdateStream.from_arrays(kind, us, ud, uw), bs,
+        ctx = gd.run_batches(gd.shipped_program("pr"), g, gd.UpdateStream.from_arrays(kind, us, ud, uw), bs,
                              {"damping": 0.85, "beta": beta, "maxiter": 100})
         og = O.OracleGraph(n, src, dst, with_reverse=True, merge_interval=mi)
         rank, od = O.OraclePR(og, 0.85, beta, 100).run_stream(kind, us, ud, uw, bs).read()
@@ -181,7 +234,7 @@ def test_tc_random_vs_oracle(gd, scale, mi, bs):
     kind, us, ud, uw = updates(rng, n, src, dst, 4 * bs)
     for directed in (False, True):
         g = gd.DynamicGraph.from_arrays(n, src, dst, directed=directed, merge_interval=mi)
-        ctx = gd.run_batches(gd.compile_source(PROG["tc"]), g, gd.UpdateStream.from_arrays(kind, us, ud, uw), bs,
+        ctx = gd.run_batches(gd.shipped_program("tc"), g, gd.UpdateStream.from_arrays(kind, us, ud, uw), bs,
                              {})
         og = O.OracleGraph(n, src, dst, directed=directed, merge_interval=mi)
         assert ctx.return_value == O.OracleTC(og).run_stream(kind, us, ud, uw, bs).read()
@@ -225,7 +278,7 @@ def test_propagate_flags_with_hubs_outside_the_giant(gd):
 def test_errors_map_to_reference_exceptions(gd):
     g = gd.DynamicGraph.build([(0, 1, 30), (0, 2, 20)], 3, weighted=True, with_reverse=True)
     with pytest.raises(gd.ExecError, match="99"):
-        gd.run_batches(gd.compile_source(PROG["sssp"]), g, gd.UpdateStream([gd.UpdateRecord("a", 0, 99, 1)]), 1,
+        gd.run_batches(gd.shipped_program("sssp"), g, gd.UpdateStream([gd.UpdateRecord("a", 0, 99, 1)]), 1,
                        {"src": 0})
     with pytest.raises(gd.ContractViolation):
         g.update_csr_del(gd.UpdateBatch([gd.UpdateRecord("d", 0, 7)]))
@@ -237,7 +290,7 @@ def test_errors_map_to_reference_exceptions(gd):
     with pytest.raises(gd.ConfigurationError):
         list(g2.nodes_to(1))
     with pytest.raises(gd.ConfigurationError):
-        gd.run_program(gd.compile_source(PROG["pr"]), g2, {"damping": 0.85, "beta": 1e-3, "maxiter": 10},
+        gd.run_program(gd.shipped_program("pr"), g2, {"damping": 0.85, "beta": 1e-3, "maxiter": 10},
                        entry="staticPR")
 
 
@@ -248,10 +301,10 @@ def test_empty_and_edge_cases(gd):
     rep = g.update_csr_del(gd.UpdateBatch([gd.UpdateRecord("d", 0, 1)]))
     assert rep.misses == 1 and rep.applied == 0
     g.merge_deltas()
-    ctx = gd.run_batches(gd.compile_source(PROG["tc"]), gd.DynamicGraph.build([], 3, directed=False),
+    ctx = gd.run_batches(gd.shipped_program("tc"), gd.DynamicGraph.build([], 3, directed=False),
                          gd.UpdateStream([]), 1, {})
     assert ctx.return_value == 0
-    ctx = gd.run_program(gd.compile_source(PROG["sssp"]),
+    ctx = gd.run_program(gd.shipped_program("sssp"),
                          gd.DynamicGraph.build([(0, 2, 5)], 3, weighted=True, with_reverse=True), {"src": 0},
                          entry="staticSSSP")
     assert ctx.properties["dist"].values() == [0, np.iinfo(np.int64).max, 5]

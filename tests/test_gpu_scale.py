@@ -77,7 +77,7 @@ def test_c1_sssp_matches_reference_emitted_openmp(gd):
     (rd, rp), _ = O.ref_run("sssp", n, s, d, w, weighted=True, kind=kind, us=us, ud=ud, uw=uw, batch_size=per,
                             threads=os.cpu_count() or 1, skip_t0=True)
     g = gd.DynamicGraph.from_arrays(n, s, d, w, weighted=True, with_reverse=True)
-    ctx = gd.run_batches(gd.compile_source("Dynamic dynamicSSSP("), g, gd.UpdateStream.from_arrays(kind, us, ud, uw),
+    ctx = gd.run_batches(gd.shipped_program("sssp"), g, gd.UpdateStream.from_arrays(kind, us, ud, uw),
                          per, {"src": 0})
     np.testing.assert_array_equal(ctx.properties["dist"].values(), rd)
     np.testing.assert_array_equal(ctx.properties["parent"].values(), rp)
@@ -96,7 +96,7 @@ def test_c2_pagerank_batch_matches_reference_emitted_openmp(gd):
         ref, _ = O.ref_run("pr", n, s, d, None, kind=kind, us=us, ud=ud, uw=uw, batch_size=per,
                            threads=os.cpu_count() or 1, beta=beta, skip_t0=True)
         g = gd.DynamicGraph.from_arrays(n, s, d, with_reverse=True)
-        ctx = gd.run_batches(gd.compile_source("Dynamic dynamicPR("), g,
+        ctx = gd.run_batches(gd.shipped_program("pr"), g,
                              gd.UpdateStream.from_arrays(kind, us, ud, uw), per,
                              {"damping": 0.85, "beta": beta, "maxiter": 100})
         got = ctx.properties["pagerank"].data
@@ -116,13 +116,13 @@ def test_sssp_dynamic_equals_static_on_final_graph(gd, graph, scale, pct, nbatch
         s, d, w, n = G.grid(scale, scale, seed=5)
     kind, us, ud, uw, per = G.updates(s, d, n, percent=pct, batches=nbatch, seed=9, max_weight=100)
     g = gd.DynamicGraph.from_arrays(n, s, d, w, weighted=True, with_reverse=True)
-    ctx = gd.run_batches(gd.compile_source("Dynamic dynamicSSSP("), g, gd.UpdateStream.from_arrays(kind, us, ud, uw),
+    ctx = gd.run_batches(gd.shipped_program("sssp"), g, gd.UpdateStream.from_arrays(kind, us, ud, uw),
                          per, {"src": 0})
     dist = np.asarray(ctx.properties["dist"].data)
     parent = np.asarray(ctx.properties["parent"].data)
     fs, fd, fw = final_edges(g)
     g2 = gd.DynamicGraph.from_arrays(n, fs, fd, fw, weighted=True, with_reverse=True)
-    st = gd.run_program(gd.compile_source("Dynamic dynamicSSSP("), g2, {"src": 0}, entry="staticSSSP")
+    st = gd.run_program(gd.shipped_program("sssp"), g2, {"src": 0}, entry="staticSSSP")
     np.testing.assert_array_equal(dist, st.properties["dist"].data)
     tree_valid(dist, parent, 0, fs, fd, fw)
 
@@ -134,12 +134,12 @@ def test_tc_dynamic_equals_static_on_final_graph(gd, n, m, pct):
     s, d, _, n = G.uniform(n, m, seed=3, undirected=True)
     kind, us, ud, uw, per = G.updates(s, d, n, percent=pct, batches=2, seed=4, undirected=True)
     g = gd.DynamicGraph.from_arrays(n, s, d, directed=False)
-    ctx = gd.run_batches(gd.compile_source("Dynamic dynamicTC("), g, gd.UpdateStream.from_arrays(kind, us, ud, uw),
+    ctx = gd.run_batches(gd.shipped_program("tc"), g, gd.UpdateStream.from_arrays(kind, us, ud, uw),
                          per, {})
     fs, fd, fw = final_edges(g)
     keep = fs < fd  # each undirected edge once
     g2 = gd.DynamicGraph.from_arrays(n, fs[keep], fd[keep], directed=False)
-    st = gd.run_program(gd.compile_source("Dynamic dynamicTC("), g2, {}, entry="staticTC")
+    st = gd.run_program(gd.shipped_program("tc"), g2, {}, entry="staticTC")
     assert ctx.return_value == st.return_value
 
 
@@ -159,7 +159,7 @@ def test_sssp_near_far_width_does_not_change_results(gd, graph, delta, decr, mon
     monkeypatch.setenv("GD_SSSP_DELTA", delta)
     monkeypatch.setenv("GD_SSSP_DECR", decr)  # 0: the pull fixpoint instead of sweep + push
     g = gd.DynamicGraph.from_arrays(n, s, d, w, weighted=True, with_reverse=True)
-    ctx = gd.run_batches(gd.compile_source("Dynamic dynamicSSSP("), g, gd.UpdateStream.from_arrays(kind, us, ud, uw),
+    ctx = gd.run_batches(gd.shipped_program("sssp"), g, gd.UpdateStream.from_arrays(kind, us, ud, uw),
                          per, {"src": 0})
     og = O.OracleGraph(n, s, d, w, directed=True, weighted=True, with_reverse=True)
     want_d, want_p = O.OracleSSSP(og, 0).run_stream(kind, us, ud, uw, per).read()
@@ -196,7 +196,7 @@ def test_tc_hub_bitmaps_and_work_items_match_oracle(gd, dup):
     uw = np.ones(k, np.int64)
     for bs in (500, 4000):
         g = gd.DynamicGraph.from_arrays(n, s, d, directed=False)
-        ctx = gd.run_batches(gd.compile_source("Dynamic dynamicTC("), g,
+        ctx = gd.run_batches(gd.shipped_program("tc"), g,
                              gd.UpdateStream.from_arrays(kind, us, ud, uw), bs, {})
         og = O.OracleGraph(n, s, d, directed=False)
         assert ctx.return_value == O.OracleTC(og).run_stream(kind, us, ud, uw, bs).read()
