@@ -216,12 +216,13 @@ def load_peaks():
 
 # ------------------------------------------------------------------ reference ----
 
-def reference_run(wl, steps, threads, sample_batches=None):
-    """The reference's own dynamicPR/SSSP/TC (oracle/_ref) on the host cores.
-    Per-batch time = (T_k - T_0)/k as the reference's bench does (cli.py:436-442)."""
+def reference_run(wl, batches, threads):
+    """The reference's own dynamicPR/SSSP/TC (oracle/_ref) on the host cores,
+    over `batches` successive batches.  Per-batch time = (T_k - T_0)/k as the
+    reference's bench does (cli.py:436-442)."""
     from oracle import oracle as O
 
-    k = steps if sample_batches is None else min(steps, sample_batches)
+    k = max(1, int(batches))
     if "ref_sample" in wl:
         wl = {**wl, **wl["ref_sample"]}
     n, s, d, w, kind, us, ud, uw, per = make_inputs(wl, k)
@@ -235,7 +236,7 @@ def reference_run(wl, steps, threads, sample_batches=None):
     used = 1 if algo == "tc" else threads
     log(f"[reference] T0={times[0]:.2f}s Tk={times[1]:.2f}s k={k} per-batch={per_batch:.3f}s wall={time.time()-t:.1f}s")
     return {"value": per / per_batch, "unit": UNIT, "cores": used, "kind": "reference",
-            "per_batch_s": per_batch,
+            "per_batch_s": per_batch, "batches": k, "T0_s": float(times[0]), "Tk_s": float(times[1]),
             "sample": (f"{wl['desc']}: the reference's emitted OpenMP driver "
                        f"({algo}_dynamic_omp.cc + graphdyn_rt.h, g++ -O2 -fopenmp) on {k} successive batches of "
                        f"{per} records, (T_k - T_0)/k per batch (cli.py:436-442); "
@@ -243,6 +244,9 @@ def reference_run(wl, steps, threads, sample_batches=None):
 
 
 # ------------------------------------------------------------------------ ours ----
+
+EXTRAS = ("tc", "sssp-grid")  # BASELINE configs[2] and configs[3], timed in the same default run
+
 
 def main():
     ap = argparse.ArgumentParser()
@@ -253,6 +257,10 @@ def main():
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="pr")
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="time only --workload (by default the PR headline also times TC configs[2] and SSSP "
+                         "configs[3] in the same run, under the 'extras' key)")
+    ap.add_argument("--extra-steps", type=int, default=6, help="timed steps of each extra workload")
     ap.add_argument("--percent", type=float, default=None, help="override the workload's batch percentage")
     ap.add_argument("--force-dist", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--static", action="store_true",
@@ -260,8 +268,8 @@ def main():
                          "(staticSSSP / staticPR / staticTC), on up to 3 batches")
     ap.add_argument("--gen", choices=("fast", "python"), default="fast",
                     help="input generator: fast (parallel) or python (the reference's generate.py, seed-compatible)")
-    ap.add_argument("--ref-batches", type=int, default=1,
-                    help="bounded sample for the reference arm: at most this many batches")
+    ap.add_argument("--ref-batches", type=int, default=3,
+                    help="bounded sample for the reference arm: this many successive batches (>= 1)")
     args = ap.parse_args()
     wl = dict(WORKLOADS[args.workload])
     if args.percent is not None:
@@ -279,16 +287,19 @@ def main():
             return 0
         threads = os.cpu_count() or 1
         try:
-            cb = reference_run(wl, args.steps, threads, sample_batches=args.ref_batches)
+            cb = reference_run(wl, args.ref_batches, threads)
         except Exception as exc:  # noqa: BLE001
             print(json.dumps({"impl": "reference", "unavailable": f"{type(exc).__name__}: {exc}"}))
             return 0
+        # steps = the batches actually timed (T_k - T_0 over k successive batches)
         line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": args.gpus,
-                "steps": args.steps, "warmup": args.warmup, "ms_per_step": cb["per_batch_s"] * 1e3,
+                "steps": cb["batches"], "warmup": 0, "ms_per_step": cb["per_batch_s"] * 1e3,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": _dtype(wl),
                 "data": "synthetic", "config": _config(wl, args, world),
                 "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
-                "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+                "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+                "reference_timing": {"T0_s": cb["T0_s"], "Tk_s": cb["Tk_s"], "batches": cb["batches"],
+                                     "requested_steps": args.steps}}
         print(json.dumps(line))
         return 0
 
@@ -305,7 +316,70 @@ def main():
     import paper_2507_11094_b200 as gd
 
     e2e_steps = args.e2e_steps if args.e2e_steps is not None else max(1, min(args.steps, 10))
-    nb = args.warmup + args.steps + 1 + e2e_steps  # +1: the untimed e2e warm-up step
+    res = run_ours(gd, torch, wl, args, args.steps, args.warmup, e2e_steps, world, rank, local, dist_on,
+                   static=args.static)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = _cpu_baseline(wl, args.ref_batches)
+
+    extras = None
+    if world == 1 and not dist_on and not args.no_extras and args.workload == "pr" and args.percent is None:
+        extras = {}
+        for name in EXTRAS:
+            xwl = dict(WORKLOADS[name])
+            try:
+                xr = run_ours(gd, torch, xwl, args, args.extra_steps, max(3, min(args.warmup, 3)),
+                              max(1, min(args.extra_steps, 4)), world, rank, local, dist_on, static=False)
+                xr["config"] = _config(xwl, args, world)
+                xr["dtype"] = _dtype(xwl)
+                if not args.no_cpu_baseline:
+                    xr["cpu_baseline"] = _cpu_baseline(xwl, 1)
+                extras[name] = xr
+            except Exception as exc:  # noqa: BLE001
+                extras[name] = {"error": f"{type(exc).__name__}: {exc}"}
+            torch.cuda.empty_cache()
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": res["ms_per_step"], "higher_is_better": True,
+            "scaling": res["scaling"], "vs_baseline": None, "dtype": _dtype(wl),
+            "data": "synthetic", "config": _config(wl, args, world),
+            "e2e": res["e2e"],
+            "gpu_launches": res["gpu_launches"],
+            "roofline": res["roofline"],
+            "kernels": res["kernels"],
+            "cpu_baseline": cpu,
+            "clocks": res["clocks"],
+            "records_per_step": res["records_per_step"],
+        }
+        if res.get("comm") is not None:
+            line["comm"] = res["comm"]
+        if res.get("static") is not None:
+            line["static"] = res["static"]
+        if extras is not None:
+            line["extras"] = extras
+        print(json.dumps(line))
+    if dist_on:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def _cpu_baseline(wl, batches):
+    try:
+        cb = reference_run(wl, batches, os.cpu_count() or 1)
+        return {k_: cb[k_] for k_ in ("value", "unit", "cores", "kind", "sample")}
+    except Exception as exc:  # noqa: BLE001
+        return {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
+                "sample": f"unavailable: {type(exc).__name__}: {exc}"}
+
+
+def run_ours(gd, torch, wl, args, steps, warmup, e2e_steps, world, rank, local, dist_on, static=False):
+    """One workload on the device path: W warm-up steps, K timed steps with
+    inputs resident in HBM (CUDA events on the store's stream, max over
+    ranks), then e2e steps through the host-buffer C-ABI call."""
+    nb = warmup + steps + 1 + e2e_steps  # +1: the untimed e2e warm-up step
     # sharded PR / TC: every rank holds a replica of ONE job's store, so all
     # ranks build the same graph and stream; SSSP replicas each get their own
     one_job = dist_on and wl["algo"] in ("pr", "tc")
@@ -322,8 +396,10 @@ def main():
     else:
         algo = gd.TCHandle(g)
     torch.cuda.synchronize()
-    log(f"[bench] store + static pass: {time.time() - t:.1f}s; device bytes {g.device_bytes() / 2**30:.2f} GiB")
+    log(f"[bench] {wl['algo']}: store + static pass: {time.time() - t:.1f}s; "
+        f"device bytes {g.device_bytes() / 2**30:.2f} GiB")
     sharded = dist_on and wl["algo"] in ("pr", "tc")
+    comm = None
     if sharded:  # vertex-range PR pull + NCCL all-gather / record-sliced TC + all-reduce
         from paper_2507_11094_b200.dist import Communicator
 
@@ -343,7 +419,7 @@ def main():
         return b - a
 
     stream = torch.cuda.ExternalStream(_graph_stream(g))
-    for i in range(args.warmup):
+    for i in range(warmup):
         dev_step(i)
     torch.cuda.synchronize()
 
@@ -363,7 +439,7 @@ def main():
     ev1 = torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
     done = 0
-    for i in range(args.warmup, args.warmup + args.steps):
+    for i in range(warmup, warmup + steps):
         done += dev_step(i)
     ev1.record(stream)
     torch.cuda.synchronize()
@@ -375,7 +451,7 @@ def main():
     comm_stats = None
     if sharded:  # CommStats analogue: NCCL traffic of this rank per timed step
         cs = comm.stats()
-        comm_stats = {k: v / args.steps for k, v in cs.items()}
+        comm_stats = {k: v / steps for k, v in cs.items()}
         comm_stats["per"] = "rank and step"
     clocks.mark(wall0, time.time())
     clk = clocks.stop()
@@ -395,13 +471,13 @@ def main():
                           dtype=torch.float64 if wl["algo"] == "pr" else torch.int64).pin_memory()
     # one untimed step through the host-buffer path first (creates the copy
     # stream and the snapshot buffers of the asynchronous read-back)
-    wi = args.warmup + args.steps
+    wi = warmup + steps
     wa, wb = wi * per, min((wi + 1) * per, len(kind))
     if wb > wa:
         _host_batch(gd, algo, pin, wa, wb - wa, wi)
         _read_result(gd, algo, wl, out_pin, n)
         gd._native.check(gd._native.lib().gd_wait(algo.h))
-    e_start = args.warmup + args.steps + 1
+    e_start = warmup + steps + 1
     h2d = d2h = 0
     if dist_on:
         torch.distributed.barrier()
@@ -437,7 +513,7 @@ def main():
     e2e_value = (e_done * (1 if (dist_on and wl["algo"] in ("pr", "tc")) else world)) / (e2e_ms / 1e3) \
         if e2e_ms > 0 else None
 
-    static = _static_compare(gd, torch, wl, args, local, n, s, d, w, kind, us, ud, uw, per) if args.static else None
+    stat = _static_compare(gd, torch, wl, args, local, n, s, d, w, kind, us, ud, uw, per) if static else None
 
     shards = dist_on and wl["algo"] in ("pr", "tc")  # one job over all GPUs vs independent replicas
     value = (done * (1 if shards else world)) / (elapsed_ms / 1e3)
@@ -450,48 +526,26 @@ def main():
         avg_ms = ms / nl
         ach = (b_per_launch / 1e9) / (avg_ms / 1e3) if b_per_launch else None
         roof = {"bound": "hbm", "kernel": name, "achieved": ach, "peak": peak, "unit": "GB/s",
-                "frac": (ach / peak) if ach else None, "traffic": _ncu_traffic(args.workload, name),
+                "frac": (ach / peak) if ach else None, "traffic": _ncu_traffic(wl, name),
                 "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured" else
                 "fallback 6.65 TB/s (B200_PROFILING.md)",
                 "bytes_per_launch": b_per_launch, "avg_launch_ms": avg_ms, "launches": nl,
                 "share_of_step": ms / elapsed_ms if elapsed_ms else None}
-
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        try:
-            cb = reference_run(wl, args.steps, os.cpu_count() or 1, sample_batches=args.ref_batches)
-            cpu = {k_: cb[k_] for k_ in ("value", "unit", "cores", "kind", "sample")}
-        except Exception as exc:  # noqa: BLE001
-            cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
-                   "sample": f"unavailable: {type(exc).__name__}: {exc}"}
-
-    if rank == 0:
-        line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
-            "scaling": "strong" if shards else "weak", "vs_baseline": None, "dtype": _dtype(wl),
-            "data": "synthetic", "config": _config(wl, args, world),
-            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d // max(e2e_steps, 1),
-                    "d2h_bytes_per_step": d2h // max(e2e_steps, 1), "steps": e2e_steps,
-                    "ms_per_step": e2e_ms / max(e2e_steps, 1)},
-            "gpu_launches": int(launches),
-            "roofline": roof,
-            "kernels": {k_: {"ms_total": v[0], "launches": v[1], "share": v[0] / elapsed_ms,
-                             "gbs": (v[2] / 1e9) / (v[0] / 1e3) if v[2] and v[0] else None}
-                        for k_, v in sorted(kstats.items(), key=lambda kv: -kv[1][0])},
-            "cpu_baseline": cpu,
-            "clocks": clk,
-            "records_per_step": records_per_step,
-        }
-        if comm_stats is not None:
-            line["comm"] = comm_stats
-        if static is not None:
-            static["dynamic_speedup"] = static["ms_per_step"] / (elapsed_ms / args.steps)
-            line["static"] = static
-        print(json.dumps(line))
-    if dist_on:
-        torch.distributed.destroy_process_group()
-    return 0
+    out = {"value": value, "ms_per_step": elapsed_ms / steps, "steps": steps, "warmup": warmup,
+           "scaling": "strong" if shards else "weak",
+           "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d // max(e2e_steps, 1),
+                   "d2h_bytes_per_step": d2h // max(e2e_steps, 1), "steps": e2e_steps,
+                   "ms_per_step": e2e_ms / max(e2e_steps, 1)},
+           "gpu_launches": int(launches), "roofline": roof,
+           "kernels": {k_: {"ms_total": v[0], "launches": v[1], "share": v[0] / elapsed_ms,
+                            "gbs": (v[2] / 1e9) / (v[0] / 1e3) if v[2] and v[0] else None}
+                       for k_, v in sorted(kstats.items(), key=lambda kv: -kv[1][0])},
+           "clocks": clk, "records_per_step": records_per_step, "comm": comm_stats}
+    if stat is not None:
+        stat["dynamic_speedup"] = stat["ms_per_step"] / (elapsed_ms / steps)
+        out["static"] = stat
+    del algo, g
+    return out
 
 
 def _static_compare(gd, torch, wl, args, local, n, s, d, w, kind, us, ud, uw, per):
@@ -572,14 +626,15 @@ def _read_result(gd, algo, wl, out_pin, n):
     return 8
 
 
-def _ncu_traffic(workload, name):
+def _ncu_traffic(wl, name):
     """Per-launch DRAM bytes of `name` from the committed `ncu --set full`
     capture of this workload (tools/summarize_profiles.py), else None."""
     p = os.path.join(REPO, "profiles", "ncu_traffic.json")
+    key = next((k for k, v in WORKLOADS.items() if v["desc"] == wl["desc"]), None)
     try:
         with open(p) as fh:
             t = json.load(fh)
-        return t.get(f"{workload}/{name}", t.get(name) if workload == "pr" else None)
+        return t.get(f"{key}/{name}")
     except Exception:
         return None
 

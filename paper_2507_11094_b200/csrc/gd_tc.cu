@@ -92,7 +92,7 @@ __global__ void k_tc_prep(const int32_t* s, const int32_t* d, int64_t k, IdxView
         int64_t dS = walk_u ? du : dv, dL = walk_u ? dv : du;
         r.L[i] = L;
         r.S[i] = S;
-        const bool sh = dS <= 64;  // kShortWalk: a sub-warp group takes it whole
+        const bool sh = dS <= 64;  // kShortWalk: a sub-warp group takes it whole (kernel below)
         isshort[i] = sh;
         r.nch[i] = sh ? 0 : (dS + kWalkChunk - 1) / kWalkChunk;
         if (dL >= kBmDeg) hubmark[L] = 1;
@@ -210,14 +210,114 @@ __global__ void __launch_bounds__(kThreads) k_tc_count(const int32_t* s, const i
     if (lane == 0 && acc) atomicAdd(total, (unsigned long long)acc);
 }
 
-// short records (walk <= kShortWalk arcs): 8 lanes each, 4 records per warp
-// in flight instead of one latency chain per warp
+// Short records, first pass: every record of the phase.  A group of kMG
+// lanes takes one record (32/kMG per warp in flight) and, when both rows are
+// short -- S <= kShortWalk arcs and L <= kStageL, i.e. every record of a
+// uniform graph -- counts it here as a sorted MERGE (SURVEY.md §8(d):
+// (deg u + deg v) * idx, streamed).  Both rows are staged in shared memory
+// with 16-byte loads aligned to the 16-byte grid, so each sector of a row is
+// requested once; then every lane takes a contiguous slice of S's row, finds
+// its start in L by one binary search and walks both rows forward.
+// Multiplicities are the runs of equal entries in L, so parallel arcs count
+// as the reference's slot pairs do.  Records with a long row are appended to
+// a deferred list for the lookup-based kernels below.
 constexpr int kShortWalk = 64;
-constexpr int kShortG = 8;
+constexpr int kStageL = 128;
+#ifndef GD_TC_MG
+#define GD_TC_MG 8
+#endif
+constexpr int kMG = GD_TC_MG;
+#ifndef GD_TCM_MINB
+#define GD_TCM_MINB 6
+#endif
 
-// 8 resident CTAs (32 registers, a 40-byte spill): the random neighbour
-// lookups want warps in flight more than registers; C3 tc_count 1.10 ->
-// 0.88 ms per batch (A/B, gpu_variants.sh)
+__device__ __forceinline__ int64_t skip_mult(int32_t u, int32_t v, int32_t w, int64_t rk, int64_t n, int64_t m,
+                                             const int64_t* R, int64_t nr, const uint32_t* filt, uint64_t fmask) {
+    int64_t ru = pair_rank(u, w, n), rv = pair_rank(v, w, n);
+    bool skip = (ru < rk && maybe_in(filt, fmask, ru) && in_sorted(R, nr, ru)) ||
+                (rv < rk && maybe_in(filt, fmask, rv) && in_sorted(R, nr, rv));
+    return skip ? 0 : m;
+}
+
+// coalesced 16-byte staging of col[a, b) into buf; returns a's offset in buf
+__device__ __forceinline__ int stage_row(const int32_t* col, int64_t a, int64_t b, int32_t* buf, int gl) {
+    const int64_t a4 = a >> 2;
+    const int nq = (int)(((b + 3) >> 2) - a4);
+    const int4* src = reinterpret_cast<const int4*>(col) + a4;
+    for (int q = gl; q < nq; q += kMG) reinterpret_cast<int4*>(buf)[q] = src[q];
+    return (int)(a & 3);
+}
+
+__global__ void __launch_bounds__(kThreads, GD_TCM_MINB) k_tc_merge(const int32_t* s, const int32_t* d, int64_t k,
+                                                                    IdxView ix, int64_t n, const int64_t* R, int64_t nr,
+                                                                    const uint32_t* filt, uint64_t fmask,
+                                                                    int32_t* defer, unsigned long long* ndefer,
+                                                                    unsigned long long* total) {
+    __shared__ __align__(16) int32_t stS[kThreads / kMG][kShortWalk + 8];
+    __shared__ __align__(16) int32_t stL[kThreads / kMG][kStageL + 8];
+    const int gl = threadIdx.x & (kMG - 1), gw = (threadIdx.x & 31) / kMG;
+    const unsigned gmask = (kMG == 32 ? 0xffffffffu : ((1u << kMG) - 1)) << ((threadIdx.x & 31) & ~(kMG - 1));
+    constexpr int kPer = 32 / kMG;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    int32_t* sS = stS[threadIdx.x / kMG];
+    int32_t* sL = stL[threadIdx.x / kMG];
+    int64_t acc = 0;
+    unsigned long long bytes = 0;
+    for (int64_t t0 = warp * kPer; t0 < k; t0 += nwarps * kPer) {
+        const int64_t i = t0 + gw;
+        if (i >= k) continue;
+        const int32_t u = s[i], v = d[i];
+        const int64_t ua = ix.off[u], ub = ix.off[u + 1], va = ix.off[v], vb = ix.off[v + 1];
+        const bool walk_u = ub - ua <= vb - va;  // walk the shorter row (ties: u)
+        const int64_t sa = walk_u ? ua : va, sb = walk_u ? ub : vb;
+        const int64_t la = walk_u ? va : ua, lb = walk_u ? vb : ub;
+        const int ns = (int)(sb - sa), nl = (int)(lb - la);
+        if (sb - sa > kShortWalk || lb - la > kStageL) {
+            if (gl == 0) defer[atomicAdd(ndefer, 1ULL)] = (int32_t)i;
+            continue;
+        }
+        if (gl == 0) bytes += 32 + 4 * (unsigned long long)(ns + nl);
+        const int s0 = stage_row(ix.col, sa, sb, sS, gl);
+        const int l0 = stage_row(ix.col, la, lb, sL, gl);
+        __syncwarp(gmask);
+        const int c = (ns + kMG - 1) / kMG;
+        int e = s0 + gl * c;
+        const int e1 = min(e + c, s0 + ns), l1 = l0 + nl;
+        if (e < e1) {
+            const int64_t rk = pair_rank(u, v, n);
+            const int32_t w0 = sS[e];
+            int lo = l0, hi = l1;  // first entry of L >= w0
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (sL[mid] < w0) lo = mid + 1;
+                else hi = mid;
+            }
+            int p = lo;
+            for (; e < e1 && p < l1; ++e) {
+                const int32_t w = sS[e];
+                while (p < l1 && sL[p] < w) ++p;
+                if (w < 0 || w == v) continue;
+                int r = p;
+                while (r < l1 && sL[r] == w) ++r;
+                if (r > p) acc += skip_mult(u, v, w, rk, n, r - p, R, nr, filt, fmask);
+            }
+        }
+        __syncwarp(gmask);  // the group's buffers are reused by its next record
+    }
+    for (int o = 16; o; o >>= 1) {
+        acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        bytes += __shfl_xor_sync(0xffffffffu, bytes, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (acc) atomicAdd(total, (unsigned long long)acc);
+        if (bytes) atomicAdd(total + 1, bytes);
+    }
+}
+
+// Deferred records whose walk is still short (S <= kShortWalk arcs, L a long
+// row): 8 lanes each, 4 records per warp in flight, lookups per neighbour.
+constexpr int kShortG = 8;
 #ifndef GD_TCS_MINB
 #define GD_TCS_MINB 8
 #endif
@@ -244,6 +344,14 @@ __global__ void __launch_bounds__(kThreads, GD_TCS_MINB) k_tc_count_short(const 
     }
     for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if ((threadIdx.x & 31) == 0 && acc) atomicAdd(total, (unsigned long long)acc);
+}
+
+__global__ void k_tc_gather_rec(const int32_t* s, const int32_t* d, const int32_t* idx, int64_t m, int32_t* os,
+                                int32_t* od) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < m; j += (int64_t)gridDim.x * blockDim.x) {
+        os[j] = s[idx[j]];
+        od[j] = d[idx[j]];
+    }
 }
 
 // staticTC (tc_dynamic.sp:7-19): sum over arcs (v,a), a > v, and arcs (a,b),
@@ -286,99 +394,122 @@ int64_t TC::count_records(const int32_t* s, const int32_t* d, int64_t k) {
     const uint64_t fmask = (uint64_t(1) << fbits) - 1;
     GD_KERNEL(k_ranks, grid_for(k, 256), 256, 0, st, s, d, k, n, R.get(), filt.get(), fmask);
     sort_keys_u64(st, R.get(), k);
-    DBuf<unsigned long long> ctr(2, st);  // [0] count delta, [1] algorithmic bytes
+    DBuf<unsigned long long> ctr(3, st);  // [0] count delta, [1] algorithmic bytes, [2] deferred records
     ctr.zero(st);
     // ranks are over ALL records of the phase; the counted slice is this rank's
     const int64_t a = comm ? k * comm->rank / comm->world : 0;
     const int64_t b = comm ? k * (comm->rank + 1) / comm->world : k;
     const int64_t m = b - a;
+    const int64_t* Rp = reinterpret_cast<const int64_t*>(R.get());
     if (m > 0) {
-        if (hubmark.n < (size_t)n) {
-            hubmark.alloc(n, st);
-            hubmark.zero(st);
-            hub_slot.alloc(n, st);
-            fill_i32(st, hub_slot.get(), n, -1);
-        }
-        DBuf<int32_t> L(m, st), S(m, st);
-        DBuf<int64_t> nch(m + 1, st), choff(m + 1, st);
-        GD_CUDA(cudaMemsetAsync(nch.get() + m, 0, sizeof(int64_t), st));
-        TcRec rr{L.get(), S.get(), nch.get()};
-        DBuf<uint8_t> isshort(m, st);
-        GD_KERNEL(k_tc_prep, grid_for(m, 256), 256, 0, st, s + a, d + a, m, ix.view(), rr, hubmark.get(),
-                  isshort.get(), ctr.get() + 1);
-        DBuf<int32_t> shortl(m, st);
-        DBuf<int64_t> nshort(1, st);
-        select_flagged_index_async(st, isshort.get(), m, shortl.get(), nshort.get());
-        // hubs of this phase (L endpoints with >= kBmDeg arcs) and the work
-        // item total, read back together
-        exclusive_scan_i64(st, nch.get(), choff.get(), m + 1);
-        DBuf<int32_t> hubs(n, st);
-        DBuf<int64_t> cnt2(2, st);
-        GD_CUDA(cudaMemcpyAsync(cnt2.get(), choff.get() + m, sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
-        select_flagged_index_async(st, hubmark.get(), n, hubs.get(), cnt2.get() + 1);
-        int64_t hc[2];
-        read_small(st, hc, cnt2.get(), sizeof hc);
-        const int64_t nwork = hc[0], nhubs = hc[1];
-        // with hub rows in play, work items go in L order: warps running side
-        // by side (grid-stride neighbours) meet the same long rows and share
-        // their L2 lines; without hubs the record order stands
-        DBuf<int32_t> perm;
-        if (nhubs > 0) {
-            DBuf<uint32_t> lkey(m, st);
-            perm.alloc(m, st);
-            GD_KERNEL(k_tc_lkeys, grid_for(m, 256), 256, 0, st, L.get(), m, lkey.get(), perm.get());
-            sort_pairs_u32(st, lkey.get(), perm.get(), m, bits_for((uint64_t)std::max<int64_t>(n - 1, 1)));
-            DBuf<int64_t> nchp(m + 1, st);
-            GD_KERNEL(k_tc_perm_nch, grid_for(m + 1, 256), 256, 0, st, perm.get(), nch.get(), m, nchp.get());
-            exclusive_scan_i64(st, nchp.get(), choff.get(), m + 1);
-        }
-        rr.nch = choff.get();
-        // work items: exact count (records may share a long S row)
-        DBuf<int32_t> rec_of(std::max<int64_t>(nwork, 1), st);
-        GD_KERNEL(k_tc_chunk_table, grid_for(m, 256), 256, 0, st, choff.get(), m, rec_of.get());
-        // bitmaps for as many hubs as the budget allows (grow-only; every
-        // phase leaves them clean)
-        const int64_t words = (n + 31) / 32;
-        const int64_t hmax = std::min<int64_t>(nhubs, kBmBudget / (words * 4));
-        if (hmax > 0 && bm.n < (size_t)(hmax * words)) {
-            bm.alloc((size_t)(hmax * words), st);
-            GD_CUDA(cudaMemsetAsync(bm.get(), 0, bm.n * 4, st));
-            bm_multi.alloc(hmax, st);
-            bm_multi.zero(st);
-        }
-        const int64_t* nhub = cnt2.get() + 1;
-        if (hmax > 0) {
-            GD_KERNEL(k_tc_hub_slots, grid_for(hmax, 256), 256, 0, st, hubs.get(), nhub, hmax, hub_slot.get());
-            GD_KERNEL_T("tc_bitmap", 0, k_tc_bitmaps, 148 * 4, 256, 0, st, hubs.get(), nhub, hmax, ix.view(), words,
-                        bm.get(), bm_multi.get(), false);
-        }
+        DBuf<int32_t> defer(m, st);
         int pi = prof_begin("tc_count", 0, st);
-        k_tc_count<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((nwork + 7) / 8, 148 * 16)), kThreads, 0,
-                     st>>>(s + a, d + a, rr, nhubs > 0 ? perm.get() : nullptr, rec_of.get(), choff.get() + m, ix.view(), n,
-                                                 reinterpret_cast<const int64_t*>(R.get()), k, hub_slot.get(),
-                                                 bm.get(), words, bm_multi.get(), filt.get(), fmask, ctr.get());
-        count_launch();
-        GD_LAUNCH_CHECK();
-        k_tc_count_short<<<148 * 16, kThreads, 0, st>>>(s + a, d + a, rr, shortl.get(), nshort.get(), ix.view(), n,
-                                                        reinterpret_cast<const int64_t*>(R.get()), k, hub_slot.get(),
-                                                        bm.get(), words, bm_multi.get(), filt.get(), fmask,
-                                                        ctr.get());
+        k_tc_merge<<<148 * 16, kThreads, 0, st>>>(s + a, d + a, m, ix.view(), n, Rp, k, filt.get(), fmask,
+                                                   defer.get(), ctr.get() + 2, ctr.get());
         count_launch();
         GD_LAUNCH_CHECK();
         prof_end(pi, st);
-        if (hmax > 0)
-            GD_KERNEL_T("tc_bitmap", 0, k_tc_bitmaps, 148 * 4, 256, 0, st, hubs.get(), nhub, hmax, ix.view(), words,
-                        bm.get(), bm_multi.get(), true);
-        if (nhubs > 0)
-            GD_KERNEL(k_tc_reset, grid_for(nhubs, 256), 256, 0, st, hubs.get(), nhub, hubmark.get(), hub_slot.get());
         if (pi >= 0) count_rec.push_back(pi);
+        const int64_t md = (int64_t)read_scalar(st, ctr.get() + 2);
+        if (md > 0) {
+            DBuf<int32_t> ds(md, st), dd(md, st);
+            GD_KERNEL(k_tc_gather_rec, grid_for(md, 256), 256, 0, st, s + a, d + a, defer.get(), md, ds.get(),
+                      dd.get());
+            count_deferred(ds.get(), dd.get(), md, Rp, k, filt.get(), fmask, ctr.get());
+        }
     }
     if (comm) comm->allreduce_sum_i64(reinterpret_cast<int64_t*>(ctr.get()), 1, st);
     unsigned long long h[2];
     read_small(st, h, ctr.get(), sizeof h);
-    for (int pi : count_rec) prof.pending[(size_t)pi].bytes = (int64_t)h[1];
+    for (size_t j = 0; j < count_rec.size(); ++j) prof.pending[(size_t)count_rec[j]].bytes = j ? 0 : (int64_t)h[1];
     count_rec.clear();
     return (int64_t)h[0];
+}
+
+// records with a long row: one walk per record, per-neighbour lookups in L
+// (hub bitmap or binary search), long walks cut into work items
+void TC::count_deferred(const int32_t* s, const int32_t* d, int64_t m, const int64_t* R, int64_t k,
+                        const uint32_t* filt, uint64_t fmask, unsigned long long* ctr) {
+    cudaStream_t st = stream();
+    SortedIndex& ix = g->tc_index();
+    const int64_t n = g->n;
+    if (hubmark.n < (size_t)n) {
+        hubmark.alloc(n, st);
+        hubmark.zero(st);
+        hub_slot.alloc(n, st);
+        fill_i32(st, hub_slot.get(), n, -1);
+    }
+    DBuf<int32_t> L(m, st), S(m, st);
+    DBuf<int64_t> nch(m + 1, st), choff(m + 1, st);
+    GD_CUDA(cudaMemsetAsync(nch.get() + m, 0, sizeof(int64_t), st));
+    TcRec rr{L.get(), S.get(), nch.get()};
+    DBuf<uint8_t> isshort(m, st);
+    GD_KERNEL(k_tc_prep, grid_for(m, 256), 256, 0, st, s, d, m, ix.view(), rr, hubmark.get(), isshort.get(),
+              ctr + 1);
+    DBuf<int32_t> shortl(m, st);
+    DBuf<int64_t> nshort(1, st);
+    select_flagged_index_async(st, isshort.get(), m, shortl.get(), nshort.get());
+    // hubs of this phase (L endpoints with >= kBmDeg arcs) and the work
+    // item total, read back together
+    exclusive_scan_i64(st, nch.get(), choff.get(), m + 1);
+    DBuf<int32_t> hubs(n, st);
+    DBuf<int64_t> cnt2(2, st);
+    GD_CUDA(cudaMemcpyAsync(cnt2.get(), choff.get() + m, sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
+    select_flagged_index_async(st, hubmark.get(), n, hubs.get(), cnt2.get() + 1);
+    int64_t hc[2];
+    read_small(st, hc, cnt2.get(), sizeof hc);
+    const int64_t nwork = hc[0], nhubs = hc[1];
+    // with hub rows in play, work items go in L order: warps running side
+    // by side (grid-stride neighbours) meet the same long rows and share
+    // their L2 lines; without hubs the record order stands
+    DBuf<int32_t> perm;
+    if (nhubs > 0) {
+        DBuf<uint32_t> lkey(m, st);
+        perm.alloc(m, st);
+        GD_KERNEL(k_tc_lkeys, grid_for(m, 256), 256, 0, st, L.get(), m, lkey.get(), perm.get());
+        sort_pairs_u32(st, lkey.get(), perm.get(), m, bits_for((uint64_t)std::max<int64_t>(n - 1, 1)));
+        DBuf<int64_t> nchp(m + 1, st);
+        GD_KERNEL(k_tc_perm_nch, grid_for(m + 1, 256), 256, 0, st, perm.get(), nch.get(), m, nchp.get());
+        exclusive_scan_i64(st, nchp.get(), choff.get(), m + 1);
+    }
+    rr.nch = choff.get();
+    // work items: exact count (records may share a long S row)
+    DBuf<int32_t> rec_of(std::max<int64_t>(nwork, 1), st);
+    GD_KERNEL(k_tc_chunk_table, grid_for(m, 256), 256, 0, st, choff.get(), m, rec_of.get());
+    // bitmaps for as many hubs as the budget allows (grow-only; every
+    // phase leaves them clean)
+    const int64_t words = (n + 31) / 32;
+    const int64_t hmax = std::min<int64_t>(nhubs, kBmBudget / (words * 4));
+    if (hmax > 0 && bm.n < (size_t)(hmax * words)) {
+        bm.alloc((size_t)(hmax * words), st);
+        GD_CUDA(cudaMemsetAsync(bm.get(), 0, bm.n * 4, st));
+        bm_multi.alloc(hmax, st);
+        bm_multi.zero(st);
+    }
+    const int64_t* nhub = cnt2.get() + 1;
+    if (hmax > 0) {
+        GD_KERNEL(k_tc_hub_slots, grid_for(hmax, 256), 256, 0, st, hubs.get(), nhub, hmax, hub_slot.get());
+        GD_KERNEL_T("tc_bitmap", 0, k_tc_bitmaps, 148 * 4, 256, 0, st, hubs.get(), nhub, hmax, ix.view(), words,
+                    bm.get(), bm_multi.get(), false);
+    }
+    int pi = prof_begin("tc_count", 0, st);
+    k_tc_count<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((nwork + 7) / 8, 148 * 16)), kThreads, 0, st>>>(
+        s, d, rr, nhubs > 0 ? perm.get() : nullptr, rec_of.get(), choff.get() + m, ix.view(), n, R, k,
+        hub_slot.get(), bm.get(), words, bm_multi.get(), filt, fmask, ctr);
+    count_launch();
+    GD_LAUNCH_CHECK();
+    k_tc_count_short<<<148 * 16, kThreads, 0, st>>>(s, d, rr, shortl.get(), nshort.get(), ix.view(), n, R, k,
+                                                    hub_slot.get(), bm.get(), words, bm_multi.get(), filt, fmask,
+                                                    ctr);
+    count_launch();
+    GD_LAUNCH_CHECK();
+    prof_end(pi, st);
+    if (hmax > 0)
+        GD_KERNEL_T("tc_bitmap", 0, k_tc_bitmaps, 148 * 4, 256, 0, st, hubs.get(), nhub, hmax, ix.view(), words,
+                    bm.get(), bm_multi.get(), true);
+    if (nhubs > 0)
+        GD_KERNEL(k_tc_reset, grid_for(nhubs, 256), 256, 0, st, hubs.get(), nhub, hubmark.get(), hub_slot.get());
+    if (pi >= 0) count_rec.push_back(pi);
 }
 
 TC::TC(Store* st) : AlgoBase(ALGO_TC, st) {

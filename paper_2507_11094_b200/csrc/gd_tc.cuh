@@ -21,6 +21,8 @@ struct TC : AlgoBase {
 
   private:
     int64_t count_records(const int32_t* s, const int32_t* d, int64_t k);
+    void count_deferred(const int32_t* s, const int32_t* d, int64_t m, const int64_t* R, int64_t k,
+                        const uint32_t* filt, uint64_t fmask, unsigned long long* ctr);
 };
 
 }  // namespace gdb
