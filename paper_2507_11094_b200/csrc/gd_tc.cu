@@ -253,15 +253,15 @@ __global__ void __launch_bounds__(kThreads, GD_TCM_MINB) k_tc_merge(const int32_
                                                                     const uint32_t* filt, uint64_t fmask,
                                                                     int32_t* defer, unsigned long long* ndefer,
                                                                     unsigned long long* total) {
-    __shared__ __align__(16) int32_t stS[kThreads / kMG][kShortWalk + 8];
-    __shared__ __align__(16) int32_t stL[kThreads / kMG][kStageL + 8];
+    extern __shared__ __align__(16) int32_t tc_smem[];  // per group: S row, then L row
+    constexpr int kSW = kShortWalk + 8, kLW = kStageL + 8;
     const int gl = threadIdx.x & (kMG - 1), gw = (threadIdx.x & 31) / kMG;
     const unsigned gmask = (kMG == 32 ? 0xffffffffu : ((1u << kMG) - 1)) << ((threadIdx.x & 31) & ~(kMG - 1));
     constexpr int kPer = 32 / kMG;
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    int32_t* sS = stS[threadIdx.x / kMG];
-    int32_t* sL = stL[threadIdx.x / kMG];
+    int32_t* sS = tc_smem + (threadIdx.x / kMG) * (kSW + kLW);
+    int32_t* sL = sS + kSW;
     int64_t acc = 0;
     unsigned long long bytes = 0;
     for (int64_t t0 = warp * kPer; t0 < k; t0 += nwarps * kPer) {
@@ -404,7 +404,12 @@ int64_t TC::count_records(const int32_t* s, const int32_t* d, int64_t k) {
     if (m > 0) {
         DBuf<int32_t> defer(m, st);
         int pi = prof_begin("tc_count", 0, st);
-        k_tc_merge<<<148 * 16, kThreads, 0, st>>>(s + a, d + a, m, ix.view(), n, Rp, k, filt.get(), fmask,
+        static const int smem = [] {
+            const int b = (kThreads / kMG) * (kShortWalk + 8 + kStageL + 8) * 4;
+            GD_CUDA(cudaFuncSetAttribute(k_tc_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+            return b;
+        }();
+        k_tc_merge<<<148 * 16, kThreads, smem, st>>>(s + a, d + a, m, ix.view(), n, Rp, k, filt.get(), fmask,
                                                    defer.get(), ctr.get() + 2, ctr.get());
         count_launch();
         GD_LAUNCH_CHECK();
