@@ -310,6 +310,7 @@ def ref_run(algo: str, n, src, dst, w, *, directed=True, weighted=False, merge_i
         res = (o_a[:n], o_b[:n])
     elif a == 1:
         res = o_f[:n]
+        ref_run.last_outdeg = o_a[:n]  # live out-degree of the final graph
     else:
         res = int(o_a[0])
     return res, times

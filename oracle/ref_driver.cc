@@ -75,7 +75,8 @@ extern "C" {
 // algo: 0 = SSSP, 1 = PR, 2 = TC.  Runs the reference driver twice (empty
 // stream, then the k records in batches of batchsize) on fresh copies of the
 // graph.  times[0] = T_0 seconds, times[1] = T_k seconds.  Outputs of the
-// full run: SSSP -> out_i64a (dist), out_i64b (parent); PR -> out_f64 (rank);
+// full run: SSSP -> out_i64a (dist), out_i64b (parent); PR -> out_f64 (rank),
+// out_i64a (live out-degree of the final graph);
 // TC -> out_i64a[0] (count).  Pass k = 0 to run the static pass only.
 int gdref_run(int algo, int64_t n, const int64_t* src, const int64_t* dst, const int64_t* w, int64_t m,
               int directed, int weighted, int64_t merge_interval, const uint8_t* kind, const int64_t* us,
@@ -114,6 +115,17 @@ int gdref_run(int algo, int64_t n, const int64_t* src, const int64_t* dst, const
             t1 = omp_get_wtime();
             if (pass == 1 && out_f64)
                 for (int64_t v = 0; v < n; ++v) out_f64[v] = pr[v];
+            // live out-degree of the final graph (= the driver's outdeg when
+            // no delete missed, as in generate_updates streams)
+            if (pass == 1 && out_i64a)
+                for (int64_t v = 0; v < n; ++v) {
+                    int64_t c = 0;
+                    for (gd::Edge e : g.neighbors(v)) {
+                        (void)e;
+                        ++c;
+                    }
+                    out_i64a[v] = c;
+                }
         } else {
             t0 = omp_get_wtime();
             int64_t c = dynamicTC(g, st, batchsize);
