@@ -80,6 +80,23 @@ GD_API int gd_graph_create(int64_t node_count, const int64_t* src, const int64_t
                     gd_graph** out);
 GD_API int gd_graph_destroy(gd_graph* g);
 
+/* The same graph as one rank's share of a 1D vertex partition over `comm`
+ * (block ownership: rank r owns [r*q + min(r, n%W), ...), the first n % W
+ * ranks one more -- partition.py:69-78).  Every rank passes the whole edge
+ * list; it keeps the out-arcs of the sources it owns (the reference's
+ * PartitionedGraph shard, partition.py:85-133) and the in-arcs of the
+ * destinations it owns.  Directed graphs only (undirected graphs are
+ * replicated per rank).  Every later call on the graph and on algorithm
+ * handles made from it is collective: each rank passes the whole batch, the
+ * owners apply their records and route the killed / inserted arcs to the
+ * destinations' owners.  Segment exports show this rank's shard; live
+ * counts, miss flags, flood results and algorithm reads are global. */
+GD_API int gd_graph_create_dist(int64_t node_count, const int64_t* src, const int64_t* dst, const int64_t* w,
+                                int64_t m, int directed, int weighted, int with_reverse, int64_t merge_interval,
+                                int device, gd_comm* comm, gd_graph** out);
+/* the owned vertex block [lo, hi) ([0, n) for an unpartitioned graph) */
+GD_API int gd_graph_owned_range(gd_graph* g, int64_t* lo, int64_t* hi);
+
 /* DynamicGraph.update_csr_del -> DeleteReport (graph/dynamic.py:208-244).
  * miss_flags (nullable, k bytes) gets 1 for each record that missed. */
 GD_API int gd_graph_apply_deletes(gd_graph* g, const int64_t* src, const int64_t* dst, int64_t k, int64_t* applied,
@@ -176,6 +193,12 @@ GD_API int gd_tc_destroy(gd_tc* t);
  *      reference has no multi-process path (partition.py simulates one). */
 GD_API int gd_comm_unique_id(uint8_t id[128]);
 GD_API int gd_comm_create(int world, int rank, const uint8_t id[128], int device, gd_comm** out);
+/* A member of an in-process group of `world` ranks that share the calling
+ * process (one host thread per rank, any common `group` id).  Collectives
+ * meet at a host barrier and move data with device copies -- the NCCL call
+ * sequence without NCCL, so the partitioned code paths run on one GPU (tests).
+ * No reference counterpart. */
+GD_API int gd_comm_create_local(int world, int rank, int64_t group, int device, gd_comm** out);
 GD_API int gd_comm_destroy(gd_comm* c);
 /* communication accounting (the CommStats analogue of partition.py:32-66):
  * out[0] collective calls, out[1] all-gather payload bytes, out[2] all-reduce

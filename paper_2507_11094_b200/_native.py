@@ -34,6 +34,9 @@ SIGNATURES = [
     ("gd_kernel_launches", C.c_int64, []),
     ("gd_graph_create", C.c_int, [i64, vp, vp, vp, i64, C.c_int, C.c_int, C.c_int, i64, C.c_int, C.POINTER(vp)]),
     ("gd_graph_destroy", C.c_int, [vp]),
+    ("gd_graph_create_dist", C.c_int, [i64, vp, vp, vp, i64, C.c_int, C.c_int, C.c_int, i64, C.c_int, vp,
+                                       C.POINTER(vp)]),
+    ("gd_graph_owned_range", C.c_int, [vp, i64p, i64p]),
     ("gd_graph_apply_deletes", C.c_int, [vp, vp, vp, i64, i64p, i64p, vp]),
     ("gd_graph_apply_adds", C.c_int, [vp, vp, vp, vp, i64]),
     ("gd_graph_merge", C.c_int, [vp]),
@@ -67,6 +70,7 @@ SIGNATURES = [
     ("gd_tc_destroy", C.c_int, [vp]),
     ("gd_comm_unique_id", C.c_int, [vp]),
     ("gd_comm_create", C.c_int, [C.c_int, C.c_int, vp, C.c_int, C.POINTER(vp)]),
+    ("gd_comm_create_local", C.c_int, [C.c_int, C.c_int, i64, C.c_int, C.POINTER(vp)]),
     ("gd_comm_destroy", C.c_int, [vp]),
     ("gd_pr_set_comm", C.c_int, [vp, vp]),
     ("gd_tc_set_comm", C.c_int, [vp, vp]),

@@ -389,6 +389,95 @@ __global__ void k_uf_mark(const int32_t* p, int64_t n, const uint8_t* root_has_s
 
 }  // namespace
 
+namespace {
+
+// owned flagged vertices -> the first frontier
+__global__ void k_bfs_seed(const uint8_t* flags, int64_t lo, int64_t hi, int32_t* q, unsigned long long* cnt) {
+    for (int64_t v = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < hi;
+         v += (int64_t)gridDim.x * blockDim.x)
+        if (flags[v]) q[atomicAdd(cnt, 1ULL)] = (int32_t)v;
+}
+
+// one warp per frontier vertex: touch every neighbour over the live out-arcs
+// (all segments) and in-arcs, in the padded owner-major layout of the
+// reduce-scatter (vertex w at owner(w) * chunk + w - lo(owner(w)))
+__global__ void __launch_bounds__(256) k_bfs_expand(const int32_t* q, const unsigned long long* nq, OutView ov,
+                                                    IdxView in, Blocks b, uint8_t* touched) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t m = (int64_t)*nq;
+    const int64_t ch = b.chunk();
+    for (int64_t t = warp; t < m; t += nwarps) {
+        const int32_t v = q[t];
+        for (int sg = 0; sg < ov.nseg; ++sg)
+            for (int64_t e = ov.off[sg][v] + lane; e < ov.off[sg][v + 1]; e += 32) {
+                const int32_t w = ov.col[sg][e];
+                if (w >= 0) {
+                    const int o = b.owner(w);
+                    touched[o * ch + (w - b.lo(o))] = 1;
+                }
+            }
+        if (in.off)
+            for (int64_t e = in.off[v] + lane; e < in.off[v + 1]; e += 32) {
+                const int32_t u = in.col[e];
+                if (u >= 0) {
+                    const int o = b.owner(u);
+                    touched[o * ch + (u - b.lo(o))] = 1;
+                }
+            }
+    }
+}
+
+// owned vertices touched this level and not yet flagged -> the next frontier
+__global__ void k_bfs_next(const uint8_t* mine, int64_t lo, int64_t hi, uint8_t* flags, int32_t* q,
+                           unsigned long long* cnt) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < hi - lo;
+         j += (int64_t)gridDim.x * blockDim.x)
+        if (mine[j] && !flags[lo + j]) {
+            flags[lo + j] = 1;
+            q[atomicAdd(cnt, 1ULL)] = (int32_t)(lo + j);
+        }
+}
+
+}  // namespace
+
+int64_t flood_weak_components_dist(Store& g, uint8_t* flags, KernelProf* prof) {
+    (void)prof;
+    cudaStream_t s = g.stream;
+    const int64_t n = g.n;
+    if (n == 0) return 0;
+    IdxView in{nullptr, nullptr, nullptr};
+    if (g.rev.built) {
+        g.compact_rev();
+        in = g.rev.view();
+    }
+    const Blocks& b = g.blocks;
+    const int64_t ch = b.chunk(), lo = g.own_lo, hi = g.own_hi;
+    DBuf<uint8_t> touched(std::max<int64_t>(ch * b.world, 1), s), mine(std::max<int64_t>(ch, 1), s);
+    DBuf<int32_t> q(std::max<int64_t>(hi - lo, 1), s);
+    DBuf<unsigned long long> cnt(1, s);
+    DBuf<int64_t> tot(1, s);
+    cnt.zero(s);
+    if (hi > lo) GD_KERNEL(k_bfs_seed, grid_for(hi - lo, 256), 256, 0, s, flags, lo, hi, q.get(), cnt.get());
+    OutView ov = g.out_view();
+    int64_t levels = 0;
+    while (true) {
+        // frontier sizes summed over ranks: the loop ends on every rank together
+        GD_CUDA(cudaMemcpyAsync(tot.get(), cnt.get(), 8, cudaMemcpyDeviceToDevice, s));
+        g.part->allreduce_sum_i64(tot.get(), 1, s);
+        if (read_scalar(s, tot.get()) == 0) break;
+        ++levels;
+        GD_CUDA(cudaMemsetAsync(touched.get(), 0, ch * b.world, s));
+        GD_KERNEL_T("flood_bfs", 0, k_bfs_expand, 148 * 8, 256, 0, s, q.get(), cnt.get(), ov, in, b, touched.get());
+        g.part->reducescatter_max_u8(touched.get(), mine.get(), ch, s);
+        cnt.zero(s);
+        if (hi > lo) GD_KERNEL(k_bfs_next, grid_for(hi - lo, 256), 256, 0, s, mine.get(), lo, hi, flags, q.get(),
+                               cnt.get());
+    }
+    return levels;
+}
+
 int64_t flood_weak_components(Store& g, uint8_t* flags, KernelProf* prof) {
     (void)prof;
     cudaStream_t s = g.stream;

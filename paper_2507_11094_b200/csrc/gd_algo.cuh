@@ -78,6 +78,15 @@ struct Frontier {
 // union-find hooking passes.
 int64_t flood_weak_components(Store& g, uint8_t* d_flags, KernelProf* prof);
 
+// The same flood on a vertex-partitioned store (Store::part): a
+// level-synchronous BFS over the weak view, each rank expanding the frontier
+// vertices it owns over their out-rows (its out-store) and in-rows (its
+// in-index), the touched flags meeting at their owners through one
+// reduce-scatter (max over bytes) per level.  The seed flags are the same on
+// every rank (records are replicated); on return the OWNED block of d_flags
+// is final (gather it for the whole vector).  Returns the BFS levels.
+int64_t flood_weak_components_dist(Store& g, uint8_t* d_flags, KernelProf* prof);
+
 // out-degree (live arcs over all segments) per node, int32
 void out_degrees(Store& g, int32_t* deg);
 

@@ -221,8 +221,9 @@ const char* gd_last_error(void) { return tl_err.c_str(); }
 int gd_abi_version(void) { return 100; }
 int64_t gd_kernel_launches(void) { return gdb::launches_total(); }
 
-int gd_graph_create(int64_t n, const int64_t* src, const int64_t* dst, const int64_t* w, int64_t m, int directed,
-                    int weighted, int with_reverse, int64_t merge_interval, int device, gd_graph** out) {
+static int graph_create(int64_t n, const int64_t* src, const int64_t* dst, const int64_t* w, int64_t m, int directed,
+                        int weighted, int with_reverse, int64_t merge_interval, int device, const gdb::Comm* part,
+                        gd_graph** out) {
     return guard([&] {
         if (!out) throw gdb::GdError(GD_ERR_CONTRACT, "null output handle");
         if (n < 0 || n >= INT32_MAX)
@@ -249,9 +250,28 @@ int gd_graph_create(int64_t n, const int64_t* src, const int64_t* dst, const int
         if (device < 0 || device >= ndev) throw gdb::GdError(GD_ERR_CUDA, "bad CUDA device index");
         auto* g = new gd_graph;
         g->st.reset(new gdb::Store(device, n, src, dst, weighted ? w : nullptr, m, directed != 0, weighted != 0,
-                                   with_reverse != 0, merge_interval, as_arcs));
+                                   with_reverse != 0, merge_interval, as_arcs, part));
         *out = g;
     });
+}
+
+int gd_graph_create(int64_t n, const int64_t* src, const int64_t* dst, const int64_t* w, int64_t m, int directed,
+                    int weighted, int with_reverse, int64_t merge_interval, int device, gd_graph** out) {
+    return graph_create(n, src, dst, w, m, directed, weighted, with_reverse, merge_interval, device, nullptr, out);
+}
+
+int gd_graph_create_dist(int64_t n, const int64_t* src, const int64_t* dst, const int64_t* w, int64_t m,
+                         int directed, int weighted, int with_reverse, int64_t merge_interval, int device,
+                         gd_comm* comm, gd_graph** out) {
+    if (!comm) return null_handle();
+    return graph_create(n, src, dst, w, m, directed, weighted, with_reverse, merge_interval, device, comm->c, out);
+}
+
+int gd_graph_owned_range(gd_graph* g, int64_t* lo, int64_t* hi) {
+    if (!g) return null_handle();
+    if (lo) *lo = g->st->own_lo;
+    if (hi) *hi = g->st->own_hi;
+    return ok();
 }
 
 int gd_graph_destroy(gd_graph* g) {
@@ -272,6 +292,7 @@ int gd_graph_apply_deletes(gd_graph* g, const int64_t* src, const int64_t* dst, 
         HostIds h = upload_ids(st.stream, src, dst, nullptr, k);
         gdb::DBuf<uint8_t> found(k, st.stream);
         int64_t a = st.apply_deletes(h.s.get(), h.d.get(), k, found.get(), true);
+        if (st.part && k) st.part->allreduce_max_u8(found.get(), k, st.stream);  // owners' flags to every rank
         if (miss_flags && k) {
             GD_CUDA(cudaMemcpyAsync(miss_flags, found.get(), k, cudaMemcpyDeviceToHost, st.stream));
             GD_CUDA(cudaStreamSynchronize(st.stream));
@@ -307,7 +328,15 @@ int gd_graph_merge(gd_graph* g) {
 int gd_graph_stats(gd_graph* g, int64_t* live, int64_t* nseg, int64_t* slots) {
     if (!g) return null_handle();
     return guard([&] {
-        if (live) *live = g->st->live_count();
+        if (live) {
+            *live = g->st->live_count();
+            if (g->st->part) {  // live_edge_count of the whole graph
+                gdb::DBuf<int64_t> t(1, g->st->stream);
+                GD_CUDA(cudaMemcpyAsync(t.get(), live, 8, cudaMemcpyHostToDevice, g->st->stream));
+                g->st->part->allreduce_sum_i64(t.get(), 1, g->st->stream);
+                *live = gdb::read_scalar(g->st->stream, t.get());
+            }
+        }
         if (nseg) *nseg = (int64_t)g->st->segs.size();
         if (slots) *slots = g->st->total_slots();
     });
@@ -381,7 +410,9 @@ int gd_graph_propagate_flags(gd_graph* g, uint8_t* flags, int64_t* rounds) {
             throw gdb::GdError(GD_ERR_CONFIG, "propagateNodeFlags on a directed graph needs reverse adjacency");
         gdb::DBuf<uint8_t> f(std::max<int64_t>(st.n, 1), st.stream);
         if (st.n) GD_CUDA(cudaMemcpyAsync(f.get(), flags, st.n, cudaMemcpyHostToDevice, st.stream));
-        int64_t r = gdb::flood_weak_components(st, f.get(), nullptr);
+        int64_t r = st.part ? gdb::flood_weak_components_dist(st, f.get(), nullptr)
+                            : gdb::flood_weak_components(st, f.get(), nullptr);
+        if (st.part) st.part->allgatherv(f.get(), st.blocks, 1, st.stream);
         if (st.n) GD_CUDA(cudaMemcpyAsync(flags, f.get(), st.n, cudaMemcpyDeviceToHost, st.stream));
         GD_CUDA(cudaStreamSynchronize(st.stream));
         if (rounds) *rounds = r;
@@ -471,6 +502,7 @@ int gd_pr_read(gd_pr* p, double* rank, int64_t* outdeg) {
     if (!p) return null_handle();
     return guard([&] {
         GD_CUDA(cudaSetDevice(p->a->g->device));
+        p->a->gather();
         p->a->read(rank, outdeg);
     });
 }
@@ -478,6 +510,7 @@ int gd_pr_read_affected(gd_pr* p, uint8_t* affected) {
     if (!p) return null_handle();
     return guard([&] {
         GD_CUDA(cudaSetDevice(p->a->g->device));
+        p->a->gather();
         p->a->read_affected(affected);
     });
 }
@@ -485,13 +518,17 @@ int gd_pr_read_async(gd_pr* p, double* rank) {
     if (!p) return null_handle();
     return guard([&] {
         GD_CUDA(cudaSetDevice(p->a->g->device));
+        p->a->gather();
         p->a->copy_out_async(rank, p->a->rank.get(), (size_t)p->a->g->n * 8, 0);
     });
 }
 int gd_pr_rank_device(gd_pr* p, const double** rank) {
     if (!p) return null_handle();
-    *rank = p->a->rank.get();
-    return ok();
+    return guard([&] {
+        GD_CUDA(cudaSetDevice(p->a->g->device));
+        p->a->gather();
+        *rank = p->a->rank.get();
+    });
 }
 int gd_pr_destroy(gd_pr* p) {
     if (!p) return ok();
@@ -536,6 +573,19 @@ int gd_comm_create(int world, int rank, const uint8_t id[128], int device, gd_co
         auto* h = new gd_comm{nullptr};
         try {
             h->c = gdb::comm_create(world, rank, id, device);
+        } catch (...) {
+            delete h;
+            throw;
+        }
+        *out = h;
+    });
+}
+int gd_comm_create_local(int world, int rank, int64_t group, int device, gd_comm** out) {
+    return guard([&] {
+        if (!out) throw gdb::GdError(GD_ERR_CONTRACT, "null output handle");
+        auto* h = new gd_comm{nullptr};
+        try {
+            h->c = gdb::comm_create_local(world, rank, group, device);
         } catch (...) {
             delete h;
             throw;

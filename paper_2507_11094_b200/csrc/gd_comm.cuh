@@ -48,11 +48,6 @@ struct Comm {
     // (p2p: the bytes this rank sends to other ranks)
     mutable int64_t n_calls = 0, ag_bytes = 0, ar_bytes = 0, sent_bytes = 0, p2p_bytes = 0;
 
-    // vertex range owned by this rank: [lo, hi), chunk = ceil(n / world)
-    int64_t chunk(int64_t n) const { return (n + world - 1) / world; }
-    int64_t lo(int64_t n) const { return std::min<int64_t>(n, (int64_t)rank * chunk(n)); }
-    int64_t hi(int64_t n) const { return std::min<int64_t>(n, lo(n) + chunk(n)); }
-
     // In-place all-gather of `chunk` doubles per rank into buf (n_pad = chunk * world).
     void allgather_f64(double* buf, int64_t chunk, cudaStream_t s) const;
     void allreduce_max_f64(double* x, int64_t count, cudaStream_t s) const;

@@ -401,22 +401,8 @@ PR::PR(Store* st, double d, double b, int64_t mi) : AlgoBase(ALGO_PR, st), dampi
 }
 
 void PR::set_comm(Comm* c) {
-    cudaStream_t s = stream();
-    int64_t n = g->n;
+    if (c && g->part) throw GdError(GD_ERR_CONFIG, "the graph is partitioned: its handles use the graph's communicator");
     comm = c;
-    if (!c) return;
-    // rank / rank_new padded to chunk * world for the in-place all-gather
-    int64_t npad = std::max<int64_t>(c->chunk(n) * c->world, 1);
-    DBuf<double> r2(npad, s), n2(npad, s);
-    r2.zero(s);
-    n2.zero(s);
-    if (n) {
-        GD_CUDA(cudaMemcpyAsync(r2.get(), rank.get(), n * 8, cudaMemcpyDeviceToDevice, s));
-        GD_CUDA(cudaMemcpyAsync(n2.get(), rank_new.get(), n * 8, cudaMemcpyDeviceToDevice, s));
-    }
-    rank = std::move(r2);
-    rank_new = std::move(n2);
-    GD_CUDA(cudaStreamSynchronize(s));
 }
 
 // One sweep (pr_dynamic_omp.cc:66-99): dangling mass + contrib over all V,
@@ -429,13 +415,20 @@ void PR::sweep(int64_t tag) {
     const double base = (1.0 - damping) / (double)n;
     const double inv_n = 1.0 / (double)n;
     int64_t* c = ctl.get();
-    int pc = prof_begin("pr_contrib", n * 20, s);
+    const Comm* part = g->part;  // vertex-partitioned store: contrib of the owned sources, then gathered
+    const int64_t clo = part ? g->own_lo : 0, cn = part ? g->own_hi - g->own_lo : n;
+    int pc = prof_begin("pr_contrib", cn * 20, s);
     prof_tag(pc, tag);
-    k_pr_contrib<<<kRedBlocks, 256, 0, s>>>(rank.get(), outdeg.get(), n, contrib.get(), partial.get(), c);
+    k_pr_contrib<<<kRedBlocks, 256, 0, s>>>(rank.get() + clo, outdeg.get() + clo, cn, contrib.get() + clo,
+                                            partial.get(), c);
     count_launch();
     GD_LAUNCH_CHECK();
     prof_end(pc, s);
     GD_KERNEL(k_sum_partials, 1, 1024, 0, s, partial.get(), kRedBlocks, scal.get(), c);
+    if (part) {  // dangling mass over all ranks; every rank's contrib block to every rank
+        part->allreduce_sum_f64(scal.get(), 1, s);
+        part->allgatherv(contrib.get(), g->blocks, 8, s);
+    }
     // algorithmic bytes: |A| (off + 2 f64) + E_in(A) (idx + f64), filled in from the bin
     // counts once the loop has read them back
     static const bool split = getenv("GD_PR_SPLIT_BINS") != nullptr;
@@ -480,9 +473,10 @@ void PR::sweep(int64_t tag) {
     GD_KERNEL(k_pr_commit, 148 * 8, 256, 0, s, bins[0].get(), bins[1].get(), bins[2].get(), c, rank_new.get(),
               rank.get());
     if (comm) {  // every rank gets every owned range; the residual is the max over ranks
-        comm->allgather_f64(rank.get(), comm->chunk(n), s);
+        comm->allgatherv(rank.get(), Blocks(n, comm->world), 8, s);
         comm->allreduce_max_f64(scal.get() + 1, 1, s);
     }
+    if (part) part->allreduce_max_f64(scal.get() + 1, 1, s);
     GD_KERNEL(k_pr_check, 1, 1, 0, s, c, scal.get() + 1, beta, maxiter);
 }
 
@@ -498,7 +492,8 @@ void PR::recompute(const uint8_t* flags) {
     g->compact_rev();
     GD_CUDA(cudaMemsetAsync(ctl.get(), 0, C_LEN * sizeof(int64_t), s));
     if (maxiter <= 0) return;
-    const int64_t lo = comm ? comm->lo(n) : 0, hi = comm ? comm->hi(n) : n;
+    const int64_t lo = g->part ? g->own_lo : (comm ? Blocks(n, comm->world).lo(comm->rank) : 0);
+    const int64_t hi = g->part ? g->own_hi : (comm ? Blocks(n, comm->world).hi(comm->rank) : n);
     if (hi > lo)
         GD_KERNEL(k_pr_bin, (unsigned)std::min<int64_t>((hi - lo + kBinChunk - 1) / kBinChunk, 148LL * 8),
                   kBinThreads, 0, s, flags, lo, hi, g->rev.off.get(), bins[0].get(), bins[1].get(), bins[2].get(),
@@ -509,7 +504,7 @@ void PR::recompute(const uint8_t* flags) {
     while (!done) {
         // multi-GPU: one sweep at a time -- a queued no-op sweep would still
         // move the rank vector through its all-gather
-        const int64_t ahead = comm ? 1 : std::max<int64_t>(1, std::min<int64_t>(ahead_hint, 16));
+        const int64_t ahead = (comm || g->part) ? 1 : std::max<int64_t>(1, std::min<int64_t>(ahead_hint, 16));
         for (int64_t k = 0; k < ahead; ++k) sweep(sweeps + k);
         read_small(s, hctl, ctl.get(), sizeof hctl);
         done = hctl[C_DONE];
@@ -555,9 +550,18 @@ void PR::batch(DevBatch& b, int64_t batch_index) {
         g->merge();
     }
     timer.begin(PH_PROP);
-    flood_weak_components(*g, affected.get(), &prof);
+    if (g->part) flood_weak_components_dist(*g, affected.get(), &prof);
+    else flood_weak_components(*g, affected.get(), &prof);
     recompute(affected.get());
     timer.end_all();
+}
+
+void PR::gather() {
+    if (!g->part || g->n == 0) return;
+    cudaStream_t s = stream();
+    g->part->allgatherv(rank.get(), g->blocks, 8, s);
+    g->part->allgatherv(outdeg.get(), g->blocks, 4, s);
+    g->part->allgatherv(affected.get(), g->blocks, 1, s);
 }
 
 void PR::read_affected(uint8_t* h_aff) {

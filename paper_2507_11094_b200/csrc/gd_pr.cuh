@@ -28,6 +28,9 @@ struct PR : AlgoBase {
     void batch(DevBatch& b, int64_t batch_index);                 // one Batch body
     void read(double* rank, int64_t* outdeg);
     void read_affected(uint8_t* aff);  // the last batch's flooded flags
+    // vertex-partitioned store: every rank's owned blocks of rank, outdeg
+    // and affected to every rank (collective; before a read)
+    void gather();
 
   private:
     void recompute(const uint8_t* flags);  // bin + sweep loop; flags == nullptr: all vertices

@@ -649,6 +649,7 @@ SSSP::SSSP(Store* st, int64_t s, int64_t cap) : AlgoBase(ALGO_SSSP, st), src((in
     if (!st->with_reverse)
         throw GdError(GD_ERR_CONFIG, "graph was loaded without reverse-adjacency maintenance");
     if (s < 0 || s >= st->n) throw GdError(GD_ERR_EXEC, "source node out of range");
+    if (st->part) throw GdError(GD_ERR_CONFIG, "SSSP on a partitioned store is not available yet");
     cudaStream_t cs = stream();
     int64_t n = g->n;
     dist.alloc(n, cs);

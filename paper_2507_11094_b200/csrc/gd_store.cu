@@ -456,6 +456,75 @@ __global__ void k_del_kill(OutView ov, const uint64_t* rq_key, const int32_t* rq
     if ((threadIdx.x & 31) == 0 && killed) atomicAdd(k_cnt, killed);
 }
 
+// ------------------------------------------------------- partitioning ----
+
+// arcs of owned sources (out-store) / owned destinations (in-index)
+__global__ void k_part_flags(const uint32_t* src, const int32_t* dst, int64_t m, Blocks b, int rank, uint8_t* fo,
+                             uint8_t* fi) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+        fo[i] = b.owner((int64_t)src[i]) == rank;
+        fi[i] = b.owner((int64_t)dst[i]) == rank;
+    }
+}
+
+__global__ void k_owned_flags(const int32_t* s, int64_t k, Blocks b, int rank, uint8_t* f) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < k; i += (int64_t)gridDim.x * blockDim.x)
+        f[i] = b.owner((int64_t)s[i]) == rank;
+}
+
+__global__ void k_scatter_u8(const uint8_t* in, const int32_t* idx, int64_t m, uint8_t* out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+        out[idx[i]] = in[i];
+}
+
+// per-destination-owner counts of the routed arcs (gid < 0: nothing to route)
+__global__ void k_route_count(const int32_t* col, const int64_t* gid, int64_t m, Blocks b,
+                              unsigned long long* cnt) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+        if (gid && gid[i] < 0) continue;
+        const int o = b.owner((int64_t)col[i]);
+        const unsigned peers = __match_any_sync(__activemask(), o);  // warp-aggregated per owner
+        if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&cnt[o], (unsigned long long)__popc(peers));
+    }
+}
+
+// exclusive offsets of the per-owner counts (world entries)
+__global__ void k_route_offsets(const unsigned long long* cnt, int world, unsigned long long* cur) {
+    unsigned long long a = 0;
+    for (int p = 0; p < world; ++p) {
+        cur[p] = a;
+        a += cnt[p];
+    }
+}
+
+// packed (row, col, w) triples in owner-major order (order within an owner
+// is arbitrary: the in-index is a sorted multiset)
+__global__ void k_route_scatter(const int32_t* row, const int32_t* col, const int32_t* w, const int64_t* gid,
+                                int64_t m, Blocks b, unsigned long long* cur, int32_t* packed) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+        if (gid && gid[i] < 0) continue;
+        const int o = b.owner((int64_t)col[i]);
+        const unsigned peers = __match_any_sync(__activemask(), o);
+        const int leader = __ffs(peers) - 1, lane = threadIdx.x & 31;
+        unsigned long long base = 0;
+        if (lane == leader) base = atomicAdd(&cur[o], (unsigned long long)__popc(peers));
+        base = __shfl_sync(peers, base, leader);
+        const int64_t pos = (int64_t)base + __popc(peers & ((1u << lane) - 1));
+        packed[3 * pos] = row[i];
+        packed[3 * pos + 1] = col[i];
+        packed[3 * pos + 2] = w ? w[i] : 1;
+    }
+}
+
+__global__ void k_unpack3(const int32_t* packed, int64_t m, int32_t* row, int32_t* col, int32_t* w, int64_t* gid) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+        row[i] = packed[3 * i];
+        col[i] = packed[3 * i + 1];
+        w[i] = packed[3 * i + 2];
+        if (gid) gid[i] = 0;
+    }
+}
+
 // ---------------------------------------------------------------- adds -----
 
 __global__ void k_add_arcs(const int32_t* s, const int32_t* d, const int32_t* w, int64_t k, bool directed,
@@ -857,9 +926,18 @@ void edit_merge(cudaStream_t s, int64_t n, const int64_t* off, int32_t* col, con
 // ==========================================================================
 
 Store::Store(int dev, int64_t n_, const int64_t* src, const int64_t* dst, const int64_t* w, int64_t m, bool dir,
-             bool wtd, bool with_rev, int64_t mi, bool as_arcs)
-    : device(dev), n(n_), directed(dir), weighted(wtd), with_reverse(with_rev), merge_interval(mi) {
+             bool wtd, bool with_rev, int64_t mi, bool as_arcs, const Comm* pc)
+    : device(dev), part(pc), n(n_), directed(dir), weighted(wtd), with_reverse(with_rev), merge_interval(mi) {
     sh = bits_for((uint64_t)std::max<int64_t>(n - 1, 1));
+    own_hi = n;
+    if (part) {
+        if (!directed)
+            throw GdError(GD_ERR_CONFIG, "vertex-partitioned stores hold directed graphs (undirected graphs are "
+                                         "replicated per rank)");
+        blocks = Blocks(n, part->world);
+        own_lo = blocks.lo(part->rank);
+        own_hi = blocks.hi(part->rank);
+    }
     GD_CUDA(cudaSetDevice(device));
     GD_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
     // keep freed stream-ordered memory in the pool across syncs: per-batch
@@ -883,6 +961,37 @@ Store::Store(int dev, int64_t n_, const int64_t* src, const int64_t* dst, const 
     if (m)
         GD_KERNEL(k_expand_edges, grid_for(m, 256), 256, 0, s, hs.get(), hd.get(), w ? hw.get() : nullptr, m,
                   !expand, key.get(), val.get(), adst.get(), aw.get());
+    DBuf<int32_t> in_src, in_dst, in_w;
+    int64_t m_in = 0;
+    if (part && na) {  // owned sources' out-arcs stay (stream order kept); owned destinations' in-arcs aside
+        DBuf<uint8_t> fo(na, s), fi(na, s);
+        GD_KERNEL(k_part_flags, grid_for(na, 256), 256, 0, s, key.get(), adst.get(), na, blocks, part->rank, fo.get(),
+                  fi.get());
+        DBuf<int32_t> so(na, s), si(na, s);
+        const int64_t mo = select_flagged_index(s, fo.get(), na, so.get());
+        m_in = select_flagged_index(s, fi.get(), na, si.get());
+        in_src.alloc(m_in, s);
+        in_dst.alloc(m_in, s);
+        in_w.alloc(m_in, s);
+        if (m_in) {
+            GD_KERNEL(k_gather<int32_t>, grid_for(m_in, 256), 256, 0, s, reinterpret_cast<const int32_t*>(key.get()),
+                      si.get(), m_in, in_src.get());
+            GD_KERNEL(k_gather<int32_t>, grid_for(m_in, 256), 256, 0, s, adst.get(), si.get(), m_in, in_dst.get());
+            GD_KERNEL(k_gather<int32_t>, grid_for(m_in, 256), 256, 0, s, aw.get(), si.get(), m_in, in_w.get());
+        }
+        DBuf<uint32_t> k2(mo, s);
+        DBuf<int32_t> d2(mo, s), w2(mo, s);
+        if (mo) {
+            GD_KERNEL(k_gather<uint32_t>, grid_for(mo, 256), 256, 0, s, key.get(), so.get(), mo, k2.get());
+            GD_KERNEL(k_gather<int32_t>, grid_for(mo, 256), 256, 0, s, adst.get(), so.get(), mo, d2.get());
+            GD_KERNEL(k_gather<int32_t>, grid_for(mo, 256), 256, 0, s, aw.get(), so.get(), mo, w2.get());
+        }
+        key = std::move(k2);
+        adst = std::move(d2);
+        aw = std::move(w2);
+        na = mo;
+        iota_i32(s, val.get(), na);
+    }
     // stable sort by source keeps insertion order within a source (dynamic.py:116)
     sort_pairs_u32(s, key.get(), val.get(), na, sh);
     OutSeg base;
@@ -905,7 +1014,10 @@ Store::Store(int dev, int64_t n_, const int64_t* src, const int64_t* dst, const 
     dcounts.alloc(2, s);
     dcounts.zero(s);
     upload_tables();
-    if (with_reverse) build_index(rev, true);
+    if (with_reverse) {
+        if (part) index_from_arcs(rev, true, in_src.get(), in_dst.get(), in_w.get(), m_in);
+        else build_index(rev, true);
+    }
     GD_CUDA(cudaStreamSynchronize(s));
 }
 
@@ -993,10 +1105,8 @@ int64_t Store::device_bytes() const {
 // Build a sorted index from the current live out-arcs (all segments).
 void Store::build_index(SortedIndex& ix, bool rows_are_dst) {
     cudaStream_t s = stream;
-    ix.rows_are_dst = rows_are_dst;
     int64_t tot = total_slots();
-    DBuf<uint64_t> key(tot, s);
-    DBuf<int32_t> val(tot, s), wv(tot, s);
+    DBuf<int32_t> asrc(tot, s), adst(tot, s), aw(tot, s);
     int64_t m = 0;
     for (auto& sg : segs) {
         if (!sg.nslots) continue;
@@ -1007,22 +1117,28 @@ void Store::build_index(SortedIndex& ix, bool rows_are_dst) {
         DBuf<int32_t> sel(sg.nslots, s);
         int64_t c = select_flagged_index(s, livef.get(), sg.nslots, sel.get());
         if (!c) continue;
-        AddedArcs tmp;
-        tmp.row.alloc(c, s);
-        tmp.col.alloc(c, s);
-        tmp.w.alloc(c, s);
-        GD_KERNEL(k_gather<int32_t>, grid_for(c, 256), 256, 0, s, row.get(), sel.get(), c, tmp.row.get());
-        GD_KERNEL(k_gather<int32_t>, grid_for(c, 256), 256, 0, s, sg.col.get(), sel.get(), c, tmp.col.get());
+        GD_KERNEL(k_gather<int32_t>, grid_for(c, 256), 256, 0, s, row.get(), sel.get(), c, asrc.get() + m);
+        GD_KERNEL(k_gather<int32_t>, grid_for(c, 256), 256, 0, s, sg.col.get(), sel.get(), c, adst.get() + m);
         if (weighted)
-            GD_KERNEL(k_gather<int32_t>, grid_for(c, 256), 256, 0, s, sg.w.get(), sel.get(), c, tmp.w.get());
+            GD_KERNEL(k_gather<int32_t>, grid_for(c, 256), 256, 0, s, sg.w.get(), sel.get(), c, aw.get() + m);
         else
-            fill_i32(s, tmp.w.get(), c, 1);
-        GD_KERNEL(k_added_to_index, grid_for(c, 256), 256, 0, s, tmp.row.get(), tmp.col.get(), c, rows_are_dst, sh,
-                  key.get() + m, val.get() + m);
-        GD_CUDA(cudaMemcpyAsync(wv.get() + m, tmp.w.get(), c * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+            fill_i32(s, aw.get() + m, c, 1);
         m += c;
     }
-    // val = position in the concatenation (indexes wv); the key carries (row, col)
+    index_from_arcs(ix, rows_are_dst, asrc.get(), adst.get(), aw.get(), m);
+}
+
+// A clean sorted index over the given arcs (src -> dst, weight): rows are the
+// destinations (rev) or the sources (fwd), columns ascending within a row.
+void Store::index_from_arcs(SortedIndex& ix, bool rows_are_dst, const int32_t* asrc, const int32_t* adst,
+                            const int32_t* aw, int64_t m) {
+    cudaStream_t s = stream;
+    ix.rows_are_dst = rows_are_dst;
+    DBuf<uint64_t> key(m, s);
+    DBuf<int32_t> val(m, s);
+    if (m) GD_KERNEL(k_added_to_index, grid_for(m, 256), 256, 0, s, asrc, adst, m, rows_are_dst, sh, key.get(),
+                     val.get());
+    // val = position in the arc arrays (indexes aw); the key carries (row, col)
     iota_i32(s, val.get(), m);
     sort_pairs_u64(s, key.get(), val.get(), m, 2 * sh);
     ix.nnz = m;
@@ -1031,7 +1147,7 @@ void Store::build_index(SortedIndex& ix, bool rows_are_dst) {
     if (m) GD_KERNEL(k_key_split, grid_for(m, 256), 256, 0, s, key.get(), m, sh, rows.get(), ix.col.get());
     if (weighted) {
         ix.w.alloc(m, s);
-        if (m) GD_KERNEL(k_gather<int32_t>, grid_for(m, 256), 256, 0, s, wv.get(), val.get(), m, ix.w.get());
+        if (m) GD_KERNEL(k_gather<int32_t>, grid_for(m, 256), 256, 0, s, aw, val.get(), m, ix.w.get());
     } else {
         ix.w.release();
     }
@@ -1144,10 +1260,102 @@ void Store::append_out_tombs(const int64_t* d_pos, const int32_t* d_row, int64_t
     notomb = tot;
 }
 
+// ---------------------------------------------------------------- partitioned stores
+
+int64_t Store::owned_records(const int32_t* src, const int32_t* dst, const int32_t* w, int64_t k, DBuf<int32_t>& idx,
+                             DBuf<int32_t>& os, DBuf<int32_t>& od, DBuf<int32_t>& ow) {
+    cudaStream_t s = stream;
+    DBuf<uint8_t> f(std::max<int64_t>(k, 1), s);
+    idx.alloc(std::max<int64_t>(k, 1), s);
+    if (k) GD_KERNEL(k_owned_flags, grid_for(k, 256), 256, 0, s, src, k, blocks, part->rank, f.get());
+    const int64_t kl = k ? select_flagged_index(s, f.get(), k, idx.get()) : 0;
+    os.alloc(std::max<int64_t>(kl, 1), s);
+    od.alloc(std::max<int64_t>(kl, 1), s);
+    if (w) ow.alloc(std::max<int64_t>(kl, 1), s);
+    if (kl) {
+        GD_KERNEL(k_gather<int32_t>, grid_for(kl, 256), 256, 0, s, src, idx.get(), kl, os.get());
+        GD_KERNEL(k_gather<int32_t>, grid_for(kl, 256), 256, 0, s, dst, idx.get(), kl, od.get());
+        if (w) GD_KERNEL(k_gather<int32_t>, grid_for(kl, 256), 256, 0, s, w, idx.get(), kl, ow.get());
+    }
+    return kl;
+}
+
+void Store::route_arcs(const int32_t* row, const int32_t* col, const int32_t* w, const int64_t* gid, int64_t m,
+                       DBuf<int32_t>& orow, DBuf<int32_t>& ocol, DBuf<int32_t>& ow, int64_t& count) {
+    cudaStream_t s = stream;
+    const int W = part->world;
+    DBuf<unsigned long long> cnt(2 * W, s);  // [counts | cursors]
+    cnt.zero(s);
+    DBuf<int32_t> packed(std::max<int64_t>(3 * m, 1), s);
+    if (m) {
+        GD_KERNEL(k_route_count, grid_for(m, 256), 256, 0, s, col, gid, m, blocks, cnt.get());
+        GD_KERNEL(k_route_offsets, 1, 1, 0, s, cnt.get(), W, cnt.get() + W);
+        GD_KERNEL(k_route_scatter, grid_for(m, 256), 256, 0, s, row, col, w, gid, m, blocks, cnt.get() + W,
+                  packed.get());
+    }
+    DBuf<int32_t> recv;
+    count = part->alltoallv_i32(packed.get(), reinterpret_cast<const int64_t*>(cnt.get()), 3, recv, s);
+    orow.alloc(std::max<int64_t>(count, 1), s);
+    ocol.alloc(std::max<int64_t>(count, 1), s);
+    ow.alloc(std::max<int64_t>(count, 1), s);
+    if (count) GD_KERNEL(k_unpack3, grid_for(count, 256), 256, 0, s, recv.get(), count, orow.get(), ocol.get(),
+                         ow.get(), nullptr);
+}
+
+// the in-index keeps the arcs of owned destinations: killed / inserted arcs
+// travel to the owner of their destination (partition.py routes records to
+// the source's owner, :206-235; the in-index is the destination's)
+void Store::rev_delete(const KilledArcs& ka) {
+    if (!part || !rev.built) {
+        index_delete(rev, ka);
+        return;
+    }
+    KilledArcs rk;
+    route_arcs(ka.row.get(), ka.col.get(), ka.w.get(), ka.gid.get(), ka.count, rk.row, rk.col, rk.w, rk.count);
+    rk.gid.alloc(std::max<int64_t>(rk.count, 1), stream);
+    fill_i64(stream, rk.gid.get(), rk.count, 0);
+    index_delete(rev, rk);
+}
+
+void Store::rev_add(const AddedArcs& aa) {
+    if (!part || !rev.built) {
+        index_add(rev, aa);
+        return;
+    }
+    AddedArcs ra;
+    route_arcs(aa.row.get(), aa.col.get(), aa.w.get(), nullptr, aa.count, ra.row, ra.col, ra.w, ra.count);
+    index_add(rev, ra);
+}
+
 int64_t Store::apply_deletes(const int32_t* d_src, const int32_t* d_dst, int64_t k, uint8_t* d_found,
                              bool want_count) {
+    if (!part) return apply_deletes_local(d_src, d_dst, k, d_found, want_count);
     cudaStream_t s = stream;
-    if (k == 0) return 0;
+    DBuf<int32_t> idx, os, od, ow;
+    const int64_t kl = owned_records(d_src, d_dst, nullptr, k, idx, os, od, ow);
+    DBuf<uint8_t> lf;
+    if (d_found) lf.alloc(std::max<int64_t>(kl, 1), s);
+    int64_t applied = apply_deletes_local(os.get(), od.get(), kl, d_found ? lf.get() : nullptr, want_count);
+    if (d_found && k) {  // flags of the owned records; other ranks hold the rest
+        GD_CUDA(cudaMemsetAsync(d_found, 0, k, s));
+        if (kl) GD_KERNEL(k_scatter_u8, grid_for(kl, 256), 256, 0, s, lf.get(), idx.get(), kl, d_found);
+    }
+    if (want_count) {
+        DBuf<int64_t> a(1, s);
+        GD_CUDA(cudaMemcpyAsync(a.get(), &applied, 8, cudaMemcpyHostToDevice, s));
+        part->allreduce_sum_i64(a.get(), 1, s);
+        applied = read_scalar(s, a.get());
+    }
+    return applied;
+}
+
+int64_t Store::apply_deletes_local(const int32_t* d_src, const int32_t* d_dst, int64_t k, uint8_t* d_found,
+                                   bool want_count) {
+    cudaStream_t s = stream;
+    if (k == 0) {
+        if (part) rev_delete(KilledArcs{});  // the routing is collective
+        return 0;
+    }
     if (rev.built) compact_index(rev);
     if (fwd.built) compact_index(fwd);
     first_clean_delta = segs.size();  // deltas made before this delete may now hold tombstones
@@ -1283,7 +1491,7 @@ int64_t Store::apply_deletes(const int32_t* d_src, const int32_t* d_dst, int64_t
     // the tomb logs take every slot (gid -1 = none; delta-segment gids are
     // ignored by the merge), unordered: no select, no sort
     append_out_tombs(ka.gid.get(), ka.row.get(), nrq);
-    index_delete(rev, ka);
+    rev_delete(ka);
     if (fwd.built) index_delete(fwd, ka);
     if (!want_count) return -1;
     unsigned long long applied = 0;
@@ -1300,8 +1508,18 @@ int64_t Store::live_count() {
 }
 
 void Store::apply_adds(const int32_t* d_src, const int32_t* d_dst, const int32_t* d_w, int64_t k) {
+    if (!part) return apply_adds_local(d_src, d_dst, d_w, k);
+    DBuf<int32_t> idx, os, od, ow;
+    const int64_t kl = owned_records(d_src, d_dst, d_w, k, idx, os, od, ow);
+    apply_adds_local(os.get(), od.get(), d_w ? ow.get() : nullptr, kl);
+}
+
+void Store::apply_adds_local(const int32_t* d_src, const int32_t* d_dst, const int32_t* d_w, int64_t k) {
     cudaStream_t s = stream;
-    if (k == 0) return;
+    if (k == 0) {
+        if (part) rev_add(AddedArcs{});
+        return;
+    }
     int64_t na = directed ? k : 2 * k;
     DBuf<uint32_t> key(na, s);
     DBuf<int32_t> val(na, s);
@@ -1346,7 +1564,7 @@ void Store::apply_adds(const int32_t* d_src, const int32_t* d_dst, const int32_t
     }
     if (with_reverse) claim_logs.push_back(std::move(cl));
     live += na;
-    index_add(rev, aa);
+    rev_add(aa);
     if (fwd.built) index_add(fwd, aa);
 }
 

@@ -21,6 +21,7 @@
 
 #include <vector>
 
+#include "gd_comm.cuh"
 #include "gd_common.cuh"
 
 namespace gdb {
@@ -89,8 +90,18 @@ struct AddedArcs {
 
 class Store {
   public:
+    // part != nullptr: this rank's share of a vertex-partitioned store (1D
+    // blocks, Blocks in gd_comm.cuh; directed graphs).  Every rank is given
+    // the whole edge list and every batch; it keeps the out-arcs whose
+    // source it owns (the out-store keeps the global id space, rows of
+    // other ranks are empty -- the reference's PartitionedGraph shards,
+    // partition.py:85-133) and the in-index of the arcs whose destination it
+    // owns.  Deletes and adds run on the records of owned sources; the
+    // killed and inserted arcs are routed to the owner of their destination
+    // (one all-to-all each) to keep its in-index.
     Store(int device, int64_t n, const int64_t* src, const int64_t* dst, const int64_t* w, int64_t m,
-          bool directed, bool weighted, bool with_reverse, int64_t merge_interval, bool as_arcs = false);
+          bool directed, bool weighted, bool with_reverse, int64_t merge_interval, bool as_arcs = false,
+          const Comm* part = nullptr);
     ~Store();
 
     // update_csr_del on device-resident records (int32).  Returns applied;
@@ -124,6 +135,9 @@ class Store {
 
     int device;
     cudaStream_t stream = nullptr;
+    const Comm* part = nullptr;  // partitioned store (see the constructor)
+    Blocks blocks;               // vertex ownership when partitioned
+    int64_t own_lo = 0, own_hi = 0;  // this rank's block ([0, n) unpartitioned)
     int64_t n;
     int sh = 1;  // pair keys: row << sh | col
     bool directed, weighted, with_reverse;
@@ -142,6 +156,19 @@ class Store {
     std::vector<ClaimLog> claim_logs;  // add calls since the last rebuild (with_reverse only)
 
   private:
+    int64_t apply_deletes_local(const int32_t* d_src, const int32_t* d_dst, int64_t k, uint8_t* d_found,
+                                bool want_count);
+    void apply_adds_local(const int32_t* d_src, const int32_t* d_dst, const int32_t* d_w, int64_t k);
+    // partitioned: the records whose source this rank owns (compacted copies)
+    int64_t owned_records(const int32_t* s, const int32_t* d, const int32_t* w, int64_t k, DBuf<int32_t>& idx,
+                          DBuf<int32_t>& os, DBuf<int32_t>& od, DBuf<int32_t>& ow);
+    // in-index upkeep, routed to the destination's owner when partitioned
+    void rev_delete(const KilledArcs& ka);
+    void rev_add(const AddedArcs& aa);
+    void route_arcs(const int32_t* row, const int32_t* col, const int32_t* w, const int64_t* gid, int64_t m,
+                    DBuf<int32_t>& orow, DBuf<int32_t>& ocol, DBuf<int32_t>& ow, int64_t& count);
+    void index_from_arcs(SortedIndex& ix, bool rows_are_dst, const int32_t* rows, const int32_t* cols,
+                         const int32_t* w, int64_t m);
     // segment table on the device: [off ptrs | col ptrs | w ptrs | bases]
     DBuf<uintptr_t> tab;
     std::vector<uintptr_t> h_tab;

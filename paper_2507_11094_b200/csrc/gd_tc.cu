@@ -518,6 +518,9 @@ void TC::count_deferred(const int32_t* s, const int32_t* d, int64_t m, const int
 }
 
 TC::TC(Store* st) : AlgoBase(ALGO_TC, st) {
+    if (st->part)
+        throw GdError(GD_ERR_CONFIG, "triangle counting runs on replicated stores (each rank holds the whole "
+                                     "undirected graph and counts a slice of the records, gd_tc_set_comm)");
     cudaStream_t s = stream();
     ProfScope ps(&prof);
     timer.begin(PH_STATIC);

@@ -19,20 +19,35 @@ from . import _native as N
 
 @dataclass(frozen=True)
 class ShardPlan:
+    """1D block ownership of the vertex ids, as the device code uses it
+    (csrc/gd_comm.cuh Blocks): the reference's block_ranges
+    (partition.py:69-78) -- the first n % world ranks get one vertex more."""
+
     n: int
     world: int
 
     @property
     def chunk(self) -> int:
-        return (self.n + self.world - 1) // self.world if self.world else self.n
+        """The largest block (the padded per-rank size of a reduce-scatter)."""
+        return self.n // self.world + (1 if self.n % self.world else 0)
 
     @property
     def padded(self) -> int:
         return self.chunk * self.world
 
     def range(self, rank: int):
-        lo = min(self.n, rank * self.chunk)
-        return lo, min(self.n, lo + self.chunk)
+        base, rem = divmod(self.n, self.world)
+        lo = rank * base + min(rank, rem)
+        return lo, lo + base + (1 if rank < rem else 0)
+
+    def owner(self, v):
+        """Owner rank of vertex id(s) v (scalar or numpy array)."""
+        import numpy as np
+
+        base, rem = divmod(self.n, self.world)
+        big = rem * (base + 1)
+        v = np.asarray(v)
+        return np.where(v < big, v // (base + 1), rem + (v - big) // max(base, 1))
 
     def record_slice(self, k: int, rank: int):
         """Contiguous slice of k batch records counted by `rank` (TC)."""
@@ -48,13 +63,28 @@ def unique_id() -> bytes:
 class Communicator:
     """NCCL communicator owned by the C ABI."""
 
-    def __init__(self, world: int, rank: int, nccl_id: bytes, device: int = 0):
-        buf = (C.c_uint8 * 128).from_buffer_copy(nccl_id)
-        h = C.c_void_p()
-        N.check(N.lib().gd_comm_create(int(world), int(rank), buf, int(device), C.byref(h)))
+    def __init__(self, world: int, rank: int, nccl_id: bytes, device: int = 0, *, _handle=None):
+        if _handle is None:
+            buf = (C.c_uint8 * 128).from_buffer_copy(nccl_id)
+            h = C.c_void_p()
+            N.check(N.lib().gd_comm_create(int(world), int(rank), buf, int(device), C.byref(h)))
+        else:
+            h = _handle
         self.h = h
         self.world = world
         self.rank = rank
+
+    @classmethod
+    def local_group(cls, world: int, device: int = 0, group: int = 0) -> list:
+        """`world` members of an in-process group (gd_comm_create_local): one
+        per host thread, all on `device` -- the partitioned code paths on a
+        single GPU, for tests."""
+        out = []
+        for r in range(world):
+            h = C.c_void_p()
+            N.check(N.lib().gd_comm_create_local(int(world), r, int(group), int(device), C.byref(h)))
+            out.append(cls(world, r, b"", device, _handle=h))
+        return out
 
     @classmethod
     def from_torch_distributed(cls, device: int) -> "Communicator":

@@ -101,16 +101,21 @@ class DynamicGraph:
         self._revl = None
         self._revl_version = -1
         self._mutate_lock = threading.Lock()
+        self.comm = None
 
     # -- construction -----------------------------------------------------------------
 
     @classmethod
     def from_arrays(cls, node_count: int, src, dst, weight=None, *, directed: bool = True, weighted: bool = False,
                     merge_interval: int = 1, with_reverse: bool = False, device: int = 0,
-                    arcs: bool = False) -> "DynamicGraph":
+                    arcs: bool = False, comm=None) -> "DynamicGraph":
         """Columnar DynamicGraph.build.  arcs=True stores the triples as arcs
         as given (no reverse arcs added for undirected graphs), as the
-        reference's DynamicGraph constructor does for merged()."""
+        reference's DynamicGraph constructor does for merged().
+
+        comm (a dist.Communicator): this rank's share of a 1D vertex
+        partition (gd_graph_create_dist) -- every rank passes the whole
+        edge list and, later, every batch; directed graphs only."""
         if node_count >= SENTINEL:
             raise ContractViolation("node_count collides with the deletion sentinel")
         if merge_interval < 1:
@@ -119,11 +124,25 @@ class DynamicGraph:
         w = None if weight is None else _i64(weight)
         h = C.c_void_p()
         flags = int(directed) | (2 if arcs else 0)
-        N.check(N.lib().gd_graph_create(int(node_count), N.ptr(s), N.ptr(d), N.ptr(w), len(s), flags,
-                                        int(weighted), int(with_reverse), int(merge_interval), int(device),
-                                        C.byref(h)))
-        return cls(h, int(node_count), directed=directed, weighted=weighted, merge_interval=merge_interval,
-                   with_reverse=with_reverse, device=device)
+        if comm is None:
+            N.check(N.lib().gd_graph_create(int(node_count), N.ptr(s), N.ptr(d), N.ptr(w), len(s), flags,
+                                            int(weighted), int(with_reverse), int(merge_interval), int(device),
+                                            C.byref(h)))
+        else:
+            N.check(N.lib().gd_graph_create_dist(int(node_count), N.ptr(s), N.ptr(d), N.ptr(w), len(s), flags,
+                                                 int(weighted), int(with_reverse), int(merge_interval), int(device),
+                                                 comm.h, C.byref(h)))
+        g = cls(h, int(node_count), directed=directed, weighted=weighted, merge_interval=merge_interval,
+                with_reverse=with_reverse, device=device)
+        g.comm = comm  # keeps the communicator alive
+        return g
+
+    @property
+    def owned_range(self) -> Tuple[int, int]:
+        """[lo, hi) of the vertices this rank owns (all of them unpartitioned)."""
+        lo, hi = C.c_int64(), C.c_int64()
+        N.check(N.lib().gd_graph_owned_range(self._h, C.byref(lo), C.byref(hi)))
+        return lo.value, hi.value
 
     @classmethod
     def build(cls, edge_list: Sequence[Tuple[int, int, int]], node_count: int, *, directed: bool = True,

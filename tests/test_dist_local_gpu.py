@@ -1,0 +1,164 @@
+"""The vertex-partitioned store and the partitioned PageRank / flood, run as
+W ranks of an in-process group on one GPU (gd_comm_create_local: one host
+thread per rank, every collective a host barrier + device copies -- the NCCL
+call sequence, no kernel waiting on another rank).  Every result must equal
+the unpartitioned path's: the store's per-row slot chains, DeleteReports and
+in-index, the flood, and PageRank (summation order of the dangling mass aside).
+"""
+
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+SENT = np.iinfo(np.int64).max
+
+
+@pytest.fixture(scope="module")
+def gd():
+    import paper_2507_11094_b200 as gd
+
+    return gd
+
+
+def run_ranks(world, fn):
+    """fn(rank, comm) on `world` threads sharing an in-process group."""
+    from paper_2507_11094_b200.dist import Communicator
+
+    comms = Communicator.local_group(world, group=id(fn) & 0xFFFFFFF)
+    with ThreadPoolExecutor(world) as ex:
+        futs = [ex.submit(fn, r, comms[r]) for r in range(world)]
+        return [f.result(timeout=600) for f in futs]
+
+
+def random_stream(rng, n, m, k, nb, weighted=True):
+    src = rng.integers(0, n, m)
+    dst = rng.integers(0, n, m)
+    w = rng.integers(1, 9, m) if weighted else np.ones(m, np.int64)
+    batches = []
+    for _ in range(nb):
+        kind = np.where(rng.random(k) < 0.5, ord("d"), ord("a")).astype(np.uint8)
+        pick = rng.integers(0, m, k)
+        # deletes mostly of existing pairs (parallel copies, misses included)
+        us = np.where(kind == ord("d"), np.where(rng.random(k) < 0.8, src[pick], rng.integers(0, n, k)),
+                      rng.integers(0, n, k))
+        ud = np.where(kind == ord("d"), np.where(rng.random(k) < 0.8, dst[pick], rng.integers(0, n, k)),
+                      rng.integers(0, n, k))
+        uw = rng.integers(1, 9, k)
+        batches.append((kind, us, ud, uw))
+    return src, dst, w, batches
+
+
+def chains(g, rows):
+    """Per-row slot chains (base, then deltas) over the given rows."""
+    segs = g.segments()
+    out = {}
+    for v in rows:
+        c = []
+        for seg in segs:
+            lo, hi = seg.slot_range(v)
+            c += list(zip(seg.coordinates[lo:hi].tolist(),
+                          (seg.weights[lo:hi] if seg.weights is not None else np.ones(hi - lo, np.int64)).tolist()))
+        out[v] = c
+    return out
+
+
+def rev_rows(g, rows):
+    off, s, w = g._reverse_snapshot()
+    return {v: sorted(zip(s[off[v]:off[v + 1]].tolist(), w[off[v]:off[v + 1]].tolist())) for v in rows}
+
+
+@pytest.mark.parametrize("world", [1, 2, 3])
+@pytest.mark.parametrize("merge_interval", [1, 2])
+def test_partitioned_store_matches_unpartitioned(gd, world, merge_interval):
+    rng = np.random.default_rng(11 + world)
+    n, m = 300, 2400
+    src, dst, w, batches = random_stream(rng, n, m, 300, 4)
+    ref = gd.DynamicGraph.from_arrays(n, src, dst, w, weighted=True, with_reverse=True,
+                                      merge_interval=merge_interval)
+    want = []
+    for i, (kind, us, ud, uw) in enumerate(batches):
+        b = gd.UpdateStream.from_arrays(kind, us, ud, uw).as_batch()
+        rep = ref.update_csr_del(b.only_deletes())
+        ref.update_csr_add(b.only_adds())
+        if (i + 1) % merge_interval == 0:
+            ref.merge_deltas()
+        want.append(((rep.applied, rep.misses, [(r.src, r.dst) for r in rep.missed]), ref.live_edge_count,
+                     chains(ref, range(n)), rev_rows(ref, range(n))))
+
+    def rank_fn(r, comm):
+        g = gd.DynamicGraph.from_arrays(n, src, dst, w, weighted=True, with_reverse=True,
+                                        merge_interval=merge_interval, comm=comm)
+        lo, hi = g.owned_range
+        # the shard holds exactly the out-arcs of owned sources, the in-index
+        # exactly the in-arcs of owned destinations
+        others = [v for v in range(n) if not lo <= v < hi]
+        assert all(not c for c in chains(g, others).values())
+        off, _, _ = g._reverse_snapshot()
+        assert all(off[v + 1] == off[v] for v in others)
+        got = []
+        for i, (kind, us, ud, uw) in enumerate(batches):
+            b = gd.UpdateStream.from_arrays(kind, us, ud, uw).as_batch()
+            rep = g.update_csr_del(b.only_deletes())
+            g.update_csr_add(b.only_adds())
+            if (i + 1) % merge_interval == 0:
+                g.merge_deltas()
+            got.append(((rep.applied, rep.misses, [(x.src, x.dst) for x in rep.missed]), g.live_edge_count,
+                        chains(g, range(lo, hi)), rev_rows(g, range(lo, hi))))
+        return (lo, hi), got
+
+    res = run_ranks(world, rank_fn)
+    covered = sorted(v for (lo, hi), _ in res for v in range(lo, hi))
+    assert covered == list(range(n))
+    for (lo, hi), got in res:
+        for i, (g_rep, g_live, g_ch, g_rev) in enumerate(got):
+            w_rep, w_live, w_ch, w_rev = want[i]
+            assert g_rep == w_rep, f"batch {i}: DeleteReport"
+            assert g_live == w_live, f"batch {i}: live_edge_count"
+            for v in range(lo, hi):
+                assert g_ch[v] == w_ch[v], f"batch {i}: chain of row {v}"
+                assert g_rev[v] == w_rev[v], f"batch {i}: in-arcs of {v}"
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_partitioned_flood_matches_unpartitioned(gd, world):
+    rng = np.random.default_rng(5)
+    n, m = 2000, 2600  # sparse: many weak components
+    src, dst = rng.integers(0, n, m), rng.integers(0, n, m)
+    flags = np.zeros(n, np.uint8)
+    flags[rng.integers(0, n, 12)] = 1
+    ref = gd.DynamicGraph.from_arrays(n, src, dst, with_reverse=True)
+    want = ref.propagate_flags(flags)
+
+    def rank_fn(r, comm):
+        g = gd.DynamicGraph.from_arrays(n, src, dst, with_reverse=True, comm=comm)
+        return g.propagate_flags(flags)
+
+    for got in run_ranks(world, rank_fn):
+        np.testing.assert_array_equal(got, want)
+
+
+@pytest.mark.parametrize("world", [1, 2, 4])
+def test_partitioned_pagerank_matches_unpartitioned(gd, world):
+    from paper_2507_11094_b200 import generate as G
+
+    s, d, _, n = G.rmat(12, 40_000, seed=3)
+    kind, us, ud, uw, per = G.updates(s, d, n, percent=2, batches=4, seed=4)
+    stream = gd.UpdateStream.from_arrays(kind, us, ud, uw)
+    inputs = {"damping": 0.85, "beta": 1e-10, "maxiter": 300}
+    ref = gd.run_batches(gd.shipped_program("pr"), gd.DynamicGraph.from_arrays(n, s, d, with_reverse=True), stream,
+                         per, inputs)
+
+    def rank_fn(r, comm):
+        g = gd.DynamicGraph.from_arrays(n, s, d, with_reverse=True, comm=comm)
+        ctx = gd.run_batches(gd.shipped_program("pr"), g, stream, per, inputs)
+        return {k: np.asarray(v.data) for k, v in ctx.properties.items()}
+
+    want_rank = np.asarray(ref.properties["pagerank"].data)
+    for got in run_ranks(world, rank_fn):
+        err = np.abs(got["pagerank"] - want_rank)
+        assert err.max() <= 1e-13, err.max()  # the dangling sum is added per rank
+        np.testing.assert_array_equal(got["outdeg"], ref.properties["outdeg"].data)
+        np.testing.assert_array_equal(got["affected"], ref.properties["affected"].data)
