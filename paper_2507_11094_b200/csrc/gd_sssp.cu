@@ -125,7 +125,22 @@ struct FpArgs {
     unsigned long long* fcnt;  // [3]
     long long* fmin;           // [3] lower bound of the pile's distances
     int32_t* infar;            // 1 while a vertex sits in the pile
+    // vertex-partitioned store (outbox != nullptr): only owned vertices
+    // [lo, hi) are queued; a relaxation or invalidation of another rank's
+    // vertex updates this rank's copy and lists the vertex once per launch
+    // (gstamp) in the outbox for its owner (SSSP::fixpoint_dist)
+    int64_t own_lo, own_hi;
+    int32_t* outbox;
+    unsigned long long* noutbox;
+    int32_t* gstamp;
+    int32_t launch;
 };
+
+__device__ __forceinline__ bool ghost(const FpArgs& a, int32_t t) { return a.outbox && (t < a.own_lo || t >= a.own_hi); }
+
+__device__ __forceinline__ void to_outbox(const FpArgs& a, int32_t t) {
+    if (atomicMax(&a.gstamp[t], a.launch) < a.launch) a.outbox[atomicAdd(a.noutbox, 1ULL)] = t;
+}
 
 struct Round {
     int32_t id;
@@ -172,7 +187,9 @@ __device__ __forceinline__ void out_act(const FpArgs& a, const Round& r, int32_t
         int64_t c = sat_add(dv, (int64_t)w);
         if (c < pre) {
             long long old = atomicMin(reinterpret_cast<long long*>(&a.dist[t]), (long long)c);
-            if (c < old) {
+            if (c < old && ghost(a, t)) {  // the owner applies it after the launch
+                to_outbox(a, t);
+            } else if (c < old) {
                 if (a.flags) a.flags[t] = 1;
                 if (c < r.theta) {
                     if (claim(a.stamp, t, r.id)) enqueue(r.qout, r.qcnt, t);
@@ -189,7 +206,8 @@ __device__ __forceinline__ void out_act(const FpArgs& a, const Round& r, int32_t
             a.dist[t] = kInf;
             a.parent[t] = -1;
             a.flags[t] = 1;
-            if (claim(a.stamp, t, r.id)) enqueue(r.qout, r.qcnt, t);
+            if (ghost(a, t)) to_outbox(a, t);
+            else if (claim(a.stamp, t, r.id)) enqueue(r.qout, r.qcnt, t);
         }
     } else {
         if (pre && claim(a.stamp, t, r.id)) enqueue(r.qout, r.qcnt, t);
@@ -623,6 +641,80 @@ __global__ void k_read_parent(const int32_t* p, int64_t n, int64_t* out) {
         out[i] = p[i];
 }
 
+// ---------------------------------------------------------------------------
+// Partitioned store (SSSP::fixpoint_dist): owned flagged vertices as a list,
+// the outbox packed as (vertex, value) messages by owner, and the owners'
+// application of the messages they receive.
+// ---------------------------------------------------------------------------
+__global__ void k_select_owned(const uint8_t* flags, int64_t lo, int64_t hi, int32_t* list, int64_t* cnt) {
+    for (int64_t v = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < hi;
+         v += (int64_t)gridDim.x * blockDim.x) {
+        const bool f = flags[v] != 0;
+        const unsigned mk = __ballot_sync(__activemask(), f);
+        if (!f) continue;
+        const int lane = threadIdx.x & 31, leader = __ffs(mk) - 1;
+        unsigned long long base = 0;
+        if (lane == leader) base = atomicAdd(reinterpret_cast<unsigned long long*>(cnt), (unsigned long long)__popc(mk));
+        base = __shfl_sync(mk, base, leader);
+        list[base + __popc(mk & ((1u << lane) - 1))] = (int32_t)v;
+    }
+}
+
+__global__ void k_msg_count(const int32_t* box, const unsigned long long* nbox, Blocks b, unsigned long long* cnt) {
+    const int64_t m = (int64_t)*nbox;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+        atomicAdd(&cnt[b.owner(box[i])], 1ULL);
+}
+
+__global__ void k_msg_offsets(const unsigned long long* cnt, int world, unsigned long long* cur) {
+    unsigned long long a = 0;
+    for (int p = 0; p < world; ++p) {
+        cur[p] = a;
+        a += cnt[p];
+    }
+}
+
+// (vertex, dist lo32, dist hi32) in owner-major order
+__global__ void k_msg_pack(const int32_t* box, const unsigned long long* nbox, Blocks b, const int64_t* dist,
+                           unsigned long long* cur, int32_t* packed) {
+    const int64_t m = (int64_t)*nbox;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t t = box[i];
+        const int64_t pos = (int64_t)atomicAdd(&cur[b.owner(t)], 1ULL);
+        const uint64_t d = (uint64_t)dist[t];
+        packed[3 * pos] = t;
+        packed[3 * pos + 1] = (int32_t)(uint32_t)d;
+        packed[3 * pos + 2] = (int32_t)(uint32_t)(d >> 32);
+    }
+}
+
+// owner side: min the received distance in (relax) or invalidate (walk);
+// each changed vertex seeds the next local fixpoint once (sstamp)
+__global__ void k_msg_apply(const int32_t* msg, int64_t m, int mode, int64_t* dist, int32_t* parent, uint8_t* flags,
+                            int32_t* sstamp, int32_t step, int32_t* seeds, int64_t* nseeds) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t t = msg[3 * i];
+        bool changed = false;
+        if (mode == FP_RELAX) {
+            const int64_t c = (int64_t)(((uint64_t)(uint32_t)msg[3 * i + 2] << 32) | (uint32_t)msg[3 * i + 1]);
+            if (c < dist[t]) {
+                const long long old = atomicMin(reinterpret_cast<long long*>(&dist[t]), (long long)c);
+                changed = c < old;
+                if (changed && flags) flags[t] = 1;  // touched
+            }
+        } else {  // FP_WALK: the sender saw parent[t] == its walked vertex
+            if (!flags[t]) {
+                flags[t] = 1;  // stale
+                dist[t] = kInf;
+                parent[t] = -1;
+                changed = true;
+            }
+        }
+        if (changed && atomicMax(&sstamp[t], step) < step)
+            seeds[atomicAdd(reinterpret_cast<unsigned long long*>(nseeds), 1ULL)] = t;
+    }
+}
+
 inline unsigned group_grid(int64_t m) { return grid_for(((m + kPerWarp - 1) / kPerWarp) * 32, kThreads, 148LL * 32); }
 
 // co-resident grid for the cooperative fixpoint: <= 4 CTAs per SM keeps the
@@ -649,7 +741,6 @@ SSSP::SSSP(Store* st, int64_t s, int64_t cap) : AlgoBase(ALGO_SSSP, st), src((in
     if (!st->with_reverse)
         throw GdError(GD_ERR_CONFIG, "graph was loaded without reverse-adjacency maintenance");
     if (s < 0 || s >= st->n) throw GdError(GD_ERR_EXEC, "source node out of range");
-    if (st->part) throw GdError(GD_ERR_CONFIG, "SSSP on a partitioned store is not available yet");
     cudaStream_t cs = stream();
     int64_t n = g->n;
     dist.alloc(n, cs);
@@ -679,6 +770,15 @@ SSSP::SSSP(Store* st, int64_t s, int64_t cap) : AlgoBase(ALGO_SSSP, st), src((in
     if (const char* e = getenv("GD_SSSP_DELTA")) delta = atoll(e);
     ctr.zero(cs);
     dcount.alloc(1, cs);
+    if (g->part) {
+        outbox.alloc(std::max<int64_t>(n, 1), cs);
+        gstamp.alloc(std::max<int64_t>(n, 1), cs);
+        gstamp.zero(cs);
+        sstamp.alloc(std::max<int64_t>(n, 1), cs);
+        sstamp.zero(cs);
+        seeds2.alloc(std::max<int64_t>(n, 1), cs);
+        nbox.alloc(1, cs);
+    }
     ProfScope ps(&prof);
     timer.begin(PH_STATIC);
     GD_KERNEL(k_init, grid_for(n, 256), 256, 0, cs, dist.get(), parent.get(), stamp.get(), hstamp.get(), n);
@@ -686,8 +786,24 @@ SSSP::SSSP(Store* st, int64_t s, int64_t cap) : AlgoBase(ALGO_SSSP, st), src((in
     int32_t seed = src;
     DBuf<int32_t> sq(1, cs);
     GD_CUDA(cudaMemcpyAsync(sq.get(), &seed, 4, cudaMemcpyHostToDevice, cs));
-    fixpoint(FP_RELAX, sq.get(), nullptr, 1, nullptr);
-    fix_parents(nullptr, nullptr, n);
+    if (g->part) {  // the source's owner seeds the supersteps
+        DBuf<int64_t> ns(1, cs);
+        const int64_t one = src >= g->own_lo && src < g->own_hi ? 1 : 0;
+        GD_CUDA(cudaMemcpyAsync(ns.get(), &one, 8, cudaMemcpyHostToDevice, cs));
+        DBuf<int32_t> sl(std::max<int64_t>(n, 1), cs);
+        GD_CUDA(cudaMemcpyAsync(sl.get(), sq.get(), 4, cudaMemcpyDeviceToDevice, cs));
+        fixpoint_dist(FP_RELAX, sl.get(), ns.get(), nullptr);
+        sync(true, false, nullptr);
+        DBuf<uint8_t> all(std::max<int64_t>(n, 1), cs);
+        GD_CUDA(cudaMemsetAsync(all.get(), 1, n, cs));
+        DBuf<int32_t> list(std::max<int64_t>(n, 1), cs);
+        owned_list(all.get(), list.get(), ns.get());
+        fix_parents(list.get(), ns.get(), n);
+        sync(false, true, nullptr);
+    } else {
+        fixpoint(FP_RELAX, sq.get(), nullptr, 1, nullptr);
+        fix_parents(nullptr, nullptr, n);
+    }
     finish();
     // low-diameter graphs (R-MAT: tens of rounds) gain nothing from buckets
     // and pay their extra rounds; keep near-far for the deep ones (grids)
@@ -703,6 +819,20 @@ void SSSP::fixpoint(int mode, const int32_t* seeds, const int64_t* d_nseeds, int
     GD_KERNEL(k_fp_prep, 1, 1, 0, s, fr.cnt.get(), d_nseeds, nseeds, nf ? fcnt.get() : nullptr,
               nf ? fmin.get() : nullptr);
     FpArgs a;
+    a.outbox = nullptr;  // set by fixpoint_dist
+    a.noutbox = nullptr;
+    a.gstamp = nullptr;
+    a.launch = 0;
+    a.own_lo = 0;
+    a.own_hi = g->n;
+    if (g->part) {
+        a.own_lo = g->own_lo;
+        a.own_hi = g->own_hi;
+        a.outbox = outbox.get();
+        a.noutbox = nbox.get();
+        a.gstamp = gstamp.get();
+        a.launch = ++launch_id;
+    }
     a.delta = nf ? delta : 0;
     for (int j = 0; j < 3; ++j) a.far[j] = nf ? far[j].get() : nullptr;
     a.fcnt = fcnt.get();
@@ -753,6 +883,69 @@ void SSSP::fixpoint(int mode, const int32_t* seeds, const int64_t* d_nseeds, int
     prof_end(pi, s);
 }
 
+void SSSP::owned_list(const uint8_t* flags, int32_t* list, int64_t* d_m) {
+    cudaStream_t s = stream();
+    GD_CUDA(cudaMemsetAsync(d_m, 0, 8, s));
+    const int64_t lo = g->own_lo, hi = g->own_hi;
+    if (hi > lo) GD_KERNEL(k_select_owned, grid_for(hi - lo, 256), 256, 0, s, flags, lo, hi, list, d_m);
+}
+
+void SSSP::sync(bool d, bool p, uint8_t* flags) {
+    if (!g->part) return;
+    cudaStream_t s = stream();
+    if (d) g->part->allgatherv(dist.get(), g->blocks, 8, s);
+    if (p) g->part->allgatherv(parent.get(), g->blocks, 4, s);
+    if (flags) g->part->allgatherv(flags, g->blocks, 1, s);
+}
+
+// Supersteps over the partition: a local fixpoint over the owned vertices
+// (the cooperative kernel, ghost targets listed in the outbox), then the
+// outboxes go to the vertices' owners (one all-to-all), which apply them --
+// min for a relaxation, invalidation for a walk -- and seed the next local
+// fixpoint with what changed.  Ends when no rank has seeds (an all-reduce).
+// Relaxation is monotone and the walk's descendant set schedule-free, so
+// the result is the single-GPU fixpoint.
+void SSSP::fixpoint_dist(int mode, int32_t* seeds, int64_t* d_nseeds, uint8_t* flags, const uint8_t* only) {
+    cudaStream_t s = stream();
+    const Comm* c = g->part;
+    const Blocks& b = g->blocks;
+    const int W = c->world;
+    const int64_t n = g->n;
+    int32_t* cur = seeds;
+    int32_t* nxt = seeds2.get();
+    DBuf<int64_t> tot(1, s), nn(1, s);
+    packed.ensure(3 * std::max<int64_t>(n, 1), s);
+    const int64_t cap = std::max<int64_t>(1, cap_factor * std::max<int64_t>(n, 1));
+    for (int64_t step = 0;; ++step) {
+        if (step >= cap) throw GdError(GD_ERR_DIVERGED, "fixed point diverged");
+        GD_CUDA(cudaMemsetAsync(nbox.get(), 0, sizeof(unsigned long long), s));
+        fixpoint(mode, cur, d_nseeds, 0, flags, only);
+        DBuf<unsigned long long> cnt(2 * W, s);
+        cnt.zero(s);
+        GD_KERNEL(k_msg_count, 148 * 4, 256, 0, s, outbox.get(), nbox.get(), b, cnt.get());
+        GD_KERNEL(k_msg_offsets, 1, 1, 0, s, cnt.get(), W, cnt.get() + W);
+        GD_KERNEL(k_msg_pack, 148 * 4, 256, 0, s, outbox.get(), nbox.get(), b, dist.get(), cnt.get() + W,
+                  packed.get());
+        DBuf<int32_t> recv;
+        const int64_t m = c->alltoallv_i32(packed.get(), reinterpret_cast<const int64_t*>(cnt.get()), 3, recv, s);
+        GD_CUDA(cudaMemsetAsync(nn.get(), 0, 8, s));
+        ++step_id;
+        if (m) GD_KERNEL(k_msg_apply, grid_for(m, 256), 256, 0, s, recv.get(), m, mode, dist.get(), parent.get(),
+                         flags, sstamp.get(), step_id, nxt, nn.get());
+        GD_CUDA(cudaMemcpyAsync(tot.get(), nn.get(), 8, cudaMemcpyDeviceToDevice, s));
+        c->allreduce_sum_i64(tot.get(), 1, s);
+        const int64_t total = read_scalar(s, tot.get());
+        static const bool dbg = getenv("GD_SSSP_DEBUG") != nullptr;
+        if (dbg)
+            fprintf(stderr, "[sssp-dist] rank %d mode %d step %lld: sent %llu received %lld seeds(all) %lld\n",
+                    c->rank, mode, (long long)step, (unsigned long long)read_scalar(s, nbox.get()), (long long)m,
+                    (long long)total);
+        if (total == 0) break;
+        GD_CUDA(cudaMemcpyAsync(d_nseeds, nn.get(), 8, cudaMemcpyDeviceToDevice, s));
+        std::swap(cur, nxt);
+    }
+}
+
 void SSSP::fix_parents(const int32_t* list, const int64_t* d_m, int64_t m) {
     if (m == 0) return;
     cudaStream_t s = stream();
@@ -787,7 +980,77 @@ void SSSP::finish() {
     }
 }
 
+// One Batch body on a vertex-partitioned store: the record handlers run on
+// every rank over all records (dist / parent are replicated), the
+// structural updates on the owners, each fixpoint as supersteps, and every
+// phase ends with the owned blocks of what it changed gathered to all ranks
+// -- so each phase starts from the same state on every rank.
+void SSSP::batch_dist(DevBatch& b, int64_t batch_index) {
+    cudaStream_t s = stream();
+    const int64_t n = g->n;
+    uint8_t* seed_del = fa.get();  // activeOnDelete, then stale
+    uint8_t* seed_add = fb.get();  // activeOnAdd, then touched
+    DBuf<int32_t> list(std::max<int64_t>(n, 1), s);
+    DBuf<int64_t> nl(1, s);
+    timer.begin(PH_PRE);
+    fa.zero(s);
+    fb.zero(s);
+    if (b.kdel) GD_KERNEL(k_on_delete, grid_for(b.kdel, 256), 256, 0, s, b.ds.get(), b.dd.get(), b.kdel, dist.get(),
+                          parent.get(), seed_del);
+    timer.begin(PH_STRUCT);
+    g->apply_deletes(b.ds.get(), b.dd.get(), b.kdel, nullptr);
+    // decrementalSSSP (sssp_dynamic.sp:37-99)
+    timer.begin(PH_PROP);
+    GD_KERNEL(k_set_i64, 1, 1, 0, s, dist.get(), (int64_t)src, (int64_t)0);
+    owned_list(seed_del, list.get(), nl.get());
+    fixpoint_dist(FP_WALK, list.get(), nl.get(), seed_del);
+    sync(true, true, seed_del);
+    GD_KERNEL(k_set_i64, 1, 1, 0, s, dist.get(), (int64_t)src, (int64_t)0);
+    owned_list(seed_del, list.get(), nl.get());
+    {  // one pull sweep over the owned stale vertices, then the push restricted to stale targets
+        IdxView ix = g->rev.view();
+        heavy.ensure(g->rev.nnz / kHeavy + 64, s);
+        GD_CUDA(cudaMemsetAsync(fr.cnt.get() + 9, 0, sizeof(unsigned long long), s));
+        GD_KERNEL_T("sssp_pull", 0, k_pull_once, group_grid(n), kThreads, 0, s, list.get(), nl.get(), ix, dist.get(),
+                    heavy.get(), fr.cnt.get() + 9);
+        GD_KERNEL_T("sssp_pull", 0, k_pull_heavy, 148 * 4, kThreads, 0, s, heavy.get(), fr.cnt.get() + 9, ix,
+                    dist.get());
+    }
+    sync(true, false, nullptr);  // the pulled distances seed pushes on other ranks
+    fixpoint_dist(FP_RELAX, list.get(), nl.get(), nullptr, seed_del);
+    sync(true, false, nullptr);
+    owned_list(seed_del, list.get(), nl.get());
+    fix_parents(list.get(), nl.get(), n);
+    sync(false, true, nullptr);
+    timer.begin(PH_PRE);
+    if (b.kadd) GD_KERNEL(k_on_add, grid_for(b.kadd, 256), 256, 0, s, b.as.get(), b.ad.get(), b.aw.get(), b.kadd,
+                          g->weighted, dist.get(), seed_add);
+    timer.begin(PH_STRUCT);
+    g->apply_adds(b.as.get(), b.ad.get(), b.aw.get(), b.kadd);
+    if (g->merge_due(batch_index)) {
+        timer.begin(PH_MERGE);
+        g->merge();
+    } else {
+        g->compact_rev();
+    }
+    // incrementalSSSP (sssp_dynamic.sp:101-130)
+    timer.begin(PH_PROP);
+    owned_list(seed_add, list.get(), nl.get());
+    fixpoint_dist(FP_RELAX, list.get(), nl.get(), seed_add);
+    sync(true, false, seed_add);
+    owned_list(seed_add, list.get(), nl.get());
+    fix_parents(list.get(), nl.get(), n);
+    sync(false, true, nullptr);
+    finish();
+    timer.end_all();
+}
+
 void SSSP::batch(DevBatch& b, int64_t batch_index) {
+    if (g->part) {
+        ProfScope ps(&prof);
+        prof.reset_last();
+        return batch_dist(b, batch_index);
+    }
     cudaStream_t s = stream();
     int64_t n = g->n;
     ProfScope ps(&prof);

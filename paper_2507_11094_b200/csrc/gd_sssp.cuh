@@ -29,9 +29,17 @@ struct SSSP : AlgoBase {
     DBuf<int32_t> heavy;
     DBuf<int64_t> parent64;  // int64 widening of parent for the async read   // stale vertices with > kHeavy in-arcs (pull sweep)
     DBuf<int64_t> dcount;  // device-side list sizes (no host read-back per fixpoint)
+    // vertex-partitioned store: dist / parent are replicated and agree on
+    // every rank between phases; the fixpoints run as supersteps of local
+    // fixpoints over owned vertices + one message exchange with the owners
+    DBuf<int32_t> outbox, gstamp, sstamp, seeds2;
+    DBuf<int32_t> packed;
+    DBuf<unsigned long long> nbox;
+    int32_t launch_id = 0, step_id = 0;
 
     SSSP(Store* st, int64_t src, int64_t cap_factor = 10);  // = staticSSSP
     void batch(DevBatch& b, int64_t batch_index);
+    void batch_dist(DevBatch& b, int64_t batch_index);  // vertex-partitioned store
     void read(int64_t* dist, int64_t* parent);
     void read_async(int64_t* dist, int64_t* parent);  // see AlgoBase::copy_out_async
 
@@ -43,6 +51,13 @@ struct SSSP : AlgoBase {
     // list == nullptr: every node; d_m (device) overrides m, which bounds the grid
     void fix_parents(const int32_t* list, const int64_t* d_m, int64_t m);
     void finish();
+    // partitioned: the fixpoint as supersteps (see gd_sssp.cu); seeds are
+    // owned vertices
+    void fixpoint_dist(int mode, int32_t* seeds, int64_t* d_nseeds, uint8_t* flags, const uint8_t* only = nullptr);
+    // partitioned: owned flagged vertices -> list (device count in d_m)
+    void owned_list(const uint8_t* flags, int32_t* list, int64_t* d_m);
+    // partitioned: every rank's owned blocks to every rank
+    void sync(bool d, bool p, uint8_t* flags);
 };
 
 }  // namespace gdb

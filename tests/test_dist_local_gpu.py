@@ -162,3 +162,30 @@ def test_partitioned_pagerank_matches_unpartitioned(gd, world):
         assert err.max() <= 1e-13, err.max()  # the dangling sum is added per rank
         np.testing.assert_array_equal(got["outdeg"], ref.properties["outdeg"].data)
         np.testing.assert_array_equal(got["affected"], ref.properties["affected"].data)
+
+
+@pytest.mark.parametrize("graph", ["rmat", "grid"])
+@pytest.mark.parametrize("world", [1, 2, 3])
+def test_partitioned_sssp_matches_unpartitioned(gd, graph, world):
+    """Supersteps of local fixpoints + owner message exchange, with dist and
+    parent gathered after every phase: exact dist and parent."""
+    from paper_2507_11094_b200 import generate as G
+
+    if graph == "rmat":
+        s, d, w, n = G.rmat(12, 40_000, seed=7, weighted=True, max_weight=100)
+    else:
+        s, d, w, n = G.grid(60, 60, seed=7)
+    kind, us, ud, uw, per = G.updates(s, d, n, percent=5, batches=3, seed=8, max_weight=100)
+    stream = gd.UpdateStream.from_arrays(kind, us, ud, uw)
+    ref = gd.run_batches(gd.shipped_program("sssp"),
+                         gd.DynamicGraph.from_arrays(n, s, d, w, weighted=True, with_reverse=True), stream, per,
+                         {"src": 0})
+
+    def rank_fn(r, comm):
+        g = gd.DynamicGraph.from_arrays(n, s, d, w, weighted=True, with_reverse=True, comm=comm)
+        ctx = gd.run_batches(gd.shipped_program("sssp"), g, stream, per, {"src": 0})
+        return np.asarray(ctx.properties["dist"].data), np.asarray(ctx.properties["parent"].data)
+
+    for dist, parent in run_ranks(world, rank_fn):
+        np.testing.assert_array_equal(dist, ref.properties["dist"].data)
+        np.testing.assert_array_equal(parent, ref.properties["parent"].data)
