@@ -380,15 +380,23 @@ def run_ours(gd, torch, wl, args, steps, warmup, e2e_steps, world, rank, local, 
     inputs resident in HBM (CUDA events on the store's stream, max over
     ranks), then e2e steps through the host-buffer C-ABI call."""
     nb = warmup + steps + 1 + e2e_steps  # +1: the untimed e2e warm-up step
-    # sharded PR / TC: every rank holds a replica of ONE job's store, so all
-    # ranks build the same graph and stream; SSSP replicas each get their own
-    one_job = dist_on and wl["algo"] in ("pr", "tc")
-    n, s, d, w, kind, us, ud, uw, per = make_inputs(wl, nb, seed=22 if one_job else 22 + 1000 * rank)
+    # N > 1 runs ONE job: every rank builds the same graph and stream.  PR and
+    # SSSP partition the store by 1D vertex blocks (each rank keeps the arcs
+    # of its sources and the in-arcs of its destinations); TC keeps a replica
+    # of the undirected graph per rank and counts a slice of the records.
+    n, s, d, w, kind, us, ud, uw, per = make_inputs(wl, nb, seed=22)
     records_per_step = per
+    comm = None
+    if dist_on:
+        from paper_2507_11094_b200.dist import Communicator
+
+        comm = Communicator.from_torch_distributed(local)
+    partitioned = comm is not None and wl["algo"] in ("pr", "sssp") and wl["directed"]
 
     t = time.time()
     g = gd.DynamicGraph.from_arrays(n, s, d, w if wl["weighted"] else None, directed=wl["directed"],
-                                    weighted=wl["weighted"], with_reverse=wl["algo"] != "tc", device=local)
+                                    weighted=wl["weighted"], with_reverse=wl["algo"] != "tc", device=local,
+                                    comm=comm if partitioned else None)
     if wl["algo"] == "pr":
         algo = gd.PRHandle(g, 0.85, 1e-3, 100)
     elif wl["algo"] == "sssp":
@@ -398,13 +406,9 @@ def run_ours(gd, torch, wl, args, steps, warmup, e2e_steps, world, rank, local, 
     torch.cuda.synchronize()
     log(f"[bench] {wl['algo']}: store + static pass: {time.time() - t:.1f}s; "
         f"device bytes {g.device_bytes() / 2**30:.2f} GiB")
-    sharded = dist_on and wl["algo"] in ("pr", "tc")
-    comm = None
-    if sharded:  # vertex-range PR pull + NCCL all-gather / record-sliced TC + all-reduce
-        from paper_2507_11094_b200.dist import Communicator
-
-        comm = Communicator.from_torch_distributed(local)
-        comm.attach(algo)
+    sharded = dist_on
+    if comm is not None and not partitioned and wl["algo"] in ("pr", "tc"):
+        comm.attach(algo)  # replicated store: TC record slices / PR destination ranges
 
     # records resident in HBM for the device-path steps (int32 ids, uint8 kind)
     dk = torch.from_numpy(kind).to(f"cuda:{local}")
@@ -510,13 +514,12 @@ def run_ours(gd, torch, wl, args, steps, warmup, e2e_steps, world, rank, local, 
         tt = torch.tensor([e2e_ms], device=f"cuda:{local}")
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
         e2e_ms = float(tt.item())
-    e2e_value = (e_done * (1 if (dist_on and wl["algo"] in ("pr", "tc")) else world)) / (e2e_ms / 1e3) \
-        if e2e_ms > 0 else None
+    e2e_value = e_done / (e2e_ms / 1e3) if e2e_ms > 0 else None  # one job over all ranks
 
     stat = _static_compare(gd, torch, wl, args, local, n, s, d, w, kind, us, ud, uw, per) if static else None
 
-    shards = dist_on and wl["algo"] in ("pr", "tc")  # one job over all GPUs vs independent replicas
-    value = (done * (1 if shards else world)) / (elapsed_ms / 1e3)
+    shards = dist_on  # one job over all GPUs
+    value = done / (elapsed_ms / 1e3)
     peak, peak_kind = load_peaks()
     dom = max(kstats.items(), key=lambda kv: kv[1][0]) if kstats else None
     roof = None
@@ -584,7 +587,7 @@ def _static_compare(gd, torch, wl, args, local, n, s, d, w, kind, us, ud, uw, pe
             "what": "apply batch + merge + static recompute from scratch (the reference bench's static column)"}
 
 
-KERNELS = ("pr_pull", "pr_contrib", "tc_bitmap", "merge_copy", "flood_sample", "flood_rest", "flood_mark", "del_scan_head", "del_scan_tail",
+KERNELS = ("pr_pull", "pr_contrib", "tc_bitmap", "merge_copy", "flood_sample", "flood_rest", "flood_mark", "flood_link", "del_scan_head", "del_scan_tail",
            "add_vacancies", "tc_count", "sssp_relax", "sssp_walk", "sssp_pull", "sssp_parent")
 
 def _graph_stream(g):
@@ -646,9 +649,11 @@ def _dtype(wl):
 def _config(wl, args, world):
     c = {"workload": wl["desc"], "algo": wl["algo"], "batch_percent": wl["percent"], "merge_interval": 1,
          "parallelism": ("single-gpu" if world == 1 else
-                         "replicated store, PR pull by dst range + NCCL all-gather" if wl["algo"] == "pr" else
-                         "replicated store, TC record slices + NCCL all-reduce" if wl["algo"] == "tc" else
-                         "replicas"),
+                         "1D vertex blocks: partitioned store, owner-routed arcs; PR contrib all-gather + BFS flood "
+                         "reduce-scatter per level" if wl["algo"] == "pr" else
+                         "1D vertex blocks: partitioned store, owner-routed arcs; SSSP supersteps with owner "
+                         "message exchange" if wl["algo"] == "sssp" else
+                         "replicated undirected store, TC record slices + NCCL all-reduce"),
          "l2": "inputs larger than L2 (graph store >> 126 MB L2)",
          "generator": ("reference generate.py recipes, seed-compatible" if GEN == "python" and wl["graph"] != "grid"
                        else "parallel counter-based RNG, reference recipes")}

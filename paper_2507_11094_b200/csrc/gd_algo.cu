@@ -382,6 +382,8 @@ __global__ void k_uf_compress_seed(int32_t* p, int64_t n, const uint8_t* flags, 
     }
 }
 
+__global__ void k_i32_to_u8(const int32_t* a, uint8_t* b) { *b = *a ? 1 : 0; }
+
 __global__ void k_uf_mark(const int32_t* p, int64_t n, const uint8_t* root_has_seed, uint8_t* flags) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         if (root_has_seed[p[i]]) flags[i] = 1;
@@ -391,53 +393,15 @@ __global__ void k_uf_mark(const int32_t* p, int64_t n, const uint8_t* root_has_s
 
 namespace {
 
-// owned flagged vertices -> the first frontier
-__global__ void k_bfs_seed(const uint8_t* flags, int64_t lo, int64_t hi, int32_t* q, unsigned long long* cnt) {
-    for (int64_t v = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < hi;
-         v += (int64_t)gridDim.x * blockDim.x)
-        if (flags[v]) q[atomicAdd(cnt, 1ULL)] = (int32_t)v;
-}
-
-// one warp per frontier vertex: touch every neighbour over the live out-arcs
-// (all segments) and in-arcs, in the padded owner-major layout of the
-// reduce-scatter (vertex w at owner(w) * chunk + w - lo(owner(w)))
-__global__ void __launch_bounds__(256) k_bfs_expand(const int32_t* q, const unsigned long long* nq, OutView ov,
-                                                    IdxView in, Blocks b, uint8_t* touched) {
-    const int lane = threadIdx.x & 31;
-    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    const int64_t m = (int64_t)*nq;
-    const int64_t ch = b.chunk();
-    for (int64_t t = warp; t < m; t += nwarps) {
-        const int32_t v = q[t];
-        for (int sg = 0; sg < ov.nseg; ++sg)
-            for (int64_t e = ov.off[sg][v] + lane; e < ov.off[sg][v + 1]; e += 32) {
-                const int32_t w = ov.col[sg][e];
-                if (w >= 0) {
-                    const int o = b.owner(w);
-                    touched[o * ch + (w - b.lo(o))] = 1;
-                }
-            }
-        if (in.off)
-            for (int64_t e = in.off[v] + lane; e < in.off[v + 1]; e += 32) {
-                const int32_t u = in.col[e];
-                if (u >= 0) {
-                    const int o = b.owner(u);
-                    touched[o * ch + (u - b.lo(o))] = 1;
-                }
-            }
-    }
-}
-
-// owned vertices touched this level and not yet flagged -> the next frontier
-__global__ void k_bfs_next(const uint8_t* mine, int64_t lo, int64_t hi, uint8_t* flags, int32_t* q,
-                           unsigned long long* cnt) {
-    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < hi - lo;
-         j += (int64_t)gridDim.x * blockDim.x)
-        if (mine[j] && !flags[lo + j]) {
-            flags[lo + j] = 1;
-            q[atomicAdd(cnt, 1ULL)] = (int32_t)(lo + j);
+// adopt the smallest label any rank gives v: hook v's local root under it
+__global__ void k_uf_adopt(int32_t* p, const int32_t* L, int64_t n, int32_t* changed) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t l = L[v];
+        if (l < uf_find(p, (int32_t)v)) {
+            uf_union(p, (int32_t)v, l);
+            *changed = 1;
         }
+    }
 }
 
 }  // namespace
@@ -452,30 +416,49 @@ int64_t flood_weak_components_dist(Store& g, uint8_t* flags, KernelProf* prof) {
         g.compact_rev();
         in = g.rev.view();
     }
-    const Blocks& b = g.blocks;
-    const int64_t ch = b.chunk(), lo = g.own_lo, hi = g.own_hi;
-    DBuf<uint8_t> touched(std::max<int64_t>(ch * b.world, 1), s), mine(std::max<int64_t>(ch, 1), s);
-    DBuf<int32_t> q(std::max<int64_t>(hi - lo, 1), s);
-    DBuf<unsigned long long> cnt(1, s);
-    DBuf<int64_t> tot(1, s);
-    cnt.zero(s);
-    if (hi > lo) GD_KERNEL(k_bfs_seed, grid_for(hi - lo, 256), 256, 0, s, flags, lo, hi, q.get(), cnt.get());
+    // Afforest over the partition: sample-link the first kSample out-arcs of
+    // the owned rows, agree on labels (rounds of a min-label all-reduce: every
+    // rank hooks each vertex under the smallest root any rank knows for it,
+    // until no rank changes), find the dominant component on the agreed
+    // labels, then only vertices outside it link their remaining out-arcs
+    // and their in-arcs -- an arc between two giant vertices is already
+    // joined, any other has an endpoint outside it whose owner holds the arc
+    // (out-row or in-row) -- and agree once more.  The labels end as the
+    // weak components' minimum ids, the same on every rank.
+    DBuf<int32_t> p(n, s), L(n, s), ch(1, s);
+    DBuf<uint8_t> seed(n, s), a(1, s);
+    int64_t rounds = 0;
+    auto agree = [&] {
+        while (true) {
+            ++rounds;
+            GD_CUDA(cudaMemcpyAsync(L.get(), p.get(), n * 4, cudaMemcpyDeviceToDevice, s));
+            g.part->allreduce_min_i32(L.get(), n, s);
+            GD_CUDA(cudaMemsetAsync(ch.get(), 0, 4, s));
+            GD_KERNEL(k_uf_adopt, grid_for(n, 256), 256, 0, s, p.get(), L.get(), n, ch.get());
+            GD_KERNEL(k_uf_compress, grid_for(n, 256), 256, 0, s, p.get(), n);
+            GD_KERNEL(k_i32_to_u8, 1, 1, 0, s, ch.get(), a.get());
+            g.part->allreduce_max_u8(a.get(), 1, s);
+            uint8_t any = 0;
+            read_small(s, &any, a.get(), 1);
+            if (!any) break;
+        }
+    };
     OutView ov = g.out_view();
-    int64_t levels = 0;
-    while (true) {
-        // frontier sizes summed over ranks: the loop ends on every rank together
-        GD_CUDA(cudaMemcpyAsync(tot.get(), cnt.get(), 8, cudaMemcpyDeviceToDevice, s));
-        g.part->allreduce_sum_i64(tot.get(), 1, s);
-        if (read_scalar(s, tot.get()) == 0) break;
-        ++levels;
-        GD_CUDA(cudaMemsetAsync(touched.get(), 0, ch * b.world, s));
-        GD_KERNEL_T("flood_bfs", 0, k_bfs_expand, 148 * 8, 256, 0, s, q.get(), cnt.get(), ov, in, b, touched.get());
-        g.part->reducescatter_max_u8(touched.get(), mine.get(), ch, s);
-        cnt.zero(s);
-        if (hi > lo) GD_KERNEL(k_bfs_next, grid_for(hi - lo, 256), 256, 0, s, mine.get(), lo, hi, flags, q.get(),
-                               cnt.get());
-    }
-    return levels;
+    GD_KERNEL(k_uf_init, grid_for(n, 256), 256, 0, s, p.get(), n, seed.get());
+    GD_KERNEL_T("flood_sample", 0, k_aff_sample, grid_for(n, 256), 256, 0, s, ov, n, p.get());
+    GD_KERNEL(k_uf_compress, grid_for(n, 256), 256, 0, s, p.get(), n);
+    agree();
+    constexpr int kProbe = 256;
+    DBuf<int32_t> probe(kProbe, s), giant(1, s);
+    GD_KERNEL(k_aff_gather, 4, 256, 0, s, p.get(), n, probe.get(), kProbe);
+    GD_KERNEL(k_aff_giant, 1, kProbe, 0, s, probe.get(), kProbe, giant.get());
+    GD_KERNEL_T("flood_rest", 0, k_aff_rest, grid_for(n, 256), 256, 0, s, ov, in, n, giant.get(), p.get());
+    GD_KERNEL(k_uf_compress, grid_for(n, 256), 256, 0, s, p.get(), n);
+    agree();
+    // the same labels on every rank: flag every vertex whose component holds a seed
+    GD_KERNEL_T("flood_mark", 0, k_uf_compress_seed, grid_for(n, 256), 256, 0, s, p.get(), n, flags, seed.get());
+    GD_KERNEL(k_uf_mark, grid_for(n, 256), 256, 0, s, p.get(), n, seed.get(), flags);
+    return rounds;
 }
 
 int64_t flood_weak_components(Store& g, uint8_t* flags, KernelProf* prof) {

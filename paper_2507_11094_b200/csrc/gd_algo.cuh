@@ -78,13 +78,13 @@ struct Frontier {
 // union-find hooking passes.
 int64_t flood_weak_components(Store& g, uint8_t* d_flags, KernelProf* prof);
 
-// The same flood on a vertex-partitioned store (Store::part): a
-// level-synchronous BFS over the weak view, each rank expanding the frontier
-// vertices it owns over their out-rows (its out-store) and in-rows (its
-// in-index), the touched flags meeting at their owners through one
-// reduce-scatter (max over bytes) per level.  The seed flags are the same on
-// every rank (records are replicated); on return the OWNED block of d_flags
-// is final (gather it for the whole vector).  Returns the BFS levels.
+// The same flood on a vertex-partitioned store (Store::part): union-find
+// over the arcs each rank holds (out-arcs of owned sources, in-arcs of owned
+// destinations), then rounds of a min-label all-reduce in which every rank
+// hooks each vertex under the smallest root any rank knows for it, until no
+// rank changes.  The seed flags are the same on every rank (records are
+// replicated), and so are the final labels: on return every rank holds the
+// whole flooded vector.  Returns the label rounds.
 int64_t flood_weak_components_dist(Store& g, uint8_t* d_flags, KernelProf* prof);
 
 // out-degree (live arcs over all segments) per node, int32

@@ -249,6 +249,15 @@ void Comm::allreduce_max_u8(uint8_t* x, int64_t count, cudaStream_t s) const {
     check(api().allreduce(x, x, (size_t)count, ncclUint8, ncclMax, (ncclComm_t)nccl, s), "ncclAllReduce(max u8)");
 }
 
+void Comm::allreduce_min_i32(int32_t* x, int64_t count, cudaStream_t s) const {
+    ++n_calls;
+    ar_bytes += count * 4;
+    sent_bytes += world > 1 ? count * 4 * 2 * (world - 1) / world : 0;
+    if (world == 1) return;
+    if (local) return local_allreduce<int32_t>(*this, x, count, s, [](int32_t a, int32_t b) { return a < b ? a : b; });
+    check(api().allreduce(x, x, (size_t)count, ncclInt32, ncclMin, (ncclComm_t)nccl, s), "ncclAllReduce(min)");
+}
+
 void Comm::allgatherv(void* buf, const Blocks& b, int elem_bytes, cudaStream_t s) const {
     ++n_calls;
     ag_bytes += b.n * elem_bytes;

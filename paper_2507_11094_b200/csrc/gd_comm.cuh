@@ -54,6 +54,7 @@ struct Comm {
     void allreduce_sum_i64(int64_t* x, int64_t count, cudaStream_t s) const;
     void allreduce_sum_f64(double* x, int64_t count, cudaStream_t s) const;
     void allreduce_max_u8(uint8_t* x, int64_t count, cudaStream_t s) const;
+    void allreduce_min_i32(int32_t* x, int64_t count, cudaStream_t s) const;
     // in-place all-gather of the block layout: rank r contributes
     // buf[lo(r), hi(r)) (grouped broadcasts, unequal blocks)
     void allgatherv(void* buf, const Blocks& b, int elem_bytes, cudaStream_t s) const;
