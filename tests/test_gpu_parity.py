@@ -348,6 +348,32 @@ def test_comm_single_rank_sharded_paths_match(gd):
     assert comm.stats()["calls"] == 2  # the delete and the add phase's count all-reduce
 
 
+def test_nccl_single_rank_partitioned_store_paths_match(gd):
+    """gd_graph_create_dist over a real NCCL communicator at world 1: the
+    partitioned store, PageRank (contrib all-gather, Afforest flood with
+    label agreement) and SSSP (supersteps) equal the unpartitioned path."""
+    from paper_2507_11094_b200.dist import Communicator, unique_id
+
+    rng = np.random.default_rng(23)
+    n = 4096
+    src, dst, w = rmat(12, 8 * n, rng, weighted=True)
+    kind, us, ud, uw = updates(rng, n, src, dst, 2000, distinct_deletes=True)
+    stream = gd.UpdateStream.from_arrays(kind, us, ud, uw)
+    comm = Communicator(1, 0, unique_id(), 0)
+    res = []
+    for c in (None, comm):
+        g = gd.DynamicGraph.from_arrays(n, src, dst, with_reverse=True, comm=c)
+        pr = gd.run_batches(gd.shipped_program("pr"), g, stream, 500, {"damping": 0.85, "beta": 1e-10,
+                                                                         "maxiter": 100})
+        g = gd.DynamicGraph.from_arrays(n, src, dst, w, weighted=True, with_reverse=True, comm=c)
+        ss = gd.run_batches(gd.shipped_program("sssp"), g, stream, 500, {"src": 0})
+        res.append((np.asarray(pr.properties["pagerank"].data), pr.properties["affected"].values(),
+                    ss.properties["dist"].values(), ss.properties["parent"].values()))
+    np.testing.assert_allclose(res[0][0], res[1][0], rtol=0, atol=1e-15)
+    assert res[0][1:] == res[1][1:]
+    assert comm.stats()["calls"] > 0
+
+
 def test_async_reads_snapshot_the_state_at_the_call(gd):
     """read_async snapshots on the device: a batch issued before wait() must
     not leak into the buffers; wait() then yields exactly the read() result."""
