@@ -734,18 +734,13 @@ __global__ void k_win_ins(int64_t nwin, const int64_t* ipos, int64_t nins, int64
 // per-entry arithmetic is 32-bit and relative to the window: the 64-bit
 // output base ws - dead + ins is formed once per window.
 template <bool FULL, bool WEIGHTED>
-__device__ __forceinline__ void edit_window(const int32_t* __restrict__ col, const int32_t* __restrict__ w,
-                                            int64_t nnz, int64_t win, const int64_t* __restrict__ dead_win,
-                                            const int64_t* __restrict__ ipos, const int64_t* __restrict__ pj_win,
-                                            const int32_t* __restrict__ icol, const int32_t* __restrict__ iw,
-                                            int32_t* __restrict__ ocol, int32_t* __restrict__ ow) {
+__device__ __forceinline__ void edit_load(const int32_t* __restrict__ col, const int32_t* __restrict__ w, int64_t nnz,
+                                          int64_t win, int32_t (&v)[kWin / 32], int32_t (&wv)[kWin / 32]) {
     constexpr int Q = kWin / 32;
     const int lane = threadIdx.x & 31;
-    const unsigned lt = (1u << lane) - 1;
     const int64_t ws = win * kWin;
     const int lim = FULL ? kWin : (int)(nnz - ws);
     const int32_t* cb = col + ws;
-    int32_t v[Q], wv[Q];
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
         const int o = q * 32 + lane;
@@ -753,6 +748,18 @@ __device__ __forceinline__ void edit_window(const int32_t* __restrict__ col, con
         v[q] = in ? __ldcs(&cb[o]) : -1;
         if (WEIGHTED) wv[q] = in ? __ldcs(&w[ws + o]) : 0;
     }
+}
+
+template <bool WEIGHTED>
+__device__ __forceinline__ void edit_store(int64_t win, const int32_t (&v)[kWin / 32], const int32_t (&wv)[kWin / 32],
+                                           const int64_t* __restrict__ dead_win, const int64_t* __restrict__ ipos,
+                                           const int64_t* __restrict__ pj_win, const int32_t* __restrict__ icol,
+                                           const int32_t* __restrict__ iw, int32_t* __restrict__ ocol,
+                                           int32_t* __restrict__ ow) {
+    constexpr int Q = kWin / 32;
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1;
+    const int64_t ws = win * kWin;
     const int64_t dead0 = dead_win[win];
     const int64_t pjw = pj_win[win], pje = pj_win[win + 1];
     const int nins = (int)(pje - pjw);
@@ -813,23 +820,185 @@ __device__ __forceinline__ void edit_window(const int32_t* __restrict__ col, con
     }
 }
 
-// 5 resident CTAs (48 registers) for the unweighted copy: more loads in
-// flight per SM, 0.280 -> 0.255 ms per C2 merge, 2.31 -> 2.13 ms on C3
-// (A/B, gpu_variants.sh).  The weighted copy keeps 4: at 48 it spills.
+// The vector path of a full window with at most 32 insertions (almost every
+// window of a batch-sized edit): two 16-byte loads per lane, the survivors
+// and the window's insertions compacted into shared memory in output order,
+// then the window's output range written with 16-byte stores (scalar head
+// and tail to reach the 16-byte grid).  Same result as edit_store.  Off by
+// default (GD_EDIT_VEC): A/B on B200, C2 merge 0.258 -> 0.292 ms, C3 2.15 ->
+// 2.10 ms per batch -- the copy is bound neither by load instructions nor by
+// loads in flight (GD_EDIT_AHEAD 2/3 were slower too), see
+// profiles/round2/README.md.
 template <bool WEIGHTED>
-__global__ void __launch_bounds__(kEditThreads, WEIGHTED ? 4 : 5) k_edit_base(const int32_t* __restrict__ col,
-                                                            const int32_t* __restrict__ w, int64_t nnz,
-                                                            const int64_t* __restrict__ dead_win,
-                                                            const int64_t* __restrict__ ipos,
-                                                            const int64_t* __restrict__ pj_win,
-                                                            const int32_t* __restrict__ icol,
-                                                            const int32_t* __restrict__ iw, int64_t nwin,
-                                                            int32_t* __restrict__ ocol, int32_t* __restrict__ ow) {
+__device__ __forceinline__ void edit_window_vec(const int32_t* __restrict__ col, const int32_t* __restrict__ w,
+                                                int64_t win, const int64_t* __restrict__ dead_win,
+                                                const int64_t* __restrict__ ipos, const int64_t* __restrict__ pj_win,
+                                                const int32_t* __restrict__ icol, const int32_t* __restrict__ iw,
+                                                int32_t* __restrict__ ocol, int32_t* __restrict__ ow, int32_t* sc,
+                                                int32_t* sw) {
+    const int lane = threadIdx.x & 31;
+    const int64_t ws = win * kWin;
+    const int4* c4 = reinterpret_cast<const int4*>(col + ws);
+    const int4 a = __ldcs(c4 + lane), b = __ldcs(c4 + 32 + lane);
+    int4 wa, wb;
+    if (WEIGHTED) {
+        const int4* w4 = reinterpret_cast<const int4*>(w + ws);
+        wa = __ldcs(w4 + lane);
+        wb = __ldcs(w4 + 32 + lane);
+    }
+    const int64_t dead0 = dead_win[win];
+    const int64_t pjw = pj_win[win];
+    const int nins = (int)(pj_win[win + 1] - pjw);
+    int my_ins = INT_MAX;
+    int32_t my_icol = 0, my_iw = 1;
+    if (lane < nins) {
+        my_ins = (int)(ipos[pjw + lane] - ws);
+        my_icol = icol[pjw + lane];
+        if (WEIGHTED && iw) my_iw = iw[pjw + lane];
+    }
+    const int32_t e[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    int32_t f[8];
+    if (WEIGHTED) {
+        f[0] = wa.x, f[1] = wa.y, f[2] = wa.z, f[3] = wa.w, f[4] = wb.x, f[5] = wb.y, f[6] = wb.z, f[7] = wb.w;
+    }
+    // survivors per lane in each half, then warp-exclusive prefixes
+    unsigned al0 = 0, al1 = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        al0 |= (unsigned)(e[j] >= 0) << j;
+        al1 |= (unsigned)(e[4 + j] >= 0) << j;
+    }
+    const int s0 = __popc(al0), s1 = __popc(al1);
+    int p0 = s0, p1 = s1;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int x0 = __shfl_up_sync(0xffffffffu, p0, o), x1 = __shfl_up_sync(0xffffffffu, p1, o);
+        if (lane >= o) {
+            p0 += x0;
+            p1 += x1;
+        }
+    }
+    const int tot0 = __shfl_sync(0xffffffffu, p0, 31), tot = tot0 + __shfl_sync(0xffffffffu, p1, 31);
+    p0 -= s0;         // survivors before my first half
+    p1 += tot0 - s1;  // ... before my second half
+    // each survivor goes after the survivors and insertions before it
+    // (insertion positions are sorted, at most 32 per window)
+    {
+        int r0 = p0, r1 = p1;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int o = (q < 4 ? 0 : 128) + 4 * lane + (q & 3);
+            int ins = 0;
+            for (int k = 0; k < nins; ++k) ins += __shfl_sync(0xffffffffu, my_ins, k) <= o;
+            if (e[q] >= 0) {
+                const int r = q < 4 ? r0++ : r1++;
+                sc[r + ins] = e[q];
+                if (WEIGHTED) sw[r + ins] = f[q];
+            }
+        }
+    }
+    // an insertion lands after the survivors before its position, and after
+    // the insertions before it
+    {
+        const int P = lane < nins ? my_ins : 0;
+        const int ll = (P & 127) >> 2, jj = P & 3;
+        const int pp0 = __shfl_sync(0xffffffffu, p0, ll), pp1 = __shfl_sync(0xffffffffu, p1, ll);
+        const unsigned m0 = __shfl_sync(0xffffffffu, al0, ll), m1 = __shfl_sync(0xffffffffu, al1, ll);
+        if (lane < nins) {
+            const int before = (P >= 128 ? pp1 : pp0) + __popc((P >= 128 ? m1 : m0) & ((1u << jj) - 1));
+            sc[before + lane] = my_icol;
+            if (WEIGHTED) sw[before + lane] = my_iw;
+        }
+    }
+    __syncwarp();
+    const int64_t obase = ws - dead0 + pjw;
+    const int cnt = tot + nins;
+    // 16-byte stores on the output's 16-byte grid
+    const int head = (int)((4 - (obase & 3)) & 3) < cnt ? (int)((4 - (obase & 3)) & 3) : cnt;
+    if (lane < head) {
+        __stcs(&ocol[obase + lane], sc[lane]);
+        if (WEIGHTED) __stcs(&ow[obase + lane], sw[lane]);
+    }
+    const int nv = (cnt - head) >> 2;
+    int4* o4 = reinterpret_cast<int4*>(ocol + obase + head);
+    int4* ow4 = WEIGHTED ? reinterpret_cast<int4*>(ow + obase + head) : nullptr;
+    for (int t = lane; t < nv; t += 32) {
+        const int b0 = head + 4 * t;
+        __stcs(o4 + t, make_int4(sc[b0], sc[b0 + 1], sc[b0 + 2], sc[b0 + 3]));
+        if (WEIGHTED) __stcs(ow4 + t, make_int4(sw[b0], sw[b0 + 1], sw[b0 + 2], sw[b0 + 3]));
+    }
+    const int tail0 = head + 4 * nv;
+    if (lane < cnt - tail0) {
+        __stcs(&ocol[obase + tail0 + lane], sc[tail0 + lane]);
+        if (WEIGHTED) __stcs(&ow[obase + tail0 + lane], sw[tail0 + lane]);
+    }
+    __syncwarp();
+}
+
+// Each warp keeps the loads of GD_EDIT_AHEAD windows in flight: they are all
+// issued before the first window's shifted stores, which doubles the bytes
+// a warp has outstanding (the copy is bound by memory-level parallelism).
+#ifndef GD_EDIT_AHEAD
+#define GD_EDIT_AHEAD 1
+#endif
+#ifndef GD_EDIT_VEC
+#define GD_EDIT_VEC 0
+#endif
+#ifndef GD_EDIT_MINB_U
+#define GD_EDIT_MINB_U 5
+#endif
+#ifndef GD_EDIT_MINB_W
+#define GD_EDIT_MINB_W 4
+#endif
+template <bool WEIGHTED>
+__global__ void __launch_bounds__(kEditThreads, WEIGHTED ? GD_EDIT_MINB_W : GD_EDIT_MINB_U)
+    k_edit_base(const int32_t* __restrict__ col, const int32_t* __restrict__ w, int64_t nnz,
+                const int64_t* __restrict__ dead_win, const int64_t* __restrict__ ipos,
+                const int64_t* __restrict__ pj_win, const int32_t* __restrict__ icol, const int32_t* __restrict__ iw,
+                int64_t nwin, int32_t* __restrict__ ocol, int32_t* __restrict__ ow) {
+    constexpr int A = GD_EDIT_AHEAD;
+    constexpr int Q = kWin / 32;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const int64_t nfull = nnz / kWin;
-    for (int64_t win = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; win < nwin; win += nwarps) {
-        if (win < nfull) edit_window<true, WEIGHTED>(col, w, nnz, win, dead_win, ipos, pj_win, icol, iw, ocol, ow);
-        else edit_window<false, WEIGHTED>(col, w, nnz, win, dead_win, ipos, pj_win, icol, iw, ocol, ow);
+    const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    // full windows, A adjacent ones per warp step: A*g .. A*g + A-1 for group g
+    const int64_t ngrp = nfull / A;
+#if GD_EDIT_VEC
+    if (A == 1) {
+        __shared__ __align__(16) int32_t stc[kEditThreads / 32][kWin + 32];
+        __shared__ __align__(16) int32_t stw[WEIGHTED ? kEditThreads / 32 : 1][kWin + 32];
+        int32_t* sc = stc[threadIdx.x >> 5];
+        int32_t* sw = WEIGHTED ? stw[threadIdx.x >> 5] : nullptr;
+        for (int64_t win = w0; win < nfull; win += nwarps) {
+            if (pj_win[win + 1] - pj_win[win] <= 32) {
+                edit_window_vec<WEIGHTED>(col, w, win, dead_win, ipos, pj_win, icol, iw, ocol, ow, sc, sw);
+            } else {
+                int32_t v[Q], wv[Q];
+                edit_load<true, WEIGHTED>(col, w, nnz, win, v, wv);
+                edit_store<WEIGHTED>(win, v, wv, dead_win, ipos, pj_win, icol, iw, ocol, ow);
+            }
+        }
+        for (int64_t win = nfull + w0; win < nwin; win += nwarps) {
+            int32_t v[Q], wv[Q];
+            edit_load<false, WEIGHTED>(col, w, nnz, win, v, wv);
+            edit_store<WEIGHTED>(win, v, wv, dead_win, ipos, pj_win, icol, iw, ocol, ow);
+        }
+        return;
+    }
+#endif
+    for (int64_t g = w0; g < ngrp; g += nwarps) {
+        int32_t v[A][Q], wv[A][Q];
+#pragma unroll
+        for (int a = 0; a < A; ++a) edit_load<true, WEIGHTED>(col, w, nnz, g * A + a, v[a], wv[a]);
+#pragma unroll
+        for (int a = 0; a < A; ++a)
+            edit_store<WEIGHTED>(g * A + a, v[a], wv[a], dead_win, ipos, pj_win, icol, iw, ocol, ow);
+    }
+    for (int64_t win = ngrp * A + w0; win < nwin; win += nwarps) {  // the rest one at a time (the last may be partial)
+        int32_t v[Q], wv[Q];
+        if (win < nfull) edit_load<true, WEIGHTED>(col, w, nnz, win, v, wv);
+        else edit_load<false, WEIGHTED>(col, w, nnz, win, v, wv);
+        edit_store<WEIGHTED>(win, v, wv, dead_win, ipos, pj_win, icol, iw, ocol, ow);
     }
 }
 
