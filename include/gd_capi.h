@@ -206,9 +206,21 @@ GD_API int gd_comm_destroy(gd_comm* c);
  * ((world-1)/world of an all-gather's payload, 2(world-1)/world of an
  * all-reduce's) -- counted since creation or the last reset */
 GD_API int gd_comm_stats(const gd_comm* c, int64_t out[4]);
+/* the same plus out[4] = bytes this rank sent to other ranks through the
+ * all-to-all exchanges (routed arcs, SSSP messages) */
+GD_API int gd_comm_stats_ex(const gd_comm* c, int64_t out[5]);
 GD_API int gd_comm_reset_stats(gd_comm* c);
 GD_API int gd_pr_set_comm(gd_pr* p, gd_comm* c);
 GD_API int gd_tc_set_comm(gd_tc* t, gd_comm* c);
+
+/* ---- the store path's device primitives on host arrays (test hooks; no
+ *      reference counterpart).  gd_prim_sort: stable LSD radix sort of n keys
+ *      (key_bytes 8, values optional; or 4 with values) on bits [0, end_bit).
+ *      gd_prim_scan_select: exclusive int64 scan of `in` into `out`, and the
+ *      ordered indices of the nonzero flags into idx (count in *count). */
+GD_API int gd_prim_sort(int key_bytes, void* keys, int32_t* vals, int64_t n, int end_bit, int device);
+GD_API int gd_prim_scan_select(const int64_t* in, int64_t* out, const uint8_t* flags, int32_t* idx, int64_t n,
+                               int64_t* count, int device);
 
 /* ---- reporting (ExecContext.phase_totals / fixedpoint_iterations,
  *      engine/interp.py:112-145); h is any gd_sssp* / gd_pr* / gd_tc* ---- */

@@ -82,6 +82,9 @@ SIGNATURES = [
     ("gd_pr_read_async", C.c_int, [vp, vp]),
     ("gd_wait", C.c_int, [vp]),
     ("gd_comm_reset_stats", C.c_int, [vp]),
+    ("gd_prim_sort", C.c_int, [C.c_int, vp, vp, i64, C.c_int, C.c_int]),
+    ("gd_prim_scan_select", C.c_int, [vp, vp, vp, vp, i64, i64p, C.c_int]),
+    ("gd_comm_stats_ex", C.c_int, [vp, i64p]),
     ("gd_kernel_time_total", C.c_int, [vp, C.c_char_p, f64p, i64p, i64p]),
     ("gd_set_profiling", C.c_int, [vp, C.c_int]),
 ]

@@ -5,9 +5,10 @@ programs: `run`, `gen-updates`, `bench` and `oracle`, with the same flags,
 CSV / manifest outputs and exit codes (0 ok, 1 usage, 2 compile, 3 runtime,
 4 equivalence failure).  Every computation runs on the GPU store; `oracle`
 is the static recompute (staticSSSP / staticPR / staticTC) of the replayed
-final graph.  `emit` (OpenMP code generation) and `sim` (the partition
-simulator) belong to the reference's compiler / simulator and are out of
-scope: they exit with a usage error.
+final graph.  `sim --ranks R` runs the program on a real vertex-partitioned
+store over R in-process ranks and reports per-rank communication (DESIGN.md
+§5).  `emit` (OpenMP code generation) belongs to the reference's compiler
+and is out of scope: it exits with a usage error.
 
 Graph and update files may be the reference's text formats or the binary
 formats of io.py (detected by magic).
@@ -20,6 +21,7 @@ from __future__ import annotations
 import argparse
 import csv
 import math
+import os
 import sys
 import time
 from pathlib import Path
@@ -108,7 +110,8 @@ def make_parser() -> _Parser:
     emit.add_argument("--schedule", default="dynamic")
     emit.add_argument("--out", default="graphdyn_out")
 
-    sim = sub.add_parser("sim", help="(reference partition simulator; not part of the B200 path)")
+    sim = sub.add_parser("sim", help="run on a vertex-partitioned store over R in-process ranks (one GPU) and "
+                                     "report per-rank communication")
     sim.add_argument("program")
     sim.add_argument("graph")
     sim.add_argument("--ranks", type=int, required=True)
@@ -569,6 +572,77 @@ def cmd_oracle(args) -> int:
     return EXIT_OK
 
 
+def cmd_sim(args) -> int:
+    """cli.py:520-568 on the B200 path: instead of the reference's
+    in-process simulation of one-sided windows, the program runs on a REAL
+    vertex-partitioned store (gd_graph_create_dist) over `--ranks` ranks of
+    an in-process group on one GPU (one host thread per rank, the NCCL call
+    sequence with device copies), and commstats.csv reports what each rank
+    actually moved.  Directed SSSP / PR partition the store; TC (undirected)
+    keeps replicas and splits the records.  Results come from rank 0 (every
+    rank holds the same values)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from .dist import Communicator
+    from .graph import DynamicGraph
+
+    if args.partitioner != "block":
+        raise UsageError("the B200 path partitions by 1D vertex blocks only (--partitioner block)")
+    if args.ranks < 1:
+        raise UsageError("--ranks must be >= 1")
+    check = _compile(args.program)
+    updates = _load_updates(args.updates)
+    entry = args.entry or check.program.entry
+    if check.program.function(entry) is None:
+        raise UsageError(f"no function named {entry!r}")
+    inputs = _bind_inputs(entry, args, updates)
+    s, d, w, weighted, max_id, n_hint, _ = _read_edges(args.graph)
+    n = args.nodes if args.nodes is not None else (n_hint if n_hint is not None else max_id + 1)
+    directed = not args.undirected
+    name = check.program.name
+    partition = directed and name in ("sssp_dynamic", "pr_dynamic")
+    if args.ranks > max(n, 1):
+        raise UsageError(f"rank_count {args.ranks} exceeds node count {n}")
+    comms = Communicator.local_group(args.ranks, device=args.device, group=os.getpid())
+
+    def rank_fn(r):
+        g = DynamicGraph.from_arrays(max(n, 0), s, d, w, directed=directed, weighted=weighted,
+                                     merge_interval=args.merge_interval, with_reverse=needs_reverse(check.program),
+                                     device=args.device, comm=comms[r] if partition else None)
+        kw = {}
+        if not partition and name == "tc_dynamic":
+            kw["comm"] = comms[r]
+        ctx = run_program(check, g, inputs, entry=entry, iteration_cap_factor=args.iteration_cap_factor, **kw)
+        return ctx, comms[r].stats()
+
+    start = time.perf_counter()
+    with ThreadPoolExecutor(args.ranks) as ex:
+        res = list(ex.map(rank_fn, range(args.ranks)))
+    wall = time.perf_counter() - start
+    ctx = res[0][0]
+    files = _dump_results(ctx, args.out)
+    stats_path = Path(args.out) / "commstats.csv"
+    cols = ["rank", "collective_calls", "allgather_bytes", "allreduce_bytes", "alltoall_bytes", "bytes_moved"]
+    rows = [{"rank": r, "collective_calls": st["calls"], "allgather_bytes": st["allgather_bytes"],
+             "allreduce_bytes": st["allreduce_bytes"], "alltoall_bytes": st["alltoall_bytes"],
+             "bytes_moved": st["sent_bytes"]} for r, (_, st) in enumerate(res)]
+    with open(stats_path, "w", newline="") as fh:
+        wr = csv.DictWriter(fh, fieldnames=cols)
+        wr.writeheader()
+        for row in rows:
+            wr.writerow(row)
+    manifest = build_manifest(command="sim", args=vars(args), seed=args.seed,
+                              input_files={"program": args.program if Path(args.program).is_file() else None,
+                                           "graph": args.graph, "updates": args.updates},
+                              ctx=ctx, extra={"wall_seconds": wall, "ranks": args.ranks,
+                                              "partitioned_store": partition,
+                                              "results": files + [str(stats_path)],
+                                              "comm_totals": {c: sum(r[c] for r in rows) for c in cols[1:]}})
+    write_manifest(manifest, args.out)
+    print(f"per-rank communication stats in {stats_path}")
+    return EXIT_OK
+
+
 def cmd_out_of_scope(args) -> int:
     raise UsageError(f"'{args.command}' belongs to the reference's compiler / simulator and is not part of the "
                      f"B200 path (DESIGN.md §8)")
@@ -578,7 +652,7 @@ def main(argv: Optional[List[str]] = None) -> int:
     parser = make_parser()
     args = parser.parse_args(argv)
     handlers = {"run": cmd_run, "gen-updates": cmd_gen_updates, "bench": cmd_bench, "emit": cmd_out_of_scope,
-                "sim": cmd_out_of_scope, "oracle": cmd_oracle}
+                "sim": cmd_sim, "oracle": cmd_oracle}
     try:
         return handlers[args.command](args)
     except UsageError as exc:

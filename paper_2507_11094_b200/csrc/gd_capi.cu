@@ -580,6 +580,57 @@ int gd_comm_create(int world, int rank, const uint8_t id[128], int device, gd_co
         *out = h;
     });
 }
+// ---- the store's device primitives on host arrays (tests) ----
+int gd_prim_sort(int key_bytes, void* keys, int32_t* vals, int64_t n, int end_bit, int device) {
+    return guard([&] {
+        GD_CUDA(cudaSetDevice(device));
+        cudaStream_t s = nullptr;
+        GD_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        {
+            gdb::DBuf<uint64_t> k((n * key_bytes + 7) / 8 + 1, s);
+            gdb::DBuf<int32_t> v(vals ? n + 1 : 0, s);
+            GD_CUDA(cudaMemcpyAsync(k.get(), keys, n * key_bytes, cudaMemcpyHostToDevice, s));
+            if (vals) GD_CUDA(cudaMemcpyAsync(v.get(), vals, n * 4, cudaMemcpyHostToDevice, s));
+            if (key_bytes == 8 && vals) gdb::sort_pairs_u64(s, k.get(), v.get(), n, end_bit);
+            else if (key_bytes == 8) gdb::sort_keys_u64(s, k.get(), n, end_bit);
+            else if (key_bytes == 4 && vals)
+                gdb::sort_pairs_u32(s, reinterpret_cast<uint32_t*>(k.get()), v.get(), n, end_bit);
+            else throw gdb::GdError(GD_ERR_CONTRACT, "key_bytes 8 (values optional) or 4 (with values)");
+            GD_CUDA(cudaMemcpyAsync(keys, k.get(), n * key_bytes, cudaMemcpyDeviceToHost, s));
+            if (vals) GD_CUDA(cudaMemcpyAsync(vals, v.get(), n * 4, cudaMemcpyDeviceToHost, s));
+            GD_CUDA(cudaStreamSynchronize(s));
+        }
+        gdb::dev_cache_release(s);
+        GD_CUDA(cudaStreamSynchronize(s));
+        cudaStreamDestroy(s);
+    });
+}
+
+int gd_prim_scan_select(const int64_t* in, int64_t* out, const uint8_t* flags, int32_t* idx, int64_t n,
+                        int64_t* count, int device) {
+    return guard([&] {
+        GD_CUDA(cudaSetDevice(device));
+        cudaStream_t s = nullptr;
+        GD_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        {
+            gdb::DBuf<int64_t> a(n + 1, s), b(n + 1, s), c(1, s);
+            gdb::DBuf<uint8_t> f(n + 1, s);
+            gdb::DBuf<int32_t> o(n + 1, s);
+            GD_CUDA(cudaMemcpyAsync(a.get(), in, n * 8, cudaMemcpyHostToDevice, s));
+            GD_CUDA(cudaMemcpyAsync(f.get(), flags, n, cudaMemcpyHostToDevice, s));
+            gdb::exclusive_scan_i64(s, a.get(), b.get(), n);
+            gdb::select_flagged_index_async(s, f.get(), n, o.get(), c.get());
+            GD_CUDA(cudaMemcpyAsync(out, b.get(), n * 8, cudaMemcpyDeviceToHost, s));
+            GD_CUDA(cudaMemcpyAsync(count, c.get(), 8, cudaMemcpyDeviceToHost, s));
+            GD_CUDA(cudaMemcpyAsync(idx, o.get(), n * 4, cudaMemcpyDeviceToHost, s));
+            GD_CUDA(cudaStreamSynchronize(s));
+        }
+        gdb::dev_cache_release(s);
+        GD_CUDA(cudaStreamSynchronize(s));
+        cudaStreamDestroy(s);
+    });
+}
+
 int gd_comm_create_local(int world, int rank, int64_t group, int device, gd_comm** out) {
     return guard([&] {
         if (!out) throw gdb::GdError(GD_ERR_CONTRACT, "null output handle");
@@ -609,9 +660,16 @@ int gd_comm_stats(const gd_comm* c, int64_t out[4]) {
     return ok();
 }
 
+int gd_comm_stats_ex(const gd_comm* c, int64_t out[5]) {
+    if (!c || !c->c) return null_handle();
+    gd_comm_stats(c, out);
+    out[4] = c->c->p2p_bytes;
+    return ok();
+}
+
 int gd_comm_reset_stats(gd_comm* c) {
     if (!c || !c->c) return null_handle();
-    c->c->n_calls = c->c->ag_bytes = c->c->ar_bytes = c->c->sent_bytes = 0;
+    c->c->n_calls = c->c->ag_bytes = c->c->ar_bytes = c->c->sent_bytes = c->c->p2p_bytes = 0;
     return ok();
 }
 

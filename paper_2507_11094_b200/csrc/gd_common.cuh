@@ -167,17 +167,10 @@ void sort_pairs_u64(cudaStream_t s, uint64_t* keys, int32_t* vals, int64_t n, in
 void sort_pairs_u32(cudaStream_t s, uint32_t* keys, int32_t* vals, int64_t n, int end_bit = 32);
 void sort_keys_u64(cudaStream_t s, uint64_t* keys, int64_t n, int end_bit = 64);
 void exclusive_scan_i64(cudaStream_t s, const int64_t* in, int64_t* out, int64_t n);
-void inclusive_scan_i64(cudaStream_t s, const int64_t* in, int64_t* out, int64_t n);
-int64_t sum_i64(cudaStream_t s, const int64_t* in, int64_t n);  // synchronous result
 // Compact indices i in [0, n) with flags[i] != 0 into out (ordered); returns count (sync).
 int64_t select_flagged_index(cudaStream_t s, const uint8_t* flags, int64_t n, int32_t* out);
 // Same, count left in device memory (no sync).
 void select_flagged_index_async(cudaStream_t s, const uint8_t* flags, int64_t n, int32_t* out, int64_t* d_count);
-// Stable 3-way split of a vertex list by row length (off[v+1]-off[v]):
-// <= t1, <= t2, rest (rest in reverse order).  d_counts[0..1] = sizes of the
-// first two parts (device; asynchronous).
-void partition3_by_degree(cudaStream_t s, const int32_t* list, int64_t m, const int64_t* off, int64_t t1,
-                          int64_t t2, int32_t* out1, int32_t* out2, int32_t* out3, int* d_counts);
 void iota_i32(cudaStream_t s, int32_t* a, int64_t n);
 void fill_i64(cudaStream_t s, int64_t* a, int64_t n, int64_t v);
 void fill_i32(cudaStream_t s, int32_t* a, int64_t n, int32_t v);

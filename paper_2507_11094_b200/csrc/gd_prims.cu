@@ -1,89 +1,16 @@
-#include <vector>
-#include <mutex>
-#include <map>
+// gd_prims.cu -- device memory (a per-stream cache over the stream-ordered
+// pool), small read-backs and fills.  The sort / scan / select primitives are
+// in gd_sort.cu.
 #include <cstring>
-// gd_prims.cu -- device-wide sort / scan / select primitives (CUB, stream-ordered).
-#include <cub/cub.cuh>
-#include <thrust/iterator/counting_iterator.h>
+#include <map>
+#include <mutex>
+#include <vector>
 
 #include "gd_common.cuh"
 #include "gd_launch.cuh"
 
 namespace gdb {
 
-namespace {
-struct Temp {
-    void* p = nullptr;
-    size_t bytes = 0;
-    cudaStream_t s;
-    Temp(size_t b, cudaStream_t st) : bytes(b), s(st) {
-        if (b) p = dev_alloc(b, st);
-    }
-    ~Temp() {
-        if (p) dev_free(p, bytes, s);
-    }
-};
-}  // namespace
-
-void sort_pairs_u64(cudaStream_t s, uint64_t* keys, int32_t* vals, int64_t n, int end_bit) {
-    if (n <= 1) return;
-    DBuf<uint64_t> k2(n, s);
-    DBuf<int32_t> v2(n, s);
-    cub::DoubleBuffer<uint64_t> kb(keys, k2.get());
-    cub::DoubleBuffer<int32_t> vb(vals, v2.get());
-    size_t bytes = 0;
-    GD_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, kb, vb, n, 0, end_bit, s));
-    Temp t(bytes, s);
-    GD_CUDA(cub::DeviceRadixSort::SortPairs(t.p, bytes, kb, vb, n, 0, end_bit, s));
-    count_library_launch();
-    if (kb.Current() != keys) GD_CUDA(cudaMemcpyAsync(keys, kb.Current(), n * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
-    if (vb.Current() != vals) GD_CUDA(cudaMemcpyAsync(vals, vb.Current(), n * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
-}
-
-void sort_pairs_u32(cudaStream_t s, uint32_t* keys, int32_t* vals, int64_t n, int end_bit) {
-    if (n <= 1) return;
-    DBuf<uint32_t> k2(n, s);
-    DBuf<int32_t> v2(n, s);
-    cub::DoubleBuffer<uint32_t> kb(keys, k2.get());
-    cub::DoubleBuffer<int32_t> vb(vals, v2.get());
-    size_t bytes = 0;
-    GD_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, kb, vb, n, 0, end_bit, s));
-    Temp t(bytes, s);
-    GD_CUDA(cub::DeviceRadixSort::SortPairs(t.p, bytes, kb, vb, n, 0, end_bit, s));
-    count_library_launch();
-    if (kb.Current() != keys) GD_CUDA(cudaMemcpyAsync(keys, kb.Current(), n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
-    if (vb.Current() != vals) GD_CUDA(cudaMemcpyAsync(vals, vb.Current(), n * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
-}
-
-void sort_keys_u64(cudaStream_t s, uint64_t* keys, int64_t n, int end_bit) {
-    if (n <= 1) return;
-    DBuf<uint64_t> k2(n, s);
-    cub::DoubleBuffer<uint64_t> kb(keys, k2.get());
-    size_t bytes = 0;
-    GD_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, bytes, kb, n, 0, end_bit, s));
-    Temp t(bytes, s);
-    GD_CUDA(cub::DeviceRadixSort::SortKeys(t.p, bytes, kb, n, 0, end_bit, s));
-    count_library_launch();
-    if (kb.Current() != keys) GD_CUDA(cudaMemcpyAsync(keys, kb.Current(), n * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
-}
-
-void exclusive_scan_i64(cudaStream_t s, const int64_t* in, int64_t* out, int64_t n) {
-    if (n <= 0) return;
-    size_t bytes = 0;
-    GD_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, n, s));
-    Temp t(bytes, s);
-    GD_CUDA(cub::DeviceScan::ExclusiveSum(t.p, bytes, in, out, n, s));
-    count_library_launch();
-}
-
-void inclusive_scan_i64(cudaStream_t s, const int64_t* in, int64_t* out, int64_t n) {
-    if (n <= 0) return;
-    size_t bytes = 0;
-    GD_CUDA(cub::DeviceScan::InclusiveSum(nullptr, bytes, in, out, n, s));
-    Temp t(bytes, s);
-    GD_CUDA(cub::DeviceScan::InclusiveSum(t.p, bytes, in, out, n, s));
-    count_library_launch();
-}
 
 namespace {
 struct DevCache {
@@ -169,64 +96,6 @@ void read_small(cudaStream_t s, void* host, const void* dev, size_t bytes) {
     GD_CUDA(cudaMemcpyAsync(pin, dev, bytes, cudaMemcpyDeviceToHost, s));
     GD_CUDA(cudaStreamSynchronize(s));
     memcpy(host, pin, bytes);
-}
-
-int64_t sum_i64(cudaStream_t s, const int64_t* in, int64_t n) {
-    if (n <= 0) return 0;
-    DBuf<int64_t> o(1, s);
-    size_t bytes = 0;
-    GD_CUDA(cub::DeviceReduce::Sum(nullptr, bytes, in, o.get(), n, s));
-    Temp t(bytes, s);
-    GD_CUDA(cub::DeviceReduce::Sum(t.p, bytes, in, o.get(), n, s));
-    count_library_launch();
-    return read_scalar(s, o.get());
-}
-
-int64_t select_flagged_index(cudaStream_t s, const uint8_t* flags, int64_t n, int32_t* out) {
-    if (n <= 0) return 0;
-    DBuf<int64_t> cnt(1, s);
-    thrust::counting_iterator<int32_t> it(0);
-    size_t bytes = 0;
-    GD_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, it, flags, out, cnt.get(), n, s));
-    Temp t(bytes, s);
-    GD_CUDA(cub::DeviceSelect::Flagged(t.p, bytes, it, flags, out, cnt.get(), n, s));
-    count_library_launch();
-    return read_scalar(s, cnt.get());
-}
-
-namespace {
-struct DegAtMost {
-    const int64_t* off;
-    int64_t t;
-    __device__ bool operator()(const int32_t& v) const { return off[v + 1] - off[v] <= t; }
-};
-}  // namespace
-
-void partition3_by_degree(cudaStream_t s, const int32_t* list, int64_t m, const int64_t* off, int64_t t1,
-                          int64_t t2, int32_t* out1, int32_t* out2, int32_t* out3, int* d_counts) {
-    if (m <= 0) {
-        GD_CUDA(cudaMemsetAsync(d_counts, 0, 2 * sizeof(int), s));
-        return;
-    }
-    size_t bytes = 0;
-    DegAtMost a{off, t1}, b{off, t2};
-    GD_CUDA(cub::DevicePartition::If(nullptr, bytes, list, out1, out2, out3, d_counts, (int)m, a, b, s));
-    Temp t(bytes, s);
-    GD_CUDA(cub::DevicePartition::If(t.p, bytes, list, out1, out2, out3, d_counts, (int)m, a, b, s));
-    count_library_launch();
-}
-
-void select_flagged_index_async(cudaStream_t s, const uint8_t* flags, int64_t n, int32_t* out, int64_t* d_count) {
-    if (n <= 0) {
-        GD_CUDA(cudaMemsetAsync(d_count, 0, sizeof(int64_t), s));
-        return;
-    }
-    thrust::counting_iterator<int32_t> it(0);
-    size_t bytes = 0;
-    GD_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, it, flags, out, d_count, n, s));
-    Temp t(bytes, s);
-    GD_CUDA(cub::DeviceSelect::Flagged(t.p, bytes, it, flags, out, d_count, n, s));
-    count_library_launch();
 }
 
 __global__ void k_iota_i32(int32_t* a, int64_t n) {

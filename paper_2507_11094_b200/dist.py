@@ -106,10 +106,10 @@ class Communicator:
         """Communication accounting since creation / reset (CommStats analogue)."""
         import numpy as np
 
-        out = np.zeros(4, dtype=np.int64)
-        N.check(N.lib().gd_comm_stats(self.h, out.ctypes.data_as(C.POINTER(C.c_int64))))
+        out = np.zeros(5, dtype=np.int64)
+        N.check(N.lib().gd_comm_stats_ex(self.h, out.ctypes.data_as(C.POINTER(C.c_int64))))
         return {"calls": int(out[0]), "allgather_bytes": int(out[1]), "allreduce_bytes": int(out[2]),
-                "sent_bytes": int(out[3])}
+                "sent_bytes": int(out[3]), "alltoall_bytes": int(out[4])}
 
     def reset_stats(self) -> None:
         N.check(N.lib().gd_comm_reset_stats(self.h))

@@ -347,9 +347,13 @@ def _batch_size(inputs, stream_len: int) -> int:
 
 def run_program(check, graph: DynamicGraph, inputs: Dict[str, object], *, entry: Optional[str] = None,
                 worker_count: int = 1, iteration_cap_factor: int = 10, debug: bool = False,
-                gview=None) -> ExecContext:
+                gview=None, comm=None) -> ExecContext:
     """engine/run.py:22-41 on the B200 path.  worker_count/debug/gview are
-    accepted for signature compatibility; the GPU path has no worker pool."""
+    accepted for signature compatibility; the GPU path has no worker pool.
+
+    A graph built with a communicator (DynamicGraph.from_arrays(comm=...))
+    runs partitioned on every rank.  comm= splits a TC (or PR) handle over a
+    replicated store instead (gd_tc_set_comm / gd_pr_set_comm)."""
     program = check.program
     name = _program_name(program)
     entry = entry or getattr(program, "entry", None) or _DRIVER[name]
@@ -375,6 +379,8 @@ def run_program(check, graph: DynamicGraph, inputs: Dict[str, object], *, entry:
                         _need(inputs, "maxiter", int))
     else:
         algo = TCHandle(graph)
+    if comm is not None:
+        comm.attach(algo)
     if dynamic:
         arr = stream.arrays
         prev_it = algo.iterations()

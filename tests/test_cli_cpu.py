@@ -60,8 +60,11 @@ def test_bench_ranks_is_usage_error(tmp_path):
     assert rc == EXIT_USAGE
 
 
-@pytest.mark.parametrize("cmd", [["emit", "x.sp"], ["sim", "x.sp", "g.txt", "--ranks", "2"]])
-def test_compiler_and_simulator_commands_are_out_of_scope(cmd):
+@pytest.mark.parametrize("cmd", [["emit", "x.sp"],  # the compiler is out of scope
+                                 ["sim", "x.sp", "g.txt", "--ranks", "2"],  # unreadable program
+                                 ["sim", "pr", "g.txt", "--ranks", "2", "--partitioner", "hash"],  # blocks only
+                                 ["sim", "pr", "g.txt", "--ranks", "0"]])
+def test_emit_and_bad_sim_invocations_are_usage_errors(cmd):
     assert main(cmd) == EXIT_USAGE
 
 

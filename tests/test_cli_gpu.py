@@ -152,3 +152,33 @@ def test_binary_inputs_give_the_text_results(tmp_path):
                  "--src", "3", "--out", str(out)]) == EXIT_OK
     for f in ("dist.csv", "parent.csv", "activeOnDelete.csv", "activeOnAdd.csv"):
         assert (out / f).read_bytes() == open(g(f"run_sssp_g40/{f}"), "rb").read()
+
+
+@pytest.mark.parametrize("ranks", [1, 2, 3])
+def test_sim_runs_partitioned_and_reports_per_rank_communication(tmp_path, ranks):
+    """`sim` (cli.py:520-568): the same results as `run`, from a REAL vertex-
+    partitioned store over `--ranks` in-process ranks, with commstats.csv
+    holding what each rank moved."""
+    cases = [
+        (["sssp", g("g40.txt"), "--updates", g("gen_g40.txt"), "--batch", "5", "--src", "3"], ["dist.csv", "parent.csv"]),
+        (["pr", g("rmat9.txt"), "--updates", g("gen_rmat9.txt"), "--batch", "40"], ["outdeg.csv", "affected.csv"]),
+        (["tc", g("g60u.txt"), "--undirected", "--updates", g("gen_g60u.txt"), "--batch", "20"], []),
+    ]
+    for j, (argv, exact) in enumerate(cases):
+        o_run, o_sim = tmp_path / f"r{j}", tmp_path / f"s{j}"
+        assert main(["run", *argv, "--out", str(o_run)]) == EXIT_OK
+        assert main(["sim", argv[0], argv[1], "--ranks", str(ranks), *argv[2:], "--out", str(o_sim)]) == EXIT_OK
+        for f in exact:
+            assert (o_sim / f).read_bytes() == (o_run / f).read_bytes(), f
+        if argv[0] == "pr":
+            a, b = values(o_run / "pagerank.csv"), values(o_sim / "pagerank.csv")
+            assert max(abs(float(a[k]) - float(b[k])) for k in a) <= 1e-15
+        assert scalars(o_sim / "scalars.csv")["return" if argv[0] == "tc" else "batchsize"] == \
+            scalars(o_run / "scalars.csv")["return" if argv[0] == "tc" else "batchsize"]
+        with open(o_sim / "commstats.csv", newline="") as fh:
+            rows = list(csv.DictReader(fh))
+        assert [int(r["rank"]) for r in rows] == list(range(ranks))
+        if ranks > 1:
+            assert all(int(r["bytes_moved"]) > 0 for r in rows)
+        m = json.loads((o_sim / "manifest.json").read_text())
+        assert m["ranks"] == ranks and m["partitioned_store"] == (argv[0] != "tc")
