@@ -1,10 +1,19 @@
 // gd_prims.cu -- device memory (a per-stream cache over the stream-ordered
-// pool), small read-backs and fills.  The sort / scan / select primitives are
-// in gd_sort.cu.
+// pool), small read-backs, fills, and the sort / scan / select primitives of
+// the store path: CUB by default, or the hand-written cooperative versions of
+// gd_sort.cu with -DGD_OWN_PRIMS=1.
 #include <cstring>
 #include <map>
 #include <mutex>
 #include <vector>
+
+#ifndef GD_OWN_PRIMS
+#define GD_OWN_PRIMS 0
+#endif
+#if !GD_OWN_PRIMS
+#include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
+#endif
 
 #include "gd_common.cuh"
 #include "gd_launch.cuh"
@@ -97,6 +106,111 @@ void read_small(cudaStream_t s, void* host, const void* dev, size_t bytes) {
     GD_CUDA(cudaStreamSynchronize(s));
     memcpy(host, pin, bytes);
 }
+
+#if !GD_OWN_PRIMS
+// The store path's sort / scan / select through CUB (the default: measured
+// faster than the hand-written cooperative versions in gd_sort.cu,
+// profiles/round2/README.md).
+namespace {
+struct Temp {
+    void* p = nullptr;
+    size_t bytes = 0;
+    cudaStream_t s;
+    Temp(size_t b, cudaStream_t st) : bytes(b), s(st) {
+        if (b) p = dev_alloc(b, st);
+    }
+    ~Temp() {
+        if (p) dev_free(p, bytes, s);
+    }
+};
+}  // namespace
+
+void sort_pairs_u64(cudaStream_t s, uint64_t* keys, int32_t* vals, int64_t n, int end_bit) {
+    if (n <= 1) return;
+    DBuf<uint64_t> k2(n, s);
+    DBuf<int32_t> v2(n, s);
+    cub::DoubleBuffer<uint64_t> kb(keys, k2.get());
+    cub::DoubleBuffer<int32_t> vb(vals, v2.get());
+    size_t bytes = 0;
+    GD_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, kb, vb, n, 0, end_bit, s));
+    Temp t(bytes, s);
+    GD_CUDA(cub::DeviceRadixSort::SortPairs(t.p, bytes, kb, vb, n, 0, end_bit, s));
+    count_library_launch();
+    if (kb.Current() != keys) GD_CUDA(cudaMemcpyAsync(keys, kb.Current(), n * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
+    if (vb.Current() != vals) GD_CUDA(cudaMemcpyAsync(vals, vb.Current(), n * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+}
+
+void sort_pairs_u32(cudaStream_t s, uint32_t* keys, int32_t* vals, int64_t n, int end_bit) {
+    if (n <= 1) return;
+    DBuf<uint32_t> k2(n, s);
+    DBuf<int32_t> v2(n, s);
+    cub::DoubleBuffer<uint32_t> kb(keys, k2.get());
+    cub::DoubleBuffer<int32_t> vb(vals, v2.get());
+    size_t bytes = 0;
+    GD_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, kb, vb, n, 0, end_bit, s));
+    Temp t(bytes, s);
+    GD_CUDA(cub::DeviceRadixSort::SortPairs(t.p, bytes, kb, vb, n, 0, end_bit, s));
+    count_library_launch();
+    if (kb.Current() != keys) GD_CUDA(cudaMemcpyAsync(keys, kb.Current(), n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+    if (vb.Current() != vals) GD_CUDA(cudaMemcpyAsync(vals, vb.Current(), n * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+}
+
+void sort_keys_u64(cudaStream_t s, uint64_t* keys, int64_t n, int end_bit) {
+    if (n <= 1) return;
+    DBuf<uint64_t> k2(n, s);
+    cub::DoubleBuffer<uint64_t> kb(keys, k2.get());
+    size_t bytes = 0;
+    GD_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, bytes, kb, n, 0, end_bit, s));
+    Temp t(bytes, s);
+    GD_CUDA(cub::DeviceRadixSort::SortKeys(t.p, bytes, kb, n, 0, end_bit, s));
+    count_library_launch();
+    if (kb.Current() != keys) GD_CUDA(cudaMemcpyAsync(keys, kb.Current(), n * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
+}
+
+void exclusive_scan_i64(cudaStream_t s, const int64_t* in, int64_t* out, int64_t n) {
+    if (n <= 0) return;
+    size_t bytes = 0;
+    GD_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, n, s));
+    Temp t(bytes, s);
+    GD_CUDA(cub::DeviceScan::ExclusiveSum(t.p, bytes, in, out, n, s));
+    count_library_launch();
+}
+
+void inclusive_scan_i64(cudaStream_t s, const int64_t* in, int64_t* out, int64_t n) {
+    if (n <= 0) return;
+    size_t bytes = 0;
+    GD_CUDA(cub::DeviceScan::InclusiveSum(nullptr, bytes, in, out, n, s));
+    Temp t(bytes, s);
+    GD_CUDA(cub::DeviceScan::InclusiveSum(t.p, bytes, in, out, n, s));
+    count_library_launch();
+}
+
+int64_t select_flagged_index(cudaStream_t s, const uint8_t* flags, int64_t n, int32_t* out) {
+    if (n <= 0) return 0;
+    DBuf<int64_t> cnt(1, s);
+    thrust::counting_iterator<int32_t> it(0);
+    size_t bytes = 0;
+    GD_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, it, flags, out, cnt.get(), n, s));
+    Temp t(bytes, s);
+    GD_CUDA(cub::DeviceSelect::Flagged(t.p, bytes, it, flags, out, cnt.get(), n, s));
+    count_library_launch();
+    return read_scalar(s, cnt.get());
+}
+
+void select_flagged_index_async(cudaStream_t s, const uint8_t* flags, int64_t n, int32_t* out, int64_t* d_count) {
+    if (n <= 0) {
+        GD_CUDA(cudaMemsetAsync(d_count, 0, sizeof(int64_t), s));
+        return;
+    }
+    thrust::counting_iterator<int32_t> it(0);
+    size_t bytes = 0;
+    GD_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, it, flags, out, d_count, n, s));
+    Temp t(bytes, s);
+    GD_CUDA(cub::DeviceSelect::Flagged(t.p, bytes, it, flags, out, d_count, n, s));
+    count_library_launch();
+}
+
+#endif  // !GD_OWN_PRIMS
 
 __global__ void k_iota_i32(int32_t* a, int64_t n) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)

@@ -21,6 +21,11 @@
 //      it: dynamic.py:116 keeps stream order within a source).
 // Passes stop at end_bit; keys and values ping-pong between the caller's
 // arrays and one scratch pair, with a final copy when the pass count is odd.
+//
+// Built with -DGD_OWN_PRIMS=1 only: on the C2 batch (B200, tools/timeline.py)
+// these take 406 us for the two 44-bit sorts (CUB onesweep: 171), 150 us for
+// six 4M-entry scans (CUB: 78) and 45 us for five selects (CUB: 32), so the
+// default build keeps CUB (gd_prims.cu); see profiles/round2/README.md.
 #include <cooperative_groups.h>
 
 #include <algorithm>
@@ -28,6 +33,11 @@
 #include "gd_common.cuh"
 #include "gd_launch.cuh"
 
+#ifndef GD_OWN_PRIMS
+#define GD_OWN_PRIMS 0
+#endif
+
+#if GD_OWN_PRIMS
 namespace gdb {
 
 namespace {
@@ -39,6 +49,7 @@ constexpr int kWarps = kSortThreads / 32;
 constexpr int kRadix = 256;
 constexpr int kItems = 8;  // keys per thread per round
 constexpr int kRound = kSortThreads * kItems;
+static_assert(kSortThreads == kRadix, "one digit per thread in the totals prefix");
 
 template <typename K>
 struct SortArgs {
@@ -111,12 +122,19 @@ __global__ void __launch_bounds__(kSortThreads) k_radix_sort(SortArgs<K> a) {
             if (tid == 0) totals[d] = carry;
         }
         grid.sync();
-        if (tid == 0) {  // 256 totals: one thread prefixes them (cheap next to the pass)
-            unsigned long long acc = 0;
-            for (int d = 0; d < kRadix; ++d) {
-                prefix[d] = acc;
-                acc += totals[d];
+        {  // exclusive prefix of the 256 digit totals, one per thread (kSortThreads == kRadix)
+            const unsigned long long v = totals[tid];
+            unsigned long long x = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += y;
             }
+            if (lane == 31) hist[wid] = x;  // hist is free until the next pass
+            __syncthreads();
+            unsigned long long wpre = 0;
+            for (int w = 0; w < wid; ++w) wpre += hist[w];
+            prefix[tid] = wpre + x - v;
         }
         __syncthreads();
         for (int d = tid; d < kRadix; d += kSortThreads) base[d] = prefix[d] + a.table[(int64_t)d * G + c];
@@ -230,6 +248,7 @@ void radix_sort(cudaStream_t s, K* keys, int32_t* vals, int64_t n, int end_bit) 
 // Exclusive int64 scan: CTA sums of contiguous chunks, a barrier, every CTA
 // prefixes the (<= a few hundred) CTA sums itself, then scans its chunk.
 constexpr int kScanThreads = 512;
+constexpr int kSI = 8;  // items per thread per round (scan, select)
 
 __device__ __forceinline__ int64_t block_excl_scan(int64_t v, int64_t* wsum, int64_t& total) {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -276,13 +295,25 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_excl(const int64_t* in, i
     }
     (void)G;
     __syncthreads();
+    // rounds of kScanThreads x kSI consecutive items: each thread scans its
+    // kSI items serially, the block scans the thread totals
     int64_t carry = base;
-    for (int64_t i0 = lo; i0 < hi; i0 += kScanThreads) {
-        const int64_t i = i0 + threadIdx.x;
-        const int64_t v = i < hi ? in[i] : 0;
+    for (int64_t i0 = lo; i0 < hi; i0 += (int64_t)kScanThreads * kSI) {
+        const int64_t t0 = i0 + (int64_t)threadIdx.x * kSI;
+        int64_t v[kSI];
+        int64_t sum = 0;
+#pragma unroll
+        for (int j = 0; j < kSI; ++j) {
+            v[j] = t0 + j < hi ? in[t0 + j] : 0;
+            sum += v[j];
+        }
         int64_t tot;
-        const int64_t e = block_excl_scan(v, wsum, tot);
-        if (i < hi) out[i] = carry + e;
+        int64_t e = carry + block_excl_scan(sum, wsum, tot);
+#pragma unroll
+        for (int j = 0; j < kSI; ++j) {
+            if (t0 + j < hi) out[t0 + j] = e;
+            e += v[j];
+        }
         carry += tot;
     }
 }
@@ -317,12 +348,20 @@ __global__ void __launch_bounds__(kScanThreads) k_select(const uint8_t* flags, i
     }
     __syncthreads();
     int64_t carry = base;
-    for (int64_t i0 = lo; i0 < hi; i0 += kScanThreads) {
-        const int64_t i = i0 + threadIdx.x;
-        const int64_t v = (i < hi && flags[i]) ? 1 : 0;
+    for (int64_t i0 = lo; i0 < hi; i0 += (int64_t)kScanThreads * kSI) {
+        const int64_t t0 = i0 + (int64_t)threadIdx.x * kSI;
+        uint8_t f[kSI];
+        int64_t sum = 0;
+#pragma unroll
+        for (int j = 0; j < kSI; ++j) {
+            f[j] = t0 + j < hi ? flags[t0 + j] : 0;
+            sum += f[j] != 0;
+        }
         int64_t tot;
-        const int64_t e = block_excl_scan(v, wsum, tot);
-        if (v) out[carry + e] = (int32_t)i;
+        int64_t e = carry + block_excl_scan(sum, wsum, tot);
+#pragma unroll
+        for (int j = 0; j < kSI; ++j)
+            if (f[j]) out[e++] = (int32_t)(t0 + j);
         carry += tot;
     }
 }
@@ -382,3 +421,4 @@ int64_t select_flagged_index(cudaStream_t s, const uint8_t* flags, int64_t n, in
 }
 
 }  // namespace gdb
+#endif  // GD_OWN_PRIMS
