@@ -18,7 +18,8 @@
  *   - a handle is single-entrant (mirrors DynamicGraph._mutate_lock,
  *     graph/dynamic.py:85);
  *   - node ids are int64 at the ABI (int32 on the device: node_count must be
- *     < 2^31 - 1); weights must lie in [0, 2^31).
+ *     < 2^31 - 1); weights must lie in [0, 2^31); a store holds at most 2^31
+ *     arcs (slot ids are int64, build-time positions int32).
  * There is no CPU fallback: without a usable CUDA device every call that
  * needs one fails with GD_ERR_CUDA.
  */

@@ -232,7 +232,9 @@ static int graph_create(int64_t n, const int64_t* src, const int64_t* dst, const
         bool as_arcs = (directed & GD_ARCS) != 0;
         directed &= 1;
         int64_t arcs = (directed || as_arcs) ? m : 2 * m;
-        if (arcs >= INT32_MAX) throw gdb::GdError(GD_ERR_CONTRACT, "more than 2^31-1 arcs per store");
+        // arcs are indexed by int32 positions while a store is built and its
+        // index rebuilt (slot ids are int64): at most 2^31
+        if (arcs > (int64_t)INT32_MAX + 1) throw gdb::GdError(GD_ERR_CONTRACT, "more than 2^31 arcs per store");
         for (int64_t i = 0; i < m; ++i) {  // dynamic.py:106-112
             if (src[i] < 0 || src[i] >= n || dst[i] < 0 || dst[i] >= n)
                 throw gdb::GdError(GD_ERR_MALFORMED, "edge " + std::to_string(i) + ": node id out of range (src=" +

@@ -189,9 +189,9 @@ __global__ void k_row_chunks(OutView ov, const uint64_t* rq_key, const int32_t* 
     }
 }
 
-__global__ void k_widen(const int32_t* a, int64_t m, uint64_t* o) {
+__global__ void k_widen64(const int64_t* a, int64_t m, uint64_t* o) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
-        o[i] = (uint64_t)(uint32_t)a[i];
+        o[i] = (uint64_t)a[i];
 }
 
 // A hit on a pair with ONE delete request takes the pair's first live
@@ -204,7 +204,7 @@ struct MatchOut {
     const uint8_t* single;    // per request: its key has exactly one request
     uint64_t* okey;           // overflow matches: pair key, chain offset, gid
     int64_t* ochain;
-    int32_t* ogid;
+    int64_t* ogid;  // global slot ids: a store may hold more than 2^31 slots
     unsigned long long* ocnt;
     int64_t cap;
 };
@@ -224,7 +224,7 @@ __device__ inline void emit_matches(const MatchOut& mo, int64_t p, int32_t row, 
         if (slot < mo.cap) {
             mo.okey[slot] = pair_key(row, c, sh);
             mo.ochain[slot] = chain;
-            mo.ogid[slot] = (int32_t)gid;
+            mo.ogid[slot] = gid;
         }
     }
 }
@@ -410,7 +410,7 @@ __global__ void k_overflow_keys(uint64_t* key, const int64_t* chain, int64_t nm,
 // others against the (pair, chain)-sorted overflow matches.
 __global__ void k_del_resolve(const uint64_t* rq_key, const int32_t* rq_occ, const int32_t* rq_rec,
                               const uint8_t* rq_which, const uint8_t* single, const unsigned long long* sel,
-                              int64_t nrq, const uint64_t* m_key, const int32_t* m_gid, int64_t nm, int rb,
+                              int64_t nrq, const uint64_t* m_key, const int64_t* m_gid, int64_t nm, int rb,
                               int64_t* rq_pos, uint8_t* found_fwd, unsigned long long* applied) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nrq; i += (int64_t)gridDim.x * blockDim.x) {
         int64_t pos = -1;
@@ -1579,7 +1579,7 @@ int64_t Store::apply_deletes_local(const int32_t* d_src, const int32_t* d_dst, i
     int64_t cap = 1024;
     DBuf<uint64_t> m_key;
     DBuf<int64_t> m_chain;
-    DBuf<int32_t> m_gid;
+    DBuf<int64_t> m_gid;
     int64_t nm = 0, maxchain = 0;
     for (int attempt = 0; attempt < 2; ++attempt) {
         m_key.alloc(cap, s);
@@ -1617,20 +1617,29 @@ int64_t Store::apply_deletes_local(const int32_t* d_src, const int32_t* d_dst, i
     int rb = bits_for((uint64_t)std::max<int64_t>(maxchain, 1));
     const bool one_sort = kb + rb <= 64;  // (pair, chain offset) fits one 64-bit key
     if (!one_sort) rb = 0;
+    // the overflow matches sort through a permutation (int32: matches are
+    // per batch), their int64 slot ids follow it
     if (nm >= 1 && one_sort) {
         GD_KERNEL(k_overflow_keys, grid_for(nm, 256), 256, 0, s, m_key.get(), m_chain.get(), nm, rb);
-        if (nm > 1) sort_pairs_u64(s, m_key.get(), m_gid.get(), nm, kb + rb);
+        if (nm > 1) {
+            DBuf<int32_t> perm(nm, s);
+            iota_i32(s, perm.get(), nm);
+            sort_pairs_u64(s, m_key.get(), perm.get(), nm, kb + rb);
+            DBuf<int64_t> g2(nm, s);
+            GD_KERNEL(k_gather<int64_t>, grid_for(nm, 256), 256, 0, s, m_gid.get(), perm.get(), nm, g2.get());
+            m_gid = std::move(g2);
+        }
     } else if (nm > 1) {  // LSD: by gid (= chain order), then stable by pair key
         DBuf<uint64_t> gk(nm, s);
         DBuf<int32_t> perm(nm, s);
-        GD_KERNEL(k_widen, grid_for(nm, 256), 256, 0, s, m_gid.get(), nm, gk.get());
+        GD_KERNEL(k_widen64, grid_for(nm, 256), 256, 0, s, m_gid.get(), nm, gk.get());
         iota_i32(s, perm.get(), nm);
-        sort_pairs_u64(s, gk.get(), perm.get(), nm, 32);
+        sort_pairs_u64(s, gk.get(), perm.get(), nm, 64);
         DBuf<uint64_t> k2(nm, s);
         GD_KERNEL(k_gather<uint64_t>, grid_for(nm, 256), 256, 0, s, m_key.get(), perm.get(), nm, k2.get());
         sort_pairs_u64(s, k2.get(), perm.get(), nm, kb);
-        DBuf<int32_t> g2(nm, s);
-        GD_KERNEL(k_gather<int32_t>, grid_for(nm, 256), 256, 0, s, m_gid.get(), perm.get(), nm, g2.get());
+        DBuf<int64_t> g2(nm, s);
+        GD_KERNEL(k_gather<int64_t>, grid_for(nm, 256), 256, 0, s, m_gid.get(), perm.get(), nm, g2.get());
         m_key = std::move(k2);
         m_gid = std::move(g2);
     }
