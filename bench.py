@@ -473,43 +473,36 @@ def run_ours(gd, torch, wl, args, steps, warmup, e2e_steps, world, rank, local, 
         pin[nm] = t_
     out_pin = torch.empty((2, n) if wl["algo"] == "sssp" else n,
                           dtype=torch.float64 if wl["algo"] == "pr" else torch.int64).pin_memory()
-    # one untimed step through the host-buffer path first (creates the copy
-    # stream and the snapshot buffers of the asynchronous read-back)
+    # one untimed batch through the same call first (creates the copy stream,
+    # its events and the upload slots)
     wi = warmup + steps
     wa, wb = wi * per, min((wi + 1) * per, len(kind))
     if wb > wa:
-        _host_batch(gd, algo, pin, wa, wb - wa, wi)
-        _read_result(gd, algo, wl, out_pin, n)
-        gd._native.check(gd._native.lib().gd_wait(algo.h))
+        _host_stream(algo, wl, pin, wa, wb - wa, per, wi, out_pin)
+    # ---- e2e timed region: ONE run_batches call over the e2e steps' records
+    # from pinned host memory (gd_*_run_stream): every batch's records go up
+    # and every batch's result comes back to host memory inside the region
     e_start = warmup + steps + 1
-    h2d = d2h = 0
+    a0, b0 = e_start * per, min((e_start + e2e_steps) * per, len(kind))
+    e_done = max(b0 - a0, 0)
+    nsteps_e = (e_done + per - 1) // per
+    h2d = e_done * (1 + 8 + 8 + (8 if (wl["weighted"] or wl["algo"] == "sssp") else 0))  # w not uploaded when unused
+    d2h = nsteps_e * {"pr": 8 * n, "sssp": 16 * n, "tc": 8}[wl["algo"]]
     if dist_on:
         torch.distributed.barrier()
     torch.cuda.synchronize()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    e_done = 0
-    e2e_log = []
-    for i in range(e_start, e_start + e2e_steps):
-        a, b = i * per, min((i + 1) * per, len(kind))
-        k = b - a
-        if k <= 0:
-            break
-        h2d += k * (1 + 8 + 8 + (8 if (wl["weighted"] or wl["algo"] == "sssp") else 0))  # w not uploaded when unused
-        tb0 = time.perf_counter()
-        _host_batch(gd, algo, pin, a, k, i)
-        tb1 = time.perf_counter()
-        d2h += _read_result(gd, algo, wl, out_pin, n)
-        e2e_log.append((i, tb1 - tb0, time.perf_counter() - tb1))
-        e_done += k
-    N_ = gd._native
-    N_.check(N_.lib().gd_wait(algo.h))  # the last read-back has landed
+    tb0 = time.perf_counter()
+    if e_done:
+        _host_stream(algo, wl, pin, a0, e_done, per, e_start, out_pin)
+    tcall = time.perf_counter() - tb0
     e1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1)
-    for i, tb, tr in e2e_log:  # logged after the timed region
-        log(f"[bench] e2e step {i}: batch call {1e3 * tb:.2f} ms, read call {1e3 * tr:.2f} ms")
+    log(f"[bench] e2e: run_stream over {nsteps_e} batches: {1e3 * tcall:.2f} ms host call, "
+        f"{e2e_ms:.2f} ms device events")
     if dist_on:
         tt = torch.tensor([e2e_ms], device=f"cuda:{local}")
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
@@ -536,9 +529,9 @@ def run_ours(gd, torch, wl, args, steps, warmup, e2e_steps, world, rank, local, 
                 "share_of_step": ms / elapsed_ms if elapsed_ms else None}
     out = {"value": value, "ms_per_step": elapsed_ms / steps, "steps": steps, "warmup": warmup,
            "scaling": "strong" if shards else "weak",
-           "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d // max(e2e_steps, 1),
-                   "d2h_bytes_per_step": d2h // max(e2e_steps, 1), "steps": e2e_steps,
-                   "ms_per_step": e2e_ms / max(e2e_steps, 1)},
+           "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d // max(nsteps_e, 1),
+                   "d2h_bytes_per_step": d2h // max(nsteps_e, 1), "steps": nsteps_e,
+                   "ms_per_step": e2e_ms / max(nsteps_e, 1), "api": f"gd_{wl['algo']}_run_stream"},
            "gpu_launches": int(launches), "roofline": roof,
            "kernels": {k_: {"ms_total": v[0], "launches": v[1], "share": v[0] / elapsed_ms,
                             "gbs": (v[2] / 1e9) / (v[0] / 1e3) if v[2] and v[0] else None}
@@ -600,33 +593,19 @@ def _graph_stream(g):
     return p.value
 
 
-def _host_batch(gd, algo, pin, a, k, i):
-    import ctypes as C
-
-    from paper_2507_11094_b200 import _native as N
-
-    fn = getattr(N.lib(), f"gd_{algo.kind}_batch")
-    N.check(fn(algo.h, C.c_void_p(pin["kind"].data_ptr() + a), C.c_void_p(pin["src"].data_ptr() + 8 * a),
-               C.c_void_p(pin["dst"].data_ptr() + 8 * a), C.c_void_p(pin["w"].data_ptr() + 8 * a), k, i))
-
-
-def _read_result(gd, algo, wl, out_pin, n):
-    import ctypes as C
-
-    from paper_2507_11094_b200 import _native as N
-
-    # asynchronous read-back (snapshot + side-stream copy overlapping the next
-    # batch); the loop waits for the last one before the timed region closes
+def _host_stream(algo, wl, pin, a, k, per, first, out_pin):
+    """run_batches over host records [a, a+k) in batches of `per` through the
+    public C-ABI call (gd_*_run_stream), every batch's result read back to
+    pinned host memory (PR ranks, SSSP dist + parent, TC counts)."""
     if wl["algo"] == "pr":
-        N.check(N.lib().gd_pr_read_async(algo.h, C.c_void_p(out_pin.data_ptr())))
-        return 8 * n
-    if wl["algo"] == "sssp":
-        N.check(N.lib().gd_sssp_read_async(algo.h, C.c_void_p(out_pin[0].data_ptr()),
-                                           C.c_void_p(out_pin[1].data_ptr())))
-        return 16 * n
-    c = C.c_int64()
-    N.check(N.lib().gd_tc_read(algo.h, C.byref(c)))
-    return 8
+        outs = (out_pin.data_ptr(),)
+    elif wl["algo"] == "sssp":
+        outs = (out_pin[0].data_ptr(), out_pin[1].data_ptr())
+    else:
+        counts = np.zeros((k + per - 1) // per, dtype=np.int64)
+        outs = (counts.ctypes.data,)
+    algo.run_stream_ptrs(pin["kind"].data_ptr() + a, pin["src"].data_ptr() + 8 * a, pin["dst"].data_ptr() + 8 * a,
+                         pin["w"].data_ptr() + 8 * a, k, per, first, *outs)
 
 
 def _ncu_traffic(wl, name):

@@ -157,6 +157,17 @@ GD_API int gd_sssp_read(gd_sssp* s, int64_t* dist, int64_t* parent);
  * the next batch; the buffers are valid after gd_wait(s).  No reference
  * counterpart: ctx.properties are read after the run (interp.py:112-160). */
 GD_API int gd_sssp_read_async(gd_sssp* s, int64_t* dist, int64_t* parent);
+/* run_batches over a whole host update stream (engine/run.py:44-68): the
+ * records [0, k) in batches of batch_size (batch j = records [j*bs, ...),
+ * batch_index first_batch_index + j), pipelined -- batch j+1's records go
+ * up and batch j-1's result comes back on a copy stream while batch j runs
+ * (host arrays: pinned for the overlap; they must stay valid until return).
+ * After every batch its dist/parent are copied to dist/parent (nullable),
+ * which hold the last batch's result on return.  Errors as gd_sssp_batch;
+ * the batches before the failing one stay applied. */
+GD_API int gd_sssp_run_stream(gd_sssp* s, const uint8_t* kind, const int64_t* src, const int64_t* dst,
+                              const int64_t* w, int64_t k, int64_t batch_size, int64_t first_batch_index,
+                              int64_t* dist, int64_t* parent);
 GD_API int gd_sssp_destroy(gd_sssp* s);
 
 /* ---- dynamic PageRank: programs/pr_dynamic.sp:7-102 --------------------- */
@@ -173,6 +184,9 @@ GD_API int gd_pr_read_async(gd_pr* p, double* rank); /* as gd_sssp_read_async */
 GD_API int gd_pr_read_affected(gd_pr* p, uint8_t* affected);
 /* device pointer to the float64 rank vector (valid until the next call) */
 GD_API int gd_pr_rank_device(gd_pr* p, const double** rank);
+/* as gd_sssp_run_stream; rank (nullable) receives every batch's ranks */
+GD_API int gd_pr_run_stream(gd_pr* p, const uint8_t* kind, const int64_t* src, const int64_t* dst, const int64_t* w,
+                            int64_t k, int64_t batch_size, int64_t first_batch_index, double* rank);
 GD_API int gd_pr_destroy(gd_pr* p);
 
 /* ---- dynamic triangle counting: programs/tc_dynamic.sp:7-115 ------------ */
@@ -182,6 +196,10 @@ GD_API int gd_tc_batch(gd_tc* t, const uint8_t* kind, const int64_t* src, const 
 GD_API int gd_tc_batch_device(gd_tc* t, const uint8_t* kind, const int32_t* src, const int32_t* dst, const int32_t* w,
                        int64_t k, int64_t batch_index);
 GD_API int gd_tc_read(gd_tc* t, int64_t* count);
+/* as gd_sssp_run_stream; counts (nullable) gets the count after each batch,
+ * one int64 per batch */
+GD_API int gd_tc_run_stream(gd_tc* t, const uint8_t* kind, const int64_t* src, const int64_t* dst, const int64_t* w,
+                            int64_t k, int64_t batch_size, int64_t first_batch_index, int64_t* counts);
 GD_API int gd_tc_destroy(gd_tc* t);
 
 /* ---- multi-GPU (one process per GPU).  NCCL is loaded on

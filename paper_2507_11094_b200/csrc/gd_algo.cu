@@ -107,7 +107,7 @@ void AlgoBase::copy_out_async(void* host, const void* dev, size_t bytes, int slo
     // the snapshot buffer may still feed the previous read of this slot
     GD_CUDA(cudaStreamWaitEvent(st, ev_copied[slot], 0));
     snap[slot].ensure(bytes, st);
-    GD_CUDA(cudaMemcpyAsync(snap[slot].get(), dev, bytes, cudaMemcpyDeviceToDevice, st));
+    copy_d2d(st, snap[slot].get(), dev, bytes);
     GD_CUDA(cudaEventRecord(ev_ready[slot], st));
     GD_CUDA(cudaStreamWaitEvent(copy_stream, ev_ready[slot], 0));
     GD_CUDA(cudaMemcpyAsync(host, snap[slot].get(), bytes, cudaMemcpyDeviceToHost, copy_stream));
@@ -119,6 +119,12 @@ void AlgoBase::wait_copies() {
 }
 
 AlgoBase::~AlgoBase() {
+    for (int k = 0; k < 2; ++k) {
+        if (ev_up[k]) cudaEventDestroy(ev_up[k]);
+        if (ev_staged[k]) cudaEventDestroy(ev_staged[k]);
+        if (ev_sready[k]) cudaEventDestroy(ev_sready[k]);
+        if (ev_scopied[k]) cudaEventDestroy(ev_scopied[k]);
+    }
     if (copy_stream) {
         cudaStreamSynchronize(copy_stream);
         for (int k = 0; k < 2; ++k) {
@@ -145,13 +151,19 @@ void AlgoBase::stage_host(DevBatch& b, const uint8_t* kind, const int64_t* src, 
     GD_CUDA(cudaMemcpyAsync(h_stage.get() + k, dst, k * 8, cudaMemcpyHostToDevice, st));
     if (w) GD_CUDA(cudaMemcpyAsync(h_stage.get() + 2 * k, w, k * 8, cudaMemcpyHostToDevice, st));
     GD_CUDA(cudaMemcpyAsync(k_stage.get(), kind, k, cudaMemcpyHostToDevice, st));
+    stage_records(b, k_stage.get(), h_stage.get(), w ? h_stage.get() + 2 * k : nullptr, k, kind, src, dst);
+}
+
+// validate + split records already on the device as int64 (src | dst at d64, d64 + k)
+void AlgoBase::stage_records(DevBatch& b, const uint8_t* dkind, const int64_t* d64, const int64_t* w64, int64_t k,
+                             const uint8_t* kind, const int64_t* src, const int64_t* dst) {
+    cudaStream_t st = stream();
     DBuf<int32_t> s(k, st), d(k, st), ww(k, st);
     DBuf<uint8_t> flags(2 * k, st);
     DBuf<int64_t> hdr(4, st);  // err, bad index, kdel, kadd
-    GD_CUDA(cudaMemsetAsync(hdr.get(), 0, 16, st));
-    GD_KERNEL(k_stage_host, grid_for(k, 256), 256, 0, st, k_stage.get(), h_stage.get(), h_stage.get() + k,
-              w ? h_stage.get() + 2 * k : nullptr, k, g->n, s.get(), d.get(), ww.get(), flags.get(),
-              flags.get() + k, reinterpret_cast<int*>(hdr.get()),
+    fill_d(st, hdr.get(), 0, 16);
+    GD_KERNEL(k_stage_host, grid_for(k, 256), 256, 0, st, dkind, d64, d64 + k, w64, k, g->n, s.get(), d.get(),
+              ww.get(), flags.get(), flags.get() + k, reinterpret_cast<int*>(hdr.get()),
               reinterpret_cast<unsigned long long*>(hdr.get() + 1));
     DBuf<int32_t> sel_del(k, st), sel_add(k, st);
     select_flagged_index_async(st, flags.get(), k, sel_del.get(), hdr.get() + 2);
@@ -166,6 +178,91 @@ void AlgoBase::stage_host(DevBatch& b, const uint8_t* kind, const int64_t* src, 
     split(b, sel_del.get(), sel_add.get(), s.get(), d.get(), ww.get(), h[2], h[3]);
 }
 
+cudaStream_t AlgoBase::io_stream() {
+    if (!copy_stream) copy_out_async(nullptr, nullptr, 0, 0);  // creates the stream and its events
+    return copy_stream;
+}
+
+void AlgoBase::reserve_uploads(int64_t k) {
+    cudaStream_t st = stream();
+    io_stream();
+    for (int j = 0; j < 2; ++j) {
+        up64[j].ensure(3 * std::max<int64_t>(k, 1), st);
+        upk[j].ensure(std::max<int64_t>(k, 1), st);
+        if (!ev_up[j]) {
+            GD_CUDA(cudaEventCreateWithFlags(&ev_up[j], cudaEventDisableTiming));
+            GD_CUDA(cudaEventCreateWithFlags(&ev_staged[j], cudaEventDisableTiming));
+            GD_CUDA(cudaEventRecord(ev_staged[j], st));
+        }
+    }
+    GD_CUDA(cudaStreamSynchronize(st));  // the slots exist before the copy stream writes them
+}
+
+void AlgoBase::upload_async(int slot, const uint8_t* kind, const int64_t* src, const int64_t* dst, const int64_t* w,
+                            int64_t k) {
+    cudaStream_t io = io_stream();
+    if (!g->weighted && this->kind != ALGO_SSSP) w = nullptr;
+    up_w[slot] = w != nullptr;
+    if (k == 0) return;
+    // the slot's previous batch has been staged (its buffers are free)
+    GD_CUDA(cudaStreamWaitEvent(io, ev_staged[slot], 0));
+    int64_t* u = up64[slot].get();
+    GD_CUDA(cudaMemcpyAsync(u, src, k * 8, cudaMemcpyHostToDevice, io));
+    GD_CUDA(cudaMemcpyAsync(u + k, dst, k * 8, cudaMemcpyHostToDevice, io));
+    if (w) GD_CUDA(cudaMemcpyAsync(u + 2 * k, w, k * 8, cudaMemcpyHostToDevice, io));
+    GD_CUDA(cudaMemcpyAsync(upk[slot].get(), kind, k, cudaMemcpyHostToDevice, io));
+    GD_CUDA(cudaEventRecord(ev_up[slot], io));
+}
+
+void AlgoBase::stream_result(int par, int narr, const void* const* dev, void* const* host, const size_t* bytes) {
+    cudaStream_t st = stream();
+    cudaStream_t io = io_stream();
+    if (has_pend) stream_flush();  // the previous batch queued no structural update
+    if (!ev_sready[0])
+        for (int k = 0; k < 2; ++k) {
+            GD_CUDA(cudaEventCreateWithFlags(&ev_sready[k], cudaEventDisableTiming));
+            GD_CUDA(cudaEventCreateWithFlags(&ev_scopied[k], cudaEventDisableTiming));
+            GD_CUDA(cudaEventRecord(ev_scopied[k], io));
+        }
+    // the slot's previous read-back has left it
+    GD_CUDA(cudaStreamWaitEvent(st, ev_scopied[par], 0));
+    pend.par = par;
+    pend.narr = narr;
+    for (int i = 0; i < narr; ++i) {
+        ssnap[par][i].ensure(std::max<size_t>(bytes[i], 1), st);
+        copy_d2d(st, ssnap[par][i].get(), dev[i], bytes[i]);
+        pend.host[i] = host[i];
+        pend.bytes[i] = bytes[i];
+    }
+    GD_CUDA(cudaEventRecord(ev_sready[par], st));
+    has_pend = true;
+}
+
+void AlgoBase::stream_flush() {
+    if (!has_pend) return;
+    has_pend = false;
+    cudaStream_t io = io_stream();
+    const int par = pend.par;
+    GD_CUDA(cudaStreamWaitEvent(io, ev_sready[par], 0));
+    for (int i = 0; i < pend.narr; ++i)
+        if (pend.bytes[i])
+            GD_CUDA(cudaMemcpyAsync(pend.host[i], ssnap[par][i].get(), pend.bytes[i], cudaMemcpyDeviceToHost, io));
+    GD_CUDA(cudaEventRecord(ev_scopied[par], io));
+}
+
+void AlgoBase::stage_uploaded(DevBatch& b, int slot, const uint8_t* h_kind, const int64_t* h_src,
+                              const int64_t* h_dst, int64_t k) {
+    cudaStream_t st = stream();
+    if (k == 0) {
+        b.kdel = b.kadd = 0;
+        return;
+    }
+    GD_CUDA(cudaStreamWaitEvent(st, ev_up[slot], 0));
+    int64_t* u = up64[slot].get();
+    stage_records(b, upk[slot].get(), u, up_w[slot] ? u + 2 * k : nullptr, k, h_kind, h_src, h_dst);
+    GD_CUDA(cudaEventRecord(ev_staged[slot], st));
+}
+
 void AlgoBase::stage_device(DevBatch& b, const uint8_t* kind, const int32_t* src, const int32_t* dst,
                             const int32_t* w, int64_t k) {
     cudaStream_t st = stream();
@@ -175,7 +272,7 @@ void AlgoBase::stage_device(DevBatch& b, const uint8_t* kind, const int32_t* src
     }
     DBuf<uint8_t> flags(2 * k, st);
     DBuf<int64_t> hdr(4, st);  // err, bad index, kdel, kadd
-    GD_CUDA(cudaMemsetAsync(hdr.get(), 0, 16, st));
+    fill_d(st, hdr.get(), 0, 16);
     GD_KERNEL(k_stage_dev, grid_for(k, 256), 256, 0, st, kind, src, dst, k, g->n, flags.get(), flags.get() + k,
               reinterpret_cast<int*>(hdr.get()), reinterpret_cast<unsigned long long*>(hdr.get() + 1));
     DBuf<int32_t> sel_del(k, st), sel_add(k, st);
@@ -431,9 +528,9 @@ int64_t flood_weak_components_dist(Store& g, uint8_t* flags, KernelProf* prof) {
     auto agree = [&] {
         while (true) {
             ++rounds;
-            GD_CUDA(cudaMemcpyAsync(L.get(), p.get(), n * 4, cudaMemcpyDeviceToDevice, s));
+            copy_d2d(s, L.get(), p.get(), n * 4);
             g.part->allreduce_min_i32(L.get(), n, s);
-            GD_CUDA(cudaMemsetAsync(ch.get(), 0, 4, s));
+            fill_d(s, ch.get(), 0, 4);
             GD_KERNEL(k_uf_adopt, grid_for(n, 256), 256, 0, s, p.get(), L.get(), n, ch.get());
             GD_KERNEL(k_uf_compress, grid_for(n, 256), 256, 0, s, p.get(), n);
             GD_KERNEL(k_i32_to_u8, 1, 1, 0, s, ch.get(), a.get());

@@ -48,11 +48,53 @@ struct AlgoBase {
     void wait_copies();
     virtual ~AlgoBase();
 
+    // ---- pipelined host stream (gd_*_run_stream: run_batches over an
+    // UpdateStream, engine/run.py:44-68).  Batch j's records are uploaded
+    // into slot j % 2 on the copy stream while batch j-1 runs; the copy
+    // stream also carries the result read-backs, so each direction's copy
+    // runs alone: D2H(j-1) then H2D(j+1), both behind batch j's compute.
+    void reserve_uploads(int64_t k);  // both slots sized for k records
+    void upload_async(int slot, const uint8_t* kind, const int64_t* src, const int64_t* dst, const int64_t* w,
+                      int64_t k);
+    // stage_host's second half on an uploaded slot: the handle's stream
+    // waits for the upload, then validates and splits (host arrays only feed
+    // the error message)
+    void stage_uploaded(DevBatch& b, int slot, const uint8_t* h_kind, const int64_t* h_src, const int64_t* h_dst,
+                        int64_t k);
+    cudaStream_t io_stream();
+
+    // Result read-backs of a run_stream, placed where they cannot stall the
+    // batch: stream_result snapshots the batch's result arrays on the
+    // handle's stream at once; their D2H is queued on the copy stream only
+    // when the NEXT batch has queued its structural update (struct_done),
+    // because a copy engine serves its queue in order and the structural
+    // update's radix sorts issue copy-engine memsets (CUB) that would wait
+    // behind a tens-of-MB read-back.  stream_flush queues a pending one now.
+    void stream_result(int par, int narr, const void* const* dev, void* const* host, const size_t* bytes);
+    void stream_flush();
+    void struct_done() {
+        if (has_pend) stream_flush();
+    }
+
   private:
     void split(DevBatch& b, const int32_t* sel_del, const int32_t* sel_add, const int32_t* s, const int32_t* d,
                const int32_t* w, int64_t kdel, int64_t kadd);
     DBuf<int64_t> h_stage;  // reusable device staging for host uploads
     DBuf<uint8_t> k_stage;
+    void stage_records(DevBatch& b, const uint8_t* dkind, const int64_t* d64, const int64_t* w64, int64_t k,
+                       const uint8_t* h_kind, const int64_t* h_src, const int64_t* h_dst);
+    DBuf<int64_t> up64[2];  // run_stream upload slots: src | dst | w
+    DBuf<uint8_t> upk[2];
+    bool up_w[2] = {false, false};
+    cudaEvent_t ev_up[2] = {nullptr, nullptr}, ev_staged[2] = {nullptr, nullptr};
+    DBuf<uint8_t> ssnap[2][2];  // [batch parity][result array]
+    cudaEvent_t ev_sready[2] = {nullptr, nullptr}, ev_scopied[2] = {nullptr, nullptr};
+    struct Pending {
+        int par = 0, narr = 0;
+        void* host[2] = {nullptr, nullptr};
+        size_t bytes[2] = {0, 0};
+    } pend;
+    bool has_pend = false;
     cudaStream_t copy_stream = nullptr;
     cudaEvent_t ev_ready[2] = {nullptr, nullptr}, ev_copied[2] = {nullptr, nullptr};
     DBuf<uint8_t> snap[2];

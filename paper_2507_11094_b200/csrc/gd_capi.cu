@@ -215,6 +215,48 @@ static int algo_batch_dev(H* h, const uint8_t* kind, const int32_t* src, const i
     });
 }
 
+// run_batches over a host stream, pipelined (gd_capi.h: gd_*_run_stream).
+// The copy stream carries, in order, up(0), up(1), then per batch j:
+// D2H(j) after batch j, then up(j+2) -- so each copy runs alone on the link,
+// and both hide behind the next batch's compute.
+template <typename H, typename R>
+static int algo_run_stream(H* h, const uint8_t* kind, const int64_t* src, const int64_t* dst, const int64_t* w,
+                           int64_t k, int64_t bs, int64_t first, R&& result) {
+    if (!h) return null_handle();
+    return guard([&] {
+        if (k < 0 || bs <= 0) throw gdb::GdError(GD_ERR_CONTRACT, "run_stream needs k >= 0 and batch_size > 0");
+        if (k && (!kind || !src || !dst)) throw gdb::GdError(GD_ERR_CONTRACT, "null record array");
+        GD_CUDA(cudaSetDevice(h->a->g->device));
+        auto* a = h->a;
+        const int64_t nb = (k + bs - 1) / bs;
+        if (nb == 0) return;
+        a->reserve_uploads(std::min(bs, k));
+        auto up = [&](int64_t j) {
+            const int64_t o = j * bs, m = std::min(bs, k - o);
+            a->upload_async((int)(j & 1), kind + o, src + o, dst + o, w ? w + o : nullptr, m);
+        };
+        try {
+            up(0);
+            for (int64_t j = 0; j < nb; ++j) {
+                if (j + 1 < nb) up(j + 1);
+                const int64_t o = j * bs, m = std::min(bs, k - o);
+                gdb::DevBatch b;
+                a->stage_uploaded(b, (int)(j & 1), kind + o, src + o, dst + o, m);
+                a->batch(b, first + j);
+                result(j);
+            }
+        } catch (...) {  // no copy may touch the caller's buffers after return
+            a->stream_flush();
+            cudaStreamSynchronize(a->stream());
+            cudaStreamSynchronize(a->io_stream());
+            throw;
+        }
+        a->stream_flush();
+        GD_CUDA(cudaStreamSynchronize(a->stream()));
+        a->wait_copies();
+    });
+}
+
 extern "C" {
 
 const char* gd_last_error(void) { return tl_err.c_str(); }
@@ -479,6 +521,28 @@ int gd_wait(const void* h) {
     if (!h) return null_handle();
     return guard([&] { algo_of(h)->wait_copies(); });
 }
+int gd_sssp_run_stream(gd_sssp* s, const uint8_t* kind, const int64_t* src, const int64_t* dst, const int64_t* w,
+                       int64_t k, int64_t batch_size, int64_t first_batch_index, int64_t* dist, int64_t* parent) {
+    return algo_run_stream(s, kind, src, dst, w, k, batch_size, first_batch_index, [&](int64_t j) {
+        if (!dist && !parent) return;
+        const void* dev[2];
+        void* host[2];
+        size_t bytes[2];
+        int na = 0;
+        const size_t n = (size_t)s->a->g->n;
+        if (dist) {
+            dev[na] = s->a->dist.get();
+            host[na] = dist;
+            bytes[na++] = n * 8;
+        }
+        if (parent) {
+            dev[na] = s->a->parent_i64();
+            host[na] = parent;
+            bytes[na++] = n * 8;
+        }
+        s->a->stream_result((int)(j & 1), na, dev, host, bytes);
+    });
+}
 int gd_sssp_destroy(gd_sssp* s) {
     if (!s) return ok();
     return guard([&] {
@@ -532,6 +596,17 @@ int gd_pr_rank_device(gd_pr* p, const double** rank) {
         *rank = p->a->rank.get();
     });
 }
+int gd_pr_run_stream(gd_pr* p, const uint8_t* kind, const int64_t* src, const int64_t* dst, const int64_t* w,
+                     int64_t k, int64_t batch_size, int64_t first_batch_index, double* rank) {
+    return algo_run_stream(p, kind, src, dst, w, k, batch_size, first_batch_index, [&](int64_t j) {
+        if (!rank) return;
+        p->a->gather();
+        const void* dev[1] = {p->a->rank.get()};
+        void* host[1] = {rank};
+        const size_t bytes[1] = {(size_t)p->a->g->n * 8};
+        p->a->stream_result((int)(j & 1), 1, dev, host, bytes);
+    });
+}
 int gd_pr_destroy(gd_pr* p) {
     if (!p) return ok();
     return guard([&] {
@@ -555,6 +630,12 @@ int gd_tc_read(gd_tc* t, int64_t* count) {
     if (!t) return null_handle();
     *count = t->a->count;
     return ok();
+}
+int gd_tc_run_stream(gd_tc* t, const uint8_t* kind, const int64_t* src, const int64_t* dst, const int64_t* w,
+                     int64_t k, int64_t batch_size, int64_t first_batch_index, int64_t* counts) {
+    return algo_run_stream(t, kind, src, dst, w, k, batch_size, first_batch_index, [&](int64_t j) {
+        if (counts) counts[j] = t->a->count;
+    });
 }
 int gd_tc_destroy(gd_tc* t) {
     if (!t) return ok();

@@ -48,6 +48,9 @@ void* dev_alloc(size_t bytes, cudaStream_t s);
 void dev_free(void* p, size_t bytes, cudaStream_t s);
 void dev_cache_release(cudaStream_t s, bool all = false);  // return a stream's cached blocks (before destroying it)
 
+// memset by a kernel (gd_prims.cu): copy-engine memsets queue behind read-backs too
+void fill_d(cudaStream_t s, void* dst, int v, size_t bytes);
+
 template <typename T>
 struct DBuf {
     T* p = nullptr;
@@ -90,7 +93,7 @@ struct DBuf {
     }
     T* get() const { return p; }
     void zero(cudaStream_t st) const {
-        if (n) GD_CUDA(cudaMemsetAsync(p, 0, n * sizeof(T), st));
+        if (n) fill_d(st, p, 0, n * sizeof(T));
     }
 };
 
@@ -178,6 +181,9 @@ void fill_i32(cudaStream_t s, int32_t* a, int64_t n, int32_t v);
 // staging buffer: a pageable destination costs an extra staged copy and
 // several microseconds of latency at every such sync point.
 void read_small(cudaStream_t s, void* host, const void* dev, size_t bytes);
+// device-to-device copy by a kernel (gd_prims.cu)
+void copy_d2d(cudaStream_t s, void* dst, const void* src, size_t bytes);
+
 
 template <typename T>
 inline T read_scalar(cudaStream_t s, const T* dptr) {

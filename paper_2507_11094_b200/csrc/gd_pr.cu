@@ -490,7 +490,7 @@ void PR::recompute(const uint8_t* flags) {
     last_sweeps = 0;
     if (n == 0) return;
     g->compact_rev();
-    GD_CUDA(cudaMemsetAsync(ctl.get(), 0, C_LEN * sizeof(int64_t), s));
+    fill_d(s, ctl.get(), 0, C_LEN * sizeof(int64_t));
     if (maxiter <= 0) return;
     const int64_t lo = g->part ? g->own_lo : (comm ? Blocks(n, comm->world).lo(comm->rank) : 0);
     const int64_t hi = g->part ? g->own_hi : (comm ? Blocks(n, comm->world).hi(comm->rank) : n);
@@ -549,6 +549,7 @@ void PR::batch(DevBatch& b, int64_t batch_index) {
         timer.begin(PH_MERGE);
         g->merge();
     }
+    struct_done();
     timer.begin(PH_PROP);
     if (g->part) flood_weak_components_dist(*g, affected.get(), &prof);
     else flood_weak_components(*g, affected.get(), &prof);

@@ -93,16 +93,89 @@ void dev_cache_release(cudaStream_t s, bool all) {
     }
 }
 
+namespace {
+// byte copy by the SMs: 16-byte vectors when both ends allow it
+__global__ void k_copy_bytes(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst, size_t n) {
+    const size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x, stride = (size_t)gridDim.x * blockDim.x;
+    if ((((uintptr_t)src | (uintptr_t)dst) & 15) == 0) {
+        const size_t nv = n / 16;
+        const int4* s4 = reinterpret_cast<const int4*>(src);
+        int4* d4 = reinterpret_cast<int4*>(dst);
+        for (size_t i = t; i < nv; i += stride) d4[i] = s4[i];
+        for (size_t i = nv * 16 + t; i < n; i += stride) dst[i] = src[i];
+    } else {
+        for (size_t i = t; i < n; i += stride) dst[i] = src[i];
+    }
+}
+}  // namespace
+
+namespace {
+__global__ void k_fill_bytes(uint8_t* __restrict__ dst, int v, size_t n) {
+    const size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x, stride = (size_t)gridDim.x * blockDim.x;
+    const uint8_t b = (uint8_t)v;
+    if (((uintptr_t)dst & 15) == 0) {
+        const uint32_t w = 0x01010101u * b;
+        const int4 q = make_int4((int)w, (int)w, (int)w, (int)w);
+        const size_t nv = n / 16;
+        int4* d4 = reinterpret_cast<int4*>(dst);
+        for (size_t i = t; i < nv; i += stride) d4[i] = q;
+        for (size_t i = nv * 16 + t; i < n; i += stride) dst[i] = b;
+    } else {
+        for (size_t i = t; i < n; i += stride) dst[i] = b;
+    }
+}
+
+}  // namespace
+
+// cudaMemsetAsync's replacement on the batch path (a kernel, for the reason below)
+void fill_d(cudaStream_t s, void* dst, int v, size_t bytes) {
+    if (!bytes) return;
+    static const bool ce = getenv("GD_COPY_ENGINE") != nullptr;  // A/B: the copy-engine memset
+    if (ce) {
+        GD_CUDA(cudaMemsetAsync(dst, v, bytes, s));
+        return;
+    }
+    const unsigned g = (unsigned)std::min<size_t>((bytes / 16 + 255) / 256 + 1, 148 * 16);
+    k_fill_bytes<<<g, 256, 0, s>>>(static_cast<uint8_t*>(dst), v, bytes);
+    count_launch();
+    GD_LAUNCH_CHECK();
+}
+
+// Device-to-device copies on the store path go through the SMs, not a copy
+// engine: a copy engine serves its queue in order, so a small copy would
+// wait behind a result read-back (tens of MB) that another stream has
+// queued in the same direction (tools/e2e_probe2.py).
+void copy_d2d(cudaStream_t s, void* dst, const void* src, size_t bytes) {
+    if (!bytes) return;
+    static const bool ce = getenv("GD_COPY_ENGINE") != nullptr;
+    if (ce) {
+        GD_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, s));
+        return;
+    }
+    const unsigned g = (unsigned)std::min<size_t>((bytes / 16 + 255) / 256 + 1, 148 * 16);
+    k_copy_bytes<<<g, 256, 0, s>>>(static_cast<const uint8_t*>(src), static_cast<uint8_t*>(dst), bytes);
+    count_launch();
+    GD_LAUNCH_CHECK();
+}
+
+// Small reads land in mapped pinned memory written by a kernel, for the
+// same reason: a cudaMemcpy D2H would queue behind a concurrent read-back.
 void read_small(cudaStream_t s, void* host, const void* dev, size_t bytes) {
     constexpr size_t kCap = 4096;
     static thread_local void* pin = nullptr;
+    static thread_local void* dpin = nullptr;
     if (bytes > kCap) {
         GD_CUDA(cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, s));
         GD_CUDA(cudaStreamSynchronize(s));
         return;
     }
-    if (!pin) GD_CUDA(cudaMallocHost(&pin, kCap));
-    GD_CUDA(cudaMemcpyAsync(pin, dev, bytes, cudaMemcpyDeviceToHost, s));
+    if (!pin) {
+        GD_CUDA(cudaHostAlloc(&pin, kCap, cudaHostAllocMapped | cudaHostAllocPortable));
+        GD_CUDA(cudaHostGetDevicePointer(&dpin, pin, 0));
+    }
+    k_copy_bytes<<<1, 32, 0, s>>>(static_cast<const uint8_t*>(dev), static_cast<uint8_t*>(dpin), bytes);
+    count_launch();
+    GD_LAUNCH_CHECK();
     GD_CUDA(cudaStreamSynchronize(s));
     memcpy(host, pin, bytes);
 }
@@ -136,8 +209,8 @@ void sort_pairs_u64(cudaStream_t s, uint64_t* keys, int32_t* vals, int64_t n, in
     Temp t(bytes, s);
     GD_CUDA(cub::DeviceRadixSort::SortPairs(t.p, bytes, kb, vb, n, 0, end_bit, s));
     count_library_launch();
-    if (kb.Current() != keys) GD_CUDA(cudaMemcpyAsync(keys, kb.Current(), n * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
-    if (vb.Current() != vals) GD_CUDA(cudaMemcpyAsync(vals, vb.Current(), n * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+    if (kb.Current() != keys) copy_d2d(s, keys, kb.Current(), n * sizeof(uint64_t));
+    if (vb.Current() != vals) copy_d2d(s, vals, vb.Current(), n * sizeof(int32_t));
 }
 
 void sort_pairs_u32(cudaStream_t s, uint32_t* keys, int32_t* vals, int64_t n, int end_bit) {
@@ -151,8 +224,8 @@ void sort_pairs_u32(cudaStream_t s, uint32_t* keys, int32_t* vals, int64_t n, in
     Temp t(bytes, s);
     GD_CUDA(cub::DeviceRadixSort::SortPairs(t.p, bytes, kb, vb, n, 0, end_bit, s));
     count_library_launch();
-    if (kb.Current() != keys) GD_CUDA(cudaMemcpyAsync(keys, kb.Current(), n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
-    if (vb.Current() != vals) GD_CUDA(cudaMemcpyAsync(vals, vb.Current(), n * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+    if (kb.Current() != keys) copy_d2d(s, keys, kb.Current(), n * sizeof(uint32_t));
+    if (vb.Current() != vals) copy_d2d(s, vals, vb.Current(), n * sizeof(int32_t));
 }
 
 void sort_keys_u64(cudaStream_t s, uint64_t* keys, int64_t n, int end_bit) {
@@ -164,7 +237,7 @@ void sort_keys_u64(cudaStream_t s, uint64_t* keys, int64_t n, int end_bit) {
     Temp t(bytes, s);
     GD_CUDA(cub::DeviceRadixSort::SortKeys(t.p, bytes, kb, n, 0, end_bit, s));
     count_library_launch();
-    if (kb.Current() != keys) GD_CUDA(cudaMemcpyAsync(keys, kb.Current(), n * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
+    if (kb.Current() != keys) copy_d2d(s, keys, kb.Current(), n * sizeof(uint64_t));
 }
 
 void exclusive_scan_i64(cudaStream_t s, const int64_t* in, int64_t* out, int64_t n) {
@@ -199,7 +272,7 @@ int64_t select_flagged_index(cudaStream_t s, const uint8_t* flags, int64_t n, in
 
 void select_flagged_index_async(cudaStream_t s, const uint8_t* flags, int64_t n, int32_t* out, int64_t* d_count) {
     if (n <= 0) {
-        GD_CUDA(cudaMemsetAsync(d_count, 0, sizeof(int64_t), s));
+        fill_d(s, d_count, 0, sizeof(int64_t));
         return;
     }
     thrust::counting_iterator<int32_t> it(0);

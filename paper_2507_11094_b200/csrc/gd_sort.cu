@@ -400,7 +400,7 @@ void exclusive_scan_i64(cudaStream_t s, const int64_t* in, int64_t* out, int64_t
 
 void select_flagged_index_async(cudaStream_t s, const uint8_t* flags, int64_t n, int32_t* out, int64_t* d_count) {
     if (n <= 0) {
-        GD_CUDA(cudaMemsetAsync(d_count, 0, sizeof(int64_t), s));
+        fill_d(s, d_count, 0, sizeof(int64_t));
         return;
     }
     static const int gmax = coop_grid_of(k_select, kScanThreads, 2);

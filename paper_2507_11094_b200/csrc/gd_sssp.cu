@@ -791,11 +791,11 @@ SSSP::SSSP(Store* st, int64_t s, int64_t cap) : AlgoBase(ALGO_SSSP, st), src((in
         const int64_t one = src >= g->own_lo && src < g->own_hi ? 1 : 0;
         GD_CUDA(cudaMemcpyAsync(ns.get(), &one, 8, cudaMemcpyHostToDevice, cs));
         DBuf<int32_t> sl(std::max<int64_t>(n, 1), cs);
-        GD_CUDA(cudaMemcpyAsync(sl.get(), sq.get(), 4, cudaMemcpyDeviceToDevice, cs));
+        copy_d2d(cs, sl.get(), sq.get(), 4);
         fixpoint_dist(FP_RELAX, sl.get(), ns.get(), nullptr);
         sync(true, false, nullptr);
         DBuf<uint8_t> all(std::max<int64_t>(n, 1), cs);
-        GD_CUDA(cudaMemsetAsync(all.get(), 1, n, cs));
+        fill_d(cs, all.get(), 1, n);
         DBuf<int32_t> list(std::max<int64_t>(n, 1), cs);
         owned_list(all.get(), list.get(), ns.get());
         fix_parents(list.get(), ns.get(), n);
@@ -885,7 +885,7 @@ void SSSP::fixpoint(int mode, const int32_t* seeds, const int64_t* d_nseeds, int
 
 void SSSP::owned_list(const uint8_t* flags, int32_t* list, int64_t* d_m) {
     cudaStream_t s = stream();
-    GD_CUDA(cudaMemsetAsync(d_m, 0, 8, s));
+    fill_d(s, d_m, 0, 8);
     const int64_t lo = g->own_lo, hi = g->own_hi;
     if (hi > lo) GD_KERNEL(k_select_owned, grid_for(hi - lo, 256), 256, 0, s, flags, lo, hi, list, d_m);
 }
@@ -918,7 +918,7 @@ void SSSP::fixpoint_dist(int mode, int32_t* seeds, int64_t* d_nseeds, uint8_t* f
     const int64_t cap = std::max<int64_t>(1, cap_factor * std::max<int64_t>(n, 1));
     for (int64_t step = 0;; ++step) {
         if (step >= cap) throw GdError(GD_ERR_DIVERGED, "fixed point diverged");
-        GD_CUDA(cudaMemsetAsync(nbox.get(), 0, sizeof(unsigned long long), s));
+        fill_d(s, nbox.get(), 0, sizeof(unsigned long long));
         fixpoint(mode, cur, d_nseeds, 0, flags, only);
         DBuf<unsigned long long> cnt(2 * W, s);
         cnt.zero(s);
@@ -928,11 +928,11 @@ void SSSP::fixpoint_dist(int mode, int32_t* seeds, int64_t* d_nseeds, uint8_t* f
                   packed.get());
         DBuf<int32_t> recv;
         const int64_t m = c->alltoallv_i32(packed.get(), reinterpret_cast<const int64_t*>(cnt.get()), 3, recv, s);
-        GD_CUDA(cudaMemsetAsync(nn.get(), 0, 8, s));
+        fill_d(s, nn.get(), 0, 8);
         ++step_id;
         if (m) GD_KERNEL(k_msg_apply, grid_for(m, 256), 256, 0, s, recv.get(), m, mode, dist.get(), parent.get(),
                          flags, sstamp.get(), step_id, nxt, nn.get());
-        GD_CUDA(cudaMemcpyAsync(tot.get(), nn.get(), 8, cudaMemcpyDeviceToDevice, s));
+        copy_d2d(s, tot.get(), nn.get(), 8);
         c->allreduce_sum_i64(tot.get(), 1, s);
         const int64_t total = read_scalar(s, tot.get());
         static const bool dbg = getenv("GD_SSSP_DEBUG") != nullptr;
@@ -941,7 +941,7 @@ void SSSP::fixpoint_dist(int mode, int32_t* seeds, int64_t* d_nseeds, uint8_t* f
                     c->rank, mode, (long long)step, (unsigned long long)read_scalar(s, nbox.get()), (long long)m,
                     (long long)total);
         if (total == 0) break;
-        GD_CUDA(cudaMemcpyAsync(d_nseeds, nn.get(), 8, cudaMemcpyDeviceToDevice, s));
+        copy_d2d(s, d_nseeds, nn.get(), 8);
         std::swap(cur, nxt);
     }
 }
@@ -952,7 +952,7 @@ void SSSP::fix_parents(const int32_t* list, const int64_t* d_m, int64_t m) {
     IdxView ix = g->rev.view();
     heavy.ensure(g->rev.nnz / kHeavy + 64, s);
     unsigned long long* nh = fr.cnt.get() + 10;
-    GD_CUDA(cudaMemsetAsync(nh, 0, sizeof(unsigned long long), s));
+    fill_d(s, nh, 0, sizeof(unsigned long long));
     GD_KERNEL_T("sssp_parent", 0, k_fix_parent, group_grid(m), kThreads, 0, s, list, d_m, m, ix, dist.get(),
                 parent.get(), src, heavy.get(), nh);
     GD_KERNEL_T("sssp_parent", 0, k_fix_parent_heavy, 148 * 4, kThreads, 0, s, heavy.get(), nh, ix, dist.get(),
@@ -965,7 +965,7 @@ void SSSP::finish() {
     read_small(stream(), h, ctr.get(), (6 + nfp) * sizeof(long long));
     if (nfp) {
         for (int j = 0; j < nfp; ++j) prof_set_bytes(fp_prof[j], h[6 + j]);
-        GD_CUDA(cudaMemsetAsync(ctr.get() + 6, 0, nfp * sizeof(long long), stream()));
+        fill_d(stream(), ctr.get() + 6, 0, nfp * sizeof(long long));
         nfp = 0;
     }
     static const bool dbg = getenv("GD_SSSP_DEBUG") != nullptr;
@@ -975,7 +975,7 @@ void SSSP::finish() {
     iterations = h[1];
     if (h[2]) {  // abandoned piles leave in-far marks behind
         infar.zero(stream());
-        GD_CUDA(cudaMemsetAsync(ctr.get() + 2, 0, sizeof(long long), stream()));
+        fill_d(stream(), ctr.get() + 2, 0, sizeof(long long));
         throw GdError(GD_ERR_DIVERGED, "fixed point diverged");
     }
 }
@@ -1010,7 +1010,7 @@ void SSSP::batch_dist(DevBatch& b, int64_t batch_index) {
     {  // one pull sweep over the owned stale vertices, then the push restricted to stale targets
         IdxView ix = g->rev.view();
         heavy.ensure(g->rev.nnz / kHeavy + 64, s);
-        GD_CUDA(cudaMemsetAsync(fr.cnt.get() + 9, 0, sizeof(unsigned long long), s));
+        fill_d(s, fr.cnt.get() + 9, 0, sizeof(unsigned long long));
         GD_KERNEL_T("sssp_pull", 0, k_pull_once, group_grid(n), kThreads, 0, s, list.get(), nl.get(), ix, dist.get(),
                     heavy.get(), fr.cnt.get() + 9);
         GD_KERNEL_T("sssp_pull", 0, k_pull_heavy, 148 * 4, kThreads, 0, s, heavy.get(), fr.cnt.get() + 9, ix,
@@ -1033,6 +1033,7 @@ void SSSP::batch_dist(DevBatch& b, int64_t batch_index) {
     } else {
         g->compact_rev();
     }
+    struct_done();
     // incrementalSSSP (sssp_dynamic.sp:101-130)
     timer.begin(PH_PROP);
     owned_list(seed_add, list.get(), nl.get());
@@ -1082,7 +1083,7 @@ void SSSP::batch(DevBatch& b, int64_t batch_index) {
     if (!pull_fixpoint) {
         IdxView ix = g->rev.view();
         heavy.ensure(g->rev.nnz / kHeavy + 64, s);
-        GD_CUDA(cudaMemsetAsync(fr.cnt.get() + 9, 0, sizeof(unsigned long long), s));
+        fill_d(s, fr.cnt.get() + 9, 0, sizeof(unsigned long long));
         GD_KERNEL_T("sssp_pull", 0, k_pull_once, group_grid(n), kThreads, 0, s, list.get(), nlist, ix, dist.get(),
                     heavy.get(), fr.cnt.get() + 9);
         GD_KERNEL_T("sssp_pull", 0, k_pull_heavy, 148 * 4, kThreads, 0, s, heavy.get(), fr.cnt.get() + 9, ix,
@@ -1107,6 +1108,7 @@ void SSSP::batch(DevBatch& b, int64_t batch_index) {
     } else {
         g->compact_rev();
     }
+    struct_done();
 
     // incrementalSSSP (sssp_dynamic.sp:101-130); touched starts as the seeds
     timer.begin(PH_PROP);
@@ -1116,6 +1118,15 @@ void SSSP::batch(DevBatch& b, int64_t batch_index) {
     fix_parents(list.get(), nlist, n);
     finish();
     timer.end_all();
+}
+
+// parent widened to int64 on the handle's stream (parent64), for read-backs
+const int64_t* SSSP::parent_i64() {
+    cudaStream_t s = stream();
+    int64_t n = g->n;
+    parent64.ensure(std::max<int64_t>(n, 1), s);
+    if (n) GD_KERNEL(k_read_parent, grid_for(n, 256), 256, 0, s, parent.get(), n, parent64.get());
+    return parent64.get();
 }
 
 void SSSP::read_async(int64_t* h_dist, int64_t* h_parent) {

@@ -41,7 +41,8 @@ struct SSSP : AlgoBase {
     void batch(DevBatch& b, int64_t batch_index);
     void batch_dist(DevBatch& b, int64_t batch_index);  // vertex-partitioned store
     void read(int64_t* dist, int64_t* parent);
-    void read_async(int64_t* dist, int64_t* parent);  // see AlgoBase::copy_out_async
+    void read_async(int64_t* dist, int64_t* parent);
+    const int64_t* parent_i64();  // parent widened to int64 (device, valid until the next batch)  // see AlgoBase::copy_out_async
 
   private:
     // one cooperative launch per fixpoint (relax / walk / pull); the seed count

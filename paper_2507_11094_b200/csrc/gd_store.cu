@@ -140,6 +140,37 @@ __global__ void k_del_requests(const uint64_t* skey, const int32_t* srec, int64_
     }
 }
 
+// Undirected deletes: every record r gives requests 2r (s->d) and 2r+1
+// (d->s), keyed by their directed pair and valued by the request index, so
+// ONE stable sort by directed key leaves each key's run in record order.
+// Each record of the unordered pair {a,b} has exactly one request in the
+// (a,b) run, so a request's rank in its run is the record's rank among the
+// pair's records (the occurrence); a self-loop's two requests are adjacent
+// in its run, ranks 2j and 2j+1 (dynamic.py:231-234).
+__global__ void k_del_requests_u(const int32_t* s, const int32_t* d, int64_t k, int sh, uint64_t* rq_key,
+                                 int32_t* rq_val) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < k; i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t a = s[i], b = d[i];
+        rq_key[2 * i] = pair_key(a, b, sh);
+        rq_key[2 * i + 1] = pair_key(b, a, sh);
+        rq_val[2 * i] = (int32_t)(2 * i);
+        rq_val[2 * i + 1] = (int32_t)(2 * i + 1);
+    }
+}
+
+__global__ void k_del_requests_u_fill(const uint64_t* rq_key, const int32_t* rq_val, int64_t m, int32_t* rq_occ,
+                                      int32_t* rq_rec, uint8_t* rq_which) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t key = rq_key[i];
+        int32_t j = 0;  // rank within the run of equal keys (runs are short)
+        for (int64_t p = i - 1; p >= 0 && rq_key[p] == key; --p) ++j;
+        const int32_t v = rq_val[i];
+        rq_occ[i] = j;
+        rq_rec[i] = v >> 1;
+        rq_which[i] = (uint8_t)(v & 1);
+    }
+}
+
 // first index of each row run in a (row,col)-sorted key array
 __global__ void k_row_starts(const uint64_t* key, int64_t m, int sh, uint8_t* flag) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
@@ -750,18 +781,66 @@ __device__ __forceinline__ void edit_load(const int32_t* __restrict__ col, const
     }
 }
 
+// A window's metadata: its dead base and insertion range, and (lanes <
+// min(32, inserts)) its first 32 insertions -- loaded ahead of the window so
+// the dependent loads stay off the copy's critical path.
+struct WinMeta {
+    int64_t dead0, pjw, pje;
+    int my_ins;  // insertion position relative to the window start (INT_MAX: none)
+    int32_t my_icol, my_iw;
+};
+__device__ __forceinline__ void win_meta_head(WinMeta& m, int64_t win, const int64_t* __restrict__ dead_win,
+                                              const int64_t* __restrict__ pj_win) {
+    m.dead0 = dead_win[win];
+    m.pjw = pj_win[win];
+    m.pje = pj_win[win + 1];
+}
 template <bool WEIGHTED>
-__device__ __forceinline__ void edit_store(int64_t win, const int32_t (&v)[kWin / 32], const int32_t (&wv)[kWin / 32],
-                                           const int64_t* __restrict__ dead_win, const int64_t* __restrict__ ipos,
-                                           const int64_t* __restrict__ pj_win, const int32_t* __restrict__ icol,
-                                           const int32_t* __restrict__ iw, int32_t* __restrict__ ocol,
-                                           int32_t* __restrict__ ow) {
+__device__ __forceinline__ void win_meta_ins(WinMeta& m, int64_t win, const int64_t* __restrict__ ipos,
+                                             const int32_t* __restrict__ icol, const int32_t* __restrict__ iw) {
+    const int lane = threadIdx.x & 31;
+    m.my_ins = INT_MAX;
+    m.my_icol = 0;
+    m.my_iw = 1;
+    if (lane < m.pje - m.pjw) {
+        m.my_ins = (int)(ipos[m.pjw + lane] - win * kWin);
+        m.my_icol = icol[m.pjw + lane];
+        if (WEIGHTED && iw) m.my_iw = iw[m.pjw + lane];
+    }
+}
+
+template <bool WEIGHTED>
+__device__ __forceinline__ void edit_store_p(int64_t win, const int32_t (&v)[kWin / 32],
+                                             const int32_t (&wv)[kWin / 32], const WinMeta& mt,
+                                             const int64_t* __restrict__ ipos, const int32_t* __restrict__ icol,
+                                             const int32_t* __restrict__ iw, int32_t* __restrict__ ocol,
+                                             int32_t* __restrict__ ow);
+
+template <bool WEIGHTED>
+__device__ __forceinline__ void edit_store_m(int64_t win, const int32_t (&v)[kWin / 32],
+                                             const int32_t (&wv)[kWin / 32], int64_t dead0, int64_t pjw,
+                                             int64_t pje, const int64_t* __restrict__ ipos,
+                                             const int32_t* __restrict__ icol, const int32_t* __restrict__ iw,
+                                             int32_t* __restrict__ ocol, int32_t* __restrict__ ow) {
+    WinMeta mt;
+    mt.dead0 = dead0;
+    mt.pjw = pjw;
+    mt.pje = pje;
+    win_meta_ins<WEIGHTED>(mt, win, ipos, icol, iw);
+    edit_store_p<WEIGHTED>(win, v, wv, mt, ipos, icol, iw, ocol, ow);
+}
+
+template <bool WEIGHTED>
+__device__ __forceinline__ void edit_store_p(int64_t win, const int32_t (&v)[kWin / 32],
+                                             const int32_t (&wv)[kWin / 32], const WinMeta& mt,
+                                             const int64_t* __restrict__ ipos, const int32_t* __restrict__ icol,
+                                             const int32_t* __restrict__ iw, int32_t* __restrict__ ocol,
+                                             int32_t* __restrict__ ow) {
     constexpr int Q = kWin / 32;
     const int lane = threadIdx.x & 31;
     const unsigned lt = (1u << lane) - 1;
     const int64_t ws = win * kWin;
-    const int64_t dead0 = dead_win[win];
-    const int64_t pjw = pj_win[win], pje = pj_win[win + 1];
+    const int64_t dead0 = mt.dead0, pjw = mt.pjw, pje = mt.pje;
     const int nins = (int)(pje - pjw);
     unsigned m[Q];
 #pragma unroll
@@ -782,13 +861,8 @@ __device__ __forceinline__ void edit_store(int64_t win, const int32_t (&v)[kWin 
         }
         return;
     }
-    int my_ins = INT_MAX;
-    int32_t my_icol = 0, my_iw = 1;
-    if (lane < nins) {
-        my_ins = (int)(ipos[pjw + lane] - ws);
-        my_icol = icol[pjw + lane];
-        if (WEIGHTED && iw) my_iw = iw[pjw + lane];
-    }
+    const int my_ins = mt.my_ins;
+    const int32_t my_icol = mt.my_icol, my_iw = mt.my_iw;
     int dead = 0;
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
@@ -817,6 +891,136 @@ __device__ __forceinline__ void edit_store(int64_t win, const int32_t (&v)[kWin 
         const int np = P - d + j;
         oc[np] = ic;
         if (WEIGHTED) owb[np] = iwv;
+    }
+}
+
+template <bool WEIGHTED>
+__device__ __forceinline__ void edit_store(int64_t win, const int32_t (&v)[kWin / 32], const int32_t (&wv)[kWin / 32],
+                                           const int64_t* __restrict__ dead_win, const int64_t* __restrict__ ipos,
+                                           const int64_t* __restrict__ pj_win, const int32_t* __restrict__ icol,
+                                           const int32_t* __restrict__ iw, int32_t* __restrict__ ocol,
+                                           int32_t* __restrict__ ow) {
+    edit_store_m<WEIGHTED>(win, v, wv, dead_win[win], pj_win[win], pj_win[win + 1], ipos, icol, iw, ocol, ow);
+}
+
+// ---- the bulk-copy (TMA) merge copy ----------------------------------------
+// The register path above keeps one window's loads in flight per warp and
+// stalls on them (ncu: 28% of samples on the first use of the loaded
+// entries, 48% of DRAM bandwidth).  Here the entries stream into shared
+// memory by cp.async.bulk: one thread per CTA keeps kBulkStages chunks of
+// kTile entries (one window per warp) in flight on mbarriers, so the loads
+// are no longer bounded by registers or warps, and the warps run the same
+// compaction from shared memory.
+constexpr int kBulkStages = 4;
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_init_fence() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "GD_MBAR_WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra GD_MBAR_WAIT_%=;\n"
+        "}\n" ::"r"(smem_addr(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_addr(dst)),
+        "l"(src), "r"(bytes), "r"(smem_addr(bar))
+        : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+template <bool WEIGHTED>
+__global__ void __launch_bounds__(kEditThreads) k_edit_bulk(const int32_t* __restrict__ col,
+                                                            const int32_t* __restrict__ w, int64_t nnz,
+                                                            const int64_t* __restrict__ dead_win,
+                                                            const int64_t* __restrict__ ipos,
+                                                            const int64_t* __restrict__ pj_win,
+                                                            const int32_t* __restrict__ icol,
+                                                            const int32_t* __restrict__ iw, int64_t nwin,
+                                                            int32_t* __restrict__ ocol, int32_t* __restrict__ ow) {
+    constexpr int Q = kWin / 32;
+    constexpr int kWarps = kEditThreads / 32;
+    constexpr uint32_t kWinBytes = kWin * 4;
+    // per warp: kBulkStages windows of cols (then of weights), one mbarrier each
+    extern __shared__ __align__(128) int32_t ebuf[];
+    __shared__ __align__(8) uint64_t bar[kWarps][kBulkStages];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    int32_t* wbuf = ebuf + warp * kBulkStages * kWin * (WEIGHTED ? 2 : 1);
+    uint64_t* wbar = bar[warp];
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nfull = nnz / kWin;
+    auto issue = [&](int st, int64_t win) {
+        mbar_expect_tx(&wbar[st], WEIGHTED ? 2 * kWinBytes : kWinBytes);
+        bulk_g2s(wbuf + st * kWin, col + win * kWin, kWinBytes, &wbar[st]);
+        if (WEIGHTED) bulk_g2s(wbuf + (kBulkStages + st) * kWin, w + win * kWin, kWinBytes, &wbar[st]);
+    };
+    if (lane == 0) {
+        for (int st = 0; st < kBulkStages; ++st) mbar_init(&wbar[st], 1);
+        mbar_init_fence();
+        for (int st = 0; st < kBulkStages; ++st) {
+            const int64_t win = gw + (int64_t)st * nwarps;
+            if (win < nfull) issue(st, win);
+        }
+    }
+    __syncwarp();
+    // metadata pipeline: window i's insertions and window i+1's ranges are
+    // loaded while window i-1 is written
+    WinMeta m0, m1;
+    if (gw < nfull) {
+        win_meta_head(m0, gw, dead_win, pj_win);
+        win_meta_ins<WEIGHTED>(m0, gw, ipos, icol, iw);
+    }
+    if (gw + nwarps < nfull) win_meta_head(m1, gw + nwarps, dead_win, pj_win);
+    int it = 0;
+    for (int64_t win = gw; win < nfull; win += nwarps, ++it) {
+        const int st = it % kBulkStages;
+        WinMeta m2;
+        const int64_t w1 = win + nwarps, w2 = win + 2 * nwarps;
+        if (w2 < nfull) win_meta_head(m2, w2, dead_win, pj_win);
+        if (w1 < nfull) win_meta_ins<WEIGHTED>(m1, w1, ipos, icol, iw);
+        mbar_wait(&wbar[st], (uint32_t)(it / kBulkStages) & 1u);
+        int32_t v[Q], wv[Q];
+        const int32_t* sc = wbuf + st * kWin;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            v[q] = sc[q * 32 + lane];
+            if (WEIGHTED) wv[q] = sc[kBulkStages * kWin + q * 32 + lane];
+        }
+        __syncwarp();  // the whole window is in registers: the stage may refill
+        if (lane == 0) {
+            const int64_t wn = win + (int64_t)kBulkStages * nwarps;
+            if (wn < nfull) {
+                fence_proxy_async_smem();
+                issue(st, wn);
+            }
+        }
+        edit_store_p<WEIGHTED>(win, v, wv, m0, ipos, icol, iw, ocol, ow);
+        m0 = m1;
+        m1 = m2;
+    }
+    // the partial last window: the register path
+    for (int64_t win = nfull + gw; win < nwin; win += nwarps) {
+        int32_t v[Q], wv[Q];
+        edit_load<false, WEIGHTED>(col, w, nnz, win, v, wv);
+        edit_store<WEIGHTED>(win, v, wv, dead_win, ipos, pj_win, icol, iw, ocol, ow);
     }
 }
 
@@ -1067,7 +1271,31 @@ void edit_apply(cudaStream_t s, EditJob& j, int64_t dead_total, DBuf<int64_t>& n
         GD_KERNEL(k_win_ins, grid_for(nwin + 1, 256), 256, 0, s, nwin, j.ipos, nins, pj.get());
         unsigned g = (unsigned)std::min<int64_t>(ntiles, 148LL * 64);
         // algorithmic bytes: every base entry read once, every surviving entry written once
-        if (j.weighted)
+        static const int bulk_env = getenv("GD_EDIT_BULK") ? atoi(getenv("GD_EDIT_BULK")) : 1;
+        const bool aligned = ((uintptr_t)j.col & 15) == 0 && (!j.weighted || ((uintptr_t)j.w & 15) == 0);
+        if (bulk_env && aligned && nnz >= kTile) {
+            const int smem = kBulkStages * kTile * 4 * (j.weighted ? 2 : 1);  // kTile = kWin per warp
+            static const bool attr = [] {
+                GD_CUDA(cudaFuncSetAttribute(k_edit_bulk<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             kBulkStages * kTile * 8));
+                GD_CUDA(cudaFuncSetAttribute(k_edit_bulk<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             kBulkStages * kTile * 4));
+                return true;
+            }();
+            (void)attr;
+            int per_sm = 0;
+            GD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                &per_sm, j.weighted ? k_edit_bulk<true> : k_edit_bulk<false>, kEditThreads, smem));
+            const unsigned gb = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ntiles, 148LL * std::max(per_sm, 1)));
+            if (j.weighted)
+                GD_KERNEL_T("merge_copy", (nnz + (nnz - dead_total)) * 8, k_edit_bulk<true>, gb, kEditThreads, smem,
+                            s, j.col, j.w, nnz, j.dead_win.get(), j.ipos, pj.get(), j.icol, j.iw, nwin,
+                            new_col.get(), new_w.get());
+            else
+                GD_KERNEL_T("merge_copy", (nnz + (nnz - dead_total)) * 4, k_edit_bulk<false>, gb, kEditThreads, smem,
+                            s, j.col, nullptr, nnz, j.dead_win.get(), j.ipos, pj.get(), j.icol, nullptr, nwin,
+                            new_col.get(), nullptr);
+        } else if (j.weighted)
             GD_KERNEL_T("merge_copy", (nnz + (nnz - dead_total)) * 8, k_edit_base<true>, g, kEditThreads, 0, s, j.col,
                         j.w, nnz, j.dead_win.get(), j.ipos, pj.get(), j.icol, j.iw, nwin, new_col.get(), new_w.get());
         else
@@ -1381,8 +1609,8 @@ void Store::index_delete(SortedIndex& ix, const KilledArcs& ka) {
     DBuf<int64_t> tpos(old + m, s);
     DBuf<int32_t> trow(old + m, s);
     if (old) {
-        GD_CUDA(cudaMemcpyAsync(tpos.get(), ix.tpos.get(), old * 8, cudaMemcpyDeviceToDevice, s));
-        GD_CUDA(cudaMemcpyAsync(trow.get(), ix.trow.get(), old * 4, cudaMemcpyDeviceToDevice, s));
+        copy_d2d(s, tpos.get(), ix.tpos.get(), old * 8);
+        copy_d2d(s, trow.get(), ix.trow.get(), old * 4);
     }
     GD_KERNEL(k_index_claim, grid_for(m, 256), 256, 0, s, ka.row.get(), ka.col.get(), ka.w.get(), ka.gid.get(), m,
               ix.rows_are_dst, ix.off.get(), ix.col.get(), ix.w.n ? ix.w.get() : nullptr, tpos.get() + old,
@@ -1401,7 +1629,9 @@ void Store::index_add(SortedIndex& ix, const AddedArcs& aa) {
     DBuf<int32_t> val(m, s);
     GD_KERNEL(k_added_to_index, grid_for(m, 256), 256, 0, s, aa.row.get(), aa.col.get(), m, ix.rows_are_dst, sh,
               key.get(), val.get());
-    sort_pairs_u64(s, key.get(), val.get(), m, 2 * sh);
+    // the values only carry the weights: an unweighted index sorts its keys alone
+    if (weighted) sort_pairs_u64(s, key.get(), val.get(), m, 2 * sh);
+    else sort_keys_u64(s, key.get(), m, 2 * sh);
     ix.drow.alloc(m, s);
     ix.dcol.alloc(m, s);
     GD_KERNEL(k_key_split, grid_for(m, 256), 256, 0, s, key.get(), m, sh, ix.drow.get(), ix.dcol.get());
@@ -1419,11 +1649,11 @@ void Store::append_out_tombs(const int64_t* d_pos, const int32_t* d_row, int64_t
     DBuf<int64_t> p(tot, s);
     DBuf<int32_t> r(tot, s);
     if (notomb) {
-        GD_CUDA(cudaMemcpyAsync(p.get(), otpos.get(), notomb * 8, cudaMemcpyDeviceToDevice, s));
-        GD_CUDA(cudaMemcpyAsync(r.get(), otrow.get(), notomb * 4, cudaMemcpyDeviceToDevice, s));
+        copy_d2d(s, p.get(), otpos.get(), notomb * 8);
+        copy_d2d(s, r.get(), otrow.get(), notomb * 4);
     }
-    GD_CUDA(cudaMemcpyAsync(p.get() + notomb, d_pos, cnt * 8, cudaMemcpyDeviceToDevice, s));
-    GD_CUDA(cudaMemcpyAsync(r.get() + notomb, d_row, cnt * 4, cudaMemcpyDeviceToDevice, s));
+    copy_d2d(s, p.get() + notomb, d_pos, cnt * 8);
+    copy_d2d(s, r.get() + notomb, d_row, cnt * 4);
     otpos = std::move(p);
     otrow = std::move(r);
     notomb = tot;
@@ -1506,7 +1736,7 @@ int64_t Store::apply_deletes(const int32_t* d_src, const int32_t* d_dst, int64_t
     if (d_found) lf.alloc(std::max<int64_t>(kl, 1), s);
     int64_t applied = apply_deletes_local(os.get(), od.get(), kl, d_found ? lf.get() : nullptr, want_count);
     if (d_found && k) {  // flags of the owned records; other ranks hold the rest
-        GD_CUDA(cudaMemsetAsync(d_found, 0, k, s));
+        fill_d(s, d_found, 0, k);
         if (kl) GD_KERNEL(k_scatter_u8, grid_for(kl, 256), 256, 0, s, lf.get(), idx.get(), kl, d_found);
     }
     if (want_count) {
@@ -1529,27 +1759,22 @@ int64_t Store::apply_deletes_local(const int32_t* d_src, const int32_t* d_dst, i
     if (fwd.built) compact_index(fwd);
     first_clean_delta = segs.size();  // deltas made before this delete may now hold tombstones
     const int kb = 2 * sh;
-    DBuf<uint64_t> skey(k, s);
-    DBuf<int32_t> srec(k, s);
-    GD_KERNEL(k_del_keys, grid_for(k, 256), 256, 0, s, d_src, d_dst, k, directed, sh, skey.get(), srec.get());
-    sort_pairs_u64(s, skey.get(), srec.get(), k, kb);
-    int64_t nrq = directed ? k : 2 * k;
+    const int64_t nrq = directed ? k : 2 * k;
     DBuf<uint64_t> rq_key(nrq, s);
-    DBuf<int32_t> rq_occ(nrq, s), rq_rec(nrq, s), rq_ord(nrq, s);
+    DBuf<int32_t> rq_occ(nrq, s), rq_rec(nrq, s);
     DBuf<uint8_t> rq_which(nrq, s);
-    GD_KERNEL(k_del_requests, grid_for(k, 256), 256, 0, s, skey.get(), srec.get(), k, d_src, d_dst, directed, sh,
-              rq_key.get(), rq_occ.get(), rq_rec.get(), rq_which.get(), rq_ord.get());
-    if (!directed) {  // order the requests by directed key (stable: occ order kept)
-        sort_pairs_u64(s, rq_key.get(), rq_ord.get(), nrq, kb);
-        DBuf<int32_t> o2(nrq, s), r2(nrq, s);
-        DBuf<uint8_t> w2(nrq, s);
-        GD_KERNEL(k_gather_sel<int32_t>, grid_for(nrq, 256), 256, 0, s, rq_occ.get(), rq_ord.get(), nrq, o2.get());
-        GD_KERNEL(k_gather_sel<int32_t>, grid_for(nrq, 256), 256, 0, s, rq_rec.get(), rq_ord.get(), nrq, r2.get());
-        GD_KERNEL(k_gather_sel<uint8_t>, grid_for(nrq, 256), 256, 0, s, rq_which.get(), rq_ord.get(), nrq,
-                  w2.get());
-        rq_occ = std::move(o2);
-        rq_rec = std::move(r2);
-        rq_which = std::move(w2);
+    if (directed) {  // records sorted by (src, dst), stable: equal pairs in stream order
+        DBuf<int32_t> srec(k, s), rq_ord(nrq, s);
+        GD_KERNEL(k_del_keys, grid_for(k, 256), 256, 0, s, d_src, d_dst, k, directed, sh, rq_key.get(), srec.get());
+        sort_pairs_u64(s, rq_key.get(), srec.get(), k, kb);
+        GD_KERNEL(k_del_requests, grid_for(k, 256), 256, 0, s, rq_key.get(), srec.get(), k, d_src, d_dst, directed,
+                  sh, rq_key.get(), rq_occ.get(), rq_rec.get(), rq_which.get(), rq_ord.get());
+    } else {  // both directions of every record, one sort by directed key
+        DBuf<int32_t> rq_val(nrq, s);
+        GD_KERNEL(k_del_requests_u, grid_for(k, 256), 256, 0, s, d_src, d_dst, k, sh, rq_key.get(), rq_val.get());
+        sort_pairs_u64(s, rq_key.get(), rq_val.get(), nrq, kb);
+        GD_KERNEL(k_del_requests_u_fill, grid_for(nrq, 256), 256, 0, s, rq_key.get(), rq_val.get(), nrq,
+                  rq_occ.get(), rq_rec.get(), rq_which.get());
     }
     // distinct source rows and their chain work items
     DBuf<uint8_t> rflag(nrq, s);
@@ -1557,7 +1782,7 @@ int64_t Store::apply_deletes_local(const int32_t* d_src, const int32_t* d_dst, i
     DBuf<int32_t> row_first(nrq, s);
     // nrows, work items, longest chain, overflow matches, head / tail slots scanned
     DBuf<int64_t> hdr(6, s);
-    GD_CUDA(cudaMemsetAsync(hdr.get(), 0, 6 * sizeof(int64_t), s));
+    fill_d(s, hdr.get(), 0, 6 * sizeof(int64_t));
     select_flagged_index_async(s, rflag.get(), nrq, row_first.get(), hdr.get());
     OutView ov = out_view();
     DBuf<int64_t> chunks(nrq + 1, s), coff(nrq + 1, s);
@@ -1565,7 +1790,7 @@ int64_t Store::apply_deletes_local(const int32_t* d_src, const int32_t* d_dst, i
               sh, chunks.get(), reinterpret_cast<unsigned long long*>(hdr.get() + 2),
               reinterpret_cast<unsigned long long*>(hdr.get() + 4));
     exclusive_scan_i64(s, chunks.get(), coff.get(), nrq + 1);
-    GD_CUDA(cudaMemcpyAsync(hdr.get() + 1, coff.get() + nrq, 8, cudaMemcpyDeviceToDevice, s));
+    copy_d2d(s, hdr.get() + 1, coff.get() + nrq, 8);
     // tail pieces: at most one per kChunk slots of the requested rows
     DBuf<int32_t> wrow(total_slots() / kChunk + nrq + 1, s);
     GD_KERNEL(k_chunk_rows, grid_for(nrq, 256), 256, 0, s, coff.get(), hdr.get(), wrow.get());
@@ -1586,8 +1811,8 @@ int64_t Store::apply_deletes_local(const int32_t* d_src, const int32_t* d_dst, i
         m_chain.alloc(cap, s);
         m_gid.alloc(cap, s);
         if (attempt) {  // overflow retry: start the match collection over
-            GD_CUDA(cudaMemsetAsync(hdr.get() + 3, 0, 8, s));
-            GD_CUDA(cudaMemsetAsync(sel.get(), 0xff, nrq * 8, s));
+            fill_d(s, hdr.get() + 3, 0, 8);
+            fill_d(s, sel.get(), 0xff, nrq * 8);
         }
         MatchOut mo{sel.get(), single.get(), m_key.get(), m_chain.get(), m_gid.get(),
                     reinterpret_cast<unsigned long long*>(hdr.get() + 3), cap};
@@ -1653,7 +1878,7 @@ int64_t Store::apply_deletes_local(const int32_t* d_src, const int32_t* d_dst, i
     // every record's forward request writes its found flag (k_del_resolve): no memset
     // [0] applied records of this call, [1] killed slots since `live` was last
     // brought up to date (read lazily: live_count())
-    GD_CUDA(cudaMemsetAsync(dcounts.get(), 0, sizeof(unsigned long long), s));
+    fill_d(s, dcounts.get(), 0, sizeof(unsigned long long));
     unsigned long long* counts = dcounts.get();
     GD_KERNEL(k_del_resolve, grid_for(nrq, 256), 256, 0, s, rq_key.get(), rq_occ.get(), rq_rec.get(),
               rq_which.get(), single.get(), sel.get(), nrq, m_key.get(), m_gid.get(), nm, rb, rq_pos.get(), found,
@@ -1680,7 +1905,7 @@ int64_t Store::apply_deletes_local(const int32_t* d_src, const int32_t* d_dst, i
 int64_t Store::live_count() {
     unsigned long long killed = 0;
     read_small(stream, &killed, dcounts.get() + 1, sizeof killed);
-    GD_CUDA(cudaMemsetAsync(dcounts.get() + 1, 0, sizeof killed, stream));
+    fill_d(stream, dcounts.get() + 1, 0, sizeof killed);
     live -= (int64_t)killed;
     return live;
 }
@@ -1761,10 +1986,10 @@ void Store::merge() {
         GD_KERNEL(k_delta_rows, grid_for(d.nslots, 256), 256, 0, s, d.off.get(), n, d.col.get(), d.nslots,
                   row.get(), lf.get());
         if (i >= first_clean_delta) {  // no delete phase since it was made: every slot is live
-            GD_CUDA(cudaMemcpyAsync(irow.get() + nins, row.get(), d.nslots * 4, cudaMemcpyDeviceToDevice, s));
-            GD_CUDA(cudaMemcpyAsync(icol.get() + nins, d.col.get(), d.nslots * 4, cudaMemcpyDeviceToDevice, s));
+            copy_d2d(s, irow.get() + nins, row.get(), d.nslots * 4);
+            copy_d2d(s, icol.get() + nins, d.col.get(), d.nslots * 4);
             if (weighted)
-                GD_CUDA(cudaMemcpyAsync(iw.get() + nins, d.w.get(), d.nslots * 4, cudaMemcpyDeviceToDevice, s));
+                copy_d2d(s, iw.get() + nins, d.w.get(), d.nslots * 4);
             nins += d.nslots;
             continue;
         }
@@ -1779,7 +2004,7 @@ void Store::merge() {
     }
     if (segs.size() > 2 && nins > 1) {  // several deltas: stable sort by row keeps (segment, slot) order
         DBuf<uint32_t> rk(nins, s);
-        GD_CUDA(cudaMemcpyAsync(rk.get(), irow.get(), nins * 4, cudaMemcpyDeviceToDevice, s));
+        copy_d2d(s, rk.get(), irow.get(), nins * 4);
         DBuf<int32_t> perm(nins, s);
         iota_i32(s, perm.get(), nins);
         sort_pairs_u32(s, rk.get(), perm.get(), nins, sh);
@@ -1805,9 +2030,9 @@ void Store::merge() {
     DBuf<int64_t> rpos;
     if (rev_dirty) index_plan(rev, jr, rpos);
     DBuf<int64_t> totals(2, s);
-    GD_CUDA(cudaMemcpyAsync(totals.get(), jo.dead_win.get() + jo.nwin, 8, cudaMemcpyDeviceToDevice, s));
+    copy_d2d(s, totals.get(), jo.dead_win.get() + jo.nwin, 8);
     if (rev_dirty)
-        GD_CUDA(cudaMemcpyAsync(totals.get() + 1, jr.dead_win.get() + jr.nwin, 8, cudaMemcpyDeviceToDevice, s));
+        copy_d2d(s, totals.get() + 1, jr.dead_win.get() + jr.nwin, 8);
     int64_t ht[2] = {0, 0};
     read_small(s, ht, totals.get(), rev_dirty ? 16 : 8);
     OutSeg nb;
@@ -1822,7 +2047,7 @@ void Store::merge() {
     otrow.release();
     notomb = 0;
     live = nnz2;  // exact: pending kills are folded in
-    GD_CUDA(cudaMemsetAsync(dcounts.get() + 1, 0, sizeof(unsigned long long), s));
+    fill_d(s, dcounts.get() + 1, 0, sizeof(unsigned long long));
     first_clean_delta = 1;
     claim_logs.clear();  // _rebuild_reverse: list order restarts from the layout
     if (rev.built) compact_index(rev);

@@ -393,7 +393,8 @@ int64_t TC::count_records(const int32_t* s, const int32_t* d, int64_t k) {
     filt.zero(st);
     const uint64_t fmask = (uint64_t(1) << fbits) - 1;
     GD_KERNEL(k_ranks, grid_for(k, 256), 256, 0, st, s, d, k, n, R.get(), filt.get(), fmask);
-    sort_keys_u64(st, R.get(), k);
+    // ranks are < n^2: sort only the bits they use (48 instead of 64 at 2^24 vertices)
+    sort_keys_u64(st, R.get(), k, bits_for((uint64_t)n * (uint64_t)n - 1));
     DBuf<unsigned long long> ctr(3, st);  // [0] count delta, [1] algorithmic bytes, [2] deferred records
     ctr.zero(st);
     // ranks are over ALL records of the phase; the counted slice is this rank's
@@ -446,7 +447,7 @@ void TC::count_deferred(const int32_t* s, const int32_t* d, int64_t m, const int
     }
     DBuf<int32_t> L(m, st), S(m, st);
     DBuf<int64_t> nch(m + 1, st), choff(m + 1, st);
-    GD_CUDA(cudaMemsetAsync(nch.get() + m, 0, sizeof(int64_t), st));
+    fill_d(st, nch.get() + m, 0, sizeof(int64_t));
     TcRec rr{L.get(), S.get(), nch.get()};
     DBuf<uint8_t> isshort(m, st);
     GD_KERNEL(k_tc_prep, grid_for(m, 256), 256, 0, st, s, d, m, ix.view(), rr, hubmark.get(), isshort.get(),
@@ -487,7 +488,7 @@ void TC::count_deferred(const int32_t* s, const int32_t* d, int64_t m, const int
     const int64_t hmax = std::min<int64_t>(nhubs, kBmBudget / (words * 4));
     if (hmax > 0 && bm.n < (size_t)(hmax * words)) {
         bm.alloc((size_t)(hmax * words), st);
-        GD_CUDA(cudaMemsetAsync(bm.get(), 0, bm.n * 4, st));
+        fill_d(st, bm.get(), 0, bm.n * 4);
         bm_multi.alloc(hmax, st);
         bm_multi.zero(st);
     }
@@ -550,6 +551,7 @@ void TC::batch(DevBatch& b, int64_t batch_index) {
         timer.begin(PH_MERGE);
         g->merge();
     }
+    struct_done();
     // OnAdd marks + counts on the post-add graph (tc_dynamic.sp:71-112)
     timer.begin(PH_PRE);
     count += count_records(b.as.get(), b.ad.get(), b.kadd);

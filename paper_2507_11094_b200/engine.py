@@ -209,6 +209,27 @@ class _Algo:
                                                                  C.c_void_p(dst_ptr), C.c_void_p(w_ptr), int(k),
                                                                  int(batch_index)))
 
+    def run_stream(self, arr: RecordArrays, batch_size: int, first_index: int = 0, *outs) -> None:
+        """run_batches over a whole record stream in one call (gd_*_run_stream):
+        batches of batch_size, batch j+1 uploaded and batch j-1's result read
+        back on a copy stream while batch j runs.  outs: PR rank float64[n];
+        SSSP dist, parent int64[n]; TC counts int64[number of batches] --
+        each holds the last batch's result on return (TC: every batch's)."""
+        a = arr.contiguous()
+        addr = lambda x: 0 if x is None else x.ctypes.data  # noqa: E731
+        self.run_stream_ptrs(addr(a.kind), addr(a.src), addr(a.dst), addr(a.weight), len(a), batch_size,
+                             first_index, *[addr(o) for o in outs])
+
+    def run_stream_ptrs(self, kind_ptr: int, src_ptr: int, dst_ptr: int, w_ptr: int, k: int, batch_size: int,
+                        first_index: int, *out_ptrs: int) -> None:
+        """run_stream over host pointers (uint8 kind, int64 src/dst/w; pinned
+        memory lets the copies overlap the batches)."""
+        want = {"pr": 1, "sssp": 2, "tc": 1}[self.kind]
+        outs = [C.c_void_p(p or None) for p in out_ptrs] + [C.c_void_p()] * (want - len(out_ptrs))
+        N.check(getattr(N.lib(), f"gd_{self.kind}_run_stream")(
+            self.h, C.c_void_p(kind_ptr), C.c_void_p(src_ptr), C.c_void_p(dst_ptr), C.c_void_p(w_ptr or None),
+            int(k), int(batch_size), int(first_index), *outs[:want]))
+
     def phase_ms(self) -> Dict[str, float]:
         ms = (C.c_double * 5)()
         N.check(N.lib().gd_phase_times(self.h, ms))
