@@ -581,7 +581,8 @@ def _static_compare(gd, torch, wl, args, local, n, s, d, w, kind, us, ud, uw, pe
 
 
 KERNELS = ("pr_pull", "pr_contrib", "tc_bitmap", "merge_copy", "flood_sample", "flood_rest", "flood_mark", "flood_link", "del_scan_head", "del_scan_tail",
-           "add_vacancies", "tc_count", "sssp_relax", "sssp_walk", "sssp_pull", "sssp_parent")
+           "add_vacancies", "index_claim", "index_ins_pos", "tc_count", "sssp_relax", "sssp_walk", "sssp_pull",
+           "sssp_parent")
 
 def _graph_stream(g):
     import ctypes as C

@@ -583,42 +583,73 @@ __global__ void k_add_arcs(const int32_t* s, const int32_t* d, const int32_t* w,
     }
 }
 
-// One warp per source row with inserts: list the first `want` vacancies of
-// the chain in slot order (ballot + prefix keeps the order).
-__global__ void k_add_vacancies(OutView ov, const uint32_t* skey, const int32_t* row_first, const int64_t* d_nrows,
-                                int64_t narcs, int64_t* vac_gid) {
-    const int lane = threadIdx.x & 31;
-    const int64_t nrows = *d_nrows;
-    int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t r = warp; r < nrows; r += nwarps) {
-        int64_t lo = row_first[r];
-        int64_t hi = (r + 1 < nrows) ? row_first[r + 1] : narcs;
-        int32_t row = (int32_t)skey[lo];
-        int64_t want = hi - lo, got = 0;
-        for (int sg = 0; sg < ov.nseg && got < want; ++sg) {
-            const int64_t* off = ov.off[sg];
-            const int32_t* col = ov.col[sg];
-            int64_t a = off[row], b = off[row + 1];
-            for (int64_t base = a; base < b && got < want; base += 32 * kScanILP) {
-                int32_t cv[kScanILP];
+// The vacancy scan with a group of 8 lanes per row (4 rows per warp in
+// flight): rows of a uniform graph hold ~30 slots, and a warp per row left
+// 3/4 of its lanes idle on the loads that bound the kernel.  A row whose
+// chain is longer than kVacShort slots (R-MAT hubs) is scanned by the whole
+// warp afterwards.  Same result: the first `want` vacancies in slot order.
+constexpr int kVacG = 8;
+constexpr int64_t kVacShort = 256;
+
+template <int W>
+__device__ __forceinline__ void vac_scan(const OutView& ov, int32_t row, int64_t lo, int64_t want, int l, int gb,
+                                         unsigned mask, int64_t* vac_gid) {
+    const unsigned lanes = W == 32 ? 0xffffffffu : ((1u << W) - 1);
+    const unsigned below = (1u << l) - 1;
+    int64_t got = 0;
+    for (int sg = 0; sg < ov.nseg && got < want; ++sg) {
+        const int64_t* off = ov.off[sg];
+        const int32_t* col = ov.col[sg];
+        const int64_t a = off[row], b = off[row + 1];
+        for (int64_t base = a; base < b && got < want; base += W * kScanILP) {
+            int32_t cv[kScanILP];
 #pragma unroll
-                for (int u = 0; u < kScanILP; ++u) {
-                    int64_t i = base + u * 32 + lane;
-                    cv[u] = i < b ? col[i] : 0;
-                }
-#pragma unroll
-                for (int u = 0; u < kScanILP; ++u) {
-                    int64_t i = base + u * 32 + lane;
-                    bool vac = (i < b) && cv[u] < 0;
-                    unsigned mask = __ballot_sync(0xffffffffu, vac);
-                    if (vac) {
-                        int64_t t = got + __popc(mask & ((1u << lane) - 1));
-                        if (t < want) vac_gid[lo + t] = ov.base[sg] + i;
-                    }
-                    got += __popc(mask);
-                }
+            for (int u = 0; u < kScanILP; ++u) {
+                const int64_t i = base + u * W + l;
+                cv[u] = i < b ? col[i] : 0;
             }
+#pragma unroll
+            for (int u = 0; u < kScanILP; ++u) {
+                const int64_t i = base + u * W + l;
+                const bool vac = i < b && cv[u] < 0;
+                const unsigned mk = (__ballot_sync(mask, vac) >> gb) & lanes;
+                if (vac) {
+                    const int64_t t = got + __popc(mk & below);
+                    if (t < want) vac_gid[lo + t] = ov.base[sg] + i;
+                }
+                got += __popc(mk);
+            }
+        }
+    }
+}
+
+template <int G>
+__global__ void k_add_vacancies_g(OutView ov, const uint32_t* skey, const int32_t* row_first,
+                                  const int64_t* d_nrows, int64_t narcs, int64_t* vac_gid) {
+    constexpr int kPer = 32 / G;
+    const int lane = threadIdx.x & 31, gl = lane & (G - 1), gb = lane & ~(G - 1);
+    const unsigned gmask = G == 32 ? 0xffffffffu : ((1u << G) - 1) << gb;
+    const int64_t nrows = *d_nrows;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t r0 = warp * kPer; r0 < nrows; r0 += nwarps * kPer) {  // warp-uniform trip count
+        const int64_t r = r0 + lane / G;
+        const bool valid = r < nrows;
+        int64_t lo = 0, want = 0, chain = 0;
+        int32_t row = 0;
+        if (valid) {
+            lo = row_first[r];
+            want = ((r + 1 < nrows) ? row_first[r + 1] : narcs) - lo;
+            row = (int32_t)skey[lo];
+            for (int sg = 0; sg < ov.nseg; ++sg) chain += ov.off[sg][row + 1] - ov.off[sg][row];
+        }
+        const bool lng = G < 32 && valid && chain > kVacShort;
+        if (valid && !lng) vac_scan<G>(ov, row, lo, want, gl, gb, gmask, vac_gid);
+        for (unsigned hm = __ballot_sync(0xffffffffu, lng && gl == 0); hm; hm &= hm - 1) {
+            const int src = __ffs(hm) - 1;
+            const int64_t hlo = __shfl_sync(0xffffffffu, lo, src), hwant = __shfl_sync(0xffffffffu, want, src);
+            const int32_t hrow = __shfl_sync(0xffffffffu, row, src);
+            vac_scan<32>(ov, hrow, hlo, hwant, lane, 0, 0xffffffffu, vac_gid);
         }
     }
 }
@@ -1148,6 +1179,9 @@ __device__ __forceinline__ void edit_window_vec(const int32_t* __restrict__ col,
 #ifndef GD_EDIT_VEC
 #define GD_EDIT_VEC 0
 #endif
+#ifndef GD_EDIT_META
+#define GD_EDIT_META 0
+#endif
 #ifndef GD_EDIT_MINB_U
 #define GD_EDIT_MINB_U 5
 #endif
@@ -1190,6 +1224,35 @@ __global__ void __launch_bounds__(kEditThreads, WEIGHTED ? GD_EDIT_MINB_W : GD_E
         return;
     }
 #endif
+#if GD_EDIT_META
+    if constexpr (A == 1) {
+        // metadata pipeline: the next window's ranges and insertions load
+        // while this window's entries are in flight.  Off by default: A/B on
+        // B200, C2 merge 0.263 -> 0.304 ms, C3 2.18 -> 2.35 ms per batch
+        WinMeta m0, m1;
+        if (w0 < nfull) {
+            win_meta_head(m0, w0, dead_win, pj_win);
+            win_meta_ins<WEIGHTED>(m0, w0, ipos, icol, iw);
+        }
+        for (int64_t win = w0; win < nfull; win += nwarps) {
+            int32_t v[Q], wv[Q];
+            edit_load<true, WEIGHTED>(col, w, nnz, win, v, wv);
+            const int64_t w1 = win + nwarps;
+            if (w1 < nfull) {
+                win_meta_head(m1, w1, dead_win, pj_win);
+                win_meta_ins<WEIGHTED>(m1, w1, ipos, icol, iw);
+            }
+            edit_store_p<WEIGHTED>(win, v, wv, m0, ipos, icol, iw, ocol, ow);
+            m0 = m1;
+        }
+        for (int64_t win = nfull + w0; win < nwin; win += nwarps) {
+            int32_t v[Q], wv[Q];
+            edit_load<false, WEIGHTED>(col, w, nnz, win, v, wv);
+            edit_store<WEIGHTED>(win, v, wv, dead_win, ipos, pj_win, icol, iw, ocol, ow);
+        }
+    } else
+#endif
+    {
     for (int64_t g = w0; g < ngrp; g += nwarps) {
         int32_t v[A][Q], wv[A][Q];
 #pragma unroll
@@ -1203,6 +1266,7 @@ __global__ void __launch_bounds__(kEditThreads, WEIGHTED ? GD_EDIT_MINB_W : GD_E
         if (win < nfull) edit_load<true, WEIGHTED>(col, w, nnz, win, v, wv);
         else edit_load<false, WEIGHTED>(col, w, nnz, win, v, wv);
         edit_store<WEIGHTED>(win, v, wv, dead_win, ipos, pj_win, icol, iw, ocol, ow);
+    }
     }
 }
 
@@ -1271,7 +1335,9 @@ void edit_apply(cudaStream_t s, EditJob& j, int64_t dead_total, DBuf<int64_t>& n
         GD_KERNEL(k_win_ins, grid_for(nwin + 1, 256), 256, 0, s, nwin, j.ipos, nins, pj.get());
         unsigned g = (unsigned)std::min<int64_t>(ntiles, 148LL * 64);
         // algorithmic bytes: every base entry read once, every surviving entry written once
-        static const int bulk_env = getenv("GD_EDIT_BULK") ? atoi(getenv("GD_EDIT_BULK")) : 1;
+        // the bulk-copy (TMA) variant is opt-in: A/B on B200 it ran 0.142 vs 0.129 ms per C2 launch and
+        // 1.24 vs 1.08 ms per C3 launch (profiles/round2/README.md)
+        static const int bulk_env = getenv("GD_EDIT_BULK") ? atoi(getenv("GD_EDIT_BULK")) : 0;
         const bool aligned = ((uintptr_t)j.col & 15) == 0 && (!j.weighted || ((uintptr_t)j.w & 15) == 0);
         if (bulk_env && aligned && nnz >= kTile) {
             const int smem = kBulkStages * kTile * 4 * (j.weighted ? 2 : 1);  // kTile = kWin per warp
@@ -1567,8 +1633,8 @@ void Store::index_plan(SortedIndex& ix, EditJob& j, DBuf<int64_t>& ipos) {
     cudaStream_t s = stream;
     ipos.alloc(ix.dnnz, s);
     if (ix.dnnz)
-        GD_KERNEL(k_index_ins_pos, grid_for(ix.dnnz, 256), 256, 0, s, ix.drow.get(), ix.dcol.get(), ix.dnnz,
-                  ix.off.get(), ix.col.get(), ipos.get());
+        GD_KERNEL_T("index_ins_pos", 0, k_index_ins_pos, grid_for(ix.dnnz, 256), 256, 0, s, ix.drow.get(),
+                    ix.dcol.get(), ix.dnnz, ix.off.get(), ix.col.get(), ipos.get());
     j = EditJob{n, ix.off.get(), ix.col.get(), ix.w.n ? ix.w.get() : nullptr, ix.nnz, ix.tpos.get(), ix.trow.get(),
                 ix.ntomb, false, ix.drow.get(), ix.dcol.get(), ix.dw.n ? ix.dw.get() : nullptr, ipos.get(), ix.dnnz,
                 weighted};
@@ -1612,9 +1678,10 @@ void Store::index_delete(SortedIndex& ix, const KilledArcs& ka) {
         copy_d2d(s, tpos.get(), ix.tpos.get(), old * 8);
         copy_d2d(s, trow.get(), ix.trow.get(), old * 4);
     }
-    GD_KERNEL(k_index_claim, grid_for(m, 256), 256, 0, s, ka.row.get(), ka.col.get(), ka.w.get(), ka.gid.get(), m,
-              ix.rows_are_dst, ix.off.get(), ix.col.get(), ix.w.n ? ix.w.get() : nullptr, tpos.get() + old,
-              trow.get() + old);
+    if (m)
+        GD_KERNEL_T("index_claim", 0, k_index_claim, grid_for(m, 256), 256, 0, s, ka.row.get(), ka.col.get(),
+                    ka.w.get(), ka.gid.get(), m, ix.rows_are_dst, ix.off.get(), ix.col.get(),
+                    ix.w.n ? ix.w.get() : nullptr, tpos.get() + old, trow.get() + old);
     ix.tpos = std::move(tpos);
     ix.trow = std::move(trow);
     ix.ntomb = old + m;
@@ -1942,7 +2009,12 @@ void Store::apply_adds_local(const int32_t* d_src, const int32_t* d_dst, const i
     DBuf<int64_t> vac(na, s);
     fill_i64(s, vac.get(), na, -1);
     OutView ov = out_view();
-    GD_KERNEL_T("add_vacancies", 0, k_add_vacancies, grid_for(na * 32, 256, 148LL * 32), 256, 0, s, ov, key.get(),
+    static const bool warp_rows = getenv("GD_WARP_ROWS") != nullptr;  // A/B: the round-1 warp-per-row kernels
+    if (warp_rows)
+        GD_KERNEL_T("add_vacancies", 0, k_add_vacancies_g<32>, grid_for(na * 32, 256, 148LL * 32), 256, 0, s, ov,
+                    key.get(), row_first.get(), d_nrows.get(), na, vac.get());
+    else
+    GD_KERNEL_T("add_vacancies", 0, k_add_vacancies_g<kVacG>, grid_for(na * kVacG, 256, 148LL * 32), 256, 0, s, ov, key.get(),
                 row_first.get(), d_nrows.get(), na, vac.get());
     DBuf<uint8_t> left(na, s);
     ClaimLog cl;
