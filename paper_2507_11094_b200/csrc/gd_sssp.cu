@@ -93,6 +93,7 @@ enum { FP_RELAX = 0, FP_WALK = 1, FP_PULL = 2 };
 constexpr int kHeavy = 256;  // arcs a group scans inline
 constexpr int kPiece = 128;  // arcs per piece (one warp, 4 per lane)
 constexpr int64_t kNearFarMinRounds = 256;  // static-pass rounds below which near-far is off
+constexpr int kChainDefault = 16;           // RELAX: near targets a group may follow per round
 
 struct FpArgs {
     OutView ov;
@@ -115,6 +116,9 @@ struct FpArgs {
     // thread sums its own loads and adds them once at exit
     long long* acc;
     int64_t cap;
+    // RELAX queue rounds: a group may follow up to `chain` near targets it
+    // lowered itself within the round (see fp_round)
+    int chain;
     // near-far (RELAX, delta > 0): relaxations landing at >= theta wait in a
     // far pile (3 rotating buffers, counters fcnt/fmin) until the near queue
     // drains; then a split round raises theta by delta and moves the pile's
@@ -181,7 +185,7 @@ __device__ __forceinline__ int64_t out_pre(const FpArgs& a, int32_t t) {
 
 template <int MODE>
 __device__ __forceinline__ void out_act(const FpArgs& a, const Round& r, int32_t v, int64_t dv, int32_t t, int32_t w,
-                                        int64_t pre) {
+                                        int64_t pre, int32_t* cand = nullptr) {
     if (t < 0) return;
     if (MODE == FP_RELAX) {
         int64_t c = sat_add(dv, (int64_t)w);
@@ -192,7 +196,10 @@ __device__ __forceinline__ void out_act(const FpArgs& a, const Round& r, int32_t
             } else if (c < old) {
                 if (a.flags) a.flags[t] = 1;
                 if (c < r.theta) {
-                    if (claim(a.stamp, t, r.id)) enqueue(r.qout, r.qcnt, t);
+                    // the lane's first lowered near target may be followed by
+                    // its own group this round instead of queued (fp_round)
+                    if (cand && *cand < 0) *cand = t;
+                    else if (claim(a.stamp, t, r.id)) enqueue(r.qout, r.qcnt, t);
                 } else {
                     // one hot word: read first, the pile's floor rarely drops
                     // (L1 bypassed: the slot is reset to INF between uses)
@@ -207,6 +214,7 @@ __device__ __forceinline__ void out_act(const FpArgs& a, const Round& r, int32_t
             a.parent[t] = -1;
             a.flags[t] = 1;
             if (ghost(a, t)) to_outbox(a, t);
+            else if (cand && *cand < 0) *cand = t;  // a child the group walks on this round
             else if (claim(a.stamp, t, r.id)) enqueue(r.qout, r.qcnt, t);
         }
     } else {
@@ -217,7 +225,7 @@ __device__ __forceinline__ void out_act(const FpArgs& a, const Round& r, int32_t
 // arcs [e0, e1) of segment sg, lanes strided by W, 4 arcs in flight per lane
 template <int MODE, int W>
 __device__ __forceinline__ void out_scan(const FpArgs& a, const Round& r, int32_t v, int64_t dv, int sg, int64_t e0,
-                                         int64_t e1, int lane, int64_t& nb) {
+                                         int64_t e1, int lane, int64_t& nb, int32_t* cand = nullptr) {
     const int32_t* col = a.ov.col[sg];
     const int32_t* wt = MODE == FP_RELAX ? a.ov.w[sg] : nullptr;
     // per slot: col, then weight + dist (relax), parent (walk) or flag (pull)
@@ -235,12 +243,12 @@ __device__ __forceinline__ void out_scan(const FpArgs& a, const Round& r, int32_
 #pragma unroll
         for (int j = 0; j < 4; ++j) pre[j] = out_pre<MODE>(a, t[j]);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) out_act<MODE>(a, r, v, dv, t[j], w[j], pre[j]);
+        for (int j = 0; j < 4; ++j) out_act<MODE>(a, r, v, dv, t[j], w[j], pre[j], cand);
     }
     for (; e < e1; e += W) {
         int32_t t = col[e];
         int32_t w = wt ? wt[e] : 1;
-        out_act<MODE>(a, r, v, dv, t, w, out_pre<MODE>(a, t));
+        out_act<MODE>(a, r, v, dv, t, w, out_pre<MODE>(a, t), cand);
     }
 }
 
@@ -248,7 +256,7 @@ __device__ __forceinline__ void out_scan(const FpArgs& a, const Round& r, int32_
 // else (once per round per vertex) as pieces for the next round
 template <int MODE, int W>
 __device__ __forceinline__ void out_visit(const FpArgs& a, const Round& r, int32_t v, int64_t dv, int lane,
-                                          int64_t& nb) {
+                                          int64_t& nb, int32_t* cand = nullptr) {
     const unsigned gm = group_mask<W>();
     const int leader = (threadIdx.x & 31) & ~(W - 1);
     int64_t deg = 0;
@@ -256,7 +264,7 @@ __device__ __forceinline__ void out_visit(const FpArgs& a, const Round& r, int32
     if (lane == 0) nb += 16 * a.ov.nseg;
     if (deg <= kHeavy) {
         for (int sg = 0; sg < a.ov.nseg; ++sg)
-            out_scan<MODE, W>(a, r, v, dv, sg, a.ov.off[sg][v], a.ov.off[sg][v + 1], lane, nb);
+            out_scan<MODE, W>(a, r, v, dv, sg, a.ov.off[sg][v], a.ov.off[sg][v + 1], lane, nb, cand);
         return;
     }
     int64_t np = 0;
@@ -357,9 +365,42 @@ __device__ __forceinline__ void fp_round(const FpArgs& a, const Round& r, const 
         if (lane == 0) nb += 4 + (MODE == FP_RELAX ? 8 : 0);  // queue entry, dist[v]
         if (MODE == FP_RELAX) {
             int64_t dv = a.dist[v];
-            if (dv < kInf) out_visit<MODE, kG>(a, r, v, dv, lane, nb);
+            // Chaining: after scanning v, the group follows one near target it
+            // lowered itself (the lowest lane's) within this round, up to
+            // a.chain times; the other lowered targets are queued as usual.
+            // A high-diameter graph (the grid) then advances several hops per
+            // grid barrier.  Relaxation is monotone and the followed vertex is
+            // not stamped, so a later, lower relaxation by another group still
+            // queues it: the least fixpoint is unchanged.
+            for (int depth = 0; dv < kInf; ++depth) {
+                int32_t cand = -1;
+                out_visit<MODE, kG>(a, r, v, dv, lane, nb, depth < a.chain ? &cand : nullptr);
+                const unsigned gm = group_mask<kG>();
+                const unsigned hm = __ballot_sync(gm, cand >= 0) & gm;
+                if (!hm) break;
+                const int src = __ffs(hm) - 1;
+                const int32_t nxt = __shfl_sync(gm, cand, src);
+                if (cand >= 0 && (int)(threadIdx.x & 31) != src && claim(a.stamp, cand, r.id))
+                    enqueue(r.qout, r.qcnt, cand);
+                v = nxt;
+                dv = a.dist[v];
+                if (lane == 0) nb += 8;
+            }
         } else if (MODE == FP_WALK) {
-            out_visit<MODE, kG>(a, r, v, 0, lane, nb);
+            // the same chaining down the tree: each vertex has one parent, so a
+            // followed child is visited once either way
+            for (int depth = 0;; ++depth) {
+                int32_t cand = -1;
+                out_visit<MODE, kG>(a, r, v, 0, lane, nb, depth < a.chain ? &cand : nullptr);
+                const unsigned gm = group_mask<kG>();
+                const unsigned hm = __ballot_sync(gm, cand >= 0) & gm;
+                if (!hm) break;
+                const int src = __ffs(hm) - 1;
+                const int32_t nxt = __shfl_sync(gm, cand, src);
+                if (cand >= 0 && (int)(threadIdx.x & 31) != src && claim(a.stamp, cand, r.id))
+                    enqueue(r.qout, r.qcnt, cand);
+                v = nxt;
+            }
         } else {
             int64_t s0 = a.ix.off[v], s1 = a.ix.off[v + 1];
             if (lane == 0) nb += 16 + 8;  // in-offsets, dist[v]
@@ -863,6 +904,14 @@ void SSSP::fixpoint(int mode, const int32_t* seeds, const int64_t* d_nseeds, int
     a.cnt = fr.cnt.get();
     a.ctr = ctr.get();
     a.cap = std::max<int64_t>(1, cap_factor * std::max<int64_t>(g->n, 1));  // ExecContext.iteration_cap
+    const int chain_env = getenv("GD_SSSP_CHAIN") ? atoi(getenv("GD_SSSP_CHAIN")) : kChainDefault;
+    // a followed hop saves a round, so rounds drop below the reference's
+    // sweeps; a cap below n (iteration_cap_factor 0) must still trip where
+    // the reference's does, so those fixpoints advance one hop per round
+    // chaining pays on deep graphs only (C4 grid: relax 25.6 -> 21.5 ms, walk
+    // 6.3 -> 4.9 ms per batch); on R-MAT (near-far off, delta == 0) it
+    // unbalanced the few wide rounds (relax 0.233 -> 0.246 ms)
+    a.chain = a.cap >= g->n && delta > 0 ? chain_env : 0;
     void* args[] = {&a};
     static const char* names[] = {"sssp_relax", "sssp_walk", "sssp_pull"};
     const void* fn = mode == FP_RELAX  ? (const void*)k_fixpoint<FP_RELAX>

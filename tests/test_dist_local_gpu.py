@@ -8,6 +8,8 @@ in-index, the flood, and PageRank (summation order of the dangling mass aside).
 
 from concurrent.futures import ThreadPoolExecutor
 
+import itertools
+
 import numpy as np
 import pytest
 
@@ -23,11 +25,14 @@ def gd():
     return gd
 
 
+_GROUP_IDS = itertools.count(1 << 20)
+
+
 def run_ranks(world, fn):
     """fn(rank, comm) on `world` threads sharing an in-process group."""
     from paper_2507_11094_b200.dist import Communicator
 
-    comms = Communicator.local_group(world, group=id(fn) & 0xFFFFFFF)
+    comms = Communicator.local_group(world, group=next(_GROUP_IDS))  # never reused while a group may live
     with ThreadPoolExecutor(world) as ex:
         futs = [ex.submit(fn, r, comms[r]) for r in range(world)]
         return [f.result(timeout=600) for f in futs]

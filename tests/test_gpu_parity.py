@@ -421,9 +421,10 @@ def test_sssp_fixpoints_count_their_bytes(gd):
     h.batch(RecordArrays(kind, us, ud, uw), 0)
     ms, nl, b = h.kernel_time("sssp_walk")
     assert nl == 1
-    # the walk visits the 63 invalidated vertices 1..63: at least a queue
-    # entry and one offset pair each, and 62 of them scan one slot (col + parent)
-    assert b >= 63 * (4 + 16) + 62 * 8
+    # the walk visits the 63 invalidated vertices 1..63: at least one
+    # offset pair each, and 62 of them scan one slot (col + parent); a
+    # queued vertex adds its queue entry, a followed one (chaining) does not
+    assert b >= 63 * 16 + 62 * 8
     ms, nl, b = h.kernel_time("sssp_relax")
     assert nl >= 1 and b > 0
     og = O.OracleGraph(n, src, dst, w, weighted=True, with_reverse=True, merge_interval=1)

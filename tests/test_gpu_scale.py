@@ -211,10 +211,14 @@ def test_tc_dynamic_equals_static_on_final_graph(gd, n, m, pct):
 
 
 @pytest.mark.parametrize("graph", ["rmat", "grid"])
-@pytest.mark.parametrize("delta,decr", [("0", "1"), ("0", "0"), ("7", "1"), ("100", "1"), ("5000", "1")])
-def test_sssp_near_far_width_does_not_change_results(gd, graph, delta, decr, monkeypatch):
-    """The near-far bucket width (GD_SSSP_DELTA; 0 = plain frontier) and the
-    decremental sweep+push it enables must reproduce the reference oracle."""
+@pytest.mark.parametrize("delta,decr,chain", [("0", "1", "16"), ("0", "0", "16"), ("7", "1", "16"), ("100", "1", "16"),
+                                              ("5000", "1", "16"), ("0", "1", "0"), ("100", "1", "0"),
+                                              ("100", "0", "1"), ("7", "1", "1000")])
+def test_sssp_near_far_width_does_not_change_results(gd, graph, delta, decr, chain, monkeypatch):
+    """The near-far bucket width (GD_SSSP_DELTA; 0 = plain frontier), the
+    decremental sweep+push it enables and the in-round chaining depth of the
+    relax and walk fixpoints (GD_SSSP_CHAIN; 0 = one hop per round) must
+    reproduce the reference oracle."""
     from oracle import oracle as O
     from paper_2507_11094_b200 import generate as G
 
@@ -225,6 +229,7 @@ def test_sssp_near_far_width_does_not_change_results(gd, graph, delta, decr, mon
     kind, us, ud, uw, per = G.updates(s, d, n, percent=10, batches=3, seed=4, max_weight=100)
     monkeypatch.setenv("GD_SSSP_DELTA", delta)
     monkeypatch.setenv("GD_SSSP_DECR", decr)  # 0: the pull fixpoint instead of sweep + push
+    monkeypatch.setenv("GD_SSSP_CHAIN", chain)
     g = gd.DynamicGraph.from_arrays(n, s, d, w, weighted=True, with_reverse=True)
     ctx = gd.run_batches(gd.shipped_program("sssp"), g, gd.UpdateStream.from_arrays(kind, us, ud, uw),
                          per, {"src": 0})
