@@ -31,15 +31,72 @@ constexpr int kG = 8;  // lanes per vertex
 constexpr int kPerWarp = 32 / kG;
 
 // warp-aggregated queue append over the currently converged lanes
-__device__ inline void enqueue(int32_t* q, unsigned long long* cnt, int32_t v) {
-    cg::coalesced_group g = cg::coalesced_threads();
-    unsigned long long base = 0;
-    if (g.thread_rank() == 0) base = atomicAdd(cnt, (unsigned long long)g.size());
-    base = g.shfl(base, 0);
-    q[base + g.thread_rank()] = v;
+__device__ inline bool claim(int32_t* stamp, int32_t v, int32_t round) { return atomicMax(&stamp[v], round) < round; }
+
+// Warp-buffered appends for the fixpoint rounds.  Every lowered target used
+// to take a slot of the next queue (or the far pile) with an atomicAdd on ONE
+// global counter; coalesced lanes share one, but a grid round still sent
+// ~10^5 same-address atomics to one L2 slice, which serialise there (C4: 27
+// M visits per batch in ~200 rounds of ~200 us).  Each warp now appends to
+// its own shared-memory buffer (a shared-memory atomic) and moves it to the
+// global queue with ONE global atomicAdd per flush: when it is nearly full
+// (checked between work items) and at the end of the round.  An append that
+// finds the buffer full goes to the global queue directly.  Queue order is
+// arbitrary in every fixpoint, so results do not change.
+constexpr int kQBuf = 512;
+constexpr int kQFlushAt = kQBuf - 128;
+__shared__ int32_t s_wq[kThreads / 32][2][kQBuf];
+__shared__ int s_wqn[kThreads / 32][2];
+
+__device__ __forceinline__ void wq_init() {
+    if ((threadIdx.x & 31) < 2) s_wqn[threadIdx.x >> 5][threadIdx.x & 31] = 0;
+    __syncwarp();
 }
 
-__device__ inline bool claim(int32_t* stamp, int32_t v, int32_t round) { return atomicMax(&stamp[v], round) < round; }
+// which = 0: the next queue (q, cnt), 1: the far pile
+__device__ __forceinline__ void enqueue_w(int which, int32_t* q, unsigned long long* cnt, int32_t v) {
+    cg::coalesced_group g = cg::coalesced_threads();
+    const int w = threadIdx.x >> 5;
+    int pos = 0;
+    if (g.thread_rank() == 0) pos = atomicAdd(&s_wqn[w][which], (int)g.size());
+    pos = g.shfl(pos, 0) + (int)g.thread_rank();
+    if (pos < kQBuf) {
+        s_wq[w][which][pos] = v;
+    } else {
+        cg::coalesced_group o = cg::coalesced_threads();
+        unsigned long long base = 0;
+        if (o.thread_rank() == 0) base = atomicAdd(cnt, (unsigned long long)o.size());
+        base = o.shfl(base, 0);
+        q[base + o.thread_rank()] = v;
+    }
+}
+
+// warp-convergent: move this warp's buffers to the global queue / pile
+__device__ __forceinline__ void wq_flush(int32_t* q0, unsigned long long* c0, int32_t* q1, unsigned long long* c1);
+// warp-convergent: flush when either buffer is nearly full
+__device__ __forceinline__ void wq_maybe_flush(int32_t* q0, unsigned long long* c0, int32_t* q1,
+                                               unsigned long long* c1) {
+    __syncwarp();
+    const int w = threadIdx.x >> 5;
+    if (s_wqn[w][0] >= kQFlushAt || s_wqn[w][1] >= kQFlushAt) wq_flush(q0, c0, q1, c1);
+}
+__device__ __forceinline__ void wq_flush(int32_t* q0, unsigned long long* c0, int32_t* q1, unsigned long long* c1) {
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    __syncwarp();
+#pragma unroll
+    for (int which = 0; which < 2; ++which) {
+        const int n = min(s_wqn[w][which], kQBuf);
+        if (n == 0) continue;
+        int32_t* q = which ? q1 : q0;
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(which ? c1 : c0, (unsigned long long)n);
+        base = __shfl_sync(0xffffffffu, base, 0);
+        for (int i = lane; i < n; i += 32) q[base + i] = s_wq[w][which][i];
+        __syncwarp();
+        if (lane == 0) s_wqn[w][which] = 0;
+        __syncwarp();
+    }
+}
 
 #define GROUP_LOOP_BEGIN(M)                                                      \
     const int lane = threadIdx.x & (kG - 1);                                     \
@@ -199,12 +256,12 @@ __device__ __forceinline__ void out_act(const FpArgs& a, const Round& r, int32_t
                     // the lane's first lowered near target may be followed by
                     // its own group this round instead of queued (fp_round)
                     if (cand && *cand < 0) *cand = t;
-                    else if (claim(a.stamp, t, r.id)) enqueue(r.qout, r.qcnt, t);
+                    else if (claim(a.stamp, t, r.id)) enqueue_w(0, r.qout, r.qcnt, t);
                 } else {
                     // one hot word: read first, the pile's floor rarely drops
                     // (L1 bypassed: the slot is reset to INF between uses)
                     if (c < __ldcg(r.ffmin)) atomicMin(r.ffmin, (long long)c);
-                    if (atomicExch(&a.infar[t], 1) == 0) enqueue(r.fout, r.ffcnt, t);
+                    if (atomicExch(&a.infar[t], 1) == 0) enqueue_w(1, r.fout, r.ffcnt, t);
                 }
             }
         }
@@ -215,10 +272,10 @@ __device__ __forceinline__ void out_act(const FpArgs& a, const Round& r, int32_t
             a.flags[t] = 1;
             if (ghost(a, t)) to_outbox(a, t);
             else if (cand && *cand < 0) *cand = t;  // a child the group walks on this round
-            else if (claim(a.stamp, t, r.id)) enqueue(r.qout, r.qcnt, t);
+            else if (claim(a.stamp, t, r.id)) enqueue_w(0, r.qout, r.qcnt, t);
         }
     } else {
-        if (pre && claim(a.stamp, t, r.id)) enqueue(r.qout, r.qcnt, t);
+        if (pre && claim(a.stamp, t, r.id)) enqueue_w(0, r.qout, r.qcnt, t);
     }
 }
 
@@ -343,6 +400,7 @@ __device__ __forceinline__ void fp_round(const FpArgs& a, const Round& r, const 
         int64_t dv = MODE == FP_RELAX ? a.dist[v] : 0;
         if (wl == 0) nb += 8 + 16 + (MODE == FP_RELAX ? 8 : 0);  // key, offsets, dist[v]
         if (MODE != FP_RELAX || dv < kInf) out_scan<MODE, 32>(a, r, v, dv, sg, e0, e1, wl, nb);
+        wq_maybe_flush(r.qout, r.qcnt, r.fout, r.ffcnt);
     }
     if (MODE == FP_PULL) {
         for (int64_t p = warp; p < mi; p += nwarps) {
@@ -355,6 +413,7 @@ __device__ __forceinline__ void fp_round(const FpArgs& a, const Round& r, const 
             if (wl == 0) nb += 8 + 16 + 8;  // key, offsets, dist[v]
             int64_t best = in_min<32>(a, e0, e1, wl, nb);
             if (lower<32>(a, v, best, wl)) out_visit<MODE, 32>(a, r, v, 0, wl, nb);
+            wq_maybe_flush(r.qout, r.qcnt, r.fout, r.ffcnt);
         }
     }
     // the queue: one group of kG lanes per vertex
@@ -381,7 +440,7 @@ __device__ __forceinline__ void fp_round(const FpArgs& a, const Round& r, const 
                 const int src = __ffs(hm) - 1;
                 const int32_t nxt = __shfl_sync(gm, cand, src);
                 if (cand >= 0 && (int)(threadIdx.x & 31) != src && claim(a.stamp, cand, r.id))
-                    enqueue(r.qout, r.qcnt, cand);
+                    enqueue_w(0, r.qout, r.qcnt, cand);
                 v = nxt;
                 dv = a.dist[v];
                 if (lane == 0) nb += 8;
@@ -398,7 +457,7 @@ __device__ __forceinline__ void fp_round(const FpArgs& a, const Round& r, const 
                 const int src = __ffs(hm) - 1;
                 const int32_t nxt = __shfl_sync(gm, cand, src);
                 if (cand >= 0 && (int)(threadIdx.x & 31) != src && claim(a.stamp, cand, r.id))
-                    enqueue(r.qout, r.qcnt, cand);
+                    enqueue_w(0, r.qout, r.qcnt, cand);
                 v = nxt;
             }
         } else {
@@ -416,6 +475,7 @@ __device__ __forceinline__ void fp_round(const FpArgs& a, const Round& r, const 
             }
         }
     }
+    wq_maybe_flush(r.qout, r.qcnt, r.fout, r.ffcnt);
     GROUP_LOOP_END
 }
 
@@ -423,7 +483,12 @@ __device__ __forceinline__ void fp_round(const FpArgs& a, const Round& r, const 
 // the next pile
 __device__ __forceinline__ void split_round(const FpArgs& a, const Round& r, const int32_t* src, int64_t F,
                                             int64_t& nb) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < F; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    // warp-uniform trip count, so the buffers can flush between steps
+    for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); i0 < F; i0 += stride) {
+        wq_maybe_flush(r.qout, r.qcnt, r.fout, r.ffcnt);
+        const int64_t i = i0 + (threadIdx.x & 31);
+        if (i >= F) continue;
         int32_t v = src[i];
         nb += 4 + 8;  // pile entry, dist[v]
         int64_t d = a.dist[v];
@@ -431,11 +496,11 @@ __device__ __forceinline__ void split_round(const FpArgs& a, const Round& r, con
             a.infar[v] = 0;
         } else if (d < r.theta) {
             a.infar[v] = 0;
-            if (claim(a.stamp, v, r.id)) enqueue(r.qout, r.qcnt, v);
+            if (claim(a.stamp, v, r.id)) enqueue_w(0, r.qout, r.qcnt, v);
         } else {
             a.infar[v] = 1;
             if (d < __ldcg(r.ffmin)) atomicMin(r.ffmin, (long long)d);
-            enqueue(r.fout, r.ffcnt, v);
+            enqueue_w(1, r.fout, r.ffcnt, v);
         }
     }
 }
@@ -451,6 +516,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_fixpoint(FpArgs a) {
     int nsplit = 0;  // pile = far[nsplit % 3]
     int64_t nb = 0;  // this thread's algorithmic bytes (a.acc only)
     int64_t it = 0;
+    wq_init();
     for (;; ++it) {
         const volatile unsigned long long* c = a.cnt + 3 * (it % 3);
         int64_t m = (int64_t)c[0];
@@ -495,6 +561,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_fixpoint(FpArgs a) {
                 a.q[nx], cn, a.ho[nx], cn + 1, a.hi[nx], cn + 2};
         if (split) split_round(a, r, it == 0 ? a.seeds : a.far[p], F, nb);
         else fp_round<MODE>(a, r, it == 0 ? a.seeds : a.q[it & 1], m, a.ho[it & 1], mo, a.hi[it & 1], mi, nb);
+        wq_flush(r.qout, r.qcnt, r.fout, r.ffcnt);
         grid.sync();
         if (split) ++nsplit;
     }
