@@ -107,6 +107,15 @@ __device__ __forceinline__ void wq_flush(int32_t* q0, unsigned long long* c0, in
         int64_t _t = _t0 + gw;                                                   \
         bool valid = _t < (M);
 #define GROUP_LOOP_END }
+// the same with a group width G (template parameter of the fixpoint)
+#define GROUP_LOOP_BEGIN_G(M, G)                                                          \
+    const int lane = threadIdx.x & ((G) - 1);                                             \
+    const int gw = (threadIdx.x & 31) / (G);                                              \
+    int64_t _warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;                \
+    int64_t _nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;                             \
+    for (int64_t _t0 = _warp * (32 / (G)); _t0 < (M); _t0 += _nwarps * (32 / (G))) {     \
+        int64_t _t = _t0 + gw;                                                            \
+        bool valid = _t < (M);
 
 __global__ void k_init(int64_t* dist, int32_t* parent, int32_t* stamp, int32_t* hstamp, int64_t n) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -382,7 +391,7 @@ __device__ __forceinline__ bool lower(const FpArgs& a, int32_t v, int64_t best, 
     return __shfl_sync(group_mask<W>(), changed, (threadIdx.x & 31) & ~(W - 1));
 }
 
-template <int MODE>
+template <int MODE, int G>
 __device__ __forceinline__ void fp_round(const FpArgs& a, const Round& r, const int32_t* qin, int64_t m,
                                          const int64_t* hoin, int64_t mo, const int64_t* hiin, int64_t mi,
                                          int64_t& nb) {
@@ -416,8 +425,8 @@ __device__ __forceinline__ void fp_round(const FpArgs& a, const Round& r, const 
             wq_maybe_flush(r.qout, r.qcnt, r.fout, r.ffcnt);
         }
     }
-    // the queue: one group of kG lanes per vertex
-    GROUP_LOOP_BEGIN(m)
+    // the queue: one group of G lanes per vertex
+    GROUP_LOOP_BEGIN_G(m, G)
     (void)gw;
     if (valid) {
         int32_t v = qin[_t];
@@ -433,8 +442,8 @@ __device__ __forceinline__ void fp_round(const FpArgs& a, const Round& r, const 
             // queues it: the least fixpoint is unchanged.
             for (int depth = 0; dv < kInf; ++depth) {
                 int32_t cand = -1;
-                out_visit<MODE, kG>(a, r, v, dv, lane, nb, depth < a.chain ? &cand : nullptr);
-                const unsigned gm = group_mask<kG>();
+                out_visit<MODE, G>(a, r, v, dv, lane, nb, depth < a.chain ? &cand : nullptr);
+                const unsigned gm = group_mask<G>();
                 const unsigned hm = __ballot_sync(gm, cand >= 0) & gm;
                 if (!hm) break;
                 const int src = __ffs(hm) - 1;
@@ -450,8 +459,8 @@ __device__ __forceinline__ void fp_round(const FpArgs& a, const Round& r, const 
             // followed child is visited once either way
             for (int depth = 0;; ++depth) {
                 int32_t cand = -1;
-                out_visit<MODE, kG>(a, r, v, 0, lane, nb, depth < a.chain ? &cand : nullptr);
-                const unsigned gm = group_mask<kG>();
+                out_visit<MODE, G>(a, r, v, 0, lane, nb, depth < a.chain ? &cand : nullptr);
+                const unsigned gm = group_mask<G>();
                 const unsigned hm = __ballot_sync(gm, cand >= 0) & gm;
                 if (!hm) break;
                 const int src = __ffs(hm) - 1;
@@ -467,11 +476,11 @@ __device__ __forceinline__ void fp_round(const FpArgs& a, const Round& r, const 
                 int64_t np = (s1 - s0 + kPiece - 1) / kPiece;
                 unsigned long long base = 0;
                 if (lane == 0) base = atomicAdd(r.hicnt, (unsigned long long)np);
-                base = __shfl_sync(group_mask<kG>(), base, (threadIdx.x & 31) & ~(kG - 1));
-                for (int64_t k = lane; k < np; k += kG) r.hiout[base + k] = piece_key(v, 0, k);
+                base = __shfl_sync(group_mask<G>(), base, (threadIdx.x & 31) & ~(G - 1));
+                for (int64_t k = lane; k < np; k += G) r.hiout[base + k] = piece_key(v, 0, k);
             } else {
-                int64_t best = in_min<kG>(a, s0, s1, lane, nb);
-                if (lower<kG>(a, v, best, lane)) out_visit<MODE, kG>(a, r, v, 0, lane, nb);
+                int64_t best = in_min<G>(a, s0, s1, lane, nb);
+                if (lower<G>(a, v, best, lane)) out_visit<MODE, G>(a, r, v, 0, lane, nb);
             }
         }
     }
@@ -505,8 +514,11 @@ __device__ __forceinline__ void split_round(const FpArgs& a, const Round& r, con
     }
 }
 
-template <int MODE>
-__global__ void __launch_bounds__(kThreads, 4) k_fixpoint(FpArgs a) {
+#ifndef GD_FP_RELAX_MINB
+#define GD_FP_RELAX_MINB 4
+#endif
+template <int MODE, int G>
+__global__ void __launch_bounds__(kThreads, MODE == FP_RELAX ? GD_FP_RELAX_MINB : 4) k_fixpoint(FpArgs a) {
     cg::grid_group grid = cg::this_grid();
     const bool leader = grid.thread_rank() == 0;
     const int32_t round0 = (int32_t)a.ctr[0];
@@ -560,7 +572,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_fixpoint(FpArgs a) {
         Round r{round0 + (int32_t)it + 1, theta, a.far[fo], a.fcnt + fo, a.fmin + fo,
                 a.q[nx], cn, a.ho[nx], cn + 1, a.hi[nx], cn + 2};
         if (split) split_round(a, r, it == 0 ? a.seeds : a.far[p], F, nb);
-        else fp_round<MODE>(a, r, it == 0 ? a.seeds : a.q[it & 1], m, a.ho[it & 1], mo, a.hi[it & 1], mi, nb);
+        else fp_round<MODE, G>(a, r, it == 0 ? a.seeds : a.q[it & 1], m, a.ho[it & 1], mo, a.hi[it & 1], mi, nb);
         wq_flush(r.qout, r.qcnt, r.fout, r.ffcnt);
         grid.sync();
         if (split) ++nsplit;
@@ -827,14 +839,14 @@ inline unsigned group_grid(int64_t m) { return grid_for(((m + kPerWarp - 1) / kP
 
 // co-resident grid for the cooperative fixpoint: <= 4 CTAs per SM keeps the
 // barrier cheap while leaving 32 warps per SM for latency hiding
-template <int MODE>
+template <int MODE, int G>
 unsigned coop_grid() {
     static unsigned g = 0;
     if (!g) {
         int dev = 0, sms = 0, nb = 0;
         GD_CUDA(cudaGetDevice(&dev));
         GD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        GD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_fixpoint<MODE>, kThreads, 0));
+        GD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_fixpoint<MODE, G>, kThreads, 0));
         if (nb < 1) throw GdError(GD_ERR_CUDA, "fixpoint kernel cannot be resident");
         int per = 4;
         if (const char* e = getenv("GD_FP_CTAS_PER_SM")) per = std::max(1, atoi(e));
@@ -919,6 +931,11 @@ SSSP::SSSP(Store* st, int64_t s, int64_t cap) : AlgoBase(ALGO_SSSP, st), src((in
     timer.end_all();
 }
 
+bool SSSP::narrow_groups() const {
+    if (const char* e = getenv("GD_SSSP_G")) return atoi(e) == 4;
+    return g->n > 0 && g->total_slots() <= 6 * g->n;
+}
+
 void SSSP::fixpoint(int mode, const int32_t* seeds, const int64_t* d_nseeds, int64_t nseeds, uint8_t* flags,
                     const uint8_t* only) {
     cudaStream_t s = stream();
@@ -981,11 +998,15 @@ void SSSP::fixpoint(int mode, const int32_t* seeds, const int64_t* d_nseeds, int
     a.chain = a.cap >= g->n && delta > 0 ? chain_env : 0;
     void* args[] = {&a};
     static const char* names[] = {"sssp_relax", "sssp_walk", "sssp_pull"};
-    const void* fn = mode == FP_RELAX  ? (const void*)k_fixpoint<FP_RELAX>
-                     : mode == FP_WALK ? (const void*)k_fixpoint<FP_WALK>
-                                       : (const void*)k_fixpoint<FP_PULL>;
-    unsigned grid = mode == FP_RELAX ? coop_grid<FP_RELAX>() : mode == FP_WALK ? coop_grid<FP_WALK>()
-                                                                               : coop_grid<FP_PULL>();
+    // 4 lanes per queued vertex on low-degree graphs (the grid: 4 arcs a
+    // vertex left half of an 8-lane group idle), 8 otherwise
+    const bool narrow = narrow_groups();
+    const void* fn = mode == FP_RELAX  ? (narrow ? (const void*)k_fixpoint<FP_RELAX, 4> : (const void*)k_fixpoint<FP_RELAX, 8>)
+                     : mode == FP_WALK ? (narrow ? (const void*)k_fixpoint<FP_WALK, 4> : (const void*)k_fixpoint<FP_WALK, 8>)
+                                       : (narrow ? (const void*)k_fixpoint<FP_PULL, 4> : (const void*)k_fixpoint<FP_PULL, 8>);
+    unsigned grid = mode == FP_RELAX  ? (narrow ? coop_grid<FP_RELAX, 4>() : coop_grid<FP_RELAX, 8>())
+                    : mode == FP_WALK ? (narrow ? coop_grid<FP_WALK, 4>() : coop_grid<FP_WALK, 8>())
+                                      : (narrow ? coop_grid<FP_PULL, 4>() : coop_grid<FP_PULL, 8>());
     int pi = prof_begin(names[mode], 0, s);
     // profiled launches sum their algorithmic bytes into a slot that
     // finish() reads with the round counters (no extra read-back)

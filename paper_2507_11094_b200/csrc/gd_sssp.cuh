@@ -47,6 +47,9 @@ struct SSSP : AlgoBase {
   private:
     // one cooperative launch per fixpoint (relax / walk / pull); the seed count
     // is read from d_nseeds on the device when given, else nseeds
+    // 4-lane vertex groups in the fixpoints when the mean out-degree is <= 6
+    // (GD_SSSP_G=4/8 overrides)
+    bool narrow_groups() const;
     void fixpoint(int mode, const int32_t* seeds, const int64_t* d_nseeds, int64_t nseeds, uint8_t* flags,
                   const uint8_t* only = nullptr);
     // list == nullptr: every node; d_m (device) overrides m, which bounds the grid

@@ -67,8 +67,8 @@ def full_summary(tag, rep):
           wr = float(row[h.index("dram__bytes_write.sum")]) * scale[units[h.index("dram__bytes_write.sum")]]
           key = ("pr_pull" if "k_pr_pull" in name else "merge_copy" if "k_edit_base" in name else
                  "del_scan_head" if "k_del_scan_head" in name else "del_scan_tail" if "k_del_scan_tail" in name else "pr_contrib" if "k_pr_contrib" in name else
-                 "flood_sample" if "k_aff_sample" in name else "sssp_relax" if "k_fixpoint<0>" in name else
-               "sssp_walk" if "k_fixpoint<1>" in name else "sssp_pull" if "k_fixpoint<2>" in name else
+                 "flood_sample" if "k_aff_sample" in name else "sssp_relax" if "k_fixpoint<0" in name else
+               "sssp_walk" if "k_fixpoint<1" in name else "sssp_pull" if "k_fixpoint<2" in name else
                "tc_count" if ("k_tc_count" in name or "k_tc_merge" in name) else name)
           traffic[f"{tag}/{key}"].append(rd + wr)
 tpath = os.path.join("profiles", "ncu_traffic.json")
