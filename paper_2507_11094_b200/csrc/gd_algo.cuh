@@ -3,6 +3,7 @@
 // weak-component flood.
 #pragma once
 
+#include <functional>
 #include <map>
 #include <memory>
 #include <string>
@@ -72,7 +73,16 @@ struct AlgoBase {
     // behind a tens-of-MB read-back.  stream_flush queues a pending one now.
     void stream_result(int par, int narr, const void* const* dev, void* const* host, const size_t* bytes);
     void stream_flush();
+    // The next batch's upload is queued at the same point, ahead of the
+    // read-back: an H2D copy running under the structural update held up
+    // CUB's memsets the same way.
+    std::function<void()> pending_upload;
     void struct_done() {
+        if (pending_upload) {
+            auto f = std::move(pending_upload);
+            pending_upload = nullptr;
+            f();
+        }
         if (has_pend) stream_flush();
     }
 

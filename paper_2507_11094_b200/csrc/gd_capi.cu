@@ -235,17 +235,28 @@ static int algo_run_stream(H* h, const uint8_t* kind, const int64_t* src, const 
             const int64_t o = j * bs, m = std::min(bs, k - o);
             a->upload_async((int)(j & 1), kind + o, src + o, dst + o, w ? w + o : nullptr, m);
         };
+        // GD_UPLOAD_EARLY=1: queue batch j+1's upload before batch j starts (A/B)
+        static const bool early = getenv("GD_UPLOAD_EARLY") != nullptr;
         try {
             up(0);
             for (int64_t j = 0; j < nb; ++j) {
-                if (j + 1 < nb) up(j + 1);
+                if (j + 1 < nb) {
+                    if (early) up(j + 1);
+                    else a->pending_upload = [&up, j] { up(j + 1); };  // at batch j's struct_done
+                }
                 const int64_t o = j * bs, m = std::min(bs, k - o);
                 gdb::DevBatch b;
                 a->stage_uploaded(b, (int)(j & 1), kind + o, src + o, dst + o, m);
                 a->batch(b, first + j);
+                if (a->pending_upload) {  // a batch that queued no structural update
+                    auto f = std::move(a->pending_upload);
+                    a->pending_upload = nullptr;
+                    f();
+                }
                 result(j);
             }
         } catch (...) {  // no copy may touch the caller's buffers after return
+            a->pending_upload = nullptr;
             a->stream_flush();
             cudaStreamSynchronize(a->stream());
             cudaStreamSynchronize(a->io_stream());

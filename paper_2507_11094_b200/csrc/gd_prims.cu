@@ -2,6 +2,8 @@
 // pool), small read-backs, fills, and the sort / scan / select primitives of
 // the store path: CUB by default, or the hand-written cooperative versions of
 // gd_sort.cu with -DGD_OWN_PRIMS=1.
+#include <atomic>
+#include <chrono>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -158,25 +160,58 @@ void copy_d2d(cudaStream_t s, void* dst, const void* src, size_t bytes) {
     GD_LAUNCH_CHECK();
 }
 
+namespace {
+// copy `bytes` into mapped host memory, then publish `seq` in the flag word
+// behind a system fence: the host sees the flag only after the data
+__global__ void k_read_small(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst, size_t n,
+                             volatile uint32_t* flag, uint32_t seq) {
+    for (size_t i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+    __syncwarp();
+    __threadfence_system();
+    if (threadIdx.x == 0) *flag = seq;
+}
+}  // namespace
+
 // Small reads land in mapped pinned memory written by a kernel, for the
 // same reason: a cudaMemcpy D2H would queue behind a concurrent read-back.
+// The host then spins on a sequence flag the kernel writes after the data
+// instead of waking from cudaStreamSynchronize (a device gap of ~20 us per
+// read-back in tools/timeline_host.py); after 2 s it falls back to the sync,
+// which also surfaces any error of the work queued before.
 void read_small(cudaStream_t s, void* host, const void* dev, size_t bytes) {
     constexpr size_t kCap = 4096;
-    static thread_local void* pin = nullptr;
+    static thread_local uint8_t* pin = nullptr;
     static thread_local void* dpin = nullptr;
+    static thread_local uint32_t seq = 0;
     if (bytes > kCap) {
         GD_CUDA(cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, s));
         GD_CUDA(cudaStreamSynchronize(s));
         return;
     }
     if (!pin) {
-        GD_CUDA(cudaHostAlloc(&pin, kCap, cudaHostAllocMapped | cudaHostAllocPortable));
-        GD_CUDA(cudaHostGetDevicePointer(&dpin, pin, 0));
+        void* p = nullptr;
+        GD_CUDA(cudaHostAlloc(&p, kCap + 64, cudaHostAllocMapped | cudaHostAllocPortable));
+        GD_CUDA(cudaHostGetDevicePointer(&dpin, p, 0));
+        pin = static_cast<uint8_t*>(p);
+        *reinterpret_cast<volatile uint32_t*>(pin + kCap) = 0;
     }
-    k_copy_bytes<<<1, 32, 0, s>>>(static_cast<const uint8_t*>(dev), static_cast<uint8_t*>(dpin), bytes);
+    volatile uint32_t* flag = reinterpret_cast<volatile uint32_t*>(pin + kCap);
+    const uint32_t want = ++seq ? seq : ++seq;  // never 0, the initial flag
+    k_read_small<<<1, 32, 0, s>>>(static_cast<const uint8_t*>(dev), static_cast<uint8_t*>(dpin), bytes,
+                                  reinterpret_cast<volatile uint32_t*>(static_cast<uint8_t*>(dpin) + kCap), want);
     count_launch();
     GD_LAUNCH_CHECK();
-    GD_CUDA(cudaStreamSynchronize(s));
+    static const bool sync_reads = getenv("GD_READ_SYNC") != nullptr;  // A/B: wake from cudaStreamSynchronize
+    if (sync_reads) GD_CUDA(cudaStreamSynchronize(s));
+    const auto t0 = std::chrono::steady_clock::now();
+    for (uint32_t spin = 0; *flag != want; ++spin) {
+        if ((spin & 1023) == 1023 && std::chrono::steady_clock::now() - t0 > std::chrono::seconds(2)) {
+            GD_CUDA(cudaStreamSynchronize(s));
+            if (*flag != want) throw GdError(GD_ERR_CUDA, "read_small: the device never published the value");
+            break;
+        }
+    }
+    std::atomic_thread_fence(std::memory_order_acquire);
     memcpy(host, pin, bytes);
 }
 
