@@ -543,13 +543,13 @@ void PR::batch(DevBatch& b, int64_t batch_index) {
     timer.begin(PH_STRUCT);
     g->apply_deletes(b.ds.get(), b.dd.get(), b.kdel, nullptr);
     g->apply_adds(b.as.get(), b.ad.get(), b.aw.get(), b.kadd);
-    struct_done();  // the last radix sort of the batch's structural update is queued
     // merge-if-due runs before the recompute: it does not change the live
     // multiset the recompute reads (interp.py:877-880 runs it after).
     if (g->merge_due(batch_index)) {
         timer.begin(PH_MERGE);
         g->merge();
     }
+    struct_done();
     timer.begin(PH_PROP);
     if (g->part) flood_weak_components_dist(*g, affected.get(), &prof);
     else flood_weak_components(*g, affected.get(), &prof);

@@ -1164,13 +1164,13 @@ void SSSP::batch_dist(DevBatch& b, int64_t batch_index) {
                           g->weighted, dist.get(), seed_add);
     timer.begin(PH_STRUCT);
     g->apply_adds(b.as.get(), b.ad.get(), b.aw.get(), b.kadd);
-    struct_done();  // the last radix sort of the batch's structural update is queued
     if (g->merge_due(batch_index)) {
         timer.begin(PH_MERGE);
         g->merge();
     } else {
         g->compact_rev();
     }
+    struct_done();
     // incrementalSSSP (sssp_dynamic.sp:101-130)
     timer.begin(PH_PROP);
     owned_list(seed_add, list.get(), nl.get());
@@ -1239,13 +1239,13 @@ void SSSP::batch(DevBatch& b, int64_t batch_index) {
                           g->weighted, dist.get(), seed_add);
     timer.begin(PH_STRUCT);
     g->apply_adds(b.as.get(), b.ad.get(), b.aw.get(), b.kadd);
-    struct_done();  // the last radix sort of the batch's structural update is queued
     if (g->merge_due(batch_index)) {  // before the recompute; same live multiset
         timer.begin(PH_MERGE);
         g->merge();
     } else {
         g->compact_rev();
     }
+    struct_done();
 
     // incrementalSSSP (sssp_dynamic.sp:101-130); touched starts as the seeds
     timer.begin(PH_PROP);

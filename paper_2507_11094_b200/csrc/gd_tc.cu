@@ -547,11 +547,11 @@ void TC::batch(DevBatch& b, int64_t batch_index) {
     timer.begin(PH_STRUCT);
     g->apply_deletes(b.ds.get(), b.dd.get(), b.kdel, nullptr);
     g->apply_adds(b.as.get(), b.ad.get(), b.aw.get(), b.kadd);
-    struct_done();  // the last radix sort of the batch's structural update is queued
     if (g->merge_due(batch_index)) {  // before the add count; same live multiset
         timer.begin(PH_MERGE);
         g->merge();
     }
+    struct_done();
     // OnAdd marks + counts on the post-add graph (tc_dynamic.sp:71-112)
     timer.begin(PH_PRE);
     count += count_records(b.as.get(), b.ad.get(), b.kadd);
