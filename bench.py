@@ -478,8 +478,11 @@ def run_ours(gd, torch, wl, args, steps, warmup, e2e_steps, world, rank, local, 
     algo.set_profiling(False)
 
     # ---- e2e: host buffers through the public C-ABI call, H2D + D2H inside ----------
+    # records as uint8 kinds and int32 ids in pinned memory (gd_*_run_stream32):
+    # ids of the B200 layout are < 2^31, and 4-byte ids halve the upload
     pin = {}
-    for nm, arr in (("kind", kind), ("src", us), ("dst", ud), ("w", uw)):
+    for nm, arr in (("kind", kind), ("src", us.astype(np.int32)), ("dst", ud.astype(np.int32)),
+                    ("w", uw.astype(np.int32))):
         t_ = torch.from_numpy(np.ascontiguousarray(arr)).pin_memory()
         pin[nm] = t_
     out_pin = torch.empty((2, n) if wl["algo"] == "sssp" else n,
@@ -497,7 +500,7 @@ def run_ours(gd, torch, wl, args, steps, warmup, e2e_steps, world, rank, local, 
     a0, b0 = e_start * per, min((e_start + e2e_steps) * per, len(kind))
     e_done = max(b0 - a0, 0)
     nsteps_e = (e_done + per - 1) // per
-    h2d = e_done * (1 + 8 + 8 + (8 if (wl["weighted"] or wl["algo"] == "sssp") else 0))  # w not uploaded when unused
+    h2d = e_done * (1 + 4 + 4 + (4 if (wl["weighted"] or wl["algo"] == "sssp") else 0))  # w not uploaded when unused
     d2h = nsteps_e * {"pr": 8 * n, "sssp": 16 * n, "tc": 8}[wl["algo"]]
     if dist_on:
         torch.distributed.barrier()
@@ -542,7 +545,7 @@ def run_ours(gd, torch, wl, args, steps, warmup, e2e_steps, world, rank, local, 
            "scaling": "strong" if shards else "weak",
            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d // max(nsteps_e, 1),
                    "d2h_bytes_per_step": d2h // max(nsteps_e, 1), "steps": nsteps_e,
-                   "ms_per_step": e2e_ms / max(nsteps_e, 1), "api": f"gd_{wl['algo']}_run_stream"},
+                   "ms_per_step": e2e_ms / max(nsteps_e, 1), "api": f"gd_{wl['algo']}_run_stream32"},
            "gpu_launches": int(launches), "roofline": roof,
            "kernels": {k_: {"ms_total": v[0], "launches": v[1], "share": v[0] / elapsed_ms,
                             "gbs": (v[2] / 1e9) / (v[0] / 1e3) if v[2] and v[0] else None}
@@ -616,8 +619,8 @@ def _host_stream(algo, wl, pin, a, k, per, first, out_pin):
     else:
         counts = np.zeros((k + per - 1) // per, dtype=np.int64)
         outs = (counts.ctypes.data,)
-    algo.run_stream_ptrs(pin["kind"].data_ptr() + a, pin["src"].data_ptr() + 8 * a, pin["dst"].data_ptr() + 8 * a,
-                         pin["w"].data_ptr() + 8 * a, k, per, first, *outs)
+    algo.run_stream_ptrs(pin["kind"].data_ptr() + a, pin["src"].data_ptr() + 4 * a, pin["dst"].data_ptr() + 4 * a,
+                         pin["w"].data_ptr() + 4 * a, k, per, first, *outs, ids32=True)
 
 
 def _ncu_traffic(wl, name):

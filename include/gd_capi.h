@@ -168,6 +168,11 @@ GD_API int gd_sssp_read_async(gd_sssp* s, int64_t* dist, int64_t* parent);
 GD_API int gd_sssp_run_stream(gd_sssp* s, const uint8_t* kind, const int64_t* src, const int64_t* dst,
                               const int64_t* w, int64_t k, int64_t batch_size, int64_t first_batch_index,
                               int64_t* dist, int64_t* parent);
+/* the same with int32 record ids (half the upload of int64 ids: ids of the
+ * B200 layout are < 2^31 anyway) */
+GD_API int gd_sssp_run_stream32(gd_sssp* s, const uint8_t* kind, const int32_t* src, const int32_t* dst,
+                                const int32_t* w, int64_t k, int64_t batch_size, int64_t first_batch_index,
+                                int64_t* dist, int64_t* parent);
 GD_API int gd_sssp_destroy(gd_sssp* s);
 
 /* ---- dynamic PageRank: programs/pr_dynamic.sp:7-102 --------------------- */
@@ -187,6 +192,9 @@ GD_API int gd_pr_rank_device(gd_pr* p, const double** rank);
 /* as gd_sssp_run_stream; rank (nullable) receives every batch's ranks */
 GD_API int gd_pr_run_stream(gd_pr* p, const uint8_t* kind, const int64_t* src, const int64_t* dst, const int64_t* w,
                             int64_t k, int64_t batch_size, int64_t first_batch_index, double* rank);
+GD_API int gd_pr_run_stream32(gd_pr* p, const uint8_t* kind, const int32_t* src, const int32_t* dst,
+                              const int32_t* w, int64_t k, int64_t batch_size, int64_t first_batch_index,
+                              double* rank);
 GD_API int gd_pr_destroy(gd_pr* p);
 
 /* ---- dynamic triangle counting: programs/tc_dynamic.sp:7-115 ------------ */
@@ -200,6 +208,9 @@ GD_API int gd_tc_read(gd_tc* t, int64_t* count);
  * one int64 per batch */
 GD_API int gd_tc_run_stream(gd_tc* t, const uint8_t* kind, const int64_t* src, const int64_t* dst, const int64_t* w,
                             int64_t k, int64_t batch_size, int64_t first_batch_index, int64_t* counts);
+GD_API int gd_tc_run_stream32(gd_tc* t, const uint8_t* kind, const int32_t* src, const int32_t* dst,
+                              const int32_t* w, int64_t k, int64_t batch_size, int64_t first_batch_index,
+                              int64_t* counts);
 GD_API int gd_tc_destroy(gd_tc* t);
 
 /* ---- multi-GPU (one process per GPU).  NCCL is loaded on

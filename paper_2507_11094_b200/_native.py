@@ -83,6 +83,9 @@ SIGNATURES = [
     ("gd_pr_run_stream", C.c_int, [vp, vp, vp, vp, vp, i64, i64, i64, vp]),
     ("gd_sssp_run_stream", C.c_int, [vp, vp, vp, vp, vp, i64, i64, i64, vp, vp]),
     ("gd_tc_run_stream", C.c_int, [vp, vp, vp, vp, vp, i64, i64, i64, vp]),
+    ("gd_pr_run_stream32", C.c_int, [vp, vp, vp, vp, vp, i64, i64, i64, vp]),
+    ("gd_sssp_run_stream32", C.c_int, [vp, vp, vp, vp, vp, i64, i64, i64, vp, vp]),
+    ("gd_tc_run_stream32", C.c_int, [vp, vp, vp, vp, vp, i64, i64, i64, vp]),
     ("gd_wait", C.c_int, [vp]),
     ("gd_comm_reset_stats", C.c_int, [vp]),
     ("gd_prim_sort", C.c_int, [C.c_int, vp, vp, i64, C.c_int, C.c_int]),

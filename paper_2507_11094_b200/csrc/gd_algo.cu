@@ -10,7 +10,8 @@ namespace {
 // validation bits
 constexpr int kBadKind = 1, kBadNode = 2, kBadWeight = 4;
 
-__global__ void k_stage_host(const uint8_t* kind, const int64_t* s64, const int64_t* d64, const int64_t* w64,
+template <typename T>  // host record ids: int64 (the C ABI) or int32 (the *_run_stream32 entry points)
+__global__ void k_stage_host(const uint8_t* kind, const T* s64, const T* d64, const T* w64,
                              int64_t k, int64_t n, int32_t* s, int32_t* d, int32_t* w, uint8_t* isdel,
                              uint8_t* isadd, int* err, unsigned long long* bad_index) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < k; i += (int64_t)gridDim.x * blockDim.x) {
@@ -151,20 +152,28 @@ void AlgoBase::stage_host(DevBatch& b, const uint8_t* kind, const int64_t* src, 
     GD_CUDA(cudaMemcpyAsync(h_stage.get() + k, dst, k * 8, cudaMemcpyHostToDevice, st));
     if (w) GD_CUDA(cudaMemcpyAsync(h_stage.get() + 2 * k, w, k * 8, cudaMemcpyHostToDevice, st));
     GD_CUDA(cudaMemcpyAsync(k_stage.get(), kind, k, cudaMemcpyHostToDevice, st));
-    stage_records(b, k_stage.get(), h_stage.get(), w ? h_stage.get() + 2 * k : nullptr, k, kind, src, dst);
+    stage_records(b, k_stage.get(), h_stage.get(), h_stage.get() + k, w ? h_stage.get() + 2 * k : nullptr, 8, k,
+                  kind, src, dst);
 }
 
-// validate + split records already on the device as int64 (src | dst at d64, d64 + k)
-void AlgoBase::stage_records(DevBatch& b, const uint8_t* dkind, const int64_t* d64, const int64_t* w64, int64_t k,
-                             const uint8_t* kind, const int64_t* src, const int64_t* dst) {
+// validate + split records already on the device as `width`-byte ids
+void AlgoBase::stage_records(DevBatch& b, const uint8_t* dkind, const void* dsrc, const void* ddst, const void* dw,
+                             int width, int64_t k, const uint8_t* kind, const void* src, const void* dst) {
     cudaStream_t st = stream();
     DBuf<int32_t> s(k, st), d(k, st), ww(k, st);
     DBuf<uint8_t> flags(2 * k, st);
     DBuf<int64_t> hdr(4, st);  // err, bad index, kdel, kadd
     fill_d(st, hdr.get(), 0, 16);
-    GD_KERNEL(k_stage_host, grid_for(k, 256), 256, 0, st, dkind, d64, d64 + k, w64, k, g->n, s.get(), d.get(),
-              ww.get(), flags.get(), flags.get() + k, reinterpret_cast<int*>(hdr.get()),
-              reinterpret_cast<unsigned long long*>(hdr.get() + 1));
+    if (width == 8)
+        GD_KERNEL(k_stage_host<int64_t>, grid_for(k, 256), 256, 0, st, dkind, static_cast<const int64_t*>(dsrc),
+                  static_cast<const int64_t*>(ddst), static_cast<const int64_t*>(dw), k, g->n, s.get(), d.get(),
+                  ww.get(), flags.get(), flags.get() + k, reinterpret_cast<int*>(hdr.get()),
+                  reinterpret_cast<unsigned long long*>(hdr.get() + 1));
+    else
+        GD_KERNEL(k_stage_host<int32_t>, grid_for(k, 256), 256, 0, st, dkind, static_cast<const int32_t*>(dsrc),
+                  static_cast<const int32_t*>(ddst), static_cast<const int32_t*>(dw), k, g->n, s.get(), d.get(),
+                  ww.get(), flags.get(), flags.get() + k, reinterpret_cast<int*>(hdr.get()),
+                  reinterpret_cast<unsigned long long*>(hdr.get() + 1));
     DBuf<int32_t> sel_del(k, st), sel_add(k, st);
     select_flagged_index_async(st, flags.get(), k, sel_del.get(), hdr.get() + 2);
     select_flagged_index_async(st, flags.get() + k, k, sel_add.get(), hdr.get() + 3);
@@ -173,7 +182,10 @@ void AlgoBase::stage_records(DevBatch& b, const uint8_t* dkind, const int64_t* d
     int e = (int)(h[0] & 0xffffffff);
     if (e) {
         unsigned long long i = ~(unsigned long long)h[1];
-        raise_validation(e, i, g->n, (char)kind[i], src[i], dst[i]);
+        auto at = [&](const void* p) {
+            return width == 8 ? static_cast<const int64_t*>(p)[i] : (int64_t) static_cast<const int32_t*>(p)[i];
+        };
+        raise_validation(e, i, g->n, (char)kind[i], at(src), at(dst));
     }
     split(b, sel_del.get(), sel_add.get(), s.get(), d.get(), ww.get(), h[2], h[3]);
 }
@@ -198,18 +210,19 @@ void AlgoBase::reserve_uploads(int64_t k) {
     GD_CUDA(cudaStreamSynchronize(st));  // the slots exist before the copy stream writes them
 }
 
-void AlgoBase::upload_async(int slot, const uint8_t* kind, const int64_t* src, const int64_t* dst, const int64_t* w,
+void AlgoBase::upload_async(int slot, const uint8_t* kind, const void* src, const void* dst, const void* w, int width,
                             int64_t k) {
     cudaStream_t io = io_stream();
     if (!g->weighted && this->kind != ALGO_SSSP) w = nullptr;
     up_w[slot] = w != nullptr;
+    up_width[slot] = width;
     if (k == 0) return;
     // the slot's previous batch has been staged (its buffers are free)
     GD_CUDA(cudaStreamWaitEvent(io, ev_staged[slot], 0));
-    int64_t* u = up64[slot].get();
-    GD_CUDA(cudaMemcpyAsync(u, src, k * 8, cudaMemcpyHostToDevice, io));
-    GD_CUDA(cudaMemcpyAsync(u + k, dst, k * 8, cudaMemcpyHostToDevice, io));
-    if (w) GD_CUDA(cudaMemcpyAsync(u + 2 * k, w, k * 8, cudaMemcpyHostToDevice, io));
+    char* u = reinterpret_cast<char*>(up64[slot].get());  // src | dst | w, k ids of `width` bytes each
+    GD_CUDA(cudaMemcpyAsync(u, src, k * width, cudaMemcpyHostToDevice, io));
+    GD_CUDA(cudaMemcpyAsync(u + k * width, dst, k * width, cudaMemcpyHostToDevice, io));
+    if (w) GD_CUDA(cudaMemcpyAsync(u + 2 * k * width, w, k * width, cudaMemcpyHostToDevice, io));
     GD_CUDA(cudaMemcpyAsync(upk[slot].get(), kind, k, cudaMemcpyHostToDevice, io));
     GD_CUDA(cudaEventRecord(ev_up[slot], io));
 }
@@ -250,16 +263,18 @@ void AlgoBase::stream_flush() {
     GD_CUDA(cudaEventRecord(ev_scopied[par], io));
 }
 
-void AlgoBase::stage_uploaded(DevBatch& b, int slot, const uint8_t* h_kind, const int64_t* h_src,
-                              const int64_t* h_dst, int64_t k) {
+void AlgoBase::stage_uploaded(DevBatch& b, int slot, const uint8_t* h_kind, const void* h_src, const void* h_dst,
+                              int64_t k) {
     cudaStream_t st = stream();
     if (k == 0) {
         b.kdel = b.kadd = 0;
         return;
     }
     GD_CUDA(cudaStreamWaitEvent(st, ev_up[slot], 0));
-    int64_t* u = up64[slot].get();
-    stage_records(b, upk[slot].get(), u, up_w[slot] ? u + 2 * k : nullptr, k, h_kind, h_src, h_dst);
+    const int width = up_width[slot];
+    const char* u = reinterpret_cast<const char*>(up64[slot].get());
+    stage_records(b, upk[slot].get(), u, u + k * width, up_w[slot] ? u + 2 * k * width : nullptr, width, k, h_kind,
+                  h_src, h_dst);
     GD_CUDA(cudaEventRecord(ev_staged[slot], st));
 }
 

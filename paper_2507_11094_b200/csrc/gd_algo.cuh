@@ -55,12 +55,13 @@ struct AlgoBase {
     // stream also carries the result read-backs, so each direction's copy
     // runs alone: D2H(j-1) then H2D(j+1), both behind batch j's compute.
     void reserve_uploads(int64_t k);  // both slots sized for k records
-    void upload_async(int slot, const uint8_t* kind, const int64_t* src, const int64_t* dst, const int64_t* w,
+    // ids of `width` bytes (8: int64, 4: int32)
+    void upload_async(int slot, const uint8_t* kind, const void* src, const void* dst, const void* w, int width,
                       int64_t k);
     // stage_host's second half on an uploaded slot: the handle's stream
     // waits for the upload, then validates and splits (host arrays only feed
     // the error message)
-    void stage_uploaded(DevBatch& b, int slot, const uint8_t* h_kind, const int64_t* h_src, const int64_t* h_dst,
+    void stage_uploaded(DevBatch& b, int slot, const uint8_t* h_kind, const void* h_src, const void* h_dst,
                         int64_t k);
     cudaStream_t io_stream();
 
@@ -91,11 +92,12 @@ struct AlgoBase {
                const int32_t* w, int64_t kdel, int64_t kadd);
     DBuf<int64_t> h_stage;  // reusable device staging for host uploads
     DBuf<uint8_t> k_stage;
-    void stage_records(DevBatch& b, const uint8_t* dkind, const int64_t* d64, const int64_t* w64, int64_t k,
-                       const uint8_t* h_kind, const int64_t* h_src, const int64_t* h_dst);
+    void stage_records(DevBatch& b, const uint8_t* dkind, const void* dsrc, const void* ddst, const void* dw,
+                       int width, int64_t k, const uint8_t* h_kind, const void* h_src, const void* h_dst);
     DBuf<int64_t> up64[2];  // run_stream upload slots: src | dst | w
     DBuf<uint8_t> upk[2];
     bool up_w[2] = {false, false};
+    int up_width[2] = {8, 8};
     cudaEvent_t ev_up[2] = {nullptr, nullptr}, ev_staged[2] = {nullptr, nullptr};
     DBuf<uint8_t> ssnap[2][2];  // [batch parity][result array]
     cudaEvent_t ev_sready[2] = {nullptr, nullptr}, ev_scopied[2] = {nullptr, nullptr};

@@ -219,8 +219,8 @@ static int algo_batch_dev(H* h, const uint8_t* kind, const int32_t* src, const i
 // The copy stream carries, in order, up(0), up(1), then per batch j:
 // D2H(j) after batch j, then up(j+2) -- so each copy runs alone on the link,
 // and both hide behind the next batch's compute.
-template <typename H, typename R>
-static int algo_run_stream(H* h, const uint8_t* kind, const int64_t* src, const int64_t* dst, const int64_t* w,
+template <typename H, typename T, typename R>
+static int algo_run_stream(H* h, const uint8_t* kind, const T* src, const T* dst, const T* w,
                            int64_t k, int64_t bs, int64_t first, R&& result) {
     if (!h) return null_handle();
     return guard([&] {
@@ -233,7 +233,7 @@ static int algo_run_stream(H* h, const uint8_t* kind, const int64_t* src, const 
         a->reserve_uploads(std::min(bs, k));
         auto up = [&](int64_t j) {
             const int64_t o = j * bs, m = std::min(bs, k - o);
-            a->upload_async((int)(j & 1), kind + o, src + o, dst + o, w ? w + o : nullptr, m);
+            a->upload_async((int)(j & 1), kind + o, src + o, dst + o, w ? w + o : nullptr, (int)sizeof(T), m);
         };
         // GD_UPLOAD_EARLY=1: queue batch j+1's upload before batch j starts (A/B)
         static const bool early = getenv("GD_UPLOAD_EARLY") != nullptr;
@@ -532,8 +532,10 @@ int gd_wait(const void* h) {
     if (!h) return null_handle();
     return guard([&] { algo_of(h)->wait_copies(); });
 }
-int gd_sssp_run_stream(gd_sssp* s, const uint8_t* kind, const int64_t* src, const int64_t* dst, const int64_t* w,
-                       int64_t k, int64_t batch_size, int64_t first_batch_index, int64_t* dist, int64_t* parent) {
+}  // extern "C"
+template <typename T>
+static int sssp_run_stream(gd_sssp* s, const uint8_t* kind, const T* src, const T* dst, const T* w, int64_t k,
+                           int64_t batch_size, int64_t first_batch_index, int64_t* dist, int64_t* parent) {
     return algo_run_stream(s, kind, src, dst, w, k, batch_size, first_batch_index, [&](int64_t j) {
         if (!dist && !parent) return;
         const void* dev[2];
@@ -553,6 +555,15 @@ int gd_sssp_run_stream(gd_sssp* s, const uint8_t* kind, const int64_t* src, cons
         }
         s->a->stream_result((int)(j & 1), na, dev, host, bytes);
     });
+}
+extern "C" {
+int gd_sssp_run_stream(gd_sssp* s, const uint8_t* kind, const int64_t* src, const int64_t* dst, const int64_t* w,
+                       int64_t k, int64_t batch_size, int64_t first_batch_index, int64_t* dist, int64_t* parent) {
+    return sssp_run_stream(s, kind, src, dst, w, k, batch_size, first_batch_index, dist, parent);
+}
+int gd_sssp_run_stream32(gd_sssp* s, const uint8_t* kind, const int32_t* src, const int32_t* dst, const int32_t* w,
+                         int64_t k, int64_t batch_size, int64_t first_batch_index, int64_t* dist, int64_t* parent) {
+    return sssp_run_stream(s, kind, src, dst, w, k, batch_size, first_batch_index, dist, parent);
 }
 int gd_sssp_destroy(gd_sssp* s) {
     if (!s) return ok();
@@ -607,8 +618,10 @@ int gd_pr_rank_device(gd_pr* p, const double** rank) {
         *rank = p->a->rank.get();
     });
 }
-int gd_pr_run_stream(gd_pr* p, const uint8_t* kind, const int64_t* src, const int64_t* dst, const int64_t* w,
-                     int64_t k, int64_t batch_size, int64_t first_batch_index, double* rank) {
+}  // extern "C"
+template <typename T>
+static int pr_run_stream(gd_pr* p, const uint8_t* kind, const T* src, const T* dst, const T* w, int64_t k,
+                         int64_t batch_size, int64_t first_batch_index, double* rank) {
     return algo_run_stream(p, kind, src, dst, w, k, batch_size, first_batch_index, [&](int64_t j) {
         if (!rank) return;
         p->a->gather();
@@ -617,6 +630,15 @@ int gd_pr_run_stream(gd_pr* p, const uint8_t* kind, const int64_t* src, const in
         const size_t bytes[1] = {(size_t)p->a->g->n * 8};
         p->a->stream_result((int)(j & 1), 1, dev, host, bytes);
     });
+}
+extern "C" {
+int gd_pr_run_stream(gd_pr* p, const uint8_t* kind, const int64_t* src, const int64_t* dst, const int64_t* w,
+                     int64_t k, int64_t batch_size, int64_t first_batch_index, double* rank) {
+    return pr_run_stream(p, kind, src, dst, w, k, batch_size, first_batch_index, rank);
+}
+int gd_pr_run_stream32(gd_pr* p, const uint8_t* kind, const int32_t* src, const int32_t* dst, const int32_t* w,
+                       int64_t k, int64_t batch_size, int64_t first_batch_index, double* rank) {
+    return pr_run_stream(p, kind, src, dst, w, k, batch_size, first_batch_index, rank);
 }
 int gd_pr_destroy(gd_pr* p) {
     if (!p) return ok();
@@ -644,6 +666,12 @@ int gd_tc_read(gd_tc* t, int64_t* count) {
 }
 int gd_tc_run_stream(gd_tc* t, const uint8_t* kind, const int64_t* src, const int64_t* dst, const int64_t* w,
                      int64_t k, int64_t batch_size, int64_t first_batch_index, int64_t* counts) {
+    return algo_run_stream(t, kind, src, dst, w, k, batch_size, first_batch_index, [&](int64_t j) {
+        if (counts) counts[j] = t->a->count;
+    });
+}
+int gd_tc_run_stream32(gd_tc* t, const uint8_t* kind, const int32_t* src, const int32_t* dst, const int32_t* w,
+                       int64_t k, int64_t batch_size, int64_t first_batch_index, int64_t* counts) {
     return algo_run_stream(t, kind, src, dst, w, k, batch_size, first_batch_index, [&](int64_t j) {
         if (counts) counts[j] = t->a->count;
     });

@@ -221,12 +221,13 @@ class _Algo:
                              first_index, *[addr(o) for o in outs])
 
     def run_stream_ptrs(self, kind_ptr: int, src_ptr: int, dst_ptr: int, w_ptr: int, k: int, batch_size: int,
-                        first_index: int, *out_ptrs: int) -> None:
-        """run_stream over host pointers (uint8 kind, int64 src/dst/w; pinned
-        memory lets the copies overlap the batches)."""
+                        first_index: int, *out_ptrs: int, ids32: bool = False) -> None:
+        """run_stream over host pointers (uint8 kind, int64 src/dst/w, or
+        int32 with ids32 -- half the upload; pinned memory lets the copies
+        overlap the batches)."""
         want = {"pr": 1, "sssp": 2, "tc": 1}[self.kind]
         outs = [C.c_void_p(p or None) for p in out_ptrs] + [C.c_void_p()] * (want - len(out_ptrs))
-        N.check(getattr(N.lib(), f"gd_{self.kind}_run_stream")(
+        N.check(getattr(N.lib(), f"gd_{self.kind}_run_stream{'32' if ids32 else ''}")(
             self.h, C.c_void_p(kind_ptr), C.c_void_p(src_ptr), C.c_void_p(dst_ptr), C.c_void_p(w_ptr or None),
             int(k), int(batch_size), int(first_index), *outs[:want]))
 

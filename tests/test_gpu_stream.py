@@ -118,3 +118,44 @@ def test_run_stream_bad_batch_raises_after_earlier_batches(gd):
     pr.run_stream(arr.slice(2 * bs, 3 * bs), bs, 2, None)
     pr2.batch(arr.slice(2 * bs, 3 * bs), 2)
     np.testing.assert_array_equal(pr.read()[0], pr2.read()[0])
+
+
+@pytest.mark.parametrize("algo", ["pr", "sssp", "tc"])
+def test_run_stream32_equals_int64_records(gd, algo):
+    """gd_*_run_stream32 (int32 host ids, half the upload) gives the int64
+    call's results, and its validation reports the same bad record."""
+    from paper_2507_11094_b200.errors import ExecError
+
+    rng = np.random.default_rng(17)
+    n = 1 << 10
+    src, dst, w = rmat(10, 8 * n, rng)
+    bs = 300
+    kind, us, ud, uw = updates(rng, n, src, dst, 3 * bs + 7, distinct_deletes=True)
+    k = len(kind)
+
+    def make():
+        if algo == "pr":
+            g = gd.DynamicGraph.from_arrays(n, src, dst, with_reverse=True)
+            return gd.PRHandle(g, 0.85, 1e-10, 100), [np.zeros(n, np.float64)]
+        if algo == "sssp":
+            g = gd.DynamicGraph.from_arrays(n, src, dst, w, weighted=True, with_reverse=True)
+            return gd.SSSPHandle(g, 1), [np.zeros(n, np.int64), np.zeros(n, np.int64)]
+        g = gd.DynamicGraph.from_arrays(n, src, dst, directed=False)
+        return gd.TCHandle(g), [np.zeros((k + bs - 1) // bs, np.int64)]
+
+    kd = np.ascontiguousarray(kind.astype(np.uint8))
+    a64 = [np.ascontiguousarray(x.astype(np.int64)) for x in (us, ud, uw)]
+    a32 = [np.ascontiguousarray(x.astype(np.int32)) for x in (us, ud, uw)]
+    h64, o64 = make()
+    h64.run_stream_ptrs(kd.ctypes.data, *[x.ctypes.data for x in a64], k, bs, 0, *[o.ctypes.data for o in o64])
+    h32, o32 = make()
+    h32.run_stream_ptrs(kd.ctypes.data, *[x.ctypes.data for x in a32], k, bs, 0, *[o.ctypes.data for o in o32],
+                        ids32=True)
+    for x, y in zip(o64, o32):
+        np.testing.assert_array_equal(x, y)
+    bad = a32[0].copy()
+    bad[bs + 3] = n + 9
+    h, o = make()
+    with pytest.raises(ExecError, match=f"{n + 9}"):
+        h.run_stream_ptrs(kd.ctypes.data, bad.ctypes.data, a32[1].ctypes.data, a32[2].ctypes.data, k, bs, 0,
+                          *[x.ctypes.data for x in o], ids32=True)

@@ -1,3 +1,8 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_stream.py tests/test_dist_local_gpu.py tests/test_gpu_parity.py -x -q -p no:cacheprovider 2>&1 | tail -2
-AB_TOPK=2 AB_WORKLOADS="pr tc sssp-grid" AB_STEPS=8 AB_ENV=GD_UPLOAD_EARLY=1 bash tools/gpu_ab_env.sh
+timeout 900 python -m pytest tests/test_gpu_stream.py tests/test_dist_local_gpu.py -x -q -p no:cacheprovider 2>&1 | tail -2
+for wl in pr pr tc sssp-grid; do
+timeout 600 python bench.py --no-cpu-baseline --no-extras --workload $wl --steps 10 2>/dev/null | python -c "
+import json,sys
+j=json.loads(sys.stdin.read())
+print('$wl', round(j['ms_per_step'],3), 'e2e', round(j['e2e']['ms_per_step'],3), j['e2e']['h2d_bytes_per_step'], j['e2e']['api'])"
+done
