@@ -385,7 +385,10 @@ __global__ void k_uf_init(int32_t* p, int64_t n, uint8_t* root_has_seed) {
 // because an arc is stored at its source only.  Same components as linking
 // every arc, at a fraction of the arc reads (the giant component of an R-MAT
 // graph holds ~all non-isolated vertices).
-constexpr int kSample = 2;
+#ifndef GD_AFF_SAMPLE
+#define GD_AFF_SAMPLE 2
+#endif
+constexpr int kSample = GD_AFF_SAMPLE;
 
 __global__ void k_aff_sample(OutView ov, int64_t n, int32_t* p) {
     const int64_t* off = ov.off[0];
@@ -408,9 +411,10 @@ __global__ void k_uf_compress(int32_t* p, int64_t n) {
         p[i] = uf_find(p, (int32_t)i);
 }
 
-__global__ void k_aff_gather(const int32_t* p, int64_t n, int32_t* out, int m) {
+// the probes' roots (finds, so the forest need not be compressed first)
+__global__ void k_aff_gather(int32_t* p, int64_t n, int32_t* out, int m) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x)
-        out[i] = p[(int64_t)((unsigned long long)i * 2654435761ULL % (unsigned long long)n)];
+        out[i] = uf_find(p, (int32_t)((unsigned long long)i * 2654435761ULL % (unsigned long long)n));
 }
 
 // the most frequent root among the probe samples (one CTA; ties -> smaller
@@ -590,7 +594,10 @@ int64_t flood_weak_components(Store& g, uint8_t* flags, KernelProf* prof) {
     OutView ov = g.out_view();
     GD_KERNEL(k_uf_init, grid_for(n, 256), 256, 0, s, p.get(), n, seed.get());
     GD_KERNEL_T("flood_sample", n * (8 + 4 * kSample), k_aff_sample, grid_for(n, 256), 256, 0, s, ov, n, p.get());
-    GD_KERNEL(k_uf_compress, grid_for(n, 256), 256, 0, s, p.get(), n);
+    // the rest pass and the final compression find roots anyway: no full
+    // compression pass in between (GD_FLOOD_COMPRESS=1 restores it, A/B)
+    static const bool compress = getenv("GD_FLOOD_COMPRESS") != nullptr;
+    if (compress) GD_KERNEL(k_uf_compress, grid_for(n, 256), 256, 0, s, p.get(), n);
     constexpr int kProbe = 256;  // the giant component holds ~all non-isolated vertices
     DBuf<int32_t> probe(kProbe, s);
     GD_KERNEL(k_aff_gather, 4, 256, 0, s, p.get(), n, probe.get(), kProbe);
