@@ -1,3 +1,3 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_dist_local_gpu.py -x -q -p no:cacheprovider -k "flood or pr or propagate" 2>&1 | tail -2
-AB_TOPK=9 AB_WORKLOADS="pr" AB_ENV=GD_FLOOD_COMPRESS=1 bash tools/gpu_ab_env.sh
+timeout 900 python -m pytest tests -m gpu -x -q -p no:cacheprovider -k "tc and not test_c2_pagerank_all" 2>&1 | tail -2
+AB_TOPK=3 AB_WORKLOADS="tc" AB_STEPS=6 AB_ENV=GD_TC_META=0 bash tools/gpu_ab_env.sh
