@@ -594,13 +594,14 @@ __global__ void __launch_bounds__(kThreads, MODE == FP_RELAX ? GD_FP_RELAX_MINB 
 // non-stale distances are exact (their tree paths survive the deletes), so
 // both reach the same least fixpoint over the stale set.  Vertices with more
 // than kHeavy in-arcs go to `heavy` and are pulled by a whole CTA.
+template <int G>
 __global__ void __launch_bounds__(kThreads) k_pull_once(const int32_t* list, const int64_t* d_m, IdxView ix,
                                                         int64_t* dist, int32_t* heavy, unsigned long long* nheavy) {
     const int64_t m = *d_m;
     FpArgs a;
     a.ix = ix;
     a.dist = dist;
-    GROUP_LOOP_BEGIN(m)
+    GROUP_LOOP_BEGIN_G(m, G)
     (void)gw;
     if (valid) {
         int32_t v = list[_t];
@@ -609,7 +610,7 @@ __global__ void __launch_bounds__(kThreads) k_pull_once(const int32_t* list, con
             if (lane == 0) heavy[atomicAdd(nheavy, 1ULL)] = v;
         } else {
             int64_t nb = 0;  // unused here
-            int64_t best = in_min<kG>(a, s0, s1, lane, nb);
+            int64_t best = in_min<G>(a, s0, s1, lane, nb);
             if (lane == 0 && best < dist[v]) atomicMin(reinterpret_cast<long long*>(&dist[v]), (long long)best);
         }
     }
@@ -674,11 +675,12 @@ __global__ void k_fp_prep(unsigned long long* cnt, const int64_t* d_n, int64_t n
 }
 
 // parent = min-id in-neighbour u with dist[u] + w == dist[v] (sssp_dynamic.sp:23-34)
+template <int G>
 __global__ void __launch_bounds__(kThreads) k_fix_parent(const int32_t* list, const int64_t* d_m, int64_t m,
                                                          IdxView ix, const int64_t* dist, int32_t* parent,
                                                          int32_t src, int32_t* heavy, unsigned long long* nheavy) {
     if (d_m) m = *d_m;
-    GROUP_LOOP_BEGIN(m)
+    GROUP_LOOP_BEGIN_G(m, G)
     int32_t v = valid ? (list ? list[_t] : (int32_t)_t) : 0;
     int64_t dv = valid ? dist[v] : kInf;
     bool act = valid && v != src && dv < kInf;
@@ -687,15 +689,15 @@ __global__ void __launch_bounds__(kThreads) k_fix_parent(const int32_t* list, co
     const bool hv = heavy && b - a > kHeavy;  // group-uniform: a whole CTA takes it below
     if (hv && lane == 0) heavy[atomicAdd(nheavy, 1ULL)] = v;
     if (act && !hv) {
-        for (int64_t e = a + lane; e < b; e += kG) {
+        for (int64_t e = a + lane; e < b; e += G) {
             int32_t u = ix.col[e];
             if (u < 0) continue;
             if (sat_add(dist[u], ix.w ? (int64_t)ix.w[e] : 1) == dv && u < best) best = u;
         }
     }
 #pragma unroll
-    for (int o = kG / 2; o; o >>= 1) {
-        int32_t x = __shfl_xor_sync(0xffffffffu, best, o, kG);
+    for (int o = G / 2; o; o >>= 1) {
+        int32_t x = __shfl_xor_sync(0xffffffffu, best, o, G);
         best = x < best ? x : best;
     }
     if (act && !hv && lane == 0) parent[v] = best == INT_MAX ? -1 : best;
@@ -835,7 +837,10 @@ __global__ void k_msg_apply(const int32_t* msg, int64_t m, int mode, int64_t* di
     }
 }
 
-inline unsigned group_grid(int64_t m) { return grid_for(((m + kPerWarp - 1) / kPerWarp) * 32, kThreads, 148LL * 32); }
+inline unsigned group_grid(int64_t m, int g = kG) {
+    const int64_t per = 32 / g;
+    return grid_for(((m + per - 1) / per) * 32, kThreads, 148LL * 32);
+}
 
 // co-resident grid for the cooperative fixpoint: <= 4 CTAs per SM keeps the
 // barrier cheap while leaving 32 warps per SM for latency hiding
@@ -1090,7 +1095,13 @@ void SSSP::fix_parents(const int32_t* list, const int64_t* d_m, int64_t m) {
     heavy.ensure(g->rev.nnz / kHeavy + 64, s);
     unsigned long long* nh = fr.cnt.get() + 10;
     fill_d(s, nh, 0, sizeof(unsigned long long));
-    GD_KERNEL_T("sssp_parent", 0, k_fix_parent, group_grid(m), kThreads, 0, s, list, d_m, m, ix, dist.get(),
+    // 4 lanes per vertex on low-degree graphs, as in the fixpoints
+    const bool narrow = narrow_groups();
+    if (narrow)
+        GD_KERNEL_T("sssp_parent", 0, k_fix_parent<4>, group_grid(m, 4), kThreads, 0, s, list, d_m, m, ix,
+                    dist.get(), parent.get(), src, heavy.get(), nh);
+    else
+    GD_KERNEL_T("sssp_parent", 0, k_fix_parent<8>, group_grid(m), kThreads, 0, s, list, d_m, m, ix, dist.get(),
                 parent.get(), src, heavy.get(), nh);
     GD_KERNEL_T("sssp_parent", 0, k_fix_parent_heavy, 148 * 4, kThreads, 0, s, heavy.get(), nh, ix, dist.get(),
                 parent.get());
@@ -1148,7 +1159,7 @@ void SSSP::batch_dist(DevBatch& b, int64_t batch_index) {
         IdxView ix = g->rev.view();
         heavy.ensure(g->rev.nnz / kHeavy + 64, s);
         fill_d(s, fr.cnt.get() + 9, 0, sizeof(unsigned long long));
-        GD_KERNEL_T("sssp_pull", 0, k_pull_once, group_grid(n), kThreads, 0, s, list.get(), nl.get(), ix, dist.get(),
+        GD_KERNEL_T("sssp_pull", 0, (narrow_groups() ? &k_pull_once<4> : &k_pull_once<8>), group_grid(n, narrow_groups() ? 4 : 8), kThreads, 0, s, list.get(), nl.get(), ix, dist.get(),
                     heavy.get(), fr.cnt.get() + 9);
         GD_KERNEL_T("sssp_pull", 0, k_pull_heavy, 148 * 4, kThreads, 0, s, heavy.get(), fr.cnt.get() + 9, ix,
                     dist.get());
@@ -1221,7 +1232,7 @@ void SSSP::batch(DevBatch& b, int64_t batch_index) {
         IdxView ix = g->rev.view();
         heavy.ensure(g->rev.nnz / kHeavy + 64, s);
         fill_d(s, fr.cnt.get() + 9, 0, sizeof(unsigned long long));
-        GD_KERNEL_T("sssp_pull", 0, k_pull_once, group_grid(n), kThreads, 0, s, list.get(), nlist, ix, dist.get(),
+        GD_KERNEL_T("sssp_pull", 0, (narrow_groups() ? &k_pull_once<4> : &k_pull_once<8>), group_grid(n, narrow_groups() ? 4 : 8), kThreads, 0, s, list.get(), nlist, ix, dist.get(),
                     heavy.get(), fr.cnt.get() + 9);
         GD_KERNEL_T("sssp_pull", 0, k_pull_heavy, 148 * 4, kThreads, 0, s, heavy.get(), fr.cnt.get() + 9, ix,
                     dist.get());

@@ -19,7 +19,9 @@ import paper_2507_11094_b200 as gd
 
 wlname = sys.argv[1] if len(sys.argv) > 1 else "pr"
 nb = int(sys.argv[2]) if len(sys.argv) > 2 else 4
-wl = bench.WORKLOADS[wlname]
+wl = dict(bench.WORKLOADS[wlname])
+if len(sys.argv) > 3:
+    wl["percent"] = float(sys.argv[3])
 n, s, d, w, kind, us, ud, uw, per = bench.make_inputs(wl, nb + 3)
 g = gd.DynamicGraph.from_arrays(n, s, d, w if wl["weighted"] else None, directed=wl["directed"],
                                 weighted=wl["weighted"], with_reverse=wl["algo"] != "tc")
@@ -87,6 +89,12 @@ for a, b in zip(dev, dev[1:]):
     charge[key] += gap
     ncharge[key] += 1
 tot = sum(charge.values())
+kern = collections.defaultdict(float)
+for e in dev:
+    kern[e["name"][:80]] += e["dur"]
+print("device time per batch by kernel (us):")
+for k_, v in sorted(kern.items(), key=lambda kv: -kv[1])[:25]:
+    print(f"  {v / nb:10.1f}  {k_}")
 print(f"device idle {tot / nb:.1f} us per batch, by the host call in progress:")
 for k, v in sorted(charge.items(), key=lambda kv: -kv[1])[:30]:
     print(f"  {v / nb:8.1f} us {ncharge[k] / nb:5.1f}x  {k}")
