@@ -47,23 +47,9 @@ size_t size_class(size_t bytes) {
 // their exact size.
 constexpr size_t kCacheMax = size_t(64) << 20;
 
-// A large block is rounded up to 1/8 of its power-of-two range (at most
-// 12.5% over), so the store's arrays, whose sizes drift by a fraction of a
-// percent from merge to merge, keep landing in the size of the block the
-// previous merge freed: the pool hands that back at once, instead of mapping
-// fresh memory (R-MAT-24 TC: 26 + 14 ms of device idle per batch in
-// cudaMallocAsync at exact sizes).
-inline size_t round_large(size_t b) {
-    size_t p = 1;
-    while (p * 2 <= b) p *= 2;
-    const size_t g = std::max<size_t>(p / 8, size_t(2) << 20);
-    return (b + g - 1) / g * g;
-}
-
 void* dev_alloc(size_t bytes, cudaStream_t s) {
     const bool cached = bytes <= kCacheMax;
-    static const bool exact = getenv("GD_ALLOC_EXACT") != nullptr;  // A/B: exact-size pool blocks
-    const size_t c = cached ? size_class(bytes) : (exact ? bytes : round_large(bytes));
+    const size_t c = cached ? size_class(bytes) : bytes;
     DevCache& dc = dev_cache();
     if (cached) {
         std::lock_guard<std::mutex> lk(dc.mu);
