@@ -7,5 +7,5 @@ for wl in pr sssp tc sssp-grid; do
     > gpurun_out/forcedist_$wl.json 2> gpurun_out/forcedist_$wl.err
   echo "$wl rc=$?"
   python -c "
-import json; j=json.load(open('gpurun_out/forcedist_$wl.json')); print('$wl', round(j['ms_per_step'],3), 'ms', j['config']['parallelism'][:60], j.get('comm'))" 2>&1 | tail -1
+import json; j=json.loads([l for l in open('gpurun_out/forcedist_$wl.json') if l.startswith('{')][-1]); print('$wl', round(j['ms_per_step'],3), 'ms', j['config']['parallelism'][:60], j.get('comm'))" 2>&1 | tail -1
 done
