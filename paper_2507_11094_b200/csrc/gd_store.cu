@@ -728,6 +728,25 @@ __global__ void k_added_to_index(const int32_t* a_row, const int32_t* a_col, int
     }
 }
 
+// the in-index delta from the source-sorted arcs: keys = destinations, values = arc indices
+__global__ void k_dst_by_src(const int32_t* by_row, const int32_t* a_col, int64_t m, uint32_t* key, int32_t* val) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < m; t += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t i = by_row[t];
+        key[t] = (uint32_t)a_col[i];
+        val[t] = i;
+    }
+}
+
+__global__ void k_rev_delta_split(const uint32_t* key, const int32_t* val, int64_t m, const int32_t* a_row,
+                                  const int32_t* a_w, int32_t* drow, int32_t* dcol, int32_t* dw) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < m; t += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t i = val[t];
+        drow[t] = (int32_t)key[t];
+        dcol[t] = a_row[i];
+        if (dw) dw[t] = a_w[i];
+    }
+}
+
 // insertion point of delta entry (row, col) in the base: after equal columns
 __global__ void k_index_ins_pos(const int32_t* drow, const int32_t* dcol, int64_t m, const int64_t* off,
                                 const int32_t* col, int64_t* ipos) {
@@ -1696,6 +1715,25 @@ void Store::index_add(SortedIndex& ix, const AddedArcs& aa) {
     if (ix.dnnz) compact_index(ix);  // keep at most one delta
     cudaStream_t s = stream;
     int64_t m = aa.count;
+    static const bool full_sort = getenv("GD_INDEX_FULL_SORT") != nullptr;  // A/B: the (row, col) key sort
+    if (ix.rows_are_dst && aa.by_row && !full_sort) {
+        // the arcs already sorted by source (stable): one stable pass by
+        // destination gives (destination, source, stream) order -- the same
+        // order as sorting the (destination, source) keys with the arc index
+        // as the tie-break, in 32-bit keys of sh bits (3 passes at scale 22,
+        // not 6 over 44-bit keys)
+        DBuf<uint32_t> k32(m, s);
+        DBuf<int32_t> v32(m, s);
+        GD_KERNEL(k_dst_by_src, grid_for(m, 256), 256, 0, s, aa.by_row, aa.col.get(), m, k32.get(), v32.get());
+        sort_pairs_u32(s, k32.get(), v32.get(), m, sh);
+        ix.drow.alloc(m, s);
+        ix.dcol.alloc(m, s);
+        if (weighted) ix.dw.alloc(m, s);
+        GD_KERNEL(k_rev_delta_split, grid_for(m, 256), 256, 0, s, k32.get(), v32.get(), m, aa.row.get(),
+                  weighted ? aa.w.get() : nullptr, ix.drow.get(), ix.dcol.get(), weighted ? ix.dw.get() : nullptr);
+        ix.dnnz = m;
+        return;
+    }
     DBuf<uint64_t> key(m, s);
     DBuf<int32_t> val(m, s);
     GD_KERNEL(k_added_to_index, grid_for(m, 256), 256, 0, s, aa.row.get(), aa.col.get(), m, ix.rows_are_dst, sh,
@@ -2043,6 +2081,7 @@ void Store::apply_adds_local(const int32_t* d_src, const int32_t* d_dst, const i
     }
     if (with_reverse) claim_logs.push_back(std::move(cl));
     live += na;
+    aa.by_row = val.get();  // the source-sorted arc order (alive until return)
     rev_add(aa);
     if (fwd.built) index_add(fwd, aa);
 }

@@ -86,6 +86,10 @@ struct ClaimLog {
 struct AddedArcs {
     DBuf<int32_t> row, col, w;
     int64_t count = 0;
+    // optional, non-owning: the arc indices in (row, stream) order, i.e. the
+    // batch's stable sort by source (apply_adds); lets the in-index sort its
+    // delta with one stable 32-bit pass by destination
+    const int32_t* by_row = nullptr;
 };
 
 class Store {
