@@ -94,6 +94,9 @@ constexpr int kHubThreads = 512;
 #define GD_PR_ILP 8
 #endif
 constexpr int kILP = GD_PR_ILP;
+#ifndef GD_PR_GATHER
+#define GD_PR_GATHER __ldg  // contrib gathers through L1 (GD_PR_GATHER=__ldcg: L2 only, A/B)
+#endif
 
 template <int G>
 __device__ inline double row_sum(const int32_t* __restrict__ col, int64_t a, int64_t b, int lane,
@@ -108,7 +111,7 @@ __device__ inline double row_sum(const int32_t* __restrict__ col, int64_t a, int
         }
         double c[kILP];
 #pragma unroll
-        for (int q = 0; q < kILP; ++q) c[q] = u[q] >= 0 ? __ldg(&contrib[u[q]]) : 0.0;
+        for (int q = 0; q < kILP; ++q) c[q] = u[q] >= 0 ? GD_PR_GATHER(&contrib[u[q]]) : 0.0;
 #pragma unroll
         for (int q = 0; q < kILP; ++q) acc += c[q];
     }
